@@ -1,0 +1,22 @@
+# Build libsvb.so (sm_100a) in-tree.  `make -j8`
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+SRC := $(wildcard paper_2512_04216_b200/csrc/*.cu)
+OBJ := $(patsubst paper_2512_04216_b200/csrc/%.cu,build/%.o,$(SRC))
+HDR := $(wildcard paper_2512_04216_b200/csrc/*.h paper_2512_04216_b200/csrc/*.cuh include/*.h)
+LIB := paper_2512_04216_b200/libsvb.so
+
+all: $(LIB)
+
+build/%.o: paper_2512_04216_b200/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > build/$*.ptxas.log 2>&1 || (cat build/$*.ptxas.log; exit 1)
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

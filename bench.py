@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-vector hot path.
+
+Workload (BASELINE.json configs[1]): QFT on 30 qubits, complex128, one B200 —
+ry(0.1·(q+1)) preparation + conftest `qft(30)` = 2250 IR gates — producing the
+full amplitude vector and <Z_i> for i = 0..29.  One step = zero the state,
+run the whole gate program (fused HBM passes + the qubit-order permutation),
+and one multi-mask <Z> pass.  Metric: IR gates per second (the first metric
+BASELINE.json names); the per-pass HBM GB/s is reported as `roofline`.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* `value`: device-resident throughput, timed with CUDA events recorded on the
+  library's stream (all kernels of the state run there).
+* `e2e`: the same metric through the public API (`final_state(c, out=pinned)`
+  + `expectations`), wall-clock per step including host gate encoding, the
+  gate-program upload and the 16 GiB amplitude read-back into pinned memory.
+* `cpu_baseline` / `--impl reference`: the numpy restatement of the reference
+  algorithm (oracle/, "port") timed on this host on a bounded, evenly spaced
+  sample of the same gate list.
+* N > 1 (torchrun): independent replicas, one per GPU ("replicas only" for this
+  workload in round 1; the sharded path is described in DESIGN.md).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_QUBITS = 30
+PRECISION = "c128"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_sample_plan(n_full: int, steps: int, per_step: int):
+    """Evenly spaced gates of the QFT-n gate list, and the n it runs at."""
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    # numpy's dense 1q path needs ~3x the 16 GiB state at n=30
+    n_cpu = n_full if avail > 4 * (16 << n_full) else 26
+    from paper_2512_04216_b200 import suite
+
+    gates = [i for i in suite.qft_bench_circuit(n_cpu).instructions]
+    total = steps * per_step
+    idx = np.linspace(0, len(gates) - 1, total).astype(int)
+    return n_cpu, [gates[i] for i in idx]
+
+
+def time_cpu_port(n_cpu: int, gates, n_full: int) -> tuple[float, float]:
+    """Seconds per gate of the numpy port, scaled to n_full (cost is linear in 2^n)."""
+    from oracle import sv_oracle as orc
+
+    psi = orc.zero_state(n_cpu)
+    t0 = time.perf_counter()
+    for g in gates:
+        orc.apply_instruction(psi, n_cpu, g)
+    dt = time.perf_counter() - t0
+    scale = float(1 << (n_full - n_cpu))
+    return dt / len(gates) * scale, dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    n_cpu, sample = cpu_sample_plan(N_QUBITS, args.steps + args.warmup, 3)
+    per_step = 3
+    times = []
+    for s in range(args.warmup + args.steps):
+        spg, _ = time_cpu_port(n_cpu, sample[s * per_step:(s + 1) * per_step], N_QUBITS)
+        if s >= args.warmup:
+            times.append(spg)
+    sec_per_gate = float(np.mean(times))
+    total_gates = 2250
+    value = 1.0 / sec_per_gate
+    desc = (f"{per_step} evenly spaced gates of the 2250-gate QFT-30 list per step at n={n_cpu}"
+            + ("" if n_cpu == N_QUBITS else f", time x{1 << (N_QUBITS - n_cpu)} (cost linear in 2^n)"))
+    line = {
+        "impl": "reference",
+        "metric": "gates/sec (QFT-30 complex128, full amplitudes + <Z_i>)",
+        "value": value,
+        "unit": "gates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_gates * sec_per_gate * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (deterministic QFT circuit)",
+        "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": total_gates},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+def run_ours(args, rank: int, world: int, dist):
+    from paper_2512_04216_b200 import statevector as sv
+    from paper_2512_04216_b200 import suite
+
+    device = int(os.environ.get("LOCAL_RANK", 0))
+    c = suite.qft_bench_circuit(N_QUBITS)
+    gates = sv.gate_array(c.instructions)
+    n_gates = int(gates.size)
+    masks = [1 << q for q in range(N_QUBITS)]
+    state = sv.DeviceState(N_QUBITS, PRECISION, device)
+    plan = sv.plan(N_QUBITS, c.instructions, PRECISION)
+
+    def step():
+        state.zero()
+        state.apply_gates(gates)
+        return state.expect_z(masks)
+
+    for _ in range(max(args.warmup, 3)):
+        z = step()
+    stats = state.stats()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    barrier()
+    state.profile(True)
+    with ClockSampler(device) as clk:
+        state.timer_start()
+        for _ in range(args.steps):
+            z = step()
+        total_ms = state.timer_stop()
+    prof = state.profile_read()
+    state.profile(False)
+    barrier()
+    if dist is not None:
+        import torch
+
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * n_gates / (ms_per_step / 1e3)
+
+    # roofline of the dominant kernel (fused pass), CUDA events on the launch stream
+    pass_avg_ms = prof["pass_ms"] / max(prof["pass_launches"], 1)
+    pass_bytes = prof["pass_bytes"] / max(prof["pass_launches"], 1)
+    achieved = pass_bytes / (pass_avg_ms / 1e3) / 1e9
+    peak, peak_kind = hbm_peak()
+
+    # e2e through the public API (host gate encoding + upload + 16 GiB read-back)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    pinned = sv.PinnedBuffer(1 << N_QUBITS)
+    e2e_times = []
+    for i in range(e2e_steps + 1):
+        ci = suite.qft_bench_circuit(N_QUBITS)
+        t0 = time.perf_counter()
+        sv.final_state(ci, qubit_cap=N_QUBITS, out=pinned.array)
+        zi = sv.expectations(ci, [(q,) for q in range(N_QUBITS)], qubit_cap=N_QUBITS)
+        dt = time.perf_counter() - t0
+        del ci
+        if i > 0:  # first call pays one-time allocations
+            e2e_times.append(dt)
+    e2e_s = float(np.mean(e2e_times))
+    np.testing.assert_allclose(zi, z, atol=1e-10)
+    pinned.close()
+    state.close()
+
+    line = {
+        "metric": "gates/sec (QFT-30 complex128, full amplitudes + <Z_i>)",
+        "value": value,
+        "unit": "gates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "c128",
+        "data": "synthetic (deterministic QFT circuit; state 16 GiB >> 126 MB L2, no flush needed)",
+        "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": n_gates,
+                   "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2",
+                   "hbm_passes_per_step": stats["passes"], "plan": plan},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "k_pass<double,4>",
+                     "peak_kind": peak_kind, "bytes_per_launch": pass_bytes, "avg_launch_ms": pass_avg_ms},
+        "e2e": {"value": world * n_gates / e2e_s, "unit": "gates/s",
+                "h2d_bytes_per_step": int(gates.nbytes),
+                "d2h_bytes_per_step": int((16 << N_QUBITS) + 8 * N_QUBITS), "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": int(args.steps * (stats["launches"] + 3)),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        n_cpu, sample = cpu_sample_plan(N_QUBITS, 1, args.cpu_gates)
+        spg, dt = time_cpu_port(n_cpu, sample, N_QUBITS)
+        line["cpu_baseline"] = {
+            "value": 1.0 / spg, "unit": "gates/s", "cores": 1, "kind": "port",
+            "sample": f"{len(sample)} evenly spaced gates of the QFT-30 list at n={n_cpu}"
+                      + ("" if n_cpu == N_QUBITS else f", x{1 << (N_QUBITS - n_cpu)} scaled")
+                      + f", {dt:.1f} s wall"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-gates", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("gloo")
+        dist = tdist
+    run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

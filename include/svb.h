@@ -1,0 +1,156 @@
+/*
+ * svb.h — C ABI of the B200 state-vector backend (libsvb.so).
+ *
+ * This is the drop-in boundary for the reference's dense state-vector path
+ * (`polysim/statevector.py`).  Every entry point below names the reference
+ * interface it replaces.  Signatures carry plain pointers and sizes only; the
+ * Python boundary module `paper_2512_04216_b200/statevector.py` binds them
+ * with ctypes, exactly as a maintainer of the reference would.
+ *
+ * Conventions (identical to the reference):
+ *   - qubit 0 is the least significant bit of the amplitude index
+ *     (statevector.py:3-4);
+ *   - a 2-qubit matrix acts on local index bit(q[0]) + 2*bit(q[1])
+ *     (gates.py:3-5, 69-74);
+ *   - host amplitude buffers are interleaved complex128 (re, im) doubles,
+ *     i.e. numpy complex128 memory, regardless of the device precision.
+ *
+ * Errors: every function returns an svb_status; the message of the last
+ * failure on the calling thread is svb_last_error().  The Python layer maps
+ *   SVB_E_CAP -> QubitCapError, SVB_E_ARG -> ValueError,
+ *   SVB_E_SAMPLING -> SamplingError (a ValueError, sampling.py:17-18),
+ *   SVB_E_OOM / SVB_E_CUDA / SVB_E_NCCL -> BackendError  (result.py:12-21).
+ *
+ * Thread-safety: distinct handles may be used from distinct threads; one
+ * handle is confined to one thread at a time.  Every call that
+ * takes host buffers is synchronous on return.
+ */
+#ifndef SVB_H
+#define SVB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SVB_OK = 0,
+  SVB_E_ARG = 1,
+  SVB_E_CAP = 2,
+  SVB_E_OOM = 3,
+  SVB_E_CUDA = 4,
+  SVB_E_NCCL = 5,
+  SVB_E_SAMPLING = 6
+} svb_status;
+
+typedef enum { SVB_C64 = 0, SVB_C128 = 1 } svb_precision;
+
+typedef enum {
+  SVB_SAMPLER_ALIAS = 0, /* reference-compatible Walker/Vose table, sampling.py:30-83 */
+  SVB_SAMPLER_CDF = 1    /* fused |amp|^2 block prefix + binary-search multinomial */
+} svb_sampler;
+
+typedef struct svb_state* svb_handle;
+
+/* One unitary of a gate program.  k = 1 or 2 qubits; mat is the row-major
+ * 2^k x 2^k complex matrix as (re, im) pairs (2x2 uses the first 8 doubles).
+ * Replaces one `apply_instruction` call (statevector.py:116-122). */
+typedef struct {
+  int32_t k;
+  int32_t qubits[2];
+  int32_t reserved;
+  double mat[32];
+} svb_gate;
+
+/* Library / device info. */
+const char* svb_last_error(void);
+int svb_version(void);
+/* Largest n whose state (plus sampling workspace) fits on `device`. */
+int svb_max_qubits(int device, int precision, int* out_n);
+/* Page-locked host buffers (fast final_state copies). */
+int svb_host_alloc(uint64_t bytes, void** out);
+int svb_host_free(void* p);
+
+typedef enum {
+  SVB_OPT_FUSION = 0,   /* 1 (default): fused multi-gate HBM passes; 0: one pass per gate */
+  SVB_OPT_MAX_HIGH = 1  /* fused pass: max non-lane qubits per pass (tuning; default auto) */
+} svb_option;
+int svb_set_option(svb_handle h, int option, int value);
+/* Statistics of the last svb_apply: HBM passes launched, gates applied. */
+int svb_last_stats(svb_handle h, int64_t* n_passes, int64_t* n_gates, int64_t* n_launches);
+int svb_sync(svb_handle h);
+/* CUDA-event timing on the handle's stream (the stream every kernel of the
+ * handle is launched on).  svb_profile(h, 1) additionally times every fused
+ * pass and permutation launch; svb_profile_read fills out[6] =
+ * {pass_ms, pass_launches, pass_bytes, perm_ms, perm_launches, perm_bytes}
+ * (bytes = algorithmic 2*s*2^n per launch). */
+int svb_timer_start(svb_handle h);
+int svb_timer_stop(svb_handle h, double* ms);
+int svb_profile(svb_handle h, int enable);
+int svb_profile_read(svb_handle h, double* out);
+
+/* State lifetime: zero_state (statevector.py:125-128). */
+int svb_create(int n_qubits, int precision, int device, svb_handle* out);
+int svb_destroy(svb_handle h);
+int svb_set_zero(svb_handle h);
+int svb_copy_state(svb_handle dst, svb_handle src); /* prefix.copy(), statevector.py:168 */
+int svb_n_qubits(svb_handle h);
+
+/* Host <-> device amplitudes (final_state, statevector.py:259-274; and the
+ * kernel-level numpy-array API used by pblock.py:93-154, calibration.py:215-228). */
+int svb_set_amplitudes(svb_handle h, const double* host, uint64_t offset, uint64_t count);
+int svb_get_amplitudes(svb_handle h, double* host, uint64_t offset, uint64_t count);
+
+/* Gate program: apply_1q / apply_2q / apply_instruction over a whole circuit
+ * (statevector.py:33-122, 210-212).  The program is fused and scheduled into
+ * HBM passes natively; the result equals applying the gates
+ * one by one in order. */
+int svb_apply(svb_handle h, const svb_gate* gates, int n_gates);
+
+/* Reduced |amp|^2 over ascending `qubits` (marginal_probs, statevector.py:131-139). */
+int svb_marginal_probs(svb_handle h, const int32_t* qubits, int k, double* out);
+
+/* <Z_mask> for M masks in one pass over the state (expectation, statevector.py:277-292). */
+int svb_expect_z(svb_handle h, const uint64_t* masks, int m, double* out);
+
+/* Terminal sampling (statevector.py:213-216 + result.py:50-82 + sampling.py:30-83).
+ *   qubits[k]      ascending measured qubits;
+ *   bit_src[w]     for output bit p (clbit rank p): bit index into the marginal index;
+ *   pcg[4]         numpy PCG64 (state_hi, state_lo, inc_hi, inc_lo) of default_rng(seed);
+ *   out_codes/out_counts: capacity >= min(shots, 2^w); sorted ascending like np.unique. */
+int svb_sample(svb_handle h, const int32_t* qubits, int k, const int32_t* bit_src, int w,
+               uint64_t shots, const uint64_t* pcg, int sampler, uint64_t* out_codes,
+               uint64_t* out_counts, uint64_t* n_unique);
+
+/* AliasTable.from_probs (sampling.py:30-70) on the device for a given
+ * probability vector: the table the ALIAS sampler draws from.  Errors:
+ * SVB_E_SAMPLING for an invalid vector (sampling.py:31-40). */
+int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_row, int64_t* alias_row);
+
+/* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
+ * device; each measure/reset consumes one draw, exactly as rng.random(). */
+int svb_rng_seed(svb_handle h, const uint64_t* pcg);
+int svb_measure(svb_handle h, int qubit, int32_t* outcome);      /* _measure_qubit */
+int svb_reset(svb_handle h, int qubit);                          /* _reset_qubit   */
+
+/* Whole-shot replay of a suffix program on device: for each shot, copy
+ * `prefix`, run ops, record clbits.  ops: kind 0 = gate (index into gates),
+ * 1 = measure (qubit, clbit), 2 = reset (qubit).  out_codes[s] = packed clbits
+ * (bit p = clbit rank p), computed with the device PCG64 stream seeded by pcg. */
+int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops,
+               const svb_gate* gates, const int32_t* clbit_rank, uint64_t shots,
+               const uint64_t* pcg, uint64_t* out_codes);
+
+/* Host-only helpers (no GPU): schedule statistics of a gate program, and CPU
+ * emulation of the fused program with the same scheduler and op interpreter
+ * as the device kernel (complex128 amps in/out).  Test/diagnostic hooks. */
+int svb_plan(int n, int precision, const svb_gate* gates, int n_gates, int64_t* n_passes,
+             int64_t* n_rounds, int64_t* op_bytes, int32_t* has_perm);
+int svb_emulate_apply(int n, int precision, const svb_gate* gates, int n_gates, double* amps,
+                      int relabel_swaps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVB_H */

@@ -1,0 +1,525 @@
+// libsvb C ABI (include/svb.h): handle lifetime, host<->device transfers and
+// the dispatch of gate programs, reductions and samplers to the kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "program.h"
+
+using namespace svb;
+
+struct svb_state {
+  int n = 0, prec = SVB_C128, device = 0;
+  void* amps = nullptr;
+  cudaStream_t st = nullptr;
+  uint64_t* d_rng = nullptr;     // PCG64 (state_hi, state_lo, inc_hi, inc_lo)
+  int32_t* d_outcome = nullptr;  // last measure outcome
+  double* d_ws = nullptr;        // reduction scratch
+  size_t ws_doubles = 0;
+  int fusion = 1, max_high = -1;
+  ProgramStats stats{};
+  Profiler prof;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  size_t amp_bytes() const { return (size_t)(prec == SVB_C128 ? 16 : 8) << n; }
+};
+
+static thread_local std::string g_err;
+
+template <class F> static int guard(F&& f) {
+  try {
+    f();
+    return SVB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SVB_E_CUDA;
+  }
+}
+
+static void check_handle(svb_handle h) {
+  require(h != nullptr && h->amps != nullptr, SVB_E_ARG, "invalid svb handle");
+  SVB_CUDA(cudaSetDevice(h->device));
+}
+
+static void ensure_ws(svb_handle h, size_t doubles) {
+  if (doubles <= h->ws_doubles) return;
+  if (h->d_ws) SVB_CUDA(cudaFreeAsync(h->d_ws, h->st));
+  h->d_ws = nullptr;
+  h->ws_doubles = 0;
+  SVB_CUDA(cudaMallocAsync(&h->d_ws, doubles * sizeof(double), h->st));
+  h->ws_doubles = doubles;
+}
+
+// complex128 <-> complex64 conversion through a device staging buffer
+__global__ void k_c128_to_c64(const double2* __restrict__ in, float2* __restrict__ out, uint64_t n) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = make_float2((float)in[i].x, (float)in[i].y);
+}
+__global__ void k_c64_to_c128(const float2* __restrict__ in, double2* __restrict__ out, uint64_t n) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = make_double2((double)in[i].x, (double)in[i].y);
+}
+
+extern "C" {
+
+const char* svb_last_error(void) { return g_err.c_str(); }
+int svb_version(void) { return 1; }
+
+int svb_max_qubits(int device, int precision, int* out_n) {
+  return guard([&] {
+    SVB_CUDA(cudaSetDevice(device));
+    size_t fr = 0, tot = 0;
+    SVB_CUDA(cudaMemGetInfo(&fr, &tot));
+    size_t s = precision == SVB_C128 ? 16 : 8;
+    int n = 1;
+    while (n < 40 && ((s << (n + 1)) + (s << (n + 1)) / 8) < fr) ++n;
+    *out_n = n;
+  });
+}
+
+int svb_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] { SVB_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocPortable)); });
+}
+int svb_host_free(void* p) {
+  return guard([&] { SVB_CUDA(cudaFreeHost(p)); });
+}
+
+int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
+  svb_state* h = nullptr;
+  int rc = guard([&] {
+    require(n_qubits >= 1 && n_qubits <= 40, SVB_E_ARG, "n_qubits out of range");
+    require(precision == SVB_C64 || precision == SVB_C128, SVB_E_ARG, "bad precision");
+    SVB_CUDA(cudaSetDevice(device));
+    h = new svb_state();
+    h->n = n_qubits;
+    h->prec = precision;
+    h->device = device;
+    SVB_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    cudaError_t e = cudaMalloc(&h->amps, h->amp_bytes());
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      h->amps = nullptr;
+      throw Error(SVB_E_OOM, "cannot allocate " + std::to_string(h->amp_bytes()) +
+                                 " bytes for a " + std::to_string(n_qubits) + "-qubit state");
+    }
+    SVB_CUDA(cudaMalloc(&h->d_rng, 4 * sizeof(uint64_t) + 16));
+    h->d_outcome = reinterpret_cast<int32_t*>(h->d_rng + 4);
+    if (precision == SVB_C128) launch_zero<double>(h->amps, n_qubits, h->st);
+    else launch_zero<float>(h->amps, n_qubits, h->st);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+  if (rc != SVB_OK) {
+    if (h) {
+      if (h->amps) cudaFree(h->amps);
+      if (h->st) cudaStreamDestroy(h->st);
+      delete h;
+    }
+    *out = nullptr;
+    return rc;
+  }
+  *out = h;
+  return SVB_OK;
+}
+
+int svb_destroy(svb_handle h) {
+  if (!h) return SVB_OK;
+  return guard([&] {
+    SVB_CUDA(cudaSetDevice(h->device));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+    if (h->d_ws) cudaFreeAsync(h->d_ws, h->st);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+    cudaFree(h->amps);
+    cudaFree(h->d_rng);
+    if (h->t0) cudaEventDestroy(h->t0);
+    if (h->t1) cudaEventDestroy(h->t1);
+    cudaStreamDestroy(h->st);
+    delete h;
+  });
+}
+
+int svb_n_qubits(svb_handle h) { return h ? h->n : -1; }
+
+int svb_sync(svb_handle h) {
+  return guard([&] {
+    check_handle(h);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_set_option(svb_handle h, int option, int value) {
+  return guard([&] {
+    check_handle(h);
+    if (option == SVB_OPT_FUSION) h->fusion = value;
+    else if (option == SVB_OPT_MAX_HIGH) h->max_high = value;
+    else throw Error(SVB_E_ARG, "unknown option");
+  });
+}
+
+int svb_last_stats(svb_handle h, int64_t* n_passes, int64_t* n_gates, int64_t* n_launches) {
+  return guard([&] {
+    check_handle(h);
+    *n_passes = h->stats.passes;
+    *n_gates = h->stats.gates;
+    *n_launches = h->stats.launches;
+  });
+}
+
+int svb_set_zero(svb_handle h) {
+  return guard([&] {
+    check_handle(h);
+    if (h->prec == SVB_C128) launch_zero<double>(h->amps, h->n, h->st);
+    else launch_zero<float>(h->amps, h->n, h->st);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_copy_state(svb_handle dst, svb_handle src) {
+  return guard([&] {
+    check_handle(dst);
+    check_handle(src);
+    require(dst->n == src->n && dst->prec == src->prec, SVB_E_ARG, "state shape mismatch");
+    SVB_CUDA(cudaMemcpyAsync(dst->amps, src->amps, src->amp_bytes(), cudaMemcpyDeviceToDevice, dst->st));
+    SVB_CUDA(cudaStreamSynchronize(dst->st));
+  });
+}
+
+static constexpr uint64_t kStage = 1ull << 24;  // amplitudes per c64 conversion chunk
+
+int svb_set_amplitudes(svb_handle h, const double* host, uint64_t offset, uint64_t count) {
+  return guard([&] {
+    check_handle(h);
+    uint64_t len = 1ull << h->n;
+    require(offset <= len && count <= len - offset, SVB_E_ARG, "amplitude range out of bounds");
+    if (h->prec == SVB_C128) {
+      SVB_CUDA(cudaMemcpyAsync(static_cast<double2*>(h->amps) + offset, host, count * 16,
+                               cudaMemcpyHostToDevice, h->st));
+    } else {
+      double2* stage = nullptr;
+      uint64_t chunk = std::min(count, kStage);
+      SVB_CUDA(cudaMallocAsync(&stage, std::max<uint64_t>(chunk, 1) * 16, h->st));
+      for (uint64_t done = 0; done < count; done += chunk) {
+        uint64_t c = std::min(chunk, count - done);
+        SVB_CUDA(cudaMemcpyAsync(stage, host + 2 * done, c * 16, cudaMemcpyHostToDevice, h->st));
+        k_c128_to_c64<<<grid_for(c, 256), 256, 0, h->st>>>(stage, static_cast<float2*>(h->amps) + offset + done, c);
+        SVB_CHECK_LAUNCH();
+      }
+      SVB_CUDA(cudaFreeAsync(stage, h->st));
+    }
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_get_amplitudes(svb_handle h, double* host, uint64_t offset, uint64_t count) {
+  return guard([&] {
+    check_handle(h);
+    uint64_t len = 1ull << h->n;
+    require(offset <= len && count <= len - offset, SVB_E_ARG, "amplitude range out of bounds");
+    if (h->prec == SVB_C128) {
+      SVB_CUDA(cudaMemcpyAsync(host, static_cast<double2*>(h->amps) + offset, count * 16,
+                               cudaMemcpyDeviceToHost, h->st));
+    } else {
+      double2* stage = nullptr;
+      uint64_t chunk = std::min(count, kStage);
+      SVB_CUDA(cudaMallocAsync(&stage, std::max<uint64_t>(chunk, 1) * 16, h->st));
+      for (uint64_t done = 0; done < count; done += chunk) {
+        uint64_t c = std::min(chunk, count - done);
+        k_c64_to_c128<<<grid_for(c, 256), 256, 0, h->st>>>(static_cast<float2*>(h->amps) + offset + done, stage, c);
+        SVB_CHECK_LAUNCH();
+        SVB_CUDA(cudaMemcpyAsync(host + 2 * done, stage, c * 16, cudaMemcpyDeviceToHost, h->st));
+      }
+      SVB_CUDA(cudaFreeAsync(stage, h->st));
+    }
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+static void validate_gates(svb_handle h, const svb_gate* g, int ng) {
+  require(ng >= 0 && (ng == 0 || g != nullptr), SVB_E_ARG, "bad gate list");
+  for (int i = 0; i < ng; ++i) {
+    require(g[i].k == 1 || g[i].k == 2, SVB_E_ARG, "gate arity must be 1 or 2");
+    for (int j = 0; j < g[i].k; ++j)
+      require(g[i].qubits[j] >= 0 && g[i].qubits[j] < h->n, SVB_E_ARG, "gate qubit out of range");
+    require(g[i].k == 1 || g[i].qubits[0] != g[i].qubits[1], SVB_E_ARG, "gate repeats a qubit");
+  }
+}
+
+int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
+  return guard([&] {
+    check_handle(h);
+    validate_gates(h, gates, n_gates);
+    h->stats = ProgramStats{};
+    h->stats.prof = &h->prof;
+    if (h->prec == SVB_C128)
+      run_program_owned<double>(&h->amps, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+    else
+      run_program_owned<float>(&h->amps, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+    if (h->prof.on) h->prof.collect();
+  });
+}
+
+int svb_profile(svb_handle h, int enable) {
+  return guard([&] {
+    check_handle(h);
+    h->prof.on = enable != 0;
+    h->prof.ms[0] = h->prof.ms[1] = 0;
+    h->prof.count[0] = h->prof.count[1] = 0;
+    h->prof.bytes[0] = h->prof.bytes[1] = 0;
+  });
+}
+
+int svb_profile_read(svb_handle h, double* out) {
+  return guard([&] {
+    check_handle(h);
+    out[0] = h->prof.ms[0];
+    out[1] = (double)h->prof.count[0];
+    out[2] = h->prof.bytes[0];
+    out[3] = h->prof.ms[1];
+    out[4] = (double)h->prof.count[1];
+    out[5] = h->prof.bytes[1];
+  });
+}
+
+int svb_timer_start(svb_handle h) {
+  return guard([&] {
+    check_handle(h);
+    if (!h->t0) {
+      SVB_CUDA(cudaEventCreate(&h->t0));
+      SVB_CUDA(cudaEventCreate(&h->t1));
+    }
+    SVB_CUDA(cudaEventRecord(h->t0, h->st));
+  });
+}
+
+int svb_timer_stop(svb_handle h, double* ms) {
+  return guard([&] {
+    check_handle(h);
+    require(h->t0 != nullptr, SVB_E_ARG, "timer not started");
+    SVB_CUDA(cudaEventRecord(h->t1, h->st));
+    SVB_CUDA(cudaEventSynchronize(h->t1));
+    float t = 0.f;
+    SVB_CUDA(cudaEventElapsedTime(&t, h->t0, h->t1));
+    *ms = t;
+  });
+}
+
+int svb_marginal_probs(svb_handle h, const int32_t* qubits, int k, double* out) {
+  return guard([&] {
+    check_handle(h);
+    require(k >= 1 && k <= h->n, SVB_E_ARG, "bad qubit count");
+    for (int j = 0; j < k; ++j) {
+      require(qubits[j] >= 0 && qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
+      require(j == 0 || qubits[j] > qubits[j - 1], SVB_E_ARG, "qubits must be ascending");
+    }
+    uint64_t m = 1ull << k;
+    double* d_out = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_out, m * sizeof(double), h->st));
+    size_t wsd = marginal_ws_doubles(h->n, k);
+    ensure_ws(h, wsd + 1);
+    if (h->prec == SVB_C128) launch_marginal<double>(h->amps, h->n, qubits, k, d_out, h->d_ws, h->ws_doubles, h->st);
+    else launch_marginal<float>(h->amps, h->n, qubits, k, d_out, h->d_ws, h->ws_doubles, h->st);
+    SVB_CUDA(cudaMemcpyAsync(out, d_out, m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    SVB_CUDA(cudaFreeAsync(d_out, h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_expect_z(svb_handle h, const uint64_t* masks, int m, double* out) {
+  return guard([&] {
+    check_handle(h);
+    require(m >= 0, SVB_E_ARG, "bad mask count");
+    if (m == 0) return;
+    uint64_t full = (1ull << h->n) - 1;
+    for (int j = 0; j < m; ++j) require((masks[j] & ~full) == 0, SVB_E_ARG, "mask names a qubit out of range");
+    ensure_ws(h, expect_ws_doubles(h->n, m) + 64);
+    double* d_out = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_out, m * sizeof(double), h->st));
+    if (h->prec == SVB_C128) launch_expect_z<double>(h->amps, h->n, masks, m, d_out, h->d_ws, h->st);
+    else launch_expect_z<float>(h->amps, h->n, masks, m, d_out, h->d_ws, h->st);
+    SVB_CUDA(cudaMemcpyAsync(out, d_out, m * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    SVB_CUDA(cudaFreeAsync(d_out, h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_sample(svb_handle h, const int32_t* qubits, int k, const int32_t* bit_src, int w, uint64_t shots,
+               const uint64_t* pcg, int sampler, uint64_t* out_codes, uint64_t* out_counts,
+               uint64_t* n_unique) {
+  return guard([&] {
+    check_handle(h);
+    require(shots >= 1, SVB_E_ARG, "shots must be positive");
+    require(k >= 1 && k <= h->n, SVB_E_ARG, "bad measured-qubit count");
+    require(w >= 1 && w <= 63, SVB_E_ARG, "bad clbit count");
+    for (int j = 0; j < k; ++j) {
+      require(qubits[j] >= 0 && qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
+      require(j == 0 || qubits[j] > qubits[j - 1], SVB_E_ARG, "qubits must be ascending");
+    }
+    for (int p = 0; p < w; ++p) require(bit_src[p] >= 0 && bit_src[p] < k, SVB_E_ARG, "bad bit source");
+    require(sampler == SVB_SAMPLER_ALIAS || sampler == SVB_SAMPLER_CDF, SVB_E_ARG, "bad sampler");
+    cudaStream_t st = h->st;
+    uint64_t* d_codes = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_codes, shots * sizeof(uint64_t), st));
+    uint64_t m = 1ull << k;
+    bool full = (k == h->n);
+    if (sampler == SVB_SAMPLER_CDF && full && h->n >= 5) {
+      if (h->prec == SVB_C128) cdf_draw<double>(h->amps, h->n, shots, pcg, bit_src, w, d_codes, st);
+      else cdf_draw<float>(h->amps, h->n, shots, pcg, bit_src, w, d_codes, st);
+    } else {
+      double* d_probs = nullptr;
+      SVB_CUDA(cudaMallocAsync(&d_probs, m * sizeof(double), st));
+      ensure_ws(h, marginal_ws_doubles(h->n, k) + 1);
+      if (h->prec == SVB_C128) launch_marginal<double>(h->amps, h->n, qubits, k, d_probs, h->d_ws, h->ws_doubles, st);
+      else launch_marginal<float>(h->amps, h->n, qubits, k, d_probs, h->d_ws, h->ws_doubles, st);
+      if (sampler == SVB_SAMPLER_CDF) {
+        cdf_draw_probs(d_probs, m, shots, pcg, bit_src, w, d_codes, st);
+      } else {
+        double* d_prob_row = nullptr;
+        int64_t* d_alias = nullptr;
+        SVB_CUDA(cudaMallocAsync(&d_prob_row, m * sizeof(double), st));
+        SVB_CUDA(cudaMallocAsync(&d_alias, m * sizeof(int64_t), st));
+        try {
+          alias_build(d_probs, m, d_prob_row, d_alias, st);
+        } catch (...) {
+          cudaFreeAsync(d_prob_row, st);
+          cudaFreeAsync(d_alias, st);
+          cudaFreeAsync(d_probs, st);
+          cudaFreeAsync(d_codes, st);
+          throw;
+        }
+        alias_draw(d_prob_row, d_alias, m, shots, pcg, bit_src, w, d_codes, st);
+        SVB_CUDA(cudaFreeAsync(d_prob_row, st));
+        SVB_CUDA(cudaFreeAsync(d_alias, st));
+      }
+      SVB_CUDA(cudaFreeAsync(d_probs, st));
+    }
+    *n_unique = histogram_codes(d_codes, shots, w, out_codes, out_counts, st);
+    SVB_CUDA(cudaFreeAsync(d_codes, st));
+    SVB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_row, int64_t* alias_row) {
+  return guard([&] {
+    require(m >= 1, SVB_E_SAMPLING, "need a non-empty 1-D probability vector");
+    for (uint64_t i = 0; i < m; ++i) require(probs[i] >= 0.0, SVB_E_SAMPLING, "negative probability");
+    SVB_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    SVB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double *dp = nullptr, *dr = nullptr;
+    int64_t* da = nullptr;
+    try {
+      SVB_CUDA(cudaMallocAsync(&dp, m * sizeof(double), st));
+      SVB_CUDA(cudaMallocAsync(&dr, m * sizeof(double), st));
+      SVB_CUDA(cudaMallocAsync(&da, m * sizeof(int64_t), st));
+      SVB_CUDA(cudaMemcpyAsync(dp, probs, m * sizeof(double), cudaMemcpyHostToDevice, st));
+      alias_build(dp, m, dr, da, st);
+      SVB_CUDA(cudaMemcpyAsync(prob_row, dr, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+      SVB_CUDA(cudaMemcpyAsync(alias_row, da, m * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      SVB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaFreeAsync(dp, st); cudaFreeAsync(dr, st); cudaFreeAsync(da, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    cudaFreeAsync(dp, st); cudaFreeAsync(dr, st); cudaFreeAsync(da, st);
+    SVB_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  });
+}
+
+int svb_rng_seed(svb_handle h, const uint64_t* pcg) {
+  return guard([&] {
+    check_handle(h);
+    SVB_CUDA(cudaMemcpyAsync(h->d_rng, pcg, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+static void do_measure(svb_handle h, int q, bool reset, uint64_t* d_code, int rank) {
+  require(q >= 0 && q < h->n, SVB_E_ARG, "qubit out of range");
+  ensure_ws(h, measure_ws_doubles(h->n) + 1);
+  if (h->prec == SVB_C128)
+    launch_measure<double>(h->amps, h->n, q, reset, h->d_rng, h->d_ws, h->d_outcome, d_code, rank, h->st);
+  else
+    launch_measure<float>(h->amps, h->n, q, reset, h->d_rng, h->d_ws, h->d_outcome, d_code, rank, h->st);
+}
+
+int svb_measure(svb_handle h, int qubit, int32_t* outcome) {
+  return guard([&] {
+    check_handle(h);
+    do_measure(h, qubit, false, nullptr, 0);
+    SVB_CUDA(cudaMemcpyAsync(outcome, h->d_outcome, sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_reset(svb_handle h, int qubit) {
+  return guard([&] {
+    check_handle(h);
+    do_measure(h, qubit, true, nullptr, 0);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops, const svb_gate* gates,
+               const int32_t* clbit_rank, uint64_t shots, const uint64_t* pcg, uint64_t* out_codes) {
+  return guard([&] {
+    check_handle(work);
+    check_handle(prefix);
+    require(work->n == prefix->n && work->prec == prefix->prec, SVB_E_ARG, "state shape mismatch");
+    require(work->device == prefix->device, SVB_E_ARG, "states on different devices");
+    cudaStream_t st = work->st;
+    // prefix may have pending work on its own stream
+    SVB_CUDA(cudaStreamSynchronize(prefix->st));
+    int ngates = 0;
+    for (int i = 0; i < n_ops; ++i) {
+      int kind = ops[3 * i];
+      require(kind >= 0 && kind <= 2, SVB_E_ARG, "bad replay op");
+      if (kind == 0) ngates = std::max(ngates, ops[3 * i + 1] + 1);
+    }
+    validate_gates(work, gates, ngates);
+    uint64_t* d_codes = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_codes, shots * sizeof(uint64_t), st));
+    SVB_CUDA(cudaMemsetAsync(d_codes, 0, shots * sizeof(uint64_t), st));
+    SVB_CUDA(cudaMemcpyAsync(work->d_rng, pcg, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    ensure_ws(work, measure_ws_doubles(work->n) + 1);
+    work->stats = ProgramStats{};
+    for (uint64_t s = 0; s < shots; ++s) {
+      SVB_CUDA(cudaMemcpyAsync(work->amps, prefix->amps, prefix->amp_bytes(), cudaMemcpyDeviceToDevice, st));
+      int i = 0;
+      while (i < n_ops) {
+        int kind = ops[3 * i];
+        if (kind == 0) {  // maximal run of gates -> one program
+          int j = i;
+          std::vector<svb_gate> run;
+          while (j < n_ops && ops[3 * j] == 0) run.push_back(gates[ops[3 * j + 1]]), ++j;
+          if (work->prec == SVB_C128)
+            run_program_owned<double>(&work->amps, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+          else
+            run_program_owned<float>(&work->amps, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+          i = j;
+        } else {
+          int q = ops[3 * i + 1];
+          if (kind == 1) do_measure(work, q, false, d_codes + s, clbit_rank[ops[3 * i + 2]]);
+          else do_measure(work, q, true, nullptr, 0);
+          ++i;
+        }
+      }
+    }
+    SVB_CUDA(cudaMemcpyAsync(out_codes, d_codes, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SVB_CUDA(cudaFreeAsync(d_codes, st));
+    SVB_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,349 @@
+// sm_100a fused gate-pass kernel and the qubit-permutation pass.
+//
+// k_pass: one CTA per tile of 2^m amplitudes (the tile qubit set S always
+// contains physical qubits 0..4).  Each thread holds 2^RB amplitudes in
+// registers.  Round 0 loads straight from HBM (lanes <-> qubits 0..4, so each
+// warp-wide load is 32 consecutive amplitudes = 512 B for complex128); later
+// rounds re-distribute the tile through XOR-swizzled shared memory; the last
+// layout stores straight back to HBM.  HBM traffic per pass is one read and
+// one write of the state (2·s·2^n bytes) regardless of how many gates the
+// pass applies.
+//
+// k_permute: out-of-place bit permutation of the index (restores the qubit
+// order after swap relabeling).  Tiles cover input bits 0..4 plus the input
+// bits that land on output bits 0..4, so both the reads and the writes are
+// 32-amplitude contiguous runs.
+#include <algorithm>
+#include <cstring>
+
+#include "kernels.h"
+#include "program.h"
+
+namespace svb {
+
+template <typename R, int RB>
+__global__ void __launch_bounds__(256, 2)
+    k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx<R>* sm = reinterpret_cast<cplx<R>*>(smraw);
+  __shared__ PassDev pd;
+  {
+    const int4* src = reinterpret_cast<const int4*>(pdg);
+    int4* dst = reinterpret_cast<int4*>(&pd);
+    for (int i = threadIdx.x; i < (int)(sizeof(PassDev) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  constexpr int V = 1 << RB;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t base = tile_base(pd, blockIdx.x);
+  cplx<R> a[V];
+  uint32_t Fl;
+  uint64_t Fg;
+  uint64_t goff[RB];
+  uint32_t loff[RB];
+  {
+    const RoundDev& rd = pd.rounds[0];
+    thread_fixed(pd, rd, tid, base, &Fl, &Fg);
+#pragma unroll
+    for (int i = 0; i < RB; ++i) goff[i] = 1ull << pd.pos[rd.reg_local[i]];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uint64_t g = Fg;
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        if ((v >> i) & 1) g |= goff[i];
+      a[v] = __ldcs(state + g);
+    }
+    run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end);
+  }
+  for (int k = 1; k < pd.nrounds; ++k) {
+    // write the previous layout
+    {
+      const RoundDev& rp = pd.rounds[k - 1];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) loff[i] = 1u << rp.reg_local[i];
+      if (k > 1) __syncthreads();
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uint32_t l = Fl;
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+          if ((v >> i) & 1) l |= loff[i];
+        sm[swz<R>(l)] = a[v];
+      }
+    }
+    __syncthreads();
+    const RoundDev& rd = pd.rounds[k];
+    thread_fixed(pd, rd, tid, base, &Fl, &Fg);
+#pragma unroll
+    for (int i = 0; i < RB; ++i) loff[i] = 1u << rd.reg_local[i];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uint32_t l = Fl;
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        if ((v >> i) & 1) l |= loff[i];
+      a[v] = sm[swz<R>(l)];
+    }
+    run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end);
+  }
+  {
+    const RoundDev& rd = pd.rounds[pd.nrounds - 1];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) goff[i] = 1ull << pd.pos[rd.reg_local[i]];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      uint64_t g = Fg;
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        if ((v >> i) & 1) g |= goff[i];
+      __stcs(state + g, a[v]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- permute
+struct PermDev {
+  int32_t n, ml;        // tile local bits
+  int32_t lin[12];      // input bit of local bit l (ascending)
+  int32_t lout_src[12]; // output-local bit e (ascending output positions) -> input-local bit
+  int32_t lout_pos[12]; // output bit of output-local bit e
+  int32_t nout;
+  int32_t outin[48];    // input bits outside the tile, ascending
+  int32_t dest[64];     // output bit of input bit p
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_permute(const cplx<R>* __restrict__ in, cplx<R>* __restrict__ out,
+                                                 PermDev pd) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx<R>* sm = reinterpret_cast<cplx<R>*>(smraw);
+  const uint64_t t = blockIdx.x;
+  uint64_t bin = 0, bout = 0;
+  for (int i = 0; i < pd.nout; ++i)
+    if ((t >> i) & 1ull) {
+      bin |= 1ull << pd.outin[i];
+      bout |= 1ull << pd.dest[pd.outin[i]];
+    }
+  const uint32_t T = 1u << pd.ml;
+  for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
+    uint64_t g = bin;
+    for (int l = 0; l < pd.ml; ++l)
+      if ((j >> l) & 1u) g |= 1ull << pd.lin[l];
+    sm[j] = __ldcs(in + g);
+  }
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < T; o += blockDim.x) {
+    uint64_t g = bout;
+    uint32_t j = 0;
+    for (int e = 0; e < pd.ml; ++e)
+      if ((o >> e) & 1u) {
+        g |= 1ull << pd.lout_pos[e];
+        j |= 1u << pd.lout_src[e];
+      }
+    __stcs(out + g, sm[j]);
+  }
+}
+
+static PermDev make_perm(int n, const std::vector<int>& dest) {
+  PermDev pd{};
+  pd.n = n;
+  uint64_t inset = 0x1full;
+  for (int p = 0; p < n; ++p)
+    if (dest[p] < 5) inset |= 1ull << p;
+  int ml = 0;
+  for (int p = 0; p < n; ++p)
+    if (inset & (1ull << p)) pd.lin[ml++] = p;
+  pd.ml = ml;
+  // output-local order: ascending output bit positions of the tile's bits
+  std::vector<std::pair<int, int>> outs;  // (output bit, input-local bit)
+  for (int l = 0; l < ml; ++l) outs.push_back({dest[pd.lin[l]], l});
+  std::sort(outs.begin(), outs.end());
+  for (int e = 0; e < ml; ++e) {
+    pd.lout_pos[e] = outs[e].first;
+    pd.lout_src[e] = outs[e].second;
+  }
+  pd.nout = 0;
+  for (int p = 0; p < n; ++p)
+    if (!(inset & (1ull << p))) pd.outin[pd.nout++] = p;
+  for (int p = 0; p < n; ++p) pd.dest[p] = dest[p];
+  return pd;
+}
+
+// --------------------------------------------------------------- profiler
+void Profiler::begin(cudaStream_t st, int kind, double nbytes) {
+  Rec r;
+  SVB_CUDA(cudaEventCreate(&r.a));
+  SVB_CUDA(cudaEventCreate(&r.b));
+  r.kind = kind;
+  SVB_CUDA(cudaEventRecord(r.a, st));
+  pending.push_back(r);
+  bytes[kind] += nbytes;
+}
+void Profiler::end(cudaStream_t st) { SVB_CUDA(cudaEventRecord(pending.back().b, st)); }
+void Profiler::collect() {
+  for (Rec& r : pending) {
+    float t = 0.f;
+    SVB_CUDA(cudaEventSynchronize(r.b));
+    SVB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    count[r.kind] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  pending.clear();
+}
+
+// ------------------------------------------------------------ run_program
+template <typename R> static constexpr int rb_of() { return sizeof(R) == 8 ? 4 : 5; }
+
+template <typename R>
+static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats) {
+  constexpr int RB = rb_of<R>();
+  if (prog.passes.empty()) return;
+  size_t pbytes = prog.passes.size() * sizeof(PassDev);
+  size_t obytes = std::max<size_t>(prog.ops.size(), 16);
+  uint8_t* dbuf = nullptr;
+  SVB_CUDA(cudaMallocAsync(&dbuf, pbytes + obytes, st));
+  SVB_CUDA(cudaMemcpyAsync(dbuf, prog.passes.data(), pbytes, cudaMemcpyHostToDevice, st));
+  if (!prog.ops.empty())
+    SVB_CUDA(cudaMemcpyAsync(dbuf + pbytes, prog.ops.data(), prog.ops.size(), cudaMemcpyHostToDevice, st));
+  const PassDev* dpass = reinterpret_cast<const PassDev*>(dbuf);
+  const uint8_t* dops = dbuf + pbytes;
+  SVB_CUDA(cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  for (size_t p = 0; p < prog.passes.size(); ++p) {
+    const PassDev& pd = prog.passes[p];
+    uint64_t tiles = 1ull << pd.nout;
+    unsigned threads = 1u << (pd.m - RB);
+    Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
+    if (pf) pf->begin(st, 0, 2.0 * (double)(sizeof(cplx<R>) << n));
+    k_pass<R, RB><<<(unsigned)tiles, threads, sizeof(cplx<R>) << pd.m, st>>>(state, dpass + p, dops);
+    SVB_CHECK_LAUNCH();
+    if (pf) pf->end(st);
+    stats->passes += 1;
+    stats->launches += 1;
+  }
+  SVB_CUDA(cudaFreeAsync(dbuf, st));
+}
+
+template <typename R>
+static void launch_permute(cplx<R>** state, int n, const std::vector<int>& dest, cudaStream_t st,
+                           ProgramStats* stats) {
+  PermDev pd = make_perm(n, dest);
+  cplx<R>* out = nullptr;
+  size_t bytes = sizeof(cplx<R>) << n;
+  SVB_CUDA(cudaMalloc(&out, bytes));
+  uint64_t tiles = 1ull << pd.nout;
+  Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
+  if (pf) pf->begin(st, 1, 2.0 * (double)bytes);
+  k_permute<R><<<(unsigned)tiles, 256, sizeof(cplx<R>) << pd.ml, st>>>(*state, out, pd);
+  SVB_CHECK_LAUNCH();
+  if (pf) pf->end(st);
+  // swap buffers rather than copy back (a copy would double the traffic);
+  // cudaFree synchronizes with the permute kernel before releasing the input
+  SVB_CUDA(cudaFree(*state));
+  *state = out;
+  stats->passes += 1;
+  stats->launches += 1;
+}
+
+template <typename R>
+void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int max_high, cudaStream_t st,
+                 ProgramStats* stats) {
+  (void)max_high;
+  stats->gates += ng;
+  const SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
+  if (!fusion || n < opt.rb + 5) {
+    for (int i = 0; i < ng; ++i) {
+      launch_gate_basic<R>(state, n, g[i], st);
+      stats->passes += 1;
+      stats->launches += 1;
+    }
+    return;
+  }
+  SchedOptions o = opt;
+  o.relabel_swaps = false;  // the handle owns its buffer; permutation passes need run_program_owned
+  Program prog = build_program<R>(n, g, ng, o);
+  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats);
+}
+
+template <typename R>
+void run_program_owned(void** state, int n, const svb_gate* g, int ng, int fusion, cudaStream_t st,
+                       ProgramStats* stats) {
+  stats->gates += ng;
+  SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
+  if (!fusion || n < opt.rb + 5) {
+    for (int i = 0; i < ng; ++i) {
+      launch_gate_basic<R>(*state, n, g[i], st);
+      stats->passes += 1;
+      stats->launches += 1;
+    }
+    return;
+  }
+  // swap relabeling needs a second state-sized buffer for the final permutation
+  size_t fr = 0, tot = 0;
+  SVB_CUDA(cudaMemGetInfo(&fr, &tot));
+  opt.relabel_swaps = fr > (sizeof(cplx<R>) << n) + (256ull << 20);
+  Program prog = build_program<R>(n, g, ng, opt);
+  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats);
+  if (!prog.final_perm.empty()) {
+    cplx<R>* s = static_cast<cplx<R>*>(*state);
+    launch_permute<R>(&s, n, prog.final_perm, st, stats);
+    *state = s;
+  }
+}
+
+template void run_program<float>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
+template void run_program<double>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
+template void run_program_owned<float>(void**, int, const svb_gate*, int, int, cudaStream_t, ProgramStats*);
+template void run_program_owned<double>(void**, int, const svb_gate*, int, int, cudaStream_t, ProgramStats*);
+
+}  // namespace svb
+
+using namespace svb;
+
+extern "C" {
+
+// Schedule a gate program on the host only (no GPU needed): pass/round/op
+// statistics for tests and the design notes.
+int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_passes, int64_t* n_rounds,
+             int64_t* op_bytes, int32_t* has_perm) {
+  try {
+    SchedOptions o = default_options(precision, n);
+    Program p = precision == SVB_C128 ? build_program<double>(n, gates, ng, o) : build_program<float>(n, gates, ng, o);
+    int64_t r = 0;
+    for (auto& pd : p.passes) r += pd.nrounds;
+    *n_passes = (int64_t)p.passes.size();
+    *n_rounds = r;
+    *op_bytes = (int64_t)p.ops.size();
+    *has_perm = p.final_perm.empty() ? 0 : 1;
+    return SVB_OK;
+  } catch (const Error& e) {
+    return e.code;
+  }
+}
+
+// CPU emulation of the fused program (same scheduler, same op interpreter);
+// amps are complex128 in/out.  Test hook for the scheduler without a GPU.
+int svb_emulate_apply(int n, int precision, const svb_gate* gates, int ng, double* amps, int relabel) {
+  try {
+    SchedOptions o = default_options(precision, n);
+    o.relabel_swaps = relabel != 0;
+    uint64_t len = 1ull << n;
+    if (precision == SVB_C128) {
+      Program p = build_program<double>(n, gates, ng, o);
+      emulate_program<double>(reinterpret_cast<double2*>(amps), n, p);
+    } else {
+      Program p = build_program<float>(n, gates, ng, o);
+      std::vector<float2> s(len);
+      for (uint64_t i = 0; i < len; ++i) s[i] = make_float2((float)amps[2 * i], (float)amps[2 * i + 1]);
+      emulate_program<float>(s.data(), n, p);
+      for (uint64_t i = 0; i < len; ++i) { amps[2 * i] = s[i].x; amps[2 * i + 1] = s[i].y; }
+    }
+    return SVB_OK;
+  } catch (const Error& e) {
+    return e.code;
+  }
+}
+
+}  // extern "C"

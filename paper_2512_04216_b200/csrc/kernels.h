@@ -1,0 +1,51 @@
+// Internal launcher declarations shared by the libsvb translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/svb.h"
+
+namespace svb {
+
+// gates_basic.cu — one HBM pass per gate
+template <typename R> void launch_gate_basic(void* state, int n, const svb_gate& g, cudaStream_t st);
+template <typename R> void launch_zero(void* state, int n, cudaStream_t st);
+
+// measure.cu — reductions over the state
+template <typename R>
+void launch_marginal(const void* state, int n, const int32_t* qubits, int k, double* d_out,
+                     double* d_ws, size_t ws_doubles, cudaStream_t st);
+size_t marginal_ws_doubles(int n, int k);
+template <typename R>
+void launch_expect_z(const void* state, int n, const uint64_t* h_masks, int m, double* d_out,
+                     double* d_ws, cudaStream_t st);
+size_t expect_ws_doubles(int n, int m);
+// Measure/reset qubit q with the device PCG64 stream d_rng; outcome recorded in
+// d_out[0] (int32) and, when d_codes != nullptr, OR-ed into d_codes[0] << rank.
+template <typename R>
+void launch_measure(void* state, int n, int q, bool reset, uint64_t* d_rng, double* d_ws,
+                    int32_t* d_outcome, uint64_t* d_code, int rank, cudaStream_t st);
+size_t measure_ws_doubles(int n);
+
+// sample.cu — PCG64, pairwise sum, alias table, samplers, histogram
+void host_pcg_advance(uint64_t* pcg4, uint64_t delta);
+double pairwise_sum_device(const double* d_x, uint64_t m, double* d_ws, cudaStream_t st);
+struct SampleOut {
+  uint64_t* codes;
+  uint64_t* counts;
+  uint64_t n_unique;
+};
+void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_alias_row,
+                 cudaStream_t st);
+void alias_draw(const double* d_prob_row, const int64_t* d_alias_row, uint64_t m, uint64_t shots,
+                const uint64_t* pcg, const int32_t* bit_src, int w, uint64_t* d_codes,
+                cudaStream_t st);
+template <typename R>
+void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
+              int w, uint64_t* d_codes, cudaStream_t st);
+void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
+                    const int32_t* bit_src, int w, uint64_t* d_codes, cudaStream_t st);
+uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_codes,
+                         uint64_t* h_counts, cudaStream_t st);
+
+}  // namespace svb

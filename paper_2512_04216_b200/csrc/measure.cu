@@ -1,0 +1,275 @@
+// Read-only reductions over the state vector (HBM-bound, s·2^n bytes read):
+//   * marginal probabilities      — marginal_probs, statevector.py:131-139
+//   * multi-mask <Z_mask>         — expectation,    statevector.py:277-292
+//   * measure / reset collapse    — _measure_qubit / _reset_qubit, statevector.py:142-154
+// Every reduction has a fixed, size-determined partition and a fixed combine
+// order, so results are bitwise reproducible run to run (seed determinism,
+// SPEC.md:155).
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svb {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-order block sum (blockDim.x == 256); result valid in thread 0.
+__device__ __forceinline__ double block_sum256(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    r = ((sh[0] + sh[1]) + (sh[2] + sh[3])) + ((sh[4] + sh[5]) + (sh[6] + sh[7]));
+  }
+  __syncthreads();
+  return r;
+}
+
+static inline int reduce_blocks(uint64_t work) {
+  // size-determined (not device-determined) so results are reproducible anywhere
+  uint64_t b = work / 4096;
+  if (b < 1) b = 1;
+  if (b > 2048) b = 2048;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------- marginals
+template <typename R>
+__global__ void k_probs_full(const cplx<R>* __restrict__ s, double* __restrict__ out, uint64_t len) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    cplx<R> a = s[i];
+    double x = (double)a.x, y = (double)a.y;
+    out[i] = x * x + y * y;
+  }
+}
+
+__device__ __forceinline__ uint64_t deposit(uint64_t v, uint64_t mask) {
+  uint64_t r = 0;
+  for (uint64_t bb = 1; mask; bb <<= 1) {
+    uint64_t low = mask & (~mask + 1);
+    if (v & bb) r |= low;
+    mask &= mask - 1;
+  }
+  return r;
+}
+
+// partial[o * nch + ch] = sum over r in chunk ch of |a[dep(o,Q) | dep(r,~Q)]|^2
+template <typename R>
+__global__ void k_marg_partial(const cplx<R>* __restrict__ s, uint64_t qmask, uint64_t rmask,
+                               uint64_t rlen, uint64_t nch, uint64_t chunk, double* partial) {
+  __shared__ double sh[8];
+  const uint64_t blk = blockIdx.x;
+  const uint64_t o = blk / nch, ch = blk % nch;
+  const uint64_t obase = deposit(o, qmask);
+  double acc = 0.0;
+  uint64_t r0 = ch * chunk, r1 = r0 + chunk < rlen ? r0 + chunk : rlen;
+  for (uint64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    cplx<R> a = s[obase | deposit(r, rmask)];
+    double x = (double)a.x, y = (double)a.y;
+    acc += x * x + y * y;
+  }
+  double t = block_sum256(acc, sh);
+  if (threadIdx.x == 0) partial[blk] = t;
+}
+
+__global__ void k_sum_rows(const double* __restrict__ partial, uint64_t rows, uint64_t cols,
+                           double* __restrict__ out) {
+  uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= rows) return;
+  double acc = 0.0;
+  for (uint64_t c = 0; c < cols; ++c) acc += partial[o * cols + c];
+  out[o] = acc;
+}
+
+static void marg_geometry(int n, int k, uint64_t* nch, uint64_t* chunk) {
+  uint64_t rlen = 1ull << (n - k);
+  *chunk = rlen < 16384 ? rlen : 16384;
+  *nch = (rlen + *chunk - 1) / *chunk;
+}
+
+size_t marginal_ws_doubles(int n, int k) {
+  if (k == n) return 0;
+  uint64_t nch, chunk;
+  marg_geometry(n, k, &nch, &chunk);
+  return (size_t)((1ull << k) * nch);
+}
+
+template <typename R>
+void launch_marginal(const void* state, int n, const int32_t* qubits, int k, double* d_out,
+                     double* d_ws, size_t ws_doubles, cudaStream_t st) {
+  const cplx<R>* s = static_cast<const cplx<R>*>(state);
+  if (k == n) {
+    uint64_t len = 1ull << n;
+    k_probs_full<R><<<grid_for(len, 256), 256, 0, st>>>(s, d_out, len);
+    SVB_CHECK_LAUNCH();
+    return;
+  }
+  uint64_t qmask = 0;
+  for (int j = 0; j < k; ++j) qmask |= 1ull << qubits[j];
+  uint64_t full = (n == 64) ? ~0ull : ((1ull << n) - 1);
+  uint64_t rmask = full & ~qmask;
+  uint64_t nch, chunk;
+  marg_geometry(n, k, &nch, &chunk);
+  uint64_t rows = 1ull << k;
+  require(ws_doubles >= rows * nch, SVB_E_ARG, "marginal workspace too small");
+  uint64_t nblk = rows * nch;
+  require(nblk < (1ull << 31), SVB_E_ARG, "marginal grid too large");
+  k_marg_partial<R><<<(unsigned)nblk, 256, 0, st>>>(s, qmask, rmask, 1ull << (n - k), nch, chunk, d_ws);
+  SVB_CHECK_LAUNCH();
+  k_sum_rows<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(d_ws, rows, nch, d_out);
+  SVB_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------- multi-mask <Z...Z>
+constexpr int kMaskBatch = 32;
+struct MaskSet { uint64_t m[kMaskBatch]; };
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_expect_partial(const cplx<R>* __restrict__ s, uint64_t len,
+                                                        MaskSet ms, int nm, double* partial) {
+  __shared__ double sh[8];
+  double acc[kMaskBatch];
+#pragma unroll
+  for (int j = 0; j < kMaskBatch; ++j) acc[j] = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    cplx<R> a = s[i];
+    double x = (double)a.x, y = (double)a.y;
+    double p = x * x + y * y;
+#pragma unroll
+    for (int j = 0; j < kMaskBatch; ++j)
+      if (j < nm) acc[j] += (__popcll(i & ms.m[j]) & 1) ? -p : p;
+  }
+  for (int j = 0; j < nm; ++j) {
+    double t = block_sum256(acc[j], sh);
+    if (threadIdx.x == 0) partial[(uint64_t)j * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+size_t expect_ws_doubles(int n, int m) {
+  return (size_t)reduce_blocks(1ull << n) * (size_t)kMaskBatch;
+}
+
+template <typename R>
+void launch_expect_z(const void* state, int n, const uint64_t* h_masks, int m, double* d_out,
+                     double* d_ws, cudaStream_t st) {
+  const cplx<R>* s = static_cast<const cplx<R>*>(state);
+  uint64_t len = 1ull << n;
+  int G = reduce_blocks(len);
+  for (int b = 0; b < m; b += kMaskBatch) {
+    int nm = m - b < kMaskBatch ? m - b : kMaskBatch;
+    MaskSet ms;
+    for (int j = 0; j < kMaskBatch; ++j) ms.m[j] = j < nm ? h_masks[b + j] : 0;
+    k_expect_partial<R><<<G, 256, 0, st>>>(s, len, ms, nm, d_ws);
+    SVB_CHECK_LAUNCH();
+    k_sum_rows<<<(nm + 255) / 256, 256, 0, st>>>(d_ws, nm, G, d_out + b);
+    SVB_CHECK_LAUNCH();
+  }
+}
+
+// ------------------------------------------------------------ measure/reset
+__device__ __forceinline__ double pcg_next_double(uint64_t* rng);
+
+template <typename R>
+__global__ void k_p1_partial(const cplx<R>* __restrict__ s, uint64_t npairs, int q, double* partial) {
+  __shared__ double sh[8];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t bit = 1ull << q;
+  double acc = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
+    cplx<R> a = s[insert0(i, q) | bit];
+    double x = (double)a.x, y = (double)a.y;
+    acc += x * x + y * y;
+  }
+  double t = block_sum256(acc, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+// numpy PCG64 (XSL-RR 128/64), one step per draw — see sample.cu for the derivation.
+__device__ __forceinline__ double pcg_next_double(uint64_t* rng) {
+  const unsigned __int128 mult =
+      ((unsigned __int128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+  unsigned __int128 st = ((unsigned __int128)rng[0] << 64) | rng[1];
+  unsigned __int128 inc = ((unsigned __int128)rng[2] << 64) | rng[3];
+  st = st * mult + inc;
+  rng[0] = (uint64_t)(st >> 64);
+  rng[1] = (uint64_t)st;
+  uint64_t hi = (uint64_t)(st >> 64), lo = (uint64_t)st;
+  uint64_t x = hi ^ lo;
+  unsigned r = (unsigned)(hi >> 58);
+  uint64_t v = (x >> r) | (x << ((64u - r) & 63u));
+  return (double)(v >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ws[0..G) partials; ws[G] = scale; d_outcome[0] = outcome
+__global__ void k_measure_decide(double* ws, int G, uint64_t* rng, int32_t* d_outcome,
+                                 uint64_t* d_code, int rank) {
+  if (threadIdx.x != 0) return;
+  double p1 = 0.0;
+  for (int b = 0; b < G; ++b) p1 += ws[b];
+  double u = pcg_next_double(rng);
+  int out = (u < p1) ? 1 : 0;
+  double p = out ? p1 : 1.0 - p1;
+  ws[G] = 1.0 / sqrt(p);
+  d_outcome[0] = out;
+  if (d_code) d_code[0] = (d_code[0] & ~(1ull << rank)) | ((uint64_t)out << rank);  // last write wins
+}
+
+template <typename R>
+__global__ void k_collapse(cplx<R>* __restrict__ s, uint64_t npairs, int q, const double* ws, int G,
+                           const int32_t* d_outcome, int reset) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t bit = 1ull << q;
+  const int out = d_outcome[0];
+  const R sc = (R)ws[G];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs; i += stride) {
+    uint64_t i0 = insert0(i, q), i1 = i0 | bit;
+    cplx<R> keep = out ? s[i1] : s[i0];
+    keep.x *= sc;
+    keep.y *= sc;
+    cplx<R> z = mk<R>(R(0), R(0));
+    if (reset || !out) {
+      s[i0] = keep;
+      s[i1] = z;
+    } else {
+      s[i0] = z;
+      s[i1] = keep;
+    }
+  }
+}
+
+size_t measure_ws_doubles(int n) { return (size_t)reduce_blocks(1ull << (n - 1)) + 1; }
+
+template <typename R>
+void launch_measure(void* state, int n, int q, bool reset, uint64_t* d_rng, double* d_ws,
+                    int32_t* d_outcome, uint64_t* d_code, int rank, cudaStream_t st) {
+  cplx<R>* s = static_cast<cplx<R>*>(state);
+  uint64_t np = 1ull << (n - 1);
+  int G = reduce_blocks(np);
+  k_p1_partial<R><<<G, 256, 0, st>>>(s, np, q, d_ws);
+  SVB_CHECK_LAUNCH();
+  k_measure_decide<<<1, 32, 0, st>>>(d_ws, G, d_rng, d_outcome, d_code, rank);
+  SVB_CHECK_LAUNCH();
+  k_collapse<R><<<grid_for(np, 256), 256, 0, st>>>(s, np, q, d_ws, G, d_outcome, reset ? 1 : 0);
+  SVB_CHECK_LAUNCH();
+}
+
+#define INST(R)                                                                                 \
+  template void launch_marginal<R>(const void*, int, const int32_t*, int, double*, double*,     \
+                                   size_t, cudaStream_t);                                       \
+  template void launch_expect_z<R>(const void*, int, const uint64_t*, int, double*, double*,    \
+                                   cudaStream_t);                                               \
+  template void launch_measure<R>(void*, int, int, bool, uint64_t*, double*, int32_t*, uint64_t*, \
+                                  int, cudaStream_t);
+INST(float)
+INST(double)
+
+}  // namespace svb

@@ -1,0 +1,522 @@
+// Host-side gate fusion, pass scheduling and op encoding; CPU emulation of a
+// scheduled program.
+//
+// Pipeline (replaces the reference's one-numpy-pass-per-gate loop,
+// statevector.py:210-212 / 269-272):
+//  1. swap relabeling: an exact SWAP permutes the logical->physical qubit map
+//     instead of moving data; one permutation pass restores the order at the end;
+//  2. forward fusion: a gate merges into the open block of its qubit(s)
+//     (1q into 1q/2q blocks, 2q into the 2q block on the same pair), so
+//     cx·u·cx·u·u (the conftest controlled phase) fuses to one diagonal;
+//  3. classification: diagonal terms, 1q dense / anti-diagonal ops (with fixed
+//     controls when a 2q block preserves one of its qubits), 2q monomial or
+//     dense ops;
+//  4. pass scheduling: greedy over the op list with commutation (ops commute
+//     when every shared qubit is acted on diagonally by both); a pass admits
+//     an op when its active qubits fit in the tile set S (|S| = m);
+//  5. rounds: consecutive ops whose active qubits fit in RB register bits.
+#include <algorithm>
+#include <cstddef>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "program.h"
+
+namespace svb {
+
+using cd = std::complex<double>;
+
+namespace {
+
+struct Block {
+  int k;
+  int q[2];
+  cd M[16];
+};
+
+struct FOp {
+  int type;                               // OP_DIAG, OP_U1, OP_U1ANTI, OP_U2, OP_PERM2
+  int q[2];                               // DIAG: qa, qb(-1); U1: target; U2/PERM2: (qa, qb)
+  std::vector<std::pair<int, int>> conds; // (qubit, value) fixed controls (U1 only)
+  cd c[16];
+  int src[4];
+  uint64_t touched = 0, active = 0;
+};
+
+inline bool zero(cd z) { return z.real() == 0.0 && z.imag() == 0.0; }
+inline bool one(cd z) { return z.real() == 1.0 && z.imag() == 0.0; }
+
+// new = G(on q of block) * block.M
+void left_mul_1q(Block& b, int q, const cd* g) {
+  if (b.k == 1) {
+    cd r[4];
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) r[i * 2 + j] = g[i * 2 + 0] * b.M[0 * 2 + j] + g[i * 2 + 1] * b.M[1 * 2 + j];
+    std::copy(r, r + 4, b.M);
+    return;
+  }
+  int bitpos = (q == b.q[0]) ? 0 : 1;
+  cd r[16];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      int bi = (i >> bitpos) & 1;
+      int i0 = i & ~(1 << bitpos), i1 = i | (1 << bitpos);
+      r[i * 4 + j] = g[bi * 2 + 0] * b.M[i0 * 4 + j] + g[bi * 2 + 1] * b.M[i1 * 4 + j];
+    }
+  std::copy(r, r + 16, b.M);
+}
+
+// new = G(on (qa,qb) in gate order) * block.M   (block is 2q on the same pair)
+void left_mul_2q(Block& b, int qa, int qb, const cd* g) {
+  cd gg[16];
+  if (qa == b.q[0]) {
+    std::copy(g, g + 16, gg);
+  } else {  // reorder the gate into the block's (q0, q1) basis: swap bit roles
+    auto sw = [](int i) { return ((i & 1) << 1) | ((i >> 1) & 1); };
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) gg[sw(i) * 4 + sw(j)] = g[i * 4 + j];
+  }
+  cd r[16];
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      cd acc = 0;
+      for (int k = 0; k < 4; ++k) acc += gg[i * 4 + k] * b.M[k * 4 + j];
+      r[i * 4 + j] = acc;
+    }
+  std::copy(r, r + 16, b.M);
+}
+
+void emit_block(const Block& b, std::vector<FOp>& out) {
+  if (b.k == 1) {
+    FOp f;
+    f.q[0] = b.q[0];
+    f.q[1] = -1;
+    f.touched = 1ull << b.q[0];
+    const cd* M = b.M;
+    if (zero(M[1]) && zero(M[2])) {
+      if (one(M[0]) && one(M[3])) return;  // identity
+      f.type = OP_DIAG;
+      f.c[0] = M[0]; f.c[1] = M[3]; f.c[2] = M[0]; f.c[3] = M[3];
+    } else {
+      f.type = (zero(M[0]) && zero(M[3])) ? OP_U1ANTI : OP_U1;
+      std::copy(M, M + 4, f.c);
+      f.active = f.touched;
+    }
+    out.push_back(f);
+    return;
+  }
+  const cd* M = b.M;
+  const int qa = b.q[0], qb = b.q[1];
+  bool diag = true, pres_a = true, pres_b = true;
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) {
+      if (zero(M[r * 4 + c])) continue;
+      if (r != c) diag = false;
+      if ((r & 1) != (c & 1)) pres_a = false;
+      if ((r & 2) != (c & 2)) pres_b = false;
+    }
+  uint64_t touched = (1ull << qa) | (1ull << qb);
+  if (diag) {
+    bool ident = true;
+    for (int r = 0; r < 4; ++r) ident = ident && one(M[r * 5]);
+    if (ident) return;
+    FOp f;
+    f.type = OP_DIAG;
+    f.q[0] = qa; f.q[1] = qb;
+    for (int r = 0; r < 4; ++r) f.c[r] = M[r * 5];
+    f.touched = touched;
+    out.push_back(f);
+    return;
+  }
+  if (pres_a || pres_b) {
+    // controlled structure: for each value of the preserved qubit, a 2x2 on the other
+    const int ctl = pres_a ? qa : qb, tgt = pres_a ? qb : qa;
+    const int cbit = pres_a ? 1 : 2, tbit = pres_a ? 2 : 1;
+    for (int v = 0; v < 2; ++v) {
+      int i0 = v ? cbit : 0, i1 = i0 | tbit;
+      cd U[4] = {M[i0 * 4 + i0], M[i0 * 4 + i1], M[i1 * 4 + i0], M[i1 * 4 + i1]};
+      if (zero(U[1]) && zero(U[2]) && one(U[0]) && one(U[3])) continue;
+      FOp f;
+      f.touched = touched;
+      if (zero(U[1]) && zero(U[2])) {  // conditional diagonal -> 2q diag term
+        f.type = OP_DIAG;
+        f.q[0] = qa; f.q[1] = qb;
+        for (int r = 0; r < 4; ++r) f.c[r] = 1.0;
+        f.c[i0] = U[0];
+        f.c[i1] = U[3];
+        out.push_back(f);
+        continue;
+      }
+      f.type = (zero(U[0]) && zero(U[3])) ? OP_U1ANTI : OP_U1;
+      f.q[0] = tgt; f.q[1] = -1;
+      std::copy(U, U + 4, f.c);
+      f.conds.push_back({ctl, v});
+      f.active = 1ull << tgt;
+      out.push_back(f);
+    }
+    return;
+  }
+  FOp f;
+  f.q[0] = qa; f.q[1] = qb;
+  f.touched = f.active = touched;
+  bool mono = true;
+  for (int r = 0; r < 4 && mono; ++r) {
+    int nz = 0;
+    for (int c = 0; c < 4; ++c)
+      if (!zero(M[r * 4 + c])) { ++nz; f.src[r] = c; }
+    if (nz != 1) mono = false;
+  }
+  if (mono) {
+    f.type = OP_PERM2;
+    for (int r = 0; r < 4; ++r) f.c[r] = M[r * 4 + f.src[r]];
+  } else {
+    f.type = OP_U2;
+    std::copy(M, M + 16, f.c);
+  }
+  out.push_back(f);
+}
+
+bool is_plain_swap(const svb_gate& g) {
+  if (g.k != 2) return false;
+  static const int src[4] = {0, 2, 1, 3};
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) {
+      double re = g.mat[2 * (r * 4 + c)], im = g.mat[2 * (r * 4 + c) + 1];
+      double want = (src[r] == c) ? 1.0 : 0.0;
+      if (re != want || im != 0.0) return false;
+    }
+  return true;
+}
+
+// Fuse the gate list into classified ops over physical qubits.
+std::vector<FOp> fuse(int n, const svb_gate* gates, int ng, bool relabel, std::vector<int>& phys) {
+  phys.resize(n);
+  for (int q = 0; q < n; ++q) phys[q] = q;
+  std::vector<Block> blocks;
+  std::vector<int> order;  // block indices in creation order
+  std::vector<int> open(n, -1);
+  std::vector<bool> closed;
+  auto close = [&](int bi) {
+    if (bi < 0) return;
+    for (int j = 0; j < blocks[bi].k; ++j) open[blocks[bi].q[j]] = -1;
+  };
+  for (int i = 0; i < ng; ++i) {
+    const svb_gate& g = gates[i];
+    cd G[16];
+    int dim = g.k == 1 ? 2 : 4;
+    for (int e = 0; e < dim * dim; ++e) G[e] = cd(g.mat[2 * e], g.mat[2 * e + 1]);
+    if (g.k == 1) {
+      int a = phys[g.qubits[0]];
+      if (open[a] >= 0) {
+        left_mul_1q(blocks[open[a]], a, G);
+      } else {
+        Block b;
+        b.k = 1; b.q[0] = a; b.q[1] = -1;
+        std::copy(G, G + 4, b.M);
+        blocks.push_back(b);
+        open[a] = (int)blocks.size() - 1;
+      }
+      continue;
+    }
+    if (relabel && is_plain_swap(g)) {
+      std::swap(phys[g.qubits[0]], phys[g.qubits[1]]);
+      continue;
+    }
+    int a = phys[g.qubits[0]], b = phys[g.qubits[1]];
+    if (open[a] >= 0 && open[a] == open[b]) {
+      left_mul_2q(blocks[open[a]], a, b, G);
+      continue;
+    }
+    // earlier open blocks on a or b are closed, not absorbed: absorbing a dense
+    // 1q block would turn cheap monomial/diagonal 2q blocks dense.
+    Block nb;
+    nb.k = 2; nb.q[0] = a; nb.q[1] = b;
+    std::copy(G, G + 16, nb.M);
+    close(open[a]);
+    close(open[b]);
+    blocks.push_back(nb);
+    open[a] = open[b] = (int)blocks.size() - 1;
+  }
+  std::vector<FOp> ops;
+  for (const Block& b : blocks) emit_block(b, ops);
+  return ops;
+}
+
+template <typename R> cplx<R> cvt(cd z) { return mk<R>((R)z.real(), (R)z.imag()); }
+
+template <typename R> struct Encoder {
+  std::vector<uint8_t>& buf;
+  explicit Encoder(std::vector<uint8_t>& b) : buf(b) {}
+  size_t begin(int kind, int a, int b, int n, uint64_t fmask, uint64_t fval, uint32_t rmask, uint32_t rval) {
+    size_t at = buf.size();
+    buf.resize(at + sizeof(OpHdr));
+    OpHdr h{};
+    h.kind = kind; h.a = a; h.b = b; h.n = n;
+    h.fmask = fmask; h.fval = fval; h.rmask = rmask; h.rval = rval;
+    std::memcpy(buf.data() + at, &h, sizeof h);
+    return at;
+  }
+  template <typename T> void put(const T& x) {
+    size_t at = buf.size();
+    buf.resize(at + sizeof(T));
+    std::memcpy(buf.data() + at, &x, sizeof(T));
+  }
+  void end(size_t at) {
+    while (buf.size() % 16) buf.push_back(0);
+    uint32_t bytes = (uint32_t)(buf.size() - at);
+    std::memcpy(buf.data() + at + offsetof(OpHdr, bytes), &bytes, 4);
+  }
+};
+
+}  // namespace
+
+template <typename R>
+Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
+  Program prog;
+  prog.gates = ng;
+  std::vector<int> phys;
+  std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, phys);
+  const int m = std::min(opt.m, n);
+  const int RB = opt.rb;
+  require(m - RB >= 5 && m <= kMaxM, SVB_E_ARG, "fused program needs n >= rb + 5");
+  const uint64_t lanes = 0x1full;
+
+  std::vector<int> remaining(ops.size());
+  for (size_t i = 0; i < ops.size(); ++i) remaining[i] = (int)i;
+
+  while (!remaining.empty()) {
+    // ---- choose S and the ops of this pass
+    uint64_t S = (m == n) ? ((n == 64) ? ~0ull : ((1ull << n) - 1)) : lanes;
+    uint64_t blkA = 0, blkD = 0;
+    std::vector<int> placed, skipped;
+    for (int idx : remaining) {
+      const FOp& f = ops[idx];
+      bool conflict = (f.touched & blkA) || (f.active & blkD);
+      if (!conflict) {
+        uint64_t need = f.active & ~S;
+        if (__builtin_popcountll(S | need) <= m) {
+          S |= need;
+          placed.push_back(idx);
+          continue;
+        }
+      }
+      skipped.push_back(idx);
+      blkA |= f.active;
+      blkD |= f.touched & ~f.active;
+    }
+    for (int q = 0; q < n && __builtin_popcountll(S) < m; ++q) S |= 1ull << q;
+
+    PassDev pd{};
+    pd.m = m;
+    pd.rb = RB;
+    int l = 0;
+    int local_of[64];
+    for (int q = 0; q < 64; ++q) local_of[q] = -1;
+    for (int q = 0; q < n; ++q)
+      if (S & (1ull << q)) { pd.pos[l] = q; local_of[q] = l; ++l; }
+    pd.nout = 0;
+    for (int q = 0; q < n; ++q)
+      if (!(S & (1ull << q))) pd.outpos[pd.nout++] = q;
+
+    // ---- split into rounds by register need
+    std::vector<std::pair<uint32_t, std::vector<int>>> rounds;
+    uint32_t req = 0;
+    std::vector<int> cur;
+    for (int idx : placed) {
+      uint32_t need = 0;
+      for (int q = 0; q < n; ++q)
+        if (ops[idx].active & (1ull << q)) need |= 1u << local_of[q];
+      if (__builtin_popcount(req | need) <= RB) {
+        req |= need;
+        cur.push_back(idx);
+      } else {
+        rounds.push_back({req, cur});
+        req = need;
+        cur.assign(1, idx);
+      }
+    }
+    rounds.push_back({req, cur});
+    const uint32_t lane_local = 0x1fu;  // local bits 0..4 are physical 0..4
+    auto fill = [&](uint32_t r) {
+      for (int b = 5; b < m && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
+      for (int b = 0; b < 5 && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
+      return r;
+    };
+    std::vector<uint32_t> regsets;
+    for (auto& rd : rounds) regsets.push_back(fill(rd.first));
+    if (regsets.front() & lane_local) {
+      rounds.insert(rounds.begin(), {0u, {}});
+      regsets.insert(regsets.begin(), fill(0u));
+    }
+    if (regsets.back() & lane_local) {
+      rounds.push_back({0u, {}});
+      regsets.push_back(fill(0u));
+    }
+    if ((int)rounds.size() > kMaxRounds) {
+      // defer the tail of this pass's ops to the next pass (original order kept)
+      std::vector<int> keep_ops;
+      std::vector<std::pair<uint32_t, std::vector<int>>> kept(rounds.begin(), rounds.begin() + kMaxRounds - 1);
+      std::vector<int> deferred;
+      for (size_t k = kMaxRounds - 1; k < rounds.size(); ++k)
+        deferred.insert(deferred.end(), rounds[k].second.begin(), rounds[k].second.end());
+      rounds = kept;
+      regsets.resize(kMaxRounds - 1);
+      if (regsets.back() & lane_local) {
+        rounds.push_back({0u, {}});
+        regsets.push_back(fill(0u));
+      }
+      skipped.insert(skipped.end(), deferred.begin(), deferred.end());
+      std::sort(skipped.begin(), skipped.end());
+    }
+
+    // ---- encode the rounds
+    Encoder<R> enc(prog.ops);
+    pd.nrounds = (int)rounds.size();
+    for (size_t k = 0; k < rounds.size(); ++k) {
+      RoundDev& rd = pd.rounds[k];
+      uint32_t regs = regsets[k];
+      rd.regmask_local = regs;
+      int regidx_of_local[kMaxM];
+      for (int b = 0, i = 0; b < m; ++b) {
+        regidx_of_local[b] = -1;
+        if (regs & (1u << b)) { rd.reg_local[i] = b; regidx_of_local[b] = i; ++i; }
+      }
+      auto ridx = [&](int q) { return (q >= 0 && local_of[q] >= 0) ? regidx_of_local[local_of[q]] : -1; };
+      rd.op_off = (uint32_t)prog.ops.size();
+      const std::vector<int>& list = rounds[k].second;
+      size_t i = 0;
+      while (i < list.size()) {
+        const FOp& f = ops[list[i]];
+        if (f.type == OP_DIAG) {
+          size_t j = i;
+          while (j < list.size() && ops[list[j]].type == OP_DIAG) ++j;
+          size_t at = enc.begin(OP_DIAG, 0, 0, (int)(j - i), 0, 0, 0, 0);
+          for (size_t t = i; t < j; ++t) {
+            const FOp& d = ops[list[t]];
+            DiagTerm<R> term{};
+            term.qa = (int8_t)d.q[0];
+            term.qb = (int8_t)d.q[1];
+            term.ra = (int8_t)ridx(d.q[0]);
+            term.rb = (int8_t)ridx(d.q[1]);
+            for (int e = 0; e < 4; ++e) term.d[e] = cvt<R>(d.c[e]);
+            enc.put(term);
+          }
+          enc.end(at);
+          i = j;
+          continue;
+        }
+        if (f.type == OP_U1 || f.type == OP_U1ANTI) {
+          uint64_t fm = 0, fv = 0;
+          uint32_t rm = 0, rv = 0;
+          for (auto& cv : f.conds) {
+            int ri = ridx(cv.first);
+            if (ri >= 0) { rm |= 1u << ri; rv |= (uint32_t)cv.second << ri; }
+            else { fm |= 1ull << cv.first; fv |= (uint64_t)cv.second << cv.first; }
+          }
+          int b = ridx(f.q[0]);
+          require(b >= 0, SVB_E_CUDA, "scheduler: U1 target not in registers");
+          size_t at = enc.begin(f.type, b, 0, 0, fm, fv, rm, rv);
+          for (int e = 0; e < 4; ++e) enc.put(cvt<R>(f.c[e]));
+          enc.end(at);
+        } else {
+          int b1 = ridx(f.q[0]), b2 = ridx(f.q[1]);
+          require(b1 >= 0 && b2 >= 0, SVB_E_CUDA, "scheduler: U2 qubits not in registers");
+          size_t at = enc.begin(f.type, b1, b2, 0, 0, 0, 0, 0);
+          if (f.type == OP_U2) {
+            for (int e = 0; e < 16; ++e) enc.put(cvt<R>(f.c[e]));
+          } else {
+            int32_t s4[4] = {f.src[0], f.src[1], f.src[2], f.src[3]};
+            enc.put(s4);
+            for (int e = 0; e < 4; ++e) enc.put(cvt<R>(f.c[e]));
+          }
+          enc.end(at);
+        }
+        ++i;
+      }
+      rd.op_end = (uint32_t)prog.ops.size();
+    }
+    prog.passes.push_back(pd);
+    remaining = skipped;
+  }
+  bool ident = true;
+  for (int q = 0; q < n; ++q) ident = ident && phys[q] == q;
+  if (!ident) {
+    // data of logical qubit q sits at physical bit phys[q]; move it to bit q
+    prog.final_perm.assign(n, 0);
+    for (int q = 0; q < n; ++q) prog.final_perm[phys[q]] = q;
+  }
+  return prog;
+}
+
+template Program build_program<float>(int, const svb_gate*, int, const SchedOptions&);
+template Program build_program<double>(int, const svb_gate*, int, const SchedOptions&);
+
+// ------------------------------------------------------------- emulation
+template <typename R, int RB>
+static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t* ops) {
+  constexpr int V = 1 << RB;
+  const int m = pd.m;
+  const uint32_t NT = 1u << (m - RB);
+  std::vector<cplx<R>> tile((size_t)1 << m);
+  const uint64_t ntiles = 1ull << pd.nout;
+  for (uint64_t t = 0; t < ntiles; ++t) {
+    const uint64_t base = tile_base(pd, t);
+    for (int k = 0; k < pd.nrounds; ++k) {
+      const RoundDev& rd = pd.rounds[k];
+      for (uint32_t tid = 0; tid < NT; ++tid) {
+        uint32_t Fl;
+        uint64_t Fg;
+        thread_fixed(pd, rd, tid, base, &Fl, &Fg);
+        cplx<R> a[V];
+        uint64_t gidx[V];
+        uint32_t lidx[V];
+        for (int v = 0; v < V; ++v) {
+          uint64_t g = Fg;
+          uint32_t lo = Fl;
+          for (int i = 0; i < RB; ++i)
+            if ((v >> i) & 1) { g |= 1ull << pd.pos[rd.reg_local[i]]; lo |= 1u << rd.reg_local[i]; }
+          gidx[v] = g;
+          lidx[v] = lo;
+          a[v] = (k == 0) ? state[g] : tile[lo];
+        }
+        run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end);
+        for (int v = 0; v < V; ++v) {
+          if (k == pd.nrounds - 1) state[gidx[v]] = a[v];
+          else tile[lidx[v]] = a[v];
+        }
+      }
+    }
+  }
+}
+
+template <typename R>
+void emulate_program(cplx<R>* state, int n, const Program& prog) {
+  for (const PassDev& pd : prog.passes) {
+    if (pd.rb == 4) emulate_pass<R, 4>(state, n, pd, prog.ops.data());
+    else emulate_pass<R, 5>(state, n, pd, prog.ops.data());
+  }
+  if (!prog.final_perm.empty()) {
+    uint64_t len = 1ull << n;
+    std::vector<cplx<R>> out(len);
+    for (uint64_t i = 0; i < len; ++i) {
+      uint64_t o = 0;
+      for (int p = 0; p < n; ++p)
+        if ((i >> p) & 1) o |= 1ull << prog.final_perm[p];
+      out[o] = state[i];
+    }
+    std::copy(out.begin(), out.end(), state);
+  }
+}
+
+template void emulate_program<float>(cplx<float>*, int, const Program&);
+template void emulate_program<double>(cplx<double>*, int, const Program&);
+
+SchedOptions default_options(int precision, int n) {
+  SchedOptions o;
+  if (precision == SVB_C128) { o.rb = 4; o.m = 12; }
+  else { o.rb = 5; o.m = 13; }
+  return o;
+}
+
+}  // namespace svb

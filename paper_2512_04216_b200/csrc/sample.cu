@@ -1,0 +1,566 @@
+// Terminal-measurement sampling on the device.
+//
+// Two samplers share one uniform stream — numpy's PCG64 as seeded by
+// `np.random.default_rng(seed)` (statevector.py:215), reproduced bit-exactly:
+// 128-bit LCG, multiplier 0x2360ED051FC65DA44385DF649FCCF645, state stepped
+// BEFORE output, XSL-RR output, double = (u64 >> 11) * 2^-53.  Shot s consumes
+// draw s, so a thread owning shots [s0, s1) jumps ahead s0 steps (O(log s0)).
+//
+// * ALIAS (reference-compatible) — AliasTable.from_probs / sample_indices
+//   (sampling.py:30-83) restated as device rounds:
+//     total       : numpy pairwise summation, reproduced exactly (leaf = 8
+//                   accumulators over <=128 elements, halving tree above);
+//     scaled      : probs * (m / total);
+//     each round  : deficits / capacities -> inclusive scans -> lower_bound
+//                   (searchsorted side='left') -> owner; bincount(owner,
+//                   deficits) as a deterministic reduce-by-key (owner is
+//                   monotone); stable compactions for the next round.
+//   Differences to numpy are confined to floating-point association inside
+//   the scans and the per-owner sums (numpy is sequential); they can move a
+//   sample only when a uniform lands within a few ulps of a threshold.
+// * CDF (native) — fused |amp|^2 + per-32-amplitude leaf sums, one inclusive
+//   scan over the leaves, then per shot a binary search over leaf prefixes and
+//   a 32-element scan inside the leaf.  Passes chi^2 against |amp|^2.
+//
+// Codes (clbit-packed outcomes) are histogrammed with a radix sort + run
+// length encode, giving np.unique's ascending (value, count) pairs.
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svb {
+
+typedef unsigned __int128 u128;
+__host__ __device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ull << 64) | 0x4385DF649FCCF645ull;
+}
+
+struct Pcg {
+  u128 s, inc;
+  __host__ __device__ __forceinline__ uint64_t next64() {
+    s = s * pcg_mult() + inc;
+    uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    uint64_t x = hi ^ lo;
+    unsigned r = (unsigned)(hi >> 58);
+    return (x >> r) | (x << ((64u - r) & 63u));
+  }
+  __host__ __device__ __forceinline__ double next_double() {
+    return (double)(next64() >> 11) * (1.0 / 9007199254740992.0);
+  }
+  // skip `delta` draws (LCG jump-ahead, Brown 1994)
+  __host__ __device__ void advance(uint64_t delta) {
+    u128 acc_m = 1, acc_p = 0, cur_m = pcg_mult(), cur_p = inc;
+    while (delta) {
+      if (delta & 1) {
+        acc_m *= cur_m;
+        acc_p = acc_p * cur_m + cur_p;
+      }
+      cur_p = (cur_m + 1) * cur_p;
+      cur_m *= cur_m;
+      delta >>= 1;
+    }
+    s = acc_m * s + acc_p;
+  }
+};
+
+static inline Pcg pcg_from(const uint64_t* p) {
+  Pcg g;
+  g.s = ((u128)p[0] << 64) | p[1];
+  g.inc = ((u128)p[2] << 64) | p[3];
+  return g;
+}
+
+void host_pcg_advance(uint64_t* p, uint64_t delta) {
+  Pcg g = pcg_from(p);
+  g.advance(delta);
+  p[0] = (uint64_t)(g.s >> 64);
+  p[1] = (uint64_t)g.s;
+}
+
+// --------------------------------------------------- numpy pairwise summation
+__device__ double np_pairwise(const double* a, uint64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (uint64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    uint64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  uint64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+__global__ void k_pairwise_small(const double* a, uint64_t n, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = np_pairwise(a, n);
+}
+
+// leaves of exactly 128 (m a power of two >= 256: the halving tree bottoms out at 128)
+__global__ void k_pairwise_leaves(const double* __restrict__ a, uint64_t nleaf, double* __restrict__ out) {
+  uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nleaf) return;
+  const double* p = a + l * 128;
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = p[j];
+  for (int i = 8; i < 128; i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] += p[i + j];
+  }
+  out[l] = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+}
+
+// one halving level: out[i] = in[2i] + in[2i+1]
+__global__ void k_pair_level(const double* __restrict__ in, uint64_t nout, double* __restrict__ out) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nout) out[i] = in[2 * i] + in[2 * i + 1];
+}
+
+double pairwise_sum_device(const double* d_x, uint64_t m, double* d_ws, cudaStream_t st) {
+  double h = 0.0;
+  bool pow2 = (m & (m - 1)) == 0;
+  if (!pow2 || m < 256) {
+    k_pairwise_small<<<1, 1, 0, st>>>(d_x, m, d_ws);
+    SVB_CHECK_LAUNCH();
+    SVB_CUDA(cudaMemcpyAsync(&h, d_ws, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SVB_CUDA(cudaStreamSynchronize(st));
+    return h;
+  }
+  uint64_t nl = m / 128;
+  double* a = d_ws;
+  double* b = d_ws + nl;
+  k_pairwise_leaves<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(d_x, nl, a);
+  SVB_CHECK_LAUNCH();
+  while (nl > 1) {
+    uint64_t no = nl / 2;
+    k_pair_level<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(a, no, b);
+    SVB_CHECK_LAUNCH();
+    double* t = a; a = b; b = t;
+    nl = no;
+  }
+  SVB_CUDA(cudaMemcpyAsync(&h, a, sizeof(double), cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+// ----------------------------------------------------------- device buffers
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes) SVB_CUDA(cudaMallocAsync(&p, bytes, s));
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+
+template <typename T> static T d2h_scalar(const T* d, cudaStream_t st) {
+  T h;
+  SVB_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+template <typename In, typename Out>
+static void cub_exclusive_sum(const In* in, Out* out, uint64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  SVB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
+  DevBuf tmp(bytes, st);
+  SVB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
+}
+static void cub_inclusive_sum(const double* in, double* out, uint64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  SVB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
+  DevBuf tmp(bytes, st);
+  SVB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
+}
+
+// ------------------------------------------------------------- alias build
+__global__ void k_alias_init(const double* __restrict__ probs, uint64_t m, double factor,
+                             double* __restrict__ scaled, double* __restrict__ prob_row,
+                             int64_t* __restrict__ alias_row, int64_t* __restrict__ big) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    double v = probs[i] * factor;
+    scaled[i] = v;
+    prob_row[i] = 1.0;
+    alias_row[i] = (int64_t)i;
+    big[i] = v > 1.0 ? 1 : 0;
+  }
+}
+
+// split [0, m) into larges (flag) and smalls (!flag), order preserved
+__global__ void k_split_iota(const int64_t* __restrict__ flag, const int64_t* __restrict__ pos,
+                             uint64_t m, int64_t* __restrict__ larges, int64_t* __restrict__ smalls) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    if (flag[i]) larges[pos[i]] = (int64_t)i;
+    else smalls[i - pos[i]] = (int64_t)i;
+  }
+}
+
+__global__ void k_gather(const double* __restrict__ src, const int64_t* __restrict__ idx, uint64_t n,
+                         double* __restrict__ dst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = src[idx[i]];
+}
+
+__global__ void k_deficit(const double* __restrict__ scaled, const int64_t* __restrict__ smalls,
+                          uint64_t ns, double* __restrict__ deficit) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride)
+    deficit[i] = 1.0 - scaled[smalls[i]];
+}
+
+__global__ void k_capacity(const double* __restrict__ rem, uint64_t nl, double* __restrict__ cap) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride)
+    cap[i] = rem[i] - 1.0;
+}
+
+__global__ void k_owner(const double* __restrict__ dcum, uint64_t ns, const double* __restrict__ ccum,
+                        uint64_t nl, const int64_t* __restrict__ smalls,
+                        const int64_t* __restrict__ larges, const double* __restrict__ scaled,
+                        int64_t* __restrict__ owner, double* __restrict__ prob_row,
+                        int64_t* __restrict__ alias_row) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride) {
+    double d = dcum[i];
+    uint64_t lo = 0, hi = nl;  // first j with ccum[j] >= d
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (ccum[mid] < d) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo > nl - 1) lo = nl - 1;
+    owner[i] = (int64_t)lo;
+    int64_t s = smalls[i];
+    prob_row[s] = scaled[s];
+    alias_row[s] = larges[lo];
+  }
+}
+
+__global__ void k_absorb(const int64_t* __restrict__ uniq, const double* __restrict__ agg,
+                         const int64_t* __restrict__ nruns, double* __restrict__ rem) {
+  const int64_t nr = *nruns;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += stride)
+    rem[uniq[r]] = rem[uniq[r]] - agg[r];
+}
+
+__global__ void k_conv_flags(const double* __restrict__ rem, uint64_t nl, int64_t* __restrict__ conv) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride)
+    conv[i] = rem[i] <= 1.0 ? 1 : 0;
+}
+
+__global__ void k_convert(const int64_t* __restrict__ conv, const int64_t* __restrict__ pos, uint64_t nl,
+                          const int64_t* __restrict__ larges, const double* __restrict__ rem,
+                          int64_t* __restrict__ new_smalls, double* __restrict__ scaled,
+                          int64_t* __restrict__ new_larges, double* __restrict__ new_rem) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nl; j += stride) {
+    int64_t L = larges[j];
+    if (conv[j]) {
+      new_smalls[pos[j]] = L;
+      scaled[L] = rem[j];
+    } else {
+      uint64_t k = j - pos[j];
+      new_larges[k] = L;
+      new_rem[k] = rem[j];
+    }
+  }
+}
+
+void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_alias_row,
+                 cudaStream_t st) {
+  const int B = 256;
+  // validation + total (sampling.py:31-42)
+  DevBuf ws(sizeof(double) * (m / 64 + 16), st);
+  double total = pairwise_sum_device(d_probs, m, ws.as<double>(), st);
+  if (!(fabs(total - 1.0) <= 1e-9))  // np.isclose(total, 1, rtol=0, atol=1e-9)
+    throw Error(SVB_E_SAMPLING, "probabilities sum to " + std::to_string(total) + ", not 1");
+  double factor = (double)m / total;
+
+  DevBuf scaled(sizeof(double) * m, st), flag(sizeof(int64_t) * m, st), pos(sizeof(int64_t) * m, st);
+  k_alias_init<<<grid_for(m, B), B, 0, st>>>(d_probs, m, factor, scaled.as<double>(), d_prob_row,
+                                             d_alias_row, flag.as<int64_t>());
+  SVB_CHECK_LAUNCH();
+  cub_exclusive_sum(flag.as<int64_t>(), pos.as<int64_t>(), m, st);
+  uint64_t nl = (uint64_t)d2h_scalar(pos.as<int64_t>() + (m - 1), st) +
+                (uint64_t)d2h_scalar(flag.as<int64_t>() + (m - 1), st);
+  uint64_t ns = m - nl;
+  if (nl == 0 || ns == 0) return;
+
+  DevBuf larges(sizeof(int64_t) * nl, st), smalls(sizeof(int64_t) * m, st);
+  k_split_iota<<<grid_for(m, B), B, 0, st>>>(flag.as<int64_t>(), pos.as<int64_t>(), m,
+                                             larges.as<int64_t>(), smalls.as<int64_t>());
+  SVB_CHECK_LAUNCH();
+  DevBuf rem(sizeof(double) * nl, st);
+  k_gather<<<grid_for(nl, B), B, 0, st>>>(scaled.as<double>(), larges.as<int64_t>(), nl, rem.as<double>());
+  SVB_CHECK_LAUNCH();
+
+  // round scratch, sized for the first (largest) round
+  DevBuf deficit(sizeof(double) * ns, st), dcum(sizeof(double) * ns, st), owner(sizeof(int64_t) * ns, st);
+  DevBuf cap(sizeof(double) * nl, st), ccum(sizeof(double) * nl, st);
+  DevBuf uniq(sizeof(int64_t) * nl, st), agg(sizeof(double) * nl, st), nruns(sizeof(int64_t), st);
+  DevBuf conv(sizeof(int64_t) * nl, st), cpos(sizeof(int64_t) * nl, st);
+  DevBuf larges2(sizeof(int64_t) * nl, st), rem2(sizeof(double) * nl, st);
+  int64_t* L = larges.as<int64_t>();
+  int64_t* L2 = larges2.as<int64_t>();
+  double* Rm = rem.as<double>();
+  double* Rm2 = rem2.as<double>();
+  int64_t* S = smalls.as<int64_t>();
+  size_t rbk_bytes = 0;
+  SVB_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, rbk_bytes, owner.as<int64_t>(), uniq.as<int64_t>(),
+                                          deficit.as<double>(), agg.as<double>(), nruns.as<int64_t>(),
+                                          ::cuda::std::plus<double>(), (int64_t)ns, st));
+  DevBuf rbk_tmp(rbk_bytes, st);
+
+  while (ns > 0 && nl > 0) {
+    k_deficit<<<grid_for(ns, B), B, 0, st>>>(scaled.as<double>(), S, ns, deficit.as<double>());
+    k_capacity<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, cap.as<double>());
+    SVB_CHECK_LAUNCH();
+    cub_inclusive_sum(deficit.as<double>(), dcum.as<double>(), ns, st);
+    cub_inclusive_sum(cap.as<double>(), ccum.as<double>(), nl, st);
+    k_owner<<<grid_for(ns, B), B, 0, st>>>(dcum.as<double>(), ns, ccum.as<double>(), nl, S, L,
+                                           scaled.as<double>(), owner.as<int64_t>(), d_prob_row,
+                                           d_alias_row);
+    SVB_CHECK_LAUNCH();
+    size_t b = rbk_bytes;
+    SVB_CUDA(cub::DeviceReduce::ReduceByKey(rbk_tmp.p, b, owner.as<int64_t>(), uniq.as<int64_t>(),
+                                            deficit.as<double>(), agg.as<double>(), nruns.as<int64_t>(),
+                                            ::cuda::std::plus<double>(), (int64_t)ns, st));
+    k_absorb<<<grid_for(ns < nl ? ns : nl, B), B, 0, st>>>(uniq.as<int64_t>(), agg.as<double>(),
+                                                           nruns.as<int64_t>(), Rm);
+    k_conv_flags<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, conv.as<int64_t>());
+    SVB_CHECK_LAUNCH();
+    cub_exclusive_sum(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);
+    uint64_t nconv = (uint64_t)d2h_scalar(cpos.as<int64_t>() + (nl - 1), st) +
+                     (uint64_t)d2h_scalar(conv.as<int64_t>() + (nl - 1), st);
+    if (nconv == 0) break;  // sampling.py:60-63
+    k_convert<<<grid_for(nl, B), B, 0, st>>>(conv.as<int64_t>(), cpos.as<int64_t>(), nl, L, Rm, S,
+                                             scaled.as<double>(), L2, Rm2);
+    SVB_CHECK_LAUNCH();
+    ns = nconv;
+    nl = nl - nconv;
+    int64_t* tl = L; L = L2; L2 = tl;
+    double* tr = Rm; Rm = Rm2; Rm2 = tr;
+  }
+}
+
+// ------------------------------------------------------------- alias draws
+struct BitSrc { int8_t b[64]; };
+
+__device__ __forceinline__ uint64_t pack_code(uint64_t idx, const BitSrc& bs, int w) {
+  uint64_t code = 0;
+  for (int p = 0; p < w; ++p) code |= ((idx >> bs.b[p]) & 1ull) << p;
+  return code;
+}
+
+constexpr uint64_t kShotsPerThread = 64;
+
+__global__ void k_alias_draw(const double* __restrict__ prob_row, const int64_t* __restrict__ alias_row,
+                             uint64_t m, uint64_t shots, Pcg base, BitSrc bs, int w,
+                             uint64_t* __restrict__ codes) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t s0 = t * kShotsPerThread;
+  if (s0 >= shots) return;
+  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  Pcg g = base;
+  g.advance(s0);
+  const double fm = (double)m;
+  for (uint64_t s = s0; s < s1; ++s) {
+    double v = g.next_double() * fm;
+    int64_t idx = (int64_t)v;
+    double frac = v - (double)idx;
+    int64_t pick = frac < prob_row[idx] ? idx : alias_row[idx];
+    codes[s] = pack_code((uint64_t)pick, bs, w);
+  }
+}
+
+static BitSrc make_bitsrc(const int32_t* bit_src, int w) {
+  BitSrc bs;
+  for (int p = 0; p < 64; ++p) bs.b[p] = p < w ? (int8_t)bit_src[p] : 0;
+  return bs;
+}
+
+void alias_draw(const double* d_prob_row, const int64_t* d_alias_row, uint64_t m, uint64_t shots,
+                const uint64_t* pcg, const int32_t* bit_src, int w, uint64_t* d_codes,
+                cudaStream_t st) {
+  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_alias_draw<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
+      d_prob_row, d_alias_row, m, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes);
+  SVB_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------------------- CDF draws
+// Fused |amp|^2 + leaf sums: one warp per 32-amplitude leaf.
+template <typename R>
+__global__ void k_leaf_sums_state(const cplx<R>* __restrict__ s, uint64_t nleaf, double* __restrict__ leaf) {
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t l = gw; l < nleaf; l += nw) {
+    cplx<R> a = s[l * 32 + lane];
+    double x = (double)a.x, y = (double)a.y;
+    double p = x * x + y * y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if (lane == 0) leaf[l] = p;
+  }
+}
+
+__global__ void k_leaf_sums_probs(const double* __restrict__ pr, uint64_t m, uint64_t nleaf,
+                                  double* __restrict__ leaf) {
+  uint64_t l = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nleaf) return;
+  double acc = 0.0;
+  uint64_t e = (l + 1) * 32 < m ? (l + 1) * 32 : m;
+  for (uint64_t i = l * 32; i < e; ++i) acc += pr[i];
+  leaf[l] = acc;
+}
+
+template <typename Prob>
+__device__ __forceinline__ uint64_t cdf_pick(const double* __restrict__ cum, uint64_t nleaf, uint64_t m,
+                                             double target, Prob prob) {
+  uint64_t lo = 0, hi = nleaf;  // first leaf with cum > target
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if (cum[mid] <= target) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo >= nleaf) lo = nleaf - 1;
+  double acc = lo ? cum[lo - 1] : 0.0;
+  uint64_t i0 = lo * 32, i1 = i0 + 32 < m ? i0 + 32 : m;
+  uint64_t last_nz = i0;
+  for (uint64_t i = i0; i < i1; ++i) {
+    double p = prob(i);
+    if (p > 0.0) {
+      last_nz = i;
+      acc += p;
+      if (acc > target) return i;
+    }
+  }
+  return last_nz;  // rounding slop at the top of the leaf
+}
+
+template <typename R>
+__global__ void k_cdf_draw_state(const cplx<R>* __restrict__ s, uint64_t m, const double* __restrict__ cum,
+                                 uint64_t nleaf, uint64_t shots, Pcg base, BitSrc bs, int w,
+                                 uint64_t* __restrict__ codes) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t s0 = t * kShotsPerThread;
+  if (s0 >= shots) return;
+  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  Pcg g = base;
+  g.advance(s0);
+  const double total = cum[nleaf - 1];
+  auto prob = [&](uint64_t i) {
+    cplx<R> a = s[i];
+    double x = (double)a.x, y = (double)a.y;
+    return x * x + y * y;
+  };
+  for (uint64_t k = s0; k < s1; ++k) {
+    double target = g.next_double() * total;
+    codes[k] = pack_code(cdf_pick(cum, nleaf, m, target, prob), bs, w);
+  }
+}
+
+__global__ void k_cdf_draw_probs(const double* __restrict__ pr, uint64_t m, const double* __restrict__ cum,
+                                 uint64_t nleaf, uint64_t shots, Pcg base, BitSrc bs, int w,
+                                 uint64_t* __restrict__ codes) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t s0 = t * kShotsPerThread;
+  if (s0 >= shots) return;
+  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  Pcg g = base;
+  g.advance(s0);
+  const double total = cum[nleaf - 1];
+  auto prob = [&](uint64_t i) { return pr[i]; };
+  for (uint64_t k = s0; k < s1; ++k) {
+    double target = g.next_double() * total;
+    codes[k] = pack_code(cdf_pick(cum, nleaf, m, target, prob), bs, w);
+  }
+}
+
+template <typename R>
+void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
+              int w, uint64_t* d_codes, cudaStream_t st) {
+  uint64_t m = 1ull << n;
+  require(n >= 5, SVB_E_ARG, "cdf sampler needs n >= 5");
+  uint64_t nleaf = m / 32;
+  DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
+  k_leaf_sums_state<R><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const cplx<R>*>(state),
+                                                                    nleaf, leaf.as<double>());
+  SVB_CHECK_LAUNCH();
+  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_cdf_draw_state<R><<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
+      static_cast<const cplx<R>*>(state), m, cum.as<double>(), nleaf, shots, pcg_from(pcg),
+      make_bitsrc(bit_src, w), w, d_codes);
+  SVB_CHECK_LAUNCH();
+}
+
+void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
+                    const int32_t* bit_src, int w, uint64_t* d_codes, cudaStream_t st) {
+  uint64_t nleaf = (m + 31) / 32;
+  DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
+  k_leaf_sums_probs<<<(unsigned)((nleaf + 255) / 256), 256, 0, st>>>(d_probs, m, nleaf, leaf.as<double>());
+  SVB_CHECK_LAUNCH();
+  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_cdf_draw_probs<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
+      d_probs, m, cum.as<double>(), nleaf, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes);
+  SVB_CHECK_LAUNCH();
+}
+
+template void cdf_draw<float>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
+                              uint64_t*, cudaStream_t);
+template void cdf_draw<double>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
+                               uint64_t*, cudaStream_t);
+
+// --------------------------------------------------------------- histogram
+uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_codes,
+                         uint64_t* h_counts, cudaStream_t st) {
+  DevBuf sorted(sizeof(uint64_t) * shots, st);
+  size_t bytes = 0;
+  int end_bit = w < 1 ? 1 : w;
+  SVB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_codes, sorted.as<uint64_t>(), (int64_t)shots,
+                                          0, end_bit, st));
+  {
+    DevBuf tmp(bytes, st);
+    SVB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, d_codes, sorted.as<uint64_t>(), (int64_t)shots,
+                                            0, end_bit, st));
+  }
+  DevBuf uniq(sizeof(uint64_t) * shots, st), cnt(sizeof(uint64_t) * shots, st), nr(sizeof(int64_t), st);
+  bytes = 0;
+  SVB_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, sorted.as<uint64_t>(), uniq.as<uint64_t>(),
+                                              cnt.as<uint64_t>(), nr.as<int64_t>(), (int64_t)shots, st));
+  {
+    DevBuf tmp(bytes, st);
+    SVB_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, sorted.as<uint64_t>(), uniq.as<uint64_t>(),
+                                                cnt.as<uint64_t>(), nr.as<int64_t>(), (int64_t)shots, st));
+  }
+  int64_t nruns = d2h_scalar(nr.as<int64_t>(), st);
+  SVB_CUDA(cudaMemcpyAsync(h_codes, uniq.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaMemcpyAsync(h_counts, cnt.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaStreamSynchronize(st));
+  return (uint64_t)nruns;
+}
+
+}  // namespace svb

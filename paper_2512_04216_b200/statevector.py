@@ -1,0 +1,524 @@
+"""Drop-in B200 replacement for the reference dense state-vector backend.
+
+Same module surface as `polysim/statevector.py`:
+
+* ``run(c, shots, seed, workers=1, qubit_cap=26)`` -> ``RunResult``  (`statevector.py:182-253`)
+* ``final_state(c, qubit_cap=26)`` -> complex128 ndarray, cached per Circuit  (`:256-274`)
+* ``expectation(c, z_qubits, qubit_cap=26)`` -> float  (`:277-292`)
+* kernel level: ``zero_state``, ``apply_1q``, ``apply_2q``, ``apply_instruction``,
+  ``marginal_probs``, ``_measure_qubit``, ``_reset_qubit`` (`:33-154`), used by
+  pblock (`pblock.py:93-154`) and calibration (`calibration.py:215-228`);
+  they accept numpy arrays (copied through the device) or ``DeviceState``.
+
+Every computation runs in libsvb.so on the GPU (ctypes, include/svb.h);
+this module only marshals circuits, seeds and results.  Conventions, error
+types and their check order follow the reference exactly.  Extensions are
+keyword-only: ``precision`` ("c128" default, or "c64"), ``sampler``
+("alias" = reference-compatible counts, "cdf" = native multinomial sampler,
+"auto"), ``device``.
+"""
+from __future__ import annotations
+
+import time
+import weakref
+
+import numpy as np
+
+from . import _lib
+from ._lib import GATE_DTYPE, SvbGate, check, lib, ptr
+from .circuit import ONE_QUBIT_GATES, UNITARY_GATES
+from .features import terminal_measurement_only
+from .gates import matrix_of, single_qubit_matrix
+from .result import (
+    BackendError,
+    NoMeasurementsError,
+    QubitCapError,
+    RunResult,
+    clbit_order,
+    format_counts,
+    measurement_map,
+    output_bit_sources,
+)
+
+DEFAULT_QUBIT_CAP = 26  # statevector.py:30
+ALIAS_MAX_QUBITS = 28   # sampler="auto" switches to the CDF sampler above this
+_PREC = {"c128": _lib.SVB_C128, "c64": _lib.SVB_C64, "complex128": _lib.SVB_C128, "complex64": _lib.SVB_C64}
+_MASK64 = (1 << 64) - 1
+
+
+def _prec_code(precision) -> int:
+    try:
+        return _PREC[str(precision)]
+    except KeyError:
+        raise ValueError(f"unknown precision {precision!r}") from None
+
+
+def pcg_words(seed_or_rng) -> np.ndarray:
+    """numpy PCG64 state of default_rng(seed) (or of a Generator) as 4 uint64."""
+    g = seed_or_rng if isinstance(seed_or_rng, np.random.Generator) else np.random.default_rng(seed_or_rng)
+    st = g.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("device sampling reproduces numpy's PCG64 stream only")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    return np.array([s >> 64, s & _MASK64, inc >> 64, inc & _MASK64], dtype=np.uint64)
+
+
+# ----------------------------------------------------------- gate encoding
+def gate_array(instructions) -> np.ndarray:
+    """Unitary instructions -> svb_gate records (matrices as in gates.py)."""
+    insts = [i for i in instructions if i.kind in UNITARY_GATES]
+    arr = np.zeros(len(insts), dtype=GATE_DTYPE)
+    k = arr["k"]
+    q = arr["q"]
+    mat = arr["mat"]
+    for j, inst in enumerate(insts):
+        m = matrix_of(inst)
+        nq = len(inst.qubits)
+        k[j] = nq
+        q[j, :nq] = inst.qubits
+        mat[j, : 2 * m.size] = m.reshape(-1).view(np.float64)
+    return arr
+
+
+def _single_gate(qubits, m) -> np.ndarray:
+    m = np.asarray(m, dtype=np.complex128)
+    arr = np.zeros(1, dtype=GATE_DTYPE)
+    arr["k"][0] = len(qubits)
+    arr["q"][0, : len(qubits)] = qubits
+    arr["mat"][0, : 2 * m.size] = m.reshape(-1).view(np.float64)
+    return arr
+
+
+# ------------------------------------------------------------ device state
+class DeviceState:
+    """A 2^n amplitude vector resident in HBM (one libsvb handle)."""
+
+    def __init__(self, n: int, precision="c128", device: int = 0):
+        self.n = int(n)
+        self.precision = "c128" if _prec_code(precision) == _lib.SVB_C128 else "c64"
+        self.device = device
+        h = _lib.c_void_p()
+        check(lib().svb_create(self.n, _prec_code(precision), device, _lib.ctypes.byref(h)))
+        self._h = h
+
+    # lifetime
+    def close(self) -> None:
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().svb_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise BackendError("device state is closed")
+        return self._h
+
+    def set_option(self, option: int, value: int) -> None:
+        check(lib().svb_set_option(self.handle, option, value))
+
+    def stats(self) -> dict:
+        p, g, l = _lib.c_int64(), _lib.c_int64(), _lib.c_int64()
+        check(lib().svb_last_stats(self.handle, _lib.ctypes.byref(p), _lib.ctypes.byref(g), _lib.ctypes.byref(l)))
+        return {"passes": p.value, "gates": g.value, "launches": l.value}
+
+    # device timing (CUDA events on this state's stream)
+    def timer_start(self) -> None:
+        check(lib().svb_timer_start(self.handle))
+
+    def timer_stop(self) -> float:
+        ms = _lib.c_double()
+        check(lib().svb_timer_stop(self.handle, _lib.ctypes.byref(ms)))
+        return ms.value
+
+    def profile(self, enable: bool = True) -> None:
+        check(lib().svb_profile(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
+        out = np.zeros(6, dtype=np.float64)
+        check(lib().svb_profile_read(self.handle, ptr(out, _lib.c_double)))
+        return {"pass_ms": out[0], "pass_launches": int(out[1]), "pass_bytes": out[2],
+                "perm_ms": out[3], "perm_launches": int(out[4]), "perm_bytes": out[5]}
+
+    # data
+    def zero(self) -> "DeviceState":
+        check(lib().svb_set_zero(self.handle))
+        return self
+
+    @classmethod
+    def from_numpy(cls, amps: np.ndarray, precision="c128", device: int = 0) -> "DeviceState":
+        amps = np.ascontiguousarray(amps, dtype=np.complex128).reshape(-1)
+        n = amps.size.bit_length() - 1
+        if amps.size != 1 << n:
+            raise ValueError("amplitude vector length must be a power of two")
+        s = cls(n, precision, device)
+        s.load(amps)
+        return s
+
+    def load(self, amps: np.ndarray) -> None:
+        amps = np.ascontiguousarray(amps, dtype=np.complex128)
+        if amps.size != 1 << self.n:
+            raise ValueError("amplitude vector length mismatch")
+        check(lib().svb_set_amplitudes(self.handle, ptr(amps), 0, amps.size))
+
+    def to_numpy(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(1 << self.n, dtype=np.complex128)
+        if out.dtype != np.complex128 or out.size != 1 << self.n or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous complex128 array of length 2^n")
+        check(lib().svb_get_amplitudes(self.handle, ptr(out), 0, out.size))
+        return out
+
+    def copy_from(self, other: "DeviceState") -> None:
+        check(lib().svb_copy_state(self.handle, other.handle))
+
+    # gates
+    def apply_gates(self, gates: np.ndarray) -> None:
+        gates = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
+        if gates.size:
+            check(lib().svb_apply(self.handle, ptr(gates), int(gates.size)))
+
+    def apply_instructions(self, instructions) -> None:
+        self.apply_gates(gate_array(instructions))
+
+    # reductions
+    def marginal_probs(self, qubits) -> np.ndarray:
+        qs = np.ascontiguousarray(sorted(qubits), dtype=np.int32)
+        out = np.empty(1 << qs.size, dtype=np.float64)
+        check(lib().svb_marginal_probs(self.handle, ptr(qs, _lib.c_int32), int(qs.size), ptr(out, _lib.c_double)))
+        return out
+
+    def expect_z(self, masks) -> np.ndarray:
+        ms = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
+        out = np.empty(ms.size, dtype=np.float64)
+        check(lib().svb_expect_z(self.handle, ptr(ms, _lib.c_uint64), int(ms.size), ptr(out, _lib.c_double)))
+        return out
+
+    def sample_codes(self, qubits, bit_src, shots: int, rng_words: np.ndarray, sampler: int):
+        qs = np.ascontiguousarray(qubits, dtype=np.int32)
+        bs = np.ascontiguousarray(bit_src, dtype=np.int32)
+        w = int(bs.size)
+        cap = min(int(shots), 1 << min(w, 62))
+        codes = np.empty(cap, dtype=np.uint64)
+        freq = np.empty(cap, dtype=np.uint64)
+        nu = _lib.c_uint64()
+        words = np.ascontiguousarray(rng_words, dtype=np.uint64)
+        check(
+            lib().svb_sample(
+                self.handle, ptr(qs, _lib.c_int32), int(qs.size), ptr(bs, _lib.c_int32), w, int(shots),
+                ptr(words, _lib.c_uint64), int(sampler), ptr(codes, _lib.c_uint64), ptr(freq, _lib.c_uint64),
+                _lib.ctypes.byref(nu),
+            )
+        )
+        return codes[: nu.value], freq[: nu.value]
+
+    def seed_rng(self, rng_words) -> None:
+        words = np.ascontiguousarray(rng_words, dtype=np.uint64)
+        check(lib().svb_rng_seed(self.handle, ptr(words, _lib.c_uint64)))
+
+    def measure(self, q: int) -> int:
+        out = _lib.c_int32()
+        check(lib().svb_measure(self.handle, int(q), _lib.ctypes.byref(out)))
+        return int(out.value)
+
+    def reset(self, q: int) -> None:
+        check(lib().svb_reset(self.handle, int(q)))
+
+
+class PinnedBuffer:
+    """Page-locked host complex128 buffer (fast final_state read-back)."""
+
+    def __init__(self, count: int):
+        p = _lib.c_void_p()
+        check(lib().svb_host_alloc(int(count) * 16, _lib.ctypes.byref(p)))
+        self._p = p
+        dbl = np.ctypeslib.as_array(_lib.ctypes.cast(p, _lib.POINTER(_lib.c_double)), shape=(2 * int(count),))
+        self.array = dbl.view(np.complex128)
+
+    def close(self) -> None:
+        p, self._p = getattr(self, "_p", None), None
+        if p:
+            self.array = None
+            lib().svb_host_free(p)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_of(amps, n):
+    """numpy array -> temporary DeviceState (kernel-level API); DeviceState -> itself."""
+    if isinstance(amps, DeviceState):
+        return amps, False
+    if not isinstance(amps, np.ndarray) or amps.dtype != np.complex128:
+        raise TypeError("amps must be a complex128 ndarray or a DeviceState")
+    if amps.size != 1 << n:
+        raise ValueError("amplitude vector length does not match n")
+    return DeviceState.from_numpy(amps), True
+
+
+def _write_back(dev: DeviceState, amps) -> None:
+    if isinstance(amps, np.ndarray):
+        if amps.flags.c_contiguous:
+            dev.to_numpy(out=amps.reshape(-1))
+        else:
+            amps[...] = dev.to_numpy().reshape(amps.shape)
+        dev.close()
+
+
+# ------------------------------------------------------- kernel-level API
+def zero_state(n: int) -> np.ndarray:
+    """statevector.py:125-128 (host array; see DeviceState for device states)."""
+    return DeviceState(n).to_numpy()
+
+
+def apply_1q(amps, n: int, q: int, m) -> None:
+    dev, tmp = _device_of(amps, n)
+    dev.apply_gates(_single_gate((q,), m))
+    if tmp:
+        _write_back(dev, amps)
+
+
+def apply_2q(amps, n: int, qa: int, qb: int, m) -> None:
+    dev, tmp = _device_of(amps, n)
+    dev.apply_gates(_single_gate((qa, qb), m))
+    if tmp:
+        _write_back(dev, amps)
+
+
+def apply_instruction(amps, n: int, inst) -> None:
+    if inst.kind == "barrier":
+        return
+    dev, tmp = _device_of(amps, n)
+    dev.apply_gates(gate_array([inst]))
+    if tmp:
+        _write_back(dev, amps)
+
+
+def marginal_probs(amps, n: int, qubits) -> np.ndarray:
+    dev, tmp = _device_of(amps, n)
+    out = dev.marginal_probs(qubits)
+    if tmp:
+        dev.close()
+    return out
+
+
+def _measure_qubit(amps, n: int, q: int, rng: np.random.Generator) -> int:
+    """statevector.py:142-149: one draw of ``rng`` (its PCG64 state is used on
+    the device and then advanced by one, exactly as rng.random())."""
+    dev, tmp = _device_of(amps, n)
+    dev.seed_rng(pcg_words(rng))
+    out = dev.measure(q)
+    rng.bit_generator.advance(1)
+    if tmp:
+        _write_back(dev, amps)
+    return out
+
+
+def _reset_qubit(amps, n: int, q: int, rng: np.random.Generator) -> None:
+    dev, tmp = _device_of(amps, n)
+    dev.seed_rng(pcg_words(rng))
+    dev.reset(q)
+    rng.bit_generator.advance(1)
+    if tmp:
+        _write_back(dev, amps)
+
+
+# ------------------------------------------------------------ backend API
+def _sampler_code(sampler: str, k: int) -> int:
+    if sampler == "alias":
+        return _lib.SAMPLER_ALIAS
+    if sampler == "cdf":
+        return _lib.SAMPLER_CDF
+    if sampler == "auto":
+        return _lib.SAMPLER_ALIAS if k <= ALIAS_MAX_QUBITS else _lib.SAMPLER_CDF
+    raise ValueError(f"unknown sampler {sampler!r}")
+
+
+def run(
+    c,
+    shots: int,
+    seed: int,
+    workers: int = 1,
+    qubit_cap: int = DEFAULT_QUBIT_CAP,
+    *,
+    precision: str = "c128",
+    sampler: str = "auto",
+    device: int = 0,
+) -> RunResult:
+    """statevector.py:182-253 on the GPU.  Terminal circuits: one gate program,
+    one device sampling call.  Mid-circuit circuits: device-side replay of the
+    suffix per shot with the PCG64 stream on the device; worker w of
+    ``workers`` uses stream seed+w exactly as the reference fan-out."""
+    if c.n_qubits > qubit_cap:
+        raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
+    if shots < 1:
+        raise ValueError("shots must be positive")
+    measures = measurement_map(c)
+    if not measures:
+        raise NoMeasurementsError("circuit has no measurements")
+    start = time.perf_counter()
+    n = c.n_qubits
+    meta: dict = {"engine": "libsvb", "precision": precision}
+    if terminal_measurement_only(c):
+        state = DeviceState(n, precision, device)
+        try:
+            state.apply_instructions(c.instructions)
+            meta.update(state.stats())
+            qubits = sorted({q for q, _ in measures})
+            src = output_bit_sources(measures, qubits)
+            mode = _sampler_code(sampler, len(qubits))
+            meta["sampler"] = "alias" if mode == _lib.SAMPLER_ALIAS else "cdf"
+            codes, freq = state.sample_codes(qubits, src, shots, pcg_words(seed), mode)
+        finally:
+            state.close()
+        counts = format_counts(codes, freq, len(src))
+    else:
+        counts = _run_replay(c, shots, seed, workers, precision, device, meta)
+    wall = time.perf_counter() - start
+    res = RunResult(counts=counts, shots=shots, backend="sv", seed=seed, wall_time=wall)
+    res.metadata.update(meta)
+    return res
+
+
+def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
+    insts = c.instructions
+    split = next(i for i, x in enumerate(insts) if x.kind in ("measure", "reset"))
+    n = c.n_qubits
+    prefix = DeviceState(n, precision, device)
+    work = DeviceState(n, precision, device)
+    try:
+        prefix.apply_instructions(insts[:split])
+        suffix = [x for x in insts[split:] if x.kind != "barrier"]
+        clbits = clbit_order([(x.qubits[0], x.clbit) for x in suffix if x.kind == "measure"])
+        rank = np.full(max(clbits) + 1, -1, dtype=np.int32)
+        for p, cl in enumerate(clbits):
+            rank[cl] = p
+        gates = gate_array([x for x in suffix if x.kind in UNITARY_GATES])
+        ops = np.zeros((len(suffix), 3), dtype=np.int32)
+        g = 0
+        for j, x in enumerate(suffix):
+            if x.kind == "measure":
+                ops[j] = (1, x.qubits[0], x.clbit)
+            elif x.kind == "reset":
+                ops[j] = (2, x.qubits[0], 0)
+            else:
+                ops[j] = (0, g, 0)
+                g += 1
+        workers = max(1, min(workers, shots))
+        sizes = [shots // workers + (1 if w < shots % workers else 0) for w in range(workers)]
+        all_codes = []
+        for w, size in enumerate(sizes):
+            if size == 0:
+                continue
+            codes = np.empty(size, dtype=np.uint64)
+            words = pcg_words(seed + w)
+            check(
+                lib().svb_replay(
+                    work.handle, prefix.handle, ptr(ops, _lib.c_int32), int(len(suffix)),
+                    ptr(gates) if gates.size else None, ptr(rank, _lib.c_int32), int(size),
+                    ptr(words, _lib.c_uint64), ptr(codes, _lib.c_uint64),
+                )
+            )
+            all_codes.append(codes)
+        meta["replay_shots"] = shots
+    finally:
+        prefix.close()
+        work.close()
+    codes, freq = np.unique(np.concatenate(all_codes), return_counts=True)
+    return format_counts(codes, freq, len(clbits))
+
+
+class _Cached:
+    __slots__ = ("device", "host")
+
+    def __init__(self, device: DeviceState):
+        self.device = device
+        self.host = None
+
+
+_state_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _cached_state(c, qubit_cap: int, precision: str = "c128", device: int = 0) -> _Cached:
+    entry = _state_cache.get(c)
+    if entry is not None:
+        return entry
+    if c.n_qubits > qubit_cap:
+        raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
+    if not terminal_measurement_only(c):
+        raise BackendError("expectation values need a circuit without mid-circuit collapse")
+    state = DeviceState(c.n_qubits, precision, device)
+    state.apply_instructions(c.instructions)
+    entry = _Cached(state)
+    _state_cache[c] = entry
+    return entry
+
+
+def final_state(c, qubit_cap: int = DEFAULT_QUBIT_CAP, *, out: np.ndarray | None = None,
+                precision: str = "c128", device: int = 0) -> np.ndarray:
+    """statevector.py:259-274: the post-unitary state, cached per Circuit object.
+    ``out`` (optional) receives the amplitudes (e.g. a pinned buffer)."""
+    entry = _cached_state(c, qubit_cap, precision, device)
+    if out is not None:
+        return entry.device.to_numpy(out)
+    if entry.host is None:
+        entry.host = entry.device.to_numpy()
+    return entry.host
+
+
+def _z_mask(c, z_qubits) -> int:
+    z = tuple(z_qubits)
+    for q in z:
+        if not 0 <= q < c.n_qubits:
+            raise ValueError(f"qubit {q} out of range")
+    return sum(1 << q for q in set(z))
+
+
+def expectation(c, z_qubits, qubit_cap: int = DEFAULT_QUBIT_CAP) -> float:
+    """statevector.py:277-292: <Z..Z> from one device pass over the cached state."""
+    mask = _z_mask(c, z_qubits)
+    entry = _cached_state(c, qubit_cap)
+    return float(entry.device.expect_z([mask])[0])
+
+
+def expectations(c, z_sets, qubit_cap: int = DEFAULT_QUBIT_CAP) -> np.ndarray:
+    """Many <Z..Z> observables in one pass over the state (extension)."""
+    masks = [_z_mask(c, z) for z in z_sets]
+    entry = _cached_state(c, qubit_cap)
+    return entry.device.expect_z(masks)
+
+
+def plan(n: int, instructions, precision: str = "c128") -> dict:
+    """Host-only schedule summary of a gate program (no GPU needed)."""
+    arr = gate_array(instructions)
+    p, r, b = _lib.c_int64(), _lib.c_int64(), _lib.c_int64()
+    perm = _lib.c_int32()
+    check(lib().svb_plan(n, _prec_code(precision), ptr(arr), int(arr.size), _lib.ctypes.byref(p),
+                         _lib.ctypes.byref(r), _lib.ctypes.byref(b), _lib.ctypes.byref(perm)))
+    return {"passes": p.value, "rounds": r.value, "op_bytes": b.value, "permute": bool(perm.value),
+            "gates": int(arr.size)}
+
+
+def emulate(n: int, instructions, amps: np.ndarray, precision: str = "c128", relabel: bool = True) -> np.ndarray:
+    """Run the fused program on the CPU emulator (test hook; same scheduler and
+    op interpreter as the device kernel).  Returns the new amplitudes."""
+    arr = gate_array(instructions)
+    out = np.ascontiguousarray(amps, dtype=np.complex128).copy()
+    check(lib().svb_emulate_apply(n, _prec_code(precision), ptr(arr), int(arr.size), ptr(out), int(relabel)))
+    return out
+
+
+__all__ = [
+    "DEFAULT_QUBIT_CAP", "DeviceState", "run", "final_state", "expectation", "expectations",
+    "zero_state", "apply_1q", "apply_2q", "apply_instruction", "marginal_probs",
+    "_measure_qubit", "_reset_qubit", "plan", "emulate", "gate_array", "pcg_words",
+    "ONE_QUBIT_GATES", "single_qubit_matrix",
+]

@@ -1,0 +1,230 @@
+"""GPU parity: the libsvb CUDA path against the reference's golden outputs and
+the CPU oracle.  Tolerances (north_star): complex128 amplitudes 1e-10
+normwise relative, complex64 1e-5; <Z> 1e-10 absolute; counts bit-exact
+(alias sampler, shared PCG64 stream) or chi-square p > 1e-3 (CDF sampler)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import chisquare_pvalue, golden, golden_circuits
+from oracle import sv_oracle as orc
+from paper_2512_04216_b200 import _lib, suite
+from paper_2512_04216_b200 import statevector as sv
+from paper_2512_04216_b200.circuit import Circuit, Instruction, inverse_circuit
+from paper_2512_04216_b200.result import BackendError, NoMeasurementsError, QubitCapError
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c128": 1e-10, "c64": 1e-5}
+
+
+def relerr(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def device_state(c, precision="c128", fusion=True):
+    s = sv.DeviceState(c.n_qubits, precision)
+    if not fusion:
+        s.set_option(_lib.OPT_FUSION, 0)
+    s.apply_instructions(c.instructions)
+    return s
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_amplitudes_match_reference_golden(precision):
+    circuits = golden_circuits()
+    for key, ref in golden("amps.npz").items():
+        s = device_state(circuits[key], precision)
+        got = s.to_numpy()
+        s.close()
+        assert relerr(got, ref) < TOL[precision], key
+
+
+def test_final_state_api_and_cache():
+    circuits = golden_circuits()
+    c = circuits["qft_ry_12"]
+    amps = sv.final_state(c)
+    assert amps is sv.final_state(c)
+    assert relerr(amps, golden("amps.npz")["qft_ry_12"]) < 1e-10
+    c2 = suite.ghz_circuit(4, measured=False)
+    sv.expectation(c2, (0,))
+    first = sv._state_cache[c2]
+    sv.expectation(c2, (1, 2))
+    assert sv._state_cache[c2] is first
+
+
+def test_expectations_match_reference_golden():
+    circuits = golden_circuits()
+    for key, rows in golden("expect.json").items():
+        c = circuits[key]
+        for zq, val in rows:
+            assert abs(sv.expectation(c, zq) - val) < 1e-10, (key, zq)
+        many = sv.expectations(c, [zq for zq, _ in rows])
+        np.testing.assert_allclose(many, [v for _, v in rows], atol=1e-10)
+
+
+def test_expectation_kats():
+    g = suite.ghz_circuit(3, measured=False)
+    assert sv.expectation(g, (0, 1)) == pytest.approx(1.0, abs=1e-12)
+    assert sv.expectation(g, (0, 1, 2)) == pytest.approx(0.0, abs=1e-12)
+    ry = Circuit(1).gate("ry", 0, params=(0.9,))
+    assert sv.expectation(ry, (0,)) == pytest.approx(math.cos(0.9), abs=1e-12)
+    with pytest.raises(ValueError):
+        sv.expectation(g, (3,))
+
+
+def test_counts_bit_exact_vs_reference_golden():
+    circuits = golden_circuits()
+    for key, by_seed in golden("counts.json").items():
+        c = circuits[key]
+        workers = 3 if key.endswith("_w3") else 1
+        for seed, ref in by_seed.items():
+            shots = sum(ref.values())
+            res = sv.run(c, shots, int(seed), workers=workers, qubit_cap=max(26, c.n_qubits), sampler="alias")
+            assert res.counts == ref, (key, seed)
+            assert res.backend == "sv" and res.shots == shots
+
+
+def test_kernel_level_api_matches_reference_golden():
+    k = golden("kernels.npz")
+    for i in range(0, int(k["n_cases"]), 3):
+        kind, n, qa, qb = (int(x) for x in k[f"k{i}_meta"])
+        psi = k[f"k{i}_in"].copy()
+        if kind == 1:
+            sv.apply_1q(psi, n, qa, k[f"k{i}_mat"])
+        else:
+            sv.apply_2q(psi, n, qa, qb, k[f"k{i}_mat"])
+        np.testing.assert_allclose(psi, k[f"k{i}_out"], atol=1e-13, err_msg=str(i))
+
+
+def test_alias_tables_bit_exact_vs_reference_golden():
+    a = golden("alias.npz")
+    L = _lib.lib()
+    for i in range(int(a["n_cases"])):
+        p = np.ascontiguousarray(a[f"a{i}_p"])
+        pr = np.empty_like(p)
+        al = np.empty(p.size, dtype=np.int64)
+        _lib.check(L.svb_alias_table(0, _lib.ptr(p, _lib.c_double), p.size, _lib.ptr(pr, _lib.c_double),
+                                     _lib.ptr(al, _lib.c_int64)))
+        np.testing.assert_array_equal(pr, a[f"a{i}_prob"], err_msg=str(i))
+        np.testing.assert_array_equal(al, a[f"a{i}_alias"], err_msg=str(i))
+
+
+def test_alias_table_rejects_bad_vectors():
+    L = _lib.lib()
+    for p in (np.array([0.5, 0.6]), np.array([-0.1, 1.1])):
+        pr = np.empty_like(p)
+        al = np.empty(p.size, dtype=np.int64)
+        with pytest.raises(ValueError):
+            _lib.check(L.svb_alias_table(0, _lib.ptr(p, _lib.c_double), p.size, _lib.ptr(pr, _lib.c_double),
+                                         _lib.ptr(al, _lib.c_int64)))
+
+
+def test_marginals_match_reference_golden():
+    m = golden("marginals.npz")
+    for i in range(int(m["n_cases"])):
+        psi = m[f"m{i}_psi"]
+        n = psi.size.bit_length() - 1
+        got = sv.marginal_probs(psi.copy(), n, tuple(int(q) for q in m[f"m{i}_q"]))
+        np.testing.assert_allclose(got, m[f"m{i}_out"], rtol=1e-13, atol=1e-16)
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_random_circuits_vs_oracle_fused_and_unfused(precision):
+    rng = np.random.default_rng(3)
+    for trial in range(12):
+        n = int(rng.integers(9, 19))
+        c = suite.random_circuit(n, int(rng.integers(20, 300)), rng, measured=False)
+        ref = orc.unitary_state(c)
+        a = device_state(c, precision).to_numpy()
+        b = device_state(c, precision, fusion=False).to_numpy()
+        assert relerr(a, ref) < TOL[precision], (trial, n)
+        assert relerr(b, ref) < TOL[precision], (trial, n)
+
+
+def test_structured_families_vs_oracle():
+    for c in (
+        suite.qft_bench_circuit(16),
+        suite.sycamore_circuit(4, 4, 12, seed=1, measured=False),
+        suite.qaoa_line_circuit(18, 2, seed=5, measured=False),
+        suite.ry_ansatz_circuit(17, 2, seed=6, measured=False),
+    ):
+        ref = orc.unitary_state(c)
+        for precision in ("c128", "c64"):
+            assert relerr(device_state(c, precision).to_numpy(), ref) < TOL[precision], (c.name, precision)
+
+
+def test_qft_dft_known_answer_24_qubits():
+    n = 24
+    basis = 0xA5C3E1
+    c = Circuit(n)
+    for q in range(n):
+        if (basis >> q) & 1:
+            c.gate("x", q)
+    suite.qft(n, c)
+    got = device_state(c).to_numpy()
+    k = np.arange(1 << n, dtype=np.float64)
+    phase = np.mod(basis * k, float(1 << n)) / (1 << n)
+    want = np.exp(2j * math.pi * phase) / math.sqrt(1 << n)
+    assert relerr(got, want) < 1e-10
+
+
+def test_mirror_circuit_26_qubits():
+    rng = np.random.default_rng(9)
+    c = suite.random_circuit(26, 400, rng, measured=False)
+    s = sv.DeviceState(26)
+    s.apply_instructions(c.instructions + inverse_circuit(c).instructions)
+    amp0 = s.to_numpy()[0]
+    assert abs(abs(amp0) - 1.0) < 1e-10
+
+
+def test_cdf_sampler_chi_square():
+    rng = np.random.default_rng(12)
+    for _ in range(4):
+        n = int(rng.integers(5, 11))
+        c = suite.random_circuit(n, 40, rng)
+        psi = orc.unitary_state(c)
+        probs = np.abs(psi) ** 2
+        expected = {format(i, f"0{n}b"): float(p) for i, p in enumerate(probs) if p > 0}
+        res = sv.run(c, 100_000, int(rng.integers(2**31)), sampler="cdf")
+        assert sum(res.counts.values()) == 100_000
+        assert chisquare_pvalue(res.counts, expected, 100_000) > 1e-3
+
+
+def test_seed_determinism_and_error_order():
+    c = suite.random_circuit(12, 60, np.random.default_rng(0))
+    a = sv.run(c, 3000, 42).counts
+    assert a == sv.run(c, 3000, 42).counts
+    assert a != sv.run(c, 3000, 43).counts
+    big = Circuit(27, 27).gate("h", 0).measure(0, 0)
+    with pytest.raises(QubitCapError):
+        sv.run(big, 1, 0)
+    with pytest.raises(ValueError):
+        sv.run(Circuit(2, 2).gate("h", 0).measure(0, 0), 0, 0)
+    with pytest.raises(NoMeasurementsError):
+        sv.run(Circuit(2).gate("h", 0), 10, 0)
+    mid = Circuit(2, 2).gate("h", 0).measure(0, 0).gate("h", 0)
+    with pytest.raises(BackendError):
+        sv.final_state(mid)
+
+
+def test_kernel_level_measure_consumes_one_draw():
+    rng_ref = np.random.default_rng(5)
+    rng_dev = np.random.default_rng(5)
+    for q in range(4):
+        c = suite.random_circuit(4, 20, np.random.default_rng(q), measured=False)
+        psi_ref = orc.unitary_state(c)
+        psi_dev = psi_ref.copy()
+        o_ref = orc.measure_qubit(psi_ref, 4, q, rng_ref)
+        o_dev = sv._measure_qubit(psi_dev, 4, q, rng_dev)
+        assert o_ref == o_dev
+        np.testing.assert_allclose(psi_dev, psi_ref, atol=1e-13)
+    assert rng_ref.random() == rng_dev.random()
+
+
+def test_ghz20_config1_counts_bit_exact():
+    ref = golden("counts.json")["ghz20"]
+    c = suite.ghz_circuit(20)
+    for seed, counts in ref.items():
+        assert sv.run(c, 1024, int(seed)).counts == counts

@@ -1,0 +1,169 @@
+"""CPU-only checks of the host side: IR mirror, generators, the C ABI surface,
+and the fused-program scheduler run through its CPU emulator (same op
+interpreter as the sm_100a kernel) against the oracle."""
+import ctypes
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, golden_circuits
+from oracle import sv_oracle as orc
+from paper_2512_04216_b200 import _lib, suite
+from paper_2512_04216_b200 import statevector as sv
+from paper_2512_04216_b200.circuit import Circuit, CircuitError, Instruction, inverse_circuit
+from paper_2512_04216_b200.features import terminal_measurement_only
+from paper_2512_04216_b200.gates import single_qubit_matrix, two_qubit_matrix
+from paper_2512_04216_b200.result import output_bit_sources
+
+
+# ------------------------------------------------------------------ IR / gates
+def test_ir_validation_mirrors_reference():
+    with pytest.raises(CircuitError):
+        Instruction("cx", (1, 1))
+    with pytest.raises(CircuitError):
+        Instruction("rx", (0,))
+    with pytest.raises(CircuitError):
+        Instruction("measure", (0,))
+    with pytest.raises(CircuitError):
+        Instruction("foo", (0,))
+    with pytest.raises(CircuitError):
+        Circuit(2).gate("h", 2)
+    with pytest.raises(CircuitError):
+        Circuit(0)
+
+
+def test_gate_matrices_match_oracle_definitions():
+    for kind in ("h", "x", "y", "z", "s", "sdg", "t", "tdg"):
+        np.testing.assert_array_equal(single_qubit_matrix(kind), orc.gate_matrix(kind))
+    for kind, p in (("rx", (0.3,)), ("ry", (1.1,)), ("rz", (2.7,)), ("u", (0.3, 1.2, -0.7))):
+        np.testing.assert_array_equal(single_qubit_matrix(kind, p), orc.gate_matrix(kind, p))
+    for kind in ("cx", "cz", "swap"):
+        np.testing.assert_array_equal(two_qubit_matrix(kind), orc.gate_matrix(kind))
+
+
+def test_generators_reproduce_reference_circuits():
+    ref = golden_circuits()
+
+    def same(a, b):
+        return a.n_qubits == b.n_qubits and [
+            (i.kind, tuple(i.qubits), tuple(i.params), i.clbit) for i in a.instructions
+        ] == [(i.kind, tuple(i.qubits), tuple(i.params), i.clbit) for i in b.instructions]
+
+    for n in (5, 8, 12):
+        assert same(suite.ghz_circuit(n, measured=False), ref[f"ghz_{n}"])
+        assert same(suite.qaoa_line_circuit(n, 2, seed=n, measured=False), ref[f"qaoa_{n}"])
+        assert same(suite.ry_ansatz_circuit(n, 2, seed=n, measured=False), ref[f"ry_{n}"])
+    for n in (3, 4, 6, 9, 12):
+        c = Circuit(n)
+        for q in range(n):
+            c.gate("ry", q, params=(0.1 * (q + 1),))
+        assert same(suite.qft(n, c), ref[f"qft_ry_{n}"])
+    # reference random_circuit stream (conftest.py:47-76)
+    rng = np.random.default_rng(20260816)
+    for k in range(40):
+        n = int(rng.integers(1, 11))
+        c = suite.random_circuit(n, int(rng.integers(1, 60)), rng, measured=False)
+        assert same(c, ref[f"rand_{k}"]), k
+
+
+def test_terminal_rule():
+    c = Circuit(2, 2)
+    c.gate("h", 0).measure(0, 0).gate("x", 1)
+    assert terminal_measurement_only(c)
+    c.gate("x", 0)
+    assert not terminal_measurement_only(c)
+    r = Circuit(1, 1)
+    r.append(Instruction("reset", (0,)))
+    assert not terminal_measurement_only(r)
+
+
+def test_bit_sources_last_write_wins():
+    measures = [(0, 1), (1, 0), (2, 1)]
+    assert output_bit_sources(measures, [0, 1, 2]) == [1, 2]
+
+
+# ------------------------------------------------------------------ C ABI
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "svb.h")).read()
+    declared = set(re.findall(r"^(?:int|const char\*)\s+(svb_\w+)\(", header, flags=re.M))
+    assert declared, "no declarations parsed"
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert declared == set(_lib.EXPORTED)
+
+
+def test_library_reports_errors_without_gpu():
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    rc = L.svb_create(0, 1, 0, ctypes.byref(h))
+    assert rc == _lib.SVB_E_ARG
+    assert b"n_qubits" in L.svb_last_error()
+
+
+# ---------------------------------------------------------- scheduler (CPU)
+def _emu_check(c, prec, tol, relabel=True):
+    n = c.n_qubits
+    ref = orc.unitary_state(c)
+    psi0 = np.zeros(1 << n, dtype=complex)
+    psi0[0] = 1
+    got = sv.emulate(n, c.instructions, psi0, prec, relabel=relabel)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err < tol, (n, len(c.instructions), err)
+
+
+@pytest.mark.parametrize("prec,tol,nmin", [("c128", 1e-12, 9), ("c64", 1e-5, 10)])
+def test_fused_program_random_circuits(prec, tol, nmin):
+    rng = np.random.default_rng(7)
+    for trial in range(25):
+        n = int(rng.integers(nmin, nmin + 4))
+        c = suite.random_circuit(n, int(rng.integers(1, 150)), rng, measured=False)
+        _emu_check(c, prec, tol, relabel=bool(trial % 2))
+
+
+def test_fused_program_structured_circuits():
+    for c in (
+        suite.qft_bench_circuit(13),
+        suite.sycamore_circuit(3, 4, 8, seed=3, measured=False),
+        suite.qaoa_line_circuit(12, 2, seed=1, measured=False),
+        suite.ry_ansatz_circuit(11, 3, seed=2, measured=False),
+        suite.ghz_circuit(14, measured=False),
+    ):
+        _emu_check(c, "c128", 1e-12)
+        _emu_check(c, "c64", 1e-5)
+
+
+def test_fused_program_dft_known_answer():
+    n = 12
+    basis = 0b101100111010
+    c = Circuit(n)
+    for q in range(n):
+        if (basis >> q) & 1:
+            c.gate("x", q)
+    suite.qft(n, c)
+    psi0 = np.zeros(1 << n, dtype=complex)
+    psi0[0] = 1
+    got = sv.emulate(n, c.instructions, psi0, "c128")
+    k = np.arange(1 << n)
+    want = np.exp(2j * math.pi * basis * k / (1 << n)) / math.sqrt(1 << n)
+    np.testing.assert_allclose(got, want, atol=1e-12)
+
+
+def test_mirror_circuit_returns_to_zero():
+    rng = np.random.default_rng(11)
+    c = suite.random_circuit(11, 120, rng, measured=False)
+    body = c.instructions + inverse_circuit(c).instructions
+    psi0 = np.zeros(1 << 11, dtype=complex)
+    psi0[0] = 1
+    got = sv.emulate(11, body, psi0, "c128")
+    assert abs(got[0]) > 1 - 1e-10
+
+
+def test_plan_pass_counts():
+    p = sv.plan(30, suite.qft_bench_circuit(30).instructions, "c128")
+    assert p["passes"] <= 8 and p["permute"]
+    p = sv.plan(24, [Instruction("h", (q,)) for q in range(24)], "c128")
+    assert p["passes"] == math.ceil((24 - 5) / 7)
