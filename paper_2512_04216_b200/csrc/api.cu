@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -16,6 +19,7 @@ using namespace svb;
 struct svb_state {
   int n = 0, prec = SVB_C128, device = 0;
   void* amps = nullptr;
+  void* spare = nullptr;  // second state buffer for out-of-place permutation passes
   cudaStream_t st = nullptr;
   uint64_t* d_rng = nullptr;     // PCG64 (state_hi, state_lo, inc_hi, inc_lo)
   int32_t* d_outcome = nullptr;  // last measure outcome
@@ -138,6 +142,7 @@ int svb_destroy(svb_handle h) {
     if (h->d_ws) cudaFreeAsync(h->d_ws, h->st);
     SVB_CUDA(cudaStreamSynchronize(h->st));
     cudaFree(h->amps);
+    if (h->spare) cudaFree(h->spare);
     cudaFree(h->d_rng);
     if (h->t0) cudaEventDestroy(h->t0);
     if (h->t1) cudaEventDestroy(h->t1);
@@ -254,16 +259,24 @@ static void validate_gates(svb_handle h, const svb_gate* g, int ng) {
 
 int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
   return guard([&] {
+    auto t0 = std::chrono::steady_clock::now();
     check_handle(h);
     validate_gates(h, gates, n_gates);
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
     if (h->prec == SVB_C128)
-      run_program_owned<double>(&h->amps, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
     else
-      run_program_owned<float>(&h->amps, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+    auto t1 = std::chrono::steady_clock::now();
     SVB_CUDA(cudaStreamSynchronize(h->st));
     if (h->prof.on) h->prof.collect();
+    if (std::getenv("SVB_TRACE")) {
+      auto t2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[svb] apply host=%.2fms sync=%.2fms\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
   });
 }
 
@@ -504,9 +517,9 @@ int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops
           std::vector<svb_gate> run;
           while (j < n_ops && ops[3 * j] == 0) run.push_back(gates[ops[3 * j + 1]]), ++j;
           if (work->prec == SVB_C128)
-            run_program_owned<double>(&work->amps, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+            run_program_owned<double>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
           else
-            run_program_owned<float>(&work->amps, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+            run_program_owned<float>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
           i = j;
         } else {
           int q = ops[3 * i + 1];

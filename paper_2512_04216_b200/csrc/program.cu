@@ -100,6 +100,8 @@ void emit_block(const Block& b, std::vector<FOp>& out) {
       f.c[0] = M[0]; f.c[1] = M[3]; f.c[2] = M[0]; f.c[3] = M[3];
     } else {
       f.type = (zero(M[0]) && zero(M[3])) ? OP_U1ANTI : OP_U1;
+      if (f.type == OP_U1 && M[0].imag() == 0 && M[1].imag() == 0 && M[2].imag() == 0 && M[3].imag() == 0)
+        f.type = OP_U1R;
       std::copy(M, M + 4, f.c);
       f.active = f.touched;
     }
@@ -149,6 +151,8 @@ void emit_block(const Block& b, std::vector<FOp>& out) {
         continue;
       }
       f.type = (zero(U[0]) && zero(U[3])) ? OP_U1ANTI : OP_U1;
+      if (f.type == OP_U1 && U[0].imag() == 0 && U[1].imag() == 0 && U[2].imag() == 0 && U[3].imag() == 0)
+        f.type = OP_U1R;
       f.q[0] = tgt; f.q[1] = -1;
       std::copy(U, U + 4, f.c);
       f.conds.push_back({ctl, v});
@@ -290,14 +294,22 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     uint64_t S = (m == n) ? ((n == 64) ? ~0ull : ((1ull << n) - 1)) : lanes;
     uint64_t blkA = 0, blkD = 0;
     std::vector<int> placed, skipped;
+    size_t est_bytes = 0;  // upper bound of the encoded op bytes of this pass
+    auto op_bytes = [](const FOp& f) -> size_t {
+      const size_t c = sizeof(cplx<R>);
+      if (f.type == OP_DIAG) return sizeof(OpHdr) + sizeof(DiagHdr) + sizeof(DiagTerm<R>) + 16;
+      if (f.type == OP_U2) return sizeof(OpHdr) + 16 * c + 16;
+      return sizeof(OpHdr) + 4 * c + 32;
+    };
     for (int idx : remaining) {
       const FOp& f = ops[idx];
       bool conflict = (f.touched & blkA) || (f.active & blkD);
-      if (!conflict) {
+      if (!conflict && est_bytes + op_bytes(f) <= kMaxPassOpBytes) {
         uint64_t need = f.active & ~S;
         if (__builtin_popcountll(S | need) <= m) {
           S |= need;
           placed.push_back(idx);
+          est_bytes += op_bytes(f);
           continue;
         }
       }
@@ -345,10 +357,6 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     };
     std::vector<uint32_t> regsets;
     for (auto& rd : rounds) regsets.push_back(fill(rd.first));
-    if (regsets.front() & lane_local) {
-      rounds.insert(rounds.begin(), {0u, {}});
-      regsets.insert(regsets.begin(), fill(0u));
-    }
     if (regsets.back() & lane_local) {
       rounds.push_back({0u, {}});
       regsets.push_back(fill(0u));
@@ -373,6 +381,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     // ---- encode the rounds
     Encoder<R> enc(prog.ops);
     pd.nrounds = (int)rounds.size();
+    pd.ops_begin = (uint32_t)prog.ops.size();
     for (size_t k = 0; k < rounds.size(); ++k) {
       RoundDev& rd = pd.rounds[k];
       uint32_t regs = regsets[k];
@@ -391,22 +400,57 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
         if (f.type == OP_DIAG) {
           size_t j = i;
           while (j < list.size() && ops[list[j]].type == OP_DIAG) ++j;
-          size_t at = enc.begin(OP_DIAG, 0, 0, (int)(j - i), 0, 0, 0, 0);
+          // classify each factor by where its qubits live in this round
+          enum { NONE, TILE, THREAD, REG };
+          auto cls = [&](int q) {
+            if (q < 0) return (int)NONE;
+            if (local_of[q] < 0) return (int)TILE;
+            return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
+          };
+          const bool uniform_ok = pd.ndiag < kMaxDiag;
+          std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
           for (size_t t = i; t < j; ++t) {
             const FOp& d = ops[list[t]];
+            int qa = d.q[0], qb = d.q[1];
+            cd e[4] = {d.c[0], d.c[1], d.c[2], d.c[3]};
+            int ca = cls(qa), cb = cls(qb);
+            if (ca != REG && cb == REG) {  // register qubit first: transpose the factor
+              std::swap(qa, qb);
+              std::swap(ca, cb);
+              std::swap(e[1], e[2]);
+            }
             DiagTerm<R> term{};
-            term.qa = (int8_t)d.q[0];
-            term.qb = (int8_t)d.q[1];
-            term.ra = (int8_t)ridx(d.q[0]);
-            term.rb = (int8_t)ridx(d.q[1]);
-            for (int e = 0; e < 4; ++e) term.d[e] = cvt<R>(d.c[e]);
-            enc.put(term);
+            term.qa = (int8_t)qa;
+            term.qb = (int8_t)qb;
+            term.ra = (int8_t)(ca == REG ? ridx(qa) : -1);
+            term.rb = (int8_t)(cb == REG ? ridx(qb) : -1);
+            for (int k2 = 0; k2 < 4; ++k2) term.d[k2] = cvt<R>(e[k2]);
+            const bool ubit = (cb == TILE || cb == NONE);
+            if (ca == REG && cb == REG) rr.push_back(term);
+            else if (ca == REG && cb == THREAD) tr.push_back(term);
+            else if (ca == REG) (uniform_ok ? ur[term.ra] : tr).push_back(term);
+            else if ((ca == TILE || ca == NONE) && ubit && uniform_ok) uc.push_back(term);
+            else tc.push_back(term);
           }
+          size_t at = enc.begin(OP_DIAG, 0, 0, (int)(j - i), 0, 0, 0, 0);
+          DiagHdr hd{};
+          for (int k2 = 0; k2 < 6; ++k2) hd.nUR[k2] = (int32_t)ur[k2].size();
+          hd.nUC = (int32_t)uc.size();
+          hd.nTR = (int32_t)tr.size();
+          hd.nTC = (int32_t)tc.size();
+          hd.nRR = (int32_t)rr.size();
+          hd.slot = uniform_ok ? pd.ndiag : -1;
+          if (uniform_ok) pd.diag_off[pd.ndiag++] = (uint32_t)prog.ops.size();
+          enc.put(hd);
+          for (int k2 = 0; k2 < 6; ++k2)
+            for (auto& x : ur[k2]) enc.put(x);
+          for (auto* lst : {&uc, &tr, &tc, &rr})
+            for (auto& x : *lst) enc.put(x);
           enc.end(at);
           i = j;
           continue;
         }
-        if (f.type == OP_U1 || f.type == OP_U1ANTI) {
+        if (f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1ANTI) {
           uint64_t fm = 0, fv = 0;
           uint32_t rm = 0, rv = 0;
           for (auto& cv : f.conds) {
@@ -436,6 +480,8 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
       }
       rd.op_end = (uint32_t)prog.ops.size();
     }
+    pd.ops_bytes = (uint32_t)prog.ops.size() - pd.ops_begin;
+    require(pd.ops_bytes <= kMaxPassOpBytes, SVB_E_CUDA, "scheduler: pass op stream too large");
     prog.passes.push_back(pd);
     remaining = skipped;
   }
@@ -460,8 +506,11 @@ static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t
   const uint32_t NT = 1u << (m - RB);
   std::vector<cplx<R>> tile((size_t)1 << m);
   const uint64_t ntiles = 1ull << pd.nout;
+  std::vector<cplx<R>> uni((size_t)kMaxDiag * kUniStride);
   for (uint64_t t = 0; t < ntiles; ++t) {
     const uint64_t base = tile_base(pd, t);
+    for (int d = 0; d < pd.ndiag; ++d)
+      diag_uniform_serial<R, RB>(ops + pd.diag_off[d], base, uni.data() + (size_t)d * kUniStride);
     for (int k = 0; k < pd.nrounds; ++k) {
       const RoundDev& rd = pd.rounds[k];
       for (uint32_t tid = 0; tid < NT; ++tid) {
@@ -480,7 +529,7 @@ static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t
           lidx[v] = lo;
           a[v] = (k == 0) ? state[g] : tile[lo];
         }
-        run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end);
+        run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end, uni.data());
         for (int v = 0; v < V; ++v) {
           if (k == pd.nrounds - 1) state[gidx[v]] = a[v];
           else tile[lidx[v]] = a[v];

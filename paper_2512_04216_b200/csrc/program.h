@@ -37,7 +37,7 @@ struct ProgramStats {
   Profiler* prof = nullptr;
 };
 
-enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4 };
+enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5 };
 
 // Every op: header, then a kind-specific payload.  `bytes` = total size
 // (multiple of 16).  Condition: the op applies where
@@ -57,8 +57,23 @@ template <typename R> struct alignas(16) DiagTerm {
   cplx<R> d[4];
 };
 
+// DIAG payload: DiagHdr, then DiagTerm entries in class order
+//   UR (register bit i x tile bit, grouped by i) | UC (tile x tile) |
+//   TR (register bit x thread bit) | TC (thread-bit constants) | RR (register x register)
+// Classes U* depend only on the tile index and are evaluated once per tile per
+// CTA into the pass's uniform slots (shared memory); T* and RR per thread.
+struct alignas(16) DiagHdr {
+  int32_t nUR[6];
+  int32_t nUC, nTR, nTC, nRR;
+  int32_t slot;
+  int32_t pad[5];
+};
+static_assert(sizeof(DiagHdr) == 64, "DiagHdr layout");
+constexpr int kUniStride = 12;  // cplx per slot: C, U0[5], U1[5], pad
+
 constexpr int kMaxRounds = 24;
 constexpr int kMaxM = 14;
+constexpr int kMaxDiag = 48;
 
 struct RoundDev {
   int32_t reg_local[8];  // local bit of register bit i
@@ -71,54 +86,67 @@ struct PassDev {
   int32_t pos[16];      // physical qubit of local bit l
   int32_t outpos[48];   // physical qubits outside S, ascending (tile index bits)
   RoundDev rounds[kMaxRounds];
+  int32_t ndiag;
+  uint32_t ops_begin, ops_bytes;  // this pass's slice of the op stream (staged in smem)
+  int32_t pad;
+  uint32_t diag_off[kMaxDiag];  // op-stream offsets of this pass's DIAG payloads
 };
+constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
 
 // ------------------------------------------------------------ interpreter
 #define SVB_HD __host__ __device__ __forceinline__
 
-template <typename T> SVB_HD T ldop(const T* p) {
-#ifdef __CUDA_ARCH__
-  return __ldg(p);
-#else
-  return *p;
-#endif
-}
+// op data is staged in shared memory by the pass kernel: plain loads
+template <typename T> SVB_HD T ldop(const T* p) { return *p; }
+template <typename R> SVB_HD cplx<R> ldc(const cplx<R>* p) { return *p; }
 
-template <typename R> SVB_HD cplx<R> ldc(const cplx<R>* p) {
-#ifdef __CUDA_ARCH__
-  return __ldg(p);
-#else
-  return *p;
-#endif
-}
-
-template <typename R, int RB, int B>
+template <typename R, int RB, int B, bool COND>
 SVB_HD void u1_dense(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
   const cplx<R> m0 = ldc<R>(m), m1 = ldc<R>(m + 1), m2 = ldc<R>(m + 2), m3 = ldc<R>(m + 3);
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v) {
     if (v & (1 << B)) continue;
-    if ((v & rmask) != rval) continue;
+    if (COND && (v & rmask) != rval) continue;
     cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
     a[v] = cfma<R>(m1, x1, cmul<R>(m0, x0));
     a[v | (1 << B)] = cfma<R>(m3, x1, cmul<R>(m2, x0));
   }
 }
 
-// [[0, m1], [m2, 0]]
-template <typename R, int RB, int B>
-SVB_HD void u1_anti(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
-  const cplx<R> m1 = ldc<R>(m + 1), m2 = ldc<R>(m + 2);
-  const bool plain = m1.x == R(1) && m1.y == R(0) && m2.x == R(1) && m2.y == R(0);
+// real 2x2 (h, ry, ...): half the multiplies of the complex form
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_real(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const R m0 = ldc<R>(m).x, m1 = ldc<R>(m + 1).x, m2 = ldc<R>(m + 2).x, m3 = ldc<R>(m + 3).x;
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v) {
     if (v & (1 << B)) continue;
-    if ((v & rmask) != rval) continue;
-    cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
-    if (plain) {
-      a[v] = x1;
+    if (COND && (v & rmask) != rval) continue;
+    const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+    a[v] = mk<R>(fma(m1, x1.x, m0 * x0.x), fma(m1, x1.y, m0 * x0.y));
+    a[v | (1 << B)] = mk<R>(fma(m3, x1.x, m2 * x0.x), fma(m3, x1.y, m2 * x0.y));
+  }
+}
+
+// [[0, m1], [m2, 0]]
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_anti(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m1 = ldc<R>(m + 1), m2 = ldc<R>(m + 2);
+  const bool plain = m1.x == R(1) && m1.y == R(0) && m2.x == R(1) && m2.y == R(0);
+  if (plain) {
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v) {
+      if (v & (1 << B)) continue;
+      if (COND && (v & rmask) != rval) continue;
+      const cplx<R> x0 = a[v];
+      a[v] = a[v | (1 << B)];
       a[v | (1 << B)] = x0;
-    } else {
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v) {
+      if (v & (1 << B)) continue;
+      if (COND && (v & rmask) != rval) continue;
+      const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
       a[v] = cmul<R>(m1, x1);
       a[v | (1 << B)] = cmul<R>(m2, x0);
     }
@@ -165,93 +193,128 @@ SVB_HD void u2_perm(cplx<R>* a, const int32_t* src, const cplx<R>* ph, uint32_t 
   }
 }
 
+template <typename R> SVB_HD int fbit(uint64_t F, int q) { return q >= 0 ? (int)((F >> q) & 1ull) : 0; }
+
+// Tile-uniform factors of one DIAG payload (host emulator / reference order).
 template <typename R, int RB>
-SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const DiagTerm<R>* t, int nt) {
+SVB_HD void diag_uniform_serial(const uint8_t* payload, uint64_t base, cplx<R>* slot) {
+  const DiagHdr* h = reinterpret_cast<const DiagHdr*>(payload);
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+  const cplx<R> one = mk<R>(R(1), R(0));
+  for (int i = 0; i < RB; ++i) {
+    cplx<R> u0 = one, u1 = one;
+    for (int k = 0; k < h->nUR[i]; ++k, ++t) {
+      const int f = fbit<R>(base, t->qb);
+      u0 = cmul<R>(u0, t->d[2 * f]);
+      u1 = cmul<R>(u1, t->d[2 * f + 1]);
+    }
+    slot[1 + i] = u0;
+    slot[1 + 5 + i] = u1;
+  }
+  cplx<R> c = one;
+  for (int k = 0; k < h->nUC; ++k, ++t) c = cmul<R>(c, t->d[fbit<R>(base, t->qa) + 2 * fbit<R>(base, t->qb)]);
+  slot[0] = c;
+}
+
+template <typename R, int RB>
+SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cplx<R>* uni) {
   constexpr int V = 1 << RB;
+  const int4 h0 = ldop(reinterpret_cast<const int4*>(payload));      // nUR[0..3]
+  const int4 h1 = ldop(reinterpret_cast<const int4*>(payload) + 1);  // nUR[4..5], nUC, nTR
+  const int4 h2 = ldop(reinterpret_cast<const int4*>(payload) + 2);  // nTC, nRR, slot, -
+  const int nskip = h0.x + h0.y + h0.z + h0.w + h1.x + h1.y + h1.z;
+  const int nTR = h1.w, nTC = h2.x, nRR = h2.y;
   cplx<R> C = mk<R>(R(1), R(0));
   cplx<R> D0[RB], D1[RB];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) D0[i] = D1[i] = mk<R>(R(1), R(0));
-  for (int k = 0; k < nt; ++k) {
-    const int8_t* hb = reinterpret_cast<const int8_t*>(t + k);
-    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(hb));
-    const int ra = (int8_t)(w & 0xff), rb = (int8_t)((w >> 8) & 0xff);
-    const int qa = (int8_t)((w >> 16) & 0xff), qb = (int8_t)((w >> 24) & 0xff);
-    const int fa = (qa >= 0 && ra < 0) ? (int)((Fg >> qa) & 1) : 0;
-    const int fb = (qb >= 0 && rb < 0) ? (int)((Fg >> qb) & 1) : 0;
-    const cplx<R>* d = t[k].d;
-    if (ra < 0 && rb < 0) {
-      C = cmul<R>(C, ldc<R>(d + fa + 2 * fb));
-    } else if (rb < 0) {
-      const cplx<R> e0 = ldc<R>(d + 2 * fb), e1 = ldc<R>(d + 1 + 2 * fb);
+  for (int i = 0; i < RB; ++i) D0[i] = D1[i] = C;
+  if (h2.z >= 0) {
+    const cplx<R>* us = uni + (size_t)h2.z * kUniStride;
+    C = us[0];
 #pragma unroll
-      for (int i = 0; i < RB; ++i)
-        if (i == ra) { D0[i] = cmul<R>(D0[i], e0); D1[i] = cmul<R>(D1[i], e1); }
-    } else if (ra < 0) {
-      const cplx<R> e0 = ldc<R>(d + fa), e1 = ldc<R>(d + fa + 2);
+    for (int i = 0; i < RB; ++i) {
+      D0[i] = us[1 + i];
+      D1[i] = us[1 + 5 + i];
+    }
+  }
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr)) + nskip;
+  for (int k = 0; k < nTR; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int ra = (int8_t)(w & 0xff), qb = (int8_t)((w >> 24) & 0xff);
+    const int f = fbit<R>(Fg, qb);
+    const cplx<R> e0 = ldc<R>(t->d + 2 * f), e1 = ldc<R>(t->d + 2 * f + 1);
 #pragma unroll
-      for (int i = 0; i < RB; ++i)
-        if (i == rb) { D0[i] = cmul<R>(D0[i], e0); D1[i] = cmul<R>(D1[i], e1); }
-    } else {
-      const cplx<R> e0 = ldc<R>(d), e1 = ldc<R>(d + 1), e2 = ldc<R>(d + 2), e3 = ldc<R>(d + 3);
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int ba = (v >> ra) & 1, bb = (v >> rb) & 1;
-        const cplx<R> e = ba ? (bb ? e3 : e1) : (bb ? e2 : e0);
-        a[v] = cmul<R>(a[v], e);
+    for (int i = 0; i < RB; ++i)
+      if (i == ra) {
+        D0[i] = cmul<R>(D0[i], e0);
+        D1[i] = cmul<R>(D1[i], e1);
       }
+  }
+  for (int k = 0; k < nTC; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int qa = (int8_t)((w >> 16) & 0xff), qb = (int8_t)((w >> 24) & 0xff);
+    C = cmul<R>(C, ldc<R>(t->d + fbit<R>(Fg, qa) + 2 * fbit<R>(Fg, qb)));
+  }
+  for (int k = 0; k < nRR; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int ra = (int8_t)(w & 0xff), rb = (int8_t)((w >> 8) & 0xff);
+    const cplx<R> e0 = ldc<R>(t->d), e1 = ldc<R>(t->d + 1), e2 = ldc<R>(t->d + 2), e3 = ldc<R>(t->d + 3);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ba = (v >> ra) & 1, bb = (v >> rb) & 1;
+      a[v] = cmul<R>(a[v], ba ? (bb ? e3 : e1) : (bb ? e2 : e0));
     }
   }
-  // a[v] *= C * prod_i (v_i ? D1[i] : D0[i]): two half tables (low / high
-  // register bits) keep the register footprint at 2^(RB/2) + 2^(RB - RB/2).
-  constexpr int LB = RB / 2, HB = RB - RB / 2;
-  cplx<R> TL[1 << LB], TH[1 << HB];
-  TL[0] = C;
+  // a[v] *= C * prod_i (v_i ? D1[i] : D0[i]).  Fold D0[i] into C so each
+  // register bit contributes one ratio on its v_i = 1 half; skip factors that
+  // are exactly 1 (controlled phases leave the v_i = 0 half untouched).
+  auto is_one = [](cplx<R> z) { return z.x == R(1) && z.y == R(0); };
 #pragma unroll
-  for (int i = 0; i < LB; ++i) {
-#pragma unroll
-    for (int v = 0; v < (1 << i); ++v) {
-      TL[v | (1 << i)] = cmul<R>(TL[v], D1[i]);
-      TL[v] = cmul<R>(TL[v], D0[i]);
+  for (int i = 0; i < RB; ++i) {
+    if (!is_one(D0[i])) {
+      C = cmul<R>(C, D0[i]);
+      // unitary diagonal entries have unit modulus: 1/D0 = conj(D0)
+      D1[i] = cmul<R>(D1[i], mk<R>(D0[i].x, -D0[i].y));
     }
   }
-  TH[0] = mk<R>(R(1), R(0));
+  if (!is_one(C)) {
 #pragma unroll
-  for (int i = 0; i < HB; ++i) {
-#pragma unroll
-    for (int v = 0; v < (1 << i); ++v) {
-      TH[v | (1 << i)] = cmul<R>(TH[v], D1[LB + i]);
-      TH[v] = cmul<R>(TH[v], D0[LB + i]);
-    }
+    for (int v = 0; v < V; ++v) a[v] = cmul<R>(a[v], C);
   }
 #pragma unroll
-  for (int v = 0; v < V; ++v) a[v] = cmul<R>(a[v], cmul<R>(TL[v & ((1 << LB) - 1)], TH[v >> LB]));
+  for (int i = 0; i < RB; ++i) {
+    if (!is_one(D1[i])) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v & (1 << i)) a[v] = cmul<R>(a[v], D1[i]);
+    }
+  }
 }
 
-#define SVB_CASE_B(FN, RB_, BB, ...) \
-  case BB: FN<R, RB_, BB>(__VA_ARGS__); break;
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_kind(int kind, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  if (kind == OP_U1R) u1_real<R, RB, B, COND>(a, m, rmask, rval);
+  else if (kind == OP_U1) u1_dense<R, RB, B, COND>(a, m, rmask, rval);
+  else u1_anti<R, RB, B, COND>(a, m, rmask, rval);
+}
+
+template <typename R, int RB, bool COND>
+SVB_HD void dispatch_u1_c(int kind, int b, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  switch (b) {
+    case 0: u1_kind<R, RB, 0, COND>(kind, a, m, rmask, rval); break;
+    case 1: u1_kind<R, RB, 1, COND>(kind, a, m, rmask, rval); break;
+    case 2: u1_kind<R, RB, 2, COND>(kind, a, m, rmask, rval); break;
+    case 3: u1_kind<R, RB, 3, COND>(kind, a, m, rmask, rval); break;
+    default:
+      if constexpr (RB > 4) u1_kind<R, RB, (RB > 4 ? 4 : 0), COND>(kind, a, m, rmask, rval);
+      break;
+  }
+}
 
 template <typename R, int RB>
 SVB_HD void dispatch_u1(int kind, int b, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
-  if (kind == OP_U1) {
-    switch (b) {
-      SVB_CASE_B(u1_dense, RB, 0, a, m, rmask, rval)
-      SVB_CASE_B(u1_dense, RB, 1, a, m, rmask, rval)
-      SVB_CASE_B(u1_dense, RB, 2, a, m, rmask, rval)
-      SVB_CASE_B(u1_dense, RB, 3, a, m, rmask, rval)
-      default:
-        if constexpr (RB > 4) { u1_dense<R, RB, (RB > 4 ? 4 : 0)>(a, m, rmask, rval); }
-    }
-  } else {
-    switch (b) {
-      SVB_CASE_B(u1_anti, RB, 0, a, m, rmask, rval)
-      SVB_CASE_B(u1_anti, RB, 1, a, m, rmask, rval)
-      SVB_CASE_B(u1_anti, RB, 2, a, m, rmask, rval)
-      SVB_CASE_B(u1_anti, RB, 3, a, m, rmask, rval)
-      default:
-        if constexpr (RB > 4) { u1_anti<R, RB, (RB > 4 ? 4 : 0)>(a, m, rmask, rval); }
-    }
-  }
+  if (rmask == 0) dispatch_u1_c<R, RB, false>(kind, b, a, m, 0, 0);
+  else dispatch_u1_c<R, RB, true>(kind, b, a, m, rmask, rval);
 }
 
 template <typename R, int RB, int B1, int B2>
@@ -293,7 +356,7 @@ SVB_HD void dispatch_u2(int kind, int b1, int b2, cplx<R>* a, const uint8_t* p, 
 
 // Run the ops in [off, end) of the op stream on one thread's registers.
 template <typename R, int RB>
-SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, uint32_t end) {
+SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, uint32_t end, const cplx<R>* uni) {
   while (off < end) {
     const OpHdr* h = reinterpret_cast<const OpHdr*>(ops + off);
     const int4 w0 = ldop(reinterpret_cast<const int4*>(h));          // kind, a, b, n
@@ -304,9 +367,10 @@ SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, u
     if ((Fg & w1.x) != w1.y) continue;
     switch (w0.x) {
       case OP_DIAG:
-        diag_apply<R, RB>(a, Fg, reinterpret_cast<const DiagTerm<R>*>(payload), w0.w);
+        diag_apply<R, RB>(a, Fg, payload, uni);
         break;
       case OP_U1:
+      case OP_U1R:
       case OP_U1ANTI:
         dispatch_u1<R, RB>(w0.x, w0.y, a, reinterpret_cast<const cplx<R>*>(payload), w2.x, w2.y);
         break;
@@ -322,8 +386,10 @@ template <typename R> SVB_HD uint32_t swz(uint32_t j);
 template <> SVB_HD uint32_t swz<double>(uint32_t j) {
   return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7u);
 }
+// complex64: bit 0 is left alone so an aligned pair (j, j^1) stays one 16-byte
+// unit (cp.async copies c64 amplitudes in pairs)
 template <> SVB_HD uint32_t swz<float>(uint32_t j) {
-  return j ^ (((j >> 4) ^ (j >> 8) ^ (j >> 12)) & 15u);
+  return j ^ ((((j >> 4) ^ (j >> 7) ^ (j >> 10)) & 7u) << 1);
 }
 
 // Thread layout of round `rd`: fixed local index and fixed global index.
@@ -376,8 +442,10 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
 
 // As run_program, but may replace *state (swap relabeling ends with an
 // out-of-place permutation pass into a fresh cudaMalloc buffer).
+// *spare: a second state-sized buffer owned by the handle (allocated on first
+// use, nullptr if it cannot be); the permutation writes into it and swaps.
 template <typename R>
-void run_program_owned(void** state, int n, const svb_gate* g, int ng, int fusion, cudaStream_t st,
+void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, cudaStream_t st,
                        ProgramStats* stats);
 
 // CPU emulation of a program on a host state (same op interpreter).

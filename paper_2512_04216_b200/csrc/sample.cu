@@ -13,11 +13,11 @@
 //     scaled      : probs * (m / total);
 //     each round  : deficits / capacities -> inclusive scans -> lower_bound
 //                   (searchsorted side='left') -> owner; bincount(owner,
-//                   deficits) as a deterministic reduce-by-key (owner is
-//                   monotone); stable compactions for the next round.
-//   Differences to numpy are confined to floating-point association inside
-//   the scans and the per-owner sums (numpy is sequential); they can move a
-//   sample only when a uniform lands within a few ulps of a threshold.
+//                   deficits) as sequential per-owner sums (owner is monotone,
+//                   so each bin is one run: bit-identical to numpy); stable
+//                   compactions for the next round.
+//   The two cumsums are sequential on the device as in numpy, so given the
+//   same probability vector the table is bit-identical to the reference's.
 // * CDF (native) — fused |amp|^2 + per-32-amplitude leaf sums, one inclusive
 //   scan over the leaves, then per shot a binary search over leaf prefixes and
 //   a 32-element scan inside the leaf.  Passes chi^2 against |amp|^2.
@@ -188,6 +188,34 @@ static void cub_inclusive_sum(const double* in, double* out, uint64_t n, cudaStr
   SVB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
 }
 
+// np.cumsum is a left-to-right accumulation; ties between deficit and capacity
+// prefixes are common (symmetric distributions), so the alias build reproduces
+// it exactly: one thread runs the dependent add chain while the loads stream.
+__global__ void k_seq_cumsum(const double* __restrict__ in, double* __restrict__ out, uint64_t n) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double acc = 0.0;
+  uint64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = in[i + k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc += x[k];
+      out[i + k] = acc;
+    }
+  }
+  for (; i < n; ++i) {
+    acc += in[i];
+    out[i] = acc;
+  }
+}
+
+static void seq_cumsum(const double* in, double* out, uint64_t n, cudaStream_t st) {
+  k_seq_cumsum<<<1, 1, 0, st>>>(in, out, n);
+  SVB_CHECK_LAUNCH();
+}
+
 // ------------------------------------------------------------- alias build
 __global__ void k_alias_init(const double* __restrict__ probs, uint64_t m, double factor,
                              double* __restrict__ scaled, double* __restrict__ prob_row,
@@ -254,12 +282,31 @@ __global__ void k_owner(const double* __restrict__ dcum, uint64_t ns, const doub
   }
 }
 
-__global__ void k_absorb(const int64_t* __restrict__ uniq, const double* __restrict__ agg,
-                         const int64_t* __restrict__ nruns, double* __restrict__ rem) {
-  const int64_t nr = *nruns;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += stride)
-    rem[uniq[r]] = rem[uniq[r]] - agg[r];
+// owner is non-decreasing: a run of equal owners is one bincount bin.
+__global__ void k_run_heads(const int64_t* __restrict__ owner, uint64_t ns, int64_t* __restrict__ head) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride)
+    head[i] = (i == 0 || owner[i] != owner[i - 1]) ? 1 : 0;
+}
+__global__ void k_run_starts(const int64_t* __restrict__ head, const int64_t* __restrict__ hpos, uint64_t ns,
+                             int64_t* __restrict__ starts) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride)
+    if (head[i]) starts[hpos[i]] = (int64_t)i;
+}
+// np.bincount(owner, weights=deficits): each bin sums its weights sequentially
+// from 0.0 in index order — reproduced exactly, one thread per run.
+__global__ void k_absorb(const int64_t* __restrict__ starts, uint64_t nruns, uint64_t ns,
+                         const int64_t* __restrict__ owner, const double* __restrict__ deficit,
+                         double* __restrict__ rem) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += stride) {
+    const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
+    double acc = 0.0;
+    for (uint64_t i = b; i < e; ++i) acc += deficit[i];
+    const int64_t o = owner[b];
+    rem[o] = rem[o] - acc;
+  }
 }
 
 __global__ void k_conv_flags(const double* __restrict__ rem, uint64_t nl, int64_t* __restrict__ conv) {
@@ -317,7 +364,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
   // round scratch, sized for the first (largest) round
   DevBuf deficit(sizeof(double) * ns, st), dcum(sizeof(double) * ns, st), owner(sizeof(int64_t) * ns, st);
   DevBuf cap(sizeof(double) * nl, st), ccum(sizeof(double) * nl, st);
-  DevBuf uniq(sizeof(int64_t) * nl, st), agg(sizeof(double) * nl, st), nruns(sizeof(int64_t), st);
+  DevBuf head(sizeof(int64_t) * ns, st), hpos(sizeof(int64_t) * ns, st), starts(sizeof(int64_t) * ns, st);
   DevBuf conv(sizeof(int64_t) * nl, st), cpos(sizeof(int64_t) * nl, st);
   DevBuf larges2(sizeof(int64_t) * nl, st), rem2(sizeof(double) * nl, st);
   int64_t* L = larges.as<int64_t>();
@@ -325,28 +372,26 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
   double* Rm = rem.as<double>();
   double* Rm2 = rem2.as<double>();
   int64_t* S = smalls.as<int64_t>();
-  size_t rbk_bytes = 0;
-  SVB_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, rbk_bytes, owner.as<int64_t>(), uniq.as<int64_t>(),
-                                          deficit.as<double>(), agg.as<double>(), nruns.as<int64_t>(),
-                                          ::cuda::std::plus<double>(), (int64_t)ns, st));
-  DevBuf rbk_tmp(rbk_bytes, st);
 
   while (ns > 0 && nl > 0) {
     k_deficit<<<grid_for(ns, B), B, 0, st>>>(scaled.as<double>(), S, ns, deficit.as<double>());
     k_capacity<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, cap.as<double>());
     SVB_CHECK_LAUNCH();
-    cub_inclusive_sum(deficit.as<double>(), dcum.as<double>(), ns, st);
-    cub_inclusive_sum(cap.as<double>(), ccum.as<double>(), nl, st);
+    seq_cumsum(deficit.as<double>(), dcum.as<double>(), ns, st);
+    seq_cumsum(cap.as<double>(), ccum.as<double>(), nl, st);
     k_owner<<<grid_for(ns, B), B, 0, st>>>(dcum.as<double>(), ns, ccum.as<double>(), nl, S, L,
                                            scaled.as<double>(), owner.as<int64_t>(), d_prob_row,
                                            d_alias_row);
     SVB_CHECK_LAUNCH();
-    size_t b = rbk_bytes;
-    SVB_CUDA(cub::DeviceReduce::ReduceByKey(rbk_tmp.p, b, owner.as<int64_t>(), uniq.as<int64_t>(),
-                                            deficit.as<double>(), agg.as<double>(), nruns.as<int64_t>(),
-                                            ::cuda::std::plus<double>(), (int64_t)ns, st));
-    k_absorb<<<grid_for(ns < nl ? ns : nl, B), B, 0, st>>>(uniq.as<int64_t>(), agg.as<double>(),
-                                                           nruns.as<int64_t>(), Rm);
+    k_run_heads<<<grid_for(ns, B), B, 0, st>>>(owner.as<int64_t>(), ns, head.as<int64_t>());
+    SVB_CHECK_LAUNCH();
+    cub_exclusive_sum(head.as<int64_t>(), hpos.as<int64_t>(), ns, st);
+    k_run_starts<<<grid_for(ns, B), B, 0, st>>>(head.as<int64_t>(), hpos.as<int64_t>(), ns, starts.as<int64_t>());
+    SVB_CHECK_LAUNCH();
+    const uint64_t nruns = (uint64_t)d2h_scalar(hpos.as<int64_t>() + (ns - 1), st) +
+                           (uint64_t)d2h_scalar(head.as<int64_t>() + (ns - 1), st);
+    k_absorb<<<grid_for(nruns, 64), 64, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
+                                                 deficit.as<double>(), Rm);
     k_conv_flags<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, conv.as<int64_t>());
     SVB_CHECK_LAUNCH();
     cub_exclusive_sum(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);
