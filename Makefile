@@ -13,8 +13,14 @@ build/%.o: paper_2512_04216_b200/csrc/%.cu $(HDR)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > build/$*.ptxas.log 2>&1 || (cat build/$*.ptxas.log; exit 1)
 
-$(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+# device_core.cuh is embedded so the NVRTC JIT can compile against it
+build/device_core_src.o: paper_2512_04216_b200/csrc/device_core.cuh
+	@mkdir -p build
+	( printf 'extern const char svb_device_core_src[];\nconst char svb_device_core_src[] = R"SVBRAW('; cat $<; printf ')SVBRAW";\n' ) > build/device_core_src.cpp
+	g++ -O2 -fPIC -c build/device_core_src.cpp -o $@
+
+$(LIB): $(OBJ) build/device_core_src.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) build/device_core_src.o -ldl
 
 clean:
 	rm -rf build $(LIB)

@@ -74,7 +74,8 @@ int svb_host_free(void* p);
 
 typedef enum {
   SVB_OPT_FUSION = 0,   /* 1 (default): fused multi-gate HBM passes; 0: one pass per gate */
-  SVB_OPT_MAX_HIGH = 1  /* fused pass: max non-lane qubits per pass (tuning; default auto) */
+  SVB_OPT_MAX_HIGH = 1,  /* fused pass: max non-lane qubits per pass (tuning; default auto) */
+  SVB_OPT_JIT_MIN_N = 2  /* NVRTC-specialise fused passes for n >= value (default 20; -1 never) */
 } svb_option;
 int svb_set_option(svb_handle h, int option, int value);
 /* Statistics of the last svb_apply: HBM passes launched, gates applied. */
@@ -149,6 +150,10 @@ int svb_plan(int n, int precision, const svb_gate* gates, int n_gates, int64_t* 
              int64_t* n_rounds, int64_t* op_bytes, int32_t* has_perm);
 int svb_emulate_apply(int n, int precision, const svb_gate* gates, int n_gates, double* amps,
                       int relabel_swaps);
+/* Generate and NVRTC-compile the specialised pass kernels of a program (no
+ * GPU needed); cubin size out, compiler log into log[log_cap]. */
+int svb_jit_check(int n, int precision, const svb_gate* gates, int n_gates, int64_t* cubin_bytes, char* log,
+                  int log_cap);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb.so")
 SVB_OK, SVB_E_ARG, SVB_E_CAP, SVB_E_OOM, SVB_E_CUDA, SVB_E_NCCL, SVB_E_SAMPLING = range(7)
 SVB_C64, SVB_C128 = 0, 1
 SAMPLER_ALIAS, SAMPLER_CDF = 0, 1
-OPT_FUSION, OPT_MAX_HIGH = 0, 1
+OPT_FUSION, OPT_MAX_HIGH, OPT_JIT_MIN_N = 0, 1, 2
 
 try:  # the reference's error type when installed (sampling.py:17-18)
     from polysim.sampling import SamplingError  # type: ignore
@@ -74,6 +74,7 @@ _SIGS = {
     "svb_replay": (c_int, [_h, _h, _i32p, c_int, c_void_p, _i32p, c_uint64, _u64p, _u64p]),
     "svb_plan": (c_int, [c_int, c_int, c_void_p, c_int, _i64p, _i64p, _i64p, _i32p]),
     "svb_emulate_apply": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, c_int]),
+    "svb_jit_check": (c_int, [c_int, c_int, c_void_p, c_int, _i64p, ctypes.c_char_p, c_int]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -26,6 +26,7 @@ struct svb_state {
   double* d_ws = nullptr;        // reduction scratch
   size_t ws_doubles = 0;
   int fusion = 1, max_high = -1;
+  int jit_min_n = 20;  // NVRTC-specialised passes from this many qubits up (-1: never)
   ProgramStats stats{};
   Profiler prof;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -165,6 +166,7 @@ int svb_set_option(svb_handle h, int option, int value) {
     check_handle(h);
     if (option == SVB_OPT_FUSION) h->fusion = value;
     else if (option == SVB_OPT_MAX_HIGH) h->max_high = value;
+    else if (option == SVB_OPT_JIT_MIN_N) h->jit_min_n = value;
     else throw Error(SVB_E_ARG, "unknown option");
   });
 }
@@ -265,9 +267,9 @@ int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
     if (h->prec == SVB_C128)
-      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats);
     else
-      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->st, &h->stats);
+      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats);
     auto t1 = std::chrono::steady_clock::now();
     SVB_CUDA(cudaStreamSynchronize(h->st));
     if (h->prof.on) h->prof.collect();
@@ -517,9 +519,9 @@ int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops
           std::vector<svb_gate> run;
           while (j < n_ops && ops[3 * j] == 0) run.push_back(gates[ops[3 * j + 1]]), ++j;
           if (work->prec == SVB_C128)
-            run_program_owned<double>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+            run_program_owned<double>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats);
           else
-            run_program_owned<float>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, st, &work->stats);
+            run_program_owned<float>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats);
           i = j;
         } else {
           int q = ops[3 * i + 1];

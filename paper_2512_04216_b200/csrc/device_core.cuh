@@ -1,0 +1,780 @@
+// Device code shared by the libsvb kernels (nvcc) and the JIT-compiled pass
+// kernels (NVRTC): complex arithmetic, the op/pass data layout, the per-thread
+// op interpreter, and the persistent fused-pass skeleton.  No host-only
+// includes here: NVRTC compiles this header as-is.
+#pragma once
+#ifndef __CUDACC_RTC__
+#include <stdint.h>
+#else
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+#endif
+
+namespace svb {
+
+// ---- complex arithmetic on float2 / double2 --------------------------------
+template <typename R> struct CT;
+template <> struct CT<float> { using T = float2; };
+template <> struct CT<double> { using T = double2; };
+template <typename R> using cplx = typename CT<R>::T;
+
+template <typename R> __host__ __device__ __forceinline__ cplx<R> mk(R x, R y) {
+  cplx<R> r; r.x = x; r.y = y; return r;
+}
+template <typename R>
+__host__ __device__ __forceinline__ cplx<R> cmul(cplx<R> a, cplx<R> b) {
+  return mk<R>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc + a*b
+template <typename R>
+__host__ __device__ __forceinline__ cplx<R> cfma(cplx<R> a, cplx<R> b, cplx<R> acc) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+template <typename R> __host__ __device__ __forceinline__ R norm2(cplx<R> a) {
+  return a.x * a.x + a.y * a.y;
+}
+
+// insert a zero bit at position q
+__host__ __device__ __forceinline__ uint64_t insert0(uint64_t i, int q) {
+  uint64_t lo = i & ((1ull << q) - 1ull);
+  return ((i >> q) << (q + 1)) | lo;
+}
+
+enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5 };
+
+// Every op: header, then a kind-specific payload.  `bytes` = total size
+// (multiple of 16).  Condition: the op applies where
+// (Fg & fmask) == fval  and  (v & rmask) == rval  (v = register index).
+struct alignas(16) OpHdr {
+  int32_t kind, a, b, n;      // a, b: register bits; n: DIAG term count
+  uint64_t fmask, fval;       // condition on fixed global index bits
+  uint32_t rmask, rval, bytes, pad;
+};
+static_assert(sizeof(OpHdr) == 48, "OpHdr layout");
+
+// Diagonal factor d[bit(qa) + 2 bit(qb)]; ra/rb = register bit or -1 (then
+// the bit is read from the fixed global index at position qa/qb; q = -1 -> 0).
+template <typename R> struct alignas(16) DiagTerm {
+  int8_t ra, rb, qa, qb;
+  int32_t pad[3];
+  cplx<R> d[4];
+};
+
+// DIAG payload: DiagHdr, then DiagTerm entries in class order
+//   UR (register bit i x tile bit, grouped by i) | UC (tile x tile) |
+//   TR (register bit x thread bit) | TC (thread-bit constants) | RR (register x register)
+// Classes U* depend only on the tile index and are evaluated once per tile per
+// CTA into the pass's uniform slots (shared memory); T* and RR per thread.
+struct alignas(16) DiagHdr {
+  int32_t nUR[6];
+  int32_t nUC, nTR, nTC, nRR;
+  int32_t slot;
+  int32_t pad[5];
+};
+static_assert(sizeof(DiagHdr) == 64, "DiagHdr layout");
+constexpr int kUniStride = 12;  // cplx per slot: C, U0[5], U1[5], pad
+
+constexpr int kMaxRounds = 24;
+constexpr int kMaxM = 14;
+constexpr int kMaxDiag = 48;
+
+struct RoundDev {
+  int32_t reg_local[8];  // local bit of register bit i
+  uint32_t op_off, op_end;
+  uint32_t regmask_local, pad;
+};
+
+struct PassDev {
+  int32_t m, nrounds, nout, rb;
+  int32_t pos[16];      // physical qubit of local bit l
+  int32_t outpos[48];   // physical qubits outside S, ascending (tile index bits)
+  RoundDev rounds[kMaxRounds];
+  int32_t ndiag;
+  uint32_t ops_begin, ops_bytes;  // this pass's slice of the op stream (staged in smem)
+  int32_t pad;
+  uint32_t diag_off[kMaxDiag];  // op-stream offsets of this pass's DIAG payloads
+};
+constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
+
+// ------------------------------------------------------------ interpreter
+#define SVB_HD __host__ __device__ __forceinline__
+
+// op data is staged in shared memory by the pass kernel: plain loads
+template <typename T> SVB_HD T ldop(const T* p) { return *p; }
+template <typename R> SVB_HD cplx<R> ldc(const cplx<R>* p) { return *p; }
+
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_dense(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m0 = ldc<R>(m), m1 = ldc<R>(m + 1), m2 = ldc<R>(m + 2), m3 = ldc<R>(m + 3);
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & (1 << B)) continue;
+    if (COND && (v & rmask) != rval) continue;
+    cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+    a[v] = cfma<R>(m1, x1, cmul<R>(m0, x0));
+    a[v | (1 << B)] = cfma<R>(m3, x1, cmul<R>(m2, x0));
+  }
+}
+
+// real 2x2 (h, ry, ...): half the multiplies of the complex form
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_real(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const R m0 = ldc<R>(m).x, m1 = ldc<R>(m + 1).x, m2 = ldc<R>(m + 2).x, m3 = ldc<R>(m + 3).x;
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & (1 << B)) continue;
+    if (COND && (v & rmask) != rval) continue;
+    const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+    a[v] = mk<R>(fma(m1, x1.x, m0 * x0.x), fma(m1, x1.y, m0 * x0.y));
+    a[v | (1 << B)] = mk<R>(fma(m3, x1.x, m2 * x0.x), fma(m3, x1.y, m2 * x0.y));
+  }
+}
+
+// [[0, m1], [m2, 0]]
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_anti(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m1 = ldc<R>(m + 1), m2 = ldc<R>(m + 2);
+  const bool plain = m1.x == R(1) && m1.y == R(0) && m2.x == R(1) && m2.y == R(0);
+  if (plain) {
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v) {
+      if (v & (1 << B)) continue;
+      if (COND && (v & rmask) != rval) continue;
+      const cplx<R> x0 = a[v];
+      a[v] = a[v | (1 << B)];
+      a[v | (1 << B)] = x0;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v) {
+      if (v & (1 << B)) continue;
+      if (COND && (v & rmask) != rval) continue;
+      const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+      a[v] = cmul<R>(m1, x1);
+      a[v | (1 << B)] = cmul<R>(m2, x0);
+    }
+  }
+}
+
+template <typename R, int RB, int B1, int B2>
+SVB_HD void u2_dense(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & ((1 << B1) | (1 << B2))) continue;
+    if ((v & rmask) != rval) continue;
+    const int i0 = v, i1 = v | (1 << B1), i2 = v | (1 << B2), i3 = v | (1 << B1) | (1 << B2);
+    cplx<R> x[4] = {a[i0], a[i1], a[i2], a[i3]};
+    cplx<R> y[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      cplx<R> acc = cmul<R>(ldc<R>(m + 4 * r), x[0]);
+      acc = cfma<R>(ldc<R>(m + 4 * r + 1), x[1], acc);
+      acc = cfma<R>(ldc<R>(m + 4 * r + 2), x[2], acc);
+      acc = cfma<R>(ldc<R>(m + 4 * r + 3), x[3], acc);
+      y[r] = acc;
+    }
+    a[i0] = y[0]; a[i1] = y[1]; a[i2] = y[2]; a[i3] = y[3];
+  }
+}
+
+// out[r] = ph[r] * in[src[r]]
+template <typename R, int RB, int B1, int B2>
+SVB_HD void u2_perm(cplx<R>* a, const int32_t* src, const cplx<R>* ph, uint32_t rmask, uint32_t rval) {
+  const int s0 = ldop(src), s1 = ldop(src + 1), s2 = ldop(src + 2), s3 = ldop(src + 3);
+  const cplx<R> p0 = ldc<R>(ph), p1 = ldc<R>(ph + 1), p2 = ldc<R>(ph + 2), p3 = ldc<R>(ph + 3);
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & ((1 << B1) | (1 << B2))) continue;
+    if ((v & rmask) != rval) continue;
+    const int i0 = v, i1 = v | (1 << B1), i2 = v | (1 << B2), i3 = v | (1 << B1) | (1 << B2);
+    cplx<R> x[4] = {a[i0], a[i1], a[i2], a[i3]};
+    auto pick = [&](int s) { return s == 0 ? x[0] : s == 1 ? x[1] : s == 2 ? x[2] : x[3]; };
+    a[i0] = cmul<R>(p0, pick(s0));
+    a[i1] = cmul<R>(p1, pick(s1));
+    a[i2] = cmul<R>(p2, pick(s2));
+    a[i3] = cmul<R>(p3, pick(s3));
+  }
+}
+
+template <typename R> SVB_HD int fbit(uint64_t F, int q) { return q >= 0 ? (int)((F >> q) & 1ull) : 0; }
+
+// Tile-uniform factors of one DIAG payload (host emulator / reference order).
+template <typename R, int RB>
+SVB_HD void diag_uniform_serial(const uint8_t* payload, uint64_t base, cplx<R>* slot) {
+  const DiagHdr* h = reinterpret_cast<const DiagHdr*>(payload);
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+  const cplx<R> one = mk<R>(R(1), R(0));
+  for (int i = 0; i < RB; ++i) {
+    cplx<R> u0 = one, u1 = one;
+    for (int k = 0; k < h->nUR[i]; ++k, ++t) {
+      const int f = fbit<R>(base, t->qb);
+      u0 = cmul<R>(u0, t->d[2 * f]);
+      u1 = cmul<R>(u1, t->d[2 * f + 1]);
+    }
+    slot[1 + i] = u0;
+    slot[1 + 5 + i] = u1;
+  }
+  cplx<R> c = one;
+  for (int k = 0; k < h->nUC; ++k, ++t) c = cmul<R>(c, t->d[fbit<R>(base, t->qa) + 2 * fbit<R>(base, t->qb)]);
+  slot[0] = c;
+}
+
+template <typename R, int RB>
+SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cplx<R>* uni) {
+  constexpr int V = 1 << RB;
+  const int4 h0 = ldop(reinterpret_cast<const int4*>(payload));      // nUR[0..3]
+  const int4 h1 = ldop(reinterpret_cast<const int4*>(payload) + 1);  // nUR[4..5], nUC, nTR
+  const int4 h2 = ldop(reinterpret_cast<const int4*>(payload) + 2);  // nTC, nRR, slot, -
+  const int nskip = h0.x + h0.y + h0.z + h0.w + h1.x + h1.y + h1.z;
+  const int nTR = h1.w, nTC = h2.x, nRR = h2.y;
+  cplx<R> C = mk<R>(R(1), R(0));
+  cplx<R> D0[RB], D1[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) D0[i] = D1[i] = C;
+  if (h2.z >= 0) {
+    const cplx<R>* us = uni + (size_t)h2.z * kUniStride;
+    C = us[0];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      D0[i] = us[1 + i];
+      D1[i] = us[1 + 5 + i];
+    }
+  }
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr)) + nskip;
+  for (int k = 0; k < nTR; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int ra = (int8_t)(w & 0xff), qb = (int8_t)((w >> 24) & 0xff);
+    const int f = fbit<R>(Fg, qb);
+    const cplx<R> e0 = ldc<R>(t->d + 2 * f), e1 = ldc<R>(t->d + 2 * f + 1);
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if (i == ra) {
+        D0[i] = cmul<R>(D0[i], e0);
+        D1[i] = cmul<R>(D1[i], e1);
+      }
+  }
+  for (int k = 0; k < nTC; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int qa = (int8_t)((w >> 16) & 0xff), qb = (int8_t)((w >> 24) & 0xff);
+    C = cmul<R>(C, ldc<R>(t->d + fbit<R>(Fg, qa) + 2 * fbit<R>(Fg, qb)));
+  }
+  for (int k = 0; k < nRR; ++k, ++t) {
+    const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
+    const int ra = (int8_t)(w & 0xff), rb = (int8_t)((w >> 8) & 0xff);
+    const cplx<R> e0 = ldc<R>(t->d), e1 = ldc<R>(t->d + 1), e2 = ldc<R>(t->d + 2), e3 = ldc<R>(t->d + 3);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int ba = (v >> ra) & 1, bb = (v >> rb) & 1;
+      a[v] = cmul<R>(a[v], ba ? (bb ? e3 : e1) : (bb ? e2 : e0));
+    }
+  }
+  // a[v] *= C * prod_i (v_i ? D1[i] : D0[i]).  Fold D0[i] into C so each
+  // register bit contributes one ratio on its v_i = 1 half; skip factors that
+  // are exactly 1 (controlled phases leave the v_i = 0 half untouched).
+  auto is_one = [](cplx<R> z) { return z.x == R(1) && z.y == R(0); };
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    if (!is_one(D0[i])) {
+      C = cmul<R>(C, D0[i]);
+      // unitary diagonal entries have unit modulus: 1/D0 = conj(D0)
+      D1[i] = cmul<R>(D1[i], mk<R>(D0[i].x, -D0[i].y));
+    }
+  }
+  if (!is_one(C)) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) a[v] = cmul<R>(a[v], C);
+  }
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    if (!is_one(D1[i])) {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (v & (1 << i)) a[v] = cmul<R>(a[v], D1[i]);
+    }
+  }
+}
+
+// Value-taking entry points (JIT bodies pass immediates).
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_real_v(cplx<R>* a, R m0, R m1, R m2, R m3, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m[4] = {mk<R>(m0, R(0)), mk<R>(m1, R(0)), mk<R>(m2, R(0)), mk<R>(m3, R(0))};
+  u1_real<R, RB, B, COND>(a, m, rmask, rval);
+}
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_dense_v(cplx<R>* a, cplx<R> m0, cplx<R> m1, cplx<R> m2, cplx<R> m3, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m[4] = {m0, m1, m2, m3};
+  u1_dense<R, RB, B, COND>(a, m, rmask, rval);
+}
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_anti_v(cplx<R>* a, cplx<R> m1, cplx<R> m2, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m[4] = {mk<R>(R(0), R(0)), m1, m2, mk<R>(R(0), R(0))};
+  u1_anti<R, RB, B, COND>(a, m, rmask, rval);
+}
+
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_kind(int kind, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  if (kind == OP_U1R) u1_real<R, RB, B, COND>(a, m, rmask, rval);
+  else if (kind == OP_U1) u1_dense<R, RB, B, COND>(a, m, rmask, rval);
+  else u1_anti<R, RB, B, COND>(a, m, rmask, rval);
+}
+
+template <typename R, int RB, bool COND>
+SVB_HD void dispatch_u1_c(int kind, int b, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  switch (b) {
+    case 0: u1_kind<R, RB, 0, COND>(kind, a, m, rmask, rval); break;
+    case 1: u1_kind<R, RB, 1, COND>(kind, a, m, rmask, rval); break;
+    case 2: u1_kind<R, RB, 2, COND>(kind, a, m, rmask, rval); break;
+    case 3: u1_kind<R, RB, 3, COND>(kind, a, m, rmask, rval); break;
+    default:
+      if constexpr (RB > 4) u1_kind<R, RB, (RB > 4 ? 4 : 0), COND>(kind, a, m, rmask, rval);
+      break;
+  }
+}
+
+template <typename R, int RB>
+SVB_HD void dispatch_u1(int kind, int b, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  if (rmask == 0) dispatch_u1_c<R, RB, false>(kind, b, a, m, 0, 0);
+  else dispatch_u1_c<R, RB, true>(kind, b, a, m, rmask, rval);
+}
+
+template <typename R, int RB, int B1, int B2>
+SVB_HD void u2_any(int kind, cplx<R>* a, const uint8_t* payload, uint32_t rmask, uint32_t rval) {
+  if constexpr (B1 == B2 || B1 >= RB || B2 >= RB) {
+    return;
+  } else {
+    if (kind == OP_U2)
+      u2_dense<R, RB, B1, B2>(a, reinterpret_cast<const cplx<R>*>(payload), rmask, rval);
+    else
+      u2_perm<R, RB, B1, B2>(a, reinterpret_cast<const int32_t*>(payload),
+                             reinterpret_cast<const cplx<R>*>(payload + 16), rmask, rval);
+  }
+}
+
+template <typename R, int RB, int B1>
+SVB_HD void dispatch_u2_b2(int kind, int b2, cplx<R>* a, const uint8_t* p, uint32_t rm, uint32_t rv) {
+  switch (b2) {
+    case 0: u2_any<R, RB, B1, 0>(kind, a, p, rm, rv); break;
+    case 1: u2_any<R, RB, B1, 1>(kind, a, p, rm, rv); break;
+    case 2: u2_any<R, RB, B1, 2>(kind, a, p, rm, rv); break;
+    case 3: u2_any<R, RB, B1, 3>(kind, a, p, rm, rv); break;
+    case 4: u2_any<R, RB, B1, 4>(kind, a, p, rm, rv); break;
+    default: break;
+  }
+}
+
+template <typename R, int RB>
+SVB_HD void dispatch_u2(int kind, int b1, int b2, cplx<R>* a, const uint8_t* p, uint32_t rm, uint32_t rv) {
+  switch (b1) {
+    case 0: dispatch_u2_b2<R, RB, 0>(kind, b2, a, p, rm, rv); break;
+    case 1: dispatch_u2_b2<R, RB, 1>(kind, b2, a, p, rm, rv); break;
+    case 2: dispatch_u2_b2<R, RB, 2>(kind, b2, a, p, rm, rv); break;
+    case 3: dispatch_u2_b2<R, RB, 3>(kind, b2, a, p, rm, rv); break;
+    case 4: dispatch_u2_b2<R, RB, 4>(kind, b2, a, p, rm, rv); break;
+    default: break;
+  }
+}
+
+// Run the ops in [off, end) of the op stream on one thread's registers.
+template <typename R, int RB>
+SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, uint32_t end, const cplx<R>* uni) {
+  while (off < end) {
+    const OpHdr* h = reinterpret_cast<const OpHdr*>(ops + off);
+    const int4 w0 = ldop(reinterpret_cast<const int4*>(h));          // kind, a, b, n
+    const ulonglong2 w1 = ldop(reinterpret_cast<const ulonglong2*>(h) + 1);  // fmask, fval
+    const uint4 w2 = ldop(reinterpret_cast<const uint4*>(h) + 2);     // rmask, rval, bytes
+    const uint8_t* payload = ops + off + sizeof(OpHdr);
+    off += w2.z;
+    if ((Fg & w1.x) != w1.y) continue;
+    switch (w0.x) {
+      case OP_DIAG:
+        diag_apply<R, RB>(a, Fg, payload, uni);
+        break;
+      case OP_U1:
+      case OP_U1R:
+      case OP_U1ANTI:
+        dispatch_u1<R, RB>(w0.x, w0.y, a, reinterpret_cast<const cplx<R>*>(payload), w2.x, w2.y);
+        break;
+      default:
+        dispatch_u2<R, RB>(w0.x, w0.y, w0.z, a, payload, w2.x, w2.y);
+        break;
+    }
+  }
+}
+
+// Shared-memory slot of local index j (XOR swizzle of the bank group).
+template <typename R> SVB_HD uint32_t swz(uint32_t j);
+template <> SVB_HD uint32_t swz<double>(uint32_t j) {
+  return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7u);
+}
+// complex64: bit 0 is left alone so an aligned pair (j, j^1) stays one 16-byte
+// unit (cp.async copies c64 amplitudes in pairs)
+template <> SVB_HD uint32_t swz<float>(uint32_t j) {
+  return j ^ ((((j >> 4) ^ (j >> 7) ^ (j >> 10)) & 7u) << 1);
+}
+
+// Thread layout of round `rd`: fixed local index and fixed global index.
+SVB_HD void thread_fixed(const PassDev& pd, const RoundDev& rd, uint32_t tid, uint64_t base,
+                         uint32_t* Fl, uint64_t* Fg) {
+  uint32_t fl = 0;
+  uint64_t fg = base;
+  int tb = 0;
+  for (int l = 0; l < pd.m; ++l) {
+    if (rd.regmask_local & (1u << l)) continue;
+    if ((tid >> tb) & 1u) {
+      fl |= 1u << l;
+      fg |= 1ull << pd.pos[l];
+    }
+    ++tb;
+  }
+  *Fl = fl;
+  *Fg = fg;
+}
+
+SVB_HD uint64_t tile_base(const PassDev& pd, uint64_t t) {
+  uint64_t b = 0;
+  for (int i = 0; i < pd.nout; ++i)
+    if ((t >> i) & 1ull) b |= 1ull << pd.outpos[i];
+  return b;
+}
+
+// ------------------------------------------------ TMA bulk / mbarrier PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+constexpr int kStages = 2;
+
+template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
+
+// Tile base (bits outside S) computed warp-parallel: lane l owns tile bit l.
+__device__ __forceinline__ uint64_t tile_base_warp(const PassDev& pd, uint64_t t, uint32_t lane) {
+  uint64_t v = 0;
+  if ((int)lane < pd.nout && ((t >> lane) & 1ull)) v = 1ull << pd.outpos[lane];
+  if ((int)lane + 32 < pd.nout && ((t >> (lane + 32)) & 1ull)) v |= 1ull << pd.outpos[lane + 32];
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
+
+template <typename R> __device__ __forceinline__ cplx<R> shfl_xor_c(cplx<R> x, int o) {
+  x.x = __shfl_xor_sync(0xffffffffu, x.x, o);
+  x.y = __shfl_xor_sync(0xffffffffu, x.y, o);
+  return x;
+}
+
+// Tile-uniform factors of one DIAG payload, lanes in parallel over the terms.
+template <typename R, int RB>
+__device__ void diag_uniform_warp(const uint8_t* payload, uint64_t base, cplx<R>* slot, uint32_t lane) {
+  const int4 h0 = reinterpret_cast<const int4*>(payload)[0];
+  const int4 h1 = reinterpret_cast<const int4*>(payload)[1];
+  const int nur[6] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y};
+  const int nuc = h1.z;
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+  const cplx<R> one = mk<R>(R(1), R(0));
+  for (int i = 0; i < RB; ++i) {
+    const int n = nur[i];
+    cplx<R> u0 = one, u1 = one;
+    if (n > 0) {
+      for (int k = (int)lane; k < n; k += 32) {
+        const int qb = t[k].qb;
+        const int f = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
+        u0 = cmul<R>(u0, t[k].d[2 * f]);
+        u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        u0 = cmul<R>(u0, shfl_xor_c<R>(u0, o));
+        u1 = cmul<R>(u1, shfl_xor_c<R>(u1, o));
+      }
+    }
+    if (lane == 0) {
+      slot[1 + i] = u0;
+      slot[1 + 5 + i] = u1;
+    }
+    t += n;
+  }
+  cplx<R> c = one;
+  if (nuc > 0) {
+    for (int k = (int)lane; k < nuc; k += 32) {
+      const int qa = t[k].qa, qb = t[k].qb;
+      const int fa = qa >= 0 ? (int)((base >> qa) & 1ull) : 0, fb = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
+      c = cmul<R>(c, t[k].d[fa + 2 * fb]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c = cmul<R>(c, shfl_xor_c<R>(c, o));
+  }
+  if (lane == 0) slot[0] = c;
+}
+
+// ------------------------------------------------------- pass skeleton
+// Per-CTA context of a fused pass, shared by the interpreter body and the
+// JIT-generated bodies.
+template <typename R, int RB> struct PassCtx {
+  static constexpr int kHoist = 4;  // rounds whose thread constants live in registers
+  const PassDev& pd;
+  cplx<R>* state;
+  const uint8_t* ops;  // op stream rebased onto shared memory
+  const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
+  uint32_t tid;
+  uint32_t sFl_r[kHoist];
+  uint64_t Fg_r[kHoist];
+  __device__ PassCtx(const PassDev& p) : pd(p) {}
+};
+
+// Thread constants of round k for the tile at `base`: swizzled local slot base
+// and the fixed global index.
+template <typename R, int RB>
+__device__ __forceinline__ void round_fixed(const PassCtx<R, RB>& c, int k, uint64_t base, uint32_t& sFl,
+                                            uint64_t& Fg) {
+  if (k < PassCtx<R, RB>::kHoist) {
+#pragma unroll
+    for (int q = 0; q < PassCtx<R, RB>::kHoist; ++q)
+      if (q == k) {
+        sFl = c.sFl_r[q];
+        Fg = c.Fg_r[q] | base;
+      }
+  } else {
+    uint32_t Fl;
+    thread_fixed(c.pd, c.pd.rounds[k], c.tid, base, &Fl, &Fg);
+    sFl = swz<R>(Fl);
+  }
+}
+
+// Shared-memory slots of the thread's 2^RB amplitudes in round layout `rd`:
+// the swizzle is GF(2)-linear, so slot(v) = swz(Fl) ^ XOR_i v_i swz(1 << reg_local[i]).
+template <typename R, int RB>
+__device__ __forceinline__ void layout_slots(uint32_t sFl, const RoundDev& rd, uint32_t* slot) {
+  uint32_t sl[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) sl[i] = swz<R>(1u << rd.reg_local[i]);
+  slot[0] = sFl;
+#pragma unroll
+  for (int i = 0; i < RB; ++i)
+#pragma unroll
+    for (int v = 0; v < (1 << i); ++v) slot[v | (1 << i)] = slot[v] ^ sl[i];
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void load_slots(cplx<R>* a, const cplx<R>* cur, const uint32_t* slot) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) a[v] = cur[slot[v]];
+}
+template <typename R, int RB>
+__device__ __forceinline__ void store_slots(const cplx<R>* a, cplx<R>* cur, const uint32_t* slot) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) cur[slot[v]] = a[v];
+}
+
+// Last round: straight from registers to HBM (lanes <-> qubits 0..4).
+template <typename R, int RB>
+__device__ __forceinline__ void store_global(cplx<R>* state, uint64_t Fg, const PassDev& pd, const RoundDev& rd,
+                                             const cplx<R>* a) {
+  cplx<R>* g0 = state + Fg;
+  size_t goff[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) goff[i] = (size_t)1 << pd.pos[rd.reg_local[i]];
+  size_t gv[1 << RB];
+  gv[0] = 0;
+#pragma unroll
+  for (int i = 0; i < RB; ++i)
+#pragma unroll
+    for (int v = 0; v < (1 << i); ++v) gv[v | (1 << i)] = gv[v] | goff[i];
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) __stcs(g0 + gv[v], a[v]);
+}
+
+// Helpers for JIT-generated diagonal code.
+template <typename R> __device__ __forceinline__ cplx<R> csel(int f, cplx<R> x0, cplx<R> x1) { return f ? x1 : x0; }
+template <typename R> __device__ __forceinline__ cplx<R> conj_mul(cplx<R> x, cplx<R> u) {
+  return cmul<R>(x, mk<R>(u.x, -u.y));
+}
+template <typename R, int RB, int I>
+__device__ __forceinline__ void mul_half(cplx<R>* a, cplx<R> d) {  // a[v] *= d for v with bit I set
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v)
+    if (v & (1 << I)) a[v] = cmul<R>(a[v], d);
+}
+template <typename R, int RB>
+__device__ __forceinline__ void mul_all(cplx<R>* a, cplx<R> d) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) a[v] = cmul<R>(a[v], d);
+}
+template <typename R, int RB, int IA, int IB>
+__device__ __forceinline__ void mul_rr(cplx<R>* a, cplx<R> e0, cplx<R> e1, cplx<R> e2, cplx<R> e3) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    const int k = ((v >> IA) & 1) + 2 * ((v >> IB) & 1);
+    a[v] = cmul<R>(a[v], k == 0 ? e0 : k == 1 ? e1 : k == 2 ? e2 : e3);
+  }
+}
+
+// Interpreter body: rounds and ops read from the pass descriptor / op stream.
+struct InterpBody {
+  template <typename R, int RB>
+  __device__ static __forceinline__ void tile(int, const PassCtx<R, RB>& c, cplx<R>* a, cplx<R>* cur,
+                                              uint64_t base) {
+    const int nrounds = c.pd.nrounds;
+    for (int k = 0; k < nrounds; ++k) {
+      const RoundDev& rd = c.pd.rounds[k];
+      uint32_t sFl;
+      uint64_t Fg;
+      round_fixed<R, RB>(c, k, base, sFl, Fg);
+      uint32_t slot[1 << RB];
+      layout_slots<R, RB>(sFl, rd, slot);
+      load_slots<R, RB>(a, cur, slot);
+      run_ops<R, RB>(a, Fg, c.ops, rd.op_off, rd.op_end, c.uni);
+      if (k + 1 < nrounds) {
+        // each slot of a layout is read and rewritten by its owner only, so one
+        // barrier (after the writes) separates consecutive layouts
+        store_slots<R, RB>(a, cur, slot);
+        __syncthreads();
+      } else {
+        store_global<R, RB>(c.state, Fg, c.pd, rd, a);
+      }
+    }
+  }
+};
+
+// Persistent fused pass: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...
+// Tiles stream HBM -> shared memory with cp.async (LDGSTS, 16 B per thread,
+// lanes on consecutive amplitudes: 512 B per warp request) kStages-1 tiles
+// ahead into an XOR-swizzled ring; warps first evaluate the tile-uniform
+// factors of the pass's diagonal ops, then Body runs the tile's rounds out of
+// shared memory and stores the last layout straight from registers to HBM.
+template <typename R, int RB, class Body>
+__device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg,
+                                            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ PassDev pd;
+  __shared__ cplx<R> uni[kMaxDiag * kUniStride];
+  __shared__ uint64_t s_ldk[32];
+  __shared__ uint32_t s_sdk[32];
+  {
+    const int4* src = reinterpret_cast<const int4*>(pdg);
+    int4* dst = reinterpret_cast<int4*>(&pd);
+    for (int i = threadIdx.x; i < (int)(sizeof(PassDev) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  // stage this pass's op stream after the tile ring; `ops` is rebased so that
+  // stream offsets index shared memory
+  const uint32_t ring_bytes = (uint32_t)kStages * ((uint32_t)sizeof(cplx<R>) << pd.m);
+  {
+    const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
+    int4* dst = reinterpret_cast<int4*>(smraw + ring_bytes);
+    for (uint32_t i = threadIdx.x; i < pd.ops_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  PassCtx<R, RB> c(pd);
+  c.state = state;
+  c.ops = smraw + ring_bytes - pd.ops_begin;
+  c.uni = uni;
+  const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
+  c.tid = tid;
+  const uint32_t nwarps = nthr >> 5;
+  const int m = pd.m, nrounds = pd.nrounds, ndiag = pd.ndiag;
+  const uint32_t T = 1u << m;
+  cplx<R>* ring = reinterpret_cast<cplx<R>*>(smraw);
+  // loads: element j = (tid + k*nthr)*kPer; 16 B per copy (one c128 amplitude
+  // or an aligned c64 pair); global and smem offsets split into a tid part and
+  // a tile-independent k part (tables in shared memory)
+  constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
+  const int lo_bits = (31 - __clz(nthr)) + (kPer == 2 ? 1 : 0);
+  uint64_t ld_tid = 0;
+  for (int l = 0; l < lo_bits; ++l)
+    if (((tid * kPer) >> l) & 1u) ld_tid |= 1ull << pd.pos[l];
+  const uint32_t sd_tid = swz<R>(tid * kPer);
+  const uint32_t nld = T / (nthr * kPer);
+  if (tid < nld) {
+    uint64_t g = 0;
+    const uint32_t j = tid * nthr * kPer;
+    for (int l = lo_bits; l < m; ++l)
+      if ((j >> l) & 1u) g |= 1ull << pd.pos[l];
+    s_ldk[tid] = g;
+    s_sdk[tid] = swz<R>(j);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < PassCtx<R, RB>::kHoist; ++k) {
+    if (k < nrounds) {
+      uint32_t Fl;
+      thread_fixed(pd, pd.rounds[k], tid, 0, &Fl, &c.Fg_r[k]);
+      c.sFl_r[k] = swz<R>(Fl);
+    }
+  }
+  auto issue = [&](uint64_t base, int b) {
+    cplx<R>* dst = ring + (size_t)b * T;
+    const cplx<R>* src = state + (base | ld_tid);
+    // swizzle is linear over XOR: slot(tid part ^ k part) = swz(tid part) ^ swz(k part)
+    for (uint32_t k = 0; k < nld; ++k) cp_async16(dst + (sd_tid ^ s_sdk[k]), src + s_ldk[k]);
+  };
+  const uint32_t t0 = blockIdx.x;
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    const uint32_t ts = t0 + (uint32_t)s * gridDim.x;
+    if (ts < ntiles) issue(tile_base_warp(pd, ts, lane), s);
+    cp_async_commit();
+  }
+  cplx<R> a[1 << RB];
+  int it = 0;
+  for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
+    const uint32_t tn = t + (uint32_t)(kStages - 1) * gridDim.x;
+    if (tn < ntiles) issue(tile_base_warp(pd, tn, lane), (it + kStages - 1) % kStages);
+    cp_async_commit();
+    const uint64_t base = tile_base_warp(pd, t, lane);
+    if (ndiag > 0) {  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
+      for (int d = (int)warp; d < ndiag; d += (int)nwarps)
+        diag_uniform_warp<R, RB>(c.ops + pd.diag_off[d], base, uni + d * kUniStride, lane);
+    }
+    cp_async_wait<kStages - 1>();
+    __syncthreads();
+    Body::template tile<R, RB>(pass, c, a, ring + (size_t)(it % kStages) * T, base);
+    __syncthreads();  // ring slot and uniform factors are rewritten next tile
+  }
+  cp_async_wait<0>();
+}
+
+template <typename R, int RB>
+__global__ void __launch_bounds__(256, 1)
+    k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
+           uint32_t ntiles) {
+  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles);
+}
+
+}  // namespace svb

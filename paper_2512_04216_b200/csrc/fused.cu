@@ -19,258 +19,11 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "jit.h"
 #include "kernels.h"
 #include "program.h"
 
 namespace svb {
-
-// ------------------------------------------------ TMA bulk / mbarrier PTX
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-constexpr int kStages = 2;
-
-template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
-
-// Tile base (bits outside S) computed warp-parallel: lane l owns tile bit l.
-__device__ __forceinline__ uint64_t tile_base_warp(const PassDev& pd, uint64_t t, uint32_t lane) {
-  uint64_t v = 0;
-  if ((int)lane < pd.nout && ((t >> lane) & 1ull)) v = 1ull << pd.outpos[lane];
-  if ((int)lane + 32 < pd.nout && ((t >> (lane + 32)) & 1ull)) v |= 1ull << pd.outpos[lane + 32];
-  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
-  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
-  return ((uint64_t)hi << 32) | lo;
-}
-
-template <typename R> __device__ __forceinline__ cplx<R> shfl_xor_c(cplx<R> x, int o) {
-  x.x = __shfl_xor_sync(0xffffffffu, x.x, o);
-  x.y = __shfl_xor_sync(0xffffffffu, x.y, o);
-  return x;
-}
-
-// Tile-uniform factors of one DIAG payload, lanes in parallel over the terms.
-template <typename R, int RB>
-__device__ void diag_uniform_warp(const uint8_t* payload, uint64_t base, cplx<R>* slot, uint32_t lane) {
-  const int4 h0 = reinterpret_cast<const int4*>(payload)[0];
-  const int4 h1 = reinterpret_cast<const int4*>(payload)[1];
-  const int nur[6] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y};
-  const int nuc = h1.z;
-  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
-  const cplx<R> one = mk<R>(R(1), R(0));
-  for (int i = 0; i < RB; ++i) {
-    const int n = nur[i];
-    cplx<R> u0 = one, u1 = one;
-    if (n > 0) {
-      for (int k = (int)lane; k < n; k += 32) {
-        const int qb = t[k].qb;
-        const int f = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
-        u0 = cmul<R>(u0, t[k].d[2 * f]);
-        u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        u0 = cmul<R>(u0, shfl_xor_c<R>(u0, o));
-        u1 = cmul<R>(u1, shfl_xor_c<R>(u1, o));
-      }
-    }
-    if (lane == 0) {
-      slot[1 + i] = u0;
-      slot[1 + 5 + i] = u1;
-    }
-    t += n;
-  }
-  cplx<R> c = one;
-  if (nuc > 0) {
-    for (int k = (int)lane; k < nuc; k += 32) {
-      const int qa = t[k].qa, qb = t[k].qb;
-      const int fa = qa >= 0 ? (int)((base >> qa) & 1ull) : 0, fb = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
-      c = cmul<R>(c, t[k].d[fa + 2 * fb]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c = cmul<R>(c, shfl_xor_c<R>(c, o));
-  }
-  if (lane == 0) slot[0] = c;
-}
-
-// Persistent fused pass: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...
-// Tiles stream HBM -> shared memory with cp.async (LDGSTS, 16 B per thread,
-// lanes on consecutive amplitudes: 512 B per warp request) kStages-1 tiles
-// ahead into an XOR-swizzled ring; warps first evaluate the tile-uniform
-// factors of the pass's diagonal ops, then run the tile's rounds out of shared
-// memory; the last round stores straight from registers to HBM (lanes <->
-// qubits 0..4).  The swizzle is GF(2)-linear, so every shared-memory slot is
-// an XOR of a per-thread base and per-register-bit offsets.
-template <typename R, int RB>
-__global__ void __launch_bounds__(256, 1)
-    k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
-           uint32_t ntiles) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ PassDev pd;
-  __shared__ cplx<R> uni[kMaxDiag * kUniStride];
-  __shared__ uint64_t s_ldk[32];
-  __shared__ uint32_t s_sdk[32];
-  {
-    const int4* src = reinterpret_cast<const int4*>(pdg);
-    int4* dst = reinterpret_cast<int4*>(&pd);
-    for (int i = threadIdx.x; i < (int)(sizeof(PassDev) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  __syncthreads();
-  // stage this pass's op stream after the tile ring; `ops` is rebased so that
-  // stream offsets index shared memory
-  const uint32_t ring_bytes = (uint32_t)kStages * ((uint32_t)sizeof(cplx<R>) << pd.m);
-  {
-    const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
-    int4* dst = reinterpret_cast<int4*>(smraw + ring_bytes);
-    for (uint32_t i = threadIdx.x; i < pd.ops_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  const uint8_t* ops = smraw + ring_bytes - pd.ops_begin;
-  __syncthreads();
-  constexpr int V = 1 << RB;
-  constexpr int kHoist = 4;  // rounds whose thread constants live in registers
-  const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t nwarps = nthr >> 5;
-  const int m = pd.m, nrounds = pd.nrounds, ndiag = pd.ndiag;
-  const uint32_t T = 1u << m;
-  cplx<R>* ring = reinterpret_cast<cplx<R>*>(smraw);
-  // loads: element j = (tid + k*nthr)*kPer; 16 B per copy (one c128 amplitude
-  // or an aligned c64 pair); global and smem offsets split into a tid part and
-  // a tile-independent k part (tables in shared memory)
-  constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
-  const int lo_bits = (31 - __clz(nthr)) + (kPer == 2 ? 1 : 0);
-  uint64_t ld_tid = 0;
-  for (int l = 0; l < lo_bits; ++l)
-    if (((tid * kPer) >> l) & 1u) ld_tid |= 1ull << pd.pos[l];
-  const uint32_t sd_tid = swz<R>(tid * kPer);
-  const uint32_t nld = T / (nthr * kPer);
-  if (tid < nld) {
-    uint64_t g = 0;
-    const uint32_t j = tid * nthr * kPer;
-    for (int l = lo_bits; l < m; ++l)
-      if ((j >> l) & 1u) g |= 1ull << pd.pos[l];
-    s_ldk[tid] = g;
-    s_sdk[tid] = swz<R>(j);
-  }
-  __syncthreads();
-  uint32_t sFl_r[kHoist];
-  uint64_t Fg_r[kHoist];
-#pragma unroll
-  for (int k = 0; k < kHoist; ++k) {
-    if (k < nrounds) {
-      uint32_t Fl;
-      thread_fixed(pd, pd.rounds[k], tid, 0, &Fl, &Fg_r[k]);
-      sFl_r[k] = swz<R>(Fl);
-    }
-  }
-  auto issue = [&](uint64_t base, int b) {
-    cplx<R>* dst = ring + (size_t)b * T;
-    const cplx<R>* src = state + (base | ld_tid);
-    // swizzle is linear over XOR: slot(tid part ^ k part) = swz(tid part) ^ swz(k part)
-    for (uint32_t k = 0; k < nld; ++k) cp_async16(dst + (sd_tid ^ s_sdk[k]), src + s_ldk[k]);
-  };
-  const uint32_t t0 = blockIdx.x;
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    const uint32_t ts = t0 + (uint32_t)s * gridDim.x;
-    if (ts < ntiles) issue(tile_base_warp(pd, ts, lane), s);
-    cp_async_commit();
-  }
-  cplx<R> a[V];
-  int it = 0;
-  for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
-    const uint32_t tn = t + (uint32_t)(kStages - 1) * gridDim.x;
-    if (tn < ntiles) issue(tile_base_warp(pd, tn, lane), (it + kStages - 1) % kStages);
-    cp_async_commit();
-    const uint64_t base = tile_base_warp(pd, t, lane);
-    if (ndiag > 0) {  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
-      for (int d = (int)warp; d < ndiag; d += (int)nwarps)
-        diag_uniform_warp<R, RB>(ops + pd.diag_off[d], base, uni + d * kUniStride, lane);
-    }
-    cp_async_wait<kStages - 1>();
-    __syncthreads();
-    cplx<R>* cur = ring + (size_t)(it % kStages) * T;
-    for (int k = 0; k < nrounds; ++k) {
-      const RoundDev& rd = pd.rounds[k];
-      uint32_t sFl;
-      uint64_t Fg;
-      if (k < kHoist) {
-#pragma unroll
-        for (int q = 0; q < kHoist; ++q)
-          if (q == k) { sFl = sFl_r[q]; Fg = Fg_r[q] | base; }
-      } else {
-        uint32_t Fl;
-        thread_fixed(pd, rd, tid, base, &Fl, &Fg);
-        sFl = swz<R>(Fl);
-      }
-      uint32_t sl[RB];
-#pragma unroll
-      for (int i = 0; i < RB; ++i) sl[i] = swz<R>(1u << rd.reg_local[i]);
-      uint32_t slot[V];
-      slot[0] = sFl;
-#pragma unroll
-      for (int i = 0; i < RB; ++i)
-#pragma unroll
-        for (int v = 0; v < (1 << i); ++v) slot[v | (1 << i)] = slot[v] ^ sl[i];
-#pragma unroll
-      for (int v = 0; v < V; ++v) a[v] = cur[slot[v]];
-      run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end, uni);
-      if (k + 1 < nrounds) {
-        // each slot of a layout is read and rewritten by its owner only, so one
-        // barrier (after the writes) separates consecutive layouts
-#pragma unroll
-        for (int v = 0; v < V; ++v) cur[slot[v]] = a[v];
-        __syncthreads();
-      } else {
-        cplx<R>* g0 = state + Fg;
-        size_t goff[RB];
-#pragma unroll
-        for (int i = 0; i < RB; ++i) goff[i] = (size_t)1 << pd.pos[rd.reg_local[i]];
-        size_t gv[V];
-        gv[0] = 0;
-#pragma unroll
-        for (int i = 0; i < RB; ++i)
-#pragma unroll
-          for (int v = 0; v < (1 << i); ++v) gv[v | (1 << i)] = gv[v] | goff[i];
-#pragma unroll
-        for (int v = 0; v < V; ++v) __stcs(g0 + gv[v], a[v]);
-      }
-    }
-    __syncthreads();  // ring slot and uniform factors are rewritten next tile
-  }
-  cp_async_wait<0>();
-}
 
 // ---------------------------------------------------------------- permute
 struct PermDev {
@@ -368,7 +121,8 @@ void Profiler::collect() {
 template <typename R> static constexpr int rb_of() { return sizeof(R) == 8 ? 4 : 5; }
 
 template <typename R>
-static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats) {
+static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats,
+                          bool use_jit) {
   constexpr int RB = rb_of<R>();
   if (prog.passes.empty()) return;
   size_t pbytes = prog.passes.size() * sizeof(PassDev);
@@ -387,6 +141,10 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (use_jit && jit_launch_passes<R>(state, prog, dpass, dops, st, stats, nsm)) {
+    SVB_CUDA(cudaFreeAsync(dbuf, st));
+    return;
+  }
   for (size_t p = 0; p < prog.passes.size(); ++p) {
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
@@ -440,7 +198,7 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
   SchedOptions o = opt;
   o.relabel_swaps = false;  // the handle owns its buffer; permutation passes need run_program_owned
   Program prog = build_program<R>(n, g, ng, o);
-  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats);
+  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false);
 }
 
 static bool trace_on() {
@@ -459,8 +217,8 @@ struct TraceTimer {
 };
 
 template <typename R>
-void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, cudaStream_t st,
-                       ProgramStats* stats) {
+void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, int jit_min_n,
+                       cudaStream_t st, ProgramStats* stats) {
   TraceTimer tt;
   stats->gates += ng;
   SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
@@ -485,7 +243,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     }
   }
   const double t_build = tt.lap();
-  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats);
+  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats, jit_min_n >= 0 && n >= jit_min_n);
   const double t_launch = tt.lap();
   if (!prog.final_perm.empty()) {
     cplx<R>* s = static_cast<cplx<R>*>(*state);
@@ -502,8 +260,10 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
 
 template void run_program<float>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
 template void run_program<double>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
-template void run_program_owned<float>(void**, void**, int, const svb_gate*, int, int, cudaStream_t, ProgramStats*);
-template void run_program_owned<double>(void**, void**, int, const svb_gate*, int, int, cudaStream_t, ProgramStats*);
+template void run_program_owned<float>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
+                                       ProgramStats*);
+template void run_program_owned<double>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
+                                        ProgramStats*);
 
 }  // namespace svb
 

@@ -1,0 +1,491 @@
+// JIT specialisation of fused gate programs (NVRTC -> sm_100a cubin).
+//
+// The interpreter kernel (InterpBody) decodes ops at run time; that costs a
+// header decode per op and, worse, forces the compiler to shuffle the whole
+// register-resident amplitude array at every dispatch merge.  Here every pass
+// of a scheduled program becomes a kernel whose Body is straight-line code:
+// round layouts unrolled, register-bit positions as template arguments,
+// matrix coefficients as hexfloat immediates, conditions folded.  The skeleton
+// (streaming ring, uniform diagonal factors, stores) is the same
+// pass_kernel<> the interpreter uses: device_core.cuh is embedded in the
+// library and handed to NVRTC as an in-memory header.
+//
+// NVRTC is dlopen'ed and the driver API is reached through
+// cudaGetDriverEntryPoint, so the library loads (and runs the interpreter) on
+// machines without either.  Modules are cached per process by source hash.
+#include <cuda.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "jit.h"
+#include "program.h"
+
+extern const char svb_device_core_src[];
+
+namespace svb {
+
+namespace {
+
+// ---------------------------------------------------------------- NVRTC
+typedef int nvrtcResult_t;
+struct Nvrtc {
+  void* h = nullptr;
+  nvrtcResult_t (*create)(void**, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  nvrtcResult_t (*compile)(void*, int, const char* const*) = nullptr;
+  nvrtcResult_t (*log_size)(void*, size_t*) = nullptr;
+  nvrtcResult_t (*log)(void*, char*) = nullptr;
+  nvrtcResult_t (*cubin_size)(void*, size_t*) = nullptr;
+  nvrtcResult_t (*cubin)(void*, char*) = nullptr;
+  nvrtcResult_t (*destroy)(void**) = nullptr;
+  bool ok = false;
+  Nvrtc() {
+    const char* names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_LOCAL))) break;
+    if (!h) return;
+    create = (decltype(create))dlsym(h, "nvrtcCreateProgram");
+    compile = (decltype(compile))dlsym(h, "nvrtcCompileProgram");
+    log_size = (decltype(log_size))dlsym(h, "nvrtcGetProgramLogSize");
+    log = (decltype(log))dlsym(h, "nvrtcGetProgramLog");
+    cubin_size = (decltype(cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+    cubin = (decltype(cubin))dlsym(h, "nvrtcGetCUBIN");
+    destroy = (decltype(destroy))dlsym(h, "nvrtcDestroyProgram");
+    ok = create && compile && log_size && log && cubin_size && cubin && destroy;
+  }
+};
+
+// ---------------------------------------------------------- driver API
+struct Driver {
+  CUresult (*load)(CUmodule*, const void*) = nullptr;
+  CUresult (*getfn)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*setattr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                     void**, void**) = nullptr;
+  bool ok = false;
+  Driver() {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    ok = get("cuModuleLoadData", (void**)&load) && get("cuModuleGetFunction", (void**)&getfn) &&
+         get("cuFuncSetAttribute", (void**)&setattr) && get("cuLaunchKernel", (void**)&launch);
+    if (!ok) cudaGetLastError();
+  }
+};
+
+struct Module {
+  CUmodule mod = nullptr;
+  std::vector<CUfunction> fns;
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, Module> g_cache;  // key: device + source
+
+std::string hexf(double x, bool single) {
+  char buf[64];
+  if (single) std::snprintf(buf, sizeof buf, "%af", (double)(float)x);
+  else std::snprintf(buf, sizeof buf, "%a", x);
+  std::string s(buf);
+  if (s == "inf" || s == "-inf" || s == "nan" || s == "-nan" || s == "inff" || s == "-inff") return "0";
+  return s;
+}
+
+template <typename R> std::string cimm(const cplx<R>& z) {
+  const bool single = sizeof(R) == 4;
+  return "svb::mk<R>(" + hexf((double)z.x, single) + ", " + hexf((double)z.y, single) + ")";
+}
+
+template <typename C> bool is1(const C& z) { return z.x == 1 && z.y == 0; }
+
+// Straight-line code of one DIAG payload (see DiagHdr): tile-uniform factors
+// come from the pass's uniform slot, thread-dependent factors are evaluated
+// with immediates, and factors that are exactly 1 by construction are dropped
+// at generation time (controlled phases leave half the amplitudes untouched).
+template <typename R>
+void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
+  DiagHdr h;
+  std::memcpy(&h, payload, sizeof h);
+  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+  bool d0one[8], d1one[8], cone = true;
+  for (int i = 0; i < RB; ++i) d0one[i] = d1one[i] = true;
+  const DiagTerm<R>* u = t;
+  for (int i = 0; i < RB; ++i)
+    for (int k = 0; k < h.nUR[i]; ++k, ++u) {
+      if (!is1(u->d[0]) || !is1(u->d[2])) d0one[i] = false;
+      if (!is1(u->d[1]) || !is1(u->d[3])) d1one[i] = false;
+    }
+  for (int k = 0; k < h.nUC; ++k, ++u)
+    for (int e = 0; e < 4; ++e) cone = cone && is1(u->d[e]);
+  const DiagTerm<R>* tr = u;
+  const DiagTerm<R>* tc = tr + h.nTR;
+  const DiagTerm<R>* rr = tc + h.nTC;
+  for (int k = 0; k < h.nTR; ++k) {
+    const int i = tr[k].ra;
+    if (!is1(tr[k].d[0]) || !is1(tr[k].d[2])) d0one[i] = false;
+    if (!is1(tr[k].d[1]) || !is1(tr[k].d[3])) d1one[i] = false;
+  }
+  for (int k = 0; k < h.nTC; ++k)
+    for (int e = 0; e < 4; ++e) cone = cone && is1(tc[k].d[e]);
+  o << "    {\n";
+  const std::string us = "c.uni + " + std::to_string(h.slot * kUniStride);
+  const bool has_uc = h.slot >= 0 && h.nUC > 0;
+  if (!cone) o << "      svb::cplx<R> C = " << (has_uc ? "(" + us + ")[0]" : "svb::mk<R>(R(1), R(0))") << ";\n";
+  for (int i = 0; i < RB; ++i) {
+    const bool has_ur = h.slot >= 0 && h.nUR[i] > 0;
+    if (!d0one[i])
+      o << "      svb::cplx<R> D0_" << i << " = "
+        << (has_ur ? "(" + us + ")[" + std::to_string(1 + i) + "]" : "svb::mk<R>(R(1), R(0))") << ";\n";
+    if (!d1one[i])
+      o << "      svb::cplx<R> D1_" << i << " = "
+        << (has_ur ? "(" + us + ")[" + std::to_string(6 + i) + "]" : "svb::mk<R>(R(1), R(0))") << ";\n";
+  }
+  for (int k = 0; k < h.nTR; ++k) {
+    const int i = tr[k].ra, qb = tr[k].qb;
+    o << "      { const int f = (int)((Fg >> " << qb << ") & 1ull);";
+    if (!d0one[i]) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[0]) << ", " << cimm<R>(tr[k].d[2]) << "));";
+    if (!d1one[i]) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[1]) << ", " << cimm<R>(tr[k].d[3]) << "));";
+    o << " }\n";
+  }
+  for (int k = 0; k < h.nTC; ++k) {
+    const int qa = tc[k].qa, qb = tc[k].qb;
+    const std::string fa = qa >= 0 ? "(int)((Fg >> " + std::to_string(qa) + ") & 1ull)" : "0";
+    const std::string fb = qb >= 0 ? "(int)((Fg >> " + std::to_string(qb) + ") & 1ull)" : "0";
+    o << "      { const int fa = " << fa << ", fb = " << fb << "; C = svb::cmul<R>(C, fb ? svb::csel<R>(fa, "
+      << cimm<R>(tc[k].d[2]) << ", " << cimm<R>(tc[k].d[3]) << ") : svb::csel<R>(fa, " << cimm<R>(tc[k].d[0])
+      << ", " << cimm<R>(tc[k].d[1]) << ")); }\n";
+  }
+  for (int k = 0; k < h.nRR; ++k)
+    o << "      svb::mul_rr<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ">(a, " << cimm<R>(rr[k].d[0]) << ", "
+      << cimm<R>(rr[k].d[1]) << ", " << cimm<R>(rr[k].d[2]) << ", " << cimm<R>(rr[k].d[3]) << ");\n";
+  // fold D0 into C (unit-modulus entries: 1/D0 = conj(D0)), then apply
+  bool need_c = !cone;
+  for (int i = 0; i < RB; ++i)
+    if (!d0one[i]) {
+      if (!need_c) {
+        o << "      svb::cplx<R> C = svb::mk<R>(R(1), R(0));\n";
+        need_c = true;
+      }
+      o << "      C = svb::cmul<R>(C, D0_" << i << ");\n";
+      if (!d1one[i]) o << "      D1_" << i << " = svb::conj_mul<R>(D1_" << i << ", D0_" << i << ");\n";
+      else {
+        o << "      svb::cplx<R> D1_" << i << " = svb::mk<R>(D0_" << i << ".x, -D0_" << i << ".y);\n";
+        d1one[i] = false;
+      }
+    }
+  if (need_c) o << "      svb::mul_all<R, RB>(a, C);\n";
+  for (int i = 0; i < RB; ++i)
+    if (!d1one[i]) o << "      svb::mul_half<R, RB, " << i << ">(a, D1_" << i << ");\n";
+  o << "    }\n";
+}
+
+// Emit the straight-line Body of one pass.
+template <typename R>
+void emit_body(std::ostringstream& o, const Program& prog, int p, int RB) {
+  const PassDev& pd = prog.passes[p];
+  o << "    case " << p << ": {\n";
+  for (int k = 0; k < pd.nrounds; ++k) {
+    const RoundDev& rd = pd.rounds[k];
+    o << "    // round " << k << "\n"
+      << "    svb::round_fixed<R, RB>(c, " << k << ", base, sFl, Fg);\n"
+      << "    svb::layout_slots<R, RB>(sFl, c.pd.rounds[" << k << "], slot);\n"
+      << "    svb::load_slots<R, RB>(a, cur, slot);\n";
+    uint32_t off = rd.op_off;
+    while (off < rd.op_end) {
+      OpHdr h;
+      std::memcpy(&h, prog.ops.data() + off, sizeof h);
+      const uint32_t pay = off + (uint32_t)sizeof(OpHdr);
+      const cplx<R>* coef = reinterpret_cast<const cplx<R>*>(prog.ops.data() + pay);
+      std::string guard;
+      if (h.fmask) {
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "if ((Fg & 0x%llxull) == 0x%llxull) ", (unsigned long long)h.fmask,
+                      (unsigned long long)h.fval);
+        guard = buf;
+      }
+      const std::string cond = h.rmask ? "true" : "false";
+      const std::string rm = std::to_string(h.rmask) + "u, " + std::to_string(h.rval) + "u";
+      switch (h.kind) {
+        case OP_DIAG:
+          emit_diag<R>(o, prog.ops.data() + pay, RB);
+          break;
+        case OP_U1R:
+          o << "    " << guard << "svb::u1_real_v<R, RB, " << h.a << ", " << cond << ">(a, "
+            << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].x, sizeof(R) == 4) << ", "
+            << hexf((double)coef[2].x, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
+            << rm << ");\n";
+          break;
+        case OP_U1:
+          o << "    " << guard << "svb::u1_dense_v<R, RB, " << h.a << ", " << cond << ">(a, " << cimm<R>(coef[0])
+            << ", " << cimm<R>(coef[1]) << ", " << cimm<R>(coef[2]) << ", " << cimm<R>(coef[3]) << ", " << rm
+            << ");\n";
+          break;
+        case OP_U1ANTI:
+          o << "    " << guard << "svb::u1_anti_v<R, RB, " << h.a << ", " << cond << ">(a, " << cimm<R>(coef[1])
+            << ", " << cimm<R>(coef[2]) << ", " << rm << ");\n";
+          break;
+        case OP_U2:
+          o << "    " << guard << "svb::u2_dense<R, RB, " << h.a << ", " << h.b
+            << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
+          break;
+        case OP_PERM2:
+          o << "    " << guard << "svb::u2_perm<R, RB, " << h.a << ", " << h.b
+            << ">(a, reinterpret_cast<const int32_t*>(c.ops + " << pay
+            << "), reinterpret_cast<const svb::cplx<R>*>(c.ops + " << (pay + 16) << "), " << rm << ");\n";
+          break;
+        default:
+          throw Error(SVB_E_CUDA, "jit: unknown op kind");
+      }
+      off += h.bytes;
+    }
+    if (k + 1 < pd.nrounds)
+      o << "    svb::store_slots<R, RB>(a, cur, slot);\n    __syncthreads();\n";
+    else
+      o << "    svb::store_global<R, RB>(c.state, Fg, c.pd, c.pd.rounds[" << k << "], a);\n";
+  }
+  o << "    } break;\n";
+  (void)RB;
+}
+
+}  // namespace
+
+bool jit_available() {
+  static Nvrtc nv;
+  static Driver dr;
+  return nv.ok && dr.ok;
+}
+
+// Source of one pass kernel (skeleton + straight-line body).
+template <typename R> std::string jit_source_pass(const Program& prog, int p) {
+  constexpr int RB = sizeof(R) == 8 ? 4 : 5;
+  std::ostringstream o;
+  o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
+  o << "struct PassBody {\n  template <typename R, int RB>\n"
+       "  __device__ static __forceinline__ void tile(int pass, const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
+       "svb::cplx<R>* cur, uint64_t base) {\n"
+       "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    switch (0) {\n";
+  emit_body<R>(o, prog, p, RB);
+  o << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(256, 1) svb_jit(svb::cplx<R>* __restrict__ state, "
+       "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass) {\n"
+       "  svb::pass_kernel<R, "
+    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass);\n}\n";
+  std::string src = o.str();
+  // the body names its case by pass index; a single-case switch on 0
+  const std::string from = "    case " + std::to_string(p) + ": {";
+  const size_t at = src.find(from);
+  if (at != std::string::npos) src.replace(at, from.size(), "    case 0: {");
+  return src;
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char ch : s) {
+    h ^= ch;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+std::string cache_dir() {
+  const char* env = std::getenv("SVB_JIT_CACHE");
+  if (env) return env;
+  const char* home = std::getenv("HOME");
+  return std::string(home ? home : "/tmp") + "/.cache/svb_jit";
+}
+
+// NVRTC -> cubin; empty on failure (log in *log).
+static std::vector<char> jit_compile(const std::string& src, std::string* log) {
+  static Nvrtc nv;
+  if (!nv.ok) {
+    if (log) *log = "libnvrtc not found";
+    return {};
+  }
+  void* prog_h = nullptr;
+  const char* hdr_src[] = {svb_device_core_src};
+  const char* hdr_name[] = {"device_core.cuh"};
+  if (nv.create(&prog_h, src.c_str(), "svb_jit.cu", 1, hdr_src, hdr_name) != 0) return {};
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+  int rc = nv.compile(prog_h, 3, opts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.log_size(prog_h, &n);
+    std::string logs(n, '\0');
+    nv.log(prog_h, &logs[0]);
+    nv.destroy(&prog_h);
+    if (log) *log = logs;
+    return {};
+  }
+  size_t n = 0;
+  nv.cubin_size(prog_h, &n);
+  std::vector<char> cubin(n);
+  nv.cubin(prog_h, cubin.data());
+  nv.destroy(&prog_h);
+  return cubin;
+}
+
+template <typename R>
+bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass, const uint8_t* dops,
+                       cudaStream_t st, ProgramStats* stats, int nsm) {
+  static Driver dr;
+  if (!dr.ok || prog.passes.empty()) return false;
+  constexpr int RB = sizeof(R) == 8 ? 4 : 5;
+  int dev = 0;
+  SVB_CUDA(cudaGetDevice(&dev));
+  const size_t np = prog.passes.size();
+  std::vector<std::string> srcs(np), keys(np);
+  std::vector<CUfunction> fns(np, nullptr);
+  const uint64_t salt = fnv1a(svb_device_core_src, fnv1a("svb-jit-v1 sm_100a"));
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t p = 0; p < np; ++p) {
+      srcs[p] = jit_source_pass<R>(prog, (int)p);
+      char buf[40];
+      std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
+      keys[p] = std::to_string(dev) + ":" + buf;
+      auto it = g_cache.find(keys[p]);
+      if (it != g_cache.end()) fns[p] = it->second.fns[0];
+      else todo.push_back(p);
+    }
+  }
+  if (!todo.empty()) {
+    // disk cache, then NVRTC for the rest (one thread per pass kernel)
+    const std::string dir = cache_dir();
+    std::vector<std::vector<char>> cubins(np);
+    std::vector<size_t> compile;
+    for (size_t p : todo) {
+      const std::string path = dir + "/" + keys[p].substr(keys[p].find(':') + 1) + ".cubin";
+      FILE* f = std::fopen(path.c_str(), "rb");
+      if (f) {
+        std::fseek(f, 0, SEEK_END);
+        long sz = std::ftell(f);
+        std::fseek(f, 0, SEEK_SET);
+        cubins[p].resize(sz > 0 ? (size_t)sz : 0);
+        if (sz <= 0 || std::fread(cubins[p].data(), 1, (size_t)sz, f) != (size_t)sz) cubins[p].clear();
+        std::fclose(f);
+      }
+      if (cubins[p].empty()) compile.push_back(p);
+    }
+    std::vector<std::string> logs(np);
+    std::vector<std::thread> th;
+    for (size_t p : compile) th.emplace_back([&, p] { cubins[p] = jit_compile(srcs[p], &logs[p]); });
+    for (auto& t : th) t.join();
+    if (!compile.empty()) {
+      std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+      if (std::system(mk.c_str()) != 0) { /* cache is best effort */ }
+    }
+    for (size_t p : compile) {
+      if (cubins[p].empty()) {
+        std::fprintf(stderr, "[svb] JIT compile failed; using the interpreter kernel\n%s\n", logs[p].c_str());
+        return false;
+      }
+      const std::string path = dir + "/" + keys[p].substr(keys[p].find(':') + 1) + ".cubin";
+      const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)(uintptr_t)&cubins[p]);
+      FILE* f = std::fopen(tmp.c_str(), "wb");
+      if (f) {
+        const bool ok = std::fwrite(cubins[p].data(), 1, cubins[p].size(), f) == cubins[p].size();
+        std::fclose(f);
+        if (ok) std::rename(tmp.c_str(), path.c_str());
+        else std::remove(tmp.c_str());
+      }
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t p : todo) {
+      Module m;
+      if (dr.load(&m.mod, cubins[p].data()) != CUDA_SUCCESS) return false;
+      CUfunction f;
+      if (dr.getfn(&f, m.mod, "svb_jit") != CUDA_SUCCESS) return false;
+      m.fns.push_back(f);
+      fns[p] = f;
+      g_cache.emplace(keys[p], m);
+    }
+  }
+  for (size_t p = 0; p < np; ++p) {
+    const PassDev& pd = prog.passes[p];
+    const uint64_t tiles = 1ull << pd.nout;
+    const unsigned threads = 1u << (pd.m - RB);
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);
+    const unsigned smem = (unsigned)(kStages * (size_t)tile_bytes_of<R>(pd.m) + pd.ops_bytes);
+    CUfunction f = fns[p];
+    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+      throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
+    cplx<R>* s = state;
+    const PassDev* pdp = dpass + p;
+    const uint8_t* ob = dops;
+    uint32_t nt = (uint32_t)tiles;
+    int pass = 0;
+    void* args[] = {&s, &pdp, &ob, &nt, &pass};
+    Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
+    if (pf) pf->begin(st, 0, 2.0 * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
+    if (dr.launch(f, grid, 1, 1, threads, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS)
+      throw Error(SVB_E_CUDA, "jit: kernel launch failed");
+    if (pf) pf->end(st);
+    stats->passes += 1;
+    stats->launches += 1;
+  }
+  return true;
+}
+
+template bool jit_launch_passes<float>(cplx<float>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
+                                       ProgramStats*, int);
+template bool jit_launch_passes<double>(cplx<double>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
+                                        ProgramStats*, int);
+
+}  // namespace svb
+
+using namespace svb;
+
+// Host-only check of the JIT path (no GPU needed): schedule, generate and
+// NVRTC-compile the specialised kernels of a gate program.  Returns SVB_OK and
+// the cubin size, or an error with the compiler log in svb_last_error-like buf.
+extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng, int64_t* cubin_bytes, char* log,
+                             int log_cap) {
+  try {
+    SchedOptions o = default_options(precision, n);
+    std::vector<std::string> srcs;
+    if (precision == SVB_C128) {
+      Program p = build_program<double>(n, gates, ng, o);
+      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<double>(p, (int)k));
+    } else {
+      Program p = build_program<float>(n, gates, ng, o);
+      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<float>(p, (int)k));
+    }
+    if (std::getenv("SVB_JIT_DUMP") && !srcs.empty()) {
+      FILE* f = std::fopen(std::getenv("SVB_JIT_DUMP"), "w");
+      if (f) {
+        for (auto& x : srcs) std::fputs(x.c_str(), f);
+        std::fclose(f);
+      }
+    }
+    std::vector<std::vector<char>> cubins(srcs.size());
+    std::vector<std::string> logs(srcs.size());
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < srcs.size(); ++k) th.emplace_back([&, k] { cubins[k] = jit_compile(srcs[k], &logs[k]); });
+    for (auto& t : th) t.join();
+    int64_t total = 0;
+    for (size_t k = 0; k < srcs.size(); ++k) {
+      if (cubins[k].empty()) {
+        if (log && log_cap > 0) std::snprintf(log, (size_t)log_cap, "%s", logs[k].c_str());
+        *cubin_bytes = total;
+        return SVB_E_CUDA;
+      }
+      total += (int64_t)cubins[k].size();
+    }
+    *cubin_bytes = total;
+    return SVB_OK;
+  } catch (const Error& e) {
+    if (log && log_cap > 0) std::snprintf(log, (size_t)log_cap, "%s", e.what());
+    return e.code;
+  }
+}

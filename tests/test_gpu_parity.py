@@ -314,3 +314,29 @@ def test_ghz20_config1_counts_bit_exact():
     c = suite.ghz_circuit(20)
     for seed, counts in ref.items():
         assert sv.run(c, 1024, int(seed)).counts == counts
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_jit_matches_interpreter_and_oracle(precision):
+    """NVRTC-specialised passes == interpreter passes == oracle."""
+    rng = np.random.default_rng(21)
+    for trial in range(3):
+        n = int(rng.integers(14, 19))
+        c = suite.random_circuit(n, int(rng.integers(60, 250)), rng, measured=False)
+        ref = orc.unitary_state(c)
+        outs = []
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            s.apply_instructions(c.instructions)
+            outs.append(s.to_numpy())
+            s.close()
+        assert relerr(outs[0], ref) < TOL[precision]
+        assert relerr(outs[1], ref) < TOL[precision]
+    for c in (suite.qft_bench_circuit(15), suite.sycamore_circuit(3, 5, 10, seed=2, measured=False)):
+        ref = orc.unitary_state(c)
+        s = sv.DeviceState(c.n_qubits, precision)
+        s.set_option(_lib.OPT_JIT_MIN_N, 1)
+        s.apply_instructions(c.instructions)
+        assert relerr(s.to_numpy(), ref) < TOL[precision], c.name
+        s.close()
