@@ -129,6 +129,20 @@ int svb_sample(svb_handle h, const int32_t* qubits, int k, const int32_t* bit_sr
  * SVB_E_SAMPLING for an invalid vector (sampling.py:31-40). */
 int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_row, int64_t* alias_row);
 
+/* Sharded mode (global<->local qubit swaps, svb_dist in sharded.py):
+ * raw device pointer of the state (synchronised), and gather/scatter of the
+ * half whose bit L == bit to/from a contiguous device buffer of 2^(n-1)
+ * amplitudes (to_buf = 1: state -> buffer). */
+int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream);
+int svb_half_copy(svb_handle h, int L, int bit, void* dev_buf, int to_buf);
+int svb_clear(svb_handle h); /* all amplitudes 0 (a shard that holds no part of |0..0>) */
+/* Distributed terminal sampling: the shots of the shared PCG64 stream whose
+ * global CDF target u*total falls in [lo, hi) are drawn from this shard;
+ * bit_src[p] = local bit of output bit p or -1 (then taken from code_or). */
+int svb_sample_slice(svb_handle h, uint64_t shots, const uint64_t* pcg, double lo, double hi, double total,
+                     const int32_t* bit_src, int w, uint64_t code_or, uint64_t* out_codes, uint64_t* out_counts,
+                     uint64_t* n_unique);
+
 /* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
  * device; each measure/reset consumes one draw, exactly as rng.random(). */
 int svb_rng_seed(svb_handle h, const uint64_t* pcg);

@@ -34,6 +34,9 @@ struct svb_state {
 };
 
 static thread_local std::string g_err;
+namespace svb {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace svb
 
 template <class F> static int guard(F&& f) {
   try {
@@ -449,6 +452,50 @@ int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_ro
     cudaFreeAsync(dp, st); cudaFreeAsync(dr, st); cudaFreeAsync(da, st);
     SVB_CUDA(cudaStreamSynchronize(st));
     cudaStreamDestroy(st);
+  });
+}
+
+int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream) {
+  return guard([&] {
+    check_handle(h);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+    *ptr = h->amps;
+    *bytes = (uint64_t)h->amp_bytes();
+    *stream = (int64_t)(intptr_t)h->st;
+  });
+}
+
+int svb_clear(svb_handle h) {
+  return guard([&] {
+    check_handle(h);
+    SVB_CUDA(cudaMemsetAsync(h->amps, 0, h->amp_bytes(), h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_sample_slice(svb_handle h, uint64_t shots, const uint64_t* pcg, double lo, double hi, double total,
+                     const int32_t* bit_src, int w, uint64_t code_or, uint64_t* out_codes, uint64_t* out_counts,
+                     uint64_t* n_unique) {
+  return guard([&] {
+    check_handle(h);
+    require(shots >= 1 && w >= 1 && w <= 63 && h->n >= 5, SVB_E_ARG, "bad slice sampling arguments");
+    for (int p = 0; p < w; ++p) require(bit_src[p] >= -1 && bit_src[p] < h->n, SVB_E_ARG, "bad bit source");
+    uint64_t* d_codes = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_codes, shots * sizeof(uint64_t), h->st));
+    slice_draw(h->amps, h->prec == SVB_C128, h->n, shots, pcg, lo, hi, total, bit_src, w, code_or, d_codes, h->st);
+    *n_unique = histogram_codes(d_codes, shots, 64, out_codes, out_counts, h->st);
+    SVB_CUDA(cudaFreeAsync(d_codes, h->st));
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_half_copy(svb_handle h, int L, int bit, void* dev_buf, int to_buf) {
+  return guard([&] {
+    check_handle(h);
+    require(L >= 0 && L < h->n && (bit == 0 || bit == 1), SVB_E_ARG, "bad half selector");
+    if (h->prec == SVB_C128) launch_half_copy<double>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
+    else launch_half_copy<float>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
   });
 }
 

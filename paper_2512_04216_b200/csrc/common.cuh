@@ -29,6 +29,8 @@ struct Error : std::runtime_error {
 
 #define SVB_CHECK_LAUNCH() SVB_CUDA(cudaGetLastError())
 
+void set_last_error(const char* msg);  // api.cu (thread-local, svb_last_error)
+
 inline void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
 }

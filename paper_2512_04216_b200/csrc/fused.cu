@@ -286,6 +286,7 @@ int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_pas
     *has_perm = p.final_perm.empty() ? 0 : 1;
     return SVB_OK;
   } catch (const Error& e) {
+    set_last_error(e.what());
     return e.code;
   }
 }
@@ -309,6 +310,7 @@ int svb_emulate_apply(int n, int precision, const svb_gate* gates, int ng, doubl
     }
     return SVB_OK;
   } catch (const Error& e) {
+    set_last_error(e.what());
     return e.code;
   }
 }

@@ -26,6 +26,7 @@ template <typename R>
 void launch_measure(void* state, int n, int q, bool reset, uint64_t* d_rng, double* d_ws,
                     int32_t* d_outcome, uint64_t* d_code, int rank, cudaStream_t st);
 size_t measure_ws_doubles(int n);
+template <typename R> void launch_half_copy(void* state, int n, void* buf, int L, int bit, int to_buf, cudaStream_t st);
 
 // sample.cu — PCG64, pairwise sum, alias table, samplers, histogram
 void host_pcg_advance(uint64_t* pcg4, uint64_t delta);
@@ -45,6 +46,8 @@ void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, con
               int w, uint64_t* d_codes, cudaStream_t st);
 void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
                     const int32_t* bit_src, int w, uint64_t* d_codes, cudaStream_t st);
+void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uint64_t* pcg, double lo, double hi,
+                double total, const int32_t* bit_src, int w, uint64_t code_or, uint64_t* d_codes, cudaStream_t st);
 uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_codes,
                          uint64_t* h_counts, cudaStream_t st);
 

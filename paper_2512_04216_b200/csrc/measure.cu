@@ -273,3 +273,29 @@ INST(float)
 INST(double)
 
 }  // namespace svb
+
+namespace svb {
+// ------------------------------------------------- sharded-mode data moves
+// Gather / scatter the half of the state whose bit L equals `bit` into / out
+// of a contiguous buffer (global<->local qubit swap, sharded mode).
+template <typename R>
+__global__ void k_half_copy(cplx<R>* __restrict__ s, cplx<R>* __restrict__ buf, uint64_t nhalf, int L, int bit,
+                            int to_buf) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t b = (uint64_t)bit << L;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nhalf; i += stride) {
+    const uint64_t j = insert0(i, L) | b;
+    if (to_buf) buf[i] = s[j];
+    else s[j] = buf[i];
+  }
+}
+
+template <typename R> void launch_half_copy(void* state, int n, void* buf, int L, int bit, int to_buf, cudaStream_t st) {
+  const uint64_t nh = 1ull << (n - 1);
+  k_half_copy<R><<<grid_for(nh, 256), 256, 0, st>>>(static_cast<cplx<R>*>(state), static_cast<cplx<R>*>(buf), nh, L,
+                                                    bit, to_buf);
+  SVB_CHECK_LAUNCH();
+}
+template void launch_half_copy<float>(void*, int, void*, int, int, int, cudaStream_t);
+template void launch_half_copy<double>(void*, int, void*, int, int, int, cudaStream_t);
+}  // namespace svb

@@ -579,6 +579,69 @@ template void cdf_draw<float>(const void*, int, uint64_t, const uint64_t*, const
 template void cdf_draw<double>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
                                uint64_t*, cudaStream_t);
 
+// ------------------------------------------------- sharded CDF slice draw
+// Shot s (stream position s) belongs to this shard when its global target
+// tau = u_s * total falls in [lo, hi); its local target is tau - lo.  Codes
+// of foreign shots are set to the sentinel ~0 (dropped by the histogram).
+__global__ void k_slice_draw(const double* __restrict__ cum, const double* __restrict__ pr_unused,
+                             const void* __restrict__ state, int prec128, uint64_t m, uint64_t nleaf, uint64_t shots,
+                             Pcg base, double lo, double hi, double total, BitSrc bs, int w, uint64_t code_or,
+                             uint64_t* __restrict__ codes) {
+  uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t s0 = t * kShotsPerThread;
+  if (s0 >= shots) return;
+  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  Pcg g = base;
+  g.advance(s0);
+  auto prob = [&](uint64_t i) {
+    if (prec128) {
+      double2 a = static_cast<const double2*>(state)[i];
+      return a.x * a.x + a.y * a.y;
+    }
+    float2 a = static_cast<const float2*>(state)[i];
+    const double x = a.x, y = a.y;
+    return x * x + y * y;
+  };
+  for (uint64_t k = s0; k < s1; ++k) {
+    const double tau = g.next_double() * total;
+    if (tau < lo || tau >= hi) {
+      codes[k] = ~0ull;
+      continue;
+    }
+    double x = tau - lo;
+    const double tl = cum[nleaf - 1];
+    if (x >= tl) x = tl * (1.0 - 1e-16);
+    const uint64_t idx = cdf_pick(cum, nleaf, m, x, prob);
+    uint64_t code = code_or;
+    for (int p = 0; p < w; ++p)
+      if (bs.b[p] >= 0) code |= ((idx >> bs.b[p]) & 1ull) << p;
+    codes[k] = code;
+  }
+  (void)pr_unused;
+}
+
+void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uint64_t* pcg, double lo, double hi,
+                double total, const int32_t* bit_src, int w, uint64_t code_or, uint64_t* d_codes, cudaStream_t st) {
+  const uint64_t m = 1ull << n;
+  const uint64_t nleaf = m / 32;
+  DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
+  if (prec128)
+    k_leaf_sums_state<double><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const double2*>(state), nleaf,
+                                                                         leaf.as<double>());
+  else
+    k_leaf_sums_state<float><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const float2*>(state), nleaf,
+                                                                        leaf.as<double>());
+  SVB_CHECK_LAUNCH();
+  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  BitSrc bs;
+  for (int p = 0; p < 64; ++p) bs.b[p] = p < w ? (int8_t)bit_src[p] : (int8_t)-1;
+  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_slice_draw<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(cum.as<double>(), nullptr, state, prec128, m,
+                                                                   nleaf, shots, pcg_from(pcg), lo, hi, total, bs, w,
+                                                                   code_or, d_codes);
+  SVB_CHECK_LAUNCH();
+}
+
 // --------------------------------------------------------------- histogram
 uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_codes,
                          uint64_t* h_counts, cudaStream_t st) {
@@ -602,6 +665,7 @@ uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_c
                                                 cnt.as<uint64_t>(), nr.as<int64_t>(), (int64_t)shots, st));
   }
   int64_t nruns = d2h_scalar(nr.as<int64_t>(), st);
+  if (nruns > 0 && d2h_scalar(uniq.as<uint64_t>() + (nruns - 1), st) == ~0ull) --nruns;  // foreign shots
   SVB_CUDA(cudaMemcpyAsync(h_codes, uniq.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
   SVB_CUDA(cudaMemcpyAsync(h_counts, cnt.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
   SVB_CUDA(cudaStreamSynchronize(st));
