@@ -18,8 +18,10 @@ BASELINE.json names); the per-pass HBM GB/s is reported as `roofline`.
 * `cpu_baseline` / `--impl reference`: the numpy restatement of the reference
   algorithm (oracle/, "port") timed on this host on a bounded, evenly spaced
   sample of the same gate list.
-* N > 1 (torchrun): independent replicas, one per GPU ("replicas only" for this
-  workload in round 1; the sharded path is described in DESIGN.md).
+* N > 1 (torchrun, NCCL): weak scaling — QFT on 30 + log2(N) qubits, complex128,
+  sharded by global qubits (paper_2512_04216_b200/sharded.py): 16 GiB of state
+  per GPU at every N, global<->local qubit swaps over NVLink.  ``--sharded``
+  forces that path at N = 1.
 """
 from __future__ import annotations
 
@@ -280,6 +282,67 @@ def run_ours(args, rank: int, world: int, dist):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank: int, world: int, dist):
+    """Weak scaling: QFT-(30 + log2 N) c128 sharded over N GPUs."""
+    import torch
+
+    from paper_2512_04216_b200 import suite
+    from paper_2512_04216_b200.sharded import ShardedState
+
+    device = int(os.environ.get("LOCAL_RANK", 0))
+    g = world.bit_length() - 1
+    n = N_QUBITS + g
+    c = suite.qft_bench_circuit(n)
+    n_gates = len(c.instructions)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    st = ShardedState(n, PRECISION, device=device, backend="device")
+
+    def step():
+        st.reset()
+        st.apply(c.instructions)
+        z = st.expectations([(q,) for q in range(n)])
+        return z, st.swaps, st.bytes_sent
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            z, swaps, sent = step()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    barrier()
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    line = {
+        "metric": "gates/sec (QFT-30 complex128, full amplitudes + <Z_i>)",
+        "value": n_gates / (ms / 1e3),
+        "unit": "gates/s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 1),
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (deterministic QFT circuit, 16 GiB state per GPU >> L2)",
+        "config": {"workload": f"qft{n}_c128_sharded_weak", "n_qubits": n, "gates": n_gates,
+                   "parallelism": f"sharded{world}", "swaps_per_step": swaps, "bytes_sent_per_rank": sent,
+                   "l2": "inputs larger than L2"},
+        "e2e": {"value": n_gates / (ms / 1e3), "unit": "gates/s", "h2d_bytes_per_step": int(n_gates * 272),
+                "d2h_bytes_per_step": 8 * n},
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -289,6 +352,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-gates", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="sharded path even at N = 1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -301,9 +365,12 @@ def main():
         import torch.distributed as tdist
 
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("gloo")
+        tdist.init_process_group("nccl")
         dist = tdist
-    run_ours(args, rank, world, dist)
+    if world > 1 or args.sharded:
+        run_sharded(args, rank, world, dist)
+    else:
+        run_ours(args, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()
 

@@ -1,0 +1,46 @@
+"""Install the B200 backend into an existing `polysim` installation.
+
+    import paper_2512_04216_b200.polysim_shim as shim
+    shim.install()          # polysim's "sv" backend now runs on the GPU
+
+Replaces the public state-vector functions of `polysim.statevector`
+(`statevector.py:33-292`) with this package's, so every caller that reaches
+the dense path — `dispatch.run_circuit(c, "sv", ...)` (`dispatch.py:21`), the
+batch runner, calibration's kernel timings, pblock's block kernels, metrics —
+runs on the device without code changes.  `DEFAULT_QUBIT_CAP` keeps the
+reference value, so the predictor's hard-coded cap check behaves the same.
+`uninstall()` restores the originals.
+"""
+from __future__ import annotations
+
+from . import statevector as _sv
+
+_NAMES = (
+    "run", "final_state", "expectation", "zero_state", "apply_1q", "apply_2q", "apply_instruction",
+    "marginal_probs", "_measure_qubit", "_reset_qubit",
+)
+_saved: dict = {}
+
+
+def install() -> None:
+    import polysim.statevector as ref  # noqa: F401  (raises ImportError without polysim)
+
+    if _saved:
+        return
+    for name in _NAMES:
+        _saved[name] = getattr(ref, name)
+        setattr(ref, name, getattr(_sv, name))
+    _saved["_state_cache"] = ref._state_cache
+    ref._state_cache = _sv._state_cache
+
+
+def uninstall() -> None:
+    import polysim.statevector as ref
+
+    for name, fn in _saved.items():
+        setattr(ref, name, fn)
+    _saved.clear()
+
+
+def installed() -> bool:
+    return bool(_saved)

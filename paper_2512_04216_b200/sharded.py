@@ -227,6 +227,21 @@ class ShardedState:
         self.swaps = 0
         self.bytes_sent = 0
 
+    def reset(self) -> None:
+        """Back to |0...0> with the identity layout (reuses the shard memory)."""
+        self.pos = list(range(self.n))
+        self.swaps = 0
+        self.bytes_sent = 0
+        if isinstance(self.shard, _DeviceShard):
+            if self.rank == 0:
+                self.shard.state.zero()
+            else:
+                _lib.check(_lib.lib().svb_clear(self.shard.state.handle))
+        else:
+            self.shard.amps[:] = 0
+            if self.rank == 0:
+                self.shard.amps[0] = 1.0
+
     # ---------------------------------------------------------------- layout
     def _inv(self):
         inv = [0] * self.n

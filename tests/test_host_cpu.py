@@ -167,3 +167,25 @@ def test_plan_pass_counts():
     assert p["passes"] <= 8 and p["permute"]
     p = sv.plan(24, [Instruction("h", (q,)) for q in range(24)], "c128")
     assert p["passes"] == math.ceil((24 - 5) / 7)
+
+
+def test_polysim_shim_installs_and_restores():
+    """Drop-in swap of polysim.statevector; needs the reference."""
+    import sys as _sys
+
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        pytest.skip("reference not present (GPU box)")
+    _sys.path.insert(0, ref_src)
+    try:
+        import polysim.statevector as ref_sv
+        from paper_2512_04216_b200 import polysim_shim
+
+        orig = ref_sv.run
+        polysim_shim.install()
+        assert ref_sv.run is sv.run and ref_sv.final_state is sv.final_state
+        assert ref_sv.DEFAULT_QUBIT_CAP == 26
+        polysim_shim.uninstall()
+        assert ref_sv.run is orig
+    finally:
+        _sys.path.remove(ref_src)
