@@ -637,6 +637,12 @@ __device__ __forceinline__ void mul_all(cplx<R>* a, cplx<R> d) {
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v) a[v] = cmul<R>(a[v], d);
 }
+template <typename R, int RB, int IA, int IB, int Q>
+__device__ __forceinline__ void mul_quad(cplx<R>* a, cplx<R> d) {  // amps with bit(IA) + 2 bit(IB) == Q
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v)
+    if ((((v >> IA) & 1) + 2 * ((v >> IB) & 1)) == Q) a[v] = cmul<R>(a[v], d);
+}
 template <typename R, int RB, int IA, int IB>
 __device__ __forceinline__ void mul_rr(cplx<R>* a, cplx<R> e0, cplx<R> e1, cplx<R> e2, cplx<R> e3) {
 #pragma unroll

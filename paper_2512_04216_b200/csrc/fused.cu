@@ -26,45 +26,86 @@
 namespace svb {
 
 // ---------------------------------------------------------------- permute
+// Out-of-place bit permutation of the index: output bit dest[p] = input bit p.
+// A tile holds the ml input bits {0..4} ∪ dest^-1({0..4}) (plus fill up to 12),
+// so both the HBM reads (input bits 0..4 innermost) and the writes (output bits
+// 0..4 innermost) are 32-amplitude contiguous runs.  Per-element offsets come
+// from split tables (6 + 6 bits) built once per CTA; the tile is XOR-swizzled.
 struct PermDev {
-  int32_t n, ml;        // tile local bits
-  int32_t lin[12];      // input bit of local bit l (ascending)
-  int32_t lout_src[12]; // output-local bit e (ascending output positions) -> input-local bit
-  int32_t lout_pos[12]; // output bit of output-local bit e
+  int32_t n, ml;
+  int32_t lin[16];       // input bit of local bit l (ascending)
+  int32_t lout_src[16];  // output-local bit e (ascending output positions) -> input-local bit
+  int32_t lout_pos[16];  // output bit of output-local bit e
   int32_t nout;
-  int32_t outin[48];    // input bits outside the tile, ascending
-  int32_t dest[64];     // output bit of input bit p
+  int32_t outin[48];     // input bits outside the tile, ascending
+  int32_t dest[64];      // output bit of input bit p
 };
 
 template <typename R>
 __global__ void __launch_bounds__(256) k_permute(const cplx<R>* __restrict__ in, cplx<R>* __restrict__ out,
-                                                 PermDev pd) {
+                                                 const PermDev pd, uint64_t ntiles) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  cplx<R>* sm = reinterpret_cast<cplx<R>*>(smraw);
-  const uint64_t t = blockIdx.x;
-  uint64_t bin = 0, bout = 0;
-  for (int i = 0; i < pd.nout; ++i)
-    if ((t >> i) & 1ull) {
-      bin |= 1ull << pd.outin[i];
-      bout |= 1ull << pd.dest[pd.outin[i]];
-    }
-  const uint32_t T = 1u << pd.ml;
-  for (uint32_t j = threadIdx.x; j < T; j += blockDim.x) {
-    uint64_t g = bin;
-    for (int l = 0; l < pd.ml; ++l)
-      if ((j >> l) & 1u) g |= 1ull << pd.lin[l];
-    sm[j] = __ldcs(in + g);
+  __shared__ uint64_t in_lo[64], in_hi[64], out_lo[64], out_hi[64];
+  __shared__ uint32_t src_lo[64], src_hi[64];
+  cplx<R>* tile = reinterpret_cast<cplx<R>*>(smraw);
+  const int ml = pd.ml, lb = ml < 6 ? ml : 6, hb = ml - lb;
+  for (int x = threadIdx.x; x < 64; x += blockDim.x) {
+    uint64_t a = 0, b = 0, c = 0, d = 0;
+    uint32_t e = 0, f = 0;
+    for (int l = 0; l < lb; ++l)
+      if ((x >> l) & 1) {
+        a |= 1ull << pd.lin[l];
+        c |= 1ull << pd.lout_pos[l];
+        e |= 1u << pd.lout_src[l];
+      }
+    for (int l = 0; l < hb; ++l)
+      if ((x >> l) & 1) {
+        b |= 1ull << pd.lin[lb + l];
+        d |= 1ull << pd.lout_pos[lb + l];
+        f |= 1u << pd.lout_src[lb + l];
+      }
+    in_lo[x] = a; in_hi[x] = b; out_lo[x] = c; out_hi[x] = d; src_lo[x] = e; src_hi[x] = f;
   }
   __syncthreads();
-  for (uint32_t o = threadIdx.x; o < T; o += blockDim.x) {
-    uint64_t g = bout;
-    uint32_t j = 0;
-    for (int e = 0; e < pd.ml; ++e)
-      if ((o >> e) & 1u) {
-        g |= 1ull << pd.lout_pos[e];
-        j |= 1u << pd.lout_src[e];
+  const uint32_t T = 1u << ml, lmask = (1u << lb) - 1;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint64_t bin = 0, bout = 0;
+    for (int i = 0; i < pd.nout; ++i)
+      if ((t >> i) & 1ull) {
+        bin |= 1ull << pd.outin[i];
+        bout |= 1ull << pd.dest[pd.outin[i]];
       }
-    __stcs(out + g, sm[j]);
+    if (T == 4096 && blockDim.x == 256) {  // full tiles: 16 independent loads in flight per thread
+      cplx<R> v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t j = threadIdx.x + 256u * k;
+        v[k] = __ldcs(in + (bin | in_lo[j & lmask] | in_hi[j >> lb]));
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) tile[swz<R>(threadIdx.x + 256u * k)] = v[k];
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t o = threadIdx.x + 256u * k;
+        const uint32_t j = src_lo[o & lmask] | src_hi[o >> lb];
+        v[k] = tile[swz<R>(j)];
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t o = threadIdx.x + 256u * k;
+        __stcs(out + (bout | out_lo[o & lmask] | out_hi[o >> lb]), v[k]);
+      }
+    } else {
+      for (uint32_t j = threadIdx.x; j < T; j += blockDim.x)
+        tile[swz<R>(j)] = __ldcs(in + (bin | in_lo[j & lmask] | in_hi[j >> lb]));
+      __syncthreads();
+      for (uint32_t o = threadIdx.x; o < T; o += blockDim.x) {
+        const uint32_t j = src_lo[o & lmask] | src_hi[o >> lb];
+        __stcs(out + (bout | out_lo[o & lmask] | out_hi[o >> lb]), tile[swz<R>(j)]);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -74,6 +115,7 @@ static PermDev make_perm(int n, const std::vector<int>& dest) {
   uint64_t inset = 0x1full;
   for (int p = 0; p < n; ++p)
     if (dest[p] < 5) inset |= 1ull << p;
+  for (int p = 0; p < n && __builtin_popcountll(inset) < 12; ++p) inset |= 1ull << p;
   int ml = 0;
   for (int p = 0; p < n; ++p)
     if (inset & (1ull << p)) pd.lin[ml++] = p;
@@ -169,9 +211,15 @@ static void launch_permute(cplx<R>** state, cplx<R>** spare, int n, const std::v
   cplx<R>* out = *spare;
   size_t bytes = sizeof(cplx<R>) << n;
   uint64_t tiles = 1ull << pd.nout;
+  int dev = 0, nsm = 148;
+  SVB_CUDA(cudaGetDevice(&dev));
+  SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const size_t smem = sizeof(cplx<R>) << pd.ml;
+  SVB_CUDA(cudaFuncSetAttribute(k_permute<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * 3);
   Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
   if (pf) pf->begin(st, 1, 2.0 * (double)bytes);
-  k_permute<R><<<(unsigned)tiles, 256, sizeof(cplx<R>) << pd.ml, st>>>(*state, out, pd);
+  k_permute<R><<<grid, 256, smem, st>>>(*state, out, pd, tiles);
   SVB_CHECK_LAUNCH();
   if (pf) pf->end(st);
   // swap buffers rather than copy back (a copy would double the traffic)

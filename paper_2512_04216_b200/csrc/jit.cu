@@ -151,11 +151,13 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
       o << "      svb::cplx<R> D1_" << i << " = "
         << (has_ur ? "(" + us + ")[" + std::to_string(6 + i) + "]" : "svb::mk<R>(R(1), R(0))") << ";\n";
   }
-  for (int k = 0; k < h.nTR; ++k) {
+  for (int k = 0; k < h.nTR; ++k) {  // per term: skip the half that is exactly 1
     const int i = tr[k].ra, qb = tr[k].qb;
+    const bool t0 = is1(tr[k].d[0]) && is1(tr[k].d[2]), t1 = is1(tr[k].d[1]) && is1(tr[k].d[3]);
+    if (t0 && t1) continue;
     o << "      { const int f = (int)((Fg >> " << qb << ") & 1ull);";
-    if (!d0one[i]) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[0]) << ", " << cimm<R>(tr[k].d[2]) << "));";
-    if (!d1one[i]) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[1]) << ", " << cimm<R>(tr[k].d[3]) << "));";
+    if (!t0) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[0]) << ", " << cimm<R>(tr[k].d[2]) << "));";
+    if (!t1) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[1]) << ", " << cimm<R>(tr[k].d[3]) << "));";
     o << " }\n";
   }
   for (int k = 0; k < h.nTC; ++k) {
@@ -166,9 +168,11 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
       << cimm<R>(tc[k].d[2]) << ", " << cimm<R>(tc[k].d[3]) << ") : svb::csel<R>(fa, " << cimm<R>(tc[k].d[0])
       << ", " << cimm<R>(tc[k].d[1]) << ")); }\n";
   }
-  for (int k = 0; k < h.nRR; ++k)
-    o << "      svb::mul_rr<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ">(a, " << cimm<R>(rr[k].d[0]) << ", "
-      << cimm<R>(rr[k].d[1]) << ", " << cimm<R>(rr[k].d[2]) << ", " << cimm<R>(rr[k].d[3]) << ");\n";
+  for (int k = 0; k < h.nRR; ++k)  // only the quadrants whose factor is not exactly 1
+    for (int q = 0; q < 4; ++q)
+      if (!is1(rr[k].d[q]))
+        o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
+          << cimm<R>(rr[k].d[q]) << ");\n";
   // fold D0 into C (unit-modulus entries: 1/D0 = conj(D0)), then apply
   bool need_c = !cone;
   for (int i = 0; i < RB; ++i)

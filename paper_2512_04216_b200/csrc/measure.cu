@@ -33,10 +33,11 @@ __device__ __forceinline__ double block_sum256(double v, double* sh) {
 }
 
 static inline int reduce_blocks(uint64_t work) {
-  // size-determined (not device-determined) so results are reproducible anywhere
+  // size-determined (not device-determined) so results are reproducible anywhere;
+  // 1184 = 8 x 148: whole waves of 256-thread blocks
   uint64_t b = work / 4096;
   if (b < 1) b = 1;
-  if (b > 2048) b = 2048;
+  if (b > 1184) b = 1184;
   return (int)b;
 }
 
@@ -129,29 +130,78 @@ void launch_marginal(const void* state, int n, const int32_t* qubits, int k, dou
 }
 
 // ------------------------------------------------------- multi-mask <Z...Z>
+// For 16 amplitudes differing in 4 index bits, sum_j p_j (-1)^popc(i & mask)
+// = (-1)^popc(fixed bits & mask) * W[mask restricted to the 4 bits], where W is
+// the 16-point Walsh-Hadamard transform of the p_j — so any number of masks
+// costs one 64-add transform per 16 amplitudes plus one lookup per mask.
 constexpr int kMaskBatch = 32;
 struct MaskSet { uint64_t m[kMaskBatch]; };
 
 template <typename R>
-__global__ void __launch_bounds__(256) k_expect_partial(const cplx<R>* __restrict__ s, uint64_t len,
+__global__ void __launch_bounds__(256) k_expect_partial(const cplx<R>* __restrict__ s, uint64_t nchunks,
                                                         MaskSet ms, int nm, double* partial) {
+  // a warp owns chunks of 512 amplitudes; lane l holds index bits 0..4 = l and
+  // its 16 values differ in bits 5..8 (coalesced loads); the Walsh-Hadamard
+  // transform runs over bits 5..8, the sign of the other bits is per lane/chunk
   __shared__ double sh[8];
+  __shared__ double wsh[256 * 17];
+  double* W = wsh + threadIdx.x * 17;  // padded: conflict-free
+  const uint32_t lane = threadIdx.x & 31u;
   double acc[kMaskBatch];
 #pragma unroll
   for (int j = 0; j < kMaskBatch; ++j) acc[j] = 0.0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
-    cplx<R> a = s[i];
-    double x = (double)a.x, y = (double)a.y;
-    double p = x * x + y * y;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t c = gw; c < nchunks; c += nw) {
+    const cplx<R>* base = s + c * 512 + lane;
+    double w[16];
 #pragma unroll
-    for (int j = 0; j < kMaskBatch; ++j)
-      if (j < nm) acc[j] += (__popcll(i & ms.m[j]) & 1) ? -p : p;
+    for (int j = 0; j < 16; ++j) {
+      const cplx<R> a = __ldcs(base + 32 * j);
+      const double x = (double)a.x, y = (double)a.y;
+      w[j] = x * x + y * y;
+    }
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (!(j & h)) {
+          const double u = w[j], v = w[j | h];
+          w[j] = u + v;
+          w[j | h] = u - v;
+        }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) W[j] = w[j];
+    const uint64_t fixed = c * 512 + lane;  // bits 0..4 and >= 9
+#pragma unroll
+    for (int k = 0; k < kMaskBatch; ++k) {
+      if (k < nm) {
+        const double v = W[(ms.m[k] >> 5) & 15ull];
+        acc[k] += (__popcll(fixed & ms.m[k] & ~0x1e0ull) & 1) ? -v : v;
+      }
+    }
   }
-  for (int j = 0; j < nm; ++j) {
-    double t = block_sum256(acc[j], sh);
-    if (threadIdx.x == 0) partial[(uint64_t)j * gridDim.x + blockIdx.x] = t;
+#pragma unroll
+  for (int j = 0; j < kMaskBatch; ++j) {
+    if (j < nm) {  // nm is uniform: the barriers inside block_sum256 are safe
+      double t = block_sum256(acc[j], sh);
+      if (threadIdx.x == 0) partial[(uint64_t)j * gridDim.x + blockIdx.x] = t;
+    }
   }
+}
+
+// small states (< 16 amplitudes): direct sum
+template <typename R>
+__global__ void k_expect_small(const cplx<R>* __restrict__ s, uint64_t len, MaskSet ms, int nm, double* out) {
+  const int k = threadIdx.x;
+  if (k >= nm) return;
+  double acc = 0.0;
+  for (uint64_t i = 0; i < len; ++i) {
+    const double x = (double)s[i].x, y = (double)s[i].y;
+    const double p = x * x + y * y;
+    acc += (__popcll(i & ms.m[k]) & 1) ? -p : p;
+  }
+  out[k] = acc;
 }
 
 size_t expect_ws_doubles(int n, int m) {
@@ -168,7 +218,12 @@ void launch_expect_z(const void* state, int n, const uint64_t* h_masks, int m, d
     int nm = m - b < kMaskBatch ? m - b : kMaskBatch;
     MaskSet ms;
     for (int j = 0; j < kMaskBatch; ++j) ms.m[j] = j < nm ? h_masks[b + j] : 0;
-    k_expect_partial<R><<<G, 256, 0, st>>>(s, len, ms, nm, d_ws);
+    if (len < 512) {
+      k_expect_small<R><<<1, 32, 0, st>>>(s, len, ms, nm, d_out + b);
+      SVB_CHECK_LAUNCH();
+      continue;
+    }
+    k_expect_partial<R><<<G, 256, 0, st>>>(s, len / 512, ms, nm, d_ws);
     SVB_CHECK_LAUNCH();
     k_sum_rows<<<(nm + 255) / 256, 256, 0, st>>>(d_ws, nm, G, d_out + b);
     SVB_CHECK_LAUNCH();

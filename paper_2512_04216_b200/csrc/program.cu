@@ -17,6 +17,7 @@
 //  5. rounds: consecutive ops whose active qubits fit in RB register bits.
 #include <algorithm>
 #include <cstddef>
+#include <cmath>
 #include <complex>
 #include <cstring>
 #include <vector>
@@ -87,7 +88,20 @@ void left_mul_2q(Block& b, int qa, int qb, const cd* g) {
   std::copy(r, r + 16, b.M);
 }
 
-void emit_block(const Block& b, std::vector<FOp>& out) {
+// Fused products of exact gates pick up 1-ulp noise (e^{-it/2} e^{it/2} may
+// round to 1 - 2^-53): snap such entries back to exactly 1 / 0 so the diagonal
+// and trivial-factor structure is recognised (error <= 2^-50 per entry).
+inline cd snap(cd z) {
+  const double t = 0x1p-50;
+  double re = z.real(), im = z.imag();
+  if (std::fabs(re - 1.0) <= t && std::fabs(im) <= t) return cd(1.0, 0.0);
+  if (std::fabs(re) <= t * 1e-3 && std::fabs(im) <= t * 1e-3) return cd(0.0, 0.0);
+  return z;
+}
+
+void emit_block(const Block& b0, std::vector<FOp>& out) {
+  Block b = b0;
+  for (int e = 0; e < (b.k == 1 ? 4 : 16); ++e) b.M[e] = snap(b.M[e]);
   if (b.k == 1) {
     FOp f;
     f.q[0] = b.q[0];
