@@ -46,7 +46,7 @@ __host__ __device__ __forceinline__ uint64_t insert0(uint64_t i, int q) {
   return ((i >> q) << (q + 1)) | lo;
 }
 
-enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5 };
+enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5, OP_U1X = 6 };
 
 // Every op: header, then a kind-specific payload.  `bytes` = total size
 // (multiple of 16).  Condition: the op applies where
@@ -133,6 +133,20 @@ SVB_HD void u1_real(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval)
     const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
     a[v] = mk<R>(fma(m1, x1.x, m0 * x0.x), fma(m1, x1.y, m0 * x0.y));
     a[v | (1 << B)] = mk<R>(fma(m3, x1.x, m2 * x0.x), fma(m3, x1.y, m2 * x0.y));
+  }
+}
+
+// [[a, i b], [i c, d]] with a, b, c, d real (rx-like: sqrt(X), rx(t)): 4 FMA per output
+template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_rx(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
+  const R ma = ldc<R>(m).x, mb = ldc<R>(m + 1).y, mc = ldc<R>(m + 2).y, md = ldc<R>(m + 3).x;
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & (1 << B)) continue;
+    if (COND && (v & rmask) != rval) continue;
+    const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+    a[v] = mk<R>(fma(-mb, x1.y, ma * x0.x), fma(mb, x1.x, ma * x0.y));
+    a[v | (1 << B)] = mk<R>(fma(-mc, x0.y, md * x1.x), fma(mc, x0.x, md * x1.y));
   }
 }
 
@@ -318,8 +332,15 @@ SVB_HD void u1_anti_v(cplx<R>* a, cplx<R> m1, cplx<R> m2, uint32_t rmask, uint32
 }
 
 template <typename R, int RB, int B, bool COND>
+SVB_HD void u1_rx_v(cplx<R>* a, R ma, R mb, R mc, R md, uint32_t rmask, uint32_t rval) {
+  const cplx<R> m[4] = {mk<R>(ma, R(0)), mk<R>(R(0), mb), mk<R>(R(0), mc), mk<R>(md, R(0))};
+  u1_rx<R, RB, B, COND>(a, m, rmask, rval);
+}
+
+template <typename R, int RB, int B, bool COND>
 SVB_HD void u1_kind(int kind, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
   if (kind == OP_U1R) u1_real<R, RB, B, COND>(a, m, rmask, rval);
+  else if (kind == OP_U1X) u1_rx<R, RB, B, COND>(a, m, rmask, rval);
   else if (kind == OP_U1) u1_dense<R, RB, B, COND>(a, m, rmask, rval);
   else u1_anti<R, RB, B, COND>(a, m, rmask, rval);
 }
@@ -397,6 +418,7 @@ SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, u
         break;
       case OP_U1:
       case OP_U1R:
+      case OP_U1X:
       case OP_U1ANTI:
         dispatch_u1<R, RB>(w0.x, w0.y, a, reinterpret_cast<const cplx<R>*>(payload), w2.x, w2.y);
         break;
@@ -481,6 +503,11 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 }
 
 constexpr int kStages = 2;
+// Register bits per thread and threads per CTA of the pass kernel:
+// complex128: 16 amplitudes x 256 threads (m = 12); complex64: 16 x 512 (m = 13),
+// i.e. twice the warps per SM for the cheaper type.
+template <typename R> constexpr int kRegBits = 4;
+template <typename R> constexpr int kPassThreads = sizeof(R) == 8 ? 256 : 512;
 
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
 
@@ -632,10 +659,27 @@ __device__ __forceinline__ void mul_half(cplx<R>* a, cplx<R> d) {  // a[v] *= d 
   for (int v = 0; v < (1 << RB); ++v)
     if (v & (1 << I)) a[v] = cmul<R>(a[v], d);
 }
+template <typename R, int RB, int I>
+__device__ __forceinline__ void mul_half_r(cplx<R>* a, R d) {  // real factor (e.g. cz signs)
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v)
+    if (v & (1 << I)) a[v] = mk<R>(a[v].x * d, a[v].y * d);
+}
+template <typename R, int RB>
+__device__ __forceinline__ void mul_all_r(cplx<R>* a, R d) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) a[v] = mk<R>(a[v].x * d, a[v].y * d);
+}
 template <typename R, int RB>
 __device__ __forceinline__ void mul_all(cplx<R>* a, cplx<R> d) {
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v) a[v] = cmul<R>(a[v], d);
+}
+template <typename R, int RB, int IA, int IB, int Q>
+__device__ __forceinline__ void neg_quad(cplx<R>* a) {  // factor exactly -1 (cz)
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v)
+    if ((((v >> IA) & 1) + 2 * ((v >> IB) & 1)) == Q) a[v] = mk<R>(-a[v].x, -a[v].y);
 }
 template <typename R, int RB, int IA, int IB, int Q>
 __device__ __forceinline__ void mul_quad(cplx<R>* a, cplx<R> d) {  // amps with bit(IA) + 2 bit(IB) == Q
@@ -777,7 +821,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
 }
 
 template <typename R, int RB>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kPassThreads<R>, 1)
     k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
            uint32_t ntiles) {
   pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles);

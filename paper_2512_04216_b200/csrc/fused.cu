@@ -160,7 +160,7 @@ void Profiler::collect() {
 }
 
 // ------------------------------------------------------------ run_program
-template <typename R> static constexpr int rb_of() { return sizeof(R) == 8 ? 4 : 5; }
+template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
 template <typename R>
 static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats,

@@ -119,15 +119,21 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
   std::memcpy(&h, payload, sizeof h);
   const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
   bool d0one[8], d1one[8], cone = true;
-  for (int i = 0; i < RB; ++i) d0one[i] = d1one[i] = true;
+  bool d0real[8], d1real[8], creal = true;  // every contributing entry real
+  for (int i = 0; i < RB; ++i) d0one[i] = d1one[i] = d0real[i] = d1real[i] = true;
   const DiagTerm<R>* u = t;
   for (int i = 0; i < RB; ++i)
     for (int k = 0; k < h.nUR[i]; ++k, ++u) {
       if (!is1(u->d[0]) || !is1(u->d[2])) d0one[i] = false;
       if (!is1(u->d[1]) || !is1(u->d[3])) d1one[i] = false;
+      if (u->d[0].y != 0 || u->d[2].y != 0) d0real[i] = false;
+      if (u->d[1].y != 0 || u->d[3].y != 0) d1real[i] = false;
     }
   for (int k = 0; k < h.nUC; ++k, ++u)
-    for (int e = 0; e < 4; ++e) cone = cone && is1(u->d[e]);
+    for (int e = 0; e < 4; ++e) {
+      cone = cone && is1(u->d[e]);
+      creal = creal && u->d[e].y == 0;
+    }
   const DiagTerm<R>* tr = u;
   const DiagTerm<R>* tc = tr + h.nTR;
   const DiagTerm<R>* rr = tc + h.nTC;
@@ -135,9 +141,14 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
     const int i = tr[k].ra;
     if (!is1(tr[k].d[0]) || !is1(tr[k].d[2])) d0one[i] = false;
     if (!is1(tr[k].d[1]) || !is1(tr[k].d[3])) d1one[i] = false;
+    if (tr[k].d[0].y != 0 || tr[k].d[2].y != 0) d0real[i] = false;
+    if (tr[k].d[1].y != 0 || tr[k].d[3].y != 0) d1real[i] = false;
   }
   for (int k = 0; k < h.nTC; ++k)
-    for (int e = 0; e < 4; ++e) cone = cone && is1(tc[k].d[e]);
+    for (int e = 0; e < 4; ++e) {
+      cone = cone && is1(tc[k].d[e]);
+      creal = creal && tc[k].d[e].y == 0;
+    }
   o << "    {\n";
   const std::string us = "c.uni + " + std::to_string(h.slot * kUniStride);
   const bool has_uc = h.slot >= 0 && h.nUC > 0;
@@ -170,9 +181,13 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
   }
   for (int k = 0; k < h.nRR; ++k)  // only the quadrants whose factor is not exactly 1
     for (int q = 0; q < 4; ++q)
-      if (!is1(rr[k].d[q]))
-        o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
-          << cimm<R>(rr[k].d[q]) << ");\n";
+      if (!is1(rr[k].d[q])) {
+        if (rr[k].d[q].x == -1 && rr[k].d[q].y == 0)
+          o << "      svb::neg_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a);\n";
+        else
+          o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
+            << cimm<R>(rr[k].d[q]) << ");\n";
+      }
   // fold D0 into C (unit-modulus entries: 1/D0 = conj(D0)), then apply
   bool need_c = !cone;
   for (int i = 0; i < RB; ++i)
@@ -182,15 +197,25 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
         need_c = true;
       }
       o << "      C = svb::cmul<R>(C, D0_" << i << ");\n";
-      if (!d1one[i]) o << "      D1_" << i << " = svb::conj_mul<R>(D1_" << i << ", D0_" << i << ");\n";
-      else {
+      creal = creal && d0real[i];
+      if (!d1one[i]) {
+        o << "      D1_" << i << " = svb::conj_mul<R>(D1_" << i << ", D0_" << i << ");\n";
+        d1real[i] = d1real[i] && d0real[i];
+      } else {
         o << "      svb::cplx<R> D1_" << i << " = svb::mk<R>(D0_" << i << ".x, -D0_" << i << ".y);\n";
         d1one[i] = false;
+        d1real[i] = d0real[i];
       }
     }
-  if (need_c) o << "      svb::mul_all<R, RB>(a, C);\n";
+  if (need_c) {
+    if (creal) o << "      svb::mul_all_r<R, RB>(a, C.x);\n";
+    else o << "      svb::mul_all<R, RB>(a, C);\n";
+  }
   for (int i = 0; i < RB; ++i)
-    if (!d1one[i]) o << "      svb::mul_half<R, RB, " << i << ">(a, D1_" << i << ");\n";
+    if (!d1one[i]) {
+      if (d1real[i]) o << "      svb::mul_half_r<R, RB, " << i << ">(a, D1_" << i << ".x);\n";
+      else o << "      svb::mul_half<R, RB, " << i << ">(a, D1_" << i << ");\n";
+    }
   o << "    }\n";
 }
 
@@ -228,6 +253,12 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB) {
           o << "    " << guard << "svb::u1_real_v<R, RB, " << h.a << ", " << cond << ">(a, "
             << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].x, sizeof(R) == 4) << ", "
             << hexf((double)coef[2].x, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
+            << rm << ");\n";
+          break;
+        case OP_U1X:
+          o << "    " << guard << "svb::u1_rx_v<R, RB, " << h.a << ", " << cond << ">(a, "
+            << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].y, sizeof(R) == 4) << ", "
+            << hexf((double)coef[2].y, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
             << rm << ");\n";
           break;
         case OP_U1:
@@ -272,7 +303,7 @@ bool jit_available() {
 
 // Source of one pass kernel (skeleton + straight-line body).
 template <typename R> std::string jit_source_pass(const Program& prog, int p) {
-  constexpr int RB = sizeof(R) == 8 ? 4 : 5;
+  constexpr int RB = kRegBits<R>;
   std::ostringstream o;
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
   o << "struct PassBody {\n  template <typename R, int RB>\n"
@@ -281,7 +312,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p) {
        "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    switch (0) {\n";
   emit_body<R>(o, prog, p, RB);
   o << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(256, 1) svb_jit(svb::cplx<R>* __restrict__ state, "
+  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", 1) svb_jit(svb::cplx<R>* __restrict__ state, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass) {\n"
        "  svb::pass_kernel<R, "
     << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass);\n}\n";
@@ -343,7 +374,7 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
                        cudaStream_t st, ProgramStats* stats, int nsm) {
   static Driver dr;
   if (!dr.ok || prog.passes.empty()) return false;
-  constexpr int RB = sizeof(R) == 8 ? 4 : 5;
+  constexpr int RB = kRegBits<R>;
   int dev = 0;
   SVB_CUDA(cudaGetDevice(&dev));
   const size_t np = prog.passes.size();

@@ -116,6 +116,8 @@ void emit_block(const Block& b0, std::vector<FOp>& out) {
       f.type = (zero(M[0]) && zero(M[3])) ? OP_U1ANTI : OP_U1;
       if (f.type == OP_U1 && M[0].imag() == 0 && M[1].imag() == 0 && M[2].imag() == 0 && M[3].imag() == 0)
         f.type = OP_U1R;
+      else if (f.type == OP_U1 && M[0].imag() == 0 && M[3].imag() == 0 && M[1].real() == 0 && M[2].real() == 0)
+        f.type = OP_U1X;
       std::copy(M, M + 4, f.c);
       f.active = f.touched;
     }
@@ -167,6 +169,8 @@ void emit_block(const Block& b0, std::vector<FOp>& out) {
       f.type = (zero(U[0]) && zero(U[3])) ? OP_U1ANTI : OP_U1;
       if (f.type == OP_U1 && U[0].imag() == 0 && U[1].imag() == 0 && U[2].imag() == 0 && U[3].imag() == 0)
         f.type = OP_U1R;
+      else if (f.type == OP_U1 && U[0].imag() == 0 && U[3].imag() == 0 && U[1].real() == 0 && U[2].real() == 0)
+        f.type = OP_U1X;
       f.q[0] = tgt; f.q[1] = -1;
       std::copy(U, U + 4, f.c);
       f.conds.push_back({ctl, v});
@@ -464,7 +468,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
           i = j;
           continue;
         }
-        if (f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1ANTI) {
+        if (f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X || f.type == OP_U1ANTI) {
           uint64_t fm = 0, fv = 0;
           uint32_t rm = 0, rv = 0;
           for (auto& cv : f.conds) {
@@ -578,7 +582,7 @@ template void emulate_program<double>(cplx<double>*, int, const Program&);
 SchedOptions default_options(int precision, int n) {
   SchedOptions o;
   if (precision == SVB_C128) { o.rb = 4; o.m = 12; }
-  else { o.rb = 5; o.m = 13; }
+  else { o.rb = kRegBits<float>; o.m = 13; }
   return o;
 }
 
