@@ -75,7 +75,7 @@ int svb_host_free(void* p);
 typedef enum {
   SVB_OPT_FUSION = 0,   /* 1 (default): fused multi-gate HBM passes; 0: one pass per gate */
   SVB_OPT_MAX_HIGH = 1,  /* fused pass: max non-lane qubits per pass (tuning; default auto) */
-  SVB_OPT_JIT_MIN_N = 2  /* NVRTC-specialise fused passes for n >= value (default 20; -1 never) */
+  SVB_OPT_JIT_MIN_N = 2  /* NVRTC-specialise fused passes for n >= value (default 24; -1 never) */
 } svb_option;
 int svb_set_option(svb_handle h, int option, int value);
 /* Statistics of the last svb_apply: HBM passes launched, gates applied. */

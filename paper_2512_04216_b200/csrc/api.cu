@@ -26,7 +26,7 @@ struct svb_state {
   double* d_ws = nullptr;        // reduction scratch
   size_t ws_doubles = 0;
   int fusion = 1, max_high = -1;
-  int jit_min_n = 20;  // NVRTC-specialised passes from this many qubits up (-1: never)
+  int jit_min_n = 24;  // NVRTC-specialised passes from this many qubits up (-1: never)
   ProgramStats stats{};
   Profiler prof;
   cudaEvent_t t0 = nullptr, t1 = nullptr;

@@ -114,7 +114,14 @@ template <typename C> bool is1(const C& z) { return z.x == 1 && z.y == 0; }
 // with immediates, and factors that are exactly 1 by construction are dropped
 // at generation time (controlled phases leave half the amplitudes untouched).
 template <typename R>
-void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
+void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, int RB, bool imm) {
+  // factor e of a term: an immediate (large programs) or a load from the op
+  // payload in shared memory (structure-only code shared across angles)
+  auto dref = [&](const void* term, int e) {
+    if (imm) return cimm<R>(reinterpret_cast<const DiagTerm<R>*>(term)->d[e]);
+    const uint32_t addr = pay_off + (uint32_t)((const uint8_t*)term - payload) + 16 + e * (uint32_t)sizeof(cplx<R>);
+    return "reinterpret_cast<const svb::cplx<R>*>(c.ops + " + std::to_string(addr) + ")[0]";
+  };
   DiagHdr h;
   std::memcpy(&h, payload, sizeof h);
   const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
@@ -167,8 +174,8 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
     const bool t0 = is1(tr[k].d[0]) && is1(tr[k].d[2]), t1 = is1(tr[k].d[1]) && is1(tr[k].d[3]);
     if (t0 && t1) continue;
     o << "      { const int f = (int)((Fg >> " << qb << ") & 1ull);";
-    if (!t0) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[0]) << ", " << cimm<R>(tr[k].d[2]) << "));";
-    if (!t1) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << cimm<R>(tr[k].d[1]) << ", " << cimm<R>(tr[k].d[3]) << "));";
+    if (!t0) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << dref(tr + k, 0) << ", " << dref(tr + k, 2) << "));";
+    if (!t1) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << dref(tr + k, 1) << ", " << dref(tr + k, 3) << "));";
     o << " }\n";
   }
   for (int k = 0; k < h.nTC; ++k) {
@@ -176,8 +183,8 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
     const std::string fa = qa >= 0 ? "(int)((Fg >> " + std::to_string(qa) + ") & 1ull)" : "0";
     const std::string fb = qb >= 0 ? "(int)((Fg >> " + std::to_string(qb) + ") & 1ull)" : "0";
     o << "      { const int fa = " << fa << ", fb = " << fb << "; C = svb::cmul<R>(C, fb ? svb::csel<R>(fa, "
-      << cimm<R>(tc[k].d[2]) << ", " << cimm<R>(tc[k].d[3]) << ") : svb::csel<R>(fa, " << cimm<R>(tc[k].d[0])
-      << ", " << cimm<R>(tc[k].d[1]) << ")); }\n";
+      << dref(tc + k, 2) << ", " << dref(tc + k, 3) << ") : svb::csel<R>(fa, " << dref(tc + k, 0)
+      << ", " << dref(tc + k, 1) << ")); }\n";
   }
   for (int k = 0; k < h.nRR; ++k)  // only the quadrants whose factor is not exactly 1
     for (int q = 0; q < 4; ++q)
@@ -186,7 +193,7 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
           o << "      svb::neg_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a);\n";
         else
           o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
-            << cimm<R>(rr[k].d[q]) << ");\n";
+            << dref(rr + k, q) << ");\n";
       }
   // fold D0 into C (unit-modulus entries: 1/D0 = conj(D0)), then apply
   bool need_c = !cone;
@@ -221,7 +228,7 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, int RB) {
 
 // Emit the straight-line Body of one pass.
 template <typename R>
-void emit_body(std::ostringstream& o, const Program& prog, int p, int RB) {
+void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool imm) {
   const PassDev& pd = prog.passes[p];
   o << "    case " << p << ": {\n";
   for (int k = 0; k < pd.nrounds; ++k) {
@@ -247,29 +254,28 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB) {
       const std::string rm = std::to_string(h.rmask) + "u, " + std::to_string(h.rval) + "u";
       switch (h.kind) {
         case OP_DIAG:
-          emit_diag<R>(o, prog.ops.data() + pay, RB);
+          emit_diag<R>(o, prog.ops.data() + pay, pay, RB, imm);
           break;
         case OP_U1R:
-          o << "    " << guard << "svb::u1_real_v<R, RB, " << h.a << ", " << cond << ">(a, "
-            << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].x, sizeof(R) == 4) << ", "
-            << hexf((double)coef[2].x, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
-            << rm << ");\n";
-          break;
+          if (imm) {
+            o << "    " << guard << "svb::u1_real_v<R, RB, " << h.a << ", " << cond << ">(a, "
+              << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].x, sizeof(R) == 4) << ", "
+              << hexf((double)coef[2].x, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
+              << rm << ");\n";
+            break;
+          }
+          [[fallthrough]];
         case OP_U1X:
-          o << "    " << guard << "svb::u1_rx_v<R, RB, " << h.a << ", " << cond << ">(a, "
-            << hexf((double)coef[0].x, sizeof(R) == 4) << ", " << hexf((double)coef[1].y, sizeof(R) == 4) << ", "
-            << hexf((double)coef[2].y, sizeof(R) == 4) << ", " << hexf((double)coef[3].x, sizeof(R) == 4) << ", "
-            << rm << ");\n";
-          break;
         case OP_U1:
-          o << "    " << guard << "svb::u1_dense_v<R, RB, " << h.a << ", " << cond << ">(a, " << cimm<R>(coef[0])
-            << ", " << cimm<R>(coef[1]) << ", " << cimm<R>(coef[2]) << ", " << cimm<R>(coef[3]) << ", " << rm
-            << ");\n";
+        case OP_U1ANTI: {
+          // structure-only: coefficients stay in the op payload (shared memory), so
+          // circuits that differ only in angles share one compiled kernel
+          const char* fn = h.kind == OP_U1R ? "u1_real" : h.kind == OP_U1X ? "u1_rx" : h.kind == OP_U1 ? "u1_dense" : "u1_anti";
+          o << "    " << guard << "svb::" << fn << "<R, RB, " << h.a << ", " << cond
+            << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
+          (void)coef;
           break;
-        case OP_U1ANTI:
-          o << "    " << guard << "svb::u1_anti_v<R, RB, " << h.a << ", " << cond << ">(a, " << cimm<R>(coef[1])
-            << ", " << cimm<R>(coef[2]) << ", " << rm << ");\n";
-          break;
+        }
         case OP_U2:
           o << "    " << guard << "svb::u2_dense<R, RB, " << h.a << ", " << h.b
             << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
@@ -302,6 +308,11 @@ bool jit_available() {
 }
 
 // Source of one pass kernel (skeleton + straight-line body).
+// Programs on at least this many qubits get coefficients as immediates (a
+// one-off compile is negligible next to their passes); smaller ones get
+// structure-only code that circuits differing only in angles share.
+constexpr int kImmMinQubits = 28;
+
 template <typename R> std::string jit_source_pass(const Program& prog, int p) {
   constexpr int RB = kRegBits<R>;
   std::ostringstream o;
@@ -310,7 +321,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p) {
        "  __device__ static __forceinline__ void tile(int pass, const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
        "svb::cplx<R>* cur, uint64_t base) {\n"
        "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    switch (0) {\n";
-  emit_body<R>(o, prog, p, RB);
+  const PassDev& pd0 = prog.passes[p];
+  emit_body<R>(o, prog, p, RB, pd0.m + pd0.nout >= kImmMinQubits);
   o << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", 1) svb_jit(svb::cplx<R>* __restrict__ state, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass) {\n"

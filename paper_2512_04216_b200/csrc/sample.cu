@@ -190,29 +190,61 @@ static void cub_inclusive_sum(const double* in, double* out, uint64_t n, cudaStr
 
 // np.cumsum is a left-to-right accumulation; ties between deficit and capacity
 // prefixes are common (symmetric distributions), so the alias build reproduces
-// it exactly: one thread runs the dependent add chain while the loads stream.
-__global__ void k_seq_cumsum(const double* __restrict__ in, double* __restrict__ out, uint64_t n) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  double acc = 0.0;
-  uint64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double x[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = in[i + k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      acc += x[k];
-      out[i + k] = acc;
+// it exactly.  One block: all threads stream 2048-element chunks into shared
+// memory (double-buffered cp.async, coalesced) while thread 0 runs the
+// dependent add chain out of shared memory; results leave coalesced.
+constexpr int kSeqChunk = 2048;
+
+__device__ __forceinline__ void seq_stage(const double* __restrict__ in, uint64_t n, uint64_t c0, double* buf) {
+  for (uint32_t j = threadIdx.x; j < (uint32_t)kSeqChunk; j += blockDim.x) {
+    const uint64_t i = c0 + j;
+    if (i < n) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(buf + j);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(in + i) : "memory");
     }
   }
-  for (; i < n; ++i) {
-    acc += in[i];
-    out[i] = acc;
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// mode 0: out = inclusive running sum (cumsum); mode 1: *total = sum (bincount bin)
+__device__ void seq_block(const double* __restrict__ in, uint64_t n, double* __restrict__ out, double* total) {
+  __shared__ double buf[2][kSeqChunk];
+  __shared__ double acc_s;
+  if (threadIdx.x == 0) acc_s = 0.0;
+  const uint64_t nch = (n + kSeqChunk - 1) / kSeqChunk;
+  if (nch) seq_stage(in, n, 0, buf[0]);
+  for (uint64_t c = 0; c < nch; ++c) {
+    if (c + 1 < nch) seq_stage(in, n, (c + 1) * kSeqChunk, buf[(c + 1) & 1]);
+    else asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    double* b = buf[c & 1];
+    const uint64_t c0 = c * kSeqChunk;
+    const uint32_t len = (uint32_t)((n - c0) < (uint64_t)kSeqChunk ? (n - c0) : kSeqChunk);
+    if (threadIdx.x == 0) {
+      double acc = acc_s;
+      for (uint32_t j = 0; j < len; ++j) {
+        acc += b[j];
+        b[j] = acc;
+      }
+      acc_s = acc;
+    }
+    __syncthreads();
+    if (out)
+      for (uint32_t j = threadIdx.x; j < len; j += blockDim.x) out[c0 + j] = b[j];
+    __syncthreads();
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (total && threadIdx.x == 0) *total = acc_s;
+}
+
+__global__ void __launch_bounds__(256) k_seq_cumsum(const double* __restrict__ in, double* __restrict__ out,
+                                                    uint64_t n) {
+  seq_block(in, n, out, nullptr);
 }
 
 static void seq_cumsum(const double* in, double* out, uint64_t n, cudaStream_t st) {
-  k_seq_cumsum<<<1, 1, 0, st>>>(in, out, n);
+  k_seq_cumsum<<<1, 256, 0, st>>>(in, out, n);
   SVB_CHECK_LAUNCH();
 }
 
@@ -295,17 +327,39 @@ __global__ void k_run_starts(const int64_t* __restrict__ head, const int64_t* __
     if (head[i]) starts[hpos[i]] = (int64_t)i;
 }
 // np.bincount(owner, weights=deficits): each bin sums its weights sequentially
-// from 0.0 in index order — reproduced exactly, one thread per run.
+// from 0.0 in index order — reproduced exactly.  Runs shorter than kLongRun: one
+// thread each; longer runs are listed and summed block-cooperatively.
+constexpr uint64_t kLongRun = 1024;
+
 __global__ void k_absorb(const int64_t* __restrict__ starts, uint64_t nruns, uint64_t ns,
                          const int64_t* __restrict__ owner, const double* __restrict__ deficit,
-                         double* __restrict__ rem) {
+                         double* __restrict__ rem, uint64_t* __restrict__ long_runs, unsigned long long* n_long) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nruns; r += stride) {
     const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
+    if (e - b >= kLongRun) {
+      long_runs[atomicAdd(n_long, 1ull)] = r;
+      continue;
+    }
     double acc = 0.0;
     for (uint64_t i = b; i < e; ++i) acc += deficit[i];
     const int64_t o = owner[b];
     rem[o] = rem[o] - acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_absorb_long(const int64_t* __restrict__ starts, uint64_t nruns, uint64_t ns,
+                                                     const int64_t* __restrict__ owner,
+                                                     const double* __restrict__ deficit, double* __restrict__ rem,
+                                                     const uint64_t* __restrict__ long_runs) {
+  __shared__ double tot;
+  const uint64_t r = long_runs[blockIdx.x];
+  const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
+  seq_block(deficit + b, e - b, nullptr, &tot);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t o = owner[b];
+    rem[o] = rem[o] - tot;
   }
 }
 
@@ -365,6 +419,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
   DevBuf deficit(sizeof(double) * ns, st), dcum(sizeof(double) * ns, st), owner(sizeof(int64_t) * ns, st);
   DevBuf cap(sizeof(double) * nl, st), ccum(sizeof(double) * nl, st);
   DevBuf head(sizeof(int64_t) * ns, st), hpos(sizeof(int64_t) * ns, st), starts(sizeof(int64_t) * ns, st);
+  DevBuf long_runs(sizeof(uint64_t) * (ns / kLongRun + 2), st), nlong(sizeof(unsigned long long), st);
   DevBuf conv(sizeof(int64_t) * nl, st), cpos(sizeof(int64_t) * nl, st);
   DevBuf larges2(sizeof(int64_t) * nl, st), rem2(sizeof(double) * nl, st);
   int64_t* L = larges.as<int64_t>();
@@ -390,8 +445,17 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     SVB_CHECK_LAUNCH();
     const uint64_t nruns = (uint64_t)d2h_scalar(hpos.as<int64_t>() + (ns - 1), st) +
                            (uint64_t)d2h_scalar(head.as<int64_t>() + (ns - 1), st);
+    SVB_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(unsigned long long), st));
     k_absorb<<<grid_for(nruns, 64), 64, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
-                                                 deficit.as<double>(), Rm);
+                                                 deficit.as<double>(), Rm, long_runs.as<uint64_t>(),
+                                                 nlong.as<unsigned long long>());
+    SVB_CHECK_LAUNCH();
+    const unsigned long long nl_runs = d2h_scalar(nlong.as<unsigned long long>(), st);
+    if (nl_runs) {
+      k_absorb_long<<<(unsigned)nl_runs, 256, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
+                                                       deficit.as<double>(), Rm, long_runs.as<uint64_t>());
+      SVB_CHECK_LAUNCH();
+    }
     k_conv_flags<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, conv.as<int64_t>());
     SVB_CHECK_LAUNCH();
     cub_exclusive_sum(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);

@@ -253,6 +253,49 @@ class PinnedBuffer:
             pass
 
 
+class _StatePool:
+    """Idle device states kept for reuse by run() (small circuits pay no
+    cudaMalloc / stream creation per call).  Bounded by bytes; LIFO per key."""
+
+    def __init__(self, cap_bytes: int = 8 << 30, per_key: int = 2):
+        self.cap = cap_bytes
+        self.per_key = per_key
+        self.idle: dict = {}
+        self.bytes = 0
+
+    @staticmethod
+    def _size(n, precision):
+        return (16 if precision == "c128" else 8) << n
+
+    def acquire(self, n: int, precision: str, device: int) -> DeviceState:
+        key = (n, "c128" if _prec_code(precision) == _lib.SVB_C128 else "c64", device)
+        lst = self.idle.get(key)
+        if lst:
+            self.bytes -= self._size(n, key[1])
+            return lst.pop()
+        return DeviceState(n, precision, device)
+
+    def release(self, st: DeviceState) -> None:
+        key = (st.n, st.precision, st.device)
+        size = self._size(st.n, st.precision)
+        lst = self.idle.setdefault(key, [])
+        if len(lst) >= self.per_key or self.bytes + size > self.cap:
+            st.close()
+            return
+        lst.append(st)
+        self.bytes += size
+
+    def clear(self) -> None:
+        for lst in self.idle.values():
+            for st in lst:
+                st.close()
+        self.idle.clear()
+        self.bytes = 0
+
+
+_pool = _StatePool()
+
+
 def _device_of(amps, n):
     """numpy array -> temporary DeviceState (kernel-level API); DeviceState -> itself."""
     if isinstance(amps, DeviceState):
@@ -368,8 +411,9 @@ def run(
     n = c.n_qubits
     meta: dict = {"engine": "libsvb", "precision": precision}
     if terminal_measurement_only(c):
-        state = DeviceState(n, precision, device)
+        state = _pool.acquire(n, precision, device)
         try:
+            state.zero()
             state.apply_instructions(c.instructions)
             meta.update(state.stats())
             qubits = sorted({q for q, _ in measures})
@@ -378,7 +422,7 @@ def run(
             meta["sampler"] = "alias" if mode == _lib.SAMPLER_ALIAS else "cdf"
             codes, freq = state.sample_codes(qubits, src, shots, pcg_words(seed), mode)
         finally:
-            state.close()
+            _pool.release(state)
         counts = format_counts(codes, freq, len(src))
     else:
         counts = _run_replay(c, shots, seed, workers, precision, device, meta)
@@ -392,9 +436,10 @@ def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
     insts = c.instructions
     split = next(i for i, x in enumerate(insts) if x.kind in ("measure", "reset"))
     n = c.n_qubits
-    prefix = DeviceState(n, precision, device)
-    work = DeviceState(n, precision, device)
+    prefix = _pool.acquire(n, precision, device)
+    work = _pool.acquire(n, precision, device)
     try:
+        prefix.zero()
         prefix.apply_instructions(insts[:split])
         suffix = [x for x in insts[split:] if x.kind != "barrier"]
         clbits = clbit_order([(x.qubits[0], x.clbit) for x in suffix if x.kind == "measure"])
@@ -430,8 +475,8 @@ def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
             all_codes.append(codes)
         meta["replay_shots"] = shots
     finally:
-        prefix.close()
-        work.close()
+        _pool.release(prefix)
+        _pool.release(work)
     codes, freq = np.unique(np.concatenate(all_codes), return_counts=True)
     return format_counts(codes, freq, len(clbits))
 
