@@ -143,6 +143,16 @@ int svb_sample_slice(svb_handle h, uint64_t shots, const uint64_t* pcg, double l
                      const int32_t* bit_src, int w, uint64_t code_or, uint64_t* out_codes, uint64_t* out_counts,
                      uint64_t* n_unique);
 
+/* Batched terminal circuits that fit in shared memory (n <= 12 complex128,
+ * n <= 13 complex64): one persistent kernel, state per CTA in shared memory,
+ * CDF sampling from each circuit's PCG64 stream (replaces the sequential
+ * batch.run_batch loop, batch.py:104-222, for small circuits).  Circuit i:
+ * nq[i] qubits, gates[gate_off[i] .. +ngates[i]), pcg[4i..4i+3], w[i] output
+ * bits with sources bit_src[64i + p]; codes to out_codes[shots*i + s]. */
+int svb_batch_small(int device, int precision, int ncirc, const int32_t* nq, const int32_t* gate_off,
+                    const int32_t* ngates, const svb_gate* gates, int total_gates, const uint64_t* pcg,
+                    const int32_t* w, const int8_t* bit_src, uint64_t shots, uint64_t* out_codes);
+
 /* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
  * device; each measure/reset consumes one draw, exactly as rng.random(). */
 int svb_rng_seed(svb_handle h, const uint64_t* pcg);

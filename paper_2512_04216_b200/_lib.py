@@ -69,6 +69,8 @@ _SIGS = {
     "svb_sample": (c_int, [_h, _i32p, c_int, _i32p, c_int, c_uint64, _u64p, c_int, _u64p, _u64p, _u64p]),
     "svb_alias_table": (c_int, [c_int, _dp, c_uint64, _dp, _i64p]),
     "svb_rng_seed": (c_int, [_h, _u64p]),
+    "svb_batch_small": (c_int, [c_int, c_int, c_int, _i32p, _i32p, _i32p, c_void_p, c_int, _u64p, _i32p,
+                                POINTER(ctypes.c_int8), c_uint64, _u64p]),
     "svb_device_ptr": (c_int, [_h, POINTER(c_void_p), _u64p, _i64p]),
     "svb_half_copy": (c_int, [_h, c_int, c_int, c_void_p, c_int]),
     "svb_clear": (c_int, [_h]),

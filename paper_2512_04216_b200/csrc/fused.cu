@@ -15,6 +15,7 @@
 // 32-amplitude contiguous runs.
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -176,10 +177,15 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
     SVB_CUDA(cudaMemcpyAsync(dbuf + pbytes, prog.ops.data(), prog.ops.size(), cudaMemcpyHostToDevice, st));
   const PassDev* dpass = reinterpret_cast<const PassDev*>(dbuf);
   const uint8_t* dops = dbuf + pbytes;
-  size_t smem = 0;
-  for (const PassDev& pd : prog.passes)
-    smem = std::max(smem, kStages * (size_t)tile_bytes_of<R>(pd.m) + pd.ops_bytes);
-  SVB_CUDA(cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the attribute is per function and process-wide: set it once to the largest
+  // size any program can request (a per-call value would race between threads
+  // launching different programs)
+  static std::once_flag once_pass;
+  std::call_once(once_pass, [] {
+    const int cap = (int)(kStages * (size_t)tile_bytes_of<R>(kMaxM - 1) / 2 + kMaxPassOpBytes);
+    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         std::max(cap, (int)(kStages * (size_t)tile_bytes_of<R>(12 + (sizeof(R) == 4)) + kMaxPassOpBytes)));
+  });
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -215,7 +221,10 @@ static void launch_permute(cplx<R>** state, cplx<R>** spare, int n, const std::v
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = sizeof(cplx<R>) << pd.ml;
-  SVB_CUDA(cudaFuncSetAttribute(k_permute<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static std::once_flag once_perm;
+  std::call_once(once_perm, [] {
+    cudaFuncSetAttribute(k_permute<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(cplx<R>) << 12));
+  });
   const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * 3);
   Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
   if (pf) pf->begin(st, 1, 2.0 * (double)bytes);

@@ -465,7 +465,9 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);
     const unsigned smem = (unsigned)(kStages * (size_t)tile_bytes_of<R>(pd.m) + pd.ops_bytes);
     CUfunction f = fns[p];
-    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+    // per-function attribute: always the maximum (no race between threads)
+    const int cap = (int)(kStages * (size_t)tile_bytes_of<R>(12 + (sizeof(R) == 4)) + kMaxPassOpBytes);
+    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, cap) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
     cplx<R>* s = state;
     const PassDev* pdp = dpass + p;

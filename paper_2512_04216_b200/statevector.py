@@ -64,8 +64,8 @@ def pcg_words(seed_or_rng) -> np.ndarray:
 
 
 # ----------------------------------------------------------- gate encoding
-def gate_array(instructions) -> np.ndarray:
-    """Unitary instructions -> svb_gate records (matrices as in gates.py)."""
+def gate_array_slow(instructions) -> np.ndarray:
+    """Reference encoder: one matrix_of() per instruction (gates.py)."""
     insts = [i for i in instructions if i.kind in UNITARY_GATES]
     arr = np.zeros(len(insts), dtype=GATE_DTYPE)
     k = arr["k"]
@@ -77,6 +77,70 @@ def gate_array(instructions) -> np.ndarray:
         k[j] = nq
         q[j, :nq] = inst.qubits
         mat[j, : 2 * m.size] = m.reshape(-1).view(np.float64)
+    return arr
+
+
+_FIXED_MATS: dict = {}
+
+
+def gate_array(instructions) -> np.ndarray:
+    """Unitary instructions -> svb_gate records, vectorised per gate kind.
+
+    Same numbers as gates.py (math.cos/sin for rx/ry/u magnitudes, numpy's
+    complex exp for phases) — checked against gate_array_slow in the tests."""
+    insts = [i for i in instructions if i.kind in UNITARY_GATES]
+    n = len(insts)
+    arr = np.zeros(n, dtype=GATE_DTYPE)
+    if n == 0:
+        return arr
+    kinds = [i.kind for i in insts]
+    by_kind: dict = {}
+    for j, kd in enumerate(kinds):
+        by_kind.setdefault(kd, []).append(j)
+    mat = arr["mat"]
+    for kd, idx in by_kind.items():
+        idx = np.asarray(idx)
+        if kd in ("rx", "ry", "rz", "u"):
+            P = np.array([insts[j].params for j in idx], dtype=np.float64)
+            m = np.zeros((idx.size, 2, 2), dtype=np.complex128)
+            if kd == "rz":
+                m[:, 0, 0] = np.exp(-0.5j * P[:, 0])
+                m[:, 1, 1] = np.exp(0.5j * P[:, 0])
+            else:
+                import math as _m
+
+                c = np.array([_m.cos(t / 2) for t in P[:, 0]])
+                s_ = np.array([_m.sin(t / 2) for t in P[:, 0]])
+                if kd == "rx":
+                    m[:, 0, 0] = c
+                    m[:, 0, 1] = -1j * s_
+                    m[:, 1, 0] = -1j * s_
+                    m[:, 1, 1] = c
+                elif kd == "ry":
+                    m[:, 0, 0] = c
+                    m[:, 0, 1] = -s_
+                    m[:, 1, 0] = s_
+                    m[:, 1, 1] = c
+                else:
+                    phi, lam = P[:, 1], P[:, 2]
+                    m[:, 0, 0] = c
+                    m[:, 0, 1] = -np.exp(1j * lam) * s_
+                    m[:, 1, 0] = np.exp(1j * phi) * s_
+                    m[:, 1, 1] = np.exp(1j * (phi + lam)) * c
+            mat[idx, :8] = m.reshape(idx.size, 4).view(np.float64)
+        else:
+            if kd not in _FIXED_MATS:
+                from .gates import single_qubit_matrix, two_qubit_matrix
+
+                fm = two_qubit_matrix(kd) if kd in ("cx", "cz", "swap") else single_qubit_matrix(kd)
+                _FIXED_MATS[kd] = fm.reshape(-1).view(np.float64).copy()
+            fm = _FIXED_MATS[kd]
+            mat[idx, : fm.size] = fm
+    two = np.array([len(i.qubits) == 2 for i in insts])
+    arr["k"] = np.where(two, 2, 1)
+    arr["q"][:, 0] = [i.qubits[0] for i in insts]
+    if two.any():
+        arr["q"][two, 1] = [i.qubits[1] for i in insts if len(i.qubits) == 2]
     return arr
 
 
@@ -257,11 +321,14 @@ class _StatePool:
     """Idle device states kept for reuse by run() (small circuits pay no
     cudaMalloc / stream creation per call).  Bounded by bytes; LIFO per key."""
 
-    def __init__(self, cap_bytes: int = 8 << 30, per_key: int = 2):
+    def __init__(self, cap_bytes: int = 8 << 30, per_key: int = 4):
+        import threading
+
         self.cap = cap_bytes
         self.per_key = per_key
         self.idle: dict = {}
         self.bytes = 0
+        self.lock = threading.Lock()
 
     @staticmethod
     def _size(n, precision):
@@ -269,21 +336,23 @@ class _StatePool:
 
     def acquire(self, n: int, precision: str, device: int) -> DeviceState:
         key = (n, "c128" if _prec_code(precision) == _lib.SVB_C128 else "c64", device)
-        lst = self.idle.get(key)
-        if lst:
-            self.bytes -= self._size(n, key[1])
-            return lst.pop()
+        with self.lock:
+            lst = self.idle.get(key)
+            if lst:
+                self.bytes -= self._size(n, key[1])
+                return lst.pop()
         return DeviceState(n, precision, device)
 
     def release(self, st: DeviceState) -> None:
         key = (st.n, st.precision, st.device)
         size = self._size(st.n, st.precision)
-        lst = self.idle.setdefault(key, [])
-        if len(lst) >= self.per_key or self.bytes + size > self.cap:
-            st.close()
-            return
-        lst.append(st)
-        self.bytes += size
+        with self.lock:
+            lst = self.idle.setdefault(key, [])
+            if len(lst) < self.per_key and self.bytes + size <= self.cap:
+                lst.append(st)
+                self.bytes += size
+                return
+        st.close()
 
     def clear(self) -> None:
         for lst in self.idle.values():

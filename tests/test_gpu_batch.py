@@ -1,0 +1,78 @@
+"""Batch mode (config 4): persistent shared-memory kernel for small circuits,
+pooled fused-pass engine for the rest; per-circuit parity with the oracle."""
+import numpy as np
+import pytest
+
+from conftest import chisquare_pvalue
+from oracle import sv_oracle as orc
+from paper_2512_04216_b200 import suite
+from paper_2512_04216_b200 import statevector as sv
+from paper_2512_04216_b200.batch import run_batch
+from paper_2512_04216_b200.circuit import Circuit, Instruction
+from paper_2512_04216_b200.result import NoMeasurementsError, RunResult
+
+pytestmark = pytest.mark.gpu
+
+
+def _expected(c):
+    measures = [(i.qubits[0], i.clbit) for i in c.instructions if i.kind == "measure"]
+    qubits = tuple(sorted({q for q, _ in measures}))
+    psi = orc.unitary_state(c)
+    probs = orc.marginal_probs(psi, c.n_qubits, qubits)
+    src = {}
+    for q, cl in measures:
+        src[cl] = q
+    clbits = sorted(src)
+    pos = {q: j for j, q in enumerate(qubits)}
+    out = {}
+    for idx, p in enumerate(probs):
+        if p <= 1e-14:
+            continue
+        key = "".join(str((idx >> pos[src[cl]]) & 1) for cl in reversed(clbits))
+        out[key] = out.get(key, 0.0) + float(p)
+    return out
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_small_batch_matches_oracle(precision):
+    rng = np.random.default_rng(40)
+    circs = []
+    for i in range(30):
+        n = int(rng.integers(2, 13 if precision == "c128" else 14))
+        c = suite.random_circuit(n, int(rng.integers(5, 60)), rng)
+        circs.append(c)
+    c = Circuit(4, 3)  # subset + crossed clbits
+    c.gate("h", 0).gate("cx", 0, 2).gate("ry", 3, params=(0.4,)).measure(0, 2).measure(3, 0).measure(2, 1)
+    circs.append(c)
+    shots = 40000
+    res = run_batch(circs, shots=shots, seed=3, precision=precision)
+    for c, r in zip(circs, res):
+        assert isinstance(r, RunResult) and r.metadata["engine"] == "libsvb-batch-smem"
+        assert sum(r.counts.values()) == shots
+        assert chisquare_pvalue(r.counts, _expected(c), shots) > 1e-3
+
+
+def test_mixed_batch_routes_and_records_errors():
+    rng = np.random.default_rng(41)
+    circs = [suite.qaoa_line_circuit(n, 1, seed=n) for n in (8, 12, 14, 16)]
+    circs.append(suite.ry_ansatz_circuit(15, 2, seed=2))
+    mid = Circuit(3, 2)
+    mid.gate("h", 0).measure(0, 0).gate("x", 0).gate("h", 1).measure(1, 1)
+    circs.append(mid)
+    circs.append(Circuit(2).gate("h", 0))  # no measurements
+    res = run_batch(circs, shots=2000, seed=9)
+    assert isinstance(res[-1], NoMeasurementsError)
+    for c, r in zip(circs[:-1], res[:-1]):
+        assert isinstance(r, RunResult)
+        assert sum(r.counts.values()) == 2000
+    # circuits beyond shared memory take the regular path: identical to sv.run
+    for k in (2, 3, 4, 5):
+        assert res[k].counts == sv.run(circs[k], 2000, 9, sampler="cdf").counts
+
+
+def test_batch_workload_families_chi_square():
+    circs = suite.batch_workload(26)  # n = 12..24 QAOA / ry-ansatz (config 4 generator)
+    res = run_batch(circs[:13], shots=20000, seed=0)
+    for c, r in zip(circs[:13], res):
+        if c.n_qubits <= 16:
+            assert chisquare_pvalue(r.counts, _expected(c), 20000) > 1e-3, c.name
