@@ -179,6 +179,15 @@ int svb_emulate_apply(int n, int precision, const svb_gate* gates, int n_gates, 
 int svb_jit_check(int n, int precision, const svb_gate* gates, int n_gates, int64_t* cubin_bytes, char* log,
                   int log_cap);
 
+/* All shots of the mid-circuit replay in one launch for states that fit in
+ * shared memory (n <= 12 complex128 / 13 complex64); same op encoding and
+ * draw order as svb_replay (shot s uses draws [s*M, (s+1)*M)).  prefix is the
+ * complex128 prefix state on the host; ops[3k] as in svb_replay with the
+ * clbit operand already mapped to its output bit rank. */
+int svb_replay_small(int device, int precision, int n, const double* prefix_c128, const int32_t* ops, int n_ops,
+                     const svb_gate* gates, int n_gates, uint64_t shots, const uint64_t* pcg,
+                     uint64_t* out_codes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,8 @@ _SIGS = {
     "svb_measure": (c_int, [_h, c_int, _i32p]),
     "svb_reset": (c_int, [_h, c_int]),
     "svb_replay": (c_int, [_h, _h, _i32p, c_int, c_void_p, _i32p, c_uint64, _u64p, _u64p]),
+    "svb_replay_small": (c_int, [c_int, c_int, c_int, c_void_p, _i32p, c_int, c_void_p, c_int, c_uint64, _u64p,
+                                 _u64p]),
     "svb_plan": (c_int, [c_int, c_int, c_void_p, c_int, _i64p, _i64p, _i64p, _i32p]),
     "svb_emulate_apply": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, c_int]),
     "svb_jit_check": (c_int, [c_int, c_int, c_void_p, c_int, _i64p, ctypes.c_char_p, c_int]),

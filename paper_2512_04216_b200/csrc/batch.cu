@@ -246,3 +246,185 @@ extern "C" int svb_batch_small(int device, int precision, int ncirc, const int32
     return e.code;
   }
 }
+
+// ------------------------------------------------ mid-circuit replay (smem)
+// All shots of `_replay_shots` (statevector.py:157-179) for states that fit in
+// shared memory.  Shot s uses PCG64 draws [s*M, (s+1)*M) (M = measures +
+// resets in the suffix): the reference's single-stream order.  Ops: kind 0 =
+// gate (index), 1 = measure (qubit, clbit rank), 2 = reset (qubit).
+namespace svb {
+
+template <typename R>
+__device__ double block_sum_p1(const cplx<R>* st, uint32_t len, int q, double* red) {
+  double acc = 0.0;
+  for (uint32_t p = threadIdx.x; p < len / 2; p += blockDim.x) {
+    const uint32_t i = (uint32_t)insert0(p, q) | (1u << q);
+    const double x = (double)st[i].x, y = (double)st[i].y;
+    acc += x * x + y * y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31u) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+  for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];  // same order in every thread
+  __syncthreads();
+  return t;
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256, 1) k_replay_small(const cplx<R>* __restrict__ prefix, int n,
+                                                         const int32_t* __restrict__ ops, int nops,
+                                                         const BatchGate* __restrict__ gates, int M, uint64_t shots,
+                                                         uint64_t pcg0, uint64_t pcg1, uint64_t pcg2, uint64_t pcg3,
+                                                         uint64_t* __restrict__ codes) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cplx<R>* st = reinterpret_cast<cplx<R>*>(smraw);
+  __shared__ double red[8];
+  const uint32_t len = 1u << n, tid = threadIdx.x;
+  const u128b inc = ((u128b)pcg2 << 64) | pcg3, s0 = ((u128b)pcg0 << 64) | pcg1;
+  for (uint64_t shot = blockIdx.x; shot < shots; shot += gridDim.x) {
+    for (uint32_t i = tid; i < len; i += blockDim.x) st[i] = prefix[i];
+    u128b am, ap;
+    lcg_jump(inc, shot * (uint64_t)M, am, ap);
+    u128b s = am * s0 + ap;  // state before this shot's first draw
+    uint64_t code = 0;
+    for (int k = 0; k < nops; ++k) {
+      __syncthreads();
+      const int kind = ops[3 * k], a = ops[3 * k + 1], b = ops[3 * k + 2];
+      if (kind == 0) {
+        const BatchGate& g = gates[a];
+        if (g.kind == 0) {
+          const int q = g.q0;
+          const cplx<R> m0 = mk<R>((R)g.m[0], (R)g.m[1]), m1 = mk<R>((R)g.m[2], (R)g.m[3]);
+          const cplx<R> m2 = mk<R>((R)g.m[4], (R)g.m[5]), m3 = mk<R>((R)g.m[6], (R)g.m[7]);
+          for (uint32_t p = tid; p < len / 2; p += blockDim.x) {
+            const uint32_t i0 = (uint32_t)insert0(p, q), i1 = i0 | (1u << q);
+            const cplx<R> x0 = st[i0], x1 = st[i1];
+            st[i0] = cfma<R>(m1, x1, cmul<R>(m0, x0));
+            st[i1] = cfma<R>(m3, x1, cmul<R>(m2, x0));
+          }
+        } else {
+          const int qa = g.q0, qb = g.q1;
+          const int lo = qa < qb ? qa : qb, hi = qa < qb ? qb : qa;
+          for (uint32_t p = tid; p < len / 4; p += blockDim.x) {
+            const uint32_t base = (uint32_t)insert0(insert0(p, lo), hi);
+            const uint32_t idx[4] = {base, base | (1u << qa), base | (1u << qb), base | (1u << qa) | (1u << qb)};
+            cplx<R> x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = st[idx[j]];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              cplx<R> acc = mk<R>(R(0), R(0));
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                acc = cfma<R>(mk<R>((R)g.m[2 * (4 * r + c)], (R)g.m[2 * (4 * r + c) + 1]), x[c], acc);
+              st[idx[r]] = acc;
+            }
+          }
+        }
+      } else {
+        const int q = a;
+        const double p1 = block_sum_p1<R>(st, len, q, red);
+        s = s * mult128() + inc;
+        const double u = pcg_out(s);
+        const int out = u < p1 ? 1 : 0;
+        const double p = out ? p1 : 1.0 - p1;
+        const R sc = (R)(1.0 / sqrt(p));
+        for (uint32_t pp = tid; pp < len / 2; pp += blockDim.x) {
+          const uint32_t i0 = (uint32_t)insert0(pp, q), i1 = i0 | (1u << q);
+          cplx<R> keep = out ? st[i1] : st[i0];
+          keep.x *= sc;
+          keep.y *= sc;
+          const cplx<R> z = mk<R>(R(0), R(0));
+          if (kind == 2 || !out) {  // reset: |1> -> X -> |0>
+            st[i0] = keep;
+            st[i1] = z;
+          } else {
+            st[i0] = z;
+            st[i1] = keep;
+          }
+        }
+        if (kind == 1) code = (code & ~(1ull << b)) | ((uint64_t)out << b);
+      }
+    }
+    if (tid == 0) codes[shot] = code;
+    __syncthreads();
+  }
+}
+
+}  // namespace svb
+
+extern "C" int svb_replay_small(int device, int precision, int n, const double* prefix_c128, const int32_t* ops,
+                                int nops, const svb_gate* gates, int ngates, uint64_t shots, const uint64_t* pcg,
+                                uint64_t* out_codes) {
+  try {
+    const int nmax = precision == SVB_C128 ? 12 : 13;
+    require(n >= 1 && n <= nmax && shots >= 1 && nops >= 0 && ngates >= 0, SVB_E_ARG, "bad replay arguments");
+    int M = 0;
+    for (int k = 0; k < nops; ++k) {
+      require(ops[3 * k] >= 0 && ops[3 * k] <= 2, SVB_E_ARG, "bad replay op");
+      if (ops[3 * k] != 0) ++M;
+      else require(ops[3 * k + 1] >= 0 && ops[3 * k + 1] < ngates, SVB_E_ARG, "bad gate index");
+    }
+    std::vector<BatchGate> hg(ngates);
+    for (int i = 0; i < ngates; ++i) {
+      std::memcpy(hg[i].m, gates[i].mat, sizeof hg[i].m);
+      hg[i].kind = gates[i].k == 1 ? 0 : 1;
+      hg[i].q0 = gates[i].qubits[0];
+      hg[i].q1 = gates[i].k == 2 ? gates[i].qubits[1] : 0;
+      hg[i].src = 0;
+    }
+    const uint64_t len = 1ull << n;
+    const size_t sz = precision == SVB_C128 ? 16 : 8;
+    std::vector<unsigned char> hp(len * sz);
+    for (uint64_t i = 0; i < len; ++i) {
+      if (precision == SVB_C128) {
+        double2 v = make_double2(prefix_c128[2 * i], prefix_c128[2 * i + 1]);
+        std::memcpy(hp.data() + i * sz, &v, sz);
+      } else {
+        float2 v = make_float2((float)prefix_c128[2 * i], (float)prefix_c128[2 * i + 1]);
+        std::memcpy(hp.data() + i * sz, &v, sz);
+      }
+    }
+    SVB_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    SVB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    void* dpre = nullptr;
+    int32_t* dops = nullptr;
+    BatchGate* dg = nullptr;
+    uint64_t* dcodes = nullptr;
+    SVB_CUDA(cudaMallocAsync(&dpre, len * sz, st));
+    SVB_CUDA(cudaMallocAsync(&dops, sizeof(int32_t) * 3 * std::max(nops, 1), st));
+    SVB_CUDA(cudaMallocAsync(&dg, sizeof(BatchGate) * std::max(ngates, 1), st));
+    SVB_CUDA(cudaMallocAsync(&dcodes, sizeof(uint64_t) * shots, st));
+    SVB_CUDA(cudaMemcpyAsync(dpre, hp.data(), len * sz, cudaMemcpyHostToDevice, st));
+    if (nops) SVB_CUDA(cudaMemcpyAsync(dops, ops, sizeof(int32_t) * 3 * nops, cudaMemcpyHostToDevice, st));
+    if (ngates) SVB_CUDA(cudaMemcpyAsync(dg, hg.data(), sizeof(BatchGate) * ngates, cudaMemcpyHostToDevice, st));
+    int nsm = 148;
+    SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    const unsigned grid = (unsigned)std::min<uint64_t>(shots, (uint64_t)nsm * 2);
+    const size_t smem = len * sz;
+    if (precision == SVB_C128) {
+      SVB_CUDA(cudaFuncSetAttribute(k_replay_small<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+      k_replay_small<double><<<grid, 256, smem, st>>>(static_cast<const double2*>(dpre), n, dops, nops, dg, M, shots,
+                                                      pcg[0], pcg[1], pcg[2], pcg[3], dcodes);
+    } else {
+      SVB_CUDA(cudaFuncSetAttribute(k_replay_small<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+      k_replay_small<float><<<grid, 256, smem, st>>>(static_cast<const float2*>(dpre), n, dops, nops, dg, M, shots,
+                                                     pcg[0], pcg[1], pcg[2], pcg[3], dcodes);
+    }
+    SVB_CHECK_LAUNCH();
+    SVB_CUDA(cudaMemcpyAsync(out_codes, dcodes, sizeof(uint64_t) * shots, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(dpre, st);
+    cudaFreeAsync(dops, st);
+    cudaFreeAsync(dg, st);
+    cudaFreeAsync(dcodes, st);
+    SVB_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    return SVB_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}

@@ -528,21 +528,35 @@ def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
                 g += 1
         workers = max(1, min(workers, shots))
         sizes = [shots // workers + (1 if w < shots % workers else 0) for w in range(workers)]
+        small = n <= (12 if prefix.precision == "c128" else 13)
+        if small:  # all shots in one shared-memory launch; host copy of the prefix (<= 64 KB)
+            pre = prefix.to_numpy()
+            ops_r = ops.copy()
+            meas = ops_r[:, 0] == 1
+            ops_r[meas, 2] = rank[ops_r[meas, 2]]
         all_codes = []
         for w, size in enumerate(sizes):
             if size == 0:
                 continue
             codes = np.empty(size, dtype=np.uint64)
             words = pcg_words(seed + w)
-            check(
-                lib().svb_replay(
-                    work.handle, prefix.handle, ptr(ops, _lib.c_int32), int(len(suffix)),
-                    ptr(gates) if gates.size else None, ptr(rank, _lib.c_int32), int(size),
-                    ptr(words, _lib.c_uint64), ptr(codes, _lib.c_uint64),
+            if small:
+                check(lib().svb_replay_small(
+                    device, _prec_code(prefix.precision), n, ptr(pre), ptr(ops_r, _lib.c_int32), int(len(suffix)),
+                    ptr(gates) if gates.size else None, int(gates.size), int(size), ptr(words, _lib.c_uint64),
+                    ptr(codes, _lib.c_uint64)))
+            else:
+                check(
+                    lib().svb_replay(
+                        work.handle, prefix.handle, ptr(ops, _lib.c_int32), int(len(suffix)),
+                        ptr(gates) if gates.size else None, ptr(rank, _lib.c_int32), int(size),
+                        ptr(words, _lib.c_uint64), ptr(codes, _lib.c_uint64),
+                    )
                 )
-            )
             all_codes.append(codes)
         meta["replay_shots"] = shots
+        meta["replay_engine"] = "smem-batched" if small else "per-shot"
+
     finally:
         _pool.release(prefix)
         _pool.release(work)

@@ -340,3 +340,27 @@ def test_jit_matches_interpreter_and_oracle(precision):
         s.apply_instructions(c.instructions)
         assert relerr(s.to_numpy(), ref) < TOL[precision], c.name
         s.close()
+
+
+def _mid_circuit(n, seed):
+    rng = np.random.default_rng(seed)
+    c = suite.random_circuit(n, 30, rng, measured=False)
+    c.n_clbits = n
+    c.measure(0, 0)
+    c.append(Instruction("reset", (1,)))
+    c.gate("h", 0).gate("cx", 0, n - 1).gate("ry", 1, params=(0.8,))
+    for q in range(n):
+        c.measure(q, q)
+    return c
+
+
+@pytest.mark.parametrize("n", [8, 13])
+def test_mid_circuit_replay_bit_exact_vs_oracle(n):
+    """Replay (statevector.py:157-250): smem-batched path (n=8) and per-shot
+    path (n=13) reproduce the oracle's counts exactly, workers included."""
+    c = _mid_circuit(n, 100 + n)
+    for workers in (1, 3):
+        shots = 600 if n > 12 else 3000
+        got = sv.run(c, shots, 17, workers=workers)
+        assert got.metadata["replay_engine"] == ("per-shot" if n > 12 else "smem-batched")
+        assert got.counts == orc.run(c, shots, 17, workers=workers), (n, workers)
