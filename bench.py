@@ -44,6 +44,18 @@ PRECISION = "c128"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
+def measured_traffic():
+    """dram read+write bytes per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/r01_ncu_qft30_pass_full.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_qft30_pass_full.json")) as fh:
+            recs = json.load(fh)
+        vals = [(r["dram_read_bytes"] + r["dram_write_bytes"]) * 1e9 for r in recs]  # ncu reports GB
+        return float(sum(vals) / len(vals))
+    except Exception:
+        return None
+
+
 def hbm_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -262,7 +274,7 @@ def run_ours(args, rank: int, world: int, dist):
                    "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2",
                    "hbm_passes_per_step": stats["passes"], "plan": plan},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "k_pass<double,4>",
+                     "frac": achieved / peak, "traffic": measured_traffic(), "kernel": "svb_jit (fused pass, c128)",
                      "peak_kind": peak_kind, "bytes_per_launch": pass_bytes, "avg_launch_ms": pass_avg_ms},
         "e2e": {"value": world * n_gates / e2e_s, "unit": "gates/s",
                 "h2d_bytes_per_step": int(gates.nbytes),
