@@ -26,6 +26,7 @@ struct svb_state {
   double* d_ws = nullptr;        // reduction scratch
   size_t ws_doubles = 0;
   int fusion = 1, max_high = -1;
+  bool zero_pending = false;  // |0...0> not yet written: the next fused pass synthesises it
   int jit_min_n = 24;  // NVRTC-specialised passes from this many qubits up (-1: never)
   ProgramStats stats{};
   Profiler prof;
@@ -51,9 +52,22 @@ template <class F> static int guard(F&& f) {
   }
 }
 
-static void check_handle(svb_handle h) {
+static void check_handle_nomat(svb_handle h) {
   require(h != nullptr && h->amps != nullptr, SVB_E_ARG, "invalid svb handle");
   SVB_CUDA(cudaSetDevice(h->device));
+}
+
+// Write a pending lazy |0...0> before anything reads or partially writes the state.
+static void materialize(svb_handle h) {
+  if (!h->zero_pending) return;
+  if (h->prec == SVB_C128) launch_zero<double>(h->amps, h->n, h->st);
+  else launch_zero<float>(h->amps, h->n, h->st);
+  h->zero_pending = false;
+}
+
+static void check_handle(svb_handle h) {
+  check_handle_nomat(h);
+  materialize(h);
 }
 
 static void ensure_ws(svb_handle h, size_t doubles) {
@@ -121,9 +135,7 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
     }
     SVB_CUDA(cudaMalloc(&h->d_rng, 4 * sizeof(uint64_t) + 16));
     h->d_outcome = reinterpret_cast<int32_t*>(h->d_rng + 4);
-    if (precision == SVB_C128) launch_zero<double>(h->amps, n_qubits, h->st);
-    else launch_zero<float>(h->amps, n_qubits, h->st);
-    SVB_CUDA(cudaStreamSynchronize(h->st));
+    h->zero_pending = true;  // |0...0>, written lazily (see materialize)
   });
   if (rc != SVB_OK) {
     if (h) {
@@ -185,10 +197,8 @@ int svb_last_stats(svb_handle h, int64_t* n_passes, int64_t* n_gates, int64_t* n
 
 int svb_set_zero(svb_handle h) {
   return guard([&] {
-    check_handle(h);
-    if (h->prec == SVB_C128) launch_zero<double>(h->amps, h->n, h->st);
-    else launch_zero<float>(h->amps, h->n, h->st);
-    SVB_CUDA(cudaStreamSynchronize(h->st));
+    check_handle_nomat(h);
+    h->zero_pending = true;  // lazy: written by the first consumer (or synthesised by the next pass)
   });
 }
 
@@ -197,6 +207,7 @@ int svb_copy_state(svb_handle dst, svb_handle src) {
     check_handle(dst);
     check_handle(src);
     require(dst->n == src->n && dst->prec == src->prec, SVB_E_ARG, "state shape mismatch");
+    SVB_CUDA(cudaStreamSynchronize(src->st));
     SVB_CUDA(cudaMemcpyAsync(dst->amps, src->amps, src->amp_bytes(), cudaMemcpyDeviceToDevice, dst->st));
     SVB_CUDA(cudaStreamSynchronize(dst->st));
   });
@@ -265,14 +276,14 @@ static void validate_gates(svb_handle h, const svb_gate* g, int ng) {
 int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
   return guard([&] {
     auto t0 = std::chrono::steady_clock::now();
-    check_handle(h);
+    check_handle_nomat(h);
     validate_gates(h, gates, n_gates);
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
     if (h->prec == SVB_C128)
-      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats);
+      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats, &h->zero_pending);
     else
-      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats);
+      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats, &h->zero_pending);
     auto t1 = std::chrono::steady_clock::now();
     SVB_CUDA(cudaStreamSynchronize(h->st));
     if (h->prof.on) h->prof.collect();
@@ -467,7 +478,8 @@ int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream) {
 
 int svb_clear(svb_handle h) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);
+    h->zero_pending = false;
     SVB_CUDA(cudaMemsetAsync(h->amps, 0, h->amp_bytes(), h->st));
     SVB_CUDA(cudaStreamSynchronize(h->st));
   });
@@ -566,9 +578,9 @@ int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops
           std::vector<svb_gate> run;
           while (j < n_ops && ops[3 * j] == 0) run.push_back(gates[ops[3 * j + 1]]), ++j;
           if (work->prec == SVB_C128)
-            run_program_owned<double>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats);
+            run_program_owned<double>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats, nullptr);
           else
-            run_program_owned<float>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats);
+            run_program_owned<float>(&work->amps, &work->spare, work->n, run.data(), (int)run.size(), work->fusion, work->jit_min_n, st, &work->stats, nullptr);
           i = j;
         } else {
           int q = ops[3 * i + 1];

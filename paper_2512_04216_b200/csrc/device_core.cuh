@@ -605,6 +605,14 @@ __device__ __forceinline__ void round_fixed(const PassCtx<R, RB>& c, int k, uint
   }
 }
 
+template <typename R, int RB>
+__device__ __forceinline__ uint64_t thread_fixed_g(const PassCtx<R, RB>& c, int k) {
+  uint32_t Fl;
+  uint64_t Fg;
+  thread_fixed(c.pd, c.pd.rounds[k], c.tid, 0, &Fl, &Fg);
+  return Fg;
+}
+
 // Shared-memory slots of the thread's 2^RB amplitudes in round layout `rd`:
 // the swizzle is GF(2)-linear, so slot(v) = swz(Fl) ^ XOR_i v_i swz(1 << reg_local[i]).
 template <typename R, int RB>
@@ -698,9 +706,12 @@ __device__ __forceinline__ void mul_rr(cplx<R>* a, cplx<R> e0, cplx<R> e1, cplx<
 
 // Interpreter body: rounds and ops read from the pass descriptor / op stream.
 struct InterpBody {
+  template <typename R, int RB> struct State {};
+  template <typename R, int RB>
+  __device__ static __forceinline__ void prologue(const PassCtx<R, RB>&, State<R, RB>&) {}
   template <typename R, int RB>
   __device__ static __forceinline__ void tile(int, const PassCtx<R, RB>& c, cplx<R>* a, cplx<R>* cur,
-                                              uint64_t base) {
+                                              uint64_t base, const State<R, RB>&) {
     const int nrounds = c.pd.nrounds;
     for (int k = 0; k < nrounds; ++k) {
       const RoundDev& rd = c.pd.rounds[k];
@@ -731,7 +742,8 @@ struct InterpBody {
 // shared memory and stores the last layout straight from registers to HBM.
 template <typename R, int RB, class Body>
 __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg,
-                                            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0) {
+                                            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
+                                            int zero_input = 0) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ PassDev pd;
   __shared__ cplx<R> uni[kMaxDiag * kUniStride];
@@ -790,6 +802,15 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   }
   auto issue = [&](uint64_t base, int b) {
     cplx<R>* dst = ring + (size_t)b * T;
+    if (zero_input) {  // lazy |0...0>: synthesise the tile instead of reading HBM
+      for (uint32_t k = 0; k < nld; ++k) {
+        const uint64_t g = base | ld_tid | s_ldk[k];
+        cplx<R>* d = dst + (sd_tid ^ s_sdk[k]);
+        d[0] = mk<R>(g == 0 ? R(1) : R(0), R(0));
+        if (kPer == 2) d[1] = mk<R>(R(0), R(0));
+      }
+      return;
+    }
     const cplx<R>* src = state + (base | ld_tid);
     // swizzle is linear over XOR: slot(tid part ^ k part) = swz(tid part) ^ swz(k part)
     for (uint32_t k = 0; k < nld; ++k) cp_async16(dst + (sd_tid ^ s_sdk[k]), src + s_ldk[k]);
@@ -801,6 +822,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     if (ts < ntiles) issue(tile_base_warp(pd, ts, lane), s);
     cp_async_commit();
   }
+  // tile-independent per-thread constants of the body (e.g. products of
+  // diagonal factors that depend only on the thread's own local bits)
+  typename Body::template State<R, RB> bs;
+  Body::template prologue<R, RB>(c, bs);
   cplx<R> a[1 << RB];
   int it = 0;
   for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
@@ -814,7 +839,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     }
     cp_async_wait<kStages - 1>();
     __syncthreads();
-    Body::template tile<R, RB>(pass, c, a, ring + (size_t)(it % kStages) * T, base);
+    Body::template tile<R, RB>(pass, c, a, ring + (size_t)(it % kStages) * T, base, bs);
     __syncthreads();  // ring slot and uniform factors are rewritten next tile
   }
   cp_async_wait<0>();
@@ -823,8 +848,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
 template <typename R, int RB>
 __global__ void __launch_bounds__(kPassThreads<R>, 1)
     k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
-           uint32_t ntiles) {
-  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles);
+           uint32_t ntiles, int zero_input) {
+  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input);
 }
 
 }  // namespace svb

@@ -165,7 +165,7 @@ template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
 template <typename R>
 static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats,
-                          bool use_jit) {
+                          bool use_jit, bool zero_input) {
   constexpr int RB = rb_of<R>();
   if (prog.passes.empty()) return;
   size_t pbytes = prog.passes.size() * sizeof(PassDev);
@@ -189,7 +189,7 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (use_jit && jit_launch_passes<R>(state, prog, dpass, dops, st, stats, nsm)) {
+  if (use_jit && jit_launch_passes<R>(state, prog, dpass, dops, st, stats, nsm, zero_input)) {
     SVB_CUDA(cudaFreeAsync(dbuf, st));
     return;
   }
@@ -199,9 +199,10 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
     unsigned threads = 1u << (pd.m - RB);
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
-    if (pf) pf->begin(st, 0, 2.0 * (double)(sizeof(cplx<R>) << n));
+    const int zin = (zero_input && p == 0) ? 1 : 0;
+    if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));
     k_pass<R, RB><<<grid, threads, kStages * (size_t)tile_bytes_of<R>(pd.m) + pd.ops_bytes, st>>>(
-        state, dpass + p, dops, (uint32_t)tiles);
+        state, dpass + p, dops, (uint32_t)tiles, zin);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);
     stats->passes += 1;
@@ -255,7 +256,7 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
   SchedOptions o = opt;
   o.relabel_swaps = false;  // the handle owns its buffer; permutation passes need run_program_owned
   Program prog = build_program<R>(n, g, ng, o);
-  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false);
+  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false, false);
 }
 
 static bool trace_on() {
@@ -275,11 +276,18 @@ struct TraceTimer {
 
 template <typename R>
 void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, int jit_min_n,
-                       cudaStream_t st, ProgramStats* stats) {
+                       cudaStream_t st, ProgramStats* stats, bool* zero_pending) {
   TraceTimer tt;
   stats->gates += ng;
   SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
-  if (!fusion || n < opt.rb + 5) {
+  auto write_zero = [&] {
+    if (zero_pending && *zero_pending) {
+      launch_zero<R>(*state, n, st);
+      *zero_pending = false;
+    }
+  };
+  if (!fusion || n < opt.rb + 5 || ng == 0) {
+    write_zero();
     for (int i = 0; i < ng; ++i) {
       launch_gate_basic<R>(*state, n, g[i], st);
       stats->passes += 1;
@@ -300,7 +308,10 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     }
   }
   const double t_build = tt.lap();
-  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats, jit_min_n >= 0 && n >= jit_min_n);
+  const bool zin = zero_pending && *zero_pending && !prog.passes.empty();
+  if (prog.passes.empty()) write_zero();
+  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin);
+  if (zin) *zero_pending = false;
   const double t_launch = tt.lap();
   if (!prog.final_perm.empty()) {
     cplx<R>* s = static_cast<cplx<R>*>(*state);
@@ -318,9 +329,9 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
 template void run_program<float>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
 template void run_program<double>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
 template void run_program_owned<float>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
-                                       ProgramStats*);
+                                       ProgramStats*, bool*);
 template void run_program_owned<double>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
-                                        ProgramStats*);
+                                        ProgramStats*, bool*);
 
 }  // namespace svb
 

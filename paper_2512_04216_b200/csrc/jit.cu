@@ -113,8 +113,15 @@ template <typename C> bool is1(const C& z) { return z.x == 1 && z.y == 0; }
 // come from the pass's uniform slot, thread-dependent factors are evaluated
 // with immediates, and factors that are exactly 1 by construction are dropped
 // at generation time (controlled phases leave half the amplitudes untouched).
+struct PrologueCtx {
+  std::ostringstream* o = nullptr;  // prologue code (runs once per thread)
+  int nslots = 0;                   // per-thread complex slots
+  int round = 0;                    // round of the op being emitted
+};
+
 template <typename R>
-void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, int RB, bool imm) {
+void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, int RB, bool imm,
+               PrologueCtx& pc) {
   // factor e of a term: an immediate (large programs) or a load from the op
   // payload in shared memory (structure-only code shared across angles)
   auto dref = [&](const void* term, int e) {
@@ -169,14 +176,31 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
       o << "      svb::cplx<R> D1_" << i << " = "
         << (has_ur ? "(" + us + ")[" + std::to_string(6 + i) + "]" : "svb::mk<R>(R(1), R(0))") << ";\n";
   }
-  for (int k = 0; k < h.nTR; ++k) {  // per term: skip the half that is exactly 1
-    const int i = tr[k].ra, qb = tr[k].qb;
-    const bool t0 = is1(tr[k].d[0]) && is1(tr[k].d[2]), t1 = is1(tr[k].d[1]) && is1(tr[k].d[3]);
-    if (t0 && t1) continue;
-    o << "      { const int f = (int)((Fg >> " << qb << ") & 1ull);";
-    if (!t0) o << " D0_" << i << " = svb::cmul<R>(D0_" << i << ", svb::csel<R>(f, " << dref(tr + k, 0) << ", " << dref(tr + k, 2) << "));";
-    if (!t1) o << " D1_" << i << " = svb::cmul<R>(D1_" << i << ", svb::csel<R>(f, " << dref(tr + k, 1) << ", " << dref(tr + k, 3) << "));";
-    o << " }\n";
+  // register-bit x thread-bit terms depend only on the thread's own local bits:
+  // their products are evaluated once per thread in the prologue (st.v[slot])
+  for (int i = 0; i < RB; ++i) {
+    bool any0 = false, any1 = false;
+    for (int k = 0; k < h.nTR; ++k) {
+      if (tr[k].ra != i) continue;
+      any0 = any0 || !(is1(tr[k].d[0]) && is1(tr[k].d[2]));
+      any1 = any1 || !(is1(tr[k].d[1]) && is1(tr[k].d[3]));
+    }
+    for (int half = 0; half < 2; ++half) {
+      if (!(half ? any1 : any0)) continue;
+      const int slot = pc.nslots++;
+      std::ostringstream& P = *pc.o;
+      P << "    { svb::cplx<R> acc = svb::mk<R>(R(1), R(0)); const uint64_t F = svb::thread_fixed_g<R, RB>(c, "
+        << pc.round << ");\n";
+      for (int k = 0; k < h.nTR; ++k) {
+        if (tr[k].ra != i) continue;
+        if (half == 0 && is1(tr[k].d[0]) && is1(tr[k].d[2])) continue;
+        if (half == 1 && is1(tr[k].d[1]) && is1(tr[k].d[3])) continue;
+        P << "      acc = svb::cmul<R>(acc, svb::csel<R>((int)((F >> " << (int)tr[k].qb << ") & 1ull), "
+          << dref(tr + k, half) << ", " << dref(tr + k, 2 + half) << "));\n";
+      }
+      P << "      st.v[" << slot << "] = acc; }\n";
+      o << "      D" << half << "_" << i << " = svb::cmul<R>(D" << half << "_" << i << ", st.v[" << slot << "]);\n";
+    }
   }
   for (int k = 0; k < h.nTC; ++k) {
     const int qa = tc[k].qa, qb = tc[k].qb;
@@ -228,7 +252,7 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
 
 // Emit the straight-line Body of one pass.
 template <typename R>
-void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool imm) {
+void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool imm, PrologueCtx& pc) {
   const PassDev& pd = prog.passes[p];
   o << "    case " << p << ": {\n";
   for (int k = 0; k < pd.nrounds; ++k) {
@@ -254,7 +278,8 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       const std::string rm = std::to_string(h.rmask) + "u, " + std::to_string(h.rval) + "u";
       switch (h.kind) {
         case OP_DIAG:
-          emit_diag<R>(o, prog.ops.data() + pay, pay, RB, imm);
+          pc.round = k;
+          emit_diag<R>(o, prog.ops.data() + pay, pay, RB, imm, pc);
           break;
         case OP_U1R:
           if (imm) {
@@ -315,25 +340,34 @@ constexpr int kImmMinQubits = 28;
 
 template <typename R> std::string jit_source_pass(const Program& prog, int p) {
   constexpr int RB = kRegBits<R>;
+  std::ostringstream body, pro;
+  PrologueCtx pc;
+  pc.o = &pro;
+  const PassDev& pd0 = prog.passes[p];
+  emit_body<R>(body, prog, p, RB, pd0.m + pd0.nout >= kImmMinQubits, pc);
   std::ostringstream o;
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
-  o << "struct PassBody {\n  template <typename R, int RB>\n"
+  o << "struct PassBody {\n"
+       "  template <typename R, int RB> struct State { svb::cplx<R> v[" << (pc.nslots ? pc.nslots : 1) << "]; };\n"
+       "  template <typename R, int RB>\n"
+       "  __device__ static __forceinline__ void prologue(const svb::PassCtx<R, RB>& c, State<R, RB>& st) {\n"
+    << pro.str() << "    (void)c; (void)st;\n  }\n"
+       "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void tile(int pass, const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
-       "svb::cplx<R>* cur, uint64_t base) {\n"
-       "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    switch (0) {\n";
-  const PassDev& pd0 = prog.passes[p];
-  emit_body<R>(o, prog, p, RB, pd0.m + pd0.nout >= kImmMinQubits);
-  o << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", 1) svb_jit(svb::cplx<R>* __restrict__ state, "
-       "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass) {\n"
-       "  svb::pass_kernel<R, "
-    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass);\n}\n";
-  std::string src = o.str();
-  // the body names its case by pass index; a single-case switch on 0
+       "svb::cplx<R>* cur, uint64_t base, const State<R, RB>& st) {\n"
+       "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    (void)st;\n    switch (0) {\n";
+  std::string b = body.str();
   const std::string from = "    case " + std::to_string(p) + ": {";
-  const size_t at = src.find(from);
-  if (at != std::string::npos) src.replace(at, from.size(), "    case 0: {");
-  return src;
+  const size_t at = b.find(from);
+  if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
+  o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R>
+    << ", 1) svb_jit(svb::cplx<R>* __restrict__ state, "
+       "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
+       "int zero_input) {\n"
+       "  svb::pass_kernel<R, "
+    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input);\n}\n";
+  return o.str();
 }
 
 uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
@@ -383,7 +417,7 @@ static std::vector<char> jit_compile(const std::string& src, std::string* log) {
 
 template <typename R>
 bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass, const uint8_t* dops,
-                       cudaStream_t st, ProgramStats* stats, int nsm) {
+                       cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
   static Driver dr;
   if (!dr.ok || prog.passes.empty()) return false;
   constexpr int RB = kRegBits<R>;
@@ -474,9 +508,10 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const uint8_t* ob = dops;
     uint32_t nt = (uint32_t)tiles;
     int pass = 0;
-    void* args[] = {&s, &pdp, &ob, &nt, &pass};
+    int zin = (zero_input && p == 0) ? 1 : 0;
+    void* args[] = {&s, &pdp, &ob, &nt, &pass, &zin};
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
-    if (pf) pf->begin(st, 0, 2.0 * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
+    if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
     if (dr.launch(f, grid, 1, 1, threads, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: kernel launch failed");
     if (pf) pf->end(st);
@@ -487,9 +522,9 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
 }
 
 template bool jit_launch_passes<float>(cplx<float>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
-                                       ProgramStats*, int);
+                                       ProgramStats*, int, bool);
 template bool jit_launch_passes<double>(cplx<double>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
-                                        ProgramStats*, int);
+                                        ProgramStats*, int, bool);
 
 }  // namespace svb
 

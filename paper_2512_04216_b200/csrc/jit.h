@@ -12,6 +12,6 @@ bool jit_available();
 // caller then runs the interpreter kernel.
 template <typename R>
 bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass, const uint8_t* dops,
-                       cudaStream_t st, ProgramStats* stats, int nsm);
+                       cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input);
 
 }  // namespace svb

@@ -9,10 +9,10 @@ for _ in range(3):
     s.zero(); s.apply_gates(g); s.expect_z(masks)
 out = {}
 for name, fn in (("zero", lambda: s.zero()), ("apply", lambda: s.apply_gates(g)), ("expect30", lambda: s.expect_z(masks)),
-                 ("expect1", lambda: s.expect_z(masks[:1]))):
+                 ("expect1", lambda: s.expect_z(masks[:1])), ("zero_apply", lambda: (s.zero(), s.apply_gates(g)))):
     s.timer_start(); t0 = time.perf_counter()
     for _ in range(5): fn()
     out[name + "_ms"] = round(s.timer_stop() / 5, 3); out[name + "_wall_ms"] = round((time.perf_counter() - t0) / 5 * 1e3, 3)
-s.profile(True); s.apply_gates(g); p = s.profile_read()
+s.zero(); s.profile(True); s.apply_gates(g); p = s.profile_read()
 out["passes_ms"] = round(p["pass_ms"], 3); out["perm_ms"] = round(p["perm_ms"], 3)
 print(json.dumps(out))
