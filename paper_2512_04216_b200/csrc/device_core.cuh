@@ -46,7 +46,10 @@ __host__ __device__ __forceinline__ uint64_t insert0(uint64_t i, int q) {
   return ((i >> q) << (q + 1)) | lo;
 }
 
-enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5, OP_U1X = 6 };
+// OP_U1P / OP_U1PR: unit-pivot 1q op y_r = x_pc[r] + ratio_r * x_(1-pc[r])
+// (pc bits in OpHdr::n; payload ratio_0, ratio_1; PR = both ratios real)
+enum : int32_t { OP_DIAG = 0, OP_U1 = 1, OP_U1ANTI = 2, OP_U2 = 3, OP_PERM2 = 4, OP_U1R = 5, OP_U1X = 6,
+                 OP_U1P = 7, OP_U1PR = 8 };
 
 // Every op: header, then a kind-specific payload.  `bytes` = total size
 // (multiple of 16).  Condition: the op applies where
@@ -68,17 +71,25 @@ template <typename R> struct alignas(16) DiagTerm {
 
 // DIAG payload: DiagHdr, then DiagTerm entries in class order
 //   UR (register bit i x tile bit, grouped by i) | UC (tile x tile) |
+//   UT (thread bit x tile bit, grouped by thread qubit) |
 //   TR (register bit x thread bit) | TC (thread-bit constants) | RR (register x register)
 // Classes U* depend only on the tile index and are evaluated once per tile per
 // CTA into the pass's uniform slots (shared memory); T* and RR per thread.
+// A UT term stores, per tile-bit value f, the constant part d[2f] = e(0, f)
+// (folded into the slot's C) and the ratio d[2f+1] = e(1, f) / e(0, f) that
+// the thread applies when its thread bit is set (group product V[g]).
 struct alignas(16) DiagHdr {
   int32_t nUR[6];
   int32_t nUC, nTR, nTC, nRR;
   int32_t slot;
-  int32_t pad[5];
+  int32_t nUTg;       // UT groups (one per thread qubit)
+  uint8_t utn[16];    // terms per UT group
 };
 static_assert(sizeof(DiagHdr) == 64, "DiagHdr layout");
-constexpr int kUniStride = 12;  // cplx per slot: C, U0[5], U1[5], pad
+constexpr int kMaxUT = 12;
+// cplx per uniform slot: C, U0[5], U1[5], V[kMaxUT], pad
+constexpr int kUniStride = 24;
+constexpr int kUniV = 11;
 
 constexpr int kMaxRounds = 24;
 constexpr int kMaxM = 14;
@@ -176,6 +187,32 @@ SVB_HD void u1_anti(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval)
   }
 }
 
+// one output row of a unit-pivot op: p + r*o; RK: 0 r = 0, 1 real, 2 imaginary, 3 complex
+template <typename R, int RK> SVB_HD cplx<R> piv_row(cplx<R> p, cplx<R> o, cplx<R> r) {
+  if constexpr (RK == 0) return p;
+  else if constexpr (RK == 1) return mk<R>(fma(r.x, o.x, p.x), fma(r.x, o.y, p.y));
+  else if constexpr (RK == 2) return mk<R>(fma(-r.y, o.y, p.x), fma(r.y, o.x, p.y));
+  else return cfma<R>(r, o, p);
+}
+
+template <typename R, int RB, int B, int PC0, int PC1, int RK0, int RK1>
+SVB_HD void u1_piv(cplx<R>* a, cplx<R> r0, cplx<R> r1) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & (1 << B)) continue;
+    const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
+    a[v] = piv_row<R, RK0>(PC0 ? x1 : x0, PC0 ? x0 : x1, r0);
+    a[v | (1 << B)] = piv_row<R, RK1>(PC1 ? x1 : x0, PC1 ? x0 : x1, r1);
+  }
+}
+
+// op-stream form (interpreter and structure-only JIT): ratios from the payload
+template <typename R, int RB, int B, int PC, bool REAL>
+SVB_HD void u1_piv_p(cplx<R>* a, const cplx<R>* r) {
+  constexpr int RK = REAL ? 1 : 3;
+  u1_piv<R, RB, B, (PC & 1), (PC >> 1), RK, RK>(a, ldc<R>(r), ldc<R>(r + 1));
+}
+
 template <typename R, int RB, int B1, int B2>
 SVB_HD void u2_dense(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
 #pragma unroll
@@ -218,6 +255,12 @@ SVB_HD void u2_perm(cplx<R>* a, const int32_t* src, const cplx<R>* ph, uint32_t 
 
 template <typename R> SVB_HD int fbit(uint64_t F, int q) { return q >= 0 ? (int)((F >> q) & 1ull) : 0; }
 
+SVB_HD int diag_nut(const DiagHdr* h) {
+  int n = 0;
+  for (int g = 0; g < h->nUTg; ++g) n += h->utn[g];
+  return n;
+}
+
 // Tile-uniform factors of one DIAG payload (host emulator / reference order).
 template <typename R, int RB>
 SVB_HD void diag_uniform_serial(const uint8_t* payload, uint64_t base, cplx<R>* slot) {
@@ -236,6 +279,15 @@ SVB_HD void diag_uniform_serial(const uint8_t* payload, uint64_t base, cplx<R>* 
   }
   cplx<R> c = one;
   for (int k = 0; k < h->nUC; ++k, ++t) c = cmul<R>(c, t->d[fbit<R>(base, t->qa) + 2 * fbit<R>(base, t->qb)]);
+  for (int g = 0; g < h->nUTg; ++g) {
+    cplx<R> v = one;
+    for (int k = 0; k < h->utn[g]; ++k, ++t) {
+      const int f = fbit<R>(base, t->qb);
+      c = cmul<R>(c, t->d[2 * f]);
+      v = cmul<R>(v, t->d[2 * f + 1]);
+    }
+    slot[kUniV + g] = v;
+  }
   slot[0] = c;
 }
 
@@ -245,7 +297,9 @@ SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cp
   const int4 h0 = ldop(reinterpret_cast<const int4*>(payload));      // nUR[0..3]
   const int4 h1 = ldop(reinterpret_cast<const int4*>(payload) + 1);  // nUR[4..5], nUC, nTR
   const int4 h2 = ldop(reinterpret_cast<const int4*>(payload) + 2);  // nTC, nRR, slot, -
-  const int nskip = h0.x + h0.y + h0.z + h0.w + h1.x + h1.y + h1.z;
+  const DiagHdr* hd = reinterpret_cast<const DiagHdr*>(payload);
+  const int nut = diag_nut(hd);
+  const int nskip = h0.x + h0.y + h0.z + h0.w + h1.x + h1.y + h1.z + nut;
   const int nTR = h1.w, nTC = h2.x, nRR = h2.y;
   cplx<R> C = mk<R>(R(1), R(0));
   cplx<R> D0[RB], D1[RB];
@@ -258,6 +312,14 @@ SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cp
     for (int i = 0; i < RB; ++i) {
       D0[i] = us[1 + i];
       D1[i] = us[1 + 5 + i];
+    }
+    // UT groups: the thread's own bit of each group's thread qubit selects V[g]
+    const DiagTerm<R>* tu = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr)) + (nskip - nut);
+    for (int g = 0; g < hd->nUTg; ++g) {
+      const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(tu));
+      const int qa = (int8_t)((w >> 16) & 0xff);
+      if (fbit<R>(Fg, qa)) C = cmul<R>(C, us[kUniV + g]);
+      tu += hd->utn[g];
     }
   }
   const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr)) + nskip;
@@ -345,6 +407,35 @@ SVB_HD void u1_kind(int kind, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint
   else u1_anti<R, RB, B, COND>(a, m, rmask, rval);
 }
 
+template <typename R, int RB, int B, bool REAL>
+SVB_HD void u1_piv_pc(int pc, cplx<R>* a, const cplx<R>* r) {
+  switch (pc) {
+    case 0: u1_piv_p<R, RB, B, 0, REAL>(a, r); break;
+    case 1: u1_piv_p<R, RB, B, 1, REAL>(a, r); break;
+    case 2: u1_piv_p<R, RB, B, 2, REAL>(a, r); break;
+    default: u1_piv_p<R, RB, B, 3, REAL>(a, r); break;
+  }
+}
+
+template <typename R, int RB, int B>
+SVB_HD void u1_piv_any(bool real, int pc, cplx<R>* a, const cplx<R>* r) {
+  if constexpr (B < RB) {
+    if (real) u1_piv_pc<R, RB, B, true>(pc, a, r);
+    else u1_piv_pc<R, RB, B, false>(pc, a, r);
+  }
+}
+
+template <typename R, int RB>
+SVB_HD void dispatch_u1p(bool real, int b, int pc, cplx<R>* a, const cplx<R>* r) {
+  switch (b) {
+    case 0: u1_piv_any<R, RB, 0>(real, pc, a, r); break;
+    case 1: u1_piv_any<R, RB, 1>(real, pc, a, r); break;
+    case 2: u1_piv_any<R, RB, 2>(real, pc, a, r); break;
+    case 3: u1_piv_any<R, RB, 3>(real, pc, a, r); break;
+    default: u1_piv_any<R, RB, 4>(real, pc, a, r); break;
+  }
+}
+
 template <typename R, int RB, bool COND>
 SVB_HD void dispatch_u1_c(int kind, int b, cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
   switch (b) {
@@ -421,6 +512,10 @@ SVB_HD void run_ops(cplx<R>* a, uint64_t Fg, const uint8_t* ops, uint32_t off, u
       case OP_U1X:
       case OP_U1ANTI:
         dispatch_u1<R, RB>(w0.x, w0.y, a, reinterpret_cast<const cplx<R>*>(payload), w2.x, w2.y);
+        break;
+      case OP_U1P:
+      case OP_U1PR:
+        dispatch_u1p<R, RB>(w0.x == OP_U1PR, w0.y, w0.w, a, reinterpret_cast<const cplx<R>*>(payload));
         break;
       default:
         dispatch_u2<R, RB>(w0.x, w0.y, w0.z, a, payload, w2.x, w2.y);
@@ -528,47 +623,69 @@ template <typename R> __device__ __forceinline__ cplx<R> shfl_xor_c(cplx<R> x, i
 }
 
 // Tile-uniform factors of one DIAG payload, lanes in parallel over the terms.
+// Product over lanes of a warp (all lanes return it).
+template <typename R> __device__ __forceinline__ cplx<R> warp_prod(cplx<R> x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = cmul<R>(x, shfl_xor_c<R>(x, o));
+  return x;
+}
+
+// Tile-uniform factors of all DIAG payloads of a pass, as independent items
+// (per payload: one per register bit, the constant, one per UT group) dealt
+// round-robin to the CTA's warps; each item is a lane-parallel product.
 template <typename R, int RB>
-__device__ void diag_uniform_warp(const uint8_t* payload, uint64_t base, cplx<R>* slot, uint32_t lane) {
-  const int4 h0 = reinterpret_cast<const int4*>(payload)[0];
-  const int4 h1 = reinterpret_cast<const int4*>(payload)[1];
-  const int nur[6] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y};
-  const int nuc = h1.z;
-  const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+__device__ void diag_uniform_items(const uint8_t* ops, const uint32_t* diag_off, int ndiag, uint64_t base,
+                                   cplx<R>* uni, uint32_t warp, uint32_t nwarps, uint32_t lane) {
   const cplx<R> one = mk<R>(R(1), R(0));
-  for (int i = 0; i < RB; ++i) {
-    const int n = nur[i];
-    cplx<R> u0 = one, u1 = one;
-    if (n > 0) {
-      for (int k = (int)lane; k < n; k += 32) {
-        const int qb = t[k].qb;
-        const int f = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
-        u0 = cmul<R>(u0, t[k].d[2 * f]);
-        u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
+  uint32_t item = 0;
+  for (int d = 0; d < ndiag; ++d) {
+    const uint8_t* payload = ops + diag_off[d];
+    const DiagHdr* h = reinterpret_cast<const DiagHdr*>(payload);
+    cplx<R>* slot = uni + d * kUniStride;
+    const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+    for (int i = 0; i < RB; ++i) {
+      const int n = h->nUR[i];
+      const bool mine = item == warp;
+      if (++item == nwarps) item = 0;
+      if (mine) {
+        cplx<R> u0 = one, u1 = one;
+        for (int k = (int)lane; k < n; k += 32) {
+          const int f = fbit<R>(base, t[k].qb);
+          u0 = cmul<R>(u0, t[k].d[2 * f]);
+          u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
+        }
+        if (n > 1) { u0 = warp_prod<R>(u0); u1 = warp_prod<R>(u1); }
+        if (lane == 0) { slot[1 + i] = u0; slot[1 + 5 + i] = u1; }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        u0 = cmul<R>(u0, shfl_xor_c<R>(u0, o));
-        u1 = cmul<R>(u1, shfl_xor_c<R>(u1, o));
+      t += n;
+    }
+    // constant: UC terms and the UT constant parts
+    const DiagTerm<R>* tut = t + h->nUC;
+    const int nut = diag_nut(h);
+    const bool mine_c = item == warp;
+    if (++item == nwarps) item = 0;
+    if (mine_c) {
+      cplx<R> c = one;
+      for (int k = (int)lane; k < h->nUC; k += 32)
+        c = cmul<R>(c, t[k].d[fbit<R>(base, t[k].qa) + 2 * fbit<R>(base, t[k].qb)]);
+      for (int k = (int)lane; k < nut; k += 32) c = cmul<R>(c, tut[k].d[2 * fbit<R>(base, tut[k].qb)]);
+      if (h->nUC + nut > 1) c = warp_prod<R>(c);
+      if (lane == 0) slot[0] = c;
+    }
+    const DiagTerm<R>* tg = tut;
+    for (int g = 0; g < h->nUTg; ++g) {
+      const int n = h->utn[g];
+      const bool mine = item == warp;
+      if (++item == nwarps) item = 0;
+      if (mine) {
+        cplx<R> v = one;
+        for (int k = (int)lane; k < n; k += 32) v = cmul<R>(v, tg[k].d[2 * fbit<R>(base, tg[k].qb) + 1]);
+        if (n > 1) v = warp_prod<R>(v);
+        if (lane == 0) slot[kUniV + g] = v;
       }
+      tg += n;
     }
-    if (lane == 0) {
-      slot[1 + i] = u0;
-      slot[1 + 5 + i] = u1;
-    }
-    t += n;
   }
-  cplx<R> c = one;
-  if (nuc > 0) {
-    for (int k = (int)lane; k < nuc; k += 32) {
-      const int qa = t[k].qa, qb = t[k].qb;
-      const int fa = qa >= 0 ? (int)((base >> qa) & 1ull) : 0, fb = qb >= 0 ? (int)((base >> qb) & 1ull) : 0;
-      c = cmul<R>(c, t[k].d[fa + 2 * fb]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c = cmul<R>(c, shfl_xor_c<R>(c, o));
-  }
-  if (lane == 0) slot[0] = c;
 }
 
 // ------------------------------------------------------- pass skeleton
@@ -833,10 +950,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     if (tn < ntiles) issue(tile_base_warp(pd, tn, lane), (it + kStages - 1) % kStages);
     cp_async_commit();
     const uint64_t base = tile_base_warp(pd, t, lane);
-    if (ndiag > 0) {  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
-      for (int d = (int)warp; d < ndiag; d += (int)nwarps)
-        diag_uniform_warp<R, RB>(c.ops + pd.diag_off[d], base, uni + d * kUniStride, lane);
-    }
+    if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
+      diag_uniform_items<R, RB>(c.ops, pd.diag_off, ndiag, base, uni, warp, nwarps, lane);
     cp_async_wait<kStages - 1>();
     __syncthreads();
     Body::template tile<R, RB>(pass, c, a, ring + (size_t)(it % kStages) * T, base, bs);

@@ -148,6 +148,16 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
       cone = cone && is1(u->d[e]);
       creal = creal && u->d[e].y == 0;
     }
+  // UT groups: C also takes the group ratios selected by the thread's own bits
+  std::vector<int> ut_q;
+  for (int g = 0; g < h.nUTg; ++g) {
+    ut_q.push_back(u->qa);
+    for (int k = 0; k < h.utn[g]; ++k, ++u)
+      for (int e = 0; e < 4; ++e) {
+        cone = cone && is1(u->d[e]);
+        creal = creal && u->d[e].y == 0;
+      }
+  }
   const DiagTerm<R>* tr = u;
   const DiagTerm<R>* tc = tr + h.nTR;
   const DiagTerm<R>* rr = tc + h.nTC;
@@ -165,8 +175,10 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
     }
   o << "    {\n";
   const std::string us = "c.uni + " + std::to_string(h.slot * kUniStride);
-  const bool has_uc = h.slot >= 0 && h.nUC > 0;
+  const bool has_uc = h.slot >= 0 && (h.nUC > 0 || h.nUTg > 0);
   if (!cone) o << "      svb::cplx<R> C = " << (has_uc ? "(" + us + ")[0]" : "svb::mk<R>(R(1), R(0))") << ";\n";
+  for (size_t g = 0; g < ut_q.size(); ++g)
+    o << "      if ((Fg >> " << ut_q[g] << ") & 1ull) C = svb::cmul<R>(C, (" << us << ")[" << (kUniV + (int)g) << "]);\n";
   for (int i = 0; i < RB; ++i) {
     const bool has_ur = h.slot >= 0 && h.nUR[i] > 0;
     if (!d0one[i])
@@ -299,6 +311,20 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
           o << "    " << guard << "svb::" << fn << "<R, RB, " << h.a << ", " << cond
             << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
           (void)coef;
+          break;
+        }
+        case OP_U1P:
+        case OP_U1PR: {
+          const int pc0 = h.n & 1, pc1 = (h.n >> 1) & 1;
+          if (imm) {
+            auto rk = [](const cplx<R>& z) { return z.x == 0 && z.y == 0 ? 0 : z.y == 0 ? 1 : z.x == 0 ? 2 : 3; };
+            o << "    " << guard << "svb::u1_piv<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk(coef[0])
+              << ", " << rk(coef[1]) << ">(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
+          } else {
+            o << "    " << guard << "svb::u1_piv_p<R, RB, " << h.a << ", " << (h.n & 3) << ", "
+              << (h.kind == OP_U1PR ? "true" : "false") << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + "
+              << pay << "));\n";
+          }
           break;
         }
         case OP_U2:

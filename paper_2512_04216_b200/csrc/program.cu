@@ -309,33 +309,68 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
 
   while (!remaining.empty()) {
     // ---- choose S and the ops of this pass
-    uint64_t S = (m == n) ? ((n == 64) ? ~0ull : ((1ull << n) - 1)) : lanes;
-    uint64_t blkA = 0, blkD = 0;
-    std::vector<int> placed, skipped;
-    size_t est_bytes = 0;  // upper bound of the encoded op bytes of this pass
     auto op_bytes = [](const FOp& f) -> size_t {
       const size_t c = sizeof(cplx<R>);
       if (f.type == OP_DIAG) return sizeof(OpHdr) + sizeof(DiagHdr) + sizeof(DiagTerm<R>) + 16;
       if (f.type == OP_U2) return sizeof(OpHdr) + 16 * c + 16;
       return sizeof(OpHdr) + 4 * c + 32;
     };
-    for (int idx : remaining) {
-      const FOp& f = ops[idx];
-      bool conflict = (f.touched & blkA) || (f.active & blkD);
-      if (!conflict && est_bytes + op_bytes(f) <= kMaxPassOpBytes) {
-        uint64_t need = f.active & ~S;
-        if (__builtin_popcountll(S | need) <= m) {
-          S |= need;
-          placed.push_back(idx);
-          est_bytes += op_bytes(f);
-          continue;
+    // One in-order scan over the remaining ops: an op is placed when it does not
+    // depend on a skipped op and its active qubits lie in S (grow: S may gain
+    // qubits up to m).  Returns the number of placed ops.
+    auto place = [&](uint64_t& S, bool grow, std::vector<int>* placed, std::vector<int>* skipped) {
+      uint64_t blkA = 0, blkD = 0;
+      size_t est_bytes = 0;  // upper bound of the encoded op bytes of this pass
+      int count = 0;
+      for (int idx : remaining) {
+        const FOp& f = ops[idx];
+        bool conflict = (f.touched & blkA) || (f.active & blkD);
+        if (!conflict && est_bytes + op_bytes(f) <= kMaxPassOpBytes) {
+          uint64_t need = f.active & ~S;
+          if (need == 0 || (grow && __builtin_popcountll(S | need) <= m)) {
+            S |= need;
+            if (placed) placed->push_back(idx);
+            est_bytes += op_bytes(f);
+            ++count;
+            continue;
+          }
         }
+        if (skipped) skipped->push_back(idx);
+        blkA |= f.active;
+        blkD |= f.touched & ~f.active;
       }
-      skipped.push_back(idx);
-      blkA |= f.active;
-      blkD |= f.touched & ~f.active;
-    }
+      return count;
+    };
+    uint64_t S = (m == n) ? ((n == 64) ? ~0ull : ((1ull << n) - 1)) : lanes;
+    int best = place(S, true, nullptr, nullptr);
     for (int q = 0; q < n && __builtin_popcountll(S) < m; ++q) S |= 1ull << q;
+    if (m < n) {
+      // Local search over S: the in-order greedy fills S with the first qubits
+      // it meets (e.g. the whole state-prep layer), which can starve the long
+      // dependency chains (QFT).  Swap one non-lane qubit for one that a
+      // remaining op acts on while that places more ops.
+      uint64_t cand = 0;
+      for (int idx : remaining) cand |= ops[idx].active;
+      cand &= ~lanes;
+      for (int it = 0; it < 4 * m; ++it) {
+        int gain = 0;
+        uint64_t bestS = S;
+        for (uint64_t outs = S & ~lanes; outs; outs &= outs - 1) {
+          const uint64_t qo = outs & (~outs + 1);
+          for (uint64_t ins = cand & ~S; ins; ins &= ins - 1) {
+            const uint64_t qi = ins & (~ins + 1);
+            uint64_t T = (S & ~qo) | qi;
+            const int c = place(T, false, nullptr, nullptr);
+            if (c > best + gain) { gain = c - best; bestS = T; }
+          }
+        }
+        if (gain == 0) break;
+        best += gain;
+        S = bestS;
+      }
+    }
+    std::vector<int> placed, skipped;
+    place(S, false, &placed, &skipped);
 
     PassDev pd{};
     pd.m = m;
@@ -397,9 +432,36 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     }
 
     // ---- encode the rounds
+    //
+    // Deferred pivot diagonals: an unconditional 1q op M on q (after the
+    // pending diagonal diag(1, dl[q]) of q) is factored as diag(p0, p1) * P,
+    // where each row of P has a unit pivot: y_r = x_pc[r] + ratio_r x_(1-pc[r]).
+    // P costs one complex FMA per amplitude (two real FMAs for a real ratio)
+    // instead of two complex products; diag(p0, p1) = p0 * diag(1, p1/p0) is
+    // carried forward: the scalar p0 into the pass-global K, the rest into dl[q].
+    // Diagonals commute with diagonal ops; a conditional 1q op on q sees
+    // D^-1 M D; a 2q op absorbs its qubits' pending diagonals into its
+    // columns.  The pass's last unconditional dense 1q op absorbs K and is
+    // emitted in full; leftover pending diagonals and K are flushed as one
+    // DIAG op at the end of the last round.
     Encoder<R> enc(prog.ops);
     pd.nrounds = (int)rounds.size();
     pd.ops_begin = (uint32_t)prog.ops.size();
+    std::vector<cd> dl(n, cd(1.0, 0.0));
+    cd K(1.0, 0.0);
+    int last_u1 = -1;
+    for (auto& rd : rounds)
+      for (int idx : rd.second) {
+        const FOp& f = ops[idx];
+        if ((f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X) && f.conds.empty()) last_u1 = idx;
+      }
+    auto u1_type = [](const cd* M) {
+      if (zero(M[0]) && zero(M[3])) return (int)OP_U1ANTI;
+      if (M[0].imag() == 0 && M[1].imag() == 0 && M[2].imag() == 0 && M[3].imag() == 0) return (int)OP_U1R;
+      if (M[0].imag() == 0 && M[3].imag() == 0 && M[1].real() == 0 && M[2].real() == 0) return (int)OP_U1X;
+      return (int)OP_U1;
+    };
+    struct DT { int qa, qb; cd e[4]; };
     for (size_t k = 0; k < rounds.size(); ++k) {
       RoundDev& rd = pd.rounds[k];
       uint32_t regs = regsets[k];
@@ -410,6 +472,88 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
         if (regs & (1u << b)) { rd.reg_local[i] = b; regidx_of_local[b] = i; ++i; }
       }
       auto ridx = [&](int q) { return (q >= 0 && local_of[q] >= 0) ? regidx_of_local[local_of[q]] : -1; };
+      // one DIAG op from a list of 2-qubit (or 1-qubit, qb = -1) factors
+      auto encode_diag = [&](const std::vector<DT>& terms) {
+        // classify each factor by where its qubits live in this round
+        enum { NONE, TILE, THREAD, REG };
+        auto cls = [&](int q) {
+          if (q < 0) return (int)NONE;
+          if (local_of[q] < 0) return (int)TILE;
+          return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
+        };
+        const bool uniform_ok = pd.ndiag < kMaxDiag;
+        std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
+        std::vector<int> ut_q;                       // thread qubit of each UT group
+        std::vector<std::vector<DiagTerm<R>>> ut;    // UT terms per group
+        for (const DT& d : terms) {
+          int qa = d.qa, qb = d.qb;
+          cd e[4] = {d.e[0], d.e[1], d.e[2], d.e[3]};
+          int ca = cls(qa), cb = cls(qb);
+          // register qubit first; else thread qubit first
+          if ((ca != REG && cb == REG) || ((ca == TILE || ca == NONE) && cb == THREAD)) {
+            std::swap(qa, qb);
+            std::swap(ca, cb);
+            std::swap(e[1], e[2]);
+          }
+          DiagTerm<R> term{};
+          term.qa = (int8_t)qa;
+          term.qb = (int8_t)qb;
+          term.ra = (int8_t)(ca == REG ? ridx(qa) : -1);
+          term.rb = (int8_t)(cb == REG ? ridx(qb) : -1);
+          for (int k2 = 0; k2 < 4; ++k2) term.d[k2] = cvt<R>(e[k2]);
+          const bool ubit = (cb == TILE || cb == NONE);
+          if (ca == REG && cb == REG) rr.push_back(term);
+          else if (ca == REG && cb == THREAD) tr.push_back(term);
+          else if (ca == REG) (uniform_ok ? ur[term.ra] : tr).push_back(term);
+          else if ((ca == TILE || ca == NONE) && ubit && uniform_ok) uc.push_back(term);
+          else if (ca == THREAD && ubit && uniform_ok && !zero(e[0]) && !zero(e[2])) {
+            size_t g = 0;
+            while (g < ut_q.size() && ut_q[g] != qa) ++g;
+            if (g == ut_q.size()) {
+              if ((int)g == kMaxUT) { tc.push_back(term); continue; }
+              ut_q.push_back(qa);
+              ut.emplace_back();
+            }
+            // constant part per tile-bit value and the thread-bit ratio
+            const cd r0 = snap(e[1] / e[0]), r1 = snap(e[3] / e[2]);
+            term.d[0] = cvt<R>(e[0]);
+            term.d[1] = cvt<R>(r0);
+            term.d[2] = cvt<R>(e[2]);
+            term.d[3] = cvt<R>(r1);
+            ut[g].push_back(term);
+          } else tc.push_back(term);
+        }
+        size_t at = enc.begin(OP_DIAG, 0, 0, (int)terms.size(), 0, 0, 0, 0);
+        DiagHdr hd{};
+        for (int k2 = 0; k2 < 6; ++k2) hd.nUR[k2] = (int32_t)ur[k2].size();
+        hd.nUC = (int32_t)uc.size();
+        hd.nTR = (int32_t)tr.size();
+        hd.nTC = (int32_t)tc.size();
+        hd.nRR = (int32_t)rr.size();
+        bool any_uniform = !uc.empty() || !ut.empty();
+        for (int k2 = 0; k2 < 6; ++k2) any_uniform = any_uniform || !ur[k2].empty();
+        hd.slot = (uniform_ok && any_uniform) ? pd.ndiag : -1;
+        hd.nUTg = (int32_t)ut.size();
+        for (size_t g = 0; g < ut.size(); ++g) {
+          require(ut[g].size() <= 255, SVB_E_CUDA, "scheduler: UT group too large");
+          hd.utn[g] = (uint8_t)ut[g].size();
+        }
+        if (hd.slot >= 0) pd.diag_off[pd.ndiag++] = (uint32_t)prog.ops.size();
+        enc.put(hd);
+        for (int k2 = 0; k2 < 6; ++k2)
+          for (auto& x : ur[k2]) enc.put(x);
+        for (auto& x : uc) enc.put(x);
+        for (auto& g : ut)
+          for (auto& x : g) enc.put(x);
+        for (auto* lst : {&tr, &tc, &rr})
+          for (auto& x : *lst) enc.put(x);
+        enc.end(at);
+      };
+      auto encode_u1 = [&](int type, int b, const cd* M, uint64_t fm, uint64_t fv, uint32_t rm, uint32_t rv) {
+        size_t at = enc.begin(type, b, 0, 0, fm, fv, rm, rv);
+        for (int e = 0; e < 4; ++e) enc.put(cvt<R>(M[e]));
+        enc.end(at);
+      };
       rd.op_off = (uint32_t)prog.ops.size();
       const std::vector<int>& list = rounds[k].second;
       size_t i = 0;
@@ -418,53 +562,18 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
         if (f.type == OP_DIAG) {
           size_t j = i;
           while (j < list.size() && ops[list[j]].type == OP_DIAG) ++j;
-          // classify each factor by where its qubits live in this round
-          enum { NONE, TILE, THREAD, REG };
-          auto cls = [&](int q) {
-            if (q < 0) return (int)NONE;
-            if (local_of[q] < 0) return (int)TILE;
-            return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
-          };
-          const bool uniform_ok = pd.ndiag < kMaxDiag;
-          std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
+          std::vector<DT> terms;
           for (size_t t = i; t < j; ++t) {
             const FOp& d = ops[list[t]];
-            int qa = d.q[0], qb = d.q[1];
-            cd e[4] = {d.c[0], d.c[1], d.c[2], d.c[3]};
-            int ca = cls(qa), cb = cls(qb);
-            if (ca != REG && cb == REG) {  // register qubit first: transpose the factor
-              std::swap(qa, qb);
-              std::swap(ca, cb);
-              std::swap(e[1], e[2]);
+            if (d.q[1] < 0 && d.q[0] >= 0 && local_of[d.q[0]] >= 0 && !zero(d.c[0])) {
+              // 1q diagonal on a tile qubit: fold into the pending diagonal
+              K *= d.c[0];
+              dl[d.q[0]] *= d.c[1] / d.c[0];
+              continue;
             }
-            DiagTerm<R> term{};
-            term.qa = (int8_t)qa;
-            term.qb = (int8_t)qb;
-            term.ra = (int8_t)(ca == REG ? ridx(qa) : -1);
-            term.rb = (int8_t)(cb == REG ? ridx(qb) : -1);
-            for (int k2 = 0; k2 < 4; ++k2) term.d[k2] = cvt<R>(e[k2]);
-            const bool ubit = (cb == TILE || cb == NONE);
-            if (ca == REG && cb == REG) rr.push_back(term);
-            else if (ca == REG && cb == THREAD) tr.push_back(term);
-            else if (ca == REG) (uniform_ok ? ur[term.ra] : tr).push_back(term);
-            else if ((ca == TILE || ca == NONE) && ubit && uniform_ok) uc.push_back(term);
-            else tc.push_back(term);
+            terms.push_back(DT{d.q[0], d.q[1], {d.c[0], d.c[1], d.c[2], d.c[3]}});
           }
-          size_t at = enc.begin(OP_DIAG, 0, 0, (int)(j - i), 0, 0, 0, 0);
-          DiagHdr hd{};
-          for (int k2 = 0; k2 < 6; ++k2) hd.nUR[k2] = (int32_t)ur[k2].size();
-          hd.nUC = (int32_t)uc.size();
-          hd.nTR = (int32_t)tr.size();
-          hd.nTC = (int32_t)tc.size();
-          hd.nRR = (int32_t)rr.size();
-          hd.slot = uniform_ok ? pd.ndiag : -1;
-          if (uniform_ok) pd.diag_off[pd.ndiag++] = (uint32_t)prog.ops.size();
-          enc.put(hd);
-          for (int k2 = 0; k2 < 6; ++k2)
-            for (auto& x : ur[k2]) enc.put(x);
-          for (auto* lst : {&uc, &tr, &tc, &rr})
-            for (auto& x : *lst) enc.put(x);
-          enc.end(at);
+          if (!terms.empty()) encode_diag(terms);
           i = j;
           continue;
         }
@@ -476,25 +585,88 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
             if (ri >= 0) { rm |= 1u << ri; rv |= (uint32_t)cv.second << ri; }
             else { fm |= 1ull << cv.first; fv |= (uint64_t)cv.second << cv.first; }
           }
-          int b = ridx(f.q[0]);
+          const int q = f.q[0];
+          int b = ridx(q);
           require(b >= 0, SVB_E_CUDA, "scheduler: U1 target not in registers");
-          size_t at = enc.begin(f.type, b, 0, 0, fm, fv, rm, rv);
-          for (int e = 0; e < 4; ++e) enc.put(cvt<R>(f.c[e]));
+          const cd d1 = dl[q];
+          if (!f.conds.empty()) {
+            // conditional op: pass the pending diagonal through (D^-1 M D)
+            cd M[4] = {f.c[0], f.c[1] * d1, f.c[2] / d1, f.c[3]};
+            for (auto& z : M) z = snap(z);
+            encode_u1(u1_type(M), b, M, fm, fv, rm, rv);
+            ++i;
+            continue;
+          }
+          cd M[4] = {f.c[0], f.c[1] * d1, f.c[2], f.c[3] * d1};  // M * diag(1, d1)
+          dl[q] = cd(1.0, 0.0);
+          if (zero(M[1]) && zero(M[2])) {  // diagonal: defer entirely
+            K *= M[0];
+            dl[q] = snap(M[3] / M[0]);
+            ++i;
+            continue;
+          }
+          if (zero(M[0]) && zero(M[3])) {  // anti-diagonal: plain swap + deferred diag(m01, m10)
+            K *= M[1];
+            dl[q] = snap(M[2] / M[1]);
+            const cd sw[4] = {cd(0.0, 0.0), cd(1.0, 0.0), cd(1.0, 0.0), cd(0.0, 0.0)};
+            encode_u1(OP_U1ANTI, b, sw, 0, 0, 0, 0);
+            ++i;
+            continue;
+          }
+          if (list[i] == last_u1) {  // absorbs K; emitted in full
+            for (auto& z : M) z = snap(z * K);
+            K = cd(1.0, 0.0);
+            encode_u1(u1_type(M), b, M, 0, 0, 0, 0);
+            ++i;
+            continue;
+          }
+          // pivots: the diagonal entry unless it is much smaller than its
+          // neighbour; row 1 prefers an entry equal to p0 (keeps D scalar)
+          const int pc0 = (std::abs(M[0]) >= 0x1p-8 * std::abs(M[1])) ? 0 : 1;
+          const cd p0 = M[pc0];
+          auto close = [](cd x, cd y) { return std::abs(x - y) <= 0x1p-50 * std::abs(y); };
+          int pc1;
+          if (close(M[2], p0) && std::abs(M[2]) >= 0x1p-8 * std::abs(M[3])) pc1 = 0;
+          else if (close(M[3], p0)) pc1 = 1;
+          else pc1 = (std::abs(M[3]) >= 0x1p-8 * std::abs(M[2])) ? 1 : 0;
+          const cd p1 = M[2 + pc1];
+          const cd r0 = snap(M[1 - pc0] / p0), r1 = snap(M[2 + (1 - pc1)] / p1);
+          K *= p0;
+          dl[q] = close(p1, p0) ? cd(1.0, 0.0) : snap(p1 / p0);
+          const bool real = r0.imag() == 0 && r1.imag() == 0;
+          size_t at = enc.begin(real ? OP_U1PR : OP_U1P, b, 0, pc0 | (pc1 << 1), 0, 0, 0, 0);
+          enc.put(cvt<R>(r0));
+          enc.put(cvt<R>(r1));
           enc.end(at);
         } else {
           int b1 = ridx(f.q[0]), b2 = ridx(f.q[1]);
           require(b1 >= 0 && b2 >= 0, SVB_E_CUDA, "scheduler: U2 qubits not in registers");
+          // absorb the pending diagonals of both qubits into the input columns
+          const cd da = dl[f.q[0]], db = dl[f.q[1]];
+          auto colf = [&](int c) { return ((c & 1) ? da : cd(1.0, 0.0)) * ((c & 2) ? db : cd(1.0, 0.0)); };
+          dl[f.q[0]] = dl[f.q[1]] = cd(1.0, 0.0);
           size_t at = enc.begin(f.type, b1, b2, 0, 0, 0, 0, 0);
           if (f.type == OP_U2) {
-            for (int e = 0; e < 16; ++e) enc.put(cvt<R>(f.c[e]));
+            for (int e = 0; e < 16; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(e & 3))));
           } else {
             int32_t s4[4] = {f.src[0], f.src[1], f.src[2], f.src[3]};
             enc.put(s4);
-            for (int e = 0; e < 4; ++e) enc.put(cvt<R>(f.c[e]));
+            for (int e = 0; e < 4; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(f.src[e]))));
           }
           enc.end(at);
         }
         ++i;
+      }
+      if (k + 1 == rounds.size()) {
+        // flush: pending per-qubit diagonals and the global scalar
+        std::vector<DT> terms;
+        for (int q = 0; q < n; ++q) {
+          const cd d1 = snap(dl[q]);
+          if (!(d1.real() == 1.0 && d1.imag() == 0.0)) terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
+        }
+        K = snap(K);
+        if (!(K.real() == 1.0 && K.imag() == 0.0)) terms.push_back(DT{-1, -1, {K, K, K, K}});
+        if (!terms.empty()) encode_diag(terms);
       }
       rd.op_end = (uint32_t)prog.ops.size();
     }
