@@ -603,6 +603,9 @@ constexpr int kStages = 2;
 // i.e. twice the warps per SM for the cheaper type.
 template <typename R> constexpr int kRegBits = 4;
 template <typename R> constexpr int kPassThreads = sizeof(R) == 8 ? 256 : 512;
+// complex128 passes run two CTAs per SM (single-stage ring each, <= 128
+// registers per thread): 16 warps hide the FP64 and shared-memory latency
+template <typename R> constexpr int kPassMinBlocks = sizeof(R) == 8 ? 2 : 1;
 
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
 
@@ -700,8 +703,45 @@ template <typename R, int RB> struct PassCtx {
   uint32_t tid;
   uint32_t sFl_r[kHoist];
   uint64_t Fg_r[kHoist];
+  // single-stage ring: the body calls prefetch_next() once the last round's
+  // layout is in registers, which refills the ring with the next tile
+  cplx<R>* ring;
+  const uint64_t* ldk;
+  const uint32_t* sdk;
+  uint64_t ld_tid, next_base;
+  uint32_t sd_tid, nld;
+  int prefetch, zero_input;
   __device__ PassCtx(const PassDev& p) : pd(p) {}
 };
+
+// Copy (or, for a lazy |0...0>, synthesise) the tile at `base` into `dst`:
+// element j = (tid + k*nthr)*kPer, 16 B per cp.async (one c128 amplitude or
+// an aligned c64 pair); global and smem offsets split into a tid part and a
+// tile-independent k part (tables in shared memory; the swizzle is linear
+// over XOR: slot(tid part ^ k part) = swz(tid part) ^ swz(k part)).
+template <typename R, int RB>
+__device__ __forceinline__ void issue_tile(const PassCtx<R, RB>& c, uint64_t base, cplx<R>* dst) {
+  constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
+  if (c.zero_input) {
+    for (uint32_t k = 0; k < c.nld; ++k) {
+      const uint64_t g = base | c.ld_tid | c.ldk[k];
+      cplx<R>* d = dst + (c.sd_tid ^ c.sdk[k]);
+      d[0] = mk<R>(g == 0 ? R(1) : R(0), R(0));
+      if (kPer == 2) d[1] = mk<R>(R(0), R(0));
+    }
+    return;
+  }
+  const cplx<R>* src = c.state + (base | c.ld_tid);
+  for (uint32_t k = 0; k < c.nld; ++k) cp_async16(dst + (c.sd_tid ^ c.sdk[k]), src + c.ldk[k]);
+}
+
+template <typename R, int RB> __device__ __forceinline__ void prefetch_next(const PassCtx<R, RB>& c) {
+  if (c.prefetch) {
+    __syncthreads();  // every thread holds its last layout: the ring is free
+    issue_tile<R, RB>(c, c.next_base, c.ring);
+    cp_async_commit();
+  }
+}
 
 // Thread constants of round k for the tile at `base`: swizzled local slot base
 // and the fixed global index.
@@ -838,6 +878,7 @@ struct InterpBody {
       uint32_t slot[1 << RB];
       layout_slots<R, RB>(sFl, rd, slot);
       load_slots<R, RB>(a, cur, slot);
+      if (k + 1 == nrounds) prefetch_next<R, RB>(c);
       run_ops<R, RB>(a, Fg, c.ops, rd.op_off, rd.op_end, c.uni);
       if (k + 1 < nrounds) {
         // each slot of a layout is read and rewritten by its owner only, so one
@@ -851,19 +892,22 @@ struct InterpBody {
   }
 };
 
-// Persistent fused pass: one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...
+// Persistent fused pass: each CTA walks tiles blockIdx.x, +gridDim.x, ...
 // Tiles stream HBM -> shared memory with cp.async (LDGSTS, 16 B per thread,
-// lanes on consecutive amplitudes: 512 B per warp request) kStages-1 tiles
-// ahead into an XOR-swizzled ring; warps first evaluate the tile-uniform
-// factors of the pass's diagonal ops, then Body runs the tile's rounds out of
-// shared memory and stores the last layout straight from registers to HBM.
+// lanes on consecutive amplitudes: 512 B per warp request) into an
+// XOR-swizzled ring of `stages` tiles: with 2 stages the next tile is issued
+// at the top of the loop; with 1 stage (two CTAs per SM) the body issues it
+// through prefetch_next() as soon as the last round's layout is in registers.
+// Warps first evaluate the tile-uniform factors of the pass's diagonal ops,
+// then Body runs the tile's rounds out of shared memory and stores the last
+// layout straight from registers to HBM.
+// Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
 template <typename R, int RB, class Body>
 __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
-                                            int zero_input = 0) {
+                                            int zero_input = 0, int stages = kStages) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ PassDev pd;
-  __shared__ cplx<R> uni[kMaxDiag * kUniStride];
   __shared__ uint64_t s_ldk[32];
   __shared__ uint32_t s_sdk[32];
   {
@@ -874,12 +918,13 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   __syncthreads();
   // stage this pass's op stream after the tile ring; `ops` is rebased so that
   // stream offsets index shared memory
-  const uint32_t ring_bytes = (uint32_t)kStages * ((uint32_t)sizeof(cplx<R>) << pd.m);
+  const uint32_t ring_bytes = (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << pd.m);
   {
     const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
     int4* dst = reinterpret_cast<int4*>(smraw + ring_bytes);
     for (uint32_t i = threadIdx.x; i < pd.ops_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
   }
+  cplx<R>* uni = reinterpret_cast<cplx<R>*>(smraw + ring_bytes + ((pd.ops_bytes + 15u) & ~15u));
   PassCtx<R, RB> c(pd);
   c.state = state;
   c.ops = smraw + ring_bytes - pd.ops_begin;
@@ -890,15 +935,11 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   const int m = pd.m, nrounds = pd.nrounds, ndiag = pd.ndiag;
   const uint32_t T = 1u << m;
   cplx<R>* ring = reinterpret_cast<cplx<R>*>(smraw);
-  // loads: element j = (tid + k*nthr)*kPer; 16 B per copy (one c128 amplitude
-  // or an aligned c64 pair); global and smem offsets split into a tid part and
-  // a tile-independent k part (tables in shared memory)
   constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
   const int lo_bits = (31 - __clz(nthr)) + (kPer == 2 ? 1 : 0);
   uint64_t ld_tid = 0;
   for (int l = 0; l < lo_bits; ++l)
     if (((tid * kPer) >> l) & 1u) ld_tid |= 1ull << pd.pos[l];
-  const uint32_t sd_tid = swz<R>(tid * kPer);
   const uint32_t nld = T / (nthr * kPer);
   if (tid < nld) {
     uint64_t g = 0;
@@ -908,6 +949,15 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     s_ldk[tid] = g;
     s_sdk[tid] = swz<R>(j);
   }
+  c.ring = ring;
+  c.ldk = s_ldk;
+  c.sdk = s_sdk;
+  c.ld_tid = ld_tid;
+  c.sd_tid = swz<R>(tid * kPer);
+  c.nld = nld;
+  c.zero_input = zero_input;
+  c.prefetch = 0;
+  c.next_base = 0;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PassCtx<R, RB>::kHoist; ++k) {
@@ -917,28 +967,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
       c.sFl_r[k] = swz<R>(Fl);
     }
   }
-  auto issue = [&](uint64_t base, int b) {
-    cplx<R>* dst = ring + (size_t)b * T;
-    if (zero_input) {  // lazy |0...0>: synthesise the tile instead of reading HBM
-      for (uint32_t k = 0; k < nld; ++k) {
-        const uint64_t g = base | ld_tid | s_ldk[k];
-        cplx<R>* d = dst + (sd_tid ^ s_sdk[k]);
-        d[0] = mk<R>(g == 0 ? R(1) : R(0), R(0));
-        if (kPer == 2) d[1] = mk<R>(R(0), R(0));
-      }
-      return;
-    }
-    const cplx<R>* src = state + (base | ld_tid);
-    // swizzle is linear over XOR: slot(tid part ^ k part) = swz(tid part) ^ swz(k part)
-    for (uint32_t k = 0; k < nld; ++k) cp_async16(dst + (sd_tid ^ s_sdk[k]), src + s_ldk[k]);
-  };
   const uint32_t t0 = blockIdx.x;
-#pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
-    const uint32_t ts = t0 + (uint32_t)s * gridDim.x;
-    if (ts < ntiles) issue(tile_base_warp(pd, ts, lane), s);
-    cp_async_commit();
-  }
+  if (t0 < ntiles) issue_tile<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
+  cp_async_commit();
   // tile-independent per-thread constants of the body (e.g. products of
   // diagonal factors that depend only on the thread's own local bits)
   typename Body::template State<R, RB> bs;
@@ -946,25 +977,48 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   cplx<R> a[1 << RB];
   int it = 0;
   for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
-    const uint32_t tn = t + (uint32_t)(kStages - 1) * gridDim.x;
-    if (tn < ntiles) issue(tile_base_warp(pd, tn, lane), (it + kStages - 1) % kStages);
-    cp_async_commit();
+    const uint32_t tn = t + gridDim.x;
+    if (stages > 1) {
+      if (tn < ntiles) issue_tile<R, RB>(c, tile_base_warp(pd, tn, lane), ring + (size_t)((it + 1) & 1) * T);
+      cp_async_commit();
+    }
     const uint64_t base = tile_base_warp(pd, t, lane);
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
       diag_uniform_items<R, RB>(c.ops, pd.diag_off, ndiag, base, uni, warp, nwarps, lane);
-    cp_async_wait<kStages - 1>();
+    if (stages > 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
-    Body::template tile<R, RB>(pass, c, a, ring + (size_t)(it % kStages) * T, base, bs);
+    if (stages == 1) {
+      c.prefetch = tn < ntiles;
+      if (c.prefetch) c.next_base = tile_base_warp(pd, tn, lane);
+    }
+    Body::template tile<R, RB>(pass, c, a, ring + (size_t)(stages > 1 ? (it & 1) : 0) * T, base, bs);
     __syncthreads();  // ring slot and uniform factors are rewritten next tile
   }
   cp_async_wait<0>();
 }
 
 template <typename R, int RB>
-__global__ void __launch_bounds__(kPassThreads<R>, 1)
+__global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
     k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
-           uint32_t ntiles, int zero_input) {
-  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input);
+           uint32_t ntiles, int zero_input, int stages) {
+  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input, stages);
+}
+
+// Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM
+// when the op stream fits the per-CTA shared memory budget, else two stages
+// and one CTA per SM.  Returns the dynamic shared memory bytes.
+template <typename R>
+__host__ __device__ inline uint32_t pass_smem(int m, uint32_t ops_bytes, int ndiag, int stages) {
+  return (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << m) + ((ops_bytes + 15u) & ~15u) +
+         (uint32_t)ndiag * kUniStride * (uint32_t)sizeof(cplx<R>);
+}
+constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
+template <typename R>
+__host__ __device__ inline int pass_stages(int m, uint32_t ops_bytes, int ndiag) {
+  if (kPassMinBlocks<R> < 2) return 2;
+  const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
+  return pass_smem<R>(m, ops_bytes, ndiag, 1) <= per_cta ? 1 : 2;
 }
 
 }  // namespace svb

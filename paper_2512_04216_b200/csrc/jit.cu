@@ -270,9 +270,20 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
   for (int k = 0; k < pd.nrounds; ++k) {
     const RoundDev& rd = pd.rounds[k];
     o << "    // round " << k << "\n"
-      << "    svb::round_fixed<R, RB>(c, " << k << ", base, sFl, Fg);\n"
-      << "    svb::layout_slots<R, RB>(sFl, c.pd.rounds[" << k << "], slot);\n"
-      << "    svb::load_slots<R, RB>(a, cur, slot);\n";
+      << "    svb::round_fixed<R, RB>(c, " << k << ", base, sFl, Fg);\n";
+    // layout constants are known here: slot(v) = sFl ^ K[v] (GF(2)-linear
+    // swizzle), global offset(v) = G[v]; immediates keep them out of registers
+    uint32_t K[1 << 5];
+    uint64_t G[1 << 5];
+    K[0] = 0;
+    G[0] = 0;
+    for (int i = 0; i < RB; ++i)
+      for (int v = 0; v < (1 << i); ++v) {
+        K[v | (1 << i)] = K[v] ^ swz<R>(1u << rd.reg_local[i]);
+        G[v | (1 << i)] = G[v] | (1ull << pd.pos[rd.reg_local[i]]);
+      }
+    for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+    if (k + 1 == pd.nrounds) o << "    svb::prefetch_next<R, RB>(c);\n";
     uint32_t off = rd.op_off;
     while (off < rd.op_end) {
       OpHdr h;
@@ -341,10 +352,14 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       }
       off += h.bytes;
     }
-    if (k + 1 < pd.nrounds)
-      o << "    svb::store_slots<R, RB>(a, cur, slot);\n    __syncthreads();\n";
-    else
-      o << "    svb::store_global<R, RB>(c.state, Fg, c.pd, c.pd.rounds[" << k << "], a);\n";
+    if (k + 1 < pd.nrounds) {
+      for (int v = 0; v < (1 << RB); ++v) o << "    cur[sFl ^ " << K[v] << "u] = a[" << v << "];\n";
+      o << "    __syncthreads();\n";
+    } else {
+      o << "    { svb::cplx<R>* g0 = c.state + Fg;\n";
+      for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << G[v] << "ull, a[" << v << "]);\n";
+      o << "    }\n";
+    }
   }
   o << "    } break;\n";
   (void)RB;
@@ -381,18 +396,18 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p) {
        "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void tile(int pass, const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
        "svb::cplx<R>* cur, uint64_t base, const State<R, RB>& st) {\n"
-       "    uint32_t sFl; uint64_t Fg; uint32_t slot[1 << RB];\n    (void)st;\n    switch (0) {\n";
+       "    uint32_t sFl; uint64_t Fg;\n    (void)st;\n    switch (0) {\n";
   std::string b = body.str();
   const std::string from = "    case " + std::to_string(p) + ": {";
   const size_t at = b.find(from);
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R>
-    << ", 1) svb_jit(svb::cplx<R>* __restrict__ state, "
+  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << kPassMinBlocks<R>
+    << ") svb_jit(svb::cplx<R>* __restrict__ state, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
-       "int zero_input) {\n"
+       "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input);\n}\n";
+    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input, stages);\n}\n";
   return o.str();
 }
 
@@ -522,20 +537,23 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);
-    const unsigned smem = (unsigned)(kStages * (size_t)tile_bytes_of<R>(pd.m) + pd.ops_bytes);
+    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag);
+    const unsigned grid =
+        (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
+    const unsigned smem = pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, stages);
     CUfunction f = fns[p];
     // per-function attribute: always the maximum (no race between threads)
-    const int cap = (int)(kStages * (size_t)tile_bytes_of<R>(12 + (sizeof(R) == 4)) + kMaxPassOpBytes);
+    const int cap = (int)pass_smem<R>(12 + (sizeof(R) == 4), kMaxPassOpBytes, kMaxDiag, 2);
     if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, cap) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
+    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
     cplx<R>* s = state;
     const PassDev* pdp = dpass + p;
     const uint8_t* ob = dops;
     uint32_t nt = (uint32_t)tiles;
     int pass = 0;
     int zin = (zero_input && p == 0) ? 1 : 0;
-    void* args[] = {&s, &pdp, &ob, &nt, &pass, &zin};
+    void* args[] = {&s, &pdp, &ob, &nt, &pass, &zin, &stages};
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
     if (dr.launch(f, grid, 1, 1, threads, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS)
