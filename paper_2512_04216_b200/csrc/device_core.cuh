@@ -4,6 +4,7 @@
 // includes here: NVRTC compiles this header as-is.
 #pragma once
 #ifndef __CUDACC_RTC__
+#include <stddef.h>
 #include <stdint.h>
 #else
 typedef unsigned long long uint64_t;
@@ -60,6 +61,10 @@ struct alignas(16) OpHdr {
   uint32_t rmask, rval, bytes, pad;
 };
 static_assert(sizeof(OpHdr) == 48, "OpHdr layout");
+constexpr uint32_t kOpHdrBytesOff = 40;  // offsetof(OpHdr, bytes) (no offsetof under NVRTC)
+#ifndef __CUDACC_RTC__
+static_assert(offsetof(OpHdr, bytes) == kOpHdrBytesOff, "OpHdr layout");
+#endif
 
 // Diagonal factor d[bit(qa) + 2 bit(qb)]; ra/rb = register bit or -1 (then
 // the bit is read from the fixed global index at position qa/qb; q = -1 -> 0).
@@ -706,6 +711,8 @@ template <typename R, int RB> struct PassCtx {
   // single-stage ring: the body calls prefetch_next() once the last round's
   // layout is in registers, which refills the ring with the next tile
   cplx<R>* ring;
+  cplx<R>* pro;        // per-thread prologue slots, [slot][thread] (shared memory)
+  uint32_t nthr;
   const uint64_t* ldk;
   const uint32_t* sdk;
   uint64_t ld_tid, next_base;
@@ -905,30 +912,51 @@ struct InterpBody {
 template <typename R, int RB, class Body>
 __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
-                                            int zero_input = 0, int stages = kStages) {
+                                            int zero_input = 0, int stages = kStages, int ops_mode = 0,
+                                            int nslots = 0) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ PassDev pd;
   __shared__ uint64_t s_ldk[32];
   __shared__ uint32_t s_sdk[32];
+  __shared__ uint32_t s_doff[kMaxDiag];  // staged offsets of the uniform DIAG payloads
   {
     const int4* src = reinterpret_cast<const int4*>(pdg);
     int4* dst = reinterpret_cast<int4*>(&pd);
     for (int i = threadIdx.x; i < (int)(sizeof(PassDev) / 16); i += blockDim.x) dst[i] = __ldg(src + i);
   }
   __syncthreads();
-  // stage this pass's op stream after the tile ring; `ops` is rebased so that
-  // stream offsets index shared memory
+  // Stage the op stream after the tile ring: ops_mode 0 copies this pass's
+  // whole slice (offsets rebased so that stream offsets index shared memory);
+  // ops_mode 1 (bodies with immediate coefficients) packs only the DIAG
+  // payloads that have uniform slots.
   const uint32_t ring_bytes = (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << pd.m);
-  {
+  uint32_t staged = 0;
+  if (ops_mode == 0) {
     const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
     int4* dst = reinterpret_cast<int4*>(smraw + ring_bytes);
     for (uint32_t i = threadIdx.x; i < pd.ops_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    for (int d = threadIdx.x; d < pd.ndiag; d += blockDim.x) s_doff[d] = pd.diag_off[d] - pd.ops_begin;
+    staged = pd.ops_bytes;
+  } else {
+    for (int d = 0; d < pd.ndiag; ++d) {
+      const uint32_t off = pd.diag_off[d];
+      const uint32_t bytes = __ldg(reinterpret_cast<const uint32_t*>(ops_g + off - sizeof(OpHdr) + kOpHdrBytesOff)) -
+                             (uint32_t)sizeof(OpHdr);
+      const int4* src = reinterpret_cast<const int4*>(ops_g + off);
+      int4* dst = reinterpret_cast<int4*>(smraw + ring_bytes + staged);
+      for (uint32_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+      if (threadIdx.x == 0) s_doff[d] = staged;
+      staged += bytes;
+    }
   }
-  cplx<R>* uni = reinterpret_cast<cplx<R>*>(smraw + ring_bytes + ((pd.ops_bytes + 15u) & ~15u));
+  cplx<R>* uni = reinterpret_cast<cplx<R>*>(smraw + ring_bytes + ((staged + 15u) & ~15u));
   PassCtx<R, RB> c(pd);
   c.state = state;
-  c.ops = smraw + ring_bytes - pd.ops_begin;
+  c.ops = smraw + ring_bytes - pd.ops_begin;  // ops_mode 0 only
   c.uni = uni;
+  c.pro = uni + pd.ndiag * kUniStride;
+  c.nthr = blockDim.x;
+  (void)nslots;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
@@ -984,7 +1012,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
-      diag_uniform_items<R, RB>(c.ops, pd.diag_off, ndiag, base, uni, warp, nwarps, lane);
+      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, ndiag, base, uni, warp, nwarps, lane);
     if (stages > 1) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
@@ -1002,23 +1030,25 @@ template <typename R, int RB>
 __global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
     k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
            uint32_t ntiles, int zero_input, int stages) {
-  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input, stages);
+  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
 }
 
 // Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM
 // when the op stream fits the per-CTA shared memory budget, else two stages
 // and one CTA per SM.  Returns the dynamic shared memory bytes.
 template <typename R>
-__host__ __device__ inline uint32_t pass_smem(int m, uint32_t ops_bytes, int ndiag, int stages) {
-  return (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << m) + ((ops_bytes + 15u) & ~15u) +
-         (uint32_t)ndiag * kUniStride * (uint32_t)sizeof(cplx<R>);
+__host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages) {
+  const uint32_t nthr = 1u << (m - kRegBits<R>);
+  return (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
+         ((uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
+constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
-__host__ __device__ inline int pass_stages(int m, uint32_t ops_bytes, int ndiag) {
+__host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots) {
   if (kPassMinBlocks<R> < 2) return 2;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
-  return pass_smem<R>(m, ops_bytes, ndiag, 1) <= per_cta ? 1 : 2;
+  return pass_smem<R>(m, staged_ops, ndiag, nslots, 1) <= per_cta ? 1 : 2;
 }
 
 }  // namespace svb

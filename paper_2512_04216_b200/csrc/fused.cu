@@ -182,8 +182,7 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
   // launching different programs)
   static std::once_flag once_pass;
   std::call_once(once_pass, [] {
-    const int cap = (int)pass_smem<R>(12 + (sizeof(R) == 4), kMaxPassOpBytes, kMaxDiag, 2);
-    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxPerCTA);
     cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   });
   int dev = 0, nsm = 148;
@@ -197,12 +196,12 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
-    const int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag);
+    const int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0);
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));
-    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, stages), st>>>(
+    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages), st>>>(
         state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);

@@ -210,8 +210,9 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
         P << "      acc = svb::cmul<R>(acc, svb::csel<R>((int)((F >> " << (int)tr[k].qb << ") & 1ull), "
           << dref(tr + k, half) << ", " << dref(tr + k, 2 + half) << "));\n";
       }
-      P << "      st.v[" << slot << "] = acc; }\n";
-      o << "      D" << half << "_" << i << " = svb::cmul<R>(D" << half << "_" << i << ", st.v[" << slot << "]);\n";
+      P << "      c.pro[" << slot << " * c.nthr + c.tid] = acc; }\n";
+      o << "      D" << half << "_" << i << " = svb::cmul<R>(D" << half << "_" << i << ", c.pro[" << slot
+        << " * c.nthr + c.tid]);\n";
     }
   }
   for (int k = 0; k < h.nTC; ++k) {
@@ -316,12 +317,17 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         case OP_U1X:
         case OP_U1:
         case OP_U1ANTI: {
+          const char* fn = h.kind == OP_U1R ? "u1_real" : h.kind == OP_U1X ? "u1_rx" : h.kind == OP_U1 ? "u1_dense" : "u1_anti";
+          if (imm) {  // constant local array: folded into immediates
+            o << "    " << guard << "{ const svb::cplx<R> M[4] = {";
+            for (int e = 0; e < 4; ++e) o << (e ? ", " : "") << cimm<R>(coef[e]);
+            o << "}; svb::" << fn << "<R, RB, " << h.a << ", " << cond << ">(a, M, " << rm << "); }\n";
+            break;
+          }
           // structure-only: coefficients stay in the op payload (shared memory), so
           // circuits that differ only in angles share one compiled kernel
-          const char* fn = h.kind == OP_U1R ? "u1_real" : h.kind == OP_U1X ? "u1_rx" : h.kind == OP_U1 ? "u1_dense" : "u1_anti";
           o << "    " << guard << "svb::" << fn << "<R, RB, " << h.a << ", " << cond
             << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
-          (void)coef;
           break;
         }
         case OP_U1P:
@@ -339,10 +345,26 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
           break;
         }
         case OP_U2:
+          if (imm) {
+            o << "    " << guard << "{ const svb::cplx<R> M[16] = {";
+            for (int e = 0; e < 16; ++e) o << (e ? ", " : "") << cimm<R>(coef[e]);
+            o << "}; svb::u2_dense<R, RB, " << h.a << ", " << h.b << ">(a, M, " << rm << "); }\n";
+            break;
+          }
           o << "    " << guard << "svb::u2_dense<R, RB, " << h.a << ", " << h.b
             << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "), " << rm << ");\n";
           break;
         case OP_PERM2:
+          if (imm) {
+            int32_t src4[4];
+            std::memcpy(src4, prog.ops.data() + pay, sizeof src4);
+            const cplx<R>* ph = reinterpret_cast<const cplx<R>*>(prog.ops.data() + pay + 16);
+            o << "    " << guard << "{ const int32_t S[4] = {" << src4[0] << ", " << src4[1] << ", " << src4[2] << ", "
+              << src4[3] << "}; const svb::cplx<R> P[4] = {";
+            for (int e = 0; e < 4; ++e) o << (e ? ", " : "") << cimm<R>(ph[e]);
+            o << "}; svb::u2_perm<R, RB, " << h.a << ", " << h.b << ">(a, S, P, " << rm << "); }\n";
+            break;
+          }
           o << "    " << guard << "svb::u2_perm<R, RB, " << h.a << ", " << h.b
             << ">(a, reinterpret_cast<const int32_t*>(c.ops + " << pay
             << "), reinterpret_cast<const svb::cplx<R>*>(c.ops + " << (pay + 16) << "), " << rm << ");\n";
@@ -379,17 +401,23 @@ bool jit_available() {
 // structure-only code that circuits differing only in angles share.
 constexpr int kImmMinQubits = 28;
 
-template <typename R> std::string jit_source_pass(const Program& prog, int p) {
+// `nslots`: per-thread prologue slots (shared memory, [slot][thread]);
+// `imm`: coefficients are immediates, so only the uniform DIAG payloads are
+// staged in shared memory (ops_mode 1).
+template <typename R> std::string jit_source_pass(const Program& prog, int p, int* nslots, bool* imm_out) {
   constexpr int RB = kRegBits<R>;
   std::ostringstream body, pro;
   PrologueCtx pc;
   pc.o = &pro;
   const PassDev& pd0 = prog.passes[p];
-  emit_body<R>(body, prog, p, RB, pd0.m + pd0.nout >= kImmMinQubits, pc);
+  const bool imm = pd0.m + pd0.nout >= kImmMinQubits;
+  emit_body<R>(body, prog, p, RB, imm, pc);
+  if (nslots) *nslots = pc.nslots;
+  if (imm_out) *imm_out = imm;
   std::ostringstream o;
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
   o << "struct PassBody {\n"
-       "  template <typename R, int RB> struct State { svb::cplx<R> v[" << (pc.nslots ? pc.nslots : 1) << "]; };\n"
+       "  template <typename R, int RB> struct State {};\n"
        "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void prologue(const svb::PassCtx<R, RB>& c, State<R, RB>& st) {\n"
     << pro.str() << "    (void)c; (void)st;\n  }\n"
@@ -407,7 +435,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p) {
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input, stages);\n}\n";
+    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
+    << pc.nslots << ");\n}\n";
   return o.str();
 }
 
@@ -467,12 +496,26 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
   const size_t np = prog.passes.size();
   std::vector<std::string> srcs(np), keys(np);
   std::vector<CUfunction> fns(np, nullptr);
+  std::vector<int> nslots(np, 0);
+  std::vector<uint32_t> staged(np, 0);
   const uint64_t salt = fnv1a(svb_device_core_src, fnv1a("svb-jit-v1 sm_100a"));
   std::vector<size_t> todo;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t p = 0; p < np; ++p) {
-      srcs[p] = jit_source_pass<R>(prog, (int)p);
+      bool imm = false;
+      srcs[p] = jit_source_pass<R>(prog, (int)p, &nslots[p], &imm);
+      const PassDev& pd = prog.passes[p];
+      staged[p] = pd.ops_bytes;
+      if (imm) {  // only the uniform DIAG payloads are staged
+        staged[p] = 0;
+        for (int d = 0; d < pd.ndiag; ++d) {
+          OpHdr h;
+          std::memcpy(&h, prog.ops.data() + pd.diag_off[d] - sizeof(OpHdr), sizeof h);
+          staged[p] += h.bytes - (uint32_t)sizeof(OpHdr);
+        }
+      }
+      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2) > kSmemMaxPerCTA) return false;
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
@@ -537,14 +580,13 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag);
+    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p]);
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
-    const unsigned smem = pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, stages);
+    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages);
     CUfunction f = fns[p];
     // per-function attribute: always the maximum (no race between threads)
-    const int cap = (int)pass_smem<R>(12 + (sizeof(R) == 4), kMaxPassOpBytes, kMaxDiag, 2);
-    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, cap) != CUDA_SUCCESS)
+    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
     dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
     cplx<R>* s = state;
@@ -584,10 +626,10 @@ extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng
     std::vector<std::string> srcs;
     if (precision == SVB_C128) {
       Program p = build_program<double>(n, gates, ng, o);
-      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<double>(p, (int)k));
+      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<double>(p, (int)k, nullptr, nullptr));
     } else {
       Program p = build_program<float>(n, gates, ng, o);
-      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<float>(p, (int)k));
+      for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<float>(p, (int)k, nullptr, nullptr));
     }
     if (std::getenv("SVB_JIT_DUMP") && !srcs.empty()) {
       FILE* f = std::fopen(std::getenv("SVB_JIT_DUMP"), "w");
