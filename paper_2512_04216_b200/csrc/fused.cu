@@ -110,6 +110,77 @@ __global__ void __launch_bounds__(256) k_permute(const cplx<R>* __restrict__ in,
   }
 }
 
+// complex128 full tiles (4096 amplitudes, 256 threads): persistent CTA per SM
+// with a 2-stage cp.async ring, so tile t+1 streams in while tile t is
+// permuted through shared memory and stored.
+__global__ void __launch_bounds__(256, 1) k_permute_pipe(const cplx<double>* __restrict__ in,
+                                                        cplx<double>* __restrict__ out, const PermDev pd,
+                                                        uint64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ uint64_t in_lo[64], in_hi[64], out_lo[64], out_hi[64];
+  __shared__ uint32_t src_lo[64], src_hi[64];
+  __shared__ uint64_t t_in[48], t_out[48];
+  cplx<double>* ring = reinterpret_cast<cplx<double>*>(smraw);
+  constexpr int lb = 6;  // ml == 12
+  for (int x = threadIdx.x; x < 64; x += blockDim.x) {
+    uint64_t a = 0, b = 0, c = 0, d = 0;
+    uint32_t e = 0, f = 0;
+    for (int l = 0; l < lb; ++l)
+      if ((x >> l) & 1) {
+        a |= 1ull << pd.lin[l];
+        c |= 1ull << pd.lout_pos[l];
+        e |= 1u << pd.lout_src[l];
+        b |= 1ull << pd.lin[lb + l];
+        d |= 1ull << pd.lout_pos[lb + l];
+        f |= 1u << pd.lout_src[lb + l];
+      }
+    in_lo[x] = a; in_hi[x] = b; out_lo[x] = c; out_hi[x] = d; src_lo[x] = e; src_hi[x] = f;
+  }
+  for (int i = threadIdx.x; i < pd.nout; i += blockDim.x) {
+    t_in[i] = 1ull << pd.outin[i];
+    t_out[i] = 1ull << pd.dest[pd.outin[i]];
+  }
+  __syncthreads();
+  const uint32_t tid = threadIdx.x;
+  auto bases = [&](uint64_t t, uint64_t& bin, uint64_t& bout) {
+    bin = 0;
+    bout = 0;
+    for (int i = 0; i < pd.nout; ++i)
+      if ((t >> i) & 1ull) { bin |= t_in[i]; bout |= t_out[i]; }
+  };
+  auto issue = [&](uint64_t t, int b) {
+    uint64_t bin, bout;
+    bases(t, bin, bout);
+    cplx<double>* dst = ring + (size_t)b * 4096;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t j = tid + 256u * k;
+      cp_async16(dst + swz<double>(j), in + (bin | in_lo[j & 63u] | in_hi[j >> lb]));
+    }
+  };
+  uint64_t t = blockIdx.x;
+  if (t < ntiles) issue(t, 0);
+  cp_async_commit();
+  for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+    const uint64_t tn = t + gridDim.x;
+    if (tn < ntiles) issue(tn, (it + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    uint64_t bin, bout;
+    bases(t, bin, bout);
+    const cplx<double>* cur = ring + (size_t)(it & 1) * 4096;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t o = tid + 256u * k;
+      const uint32_t j = src_lo[o & 63u] | src_hi[o >> lb];
+      __stcs(out + (bout | out_lo[o & 63u] | out_hi[o >> lb]), cur[swz<double>(j)]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
 static PermDev make_perm(int n, const std::vector<int>& dest) {
   PermDev pd{};
   pd.n = n;
@@ -226,10 +297,24 @@ static void launch_permute(cplx<R>** state, cplx<R>** spare, int n, const std::v
   std::call_once(once_perm, [] {
     cudaFuncSetAttribute(k_permute<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(cplx<R>) << 12));
   });
-  const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * 3);
   Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
   if (pf) pf->begin(st, 1, 2.0 * (double)bytes);
-  k_permute<R><<<grid, 256, smem, st>>>(*state, out, pd, tiles);
+  if constexpr (sizeof(R) == 8) {
+    if (pd.ml == 12) {
+      static std::once_flag once_pipe;
+      std::call_once(once_pipe, [] {
+        cudaFuncSetAttribute(k_permute_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 16);
+      });
+      const unsigned g1 = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);
+      k_permute_pipe<<<g1, 256, 2 * 4096 * 16, st>>>(*state, out, pd, tiles);
+    } else {
+      const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * 3);
+      k_permute<R><<<grid, 256, smem, st>>>(*state, out, pd, tiles);
+    }
+  } else {
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * 3);
+    k_permute<R><<<grid, 256, smem, st>>>(*state, out, pd, tiles);
+  }
   SVB_CHECK_LAUNCH();
   if (pf) pf->end(st);
   // swap buffers rather than copy back (a copy would double the traffic)
