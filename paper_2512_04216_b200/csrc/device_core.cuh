@@ -742,10 +742,10 @@ __device__ __forceinline__ void issue_tile(const PassCtx<R, RB>& c, uint64_t bas
   for (uint32_t k = 0; k < c.nld; ++k) cp_async16(dst + (c.sd_tid ^ c.sdk[k]), src + c.ldk[k]);
 }
 
-template <typename R, int RB> __device__ __forceinline__ void prefetch_next(const PassCtx<R, RB>& c) {
+template <typename R, int RB, class Body> __device__ __forceinline__ void prefetch_next(const PassCtx<R, RB>& c) {
   if (c.prefetch) {
     __syncthreads();  // every thread holds its last layout: the ring is free
-    issue_tile<R, RB>(c, c.next_base, c.ring);
+    Body::template issue<R, RB>(c, c.next_base, c.ring);
     cp_async_commit();
   }
 }
@@ -872,6 +872,10 @@ __device__ __forceinline__ void mul_rr(cplx<R>* a, cplx<R> e0, cplx<R> e1, cplx<
 struct InterpBody {
   template <typename R, int RB> struct State {};
   template <typename R, int RB>
+  __device__ static __forceinline__ void issue(const PassCtx<R, RB>& c, uint64_t base, cplx<R>* dst) {
+    issue_tile<R, RB>(c, base, dst);
+  }
+  template <typename R, int RB>
   __device__ static __forceinline__ void prologue(const PassCtx<R, RB>&, State<R, RB>&) {}
   template <typename R, int RB>
   __device__ static __forceinline__ void tile(int, const PassCtx<R, RB>& c, cplx<R>* a, cplx<R>* cur,
@@ -885,7 +889,7 @@ struct InterpBody {
       uint32_t slot[1 << RB];
       layout_slots<R, RB>(sFl, rd, slot);
       load_slots<R, RB>(a, cur, slot);
-      if (k + 1 == nrounds) prefetch_next<R, RB>(c);
+      if (k + 1 == nrounds) prefetch_next<R, RB, InterpBody>(c);
       run_ops<R, RB>(a, Fg, c.ops, rd.op_off, rd.op_end, c.uni);
       if (k + 1 < nrounds) {
         // each slot of a layout is read and rewritten by its owner only, so one
@@ -954,7 +958,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   c.state = state;
   c.ops = smraw + ring_bytes - pd.ops_begin;  // ops_mode 0 only
   c.uni = uni;
-  c.pro = uni + pd.ndiag * kUniStride;
+  // uniform slots are double-buffered by tile parity (the next tile's factors
+  // are written while slow warps may still read this tile's)
+  c.pro = uni + 2 * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   (void)nslots;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
@@ -996,7 +1002,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     }
   }
   const uint32_t t0 = blockIdx.x;
-  if (t0 < ntiles) issue_tile<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
+  if (t0 < ntiles) Body::template issue<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
   cp_async_commit();
   // tile-independent per-thread constants of the body (e.g. products of
   // diagonal factors that depend only on the thread's own local bits)
@@ -1007,12 +1013,15 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
     const uint32_t tn = t + gridDim.x;
     if (stages > 1) {
-      if (tn < ntiles) issue_tile<R, RB>(c, tile_base_warp(pd, tn, lane), ring + (size_t)((it + 1) & 1) * T);
+      if (tn < ntiles)
+        Body::template issue<R, RB>(c, tile_base_warp(pd, tn, lane), ring + (size_t)((it + 1) & 1) * T);
       cp_async_commit();
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
+    c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
-      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, ndiag, base, uni, warp, nwarps, lane);
+      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, ndiag, base, const_cast<cplx<R>*>(c.uni), warp,
+                                nwarps, lane);
     if (stages > 1) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
@@ -1021,7 +1030,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
       if (c.prefetch) c.next_base = tile_base_warp(pd, tn, lane);
     }
     Body::template tile<R, RB>(pass, c, a, ring + (size_t)(stages > 1 ? (it & 1) : 0) * T, base, bs);
-    __syncthreads();  // ring slot and uniform factors are rewritten next tile
+    // two stages: the ring slot is rewritten by the next iteration's issue.
+    // One stage: prefetch_next() already fenced the ring, and the uniform
+    // slots alternate, so the next tile's leading barrier is enough.
+    if (stages > 1) __syncthreads();
   }
   cp_async_wait<0>();
 }
@@ -1040,7 +1052,7 @@ template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
   return (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
-         ((uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>);
+         (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;

@@ -284,7 +284,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         G[v | (1 << i)] = G[v] | (1ull << pd.pos[rd.reg_local[i]]);
       }
     for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
-    if (k + 1 == pd.nrounds) o << "    svb::prefetch_next<R, RB>(c);\n";
+    if (k + 1 == pd.nrounds) o << "    svb::prefetch_next<R, RB, PassBody>(c);\n";
     uint32_t off = rd.op_off;
     while (off < rd.op_end) {
       OpHdr h;
@@ -416,9 +416,35 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (imm_out) *imm_out = imm;
   std::ostringstream o;
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
+  // tile loads with the layout's offsets as immediates (see issue_tile)
+  std::ostringstream iss;
+  {
+    const int m = pd0.m;
+    const uint32_t nthr = 1u << (m - RB);
+    const int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
+    int lo_bits = 0;
+    while ((1u << lo_bits) < nthr) ++lo_bits;
+    lo_bits += (kPer == 2 ? 1 : 0);
+    const uint32_t nld = (1u << m) / (nthr * (uint32_t)kPer);
+    iss << "  template <typename R, int RB>\n"
+           "  __device__ static __forceinline__ void issue(const svb::PassCtx<R, RB>& c, uint64_t base, "
+           "svb::cplx<R>* dst) {\n"
+           "    if (c.zero_input) { svb::issue_tile<R, RB>(c, base, dst); return; }\n"
+           "    const svb::cplx<R>* src = c.state + (base | c.ld_tid);\n"
+           "    const uint32_t s0 = c.sd_tid;\n";
+    for (uint32_t k = 0; k < nld; ++k) {
+      const uint32_t j = k * nthr * (uint32_t)kPer;
+      uint64_t g = 0;
+      for (int l = lo_bits; l < m; ++l)
+        if ((j >> l) & 1u) g |= 1ull << pd0.pos[l];
+      iss << "    svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g << "ull);\n";
+    }
+    iss << "  }\n";
+  }
   o << "struct PassBody {\n"
        "  template <typename R, int RB> struct State {};\n"
-       "  template <typename R, int RB>\n"
+    << iss.str()
+    << "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void prologue(const svb::PassCtx<R, RB>& c, State<R, RB>& st) {\n"
     << pro.str() << "    (void)c; (void)st;\n  }\n"
        "  template <typename R, int RB>\n"
