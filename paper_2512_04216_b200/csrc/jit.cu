@@ -199,6 +199,23 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
     }
     for (int half = 0; half < 2; ++half) {
       if (!(half ? any1 : any0)) continue;
+      std::vector<int> terms;
+      for (int k = 0; k < h.nTR; ++k) {
+        if (tr[k].ra != i) continue;
+        if (half == 0 && is1(tr[k].d[0]) && is1(tr[k].d[2])) continue;
+        if (half == 1 && is1(tr[k].d[1]) && is1(tr[k].d[3])) continue;
+        terms.push_back(k);
+      }
+      if (terms.size() <= 2) {  // short chains: a select or one product per tile, no slot
+        std::string f;
+        for (int k : terms) {
+          const std::string sel = "svb::csel<R>((int)((Fg >> " + std::to_string((int)tr[k].qb) + ") & 1ull), " +
+                                  dref(tr + k, half) + ", " + dref(tr + k, 2 + half) + ")";
+          f = f.empty() ? sel : "svb::cmul<R>(" + f + ", " + sel + ")";
+        }
+        o << "      D" << half << "_" << i << " = svb::cmul<R>(D" << half << "_" << i << ", " << f << ");\n";
+        continue;
+      }
       const int slot = pc.nslots++;
       std::ostringstream& P = *pc.o;
       P << "    { svb::cplx<R> acc = svb::mk<R>(R(1), R(0)); const uint64_t F = svb::thread_fixed_g<R, RB>(c, "
@@ -610,6 +627,10 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages);
+    static const bool trace = std::getenv("SVB_TRACE") != nullptr;
+    if (trace)
+      std::fprintf(stderr, "[svb] jit pass %zu: m=%d rounds=%d stages=%d grid=%u smem=%u staged=%u ndiag=%d slots=%d\n",
+                   p, pd.m, pd.nrounds, stages, grid, smem, staged[p], pd.ndiag, nslots[p]);
     CUfunction f = fns[p];
     // per-function attribute: always the maximum (no race between threads)
     if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
