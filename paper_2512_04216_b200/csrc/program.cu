@@ -199,6 +199,19 @@ void emit_block(const Block& b0, std::vector<FOp>& out) {
   out.push_back(f);
 }
 
+// every row has at most one non-zero entry
+bool monomial4(const cd* M) {
+  for (int r = 0; r < 4; ++r) {
+    int nz = 0;
+    for (int c = 0; c < 4; ++c) nz += !zero(snap(M[r * 4 + c]));
+    if (nz > 1) return false;
+  }
+  return true;
+}
+bool monomial2(const cd* G) {
+  return (zero(snap(G[1])) && zero(snap(G[2]))) || (zero(snap(G[0])) && zero(snap(G[3])));
+}
+
 bool is_plain_swap(const svb_gate& g) {
   if (g.k != 2) return false;
   static const int src[4] = {0, 2, 1, 3};
@@ -230,6 +243,10 @@ std::vector<FOp> fuse(int n, const svb_gate* gates, int ng, bool relabel, std::v
     for (int e = 0; e < dim * dim; ++e) G[e] = cd(g.mat[2 * e], g.mat[2 * e + 1]);
     if (g.k == 1) {
       int a = phys[g.qubits[0]];
+      // a dense 1q gate does not enter a monomial (diagonal / permutation) 2q
+      // block: that would turn a cheap cz-like op into a dense 4x4 (four
+      // complex MACs per amplitude instead of one pivoted 1q op)
+      if (open[a] >= 0 && blocks[open[a]].k == 2 && monomial4(blocks[open[a]].M) && !monomial2(G)) close(open[a]);
       if (open[a] >= 0) {
         left_mul_1q(blocks[open[a]], a, G);
       } else {
@@ -292,6 +309,44 @@ template <typename R> struct Encoder {
 };
 
 }  // namespace
+
+// Prologue slots the JIT body of an encoded pass will use (register x
+// thread-bit chains of three or more factors, jit.cu emit_diag), and whether
+// the pass still fits the two-CTA shared memory budget with them.
+template <typename R> bool slots_fit(const Program& prog, const PassDev& pd) {
+  int slots = 0;
+  uint32_t staged = 0;
+  for (int k = 0; k < pd.nrounds; ++k) {
+    uint32_t off = pd.rounds[k].op_off;
+    while (off < pd.rounds[k].op_end) {
+      OpHdr h;
+      std::memcpy(&h, prog.ops.data() + off, sizeof h);
+      if (h.kind == OP_DIAG) {
+        DiagHdr d;
+        std::memcpy(&d, prog.ops.data() + off + sizeof(OpHdr), sizeof d);
+        if (d.slot >= 0) staged += h.bytes - (uint32_t)sizeof(OpHdr);
+        int nskip = d.nUC + d.nUR[0] + d.nUR[1] + d.nUR[2] + d.nUR[3] + d.nUR[4] + d.nUR[5];
+        for (int g = 0; g < d.nUTg; ++g) nskip += d.utn[g];
+        const DiagTerm<R>* tr =
+            reinterpret_cast<const DiagTerm<R>*>(prog.ops.data() + off + sizeof(OpHdr) + sizeof(DiagHdr)) + nskip;
+        for (int i = 0; i < pd.rb; ++i)
+          for (int half = 0; half < 2; ++half) {
+            int cnt = 0;
+            for (int t = 0; t < d.nTR; ++t) {
+              if (tr[t].ra != i) continue;
+              const cplx<R> e0 = tr[t].d[half], e1 = tr[t].d[2 + half];
+              if (!(e0.x == 1 && e0.y == 0 && e1.x == 1 && e1.y == 0)) ++cnt;
+            }
+            if (cnt >= 3) ++slots;
+          }
+      }
+      off += h.bytes;
+    }
+  }
+  if (kPassMinBlocks<R> < 2) return true;
+  const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
+  return pass_smem<R>(pd.m, staged, pd.ndiag, slots, 1) <= per_cta;
+}
 
 template <typename R>
 Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
@@ -384,294 +439,368 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     for (int q = 0; q < n; ++q)
       if (!(S & (1ull << q))) pd.outpos[pd.nout++] = q;
 
-    // ---- split into rounds by register need
-    std::vector<std::pair<uint32_t, std::vector<int>>> rounds;
-    uint32_t req = 0;
-    std::vector<int> cur;
-    for (int idx : placed) {
-      uint32_t need = 0;
-      for (int q = 0; q < n; ++q)
-        if (ops[idx].active & (1ull << q)) need |= 1u << local_of[q];
-      if (__builtin_popcount(req | need) <= RB) {
-        req |= need;
-        cur.push_back(idx);
-      } else {
-        rounds.push_back({req, cur});
-        req = need;
-        cur.assign(1, idx);
+    // Rounds are built with op reordering first; if that needs more
+    // per-thread prologue slots (register x thread-bit products, see jit.cu)
+    // than two CTAs per SM leave room for, the pass is re-encoded in program
+    // order.
+    const PassDev pd_saved = pd;
+    const size_t ops_saved = prog.ops.size();
+    const std::vector<int> skipped_saved = skipped;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool search = opt.round_search && attempt == 0;
+      // ---- split into rounds: each round picks RB register bits and runs every
+      // op (in dependency order, commuting where allowed) whose active qubits
+      // lie in them; the register set is grown greedily, then improved by
+      // single-bit swaps while that runs more ops (same scheme as the tile set)
+      std::vector<std::pair<uint32_t, std::vector<int>>> rounds;
+      {
+        std::vector<int> rem = placed;
+        std::vector<uint32_t> actl(ops.size(), 0);
+        for (int idx : placed)
+          for (int q = 0; q < n; ++q)
+            if (ops[idx].active & (1ull << q)) actl[idx] |= 1u << local_of[q];
+        auto place_r = [&](uint32_t& Rl, bool grow, std::vector<int>* took, std::vector<int>* left) {
+          uint64_t blkA = 0, blkD = 0;
+          int cnt = 0;
+          for (int idx : rem) {
+            const FOp& f = ops[idx];
+            if (!((f.touched & blkA) || (f.active & blkD))) {
+              const uint32_t need = actl[idx] & ~Rl;
+              if (need == 0 || (grow && __builtin_popcount(Rl | need) <= RB)) {
+                Rl |= need;
+                if (took) took->push_back(idx);
+                ++cnt;
+                continue;
+              }
+            }
+            if (left) left->push_back(idx);
+            blkA |= f.active;
+            blkD |= f.touched & ~f.active;
+          }
+          return cnt;
+        };
+        while (!rem.empty()) {
+          uint32_t Rl = 0;
+          int best = place_r(Rl, true, nullptr, nullptr);
+          if (search) {
+            uint32_t cand = 0;
+            for (int idx : rem) cand |= actl[idx];
+            for (int iter = 0; iter < 4 * RB; ++iter) {
+              int gain = 0;
+              uint32_t bestR = Rl;
+              for (uint32_t ins = cand & ~Rl; ins; ins &= ins - 1) {
+                const uint32_t qi = ins & (~ins + 1);
+                if (__builtin_popcount(Rl) < RB) {
+                  uint32_t T = Rl | qi;
+                  const int c2 = place_r(T, false, nullptr, nullptr);
+                  if (c2 > best + gain) { gain = c2 - best; bestR = T; }
+                }
+                for (uint32_t outs = Rl; outs; outs &= outs - 1) {
+                  const uint32_t qo = outs & (~outs + 1);
+                  uint32_t T = (Rl & ~qo) | qi;
+                  const int c2 = place_r(T, false, nullptr, nullptr);
+                  if (c2 > best + gain) { gain = c2 - best; bestR = T; }
+                }
+              }
+              if (gain == 0) break;
+              best += gain;
+              Rl = bestR;
+            }
+          }
+          std::vector<int> took, left;
+          if (search) {
+            place_r(Rl, false, &took, &left);
+          } else {  // in program order: a new round whenever the register need overflows
+            Rl = 0;
+            size_t i = 0;
+            for (; i < rem.size(); ++i) {
+              const uint32_t need = actl[rem[i]];
+              if (__builtin_popcount(Rl | need) > RB) break;
+              Rl |= need;
+              took.push_back(rem[i]);
+            }
+            left.assign(rem.begin() + (long)i, rem.end());
+          }
+          require(!took.empty(), SVB_E_CUDA, "scheduler: empty round");
+          rounds.push_back({Rl, took});
+          rem.swap(left);
+        }
       }
-    }
-    rounds.push_back({req, cur});
-    const uint32_t lane_local = 0x1fu;  // local bits 0..4 are physical 0..4
-    auto fill = [&](uint32_t r) {
-      for (int b = 5; b < m && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
-      for (int b = 0; b < 5 && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
-      return r;
-    };
-    std::vector<uint32_t> regsets;
-    for (auto& rd : rounds) regsets.push_back(fill(rd.first));
-    if (regsets.back() & lane_local) {
-      rounds.push_back({0u, {}});
-      regsets.push_back(fill(0u));
-    }
-    if ((int)rounds.size() > kMaxRounds) {
-      // defer the tail of this pass's ops to the next pass (original order kept)
-      std::vector<int> keep_ops;
-      std::vector<std::pair<uint32_t, std::vector<int>>> kept(rounds.begin(), rounds.begin() + kMaxRounds - 1);
-      std::vector<int> deferred;
-      for (size_t k = kMaxRounds - 1; k < rounds.size(); ++k)
-        deferred.insert(deferred.end(), rounds[k].second.begin(), rounds[k].second.end());
-      rounds = kept;
-      regsets.resize(kMaxRounds - 1);
+      const uint32_t lane_local = 0x1fu;  // local bits 0..4 are physical 0..4
+      auto fill = [&](uint32_t r) {
+        for (int b = 5; b < m && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
+        for (int b = 0; b < 5 && __builtin_popcount(r) < RB; ++b) r |= 1u << b;
+        return r;
+      };
+      std::vector<uint32_t> regsets;
+      for (auto& rd : rounds) regsets.push_back(fill(rd.first));
       if (regsets.back() & lane_local) {
         rounds.push_back({0u, {}});
         regsets.push_back(fill(0u));
       }
-      skipped.insert(skipped.end(), deferred.begin(), deferred.end());
-      std::sort(skipped.begin(), skipped.end());
-    }
+      if ((int)rounds.size() > kMaxRounds) {
+        // defer the tail of this pass's ops to the next pass (original order kept)
+        std::vector<int> keep_ops;
+        std::vector<std::pair<uint32_t, std::vector<int>>> kept(rounds.begin(), rounds.begin() + kMaxRounds - 1);
+        std::vector<int> deferred;
+        for (size_t k = kMaxRounds - 1; k < rounds.size(); ++k)
+          deferred.insert(deferred.end(), rounds[k].second.begin(), rounds[k].second.end());
+        rounds = kept;
+        regsets.resize(kMaxRounds - 1);
+        if (regsets.back() & lane_local) {
+          rounds.push_back({0u, {}});
+          regsets.push_back(fill(0u));
+        }
+        skipped.insert(skipped.end(), deferred.begin(), deferred.end());
+        std::sort(skipped.begin(), skipped.end());
+      }
 
-    // ---- encode the rounds
-    //
-    // Deferred pivot diagonals: an unconditional 1q op M on q (after the
-    // pending diagonal diag(1, dl[q]) of q) is factored as diag(p0, p1) * P,
-    // where each row of P has a unit pivot: y_r = x_pc[r] + ratio_r x_(1-pc[r]).
-    // P costs one complex FMA per amplitude (two real FMAs for a real ratio)
-    // instead of two complex products; diag(p0, p1) = p0 * diag(1, p1/p0) is
-    // carried forward: the scalar p0 into the pass-global K, the rest into dl[q].
-    // Diagonals commute with diagonal ops; a conditional 1q op on q sees
-    // D^-1 M D; a 2q op absorbs its qubits' pending diagonals into its
-    // columns.  The pass's last unconditional dense 1q op absorbs K and is
-    // emitted in full; leftover pending diagonals and K are flushed as one
-    // DIAG op at the end of the last round.
-    Encoder<R> enc(prog.ops);
-    pd.nrounds = (int)rounds.size();
-    pd.ops_begin = (uint32_t)prog.ops.size();
-    std::vector<cd> dl(n, cd(1.0, 0.0));
-    cd K(1.0, 0.0);
-    int last_u1 = -1;
-    for (auto& rd : rounds)
-      for (int idx : rd.second) {
-        const FOp& f = ops[idx];
-        if ((f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X) && f.conds.empty()) last_u1 = idx;
-      }
-    auto u1_type = [](const cd* M) {
-      if (zero(M[0]) && zero(M[3])) return (int)OP_U1ANTI;
-      if (M[0].imag() == 0 && M[1].imag() == 0 && M[2].imag() == 0 && M[3].imag() == 0) return (int)OP_U1R;
-      if (M[0].imag() == 0 && M[3].imag() == 0 && M[1].real() == 0 && M[2].real() == 0) return (int)OP_U1X;
-      return (int)OP_U1;
-    };
-    struct DT { int qa, qb; cd e[4]; };
-    for (size_t k = 0; k < rounds.size(); ++k) {
-      RoundDev& rd = pd.rounds[k];
-      uint32_t regs = regsets[k];
-      rd.regmask_local = regs;
-      int regidx_of_local[kMaxM];
-      for (int b = 0, i = 0; b < m; ++b) {
-        regidx_of_local[b] = -1;
-        if (regs & (1u << b)) { rd.reg_local[i] = b; regidx_of_local[b] = i; ++i; }
-      }
-      auto ridx = [&](int q) { return (q >= 0 && local_of[q] >= 0) ? regidx_of_local[local_of[q]] : -1; };
-      // one DIAG op from a list of 2-qubit (or 1-qubit, qb = -1) factors
-      auto encode_diag = [&](const std::vector<DT>& terms) {
-        // classify each factor by where its qubits live in this round
-        enum { NONE, TILE, THREAD, REG };
-        auto cls = [&](int q) {
-          if (q < 0) return (int)NONE;
-          if (local_of[q] < 0) return (int)TILE;
-          return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
-        };
-        const bool uniform_ok = pd.ndiag < kMaxDiag;
-        std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
-        std::vector<int> ut_q;                       // thread qubit of each UT group
-        std::vector<std::vector<DiagTerm<R>>> ut;    // UT terms per group
-        for (const DT& d : terms) {
-          int qa = d.qa, qb = d.qb;
-          cd e[4] = {d.e[0], d.e[1], d.e[2], d.e[3]};
-          int ca = cls(qa), cb = cls(qb);
-          // register qubit first; else thread qubit first
-          if ((ca != REG && cb == REG) || ((ca == TILE || ca == NONE) && cb == THREAD)) {
-            std::swap(qa, qb);
-            std::swap(ca, cb);
-            std::swap(e[1], e[2]);
-          }
-          DiagTerm<R> term{};
-          term.qa = (int8_t)qa;
-          term.qb = (int8_t)qb;
-          term.ra = (int8_t)(ca == REG ? ridx(qa) : -1);
-          term.rb = (int8_t)(cb == REG ? ridx(qb) : -1);
-          for (int k2 = 0; k2 < 4; ++k2) term.d[k2] = cvt<R>(e[k2]);
-          const bool ubit = (cb == TILE || cb == NONE);
-          if (ca == REG && cb == REG) rr.push_back(term);
-          else if (ca == REG && cb == THREAD) tr.push_back(term);
-          else if (ca == REG) (uniform_ok ? ur[term.ra] : tr).push_back(term);
-          else if ((ca == TILE || ca == NONE) && ubit && uniform_ok) uc.push_back(term);
-          else if (ca == THREAD && ubit && uniform_ok && !zero(e[0]) && !zero(e[2])) {
-            size_t g = 0;
-            while (g < ut_q.size() && ut_q[g] != qa) ++g;
-            if (g == ut_q.size()) {
-              if ((int)g == kMaxUT) { tc.push_back(term); continue; }
-              ut_q.push_back(qa);
-              ut.emplace_back();
+      // ---- encode the rounds
+      //
+      // Deferred pivot diagonals: an unconditional 1q op M on q (after the
+      // pending diagonal diag(1, dl[q]) of q) is factored as diag(p0, p1) * P,
+      // where each row of P has a unit pivot: y_r = x_pc[r] + ratio_r x_(1-pc[r]).
+      // P costs one complex FMA per amplitude (two real FMAs for a real ratio)
+      // instead of two complex products; diag(p0, p1) = p0 * diag(1, p1/p0) is
+      // carried forward: the scalar p0 into the pass-global K, the rest into dl[q].
+      // Diagonals commute with diagonal ops; a conditional 1q op on q sees
+      // D^-1 M D; a 2q op absorbs its qubits' pending diagonals into its
+      // columns.  The pass's last unconditional dense 1q op absorbs K and is
+      // emitted in full; leftover pending diagonals and K are flushed as one
+      // DIAG op at the end of the last round.
+      Encoder<R> enc(prog.ops);
+      pd.nrounds = (int)rounds.size();
+      pd.ops_begin = (uint32_t)prog.ops.size();
+      std::vector<cd> dl(n, cd(1.0, 0.0));
+      cd K(1.0, 0.0);
+      int last_u1 = -1;
+      for (auto& rd : rounds)
+        for (int idx : rd.second) {
+          const FOp& f = ops[idx];
+          if ((f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X) && f.conds.empty()) last_u1 = idx;
+        }
+      auto u1_type = [](const cd* M) {
+        if (zero(M[0]) && zero(M[3])) return (int)OP_U1ANTI;
+        if (M[0].imag() == 0 && M[1].imag() == 0 && M[2].imag() == 0 && M[3].imag() == 0) return (int)OP_U1R;
+        if (M[0].imag() == 0 && M[3].imag() == 0 && M[1].real() == 0 && M[2].real() == 0) return (int)OP_U1X;
+        return (int)OP_U1;
+      };
+      struct DT { int qa, qb; cd e[4]; };
+      for (size_t k = 0; k < rounds.size(); ++k) {
+        RoundDev& rd = pd.rounds[k];
+        uint32_t regs = regsets[k];
+        rd.regmask_local = regs;
+        int regidx_of_local[kMaxM];
+        for (int b = 0, i = 0; b < m; ++b) {
+          regidx_of_local[b] = -1;
+          if (regs & (1u << b)) { rd.reg_local[i] = b; regidx_of_local[b] = i; ++i; }
+        }
+        auto ridx = [&](int q) { return (q >= 0 && local_of[q] >= 0) ? regidx_of_local[local_of[q]] : -1; };
+        // one DIAG op from a list of 2-qubit (or 1-qubit, qb = -1) factors
+        auto encode_diag = [&](const std::vector<DT>& terms) {
+          // classify each factor by where its qubits live in this round
+          enum { NONE, TILE, THREAD, REG };
+          auto cls = [&](int q) {
+            if (q < 0) return (int)NONE;
+            if (local_of[q] < 0) return (int)TILE;
+            return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
+          };
+          const bool uniform_ok = pd.ndiag < kMaxDiag;
+          std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
+          std::vector<int> ut_q;                       // thread qubit of each UT group
+          std::vector<std::vector<DiagTerm<R>>> ut;    // UT terms per group
+          for (const DT& d : terms) {
+            int qa = d.qa, qb = d.qb;
+            cd e[4] = {d.e[0], d.e[1], d.e[2], d.e[3]};
+            int ca = cls(qa), cb = cls(qb);
+            // register qubit first; else thread qubit first
+            if ((ca != REG && cb == REG) || ((ca == TILE || ca == NONE) && cb == THREAD)) {
+              std::swap(qa, qb);
+              std::swap(ca, cb);
+              std::swap(e[1], e[2]);
             }
-            // constant part per tile-bit value and the thread-bit ratio
-            const cd r0 = snap(e[1] / e[0]), r1 = snap(e[3] / e[2]);
-            term.d[0] = cvt<R>(e[0]);
-            term.d[1] = cvt<R>(r0);
-            term.d[2] = cvt<R>(e[2]);
-            term.d[3] = cvt<R>(r1);
-            ut[g].push_back(term);
-          } else tc.push_back(term);
-        }
-        size_t at = enc.begin(OP_DIAG, 0, 0, (int)terms.size(), 0, 0, 0, 0);
-        DiagHdr hd{};
-        for (int k2 = 0; k2 < 6; ++k2) hd.nUR[k2] = (int32_t)ur[k2].size();
-        hd.nUC = (int32_t)uc.size();
-        hd.nTR = (int32_t)tr.size();
-        hd.nTC = (int32_t)tc.size();
-        hd.nRR = (int32_t)rr.size();
-        bool any_uniform = !uc.empty() || !ut.empty();
-        for (int k2 = 0; k2 < 6; ++k2) any_uniform = any_uniform || !ur[k2].empty();
-        hd.slot = (uniform_ok && any_uniform) ? pd.ndiag : -1;
-        hd.nUTg = (int32_t)ut.size();
-        for (size_t g = 0; g < ut.size(); ++g) {
-          require(ut[g].size() <= 255, SVB_E_CUDA, "scheduler: UT group too large");
-          hd.utn[g] = (uint8_t)ut[g].size();
-        }
-        if (hd.slot >= 0) pd.diag_off[pd.ndiag++] = (uint32_t)prog.ops.size();
-        enc.put(hd);
-        for (int k2 = 0; k2 < 6; ++k2)
-          for (auto& x : ur[k2]) enc.put(x);
-        for (auto& x : uc) enc.put(x);
-        for (auto& g : ut)
-          for (auto& x : g) enc.put(x);
-        for (auto* lst : {&tr, &tc, &rr})
-          for (auto& x : *lst) enc.put(x);
-        enc.end(at);
-      };
-      auto encode_u1 = [&](int type, int b, const cd* M, uint64_t fm, uint64_t fv, uint32_t rm, uint32_t rv) {
-        size_t at = enc.begin(type, b, 0, 0, fm, fv, rm, rv);
-        for (int e = 0; e < 4; ++e) enc.put(cvt<R>(M[e]));
-        enc.end(at);
-      };
-      rd.op_off = (uint32_t)prog.ops.size();
-      const std::vector<int>& list = rounds[k].second;
-      size_t i = 0;
-      while (i < list.size()) {
-        const FOp& f = ops[list[i]];
-        if (f.type == OP_DIAG) {
-          size_t j = i;
-          while (j < list.size() && ops[list[j]].type == OP_DIAG) ++j;
-          std::vector<DT> terms;
-          for (size_t t = i; t < j; ++t) {
-            const FOp& d = ops[list[t]];
-            if (d.q[1] < 0 && d.q[0] >= 0 && local_of[d.q[0]] >= 0 && !zero(d.c[0])) {
-              // 1q diagonal on a tile qubit: fold into the pending diagonal
-              K *= d.c[0];
-              dl[d.q[0]] *= d.c[1] / d.c[0];
+            DiagTerm<R> term{};
+            term.qa = (int8_t)qa;
+            term.qb = (int8_t)qb;
+            term.ra = (int8_t)(ca == REG ? ridx(qa) : -1);
+            term.rb = (int8_t)(cb == REG ? ridx(qb) : -1);
+            for (int k2 = 0; k2 < 4; ++k2) term.d[k2] = cvt<R>(e[k2]);
+            const bool ubit = (cb == TILE || cb == NONE);
+            if (ca == REG && cb == REG) rr.push_back(term);
+            else if (ca == REG && cb == THREAD) tr.push_back(term);
+            else if (ca == REG) (uniform_ok ? ur[term.ra] : tr).push_back(term);
+            else if ((ca == TILE || ca == NONE) && ubit && uniform_ok) uc.push_back(term);
+            else if (ca == THREAD && ubit && uniform_ok && !zero(e[0]) && !zero(e[2])) {
+              size_t g = 0;
+              while (g < ut_q.size() && ut_q[g] != qa) ++g;
+              if (g == ut_q.size()) {
+                if ((int)g == kMaxUT) { tc.push_back(term); continue; }
+                ut_q.push_back(qa);
+                ut.emplace_back();
+              }
+              // constant part per tile-bit value and the thread-bit ratio
+              const cd r0 = snap(e[1] / e[0]), r1 = snap(e[3] / e[2]);
+              term.d[0] = cvt<R>(e[0]);
+              term.d[1] = cvt<R>(r0);
+              term.d[2] = cvt<R>(e[2]);
+              term.d[3] = cvt<R>(r1);
+              ut[g].push_back(term);
+            } else tc.push_back(term);
+          }
+          size_t at = enc.begin(OP_DIAG, 0, 0, (int)terms.size(), 0, 0, 0, 0);
+          DiagHdr hd{};
+          for (int k2 = 0; k2 < 6; ++k2) hd.nUR[k2] = (int32_t)ur[k2].size();
+          hd.nUC = (int32_t)uc.size();
+          hd.nTR = (int32_t)tr.size();
+          hd.nTC = (int32_t)tc.size();
+          hd.nRR = (int32_t)rr.size();
+          bool any_uniform = !uc.empty() || !ut.empty();
+          for (int k2 = 0; k2 < 6; ++k2) any_uniform = any_uniform || !ur[k2].empty();
+          hd.slot = (uniform_ok && any_uniform) ? pd.ndiag : -1;
+          hd.nUTg = (int32_t)ut.size();
+          for (size_t g = 0; g < ut.size(); ++g) {
+            require(ut[g].size() <= 255, SVB_E_CUDA, "scheduler: UT group too large");
+            hd.utn[g] = (uint8_t)ut[g].size();
+          }
+          if (hd.slot >= 0) pd.diag_off[pd.ndiag++] = (uint32_t)prog.ops.size();
+          enc.put(hd);
+          for (int k2 = 0; k2 < 6; ++k2)
+            for (auto& x : ur[k2]) enc.put(x);
+          for (auto& x : uc) enc.put(x);
+          for (auto& g : ut)
+            for (auto& x : g) enc.put(x);
+          for (auto* lst : {&tr, &tc, &rr})
+            for (auto& x : *lst) enc.put(x);
+          enc.end(at);
+        };
+        auto encode_u1 = [&](int type, int b, const cd* M, uint64_t fm, uint64_t fv, uint32_t rm, uint32_t rv) {
+          size_t at = enc.begin(type, b, 0, 0, fm, fv, rm, rv);
+          for (int e = 0; e < 4; ++e) enc.put(cvt<R>(M[e]));
+          enc.end(at);
+        };
+        rd.op_off = (uint32_t)prog.ops.size();
+        const std::vector<int>& list = rounds[k].second;
+        size_t i = 0;
+        while (i < list.size()) {
+          const FOp& f = ops[list[i]];
+          if (f.type == OP_DIAG) {
+            size_t j = i;
+            while (j < list.size() && ops[list[j]].type == OP_DIAG) ++j;
+            std::vector<DT> terms;
+            for (size_t t = i; t < j; ++t) {
+              const FOp& d = ops[list[t]];
+              if (d.q[1] < 0 && d.q[0] >= 0 && local_of[d.q[0]] >= 0 && !zero(d.c[0])) {
+                // 1q diagonal on a tile qubit: fold into the pending diagonal
+                K *= d.c[0];
+                dl[d.q[0]] *= d.c[1] / d.c[0];
+                continue;
+              }
+              terms.push_back(DT{d.q[0], d.q[1], {d.c[0], d.c[1], d.c[2], d.c[3]}});
+            }
+            if (!terms.empty()) encode_diag(terms);
+            i = j;
+            continue;
+          }
+          if (f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X || f.type == OP_U1ANTI) {
+            uint64_t fm = 0, fv = 0;
+            uint32_t rm = 0, rv = 0;
+            for (auto& cv : f.conds) {
+              int ri = ridx(cv.first);
+              if (ri >= 0) { rm |= 1u << ri; rv |= (uint32_t)cv.second << ri; }
+              else { fm |= 1ull << cv.first; fv |= (uint64_t)cv.second << cv.first; }
+            }
+            const int q = f.q[0];
+            int b = ridx(q);
+            require(b >= 0, SVB_E_CUDA, "scheduler: U1 target not in registers");
+            const cd d1 = dl[q];
+            if (!f.conds.empty()) {
+              // conditional op: pass the pending diagonal through (D^-1 M D)
+              cd M[4] = {f.c[0], f.c[1] * d1, f.c[2] / d1, f.c[3]};
+              for (auto& z : M) z = snap(z);
+              encode_u1(u1_type(M), b, M, fm, fv, rm, rv);
+              ++i;
               continue;
             }
-            terms.push_back(DT{d.q[0], d.q[1], {d.c[0], d.c[1], d.c[2], d.c[3]}});
-          }
-          if (!terms.empty()) encode_diag(terms);
-          i = j;
-          continue;
-        }
-        if (f.type == OP_U1 || f.type == OP_U1R || f.type == OP_U1X || f.type == OP_U1ANTI) {
-          uint64_t fm = 0, fv = 0;
-          uint32_t rm = 0, rv = 0;
-          for (auto& cv : f.conds) {
-            int ri = ridx(cv.first);
-            if (ri >= 0) { rm |= 1u << ri; rv |= (uint32_t)cv.second << ri; }
-            else { fm |= 1ull << cv.first; fv |= (uint64_t)cv.second << cv.first; }
-          }
-          const int q = f.q[0];
-          int b = ridx(q);
-          require(b >= 0, SVB_E_CUDA, "scheduler: U1 target not in registers");
-          const cd d1 = dl[q];
-          if (!f.conds.empty()) {
-            // conditional op: pass the pending diagonal through (D^-1 M D)
-            cd M[4] = {f.c[0], f.c[1] * d1, f.c[2] / d1, f.c[3]};
-            for (auto& z : M) z = snap(z);
-            encode_u1(u1_type(M), b, M, fm, fv, rm, rv);
-            ++i;
-            continue;
-          }
-          cd M[4] = {f.c[0], f.c[1] * d1, f.c[2], f.c[3] * d1};  // M * diag(1, d1)
-          dl[q] = cd(1.0, 0.0);
-          if (zero(M[1]) && zero(M[2])) {  // diagonal: defer entirely
-            K *= M[0];
-            dl[q] = snap(M[3] / M[0]);
-            ++i;
-            continue;
-          }
-          if (zero(M[0]) && zero(M[3])) {  // anti-diagonal: plain swap + deferred diag(m01, m10)
-            K *= M[1];
-            dl[q] = snap(M[2] / M[1]);
-            const cd sw[4] = {cd(0.0, 0.0), cd(1.0, 0.0), cd(1.0, 0.0), cd(0.0, 0.0)};
-            encode_u1(OP_U1ANTI, b, sw, 0, 0, 0, 0);
-            ++i;
-            continue;
-          }
-          if (list[i] == last_u1) {  // absorbs K; emitted in full
-            for (auto& z : M) z = snap(z * K);
-            K = cd(1.0, 0.0);
-            encode_u1(u1_type(M), b, M, 0, 0, 0, 0);
-            ++i;
-            continue;
-          }
-          // pivots: the diagonal entry unless it is much smaller than its
-          // neighbour; row 1 prefers an entry equal to p0 (keeps D scalar)
-          const int pc0 = (std::abs(M[0]) >= 0x1p-8 * std::abs(M[1])) ? 0 : 1;
-          const cd p0 = M[pc0];
-          auto close = [](cd x, cd y) { return std::abs(x - y) <= 0x1p-50 * std::abs(y); };
-          int pc1;
-          if (close(M[2], p0) && std::abs(M[2]) >= 0x1p-8 * std::abs(M[3])) pc1 = 0;
-          else if (close(M[3], p0)) pc1 = 1;
-          else pc1 = (std::abs(M[3]) >= 0x1p-8 * std::abs(M[2])) ? 1 : 0;
-          const cd p1 = M[2 + pc1];
-          const cd r0 = snap(M[1 - pc0] / p0), r1 = snap(M[2 + (1 - pc1)] / p1);
-          K *= p0;
-          dl[q] = close(p1, p0) ? cd(1.0, 0.0) : snap(p1 / p0);
-          const bool real = r0.imag() == 0 && r1.imag() == 0;
-          size_t at = enc.begin(real ? OP_U1PR : OP_U1P, b, 0, pc0 | (pc1 << 1), 0, 0, 0, 0);
-          enc.put(cvt<R>(r0));
-          enc.put(cvt<R>(r1));
-          enc.end(at);
-        } else {
-          int b1 = ridx(f.q[0]), b2 = ridx(f.q[1]);
-          require(b1 >= 0 && b2 >= 0, SVB_E_CUDA, "scheduler: U2 qubits not in registers");
-          // absorb the pending diagonals of both qubits into the input columns
-          const cd da = dl[f.q[0]], db = dl[f.q[1]];
-          auto colf = [&](int c) { return ((c & 1) ? da : cd(1.0, 0.0)) * ((c & 2) ? db : cd(1.0, 0.0)); };
-          dl[f.q[0]] = dl[f.q[1]] = cd(1.0, 0.0);
-          size_t at = enc.begin(f.type, b1, b2, 0, 0, 0, 0, 0);
-          if (f.type == OP_U2) {
-            for (int e = 0; e < 16; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(e & 3))));
+            cd M[4] = {f.c[0], f.c[1] * d1, f.c[2], f.c[3] * d1};  // M * diag(1, d1)
+            dl[q] = cd(1.0, 0.0);
+            if (zero(M[1]) && zero(M[2])) {  // diagonal: defer entirely
+              K *= M[0];
+              dl[q] = snap(M[3] / M[0]);
+              ++i;
+              continue;
+            }
+            if (zero(M[0]) && zero(M[3])) {  // anti-diagonal: plain swap + deferred diag(m01, m10)
+              K *= M[1];
+              dl[q] = snap(M[2] / M[1]);
+              const cd sw[4] = {cd(0.0, 0.0), cd(1.0, 0.0), cd(1.0, 0.0), cd(0.0, 0.0)};
+              encode_u1(OP_U1ANTI, b, sw, 0, 0, 0, 0);
+              ++i;
+              continue;
+            }
+            if (list[i] == last_u1) {  // absorbs K; emitted in full
+              for (auto& z : M) z = snap(z * K);
+              K = cd(1.0, 0.0);
+              encode_u1(u1_type(M), b, M, 0, 0, 0, 0);
+              ++i;
+              continue;
+            }
+            // pivots: the diagonal entry unless it is much smaller than its
+            // neighbour; row 1 prefers an entry equal to p0 (keeps D scalar)
+            const int pc0 = (std::abs(M[0]) >= 0x1p-8 * std::abs(M[1])) ? 0 : 1;
+            const cd p0 = M[pc0];
+            auto close = [](cd x, cd y) { return std::abs(x - y) <= 0x1p-50 * std::abs(y); };
+            int pc1;
+            if (close(M[2], p0) && std::abs(M[2]) >= 0x1p-8 * std::abs(M[3])) pc1 = 0;
+            else if (close(M[3], p0)) pc1 = 1;
+            else pc1 = (std::abs(M[3]) >= 0x1p-8 * std::abs(M[2])) ? 1 : 0;
+            const cd p1 = M[2 + pc1];
+            const cd r0 = snap(M[1 - pc0] / p0), r1 = snap(M[2 + (1 - pc1)] / p1);
+            K *= p0;
+            dl[q] = close(p1, p0) ? cd(1.0, 0.0) : snap(p1 / p0);
+            const bool real = r0.imag() == 0 && r1.imag() == 0;
+            size_t at = enc.begin(real ? OP_U1PR : OP_U1P, b, 0, pc0 | (pc1 << 1), 0, 0, 0, 0);
+            enc.put(cvt<R>(r0));
+            enc.put(cvt<R>(r1));
+            enc.end(at);
           } else {
-            int32_t s4[4] = {f.src[0], f.src[1], f.src[2], f.src[3]};
-            enc.put(s4);
-            for (int e = 0; e < 4; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(f.src[e]))));
+            int b1 = ridx(f.q[0]), b2 = ridx(f.q[1]);
+            require(b1 >= 0 && b2 >= 0, SVB_E_CUDA, "scheduler: U2 qubits not in registers");
+            // absorb the pending diagonals of both qubits into the input columns
+            const cd da = dl[f.q[0]], db = dl[f.q[1]];
+            auto colf = [&](int c) { return ((c & 1) ? da : cd(1.0, 0.0)) * ((c & 2) ? db : cd(1.0, 0.0)); };
+            dl[f.q[0]] = dl[f.q[1]] = cd(1.0, 0.0);
+            size_t at = enc.begin(f.type, b1, b2, 0, 0, 0, 0, 0);
+            if (f.type == OP_U2) {
+              for (int e = 0; e < 16; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(e & 3))));
+            } else {
+              int32_t s4[4] = {f.src[0], f.src[1], f.src[2], f.src[3]};
+              enc.put(s4);
+              for (int e = 0; e < 4; ++e) enc.put(cvt<R>(snap(f.c[e] * colf(f.src[e]))));
+            }
+            enc.end(at);
           }
-          enc.end(at);
+          ++i;
         }
-        ++i;
-      }
-      if (k + 1 == rounds.size()) {
-        // flush: pending per-qubit diagonals and the global scalar
-        std::vector<DT> terms;
-        for (int q = 0; q < n; ++q) {
-          const cd d1 = snap(dl[q]);
-          if (!(d1.real() == 1.0 && d1.imag() == 0.0)) terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
+        if (k + 1 == rounds.size()) {
+          // flush: pending per-qubit diagonals and the global scalar
+          std::vector<DT> terms;
+          for (int q = 0; q < n; ++q) {
+            const cd d1 = snap(dl[q]);
+            if (!(d1.real() == 1.0 && d1.imag() == 0.0)) terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
+          }
+          K = snap(K);
+          if (!(K.real() == 1.0 && K.imag() == 0.0)) terms.push_back(DT{-1, -1, {K, K, K, K}});
+          if (!terms.empty()) encode_diag(terms);
         }
-        K = snap(K);
-        if (!(K.real() == 1.0 && K.imag() == 0.0)) terms.push_back(DT{-1, -1, {K, K, K, K}});
-        if (!terms.empty()) encode_diag(terms);
+        rd.op_end = (uint32_t)prog.ops.size();
       }
-      rd.op_end = (uint32_t)prog.ops.size();
+      pd.ops_bytes = (uint32_t)prog.ops.size() - pd.ops_begin;
+      require(pd.ops_bytes <= kMaxPassOpBytes, SVB_E_CUDA, "scheduler: pass op stream too large");
+    if (!search || slots_fit<R>(prog, pd)) break;
+    pd = pd_saved;
+    prog.ops.resize(ops_saved);
+    skipped = skipped_saved;
     }
-    pd.ops_bytes = (uint32_t)prog.ops.size() - pd.ops_begin;
-    require(pd.ops_bytes <= kMaxPassOpBytes, SVB_E_CUDA, "scheduler: pass op stream too large");
     prog.passes.push_back(pd);
     remaining = skipped;
   }

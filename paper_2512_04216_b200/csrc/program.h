@@ -50,6 +50,7 @@ struct SchedOptions {
   int rb = 4;        // register bits per thread
   int m = 12;        // tile qubits
   bool relabel_swaps = true;
+  bool round_search = true;  // reorder ops across rounds (else program order)
 };
 
 SchedOptions default_options(int precision, int n);
