@@ -219,12 +219,18 @@ void Profiler::begin(cudaStream_t st, int kind, double nbytes) {
 }
 void Profiler::end(cudaStream_t st) { SVB_CUDA(cudaEventRecord(pending.back().b, st)); }
 void Profiler::collect() {
-  for (Rec& r : pending) {
-    float t = 0.f;
+  static const bool trace = std::getenv("SVB_TRACE") != nullptr;
+  for (size_t i = 0; i < pending.size(); ++i) {
+    Rec& r = pending[i];
+    float t = 0.f, gap = 0.f;
     SVB_CUDA(cudaEventSynchronize(r.b));
     SVB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (i > 0) SVB_CUDA(cudaEventElapsedTime(&gap, pending[i - 1].b, r.a));
+    if (trace) std::fprintf(stderr, "[svb] launch kind=%d %.3f ms (gap %.3f ms)\n", r.kind, t, gap);
     ms[r.kind] += t;
     count[r.kind] += 1;
+  }
+  for (Rec& r : pending) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }

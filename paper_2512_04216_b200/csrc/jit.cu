@@ -92,6 +92,36 @@ struct Module {
 
 std::mutex g_mu;
 std::unordered_map<std::string, Module> g_cache;  // key: device + source
+// Whole programs seen before: their kernels and launch parameters, keyed by a
+// 128-bit hash of the encoded program (passes + op stream), so repeated
+// applies skip source generation (tens of ms of host time the GPU would idle).
+struct ProgKernels {
+  std::vector<CUfunction> fns;
+  std::vector<int> nslots;
+  std::vector<uint32_t> staged;
+};
+struct Key128 {
+  uint64_t a, b;
+  bool operator==(const Key128& o) const { return a == o.a && b == o.b; }
+};
+struct Key128Hash {
+  size_t operator()(const Key128& k) const { return (size_t)(k.a ^ (k.b * 0x9E3779B97F4A7C15ull)); }
+};
+std::unordered_map<Key128, ProgKernels, Key128Hash> g_prog;
+
+void mix_bytes(Key128& k, const void* data, size_t n) {
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; i += 8) {
+    uint64_t w = 0;
+    std::memcpy(&w, p + i, std::min<size_t>(8, n - i));
+    k.a = (k.a ^ w) * 0x100000001B3ull;
+    k.a ^= k.a >> 29;
+    k.b = (k.b + w) * 0xC2B2AE3D27D4EB4Full;
+    k.b ^= k.b >> 31;
+  }
+  k.a ^= n;
+  k.b += n * 0x9E3779B97F4A7C15ull;
+}
 
 std::string hexf(double x, bool single) {
   char buf[64];
@@ -542,8 +572,22 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
   std::vector<int> nslots(np, 0);
   std::vector<uint32_t> staged(np, 0);
   const uint64_t salt = fnv1a(svb_device_core_src, fnv1a("svb-jit-v1 sm_100a"));
-  std::vector<size_t> todo;
+  Key128 pkey{salt ^ (uint64_t)dev, 0x243F6A8885A308D3ull + sizeof(R)};
+  mix_bytes(pkey, prog.passes.data(), prog.passes.size() * sizeof(PassDev));
+  mix_bytes(pkey, prog.ops.data(), prog.ops.size());
+  bool hit = false;
   {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_prog.find(pkey);
+    if (it != g_prog.end()) {
+      fns = it->second.fns;
+      nslots = it->second.nslots;
+      staged = it->second.staged;
+      hit = true;
+    }
+  }
+  std::vector<size_t> todo;
+  if (!hit) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t p = 0; p < np; ++p) {
       bool imm = false;
@@ -618,6 +662,10 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
       fns[p] = f;
       g_cache.emplace(keys[p], m);
     }
+  }
+  if (!hit) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_prog.emplace(pkey, ProgKernels{fns, nslots, staged});
   }
   for (size_t p = 0; p < np; ++p) {
     const PassDev& pd = prog.passes[p];
