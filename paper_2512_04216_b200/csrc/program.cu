@@ -737,8 +737,13 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
               ++i;
               continue;
             }
-            if (list[i] == last_u1) {  // absorbs K; emitted in full
-              for (auto& z : M) z = snap(z * K);
+            // the stored amplitudes carry 1/K: once |K| drifts far from 1 (long
+            // passes of pivoted ops), emit this op in full to rescale (keeps
+            // complex64 values far from overflow / underflow)
+            const double klog = std::fabs(std::log2(std::abs(K)));
+            const bool rescale = klog > (sizeof(R) == 4 ? 20.0 : 100.0);
+            if (list[i] == last_u1 || rescale) {  // absorbs K; emitted in full
+              for (auto& z : M) z = snap(z) * K;  // snap is absolute: before scaling
               K = cd(1.0, 0.0);
               encode_u1(u1_type(M), b, M, 0, 0, 0, 0);
               ++i;
@@ -788,7 +793,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
             const cd d1 = snap(dl[q]);
             if (!(d1.real() == 1.0 && d1.imag() == 0.0)) terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
           }
-          K = snap(K);
+          if (std::abs(K - cd(1.0, 0.0)) <= 0x1p-50) K = cd(1.0, 0.0);  // not snap(): |K| may be tiny
           if (!(K.real() == 1.0 && K.imag() == 0.0)) terms.push_back(DT{-1, -1, {K, K, K, K}});
           if (!terms.empty()) encode_diag(terms);
         }

@@ -364,3 +364,26 @@ def test_mid_circuit_replay_bit_exact_vs_oracle(n):
         got = sv.run(c, shots, 17, workers=workers)
         assert got.metadata["replay_engine"] == ("per-shot" if n > 12 else "smem-batched")
         assert got.counts == orc.run(c, shots, 17, workers=workers), (n, workers)
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_long_passes_jit_and_interpreter(precision):
+    """Passes with hundreds of pivoted 1q ops (deferred scalar re-absorbed
+    along the way) on both kernel bodies, including immediates (n >= 28 path
+    forced via a small circuit with OPT_JIT_MIN_N)."""
+    n = 14
+    rng = np.random.default_rng(3)
+    c = Circuit(n)
+    for layer in range(40):
+        for q in range(n):
+            c.gate("ry", q, params=(float(rng.uniform(0, 3)),))
+            c.gate("rx", q, params=(float(rng.uniform(0, 3)),))
+        for q in range(layer % 2, n - 1, 2):
+            c.gate("cz", q, q + 1)
+    ref = orc.unitary_state(c)
+    for jit in (-1, 1):
+        s = sv.DeviceState(n, precision)
+        s.set_option(_lib.OPT_JIT_MIN_N, jit)
+        s.apply_instructions(c.instructions)
+        assert relerr(s.to_numpy(), ref) < 10 * TOL[precision], (precision, jit)
+        s.close()

@@ -189,3 +189,20 @@ def test_polysim_shim_installs_and_restores():
         assert ref_sv.run is orig
     finally:
         _sys.path.remove(ref_src)
+
+
+def test_long_pass_stays_in_range_c64():
+    """Hundreds of pivoted 1q ops in one pass: the deferred scalar K must be
+    re-absorbed before complex64 amplitudes drift toward overflow."""
+    n = 13
+    c = Circuit(n)
+    rng = np.random.default_rng(3)
+    for layer in range(40):
+        for q in range(n):
+            c.gate("ry", q, params=(float(rng.uniform(0, 3)),))
+            c.gate("rx", q, params=(float(rng.uniform(0, 3)),))
+        for q in range(layer % 2, n - 1, 2):
+            c.gate("cz", q, q + 1)
+    assert sv.plan(n, c.instructions, "c64")["passes"] >= 1
+    _emu_check(c, "c64", 1e-4)
+    _emu_check(c, "c128", 1e-11)
