@@ -191,10 +191,12 @@ def test_polysim_shim_installs_and_restores():
         _sys.path.remove(ref_src)
 
 
-def test_long_pass_stays_in_range_c64():
+@pytest.mark.parametrize("n", [12, 13])
+def test_long_pass_stays_in_range_c64(n):
     """Hundreds of pivoted 1q ops in one pass: the deferred scalar K must be
-    re-absorbed before complex64 amplitudes drift toward overflow."""
-    n = 13
+    re-absorbed before complex64 amplitudes drift toward overflow.  At n = 12
+    the whole circuit is one tile, so a pass overflows kMaxRounds and its tail
+    is deferred to the next pass."""
     c = Circuit(n)
     rng = np.random.default_rng(3)
     for layer in range(40):
