@@ -22,7 +22,11 @@ _NAMES = (
 _saved: dict = {}
 
 
-def install() -> None:
+def install(qubit_cap=None) -> None:
+    """Route polysim's "sv" backend to the device.  `qubit_cap` (an int, or
+    "device" for calibration.device_qubit_cap()) also raises the module
+    constant DEFAULT_QUBIT_CAP that predictor.estimate checks
+    (predictor.py:63-67); by default it keeps the reference's 26."""
     import polysim.statevector as ref  # noqa: F401  (raises ImportError without polysim)
 
     if _saved:
@@ -32,6 +36,13 @@ def install() -> None:
         setattr(ref, name, getattr(_sv, name))
     _saved["_state_cache"] = ref._state_cache
     ref._state_cache = _sv._state_cache
+    if qubit_cap is not None:
+        if qubit_cap == "device":
+            from .calibration import device_qubit_cap
+
+            qubit_cap = device_qubit_cap()
+        _saved["DEFAULT_QUBIT_CAP"] = ref.DEFAULT_QUBIT_CAP
+        ref.DEFAULT_QUBIT_CAP = int(qubit_cap)
 
 
 def uninstall() -> None:

@@ -208,3 +208,47 @@ def test_long_pass_stays_in_range_c64(n):
     assert sv.plan(n, c.instructions, "c64")["passes"] >= 1
     _emu_check(c, "c64", 1e-4)
     _emu_check(c, "c128", 1e-11)
+
+
+def test_calibration_host_logic():
+    """GPU sv cost curves slot into the reference's CalibrationModel/predictor
+    (SURVEY §8f rank 2); the timing itself is a gpu test."""
+    from paper_2512_04216_b200 import calibration as cal
+
+    assert cal.qubit_cap_for_bytes(180 * 2**30, "c128", spare=False) == 33
+    assert cal.qubit_cap_for_bytes(180 * 2**30, "c64", spare=False) == 34
+    assert cal.qubit_cap_for_bytes(180 * 2**30, "c128") == 32
+    c1, c2 = cal.fit_shot_model([1, 10, 100], [1.0 + 2e-3, 1.0 + 2e-2, 1.0 + 2e-1])
+    assert abs(c1 - 1.0) < 1e-12 and abs(c2 - 2e-3) < 1e-12
+    ref_src = "/root/reference/pkg/src"
+    if not os.path.isdir(ref_src):
+        pytest.skip("reference not present (GPU box)")
+    import sys as _sys
+
+    _sys.path.insert(0, ref_src)
+    try:
+        from polysim.calibration import CalibrationModel
+        from polysim.predictor import estimate
+        from polysim.suite import ghz_circuit
+
+        base = {
+            "version": 1, "created": "test",
+            "sv": {"grid_n": [2, 4], "curves": {"1q": [1e-8, 1e-8], "2q": [2e-8, 2e-8]}},
+            "mps": {"grid_n": [4, 8], "grid_chi": [2, 4],
+                    "surfaces": {k: [[1e-6, 1e-6], [1e-6, 1e-6]] for k in ("1q", "2q", "measure")}},
+            "stab": {"grid_n": [4, 8], "curves": {"gate": [1e-6, 1e-6], "measure": [1e-6, 1e-6]}},
+            "shots": {k: {"c1": 1e-3, "c2": 1e-6} for k in ("sv", "mps", "stab")},
+            "alpha": [1.0],
+        }
+        section = {"sv": {"grid_n": [2, 10, 20], "curves": {"1q": [1e-9, 5e-12, 1e-12], "2q": [2e-9, 6e-12, 2e-12]}},
+                   "shots": {"sv": {"c1": 2e-4, "c2": 3e-8}}}
+        model = cal.merge_sv_section(CalibrationModel.from_dict(base), section)
+        assert isinstance(model, CalibrationModel)
+        assert model.sv_grid == (2, 10, 20) and model.shot_coeffs["sv"] == (2e-4, 3e-8)
+        assert model.shot_coeffs["mps"] == (1e-3, 1e-6)
+        c = ghz_circuit(20)
+        t = estimate(c, "sv", model, shots=1000)
+        want = (1 * 1e-12 + 19 * 2e-12) * 2**20 + 2e-4 + 3e-8 * 1000
+        assert abs(t - want) < 1e-12 * want
+    finally:
+        _sys.path.remove(ref_src)
