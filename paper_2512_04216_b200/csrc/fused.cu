@@ -15,7 +15,10 @@
 // 32-amplitude contiguous runs.
 #include <algorithm>
 #include <chrono>
+#include <list>
+#include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -350,6 +353,64 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
   launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false, false);
 }
 
+// Host compile cache: the scheduled program of a gate list (fusion, pass and
+// round selection, encoding: milliseconds for large circuits) keyed by a hash
+// of the gate records and the options.  Small LRU, shared by all handles.
+namespace {
+struct ProgKey {
+  uint64_t a, b;
+  bool operator==(const ProgKey& o) const { return a == o.a && b == o.b; }
+};
+struct ProgKeyHash {
+  size_t operator()(const ProgKey& k) const { return (size_t)(k.a ^ (k.b * 0x9E3779B97F4A7C15ull)); }
+};
+std::mutex g_prog_mu;
+std::list<std::pair<ProgKey, std::shared_ptr<const void>>> g_prog_lru;
+std::unordered_map<ProgKey, decltype(g_prog_lru)::iterator, ProgKeyHash> g_prog_idx;
+constexpr size_t kProgCacheEntries = 32;
+
+ProgKey prog_key(const void* data, size_t n, uint64_t salt) {
+  ProgKey k{0xcbf29ce484222325ull ^ salt, 0x84222325cbf29ce4ull + salt};
+  const unsigned char* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; i += 8) {
+    uint64_t w = 0;
+    std::memcpy(&w, p + i, std::min<size_t>(8, n - i));
+    k.a = (k.a ^ w) * 0x100000001B3ull;
+    k.a ^= k.a >> 29;
+    k.b = (k.b + w) * 0xC2B2AE3D27D4EB4Full;
+    k.b ^= k.b >> 31;
+  }
+  return k;
+}
+}  // namespace
+
+template <typename R>
+static Program cached_program(int n, const svb_gate* g, int ng, const SchedOptions& opt) {
+  const uint64_t salt = (uint64_t)n | ((uint64_t)sizeof(R) << 8) | ((uint64_t)opt.rb << 16) |
+                        ((uint64_t)opt.m << 24) | ((uint64_t)opt.relabel_swaps << 32) |
+                        ((uint64_t)opt.round_search << 33);
+  const ProgKey key = prog_key(g, sizeof(svb_gate) * (size_t)ng, salt);
+  {
+    std::lock_guard<std::mutex> lk(g_prog_mu);
+    auto it = g_prog_idx.find(key);
+    if (it != g_prog_idx.end()) {
+      g_prog_lru.splice(g_prog_lru.begin(), g_prog_lru, it->second);
+      return *static_cast<const Program*>(it->second->second.get());
+    }
+  }
+  auto prog = std::make_shared<const Program>(build_program<R>(n, g, ng, opt));
+  std::lock_guard<std::mutex> lk(g_prog_mu);
+  if (g_prog_idx.find(key) == g_prog_idx.end()) {
+    g_prog_lru.emplace_front(key, prog);
+    g_prog_idx[key] = g_prog_lru.begin();
+    if (g_prog_lru.size() > kProgCacheEntries) {
+      g_prog_idx.erase(g_prog_lru.back().first);
+      g_prog_lru.pop_back();
+    }
+  }
+  return *prog;
+}
+
 static bool trace_on() {
   static int on = -1;
   if (on < 0) on = std::getenv("SVB_TRACE") ? 1 : 0;
@@ -389,7 +450,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   // swap relabeling needs a second state-sized buffer for the final permutation;
   // it is allocated once per handle (lazily) and reused
   const double t_info = tt.lap();
-  Program prog = build_program<R>(n, g, ng, opt);
+  Program prog = cached_program<R>(n, g, ng, opt);
   if (!prog.final_perm.empty() && *spare == nullptr) {
     if (cudaMalloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
       cudaGetLastError();

@@ -387,3 +387,15 @@ def test_long_passes_jit_and_interpreter(precision):
         s.apply_instructions(c.instructions)
         assert relerr(s.to_numpy(), ref) < 10 * TOL[precision], (precision, jit)
         s.close()
+
+
+def test_run_codes_arrays_equal_run_counts():
+    """(code, count) arrays format to exactly run()'s dict."""
+    rng = np.random.default_rng(8)
+    cases = [suite.ghz_circuit(20), suite.random_circuit(11, 80, rng), _mid_circuit(9, 4)]
+    for c in cases:
+        for seed in (0, 7):
+            a = sv.run_codes(c, 2000, seed)
+            b = sv.run(c, 2000, seed).counts
+            assert a.to_dict() == b
+            assert int(a.counts.sum()) == 2000 and np.all(np.diff(a.codes.astype(np.int64)) > 0)
