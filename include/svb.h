@@ -129,6 +129,12 @@ int svb_sample(svb_handle h, const int32_t* qubits, int k, const int32_t* bit_sr
  * SVB_E_SAMPLING for an invalid vector (sampling.py:31-40). */
 int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_row, int64_t* alias_row);
 
+/* AliasTable.from_probs(probs).sample_indices(rng, shots) (sampling.py:30-83):
+ * table build and draws on the device from the numpy PCG64 state pcg[4];
+ * m must be a power of two (a marginal).  out_idx[shots]: outcome indices. */
+int svb_alias_draw(int device, const double* probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
+                   uint64_t* out_idx);
+
 /* Sharded mode (global<->local qubit swaps, svb_dist in sharded.py):
  * raw device pointer of the state (synchronised), and gather/scatter of the
  * half whose bit L == bit to/from a contiguous device buffer of 2^(n-1)
@@ -155,6 +161,13 @@ int svb_batch_small(int device, int precision, int ncirc, const int32_t* nq, con
 
 /* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
  * device; each measure/reset consumes one draw, exactly as rng.random(). */
+/* Partitioned-block support (pblock.py:34-43,76-120): the block merge
+   np.multiply.outer(b, a) into dst (a.n + b.n qubits), a qubit reorder
+   (qubit p -> bit dest[p], reorder_qubits), and the kept half of a measured
+   block (state.reshape(-1, 2, 2^q)[:, bit, :]) into dst (src.n - 1 qubits). */
+int svb_outer(svb_handle dst, svb_handle a, svb_handle b);
+int svb_permute_qubits(svb_handle h, const int32_t* dest);
+int svb_select_half(svb_handle dst, svb_handle src, int qubit, int bit);
 int svb_rng_seed(svb_handle h, const uint64_t* pcg);
 int svb_measure(svb_handle h, int qubit, int32_t* outcome);      /* _measure_qubit */
 int svb_reset(svb_handle h, int qubit);                          /* _reset_qubit   */

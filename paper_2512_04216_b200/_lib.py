@@ -74,6 +74,10 @@ _SIGS = {
     "svb_device_ptr": (c_int, [_h, POINTER(c_void_p), _u64p, _i64p]),
     "svb_half_copy": (c_int, [_h, c_int, c_int, c_void_p, c_int]),
     "svb_clear": (c_int, [_h]),
+    "svb_outer": (c_int, [_h, _h, _h]),
+    "svb_permute_qubits": (c_int, [_h, POINTER(c_int32)]),
+    "svb_select_half": (c_int, [_h, _h, c_int, c_int]),
+    "svb_alias_draw": (c_int, [c_int, _dp, c_uint64, c_uint64, POINTER(c_uint64), POINTER(c_uint64)]),
     "svb_sample_slice": (c_int, [_h, c_uint64, _u64p, c_double, c_double, c_double, _i32p, c_int, c_uint64, _u64p,
                                  _u64p, _u64p]),
     "svb_measure": (c_int, [_h, c_int, _i32p]),

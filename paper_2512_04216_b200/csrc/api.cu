@@ -466,6 +466,48 @@ int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_ro
   });
 }
 
+// AliasTable.from_probs(probs).sample_indices(rng, shots) (sampling.py:30-83)
+// on the device: the table build and the draws of `shots` uniforms from the
+// numpy PCG64 state `pcg` (pblock's per-group terminal draws, result.py:63-66).
+int svb_alias_draw(int device, const double* probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
+                   uint64_t* out_idx) {
+  return guard([&] {
+    require(m >= 1 && (m & (m - 1)) == 0 && m <= (1ull << 40), SVB_E_ARG, "alias_draw: m must be a power of two");
+    require(shots >= 1, SVB_E_ARG, "shots must be positive");
+    for (uint64_t i = 0; i < m; ++i) require(probs[i] >= 0.0, SVB_E_SAMPLING, "negative probability");
+    SVB_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    SVB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double *dp = nullptr, *dr = nullptr;
+    int64_t* da = nullptr;
+    uint64_t* dc = nullptr;
+    int w = 0;
+    while ((1ull << w) < m) ++w;
+    std::vector<int32_t> ident(64);
+    for (int p = 0; p < 64; ++p) ident[p] = p;
+    auto cleanup = [&] {
+      cudaFreeAsync(dp, st); cudaFreeAsync(dr, st); cudaFreeAsync(da, st); cudaFreeAsync(dc, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    };
+    try {
+      SVB_CUDA(cudaMallocAsync(&dp, m * sizeof(double), st));
+      SVB_CUDA(cudaMallocAsync(&dr, m * sizeof(double), st));
+      SVB_CUDA(cudaMallocAsync(&da, m * sizeof(int64_t), st));
+      SVB_CUDA(cudaMallocAsync(&dc, shots * sizeof(uint64_t), st));
+      SVB_CUDA(cudaMemcpyAsync(dp, probs, m * sizeof(double), cudaMemcpyHostToDevice, st));
+      alias_build(dp, m, dr, da, st);
+      alias_draw(dr, da, m, shots, pcg, ident.data(), w, dc, st);
+      SVB_CUDA(cudaMemcpyAsync(out_idx, dc, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      SVB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream) {
   return guard([&] {
     check_handle(h);
@@ -508,6 +550,54 @@ int svb_half_copy(svb_handle h, int L, int bit, void* dev_buf, int to_buf) {
     if (h->prec == SVB_C128) launch_half_copy<double>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
     else launch_half_copy<float>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
     SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+// ---- partitioned-block support (pblock.py:76-120) ----------------------
+int svb_outer(svb_handle dst, svb_handle a, svb_handle b) {
+  return guard([&] {
+    check_handle_nomat(dst);
+    check_handle(a);
+    check_handle(b);
+    require(dst->n == a->n + b->n && dst->prec == a->prec && dst->prec == b->prec, SVB_E_ARG,
+            "outer: dst must hold a.n + b.n qubits of the same precision");
+    require(dst->device == a->device && dst->device == b->device, SVB_E_ARG, "outer: states on different devices");
+    SVB_CUDA(cudaStreamSynchronize(a->st));
+    SVB_CUDA(cudaStreamSynchronize(b->st));
+    if (dst->prec == SVB_C128) launch_outer<double>(dst->amps, a->amps, b->amps, a->n, b->n, dst->st);
+    else launch_outer<float>(dst->amps, a->amps, b->amps, a->n, b->n, dst->st);
+    dst->zero_pending = false;
+    SVB_CUDA(cudaStreamSynchronize(dst->st));
+  });
+}
+
+int svb_permute_qubits(svb_handle h, const int32_t* dest) {
+  return guard([&] {
+    check_handle(h);
+    std::vector<int> d(h->n);
+    uint64_t seen = 0;
+    for (int p = 0; p < h->n; ++p) {
+      d[p] = dest[p];
+      require(d[p] >= 0 && d[p] < h->n && !((seen >> d[p]) & 1ull), SVB_E_ARG, "permute: dest is not a permutation");
+      seen |= 1ull << d[p];
+    }
+    if (h->prec == SVB_C128) run_permutation<double>(&h->amps, &h->spare, h->n, d, h->st, &h->stats);
+    else run_permutation<float>(&h->amps, &h->spare, h->n, d, h->st, &h->stats);
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_select_half(svb_handle dst, svb_handle src, int qubit, int bit) {
+  return guard([&] {
+    check_handle_nomat(dst);
+    check_handle(src);
+    require(src->n >= 2 && dst->n == src->n - 1 && dst->prec == src->prec && dst->device == src->device, SVB_E_ARG,
+            "select_half: dst must hold src.n - 1 qubits of the same precision");
+    require(qubit >= 0 && qubit < src->n && (bit == 0 || bit == 1), SVB_E_ARG, "bad half selector");
+    if (src->prec == SVB_C128) launch_half_copy<double>(src->amps, src->n, dst->amps, qubit, bit, 1, src->st);
+    else launch_half_copy<float>(src->amps, src->n, dst->amps, qubit, bit, 1, src->st);
+    dst->zero_pending = false;
+    SVB_CUDA(cudaStreamSynchronize(src->st));
   });
 }
 

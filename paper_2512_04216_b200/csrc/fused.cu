@@ -353,6 +353,20 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
   launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false, false);
 }
 
+// Qubit permutation of a whole state (qubit p moves to bit dest[p]), out of
+// place through the handle's spare buffer (pblock reorders, svb_permute_qubits).
+template <typename R>
+void run_permutation(void** state, void** spare, int n, const std::vector<int>& dest, cudaStream_t st,
+                     ProgramStats* stats) {
+  bool ident = true;
+  for (int p = 0; p < n; ++p) ident = ident && dest[p] == p;
+  if (ident) return;
+  if (*spare == nullptr) SVB_CUDA(cudaMalloc(spare, sizeof(cplx<R>) << n));
+  launch_permute<R>(reinterpret_cast<cplx<R>**>(state), reinterpret_cast<cplx<R>**>(spare), n, dest, st, stats);
+}
+template void run_permutation<float>(void**, void**, int, const std::vector<int>&, cudaStream_t, ProgramStats*);
+template void run_permutation<double>(void**, void**, int, const std::vector<int>&, cudaStream_t, ProgramStats*);
+
 // Host compile cache: the scheduled program of a gate list (fusion, pass and
 // round selection, encoding: milliseconds for large circuits) keyed by a hash
 // of the gate records and the options.  Small LRU, shared by all handles.

@@ -27,6 +27,7 @@ void launch_measure(void* state, int n, int q, bool reset, uint64_t* d_rng, doub
                     int32_t* d_outcome, uint64_t* d_code, int rank, cudaStream_t st);
 size_t measure_ws_doubles(int n);
 template <typename R> void launch_half_copy(void* state, int n, void* buf, int L, int bit, int to_buf, cudaStream_t st);
+template <typename R> void launch_outer(void* dst, const void* a, const void* b, int na, int nb, cudaStream_t st);
 
 // sample.cu — PCG64, pairwise sum, alias table, samplers, histogram
 void host_pcg_advance(uint64_t* pcg4, uint64_t delta);

@@ -352,5 +352,25 @@ template <typename R> void launch_half_copy(void* state, int n, void* buf, int L
   SVB_CHECK_LAUNCH();
 }
 template void launch_half_copy<float>(void*, int, void*, int, int, int, cudaStream_t);
+
+// dst[ib << na | ia] = b[ib] * a[ia]  (np.multiply.outer(b, a).reshape(-1),
+// the block merge of pblock.py:76-83)
+template <typename R>
+__global__ void k_outer(cplx<R>* __restrict__ dst, const cplx<R>* __restrict__ a, const cplx<R>* __restrict__ b,
+                        int na, uint64_t total) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t amask = (1ull << na) - 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    dst[i] = cmul<R>(b[i >> na], a[i & amask]);
+}
+
+template <typename R> void launch_outer(void* dst, const void* a, const void* b, int na, int nb, cudaStream_t st) {
+  const uint64_t total = 1ull << (na + nb);
+  k_outer<R><<<grid_for(total, 256), 256, 0, st>>>(static_cast<cplx<R>*>(dst), static_cast<const cplx<R>*>(a),
+                                                     static_cast<const cplx<R>*>(b), na, total);
+  SVB_CHECK_LAUNCH();
+}
+template void launch_outer<float>(void*, const void*, const void*, int, int, cudaStream_t);
+template void launch_outer<double>(void*, const void*, const void*, int, int, cudaStream_t);
 template void launch_half_copy<double>(void*, int, void*, int, int, int, cudaStream_t);
 }  // namespace svb

@@ -68,6 +68,10 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
 // use, nullptr if it cannot be); the permutation writes into it and swaps.
 // fusion: 0 = one pass per gate, 1 = fused passes.  jit_min_n: specialise the
 // fused passes with NVRTC when n >= jit_min_n (negative: never).
+template <typename R>
+void run_permutation(void** state, void** spare, int n, const std::vector<int>& dest, cudaStream_t st,
+                     ProgramStats* stats);
+
 // zero_pending (may be null): the state is a lazy |0...0>; the first fused
 // pass synthesises it instead of reading HBM (other paths write it first).
 template <typename R>

@@ -20,13 +20,16 @@ _NAMES = (
     "marginal_probs", "_measure_qubit", "_reset_qubit",
 )
 _saved: dict = {}
+_saved_pb: dict = {}
 
 
-def install(qubit_cap=None) -> None:
+def install(qubit_cap=None, pblock: bool = False) -> None:
     """Route polysim's "sv" backend to the device.  `qubit_cap` (an int, or
     "device" for calibration.device_qubit_cap()) also raises the module
     constant DEFAULT_QUBIT_CAP that predictor.estimate checks
-    (predictor.py:63-67); by default it keeps the reference's 26."""
+    (predictor.py:63-67); by default it keeps the reference's 26.  With
+    `pblock=True`, polysim.pblock's single-device `run` and `PBlockState`
+    also run on the device (paper_2512_04216_b200.pblock)."""
     import polysim.statevector as ref  # noqa: F401  (raises ImportError without polysim)
 
     if _saved:
@@ -36,6 +39,15 @@ def install(qubit_cap=None) -> None:
         setattr(ref, name, getattr(_sv, name))
     _saved["_state_cache"] = ref._state_cache
     ref._state_cache = _sv._state_cache
+    if pblock:
+        import polysim.pblock as ref_pb
+
+        from . import pblock as dev_pb
+
+        _saved_pb["run"] = ref_pb.run
+        _saved_pb["PBlockState"] = ref_pb.PBlockState
+        ref_pb.run = dev_pb.run
+        ref_pb.PBlockState = dev_pb.PBlockState
     if qubit_cap is not None:
         if qubit_cap == "device":
             from .calibration import device_qubit_cap
@@ -51,6 +63,12 @@ def uninstall() -> None:
     for name, fn in _saved.items():
         setattr(ref, name, fn)
     _saved.clear()
+    if _saved_pb:
+        import polysim.pblock as ref_pb
+
+        for name, fn in _saved_pb.items():
+            setattr(ref_pb, name, fn)
+        _saved_pb.clear()
 
 
 def installed() -> bool:

@@ -181,12 +181,20 @@ def test_polysim_shim_installs_and_restores():
         import polysim.statevector as ref_sv
         from paper_2512_04216_b200 import polysim_shim
 
-        orig = ref_sv.run
+        import polysim.pblock as ref_pb
+        from paper_2512_04216_b200 import pblock as dev_pb
+
+        orig, orig_pb = ref_sv.run, ref_pb.run
         polysim_shim.install()
         assert ref_sv.run is sv.run and ref_sv.final_state is sv.final_state
-        assert ref_sv.DEFAULT_QUBIT_CAP == 26
+        assert ref_sv.DEFAULT_QUBIT_CAP == 26 and ref_pb.run is orig_pb
         polysim_shim.uninstall()
         assert ref_sv.run is orig
+        polysim_shim.install(qubit_cap=30, pblock=True)
+        assert ref_sv.DEFAULT_QUBIT_CAP == 30
+        assert ref_pb.run is dev_pb.run and ref_pb.PBlockState is dev_pb.PBlockState
+        polysim_shim.uninstall()
+        assert ref_sv.DEFAULT_QUBIT_CAP == 26 and ref_pb.run is orig_pb and ref_sv.run is orig
     finally:
         _sys.path.remove(ref_src)
 
