@@ -113,7 +113,7 @@ struct PassDev {
   RoundDev rounds[kMaxRounds];
   int32_t ndiag;
   uint32_t ops_begin, ops_bytes;  // this pass's slice of the op stream (staged in smem)
-  int32_t pad;
+  int32_t direct;                 // round 0 has no lane register bits (see pass_kernel)
   uint32_t diag_off[kMaxDiag];  // op-stream offsets of this pass's DIAG payloads
 };
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
@@ -718,6 +718,7 @@ template <typename R, int RB> struct PassCtx {
   uint64_t ld_tid, next_base;
   uint32_t sd_tid, nld;
   int prefetch, zero_input;
+  int direct;  // round 0 loads straight from HBM into registers (no ring)
   __device__ PassCtx(const PassDev& p) : pd(p) {}
 };
 
@@ -820,6 +821,24 @@ __device__ __forceinline__ void store_global(cplx<R>* state, uint64_t Fg, const 
   for (int v = 0; v < (1 << RB); ++v) __stcs(g0 + gv[v], a[v]);
 }
 
+// Direct first round: the round-0 layout has no lane register bits, so the
+// warp's lanes read consecutive amplitudes (512 B per request).
+template <typename R, int RB>
+__device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg, const RoundDev& rd, cplx<R>* a) {
+  size_t goff[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) goff[i] = (size_t)1 << c.pd.pos[rd.reg_local[i]];
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    size_t g = 0;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if (v & (1 << i)) g |= goff[i];
+    if (c.zero_input) a[v] = mk<R>((Fg | g) == 0 ? R(1) : R(0), R(0));
+    else a[v] = __ldcs(c.state + (Fg | g));
+  }
+}
+
 // Helpers for JIT-generated diagonal code.
 template <typename R> __device__ __forceinline__ cplx<R> csel(int f, cplx<R> x0, cplx<R> x1) { return f ? x1 : x0; }
 template <typename R> __device__ __forceinline__ cplx<R> conj_mul(cplx<R> x, cplx<R> u) {
@@ -888,7 +907,8 @@ struct InterpBody {
       round_fixed<R, RB>(c, k, base, sFl, Fg);
       uint32_t slot[1 << RB];
       layout_slots<R, RB>(sFl, rd, slot);
-      load_slots<R, RB>(a, cur, slot);
+      if (k == 0 && c.direct) load_global<R, RB>(c, Fg, rd, a);
+      else load_slots<R, RB>(a, cur, slot);
       if (k + 1 == nrounds) prefetch_next<R, RB, InterpBody>(c);
       run_ops<R, RB>(a, Fg, c.ops, rd.op_off, rd.op_end, c.uni);
       if (k + 1 < nrounds) {
@@ -933,7 +953,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   // whole slice (offsets rebased so that stream offsets index shared memory);
   // ops_mode 1 (bodies with immediate coefficients) packs only the DIAG
   // payloads that have uniform slots.
-  const uint32_t ring_bytes = (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << pd.m);
+  // stages: 2 = double ring, 1 = single ring + prefetch, 0 = direct first round
+  // (one tile of shared memory for the inter-round layouts, no cp.async)
+  const uint32_t ring_bytes = (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
   uint32_t staged = 0;
   if (ops_mode == 0) {
     const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
@@ -992,6 +1014,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   c.zero_input = zero_input;
   c.prefetch = 0;
   c.next_base = 0;
+  c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PassCtx<R, RB>::kHoist; ++k) {
@@ -1002,8 +1025,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     }
   }
   const uint32_t t0 = blockIdx.x;
-  if (t0 < ntiles) Body::template issue<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
-  cp_async_commit();
+  if (stages > 0) {
+    if (t0 < ntiles) Body::template issue<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
+    cp_async_commit();
+  }
   // tile-independent per-thread constants of the body (e.g. products of
   // diagonal factors that depend only on the thread's own local bits)
   typename Body::template State<R, RB> bs;
@@ -1023,7 +1048,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
       diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, ndiag, base, const_cast<cplx<R>*>(c.uni), warp,
                                 nwarps, lane);
     if (stages > 1) cp_async_wait<1>();
-    else cp_async_wait<0>();
+    else if (stages == 1) cp_async_wait<0>();
+    // ring data and uniform factors visible; (direct) the previous tile's last
+    // shared-memory reads are done before round 0 stores this tile's layout
     __syncthreads();
     if (stages == 1) {
       c.prefetch = tn < ntiles;
@@ -1051,7 +1078,7 @@ __global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
 template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
-  return (uint32_t)stages * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
+  return (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
          (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;

@@ -276,8 +276,9 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
-    const int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0);
-    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
+    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0);
+    if (stages == 1 && pd.direct && std::getenv("SVB_DIRECT")) stages = 0;  // measured slower (load latency exposed)
+    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));

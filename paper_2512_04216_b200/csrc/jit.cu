@@ -330,7 +330,19 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         K[v | (1 << i)] = K[v] ^ swz<R>(1u << rd.reg_local[i]);
         G[v | (1 << i)] = G[v] | (1ull << pd.pos[rd.reg_local[i]]);
       }
-    for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+    if (k == 0) {  // direct first round (launch-time choice, see pass_kernel)
+      o << "    if (c.direct) {\n      const svb::cplx<R>* g0 = c.state + Fg;\n"
+           "      if (c.zero_input) {\n";
+      for (int v = 0; v < (1 << RB); ++v)
+        o << "        a[" << v << "] = svb::mk<R>((Fg | " << G[v] << "ull) == 0 ? R(1) : R(0), R(0));\n";
+      o << "      } else {\n";
+      for (int v = 0; v < (1 << RB); ++v) o << "        a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
+      o << "      }\n    } else {\n";
+      for (int v = 0; v < (1 << RB); ++v) o << "      a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+      o << "    }\n";
+    } else {
+      for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+    }
     if (k + 1 == pd.nrounds) o << "    svb::prefetch_next<R, RB, PassBody>(c);\n";
     uint32_t off = rd.op_off;
     while (off < rd.op_end) {
@@ -672,8 +684,9 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
     int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p]);
+    if (stages == 1 && pd.direct && std::getenv("SVB_DIRECT")) stages = 0;  // measured slower (load latency exposed)
     const unsigned grid =
-        (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages == 1 ? kPassMinBlocks<R> : 1));
+        (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages);
     static const bool trace = std::getenv("SVB_TRACE") != nullptr;
     if (trace)

@@ -538,6 +538,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
         rounds.push_back({0u, {}});
         regsets.push_back(fill(0u));
       }
+      // (direct is set after the kMaxRounds trim below)
       if ((int)rounds.size() > kMaxRounds) {
         // defer the tail of this pass's ops to the next pass (original order kept)
         std::vector<int> keep_ops;
@@ -554,6 +555,9 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
         skipped.insert(skipped.end(), deferred.begin(), deferred.end());
         std::sort(skipped.begin(), skipped.end());
       }
+      // round 0 without lane register bits: its layout is coalesced in HBM, so
+      // a single-stage kernel can load it straight into registers (no ring)
+      pd.direct = (regsets[0] & lane_local) == 0 ? 1 : 0;
 
       // ---- encode the rounds
       //
