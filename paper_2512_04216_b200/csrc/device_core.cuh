@@ -10,6 +10,7 @@
 typedef unsigned long long uint64_t;
 typedef long long int64_t;
 typedef unsigned int uint32_t;
+typedef unsigned short uint16_t;
 typedef int int32_t;
 typedef signed char int8_t;
 typedef unsigned char uint8_t;
@@ -99,6 +100,7 @@ constexpr int kUniV = 11;
 constexpr int kMaxRounds = 24;
 constexpr int kMaxM = 14;
 constexpr int kMaxDiag = 48;
+constexpr int kMaxItems = 256;
 
 struct RoundDev {
   int32_t reg_local[8];  // local bit of register bit i
@@ -115,7 +117,14 @@ struct PassDev {
   uint32_t ops_begin, ops_bytes;  // this pass's slice of the op stream (staged in smem)
   int32_t direct;                 // round 0 has no lane register bits (see pass_kernel)
   uint32_t diag_off[kMaxDiag];  // op-stream offsets of this pass's DIAG payloads
+  // tile-uniform work items (one per non-empty UR register bit, constant and
+  // UT group of each uniform DIAG payload): d | kind << 8 | index << 10,
+  // kind 0 = UR, 1 = constant, 2 = UT group
+  int32_t nitems;
+  int32_t pad2[3];
+  uint16_t items[kMaxItems];
 };
+static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
 
 // ------------------------------------------------------------ interpreter
@@ -311,13 +320,16 @@ SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cp
 #pragma unroll
   for (int i = 0; i < RB; ++i) D0[i] = D1[i] = C;
   if (h2.z >= 0) {
+    // only entries with terms are evaluated (see PassDev::items)
     const cplx<R>* us = uni + (size_t)h2.z * kUniStride;
-    C = us[0];
+    const int nur[6] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y};
+    if (h1.z + nut > 0) C = us[0];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) {
-      D0[i] = us[1 + i];
-      D1[i] = us[1 + 5 + i];
-    }
+    for (int i = 0; i < RB; ++i)
+      if (nur[i] > 0) {
+        D0[i] = us[1 + i];
+        D1[i] = us[1 + 5 + i];
+      }
     // UT groups: the thread's own bit of each group's thread qubit selects V[g]
     const DiagTerm<R>* tu = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr)) + (nskip - nut);
     for (int g = 0; g < hd->nUTg; ++g) {
@@ -638,60 +650,51 @@ template <typename R> __device__ __forceinline__ cplx<R> warp_prod(cplx<R> x) {
   return x;
 }
 
-// Tile-uniform factors of all DIAG payloads of a pass, as independent items
-// (per payload: one per register bit, the constant, one per UT group) dealt
-// round-robin to the CTA's warps; each item is a lane-parallel product.
+// Tile-uniform factors of a pass's DIAG payloads: the host lists one work item
+// per non-empty factor (PassDev::items); warp w evaluates items w, w+nwarps,
+// ... as lane-parallel products over the item's terms.
 template <typename R, int RB>
-__device__ void diag_uniform_items(const uint8_t* ops, const uint32_t* diag_off, int ndiag, uint64_t base,
-                                   cplx<R>* uni, uint32_t warp, uint32_t nwarps, uint32_t lane) {
+__device__ void diag_uniform_items(const uint8_t* ops, const uint32_t* diag_off, const uint16_t* items, int nitems,
+                                   uint64_t base, cplx<R>* uni, uint32_t warp, uint32_t nwarps, uint32_t lane) {
   const cplx<R> one = mk<R>(R(1), R(0));
-  uint32_t item = 0;
-  for (int d = 0; d < ndiag; ++d) {
+  for (int it = (int)warp; it < nitems; it += (int)nwarps) {
+    const uint32_t code = items[it];
+    const int d = (int)(code & 0xffu), kind = (int)((code >> 8) & 3u), idx = (int)(code >> 10);
     const uint8_t* payload = ops + diag_off[d];
     const DiagHdr* h = reinterpret_cast<const DiagHdr*>(payload);
     cplx<R>* slot = uni + d * kUniStride;
     const DiagTerm<R>* t = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
-    for (int i = 0; i < RB; ++i) {
-      const int n = h->nUR[i];
-      const bool mine = item == warp;
-      if (++item == nwarps) item = 0;
-      if (mine) {
-        cplx<R> u0 = one, u1 = one;
-        for (int k = (int)lane; k < n; k += 32) {
-          const int f = fbit<R>(base, t[k].qb);
-          u0 = cmul<R>(u0, t[k].d[2 * f]);
-          u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
-        }
-        if (n > 1) { u0 = warp_prod<R>(u0); u1 = warp_prod<R>(u1); }
-        if (lane == 0) { slot[1 + i] = u0; slot[1 + 5 + i] = u1; }
+    int nur_all = 0;
+    for (int i = 0; i < 6; ++i) nur_all += h->nUR[i];
+    if (kind == 0) {  // register bit idx x tile bits
+      for (int i = 0; i < idx; ++i) t += h->nUR[i];
+      const int n = h->nUR[idx];
+      cplx<R> u0 = one, u1 = one;
+      for (int k = (int)lane; k < n; k += 32) {
+        const int f = fbit<R>(base, t[k].qb);
+        u0 = cmul<R>(u0, t[k].d[2 * f]);
+        u1 = cmul<R>(u1, t[k].d[2 * f + 1]);
       }
-      t += n;
-    }
-    // constant: UC terms and the UT constant parts
-    const DiagTerm<R>* tut = t + h->nUC;
-    const int nut = diag_nut(h);
-    const bool mine_c = item == warp;
-    if (++item == nwarps) item = 0;
-    if (mine_c) {
+      if (n > 1) { u0 = warp_prod<R>(u0); u1 = warp_prod<R>(u1); }
+      if (lane == 0) { slot[1 + idx] = u0; slot[1 + 5 + idx] = u1; }
+    } else if (kind == 1) {  // constant: UC terms and the UT constant parts
+      t += nur_all;
+      const DiagTerm<R>* tut = t + h->nUC;
+      const int nut = diag_nut(h);
       cplx<R> c = one;
       for (int k = (int)lane; k < h->nUC; k += 32)
         c = cmul<R>(c, t[k].d[fbit<R>(base, t[k].qa) + 2 * fbit<R>(base, t[k].qb)]);
       for (int k = (int)lane; k < nut; k += 32) c = cmul<R>(c, tut[k].d[2 * fbit<R>(base, tut[k].qb)]);
       if (h->nUC + nut > 1) c = warp_prod<R>(c);
       if (lane == 0) slot[0] = c;
-    }
-    const DiagTerm<R>* tg = tut;
-    for (int g = 0; g < h->nUTg; ++g) {
-      const int n = h->utn[g];
-      const bool mine = item == warp;
-      if (++item == nwarps) item = 0;
-      if (mine) {
-        cplx<R> v = one;
-        for (int k = (int)lane; k < n; k += 32) v = cmul<R>(v, tg[k].d[2 * fbit<R>(base, tg[k].qb) + 1]);
-        if (n > 1) v = warp_prod<R>(v);
-        if (lane == 0) slot[kUniV + g] = v;
-      }
-      tg += n;
+    } else {  // UT group idx: thread-bit ratio
+      t += nur_all + h->nUC;
+      for (int g = 0; g < idx; ++g) t += h->utn[g];
+      const int n = h->utn[idx];
+      cplx<R> v = one;
+      for (int k = (int)lane; k < n; k += 32) v = cmul<R>(v, t[k].d[2 * fbit<R>(base, t[k].qb) + 1]);
+      if (n > 1) v = warp_prod<R>(v);
+      if (lane == 0) slot[kUniV + idx] = v;
     }
   }
 }
@@ -1045,8 +1048,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
     const uint64_t base = tile_base_warp(pd, t, lane);
     c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
-      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, ndiag, base, const_cast<cplx<R>*>(c.uni), warp,
-                                nwarps, lane);
+      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, base, const_cast<cplx<R>*>(c.uni),
+                                warp, nwarps, lane);
     if (stages > 1) cp_async_wait<1>();
     else if (stages == 1) cp_async_wait<0>();
     // ring data and uniform factors visible; (direct) the previous tile's last

@@ -651,6 +651,8 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
     }
     for (size_t p : compile) {
       if (cubins[p].empty()) {
+        if (std::getenv("SVB_JIT_STRICT"))  // tests: a compile failure must not hide behind the interpreter
+          throw Error(SVB_E_CUDA, "JIT compile failed:\n" + logs[p]);
         std::fprintf(stderr, "[svb] JIT compile failed; using the interpreter kernel\n%s\n", logs[p].c_str());
         return false;
       }

@@ -609,7 +609,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
             if (local_of[q] < 0) return (int)TILE;
             return regidx_of_local[local_of[q]] >= 0 ? (int)REG : (int)THREAD;
           };
-          const bool uniform_ok = pd.ndiag < kMaxDiag;
+          const bool uniform_ok = pd.ndiag < kMaxDiag && pd.nitems + 7 + kMaxUT <= kMaxItems;
           std::vector<DiagTerm<R>> ur[6], uc, tr, tc, rr;
           std::vector<int> ut_q;                       // thread qubit of each UT group
           std::vector<std::vector<DiagTerm<R>>> ut;    // UT terms per group
@@ -661,6 +661,16 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
           bool any_uniform = !uc.empty() || !ut.empty();
           for (int k2 = 0; k2 < 6; ++k2) any_uniform = any_uniform || !ur[k2].empty();
           hd.slot = (uniform_ok && any_uniform) ? pd.ndiag : -1;
+          if (hd.slot >= 0) {  // the pass's tile-uniform work items (PassDev::items)
+            auto item = [&](int kind, int idx) {
+              require(pd.nitems < kMaxItems, SVB_E_CUDA, "scheduler: too many uniform items");
+              pd.items[pd.nitems++] = (uint16_t)(hd.slot | (kind << 8) | (idx << 10));
+            };
+            for (int k2 = 0; k2 < 6; ++k2)
+              if (!ur[k2].empty()) item(0, k2);
+            if (!uc.empty() || !ut.empty()) item(1, 0);
+            for (size_t g = 0; g < ut.size(); ++g) item(2, (int)g);
+          }
           hd.nUTg = (int32_t)ut.size();
           for (size_t g = 0; g < ut.size(); ++g) {
             require(ut[g].size() <= 255, SVB_E_CUDA, "scheduler: UT group too large");

@@ -13,6 +13,10 @@ import sys
 
 import numpy as np
 import pytest
+
+# a JIT compile failure must fail the test instead of silently running the
+# interpreter body (the library reads this when it first JIT-compiles)
+os.environ.setdefault("SVB_JIT_STRICT", "1")
 from scipy import stats
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -260,3 +260,28 @@ def test_calibration_host_logic():
         assert abs(t - want) < 1e-12 * want
     finally:
         _sys.path.remove(ref_src)
+
+
+@pytest.mark.parametrize("which", ["qft30_c128", "qft20_c128", "syc_c64", "random_c64"])
+def test_jit_sources_compile(which):
+    """NVRTC compiles every generated pass kernel (a failure would otherwise
+    fall back to the interpreter body at run time)."""
+    import ctypes as _ct
+
+    if which == "qft30_c128":
+        n, prec, c = 30, 1, suite.qft_bench_circuit(30)
+    elif which == "qft20_c128":
+        n, prec, c = 20, 1, suite.qft_bench_circuit(20)
+    elif which == "syc_c64":
+        n, prec, c = 28, 0, suite.sycamore_circuit(4, 7, 12, seed=0, measured=False)
+    else:
+        n, prec = 22, 0
+        c = suite.random_circuit(22, 300, np.random.default_rng(2), measured=False)
+    g = sv.gate_array(c.instructions)
+    cb = _ct.c_int64()
+    buf = _ct.create_string_buffer(1 << 14)
+    rc = _lib.lib().svb_jit_check(n, prec, g.ctypes.data_as(_ct.c_void_p), int(g.size), _ct.byref(cb), buf, 1 << 14)
+    if rc != 0 and b"nvrtc" in buf.value.lower() and b"not available" in buf.value.lower():
+        pytest.skip("NVRTC not available")
+    assert rc == 0, buf.value.decode(errors="replace")[:2000]
+    assert cb.value > 0
