@@ -199,7 +199,7 @@ def run_ours(args, rank: int, world: int, dist):
     n_gates = int(gates.size)
     masks = [1 << q for q in range(N_QUBITS)]
     state = sv.DeviceState(N_QUBITS, PRECISION, device)
-    plan = sv.plan(N_QUBITS, c.instructions, PRECISION)
+    plan = sv.plan(N_QUBITS, c.instructions, PRECISION, zero_start=True)  # each step starts from a lazy |0...0>
 
     def step():
         state.zero()

@@ -106,6 +106,10 @@ struct RoundDev {
   int32_t reg_local[8];  // local bit of register bit i
   uint32_t op_off, op_end;
   uint32_t regmask_local, pad;
+  // local bit of thread-index bit tb (the non-register local bits; ascending
+  // except in a permuted-store round, whose lanes sit on the bits that land
+  // on output qubits 0..4)
+  uint8_t thr_local[16];
 };
 
 struct PassDev {
@@ -121,8 +125,14 @@ struct PassDev {
   // UT group of each uniform DIAG payload): d | kind << 8 | index << 10,
   // kind 0 = UR, 1 = constant, 2 = UT group
   int32_t nitems;
-  int32_t pad2[3];
+  // permuted store (the program's final qubit permutation fused into its last
+  // pass): the last round writes out-of-place to bit dest(p) for every
+  // physical bit p; dpos[l] = dest(pos[l]), doutpos[i] = dest(outpos[i])
+  int32_t perm_out;
+  int32_t pad2[2];
   uint16_t items[kMaxItems];
+  int32_t dpos[16];
+  int32_t doutpos[48];
 };
 static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
@@ -557,23 +567,38 @@ SVB_HD void thread_fixed(const PassDev& pd, const RoundDev& rd, uint32_t tid, ui
                          uint32_t* Fl, uint64_t* Fg) {
   uint32_t fl = 0;
   uint64_t fg = base;
-  int tb = 0;
-  for (int l = 0; l < pd.m; ++l) {
-    if (rd.regmask_local & (1u << l)) continue;
+  const int nt = pd.m - pd.rb;
+  for (int tb = 0; tb < nt; ++tb) {
     if ((tid >> tb) & 1u) {
+      const int l = rd.thr_local[tb];
       fl |= 1u << l;
       fg |= 1ull << pd.pos[l];
     }
-    ++tb;
   }
   *Fl = fl;
   *Fg = fg;
+}
+
+// Permuted-store round: the thread's fixed index with every bit moved to its
+// destination (dest is a bit permutation, so it distributes over OR).
+SVB_HD uint64_t thread_fixed_perm(const PassDev& pd, const RoundDev& rd, uint32_t tid) {
+  uint64_t fg = 0;
+  const int nt = pd.m - pd.rb;
+  for (int tb = 0; tb < nt; ++tb)
+    if ((tid >> tb) & 1u) fg |= 1ull << pd.dpos[rd.thr_local[tb]];
+  return fg;
 }
 
 SVB_HD uint64_t tile_base(const PassDev& pd, uint64_t t) {
   uint64_t b = 0;
   for (int i = 0; i < pd.nout; ++i)
     if ((t >> i) & 1ull) b |= 1ull << pd.outpos[i];
+  return b;
+}
+SVB_HD uint64_t tile_base_perm(const PassDev& pd, uint64_t t) {
+  uint64_t b = 0;
+  for (int i = 0; i < pd.nout; ++i)
+    if ((t >> i) & 1ull) b |= 1ull << pd.doutpos[i];
   return b;
 }
 
@@ -627,10 +652,12 @@ template <typename R> constexpr int kPassMinBlocks = sizeof(R) == 8 ? 2 : 1;
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
 
 // Tile base (bits outside S) computed warp-parallel: lane l owns tile bit l.
-__device__ __forceinline__ uint64_t tile_base_warp(const PassDev& pd, uint64_t t, uint32_t lane) {
+__device__ __forceinline__ uint64_t tile_base_warp(const PassDev& pd, uint64_t t, uint32_t lane,
+                                                  bool perm = false) {
+  const int32_t* op = perm ? pd.doutpos : pd.outpos;
   uint64_t v = 0;
-  if ((int)lane < pd.nout && ((t >> lane) & 1ull)) v = 1ull << pd.outpos[lane];
-  if ((int)lane + 32 < pd.nout && ((t >> (lane + 32)) & 1ull)) v |= 1ull << pd.outpos[lane + 32];
+  if ((int)lane < pd.nout && ((t >> lane) & 1ull)) v = 1ull << op[lane];
+  if ((int)lane + 32 < pd.nout && ((t >> (lane + 32)) & 1ull)) v |= 1ull << op[lane + 32];
   const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
   const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
   return ((uint64_t)hi << 32) | lo;
@@ -706,6 +733,8 @@ template <typename R, int RB> struct PassCtx {
   static constexpr int kHoist = 4;  // rounds whose thread constants live in registers
   const PassDev& pd;
   cplx<R>* state;
+  cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
+  uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
   const uint8_t* ops;  // op stream rebased onto shared memory
   const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
   uint32_t tid;
@@ -806,14 +835,17 @@ __device__ __forceinline__ void store_slots(const cplx<R>* a, cplx<R>* cur, cons
   for (int v = 0; v < (1 << RB); ++v) cur[slot[v]] = a[v];
 }
 
-// Last round: straight from registers to HBM (lanes <-> qubits 0..4).
+// Last round: straight from registers to HBM (lanes <-> qubits 0..4, or with a
+// permuted store lanes <-> the qubits whose destinations are 0..4).
 template <typename R, int RB>
-__device__ __forceinline__ void store_global(cplx<R>* state, uint64_t Fg, const PassDev& pd, const RoundDev& rd,
+__device__ __forceinline__ void store_global(const PassCtx<R, RB>& c, uint64_t Fg, const RoundDev& rd,
                                              const cplx<R>* a) {
-  cplx<R>* g0 = state + Fg;
+  const PassDev& pd = c.pd;
+  cplx<R>* g0 = pd.perm_out ? c.out + (c.pbase | c.pthr) : c.state + Fg;
+  const int32_t* dp = pd.perm_out ? pd.dpos : pd.pos;
   size_t goff[RB];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) goff[i] = (size_t)1 << pd.pos[rd.reg_local[i]];
+  for (int i = 0; i < RB; ++i) goff[i] = (size_t)1 << dp[rd.reg_local[i]];
   size_t gv[1 << RB];
   gv[0] = 0;
 #pragma unroll
@@ -920,7 +952,7 @@ struct InterpBody {
         store_slots<R, RB>(a, cur, slot);
         __syncthreads();
       } else {
-        store_global<R, RB>(c.state, Fg, c.pd, rd, a);
+        store_global<R, RB>(c, Fg, rd, a);
       }
     }
   }
@@ -937,7 +969,8 @@ struct InterpBody {
 // layout straight from registers to HBM.
 // Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
 template <typename R, int RB, class Body>
-__device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg,
+__device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
+                                            const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
                                             int zero_input = 0, int stages = kStages, int ops_mode = 0,
                                             int nslots = 0) {
@@ -981,6 +1014,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
   cplx<R>* uni = reinterpret_cast<cplx<R>*>(smraw + ring_bytes + ((staged + 15u) & ~15u));
   PassCtx<R, RB> c(pd);
   c.state = state;
+  c.out = out;
+  c.pthr = pd.perm_out ? thread_fixed_perm(pd, pd.rounds[pd.nrounds - 1], threadIdx.x) : 0;
+  c.pbase = 0;
   c.ops = smraw + ring_bytes - pd.ops_begin;  // ops_mode 0 only
   c.uni = uni;
   // uniform slots are double-buffered by tile parity (the next tile's factors
@@ -1046,6 +1082,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
       cp_async_commit();
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
+    if (pd.perm_out) c.pbase = tile_base_warp(pd, t, lane, true);
     c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
       diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, base, const_cast<cplx<R>*>(c.uni),
@@ -1070,9 +1107,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* __restrict__ state, const P
 
 template <typename R, int RB>
 __global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
-    k_pass(cplx<R>* __restrict__ state, const PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g,
-           uint32_t ntiles, int zero_input, int stages) {
-  pass_kernel<R, RB, InterpBody>(state, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
+    k_pass(cplx<R>* state, cplx<R>* out, const PassDev* __restrict__ pdg,
+           const uint8_t* __restrict__ ops_g, uint32_t ntiles, int zero_input, int stages) {
+  pass_kernel<R, RB, InterpBody>(state, out, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
 }
 
 // Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM

@@ -244,8 +244,10 @@ void Profiler::collect() {
 template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
 template <typename R>
-static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream_t st, ProgramStats* stats,
-                          bool use_jit, bool zero_input) {
+// out: destination of the last pass when the program's final permutation is
+// fused into it (prog.perm_fused; a second state-sized buffer), else unused.
+static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& prog, cudaStream_t st,
+                          ProgramStats* stats, bool use_jit, bool zero_input) {
   constexpr int RB = rb_of<R>();
   if (prog.passes.empty()) return;
   size_t pbytes = prog.passes.size() * sizeof(PassDev);
@@ -268,7 +270,8 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (use_jit && jit_launch_passes<R>(state, prog, dpass, dops, st, stats, nsm, zero_input)) {
+  if (prog.perm_fused && out == nullptr) throw Error(SVB_E_CUDA, "permuted store without an output buffer");
+  if (use_jit && jit_launch_passes<R>(state, out, prog, dpass, dops, st, stats, nsm, zero_input)) {
     SVB_CUDA(cudaFreeAsync(dbuf, st));
     return;
   }
@@ -283,7 +286,7 @@ static void launch_passes(cplx<R>* state, int n, const Program& prog, cudaStream
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));
     k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages), st>>>(
-        state, dpass + p, dops, (uint32_t)tiles, zin, stages);
+        state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);
     stats->passes += 1;
@@ -351,7 +354,7 @@ void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int 
   SchedOptions o = opt;
   o.relabel_swaps = false;  // the handle owns its buffer; permutation passes need run_program_owned
   Program prog = build_program<R>(n, g, ng, o);
-  launch_passes<R>(static_cast<cplx<R>*>(state), n, prog, st, stats, false, false);
+  launch_passes<R>(static_cast<cplx<R>*>(state), nullptr, n, prog, st, stats, false, false);
 }
 
 // Qubit permutation of a whole state (qubit p moves to bit dest[p]), out of
@@ -403,7 +406,7 @@ template <typename R>
 static Program cached_program(int n, const svb_gate* g, int ng, const SchedOptions& opt) {
   const uint64_t salt = (uint64_t)n | ((uint64_t)sizeof(R) << 8) | ((uint64_t)opt.rb << 16) |
                         ((uint64_t)opt.m << 24) | ((uint64_t)opt.relabel_swaps << 32) |
-                        ((uint64_t)opt.round_search << 33);
+                        ((uint64_t)opt.round_search << 33) | ((uint64_t)opt.zero_start << 34);
   const ProgKey key = prog_key(g, sizeof(svb_gate) * (size_t)ng, salt);
   {
     std::lock_guard<std::mutex> lk(g_prog_mu);
@@ -465,6 +468,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   // swap relabeling needs a second state-sized buffer for the final permutation;
   // it is allocated once per handle (lazily) and reused
   const double t_info = tt.lap();
+  opt.zero_start = zero_pending && *zero_pending;
   Program prog = cached_program<R>(n, g, ng, opt);
   if (!prog.final_perm.empty() && *spare == nullptr) {
     if (cudaMalloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
@@ -477,10 +481,13 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   const double t_build = tt.lap();
   const bool zin = zero_pending && *zero_pending && !prog.passes.empty();
   if (prog.passes.empty()) write_zero();
-  launch_passes<R>(static_cast<cplx<R>*>(*state), n, prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin);
+  launch_passes<R>(static_cast<cplx<R>*>(*state), prog.perm_fused ? static_cast<cplx<R>*>(*spare) : nullptr, n,
+                   prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin);
   if (zin) *zero_pending = false;
   const double t_launch = tt.lap();
-  if (!prog.final_perm.empty()) {
+  if (prog.perm_fused) {
+    std::swap(*state, *spare);  // the last pass wrote the permuted state into the spare buffer
+  } else if (!prog.final_perm.empty()) {
     cplx<R>* s = static_cast<cplx<R>*>(*state);
     cplx<R>* sp = static_cast<cplx<R>*>(*spare);
     launch_permute<R>(&s, &sp, n, prog.final_perm, st, stats);
@@ -511,14 +518,17 @@ extern "C" {
 int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_passes, int64_t* n_rounds,
              int64_t* op_bytes, int32_t* has_perm) {
   try {
+    const bool zero_start = (precision & 0x100) != 0;  // flag bit: schedule for a lazy |0...0> input
+    precision &= 0xff;
     SchedOptions o = default_options(precision, n);
+    o.zero_start = zero_start;
     Program p = precision == SVB_C128 ? build_program<double>(n, gates, ng, o) : build_program<float>(n, gates, ng, o);
     int64_t r = 0;
     for (auto& pd : p.passes) r += pd.nrounds;
     *n_passes = (int64_t)p.passes.size();
     *n_rounds = r;
     *op_bytes = (int64_t)p.ops.size();
-    *has_perm = p.final_perm.empty() ? 0 : 1;
+    *has_perm = p.final_perm.empty() ? 0 : (p.perm_fused ? 2 : 1);  // 2: fused into the last pass
     return SVB_OK;
   } catch (const Error& e) {
     set_last_error(e.what());
@@ -532,6 +542,7 @@ int svb_emulate_apply(int n, int precision, const svb_gate* gates, int ng, doubl
   try {
     SchedOptions o = default_options(precision, n);
     o.relabel_swaps = relabel != 0;
+    o.zero_start = relabel == 2;  // caller passes |0...0> (lazy-zero layout choice)
     uint64_t len = 1ull << n;
     if (precision == SVB_C128) {
       Program p = build_program<double>(n, gates, ng, o);

@@ -436,6 +436,14 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
     if (k + 1 < pd.nrounds) {
       for (int v = 0; v < (1 << RB); ++v) o << "    cur[sFl ^ " << K[v] << "u] = a[" << v << "];\n";
       o << "    __syncthreads();\n";
+    } else if (pd.perm_out) {  // permuted store: every bit to its destination (see fuse_final_permutation)
+      uint64_t PG[1 << 5];
+      PG[0] = 0;
+      for (int i = 0; i < RB; ++i)
+        for (int v = 0; v < (1 << i); ++v) PG[v | (1 << i)] = PG[v] | (1ull << pd.dpos[rd.reg_local[i]]);
+      o << "    { svb::cplx<R>* g0 = c.out + (c.pbase | c.pthr);\n";
+      for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << PG[v] << "ull, a[" << v << "]);\n";
+      o << "    }\n";
     } else {
       o << "    { svb::cplx<R>* g0 = c.state + Fg;\n";
       for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << G[v] << "ull, a[" << v << "]);\n";
@@ -516,11 +524,11 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << kPassMinBlocks<R>
-    << ") svb_jit(svb::cplx<R>* __restrict__ state, "
+    << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody>(state, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
+    << RB << ", PassBody>(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
     << pc.nslots << ");\n}\n";
   return o.str();
 }
@@ -571,7 +579,7 @@ static std::vector<char> jit_compile(const std::string& src, std::string* log) {
 }
 
 template <typename R>
-bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass, const uint8_t* dops,
+bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
   static Driver dr;
   if (!dr.ok || prog.passes.empty()) return false;
@@ -700,12 +708,13 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
     dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
     cplx<R>* s = state;
+    cplx<R>* so = pd.perm_out ? out : state;
     const PassDev* pdp = dpass + p;
     const uint8_t* ob = dops;
     uint32_t nt = (uint32_t)tiles;
     int pass = 0;
     int zin = (zero_input && p == 0) ? 1 : 0;
-    void* args[] = {&s, &pdp, &ob, &nt, &pass, &zin, &stages};
+    void* args[] = {&s, &so, &pdp, &ob, &nt, &pass, &zin, &stages};
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
     if (dr.launch(f, grid, 1, 1, threads, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS)
@@ -717,9 +726,9 @@ bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass
   return true;
 }
 
-template bool jit_launch_passes<float>(cplx<float>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
+template bool jit_launch_passes<float>(cplx<float>*, cplx<float>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
                                        ProgramStats*, int, bool);
-template bool jit_launch_passes<double>(cplx<double>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
+template bool jit_launch_passes<double>(cplx<double>*, cplx<double>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
                                         ProgramStats*, int, bool);
 
 }  // namespace svb

@@ -11,7 +11,7 @@ bool jit_available();
 // Returns false (nothing launched) when the JIT is unavailable or fails; the
 // caller then runs the interpreter kernel.
 template <typename R>
-bool jit_launch_passes(cplx<R>* state, const Program& prog, const PassDev* dpass, const uint8_t* dops,
+bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input);
 
 }  // namespace svb

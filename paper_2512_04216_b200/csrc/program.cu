@@ -15,6 +15,8 @@
 //     when every shared qubit is acted on diagonally by both); a pass admits
 //     an op when its active qubits fit in the tile set S (|S| = m);
 //  5. rounds: consecutive ops whose active qubits fit in RB register bits.
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstddef>
 #include <cmath>
@@ -225,9 +227,18 @@ bool is_plain_swap(const svb_gate& g) {
 }
 
 // Fuse the gate list into classified ops over physical qubits.
-std::vector<FOp> fuse(int n, const svb_gate* gates, int ng, bool relabel, std::vector<int>& phys) {
+// zero_start: the input is |0...0>, which every qubit layout represents, so
+// the initial logical -> physical map is chosen such that the swap relabeling
+// ends on the identity (no final permutation at all).
+std::vector<FOp> fuse(int n, const svb_gate* gates, int ng, bool relabel, bool zero_start, std::vector<int>& phys) {
   phys.resize(n);
   for (int q = 0; q < n; ++q) phys[q] = q;
+  if (relabel && zero_start) {
+    std::vector<int> tau(phys);
+    for (int i = 0; i < ng; ++i)
+      if (gates[i].k == 2 && is_plain_swap(gates[i])) std::swap(tau[gates[i].qubits[0]], tau[gates[i].qubits[1]]);
+    for (int q = 0; q < n; ++q) phys[tau[q]] = q;
+  }
   std::vector<Block> blocks;
   std::vector<int> order;  // block indices in creation order
   std::vector<int> open(n, -1);
@@ -348,12 +359,65 @@ template <typename R> bool slots_fit(const Program& prog, const PassDev& pd) {
   return pass_smem<R>(pd.m, staged, pd.ndiag, slots, 1) <= per_cta;
 }
 
+// Fuse the program's final qubit permutation into its last pass: when that
+// pass's tile set holds every physical qubit whose destination is 0..4, its
+// last round can store out-of-place straight to the permuted addresses with
+// the warp's lanes on those qubits (512 contiguous bytes per warp store), so
+// the separate permutation pass (a full read + write of the state) goes away.
+// The last round must not keep those qubits in registers; if it does, an
+// op-free round with other register bits is appended.
+static void fuse_final_permutation(Program& prog, int n) {
+  if (prog.passes.empty() || prog.final_perm.empty()) return;
+  PassDev& pd = prog.passes.back();
+  if (std::getenv("SVB_TRACE")) {
+    for (size_t p = 0; p < prog.passes.size(); ++p) {
+      std::fprintf(stderr, "[svb] pass %zu S =", p);
+      for (int l = 0; l < prog.passes[p].m; ++l) std::fprintf(stderr, " %d", prog.passes[p].pos[l]);
+      std::fprintf(stderr, "\n");
+    }
+    std::fprintf(stderr, "[svb] final_perm:");
+    for (int p = 0; p < n; ++p) std::fprintf(stderr, " %d", prog.final_perm[p]);
+    std::fprintf(stderr, "\n");
+  }
+  int lane_l[5];
+  uint32_t lmask = 0;
+  for (int j = 0; j < 5; ++j) {
+    lane_l[j] = -1;
+    for (int p = 0; p < n; ++p)
+      if (prog.final_perm[p] == j)
+        for (int l = 0; l < pd.m; ++l)
+          if (pd.pos[l] == p) lane_l[j] = l;
+    if (lane_l[j] < 0) return;
+    lmask |= 1u << lane_l[j];
+  }
+  if (pd.rounds[pd.nrounds - 1].regmask_local & lmask) {
+    if (pd.nrounds >= kMaxRounds) return;
+    const RoundDev& prev = pd.rounds[pd.nrounds - 1];
+    RoundDev rd{};
+    uint32_t regs = 0;
+    for (int b = 0, i = 0; b < pd.m && i < pd.rb; ++b)
+      if (!(lmask & (1u << b))) { regs |= 1u << b; rd.reg_local[i++] = b; }
+    rd.regmask_local = regs;
+    rd.op_off = rd.op_end = prev.op_end;
+    pd.rounds[pd.nrounds++] = rd;
+  }
+  RoundDev& last = pd.rounds[pd.nrounds - 1];
+  int t = 0;
+  for (int j = 0; j < 5; ++j) last.thr_local[t++] = (uint8_t)lane_l[j];
+  for (int b = 0; b < pd.m; ++b)
+    if (!(last.regmask_local & (1u << b)) && !(lmask & (1u << b))) last.thr_local[t++] = (uint8_t)b;
+  for (int l = 0; l < pd.m; ++l) pd.dpos[l] = prog.final_perm[pd.pos[l]];
+  for (int i = 0; i < pd.nout; ++i) pd.doutpos[i] = prog.final_perm[pd.outpos[i]];
+  pd.perm_out = 1;
+  prog.perm_fused = true;
+}
+
 template <typename R>
 Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
   Program prog;
   prog.gates = ng;
   std::vector<int> phys;
-  std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, phys);
+  std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, opt.zero_start, phys);
   const int m = std::min(opt.m, n);
   const int RB = opt.rb;
   require(m - RB >= 5 && m <= kMaxM, SVB_E_ARG, "fused program needs n >= rb + 5");
@@ -599,6 +663,8 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
           regidx_of_local[b] = -1;
           if (regs & (1u << b)) { rd.reg_local[i] = b; regidx_of_local[b] = i; ++i; }
         }
+        for (int b = 0, t = 0; b < m; ++b)
+          if (!(regs & (1u << b))) rd.thr_local[t++] = (uint8_t)b;
         auto ridx = [&](int q) { return (q >= 0 && local_of[q] >= 0) ? regidx_of_local[local_of[q]] : -1; };
         // one DIAG op from a list of 2-qubit (or 1-qubit, qb = -1) factors
         auto encode_diag = [&](const std::vector<DT>& terms) {
@@ -829,6 +895,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     // data of logical qubit q sits at physical bit phys[q]; move it to bit q
     prog.final_perm.assign(n, 0);
     for (int q = 0; q < n; ++q) prog.final_perm[phys[q]] = q;
+    fuse_final_permutation(prog, n);
   }
   return prog;
 }
@@ -837,8 +904,18 @@ template Program build_program<float>(int, const svb_gate*, int, const SchedOpti
 template Program build_program<double>(int, const svb_gate*, int, const SchedOptions&);
 
 // ------------------------------------------------------------- emulation
+static uint64_t permute_index(const PassDev& pd, uint64_t g) {
+  uint64_t o = 0;
+  for (int l = 0; l < pd.m; ++l)
+    if ((g >> pd.pos[l]) & 1ull) o |= 1ull << pd.dpos[l];
+  for (int i = 0; i < pd.nout; ++i)
+    if ((g >> pd.outpos[i]) & 1ull) o |= 1ull << pd.doutpos[i];
+  return o;
+}
+
+// out: destination of a permuted-store pass (pd.perm_out), else unused
 template <typename R, int RB>
-static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t* ops) {
+static void emulate_pass(cplx<R>* state, cplx<R>* out, int n, const PassDev& pd, const uint8_t* ops) {
   constexpr int V = 1 << RB;
   const int m = pd.m;
   const uint32_t NT = 1u << (m - RB);
@@ -869,8 +946,9 @@ static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t
         }
         run_ops<R, RB>(a, Fg, ops, rd.op_off, rd.op_end, uni.data());
         for (int v = 0; v < V; ++v) {
-          if (k == pd.nrounds - 1) state[gidx[v]] = a[v];
-          else tile[lidx[v]] = a[v];
+          if (k < pd.nrounds - 1) tile[lidx[v]] = a[v];
+          else if (pd.perm_out) out[permute_index(pd, gidx[v])] = a[v];
+          else state[gidx[v]] = a[v];
         }
       }
     }
@@ -879,11 +957,14 @@ static void emulate_pass(cplx<R>* state, int n, const PassDev& pd, const uint8_t
 
 template <typename R>
 void emulate_program(cplx<R>* state, int n, const Program& prog) {
+  std::vector<cplx<R>> out(prog.perm_fused ? (size_t)1 << n : 0);
   for (const PassDev& pd : prog.passes) {
-    if (pd.rb == 4) emulate_pass<R, 4>(state, n, pd, prog.ops.data());
-    else emulate_pass<R, 5>(state, n, pd, prog.ops.data());
+    if (pd.rb == 4) emulate_pass<R, 4>(state, out.data(), n, pd, prog.ops.data());
+    else emulate_pass<R, 5>(state, out.data(), n, pd, prog.ops.data());
   }
-  if (!prog.final_perm.empty()) {
+  if (prog.perm_fused) {
+    std::copy(out.begin(), out.end(), state);
+  } else if (!prog.final_perm.empty()) {
     uint64_t len = 1ull << n;
     std::vector<cplx<R>> out(len);
     for (uint64_t i = 0; i < len; ++i) {

@@ -43,6 +43,7 @@ struct Program {
   std::vector<PassDev> passes;
   std::vector<uint8_t> ops;          // op stream (all passes)
   std::vector<int> final_perm;       // physical bit p must move to bit final_perm[p]; empty = identity
+  bool perm_fused = false;           // final_perm is done by the last pass's permuted store (PassDev::perm_out)
   int64_t gates = 0;
 };
 
@@ -50,6 +51,7 @@ struct SchedOptions {
   int rb = 4;        // register bits per thread
   int m = 12;        // tile qubits
   bool relabel_swaps = true;
+  bool zero_start = false;   // input is |0...0>: choose the initial qubit layout so no final permutation is needed
   bool round_search = true;  // reorder ops across rounds (else program order)
 };
 

@@ -682,15 +682,16 @@ def expectations(c, z_sets, qubit_cap: int = DEFAULT_QUBIT_CAP) -> np.ndarray:
     return entry.device.expect_z(masks)
 
 
-def plan(n: int, instructions, precision: str = "c128") -> dict:
-    """Host-only schedule summary of a gate program (no GPU needed)."""
+def plan(n: int, instructions, precision: str = "c128", zero_start: bool = False) -> dict:
+    """Host-only schedule summary of a gate program (no GPU needed).
+    zero_start: schedule for a lazy |0...0> input (free initial qubit layout)."""
     arr = gate_array(instructions)
     p, r, b = _lib.c_int64(), _lib.c_int64(), _lib.c_int64()
     perm = _lib.c_int32()
-    check(lib().svb_plan(n, _prec_code(precision), ptr(arr), int(arr.size), _lib.ctypes.byref(p),
+    check(lib().svb_plan(n, _prec_code(precision) | (0x100 if zero_start else 0), ptr(arr), int(arr.size), _lib.ctypes.byref(p),
                          _lib.ctypes.byref(r), _lib.ctypes.byref(b), _lib.ctypes.byref(perm)))
     return {"passes": p.value, "rounds": r.value, "op_bytes": b.value, "permute": bool(perm.value),
-            "gates": int(arr.size)}
+            "permute_fused": perm.value == 2, "gates": int(arr.size)}
 
 
 def emulate(n: int, instructions, amps: np.ndarray, precision: str = "c128", relabel: bool = True) -> np.ndarray:

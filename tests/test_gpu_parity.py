@@ -399,3 +399,44 @@ def test_run_codes_arrays_equal_run_counts():
             b = sv.run(c, 2000, seed).counts
             assert a.to_dict() == b
             assert int(a.counts.sum()) == 2000 and np.all(np.diff(a.codes.astype(np.int64)) > 0)
+
+
+def _swap_tail_circuit(n, seed):
+    """Random gates followed by swaps that move low qubits up: the final qubit
+    permutation of the swap relabeling is fused into the last pass's store."""
+    rng = np.random.default_rng(seed)
+    c = suite.random_circuit(n, 80, rng, measured=False)
+    for q in range(5):
+        c.gate("swap", q, 5 + q)
+    for q in range(5, 12):
+        c.gate("u", q, params=tuple(float(x) for x in rng.uniform(0, 6.3, 3)))
+    return c
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_permuted_store_and_zero_start_layout(precision):
+    """Swap relabeling on device: (a) on an arbitrary input state the final
+    permutation is fused into the last pass (out-of-place permuted store),
+    JIT and interpreter bodies; (b) on a lazy |0...0> the initial layout absorbs
+    it.  Both against the oracle."""
+    for body in (suite.qft_bench_circuit(12), _swap_tail_circuit(14, 1)):
+        n = body.n_qubits
+        prep = suite.random_circuit(n, 40, np.random.default_rng(5), measured=False)
+        assert sv.plan(n, body.instructions, precision)["permute_fused"], body.name
+        ref = orc.unitary_state(prep)
+        for inst in body.instructions:
+            orc.apply_instruction(ref, n, inst)
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            s.apply_instructions(prep.instructions)
+            s.apply_instructions(body.instructions)
+            assert relerr(s.to_numpy(), ref) < TOL[precision], (body.name, jit)
+            s.close()
+        ref0 = orc.unitary_state(body)
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            s.apply_instructions(body.instructions)
+            assert relerr(s.to_numpy(), ref0) < TOL[precision], (body.name, jit)
+            s.close()

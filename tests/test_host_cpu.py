@@ -105,7 +105,10 @@ def test_library_reports_errors_without_gpu():
 
 
 # ---------------------------------------------------------- scheduler (CPU)
-def _emu_check(c, prec, tol, relabel=True):
+def _emu_check(c, prec, tol, relabel=1):
+    """relabel: 0 = swaps as ops, 1 = swap relabeling + final permutation
+    (separate pass or fused into the last pass's store), 2 = relabeling with
+    the lazy-zero layout choice (initial layout makes the final map identity)."""
     n = c.n_qubits
     ref = orc.unitary_state(c)
     psi0 = np.zeros(1 << n, dtype=complex)
@@ -121,7 +124,7 @@ def test_fused_program_random_circuits(prec, tol, nmin):
     for trial in range(25):
         n = int(rng.integers(nmin, nmin + 4))
         c = suite.random_circuit(n, int(rng.integers(1, 150)), rng, measured=False)
-        _emu_check(c, prec, tol, relabel=bool(trial % 2))
+        _emu_check(c, prec, tol, relabel=trial % 3)
 
 
 def test_fused_program_structured_circuits():
@@ -132,8 +135,57 @@ def test_fused_program_structured_circuits():
         suite.ry_ansatz_circuit(11, 3, seed=2, measured=False),
         suite.ghz_circuit(14, measured=False),
     ):
-        _emu_check(c, "c128", 1e-12)
-        _emu_check(c, "c64", 1e-5)
+        for relabel in (1, 2):
+            _emu_check(c, "c128", 1e-12, relabel)
+            _emu_check(c, "c64", 1e-5, relabel)
+
+
+def _random_state(n, seed):
+    rng = np.random.default_rng(seed)
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return psi / np.linalg.norm(psi)
+
+
+@pytest.mark.parametrize("n", [12, 13])
+def test_permuted_store_fused_into_last_pass(n):
+    """QFT-n on an arbitrary input state: its final bit reversal lands in the
+    last pass's tile set, so the permutation is done by that pass's store."""
+    c = suite.qft_bench_circuit(n)
+    p = sv.plan(n, c.instructions, "c128")
+    if n == 12:
+        assert p["permute_fused"], p
+    psi0 = _random_state(n, n)
+    ref = psi0.copy()
+    for inst in c.instructions:
+        orc.apply_instruction(ref, n, inst)
+    for prec, tol in (("c128", 1e-12), ("c64", 1e-5)):
+        got = sv.emulate(n, c.instructions, psi0, prec, relabel=1)
+        assert np.linalg.norm(got - ref) < tol, prec
+
+
+def test_random_swap_circuits_on_arbitrary_state():
+    rng = np.random.default_rng(21)
+    fused = 0
+    for trial in range(12):
+        n = int(rng.integers(10, 13))
+        c = Circuit(n)
+        for _ in range(int(rng.integers(5, 60))):
+            r = rng.random()
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            if r < 0.35:
+                c.gate("swap", a, b)
+            elif r < 0.6:
+                c.gate("cx", a, b)
+            else:
+                c.gate("u", a, params=tuple(float(x) for x in rng.uniform(0, 6.3, 3)))
+        psi0 = _random_state(n, trial)
+        ref = psi0.copy()
+        for inst in c.instructions:
+            orc.apply_instruction(ref, n, inst)
+        fused += sv.plan(n, c.instructions, "c128")["permute_fused"]
+        got = sv.emulate(n, c.instructions, psi0, "c128", relabel=1)
+        assert np.linalg.norm(got - ref) < 1e-12, trial
+    assert fused > 0  # the permuted-store path was exercised
 
 
 def test_fused_program_dft_known_answer():
@@ -165,6 +217,8 @@ def test_mirror_circuit_returns_to_zero():
 def test_plan_pass_counts():
     p = sv.plan(30, suite.qft_bench_circuit(30).instructions, "c128")
     assert p["passes"] == 4 and p["permute"]  # ceil((30 - 5) / 7): every pass advances 7 qubits
+    p = sv.plan(30, suite.qft_bench_circuit(30).instructions, "c128", zero_start=True)
+    assert p["passes"] == 4 and not p["permute"]  # lazy |0...0>: the layout absorbs the bit reversal
     p = sv.plan(24, [Instruction("h", (q,)) for q in range(24)], "c128")
     assert p["passes"] == math.ceil((24 - 5) / 7)
 
@@ -262,7 +316,7 @@ def test_calibration_host_logic():
         _sys.path.remove(ref_src)
 
 
-@pytest.mark.parametrize("which", ["qft30_c128", "qft20_c128", "syc_c64", "random_c64"])
+@pytest.mark.parametrize("which", ["qft30_c128", "qft20_c128", "qft12_permstore", "syc_c64", "random_c64"])
 def test_jit_sources_compile(which):
     """NVRTC compiles every generated pass kernel (a failure would otherwise
     fall back to the interpreter body at run time)."""
@@ -272,6 +326,8 @@ def test_jit_sources_compile(which):
         n, prec, c = 30, 1, suite.qft_bench_circuit(30)
     elif which == "qft20_c128":
         n, prec, c = 20, 1, suite.qft_bench_circuit(20)
+    elif which == "qft12_permstore":  # last pass stores to the bit-reversed addresses
+        n, prec, c = 12, 1, suite.qft_bench_circuit(12)
     elif which == "syc_c64":
         n, prec, c = 28, 0, suite.sycamore_circuit(4, 7, 12, seed=0, measured=False)
     else:

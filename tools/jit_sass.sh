@@ -8,7 +8,9 @@ SVB_JIT_DUMP=/tmp/jit_all.cu python - "$n" "$prec" <<'PY'
 import ctypes, sys
 from paper_2512_04216_b200 import _lib, suite, statevector as sv
 n, prec = int(sys.argv[1]), int(sys.argv[2])
-g = sv.gate_array(suite.qft_bench_circuit(n).instructions)
+import os
+c = suite.sycamore_circuit(4, 8, 20, 0, measured=False) if os.environ.get("SYC") else suite.qft_bench_circuit(n)
+g = sv.gate_array(c.instructions)
 cb = ctypes.c_int64(); buf = ctypes.create_string_buffer(4096)
 rc = _lib.lib().svb_jit_check(n, prec, g.ctypes.data_as(ctypes.c_void_p), g.size, ctypes.byref(cb), buf, 4096)
 assert rc == 0, buf.value
