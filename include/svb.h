@@ -108,6 +108,13 @@ int svb_get_amplitudes(svb_handle h, double* host, uint64_t offset, uint64_t cou
  * HBM passes natively; the result equals applying the gates
  * one by one in order. */
 int svb_apply(svb_handle h, const svb_gate* gates, int n_gates);
+/* Apply a gate program and return out[j] = <Z_{z_qubits[j]}> of the resulting
+ * state (single-qubit Z; statevector.py:277-292 per qubit, after
+ * statevector.py:116-122 for every gate).  The sums are accumulated by the
+ * program's last fused pass as it stores the state, so no separate read pass
+ * is needed; unfused programs fall back to one reduction pass.  nz may be 0. */
+int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t* z_qubits, int nz,
+                double* out);
 
 /* Reduced |amp|^2 over ascending `qubits` (marginal_probs, statevector.py:131-139). */
 int svb_marginal_probs(svb_handle h, const int32_t* qubits, int k, double* out);

@@ -64,6 +64,7 @@ _SIGS = {
     "svb_set_amplitudes": (c_int, [_h, c_void_p, c_uint64, c_uint64]),
     "svb_get_amplitudes": (c_int, [_h, c_void_p, c_uint64, c_uint64]),
     "svb_apply": (c_int, [_h, c_void_p, c_int]),
+    "svb_apply_z": (c_int, [_h, c_void_p, c_int, _i32p, c_int, _dp]),
     "svb_marginal_probs": (c_int, [_h, _i32p, c_int, _dp]),
     "svb_expect_z": (c_int, [_h, _u64p, c_int, _dp]),
     "svb_sample": (c_int, [_h, _i32p, c_int, _i32p, c_int, c_uint64, _u64p, c_int, _u64p, _u64p, _u64p]),

@@ -296,6 +296,61 @@ int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
   });
 }
 
+// Apply a gate program and return <Z_q> for single qubits q (after the
+// program).  The sums are accumulated by the program's last fused pass while it
+// stores the state (no separate read pass); programs that are not fused fall
+// back to one multi-mask reduction pass.  statevector.py:277-292 per qubit.
+int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t* z_qubits, int nz, double* out) {
+  return guard([&] {
+    check_handle_nomat(h);
+    validate_gates(h, gates, n_gates);
+    require(nz >= 0, SVB_E_ARG, "bad qubit count");
+    for (int j = 0; j < nz; ++j) require(z_qubits[j] >= 0 && z_qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
+    h->stats = ProgramStats{};
+    h->stats.prof = &h->prof;
+    ensure_ws(h, (size_t)kZaccRows * kZaccCols + kZaccRows + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
+    ZRequest z;
+    z.want = nz > 0;
+    z.d_acc = h->d_ws;
+    z.d_out = h->d_ws + (size_t)kZaccRows * kZaccCols;
+    if (h->prec == SVB_C128)
+      run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats,
+                                &h->zero_pending, &z);
+    else
+      run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats,
+                               &h->zero_pending, &z);
+    if (nz == 0) {
+      SVB_CUDA(cudaStreamSynchronize(h->st));
+      if (h->prof.on) h->prof.collect();
+      return;
+    }
+    if (z.fused) {
+      std::vector<double> vals(z.logical.size());
+      SVB_CUDA(cudaMemcpyAsync(vals.data(), z.d_out, vals.size() * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      SVB_CUDA(cudaStreamSynchronize(h->st));
+      std::vector<double> by_q(h->n, 0.0);
+      std::vector<int> seen(h->n, 0);
+      for (size_t k = 0; k < z.logical.size(); ++k)
+        if (z.logical[k] >= 0) { by_q[z.logical[k]] = vals[k]; seen[z.logical[k]] = 1; }
+      for (int j = 0; j < nz; ++j) {
+        require(seen[z_qubits[j]], SVB_E_CUDA, "fused <Z>: qubit not covered");
+        out[j] = by_q[z_qubits[j]];
+      }
+    } else {
+      materialize(h);
+      std::vector<uint64_t> masks(nz);
+      for (int j = 0; j < nz; ++j) masks[j] = 1ull << z_qubits[j];
+      double* d_out = z.d_out;
+      double* d_ws = z.d_out + kZaccRows;
+      if (h->prec == SVB_C128) launch_expect_z<double>(h->amps, h->n, masks.data(), nz, d_out, d_ws, h->st);
+      else launch_expect_z<float>(h->amps, h->n, masks.data(), nz, d_out, d_ws, h->st);
+      SVB_CUDA(cudaMemcpyAsync(out, d_out, nz * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      SVB_CUDA(cudaStreamSynchronize(h->st));
+    }
+    if (h->prof.on) h->prof.collect();
+  });
+}
+
 int svb_profile(svb_handle h, int enable) {
   return guard([&] {
     check_handle(h);

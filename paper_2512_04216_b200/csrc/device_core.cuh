@@ -129,13 +129,21 @@ struct PassDev {
   // pass): the last round writes out-of-place to bit dest(p) for every
   // physical bit p; dpos[l] = dest(pos[l]), doutpos[i] = dest(outpos[i])
   int32_t perm_out;
-  int32_t pad2[2];
+  // fused <Z_q> sums (last pass of an apply that asked for single-qubit <Z>):
+  // per-CTA partials of sum p (-1)^bit for every register bit of the last
+  // round, every thread bit and every tile bit, plus sum p, are written to
+  // zacc[k * kZaccCols + blockIdx.x] (see zsum_tile / zsum_finish)
+  int32_t zsum;
+  int32_t pad2;
   uint16_t items[kMaxItems];
   int32_t dpos[16];
   int32_t doutpos[48];
+  uint64_t zacc;
+  uint64_t pad3;
 };
 static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
+constexpr int kZaccRows = 64, kZaccCols = 1024;  // fused <Z> partials: values x CTAs (grid <= kZaccCols)
 
 // ------------------------------------------------------------ interpreter
 #define SVB_HD __host__ __device__ __forceinline__
@@ -734,6 +742,8 @@ template <typename R, int RB> struct PassCtx {
   const PassDev& pd;
   cplx<R>* state;
   cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
+  double* zs;            // fused <Z>: per-thread sums [RB + 1][nthr] (shared memory)
+  double* zw;            // fused <Z>: per-warp tile-bit sums [nwarps][64] (shared memory)
   uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
   const uint8_t* ops;  // op stream rebased onto shared memory
   const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
@@ -874,6 +884,62 @@ __device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg
   }
 }
 
+// Fused <Z_q> of the last round (pd.zsum): p_v = |a_v|^2 of the thread's 2^RB
+// amplitudes; the thread adds T = sum p and W_i = sum p (-1)^(v_i) to its
+// shared-memory slots; the warp adds +-(warp sum of T) to the slot of every
+// tile bit (lane j owns tile bits j and j + 32).  Thread-bit signs are applied
+// once at the end (zsum_finish), since a thread's fixed bits never change.
+template <typename R, int RB>
+__device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>* a, uint64_t base) {
+  double p[1 << RB];
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) p[v] = (double)a[v].x * (double)a[v].x + (double)a[v].y * (double)a[v].y;
+  double T = 0.0;
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) T += p[v];
+  const uint32_t nthr = c.nthr, tid = c.tid;
+  c.zs[tid] += T;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    double s1 = 0.0;
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v)
+      if (v & (1 << i)) s1 += p[v];
+    c.zs[(1 + i) * nthr + tid] += fma(-2.0, s1, T);
+  }
+  double tw = T;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
+  const uint32_t lane = tid & 31u, w = tid >> 5;
+  double* zw = c.zw + w * 64;
+  if ((int)lane < c.pd.nout) zw[lane] += ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw;
+  if ((int)lane + 32 < c.pd.nout) zw[lane + 32] += ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw;
+}
+
+// After the tile loop (all threads, after a barrier): CTA partials
+// [W_0..W_{RB-1} | thread bits 0..nt-1 | tile bits 0..nout-1 | sum p].
+template <typename R, int RB>
+__device__ __forceinline__ void zsum_finish(const PassCtx<R, RB>& c) {
+  const PassDev& pd = c.pd;
+  const int nt = pd.m - pd.rb, nw = (int)(c.nthr >> 5);
+  const int nv = RB + nt + pd.nout + 1;
+  const int k = (int)c.tid;
+  if (k >= nv) return;
+  double acc = 0.0;
+  if (k < RB) {
+    for (uint32_t t = 0; t < c.nthr; ++t) acc += c.zs[(1 + k) * c.nthr + t];
+  } else if (k < RB + nt) {
+    const int b = k - RB;
+    for (uint32_t t = 0; t < c.nthr; ++t) acc += ((t >> b) & 1u) ? -c.zs[t] : c.zs[t];
+  } else if (k < RB + nt + pd.nout) {
+    const int j = k - RB - nt;
+    for (int w = 0; w < nw; ++w) acc += c.zw[w * 64 + j];
+  } else {
+    for (uint32_t t = 0; t < c.nthr; ++t) acc += c.zs[t];
+  }
+  reinterpret_cast<double*>(pd.zacc)[(size_t)k * kZaccCols + blockIdx.x] = acc;
+}
+
 // Helpers for JIT-generated diagonal code.
 template <typename R> __device__ __forceinline__ cplx<R> csel(int f, cplx<R> x0, cplx<R> x1) { return f ? x1 : x0; }
 template <typename R> __device__ __forceinline__ cplx<R> conj_mul(cplx<R> x, cplx<R> u) {
@@ -906,6 +972,12 @@ __device__ __forceinline__ void neg_quad(cplx<R>* a) {  // factor exactly -1 (cz
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v)
     if ((((v >> IA) & 1) + 2 * ((v >> IB) & 1)) == Q) a[v] = mk<R>(-a[v].x, -a[v].y);
+}
+template <typename R, int RB, int IA, int IB, int Q, int S>
+__device__ __forceinline__ void imul_quad(cplx<R>* a) {  // factor exactly S*i (S = +-1): no flops
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v)
+    if ((((v >> IA) & 1) + 2 * ((v >> IB) & 1)) == Q) a[v] = S > 0 ? mk<R>(-a[v].y, a[v].x) : mk<R>(a[v].y, -a[v].x);
 }
 template <typename R, int RB, int IA, int IB, int Q>
 __device__ __forceinline__ void mul_quad(cplx<R>* a, cplx<R> d) {  // amps with bit(IA) + 2 bit(IB) == Q
@@ -952,6 +1024,7 @@ struct InterpBody {
         store_slots<R, RB>(a, cur, slot);
         __syncthreads();
       } else {
+        if (c.pd.zsum) zsum_tile<R, RB>(c, a, base);
         store_global<R, RB>(c, Fg, rd, a);
       }
     }
@@ -1023,7 +1096,11 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // are written while slow warps may still read this tile's)
   c.pro = uni + 2 * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
-  (void)nslots;
+  c.zs = reinterpret_cast<double*>(c.pro + (size_t)nslots * blockDim.x);
+  c.zw = c.zs + (size_t)(RB + 1) * blockDim.x;
+  if (pd.zsum) {
+    for (uint32_t i = threadIdx.x; i < (RB + 1) * blockDim.x + (blockDim.x >> 5) * 64; i += blockDim.x) c.zs[i] = 0.0;
+  }
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
@@ -1103,6 +1180,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages > 1) __syncthreads();
   }
   cp_async_wait<0>();
+  if (pd.zsum) {
+    __syncthreads();
+    zsum_finish<R, RB>(c);
+  }
 }
 
 template <typename R, int RB>
@@ -1115,19 +1196,23 @@ __global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
 // Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM
 // when the op stream fits the per-CTA shared memory budget, else two stages
 // and one CTA per SM.  Returns the dynamic shared memory bytes.
+// zsum: the pass accumulates fused <Z> sums (PassDev::zsum): (RB + 1) doubles
+// per thread and 64 per warp.
 template <typename R>
-__host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages) {
+__host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
+                                              int zsum = 0) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
   return (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
-         (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>);
+         (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
+         (zsum ? ((uint32_t)(kRegBits<R> + 1) * nthr + (nthr >> 5) * 64u) * 8u : 0u);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
-__host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots) {
+__host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {
   if (kPassMinBlocks<R> < 2) return 2;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
-  return pass_smem<R>(m, staged_ops, ndiag, nslots, 1) <= per_cta ? 1 : 2;
+  return pass_smem<R>(m, staged_ops, ndiag, nslots, 1, zsum) <= per_cta ? 1 : 2;
 }
 
 }  // namespace svb

@@ -243,11 +243,12 @@ void Profiler::collect() {
 // ------------------------------------------------------------ run_program
 template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
-template <typename R>
 // out: destination of the last pass when the program's final permutation is
 // fused into it (prog.perm_fused; a second state-sized buffer), else unused.
+// zacc: fused <Z> scratch (kZaccRows x kZaccCols doubles) when the last pass has zsum.
+template <typename R>
 static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& prog, cudaStream_t st,
-                          ProgramStats* stats, bool use_jit, bool zero_input) {
+                          ProgramStats* stats, bool use_jit, bool zero_input, double* zacc = nullptr) {
   constexpr int RB = rb_of<R>();
   if (prog.passes.empty()) return;
   size_t pbytes = prog.passes.size() * sizeof(PassDev);
@@ -259,6 +260,14 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     SVB_CUDA(cudaMemcpyAsync(dbuf + pbytes, prog.ops.data(), prog.ops.size(), cudaMemcpyHostToDevice, st));
   const PassDev* dpass = reinterpret_cast<const PassDev*>(dbuf);
   const uint8_t* dops = dbuf + pbytes;
+  if (prog.passes.back().zsum) {  // device-side pointer only: the host PassDev (and JIT cache keys) keep zacc = 0
+    if (zacc == nullptr) throw Error(SVB_E_CUDA, "fused <Z> without a scratch buffer");
+    const uint64_t zp = (uint64_t)(uintptr_t)zacc;
+    PassDev* last = reinterpret_cast<PassDev*>(dbuf) + (prog.passes.size() - 1);
+    SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * kZaccRows * kZaccCols, st));
+    SVB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp,
+                             cudaMemcpyHostToDevice, st));
+  }
   // the attribute is per function and process-wide: set it once to the largest
   // size any program can request (a per-call value would race between threads
   // launching different programs)
@@ -279,13 +288,13 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0);
+    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, pd.zsum);
     if (stages == 1 && pd.direct && std::getenv("SVB_DIRECT")) stages = 0;  // measured slower (load latency exposed)
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));
-    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages), st>>>(
+    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, pd.zsum), st>>>(
         state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);
@@ -446,7 +455,7 @@ struct TraceTimer {
 
 template <typename R>
 void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, int jit_min_n,
-                       cudaStream_t st, ProgramStats* stats, bool* zero_pending) {
+                       cudaStream_t st, ProgramStats* stats, bool* zero_pending, ZRequest* z) {
   TraceTimer tt;
   stats->gates += ng;
   SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
@@ -470,6 +479,24 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   const double t_info = tt.lap();
   opt.zero_start = zero_pending && *zero_pending;
   Program prog = cached_program<R>(n, g, ng, opt);
+  // fused <Z>: the last pass's value k -> logical qubit
+  auto z_setup = [&](Program& pr) {
+    if (!z || !z->want || pr.passes.empty()) return;
+    PassDev& pd = pr.passes.back();
+    const RoundDev& rd = pd.rounds[pd.nrounds - 1];
+    const int RBv = pd.rb, nt = pd.m - pd.rb;
+    if (RBv + nt + pd.nout + 1 > kZaccRows) return;
+    std::vector<int> phys;
+    for (int i = 0; i < RBv; ++i) phys.push_back(pd.pos[rd.reg_local[i]]);
+    for (int b = 0; b < nt; ++b) phys.push_back(pd.pos[rd.thr_local[b]]);
+    for (int j = 0; j < pd.nout; ++j) phys.push_back(pd.outpos[j]);
+    z->logical.clear();
+    for (int p : phys) z->logical.push_back(pr.final_perm.empty() ? p : pr.final_perm[p]);
+    z->logical.push_back(-1);
+    pd.zsum = 1;
+    z->fused = true;
+  };
+  if (z) z->fused = false;
   if (!prog.final_perm.empty() && *spare == nullptr) {
     if (cudaMalloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
       cudaGetLastError();
@@ -479,10 +506,12 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     }
   }
   const double t_build = tt.lap();
+  z_setup(prog);
   const bool zin = zero_pending && *zero_pending && !prog.passes.empty();
   if (prog.passes.empty()) write_zero();
   launch_passes<R>(static_cast<cplx<R>*>(*state), prog.perm_fused ? static_cast<cplx<R>*>(*spare) : nullptr, n,
-                   prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin);
+                   prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
+  if (z && z->fused) launch_sum_rows(z->d_acc, (uint64_t)z->logical.size(), kZaccCols, z->d_out, st);
   if (zin) *zero_pending = false;
   const double t_launch = tt.lap();
   if (prog.perm_fused) {
@@ -503,9 +532,9 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
 template void run_program<float>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
 template void run_program<double>(void*, int, const svb_gate*, int, int, int, cudaStream_t, ProgramStats*);
 template void run_program_owned<float>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
-                                       ProgramStats*, bool*);
+                                       ProgramStats*, bool*, ZRequest*);
 template void run_program_owned<double>(void**, void**, int, const svb_gate*, int, int, int, cudaStream_t,
-                                        ProgramStats*, bool*);
+                                        ProgramStats*, bool*, ZRequest*);
 
 }  // namespace svb
 

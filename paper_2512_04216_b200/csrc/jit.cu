@@ -275,6 +275,9 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
       if (!is1(rr[k].d[q])) {
         if (rr[k].d[q].x == -1 && rr[k].d[q].y == 0)
           o << "      svb::neg_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a);\n";
+        else if (rr[k].d[q].x == 0 && (rr[k].d[q].y == 1 || rr[k].d[q].y == -1))
+          o << "      svb::imul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ", "
+            << (rr[k].d[q].y > 0 ? 1 : -1) << ">(a);\n";
         else
           o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
             << dref(rr + k, q) << ");\n";
@@ -433,6 +436,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       }
       off += h.bytes;
     }
+    if (k + 1 == pd.nrounds && pd.zsum) o << "    svb::zsum_tile<R, RB>(c, a, base);\n";
     if (k + 1 < pd.nrounds) {
       for (int v = 0; v < (1 << RB); ++v) o << "    cur[sFl ^ " << K[v] << "u] = a[" << v << "];\n";
       o << "    __syncthreads();\n";
@@ -622,7 +626,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
           staged[p] += h.bytes - (uint32_t)sizeof(OpHdr);
         }
       }
-      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2) > kSmemMaxPerCTA) return false;
+      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2, pd.zsum) > kSmemMaxPerCTA) return false;
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
@@ -693,11 +697,11 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p]);
+    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p], pd.zsum);
     if (stages == 1 && pd.direct && std::getenv("SVB_DIRECT")) stages = 0;  // measured slower (load latency exposed)
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
-    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages);
+    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum);
     static const bool trace = std::getenv("SVB_TRACE") != nullptr;
     if (trace)
       std::fprintf(stderr, "[svb] jit pass %zu: m=%d rounds=%d stages=%d grid=%u smem=%u staged=%u ndiag=%d slots=%d\n",
@@ -741,13 +745,19 @@ using namespace svb;
 extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng, int64_t* cubin_bytes, char* log,
                              int log_cap) {
   try {
+    const bool zero_start = (precision & 0x100) != 0;  // flag bit: schedule for a lazy |0...0> input
+    const bool zsum = (precision & 0x200) != 0;        // flag bit: last pass accumulates fused <Z>
+    precision &= 0xff;
     SchedOptions o = default_options(precision, n);
+    o.zero_start = zero_start;
     std::vector<std::string> srcs;
     if (precision == SVB_C128) {
       Program p = build_program<double>(n, gates, ng, o);
+      if (zsum && !p.passes.empty()) p.passes.back().zsum = 1;
       for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<double>(p, (int)k, nullptr, nullptr));
     } else {
       Program p = build_program<float>(n, gates, ng, o);
+      if (zsum && !p.passes.empty()) p.passes.back().zsum = 1;
       for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<float>(p, (int)k, nullptr, nullptr));
     }
     if (std::getenv("SVB_JIT_DUMP") && !srcs.empty()) {

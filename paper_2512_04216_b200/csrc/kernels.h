@@ -20,6 +20,8 @@ template <typename R>
 void launch_expect_z(const void* state, int n, const uint64_t* h_masks, int m, double* d_out,
                      double* d_ws, cudaStream_t st);
 size_t expect_ws_doubles(int n, int m);
+// out[r] = sum_c partial[r * cols + c]
+void launch_sum_rows(const double* d_partial, uint64_t rows, uint64_t cols, double* d_out, cudaStream_t st);
 // Measure/reset qubit q with the device PCG64 stream d_rng; outcome recorded in
 // d_out[0] (int32) and, when d_codes != nullptr, OR-ed into d_codes[0] << rank.
 template <typename R>

@@ -90,6 +90,11 @@ __global__ void k_sum_rows(const double* __restrict__ partial, uint64_t rows, ui
   out[o] = acc;
 }
 
+void launch_sum_rows(const double* d_partial, uint64_t rows, uint64_t cols, double* d_out, cudaStream_t st) {
+  k_sum_rows<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(d_partial, rows, cols, d_out);
+  SVB_CHECK_LAUNCH();
+}
+
 static void marg_geometry(int n, int k, uint64_t* nch, uint64_t* chunk) {
   uint64_t rlen = 1ull << (n - k);
   *chunk = rlen < 16384 ? rlen : 16384;

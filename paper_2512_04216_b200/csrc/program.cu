@@ -98,6 +98,10 @@ inline cd snap(cd z) {
   double re = z.real(), im = z.imag();
   if (std::fabs(re - 1.0) <= t && std::fabs(im) <= t) return cd(1.0, 0.0);
   if (std::fabs(re) <= t * 1e-3 && std::fabs(im) <= t * 1e-3) return cd(0.0, 0.0);
+  // the other unit phases (-1, +-i: e.g. e^{i pi/2} = 6e-17 + 1i) become exact,
+  // so the code generator emits swaps / negations instead of complex products
+  if (std::fabs(re + 1.0) <= t && std::fabs(im) <= t) return cd(-1.0, 0.0);
+  if (std::fabs(re) <= t && std::fabs(std::fabs(im) - 1.0) <= t) return cd(0.0, im > 0 ? 1.0 : -1.0);
   return z;
 }
 

@@ -74,11 +74,24 @@ template <typename R>
 void run_permutation(void** state, void** spare, int n, const std::vector<int>& dest, cudaStream_t st,
                      ProgramStats* stats);
 
+// Fused single-qubit <Z> (optional argument of run_program_owned): when
+// `want`, the last fused pass accumulates sum p (-1)^bit for every qubit and
+// d_out (device, >= kZaccRows doubles) receives them; `fused` reports whether
+// that happened (else the caller runs a separate reduction) and logical[k] is
+// the logical qubit of value k (-1: the total sum p).
+struct ZRequest {
+  bool want = false;
+  double* d_out = nullptr;
+  double* d_acc = nullptr;  // kZaccRows x kZaccCols scratch (device)
+  bool fused = false;
+  std::vector<int> logical;
+};
+
 // zero_pending (may be null): the state is a lazy |0...0>; the first fused
 // pass synthesises it instead of reading HBM (other paths write it first).
 template <typename R>
 void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int ng, int fusion, int jit_min_n,
-                       cudaStream_t st, ProgramStats* stats, bool* zero_pending);
+                       cudaStream_t st, ProgramStats* stats, bool* zero_pending, ZRequest* z = nullptr);
 
 // CPU emulation of a program on a host state (same op interpreter).
 template <typename R>

@@ -251,6 +251,16 @@ class DeviceState:
     def apply_instructions(self, instructions) -> None:
         self.apply_gates(gate_array(instructions))
 
+    def apply_gates_z(self, gates: np.ndarray, z_qubits) -> np.ndarray:
+        """Apply a gate program and return <Z_q> for each q in z_qubits, summed by
+        the program's last fused pass while it stores the state (svb_apply_z)."""
+        gates = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
+        qs = np.ascontiguousarray(z_qubits, dtype=np.int32).reshape(-1)
+        out = np.empty(qs.size, dtype=np.float64)
+        check(lib().svb_apply_z(self.handle, ptr(gates), int(gates.size), ptr(qs, _lib.c_int32), int(qs.size),
+                                ptr(out, _lib.c_double)))
+        return out
+
     # reductions
     def marginal_probs(self, qubits) -> np.ndarray:
         qs = np.ascontiguousarray(sorted(qubits), dtype=np.int32)
@@ -676,8 +686,21 @@ def expectation(c, z_qubits, qubit_cap: int = DEFAULT_QUBIT_CAP) -> float:
 
 
 def expectations(c, z_sets, qubit_cap: int = DEFAULT_QUBIT_CAP) -> np.ndarray:
-    """Many <Z..Z> observables in one pass over the state (extension)."""
+    """Many <Z..Z> observables in one pass over the state (extension).  When
+    the state is not cached yet and every observable is a single-qubit Z, the
+    sums are taken by the program's last fused pass (no extra read pass); the
+    state is cached as by final_state."""
     masks = [_z_mask(c, z) for z in z_sets]
+    if c not in _state_cache and masks and all(m and (m & (m - 1)) == 0 for m in masks):
+        if c.n_qubits > qubit_cap:
+            raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
+        if not terminal_measurement_only(c):
+            raise BackendError("expectation values need a circuit without mid-circuit collapse")
+        state = DeviceState(c.n_qubits, "c128")
+        qs = [m.bit_length() - 1 for m in masks]
+        vals = state.apply_gates_z(gate_array(c.instructions), qs)
+        _state_cache[c] = _Cached(state)
+        return vals
     entry = _cached_state(c, qubit_cap)
     return entry.device.expect_z(masks)
 

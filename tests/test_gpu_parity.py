@@ -440,3 +440,38 @@ def test_permuted_store_and_zero_start_layout(precision):
             s.apply_instructions(body.instructions)
             assert relerr(s.to_numpy(), ref0) < TOL[precision], (body.name, jit)
             s.close()
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_fused_z_sums_match_reduction_pass(precision):
+    """svb_apply_z: <Z_q> summed by the last fused pass == the separate
+    multi-mask reduction == the oracle, for lazy-zero and arbitrary inputs,
+    fused and separate final permutations, JIT and interpreter bodies."""
+    tol = 1e-10 if precision == "c128" else 2e-5
+    cases = [suite.qft_bench_circuit(14), suite.random_circuit(15, 120, np.random.default_rng(4), measured=False),
+             _swap_tail_circuit(14, 1), suite.sycamore_circuit(3, 5, 6, seed=1, measured=False)]
+    for c in cases:
+        n = c.n_qubits
+        qs = list(range(n))
+        ref = orc.unitary_state(c)
+        want = np.array([orc.expectation_from_state(ref, (q,)) for q in qs])
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            got = s.apply_gates_z(sv.gate_array(c.instructions), qs)
+            np.testing.assert_allclose(got, want, atol=tol, err_msg=f"{c.name} jit={jit}")
+            np.testing.assert_allclose(s.expect_z([1 << q for q in qs]), want, atol=tol)
+            # arbitrary input state (not the lazy zero): permutation fused or separate
+            got2 = s.apply_gates_z(sv.gate_array(c.instructions), qs[::-1])
+            ref2 = ref.copy()
+            for inst in c.instructions:
+                orc.apply_instruction(ref2, n, inst)
+            want2 = np.array([orc.expectation_from_state(ref2, (q,)) for q in qs[::-1]])
+            np.testing.assert_allclose(got2, want2, atol=tol, err_msg=f"{c.name} jit={jit} (2nd apply)")
+            s.close()
+    # public API: expectations() of single-qubit Z on an uncached circuit takes the fused path
+    c = suite.qft_bench_circuit(13)
+    z = sv.expectations(c, [(q,) for q in range(13)], qubit_cap=13)
+    ref = orc.unitary_state(c)
+    np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(13)], atol=1e-10)
+    assert relerr(sv.final_state(c, qubit_cap=13), ref) < 1e-10

@@ -7,7 +7,7 @@ rm -f /tmp/jit_pass*.cu
 SVB_JIT_DUMP=/tmp/jit_all.cu python - "$n" "$prec" <<'PY'
 import ctypes, sys
 from paper_2512_04216_b200 import _lib, suite, statevector as sv
-n, prec = int(sys.argv[1]), int(sys.argv[2])
+n, prec = int(sys.argv[1]), int(sys.argv[2], 0)
 import os
 c = suite.sycamore_circuit(4, 8, 20, 0, measured=False) if os.environ.get("SYC") else suite.qft_bench_circuit(n)
 g = sv.gate_array(c.instructions)
