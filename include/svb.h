@@ -90,6 +90,9 @@ int svb_timer_start(svb_handle h);
 int svb_timer_stop(svb_handle h, double* ms);
 int svb_profile(svb_handle h, int enable);
 int svb_profile_read(svb_handle h, double* out);
+/* Per pass index of the programs applied while profiling: out[3*i .. 3*i+2] =
+ * (summed ms, summed HBM bytes moved, launches) for i < min(*n, cap). */
+int svb_profile_passes(svb_handle h, double* out, int cap, int* n);
 
 /* State lifetime: zero_state (statevector.py:125-128). */
 int svb_create(int n_qubits, int precision, int device, svb_handle* out);

@@ -56,6 +56,7 @@ _SIGS = {
     "svb_timer_stop": (c_int, [_h, _dp]),
     "svb_profile": (c_int, [_h, c_int]),
     "svb_profile_read": (c_int, [_h, _dp]),
+    "svb_profile_passes": (c_int, [_h, _dp, c_int, _i32p]),
     "svb_create": (c_int, [c_int, c_int, c_int, POINTER(c_void_p)]),
     "svb_destroy": (c_int, [_h]),
     "svb_set_zero": (c_int, [_h]),

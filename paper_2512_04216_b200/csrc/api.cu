@@ -332,10 +332,9 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
       std::vector<int> seen(h->n, 0);
       for (size_t k = 0; k < z.logical.size(); ++k)
         if (z.logical[k] >= 0) { by_q[z.logical[k]] = vals[k]; seen[z.logical[k]] = 1; }
-      for (int j = 0; j < nz; ++j) {
-        require(seen[z_qubits[j]], SVB_E_CUDA, "fused <Z>: qubit not covered");
-        out[j] = by_q[z_qubits[j]];
-      }
+      // a qubit outside the passes' support (zero_start) is |0> in every
+      // amplitude that is not zero: <Z> = sum p
+      for (int j = 0; j < nz; ++j) out[j] = seen[z_qubits[j]] ? by_q[z_qubits[j]] : vals.back();
     } else {
       materialize(h);
       std::vector<uint64_t> masks(nz);
@@ -358,6 +357,9 @@ int svb_profile(svb_handle h, int enable) {
     h->prof.ms[0] = h->prof.ms[1] = 0;
     h->prof.count[0] = h->prof.count[1] = 0;
     h->prof.bytes[0] = h->prof.bytes[1] = 0;
+    h->prof.idx_ms.clear();
+    h->prof.idx_bytes.clear();
+    h->prof.idx_count.clear();
   });
 }
 
@@ -370,6 +372,21 @@ int svb_profile_read(svb_handle h, double* out) {
     out[3] = h->prof.ms[1];
     out[4] = (double)h->prof.count[1];
     out[5] = h->prof.bytes[1];
+  });
+}
+
+// Per pass index of the applied programs since profiling was enabled:
+// out[3*i + {0,1,2}] = (ms, HBM bytes, launches); returns the count in *n.
+int svb_profile_passes(svb_handle h, double* out, int cap, int* n) {
+  return guard([&] {
+    check_handle(h);
+    const int k = (int)h->prof.idx_ms.size();
+    *n = k;
+    for (int i = 0; i < k && i < cap; ++i) {
+      out[3 * i] = h->prof.idx_ms[i];
+      out[3 * i + 1] = h->prof.idx_bytes[i];
+      out[3 * i + 2] = (double)h->prof.idx_count[i];
+    }
   });
 }
 

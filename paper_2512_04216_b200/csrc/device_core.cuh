@@ -139,7 +139,9 @@ struct PassDev {
   int32_t dpos[16];
   int32_t doutpos[48];
   uint64_t zacc;
-  uint64_t pad3;
+  // zero_start support tracking: positions of the tile with a bit in dmask are
+  // |0...0>-only so far (never written): the loader synthesises zeros there
+  uint64_t dmask;
 };
 static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
@@ -782,6 +784,18 @@ __device__ __forceinline__ void issue_tile(const PassCtx<R, RB>& c, uint64_t bas
     return;
   }
   const cplx<R>* src = c.state + (base | c.ld_tid);
+  if (c.pd.dmask) {
+    for (uint32_t k = 0; k < c.nld; ++k) {
+      cplx<R>* d = dst + (c.sd_tid ^ c.sdk[k]);
+      if ((c.ld_tid | c.ldk[k]) & c.pd.dmask) {
+        d[0] = mk<R>(R(0), R(0));
+        if (kPer == 2) d[1] = mk<R>(R(0), R(0));
+      } else {
+        cp_async16(d, src + c.ldk[k]);
+      }
+    }
+    return;
+  }
   for (uint32_t k = 0; k < c.nld; ++k) cp_async16(dst + (c.sd_tid ^ c.sdk[k]), src + c.ldk[k]);
 }
 
@@ -1196,6 +1210,16 @@ __global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
 // Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM
 // when the op stream fits the per-CTA shared memory budget, else two stages
 // and one CTA per SM.  Returns the dynamic shared memory bytes.
+// HBM bytes a pass moves: every live tile is written; reads skip the
+// never-written positions (dmask) and the lazy |0...0> input (zin).
+#ifndef __CUDACC_RTC__
+template <typename R> inline double pass_hbm_bytes(const PassDev& pd, bool zin) {
+  const double tile = (double)(sizeof(cplx<R>) << pd.m) * (double)(1ull << pd.nout);
+  const double rd = zin ? 0.0 : tile / (double)(1ull << __builtin_popcountll(pd.dmask));
+  return tile + rd;
+}
+#endif
+
 // zsum: the pass accumulates fused <Z> sums (PassDev::zsum): (RB + 1) doubles
 // per thread and 64 per warp.
 template <typename R>

@@ -211,11 +211,13 @@ static PermDev make_perm(int n, const std::vector<int>& dest) {
 }
 
 // --------------------------------------------------------------- profiler
-void Profiler::begin(cudaStream_t st, int kind, double nbytes) {
+void Profiler::begin(cudaStream_t st, int kind, double nbytes, int idx) {
   Rec r;
   SVB_CUDA(cudaEventCreate(&r.a));
   SVB_CUDA(cudaEventCreate(&r.b));
   r.kind = kind;
+  r.idx = idx;
+  r.bytes = nbytes;
   SVB_CUDA(cudaEventRecord(r.a, st));
   pending.push_back(r);
   bytes[kind] += nbytes;
@@ -232,6 +234,16 @@ void Profiler::collect() {
     if (trace) std::fprintf(stderr, "[svb] launch kind=%d %.3f ms (gap %.3f ms)\n", r.kind, t, gap);
     ms[r.kind] += t;
     count[r.kind] += 1;
+    if (r.idx >= 0) {
+      if ((int)idx_ms.size() <= r.idx) {
+        idx_ms.resize(r.idx + 1, 0.0);
+        idx_bytes.resize(r.idx + 1, 0.0);
+        idx_count.resize(r.idx + 1, 0);
+      }
+      idx_ms[r.idx] += t;
+      idx_bytes[r.idx] += r.bytes;
+      idx_count[r.idx] += 1;
+    }
   }
   for (Rec& r : pending) {
     cudaEventDestroy(r.a);
@@ -293,7 +305,7 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
-    if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << n));
+    if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
     k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, pd.zsum), st>>>(
         state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
@@ -509,6 +521,9 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   z_setup(prog);
   const bool zin = zero_pending && *zero_pending && !prog.passes.empty();
   if (prog.passes.empty()) write_zero();
+  const uint64_t full = n == 64 ? ~0ull : (1ull << n) - 1;
+  if (zin && (prog.support & full) != full)  // positions outside the passes' support are never written
+    SVB_CUDA(cudaMemsetAsync(*state, 0, sizeof(cplx<R>) << n, st));
   launch_passes<R>(static_cast<cplx<R>*>(*state), prog.perm_fused ? static_cast<cplx<R>*>(*spare) : nullptr, n,
                    prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
   if (z && z->fused) launch_sum_rows(z->d_acc, (uint64_t)z->logical.size(), kZaccCols, z->d_out, st);

@@ -481,7 +481,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   PrologueCtx pc;
   pc.o = &pro;
   const PassDev& pd0 = prog.passes[p];
-  const bool imm = pd0.m + pd0.nout >= kImmMinQubits;
+  const bool imm = prog.n >= kImmMinQubits;  // (not m + nout: support tracking shrinks nout)
   emit_body<R>(body, prog, p, RB, imm, pc);
   if (nslots) *nslots = pc.nslots;
   if (imm_out) *imm_out = imm;
@@ -503,12 +503,28 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
            "    if (c.zero_input) { svb::issue_tile<R, RB>(c, base, dst); return; }\n"
            "    const svb::cplx<R>* src = c.state + (base | c.ld_tid);\n"
            "    const uint32_t s0 = c.sd_tid;\n";
+    // support tracking (PassDev::dmask): never-written positions load as zeros;
+    // the k part of the offset is known here, the thread part at run time
+    uint64_t tmask = 0;
+    for (int l = 0; l < lo_bits; ++l) tmask |= 1ull << pd0.pos[l];
+    const uint64_t dm_thr = pd0.dmask & tmask;
+    if (dm_thr) iss << "    const bool tdead = (c.ld_tid & " << dm_thr << "ull) != 0;\n";
+    const std::string zero_pair = kPer == 2 ? "; dz[1] = svb::mk<R>(R(0), R(0))" : "";
     for (uint32_t k = 0; k < nld; ++k) {
       const uint32_t j = k * nthr * (uint32_t)kPer;
       uint64_t g = 0;
       for (int l = lo_bits; l < m; ++l)
         if ((j >> l) & 1u) g |= 1ull << pd0.pos[l];
-      iss << "    svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g << "ull);\n";
+      const std::string zero = "{ svb::cplx<R>* dz = dst + (s0 ^ " + std::to_string(swz<R>(j)) +
+                               "u); dz[0] = svb::mk<R>(R(0), R(0))" + zero_pair + "; }";
+      if (g & pd0.dmask) {
+        iss << "    " << zero << "\n";
+      } else if (dm_thr) {
+        iss << "    if (tdead) " << zero << " else svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g
+            << "ull);\n";
+      } else {
+        iss << "    svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g << "ull);\n";
+      }
     }
     iss << "  }\n";
   }
@@ -720,7 +736,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     int zin = (zero_input && p == 0) ? 1 : 0;
     void* args[] = {&s, &so, &pdp, &ob, &nt, &pass, &zin, &stages};
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
-    if (pf) pf->begin(st, 0, (zin ? 1.0 : 2.0) * (double)(sizeof(cplx<R>) << (pd.m + pd.nout)));
+    if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
     if (dr.launch(f, grid, 1, 1, threads, 1, 1, smem, (CUstream)st, args, nullptr) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: kernel launch failed");
     if (pf) pf->end(st);

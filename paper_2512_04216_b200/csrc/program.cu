@@ -420,6 +420,7 @@ template <typename R>
 Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
   Program prog;
   prog.gates = ng;
+  prog.n = n;
   std::vector<int> phys;
   std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, opt.zero_start, phys);
   const int m = std::min(opt.m, n);
@@ -429,6 +430,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
 
   std::vector<int> remaining(ops.size());
   for (size_t i = 0; i < ops.size(); ++i) remaining[i] = (int)i;
+  uint64_t support = 0;  // zero_start: physical qubits written by an earlier pass
 
   while (!remaining.empty()) {
     // ---- choose S and the ops of this pass
@@ -504,8 +506,14 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     for (int q = 0; q < n; ++q)
       if (S & (1ull << q)) { pd.pos[l] = q; local_of[q] = l; ++l; }
     pd.nout = 0;
+    // zero_start: only tiles whose fixed bits lie in the support (qubits some
+    // earlier pass has already written) hold anything but zeros, and they stay
+    // zero through a pass (non-diagonal ops act inside the tile): those tiles
+    // are the whole launch; inside a tile, positions with a bit outside the
+    // support are synthesised as zeros instead of read (PassDev::dmask)
     for (int q = 0; q < n; ++q)
-      if (!(S & (1ull << q))) pd.outpos[pd.nout++] = q;
+      if (!(S & (1ull << q)) && (!opt.zero_start || (support & (1ull << q)))) pd.outpos[pd.nout++] = q;
+    pd.dmask = opt.zero_start && !prog.passes.empty() ? (S & ~support) : 0;
 
     // Rounds are built with op reordering first; if that needs more
     // per-thread prologue slots (register x thread-bit products, see jit.cu)
@@ -625,7 +633,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
       }
       // round 0 without lane register bits: its layout is coalesced in HBM, so
       // a single-stage kernel can load it straight into registers (no ring)
-      pd.direct = (regsets[0] & lane_local) == 0 ? 1 : 0;
+      pd.direct = (regsets[0] & lane_local) == 0 && pd.dmask == 0 ? 1 : 0;
 
       // ---- encode the rounds
       //
@@ -891,8 +899,10 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     skipped = skipped_saved;
     }
     prog.passes.push_back(pd);
+    support |= S;
     remaining = skipped;
   }
+  prog.support = opt.zero_start ? support : ~0ull;
   bool ident = true;
   for (int q = 0; q < n; ++q) ident = ident && phys[q] == q;
   if (!ident) {

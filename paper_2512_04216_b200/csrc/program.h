@@ -23,12 +23,16 @@ namespace svb {
 // Optional per-kernel CUDA-event timing on the launching stream.
 struct Profiler {
   bool on = false;
-  struct Rec { cudaEvent_t a, b; int kind; };  // kind 0 = k_pass, 1 = k_permute
+  struct Rec { cudaEvent_t a, b; int kind, idx; double bytes; };  // kind 0 = k_pass, 1 = k_permute
   std::vector<Rec> pending;
   double ms[2] = {0, 0};
   int64_t count[2] = {0, 0};
   double bytes[2] = {0, 0};
-  void begin(cudaStream_t st, int kind, double nbytes);
+  // per pass index of a program (idx): summed ms, HBM bytes and launches,
+  // so the dominant pass of repeated applies can be reported on its own
+  std::vector<double> idx_ms, idx_bytes;
+  std::vector<int64_t> idx_count;
+  void begin(cudaStream_t st, int kind, double nbytes, int idx = -1);
   void end(cudaStream_t st);
   void collect();  // after a stream sync
 };
@@ -43,8 +47,10 @@ struct Program {
   std::vector<PassDev> passes;
   std::vector<uint8_t> ops;          // op stream (all passes)
   std::vector<int> final_perm;       // physical bit p must move to bit final_perm[p]; empty = identity
-  bool perm_fused = false;           // final_perm is done by the last pass's permuted store (PassDev::perm_out)
+  bool perm_fused = false;
+  uint64_t support = ~0ull;          // zero_start: qubits the passes wrote; positions with other bits are never written           // final_perm is done by the last pass's permuted store (PassDev::perm_out)
   int64_t gates = 0;
+  int n = 0;                         // qubits of the state
 };
 
 struct SchedOptions {

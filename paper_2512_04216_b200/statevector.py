@@ -210,6 +210,14 @@ class DeviceState:
         return {"pass_ms": out[0], "pass_launches": int(out[1]), "pass_bytes": out[2],
                 "perm_ms": out[3], "perm_launches": int(out[4]), "perm_bytes": out[5]}
 
+    def profile_passes(self) -> list:
+        """Per pass index of the profiled programs: dicts of ms, HBM bytes, launches."""
+        out = np.zeros(3 * 64, dtype=np.float64)
+        k = _lib.c_int32()
+        check(lib().svb_profile_passes(self.handle, ptr(out, _lib.c_double), 64, _lib.ctypes.byref(k)))
+        return [{"ms": out[3 * i], "bytes": out[3 * i + 1], "launches": int(out[3 * i + 2])}
+                for i in range(min(k.value, 64))]
+
     # data
     def zero(self) -> "DeviceState":
         check(lib().svb_set_zero(self.handle))

@@ -475,3 +475,42 @@ def test_fused_z_sums_match_reduction_pass(precision):
     ref = orc.unitary_state(c)
     np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(13)], atol=1e-10)
     assert relerr(sv.final_state(c, qubit_cap=13), ref) < 1e-10
+
+
+def _partial_support_circuit(n, seed):
+    """Gates on the low qubits only, plus diagonal-only gates (rz, cz) on some
+    high ones: those qubits stay |0> and the passes never write their half."""
+    rng = np.random.default_rng(seed)
+    c = suite.random_circuit(n - 3, 90, rng, measured=False)
+    full = Circuit(n)
+    for inst in c.instructions:
+        full.gate(inst.kind, *inst.qubits, params=inst.params)
+    full.gate("rz", n - 2, params=(0.3,))
+    full.gate("cz", n - 2, 0)
+    return full
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_zero_start_support_tracking(precision):
+    """Lazy |0...0> programs only launch the tiles inside the support (qubits
+    already written) and synthesise never-written positions as zeros; circuits
+    that leave qubits untouched zero-fill first.  Amplitudes and fused <Z>
+    against the oracle, JIT and interpreter bodies."""
+    tol = TOL[precision]
+    for c in (suite.qft_bench_circuit(15), _partial_support_circuit(15, 2), _partial_support_circuit(14, 5),
+              suite.sycamore_circuit(3, 5, 4, seed=4, measured=False)):
+        n = c.n_qubits
+        ref = orc.unitary_state(c)
+        want = np.array([orc.expectation_from_state(ref, (q,)) for q in range(n)])
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            s.apply_instructions(c.instructions)
+            assert relerr(s.to_numpy(), ref) < tol, (c.name, jit)
+            s.close()
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            z = s.apply_gates_z(sv.gate_array(c.instructions), list(range(n)))
+            np.testing.assert_allclose(z, want, atol=10 * tol, err_msg=f"{c.name} jit={jit}")
+            assert relerr(s.to_numpy(), ref) < tol, (c.name, jit)
+            s.close()
