@@ -308,11 +308,13 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
     for (int j = 0; j < nz; ++j) require(z_qubits[j] >= 0 && z_qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
-    ensure_ws(h, (size_t)kZaccRows * kZaccCols + kZaccRows + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
+    const size_t zacc = zacc_doubles(kPassThreads<float> > kPassThreads<double> ? kPassThreads<float>
+                                                                                 : kPassThreads<double>, kRegBits<double>);
+    ensure_ws(h, zacc + kZaccRows + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
     ZRequest z;
     z.want = nz > 0;
     z.d_acc = h->d_ws;
-    z.d_out = h->d_ws + (size_t)kZaccRows * kZaccCols;
+    z.d_out = h->d_ws + zacc;
     if (h->prec == SVB_C128)
       run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats,
                                 &h->zero_pending, &z);

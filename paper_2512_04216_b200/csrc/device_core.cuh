@@ -130,9 +130,9 @@ struct PassDev {
   // physical bit p; dpos[l] = dest(pos[l]), doutpos[i] = dest(outpos[i])
   int32_t perm_out;
   // fused <Z_q> sums (last pass of an apply that asked for single-qubit <Z>):
-  // per-CTA partials of sum p (-1)^bit for every register bit of the last
-  // round, every thread bit and every tile bit, plus sum p, are written to
-  // zacc[k * kZaccCols + blockIdx.x] (see zsum_tile / zsum_finish)
+  // sums of p (-1)^bit for every register bit of the last round, every
+  // thread bit and every tile bit, plus sum p, accumulate in zacc (see
+  // zsum_tile; reduced by k_zsum_finish)
   int32_t zsum;
   int32_t pad2;
   uint16_t items[kMaxItems];
@@ -145,7 +145,11 @@ struct PassDev {
 };
 static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
-constexpr int kZaccRows = 64, kZaccCols = 1024;  // fused <Z> partials: values x CTAs (grid <= kZaccCols)
+constexpr int kZaccRows = 64, kZaccCols = 1024;  // fused <Z>: values, CTAs (grid <= kZaccCols)
+// fused <Z> accumulators (doubles) for up to kZaccCols CTAs of nthr threads
+__host__ __device__ constexpr uint64_t zacc_doubles(uint32_t nthr, int rb) {
+  return (uint64_t)kZaccCols * ((uint64_t)(rb + 1) * nthr + (nthr >> 5) * 64u);
+}
 
 // ------------------------------------------------------------ interpreter
 #define SVB_HD __host__ __device__ __forceinline__
@@ -744,8 +748,6 @@ template <typename R, int RB> struct PassCtx {
   const PassDev& pd;
   cplx<R>* state;
   cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
-  double* zs;            // fused <Z>: per-thread sums [RB + 1][nthr] (shared memory)
-  double* zw;            // fused <Z>: per-warp tile-bit sums [nwarps][64] (shared memory)
   uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
   const uint8_t* ops;  // op stream rebased onto shared memory
   const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
@@ -899,59 +901,39 @@ __device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg
 }
 
 // Fused <Z_q> of the last round (pd.zsum): p_v = |a_v|^2 of the thread's 2^RB
-// amplitudes; the thread adds T = sum p and W_i = sum p (-1)^(v_i) to its
-// shared-memory slots; the warp adds +-(warp sum of T) to the slot of every
-// tile bit (lane j owns tile bits j and j + 32).  Thread-bit signs are applied
-// once at the end (zsum_finish), since a thread's fixed bits never change.
+// amplitudes; the thread adds T = sum p and W_i = sum p (-1)^(v_i) to its own
+// accumulators in global memory (fire-and-forget RED.ADD.F64: no shared
+// memory, no latency on the pass), and the warp adds +-(warp sum of T) for
+// every tile bit (lane j owns tile bits j and j + 32).  Thread-bit signs and
+// the sums over CTAs are applied afterwards (k_zsum_finish, fused.cu).
+// Layout (doubles): per thread [cta][RB + 1][nthr], then per warp [cta][nwarps][64].
 template <typename R, int RB>
 __device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>* a, uint64_t base) {
-  double p[1 << RB];
+  double T = 0.0, s1[RB];
 #pragma unroll
-  for (int v = 0; v < (1 << RB); ++v) p[v] = (double)a[v].x * (double)a[v].x + (double)a[v].y * (double)a[v].y;
-  double T = 0.0;
+  for (int i = 0; i < RB; ++i) s1[i] = 0.0;
 #pragma unroll
-  for (int v = 0; v < (1 << RB); ++v) T += p[v];
-  const uint32_t nthr = c.nthr, tid = c.tid;
-  c.zs[tid] += T;
+  for (int v = 0; v < (1 << RB); ++v) {  // running sums: no array of p_v
+    const double pv = (double)a[v].x * (double)a[v].x + (double)a[v].y * (double)a[v].y;
+    T += pv;
 #pragma unroll
-  for (int i = 0; i < RB; ++i) {
-    double s1 = 0.0;
-#pragma unroll
-    for (int v = 0; v < (1 << RB); ++v)
-      if (v & (1 << i)) s1 += p[v];
-    c.zs[(1 + i) * nthr + tid] += fma(-2.0, s1, T);
+    for (int i = 0; i < RB; ++i)
+      if (v & (1 << i)) s1[i] += pv;
   }
+  const uint32_t nthr = c.nthr, tid = c.tid;
+  // accumulator addresses from the staged PassDev (no long-lived registers)
+  double* zs = reinterpret_cast<double*>(c.pd.zacc) + (size_t)blockIdx.x * (RB + 1) * nthr;
+  double* zw = reinterpret_cast<double*>(c.pd.zacc) + (size_t)kZaccCols * (RB + 1) * nthr +
+               ((size_t)blockIdx.x * (nthr >> 5) + (tid >> 5)) * 64;
+  atomicAdd(zs + tid, T);
+#pragma unroll
+  for (int i = 0; i < RB; ++i) atomicAdd(zs + (1 + i) * nthr + tid, fma(-2.0, s1[i], T));
   double tw = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
-  const uint32_t lane = tid & 31u, w = tid >> 5;
-  double* zw = c.zw + w * 64;
-  if ((int)lane < c.pd.nout) zw[lane] += ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw;
-  if ((int)lane + 32 < c.pd.nout) zw[lane + 32] += ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw;
-}
-
-// After the tile loop (all threads, after a barrier): CTA partials
-// [W_0..W_{RB-1} | thread bits 0..nt-1 | tile bits 0..nout-1 | sum p].
-template <typename R, int RB>
-__device__ __forceinline__ void zsum_finish(const PassCtx<R, RB>& c) {
-  const PassDev& pd = c.pd;
-  const int nt = pd.m - pd.rb, nw = (int)(c.nthr >> 5);
-  const int nv = RB + nt + pd.nout + 1;
-  const int k = (int)c.tid;
-  if (k >= nv) return;
-  double acc = 0.0;
-  if (k < RB) {
-    for (uint32_t t = 0; t < c.nthr; ++t) acc += c.zs[(1 + k) * c.nthr + t];
-  } else if (k < RB + nt) {
-    const int b = k - RB;
-    for (uint32_t t = 0; t < c.nthr; ++t) acc += ((t >> b) & 1u) ? -c.zs[t] : c.zs[t];
-  } else if (k < RB + nt + pd.nout) {
-    const int j = k - RB - nt;
-    for (int w = 0; w < nw; ++w) acc += c.zw[w * 64 + j];
-  } else {
-    for (uint32_t t = 0; t < c.nthr; ++t) acc += c.zs[t];
-  }
-  reinterpret_cast<double*>(pd.zacc)[(size_t)k * kZaccCols + blockIdx.x] = acc;
+  const uint32_t lane = tid & 31u;
+  if ((int)lane < c.pd.nout) atomicAdd(zw + lane, ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw);
+  if ((int)lane + 32 < c.pd.nout) atomicAdd(zw + lane + 32, ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw);
 }
 
 // Helpers for JIT-generated diagonal code.
@@ -1110,11 +1092,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // are written while slow warps may still read this tile's)
   c.pro = uni + 2 * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
-  c.zs = reinterpret_cast<double*>(c.pro + (size_t)nslots * blockDim.x);
-  c.zw = c.zs + (size_t)(RB + 1) * blockDim.x;
-  if (pd.zsum) {
-    for (uint32_t i = threadIdx.x; i < (RB + 1) * blockDim.x + (blockDim.x >> 5) * 64; i += blockDim.x) c.zs[i] = 0.0;
-  }
+  (void)nslots;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
@@ -1194,10 +1172,6 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages > 1) __syncthreads();
   }
   cp_async_wait<0>();
-  if (pd.zsum) {
-    __syncthreads();
-    zsum_finish<R, RB>(c);
-  }
 }
 
 template <typename R, int RB>
@@ -1220,15 +1194,13 @@ template <typename R> inline double pass_hbm_bytes(const PassDev& pd, bool zin) 
 }
 #endif
 
-// zsum: the pass accumulates fused <Z> sums (PassDev::zsum): (RB + 1) doubles
-// per thread and 64 per warp.
 template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
                                               int zsum = 0) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
   return (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
          (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
-         (zsum ? ((uint32_t)(kRegBits<R> + 1) * nthr + (nthr >> 5) * 64u) * 8u : 0u);
+         0u * (uint32_t)zsum;  // fused <Z> accumulates in global memory (zsum_tile)
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;

@@ -252,12 +252,44 @@ void Profiler::collect() {
   pending.clear();
 }
 
+// ------------------------------------------------------- fused <Z> finish
+// One block per value k of the last pass's zsum accumulators (zsum_tile):
+// register bits (W_i), thread bits (signed per-thread T), tile bits (per-warp
+// sums) and the total; sums over every CTA slot (unused ones are zero).
+__global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ zacc, uint32_t nthr, int rb, int nt,
+                                                     int nout, double* __restrict__ out) {
+  __shared__ double sh[256];
+  const int k = blockIdx.x;
+  const uint32_t nw = nthr >> 5;
+  const double* zw = zacc + (uint64_t)kZaccCols * (rb + 1) * nthr;
+  double acc = 0.0;
+  if (k < rb + nt || k == rb + nt + nout) {
+    const int row = k < rb ? 1 + k : 0;
+    const int b = k - rb;
+    for (uint64_t i = threadIdx.x; i < (uint64_t)kZaccCols * nthr; i += blockDim.x) {
+      const uint64_t cta = i / nthr, t = i % nthr;
+      const double v = zacc[(cta * (rb + 1) + row) * nthr + t];
+      acc += (k >= rb && k < rb + nt && ((t >> b) & 1u)) ? -v : v;
+    }
+  } else {
+    const int j = k - rb - nt;
+    for (uint64_t i = threadIdx.x; i < (uint64_t)kZaccCols * nw; i += blockDim.x) acc += zw[i * 64 + j];
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[k] = sh[0];
+}
+
 // ------------------------------------------------------------ run_program
 template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
 // out: destination of the last pass when the program's final permutation is
 // fused into it (prog.perm_fused; a second state-sized buffer), else unused.
-// zacc: fused <Z> scratch (kZaccRows x kZaccCols doubles) when the last pass has zsum.
+// zacc: fused <Z> accumulators (zacc_doubles) when the last pass has zsum.
 template <typename R>
 static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& prog, cudaStream_t st,
                           ProgramStats* stats, bool use_jit, bool zero_input, double* zacc = nullptr) {
@@ -276,7 +308,8 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     if (zacc == nullptr) throw Error(SVB_E_CUDA, "fused <Z> without a scratch buffer");
     const uint64_t zp = (uint64_t)(uintptr_t)zacc;
     PassDev* last = reinterpret_cast<PassDev*>(dbuf) + (prog.passes.size() - 1);
-    SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * kZaccRows * kZaccCols, st));
+    const PassDev& lp = prog.passes.back();
+    SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * zacc_doubles(1u << (lp.m - lp.rb), lp.rb), st));
     SVB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp,
                              cudaMemcpyHostToDevice, st));
   }
@@ -526,7 +559,12 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     SVB_CUDA(cudaMemsetAsync(*state, 0, sizeof(cplx<R>) << n, st));
   launch_passes<R>(static_cast<cplx<R>*>(*state), prog.perm_fused ? static_cast<cplx<R>*>(*spare) : nullptr, n,
                    prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
-  if (z && z->fused) launch_sum_rows(z->d_acc, (uint64_t)z->logical.size(), kZaccCols, z->d_out, st);
+  if (z && z->fused) {
+    const PassDev& lp = prog.passes.back();
+    k_zsum_finish<<<(unsigned)z->logical.size(), 256, 0, st>>>(z->d_acc, 1u << (lp.m - lp.rb), lp.rb, lp.m - lp.rb,
+                                                                lp.nout, z->d_out);
+    SVB_CHECK_LAUNCH();
+  }
   if (zin) *zero_pending = false;
   const double t_launch = tt.lap();
   if (prog.perm_fused) {

@@ -903,6 +903,9 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
     remaining = skipped;
   }
   prog.support = opt.zero_start ? support : ~0ull;
+  if (opt.zero_start && std::getenv("SVB_TRACE"))
+    std::fprintf(stderr, "[svb] zero-start support %llx over %zu passes\n", (unsigned long long)support,
+                 prog.passes.size());
   bool ident = true;
   for (int q = 0; q < n; ++q) ident = ident && phys[q] == q;
   if (!ident) {

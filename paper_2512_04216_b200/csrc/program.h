@@ -88,7 +88,7 @@ void run_permutation(void** state, void** spare, int n, const std::vector<int>& 
 struct ZRequest {
   bool want = false;
   double* d_out = nullptr;
-  double* d_acc = nullptr;  // kZaccRows x kZaccCols scratch (device)
+  double* d_acc = nullptr;  // zacc_doubles() accumulators (device)
   bool fused = false;
   std::vector<int> logical;
 };
