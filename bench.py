@@ -223,8 +223,10 @@ def run_ours(args, rank: int, world: int, dist):
     state.profile(True)
     with ClockSampler(device) as clk:
         state.timer_start()
+        w0 = time.perf_counter()
         for _ in range(args.steps):
-            z = step()
+            z = step()  # synchronous: each apply ends with a stream sync
+        wall_ms = (time.perf_counter() - w0) * 1e3
         total_ms = state.timer_stop()
     prof = state.profile_read()
     barrier()
@@ -305,7 +307,8 @@ def run_ours(args, rank: int, world: int, dist):
         "data": "synthetic (deterministic QFT circuit; state 16 GiB >> 126 MB L2, no flush needed)",
         "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": n_gates,
                    "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2",
-                   "hbm_passes_per_step": stats["passes"], "plan": plan},
+                   "hbm_passes_per_step": stats["passes"], "plan": plan,
+                   "wall_ms_per_step": wall_ms / args.steps},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": measured_traffic(),
                      "kernel": f"svb_jit (fused pass {top} of {len(per_pass)}, c128)",

@@ -310,7 +310,7 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
     h->stats.prof = &h->prof;
     const size_t zacc = zacc_doubles(kPassThreads<float> > kPassThreads<double> ? kPassThreads<float>
                                                                                  : kPassThreads<double>, kRegBits<double>);
-    ensure_ws(h, zacc + kZaccRows + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
+    ensure_ws(h, zacc + kZaccRows + (size_t)kZaccRows * 32 + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
     ZRequest z;
     z.want = nz > 0;
     z.d_acc = h->d_ws;
@@ -342,7 +342,7 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
       std::vector<uint64_t> masks(nz);
       for (int j = 0; j < nz; ++j) masks[j] = 1ull << z_qubits[j];
       double* d_out = z.d_out;
-      double* d_ws = z.d_out + kZaccRows;
+      double* d_ws = z.d_out + kZaccRows + (size_t)kZaccRows * 32;
       if (h->prec == SVB_C128) launch_expect_z<double>(h->amps, h->n, masks.data(), nz, d_out, d_ws, h->st);
       else launch_expect_z<float>(h->amps, h->n, masks.data(), nz, d_out, d_ws, h->st);
       SVB_CUDA(cudaMemcpyAsync(out, d_out, nz * sizeof(double), cudaMemcpyDeviceToHost, h->st));

@@ -749,6 +749,7 @@ template <typename R, int RB> struct PassCtx {
   cplx<R>* state;
   cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
   uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
+  double* zl;            // fused <Z>: the thread's running sums [RB + 3] (zsum_tile)
   const uint8_t* ops;  // op stream rebased onto shared memory
   const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
   uint32_t tid;
@@ -901,12 +902,13 @@ __device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg
 }
 
 // Fused <Z_q> of the last round (pd.zsum): p_v = |a_v|^2 of the thread's 2^RB
-// amplitudes; the thread adds T = sum p and W_i = sum p (-1)^(v_i) to its own
-// accumulators in global memory (fire-and-forget RED.ADD.F64: no shared
-// memory, no latency on the pass), and the warp adds +-(warp sum of T) for
-// every tile bit (lane j owns tile bits j and j + 32).  Thread-bit signs and
-// the sums over CTAs are applied afterwards (k_zsum_finish, fused.cu).
-// Layout (doubles): per thread [cta][RB + 1][nthr], then per warp [cta][nwarps][64].
+// amplitudes; the thread adds T = sum p and W_i = sum p (-1)^(v_i) to its
+// running sums, and lane j adds +-(warp sum of T) for tile bits j and j + 32.
+// The running sums are thread-local (c.zl: local memory if the registers run
+// out -- no shared memory, no atomics); zsum_store writes them once per thread
+// at the end, and k_zsum_finish (fused.cu) applies the thread-bit signs and
+// sums over the CTAs.
+// Global layout (doubles): per thread [cta][RB + 1][nthr], then per warp [cta][nwarps][64].
 template <typename R, int RB>
 __device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>* a, uint64_t base) {
   double T = 0.0, s1[RB];
@@ -920,20 +922,28 @@ __device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>
     for (int i = 0; i < RB; ++i)
       if (v & (1 << i)) s1[i] += pv;
   }
-  const uint32_t nthr = c.nthr, tid = c.tid;
-  // accumulator addresses from the staged PassDev (no long-lived registers)
-  double* zs = reinterpret_cast<double*>(c.pd.zacc) + (size_t)blockIdx.x * (RB + 1) * nthr;
-  double* zw = reinterpret_cast<double*>(c.pd.zacc) + (size_t)kZaccCols * (RB + 1) * nthr +
-               ((size_t)blockIdx.x * (nthr >> 5) + (tid >> 5)) * 64;
-  atomicAdd(zs + tid, T);
+  double* zl = c.zl;
+  zl[0] += T;
 #pragma unroll
-  for (int i = 0; i < RB; ++i) atomicAdd(zs + (1 + i) * nthr + tid, fma(-2.0, s1[i], T));
+  for (int i = 0; i < RB; ++i) zl[1 + i] += fma(-2.0, s1[i], T);
   double tw = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
-  const uint32_t lane = tid & 31u;
-  if ((int)lane < c.pd.nout) atomicAdd(zw + lane, ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw);
-  if ((int)lane + 32 < c.pd.nout) atomicAdd(zw + lane + 32, ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw);
+  const uint32_t lane = c.tid & 31u;
+  if ((int)lane < c.pd.nout) zl[RB + 1] += ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw;
+  if ((int)lane + 32 < c.pd.nout) zl[RB + 2] += ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw;
+}
+
+template <typename R, int RB>
+__device__ __forceinline__ void zsum_store(const PassCtx<R, RB>& c) {
+  const uint32_t nthr = c.nthr, tid = c.tid, lane = tid & 31u;
+  double* zs = reinterpret_cast<double*>(c.pd.zacc) + (size_t)blockIdx.x * (RB + 1) * nthr;
+  double* zw = reinterpret_cast<double*>(c.pd.zacc) + (size_t)kZaccCols * (RB + 1) * nthr +
+               ((size_t)blockIdx.x * (nthr >> 5) + (tid >> 5)) * 64;
+#pragma unroll
+  for (int i = 0; i <= RB; ++i) zs[i * nthr + tid] = c.zl[i];
+  zw[lane] = c.zl[RB + 1];
+  zw[lane + 32] = c.zl[RB + 2];
 }
 
 // Helpers for JIT-generated diagonal code.
@@ -1093,6 +1103,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.pro = uni + 2 * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   (void)nslots;
+  double zl[RB + 3];
+#pragma unroll
+  for (int i = 0; i < RB + 3; ++i) zl[i] = 0.0;
+  c.zl = zl;
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
@@ -1172,6 +1186,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages > 1) __syncthreads();
   }
   cp_async_wait<0>();
+  if (pd.zsum) zsum_store<R, RB>(c);
 }
 
 template <typename R, int RB>

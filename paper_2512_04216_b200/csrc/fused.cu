@@ -253,27 +253,31 @@ void Profiler::collect() {
 }
 
 // ------------------------------------------------------- fused <Z> finish
-// One block per value k of the last pass's zsum accumulators (zsum_tile):
-// register bits (W_i), thread bits (signed per-thread T), tile bits (per-warp
-// sums) and the total; sums over every CTA slot (unused ones are zero).
-__global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ zacc, uint32_t nthr, int rb, int nt,
-                                                     int nout, double* __restrict__ out) {
+// Block (k, slice) sums value k of the last pass's <Z> slots (zsum_store) over
+// a slice of the `ncta` CTAs: register bits (W_i), thread bits (per-thread T
+// with the sign of thread bit b), tile bits (per-warp lane sums), the total.
+// partial[k * kZsumSlices + slice]; k_sum_rows finishes.
+constexpr int kZsumSlices = 32;
+__global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ zacc, uint32_t ncta, uint32_t nthr,
+                                                     int rb, int nt, int nout, double* __restrict__ partial) {
   __shared__ double sh[256];
   const int k = blockIdx.x;
   const uint32_t nw = nthr >> 5;
+  const uint32_t c0 = (uint32_t)(((uint64_t)ncta * blockIdx.y) / kZsumSlices);
+  const uint32_t c1 = (uint32_t)(((uint64_t)ncta * (blockIdx.y + 1)) / kZsumSlices);
   const double* zw = zacc + (uint64_t)kZaccCols * (rb + 1) * nthr;
   double acc = 0.0;
   if (k < rb + nt || k == rb + nt + nout) {
     const int row = k < rb ? 1 + k : 0;
     const int b = k - rb;
-    for (uint64_t i = threadIdx.x; i < (uint64_t)kZaccCols * nthr; i += blockDim.x) {
+    for (uint64_t i = (uint64_t)c0 * nthr + threadIdx.x; i < (uint64_t)c1 * nthr; i += blockDim.x) {
       const uint64_t cta = i / nthr, t = i % nthr;
       const double v = zacc[(cta * (rb + 1) + row) * nthr + t];
       acc += (k >= rb && k < rb + nt && ((t >> b) & 1u)) ? -v : v;
     }
   } else {
     const int j = k - rb - nt;
-    for (uint64_t i = threadIdx.x; i < (uint64_t)kZaccCols * nw; i += blockDim.x) acc += zw[i * 64 + j];
+    for (uint64_t i = (uint64_t)c0 * nw + threadIdx.x; i < (uint64_t)c1 * nw; i += blockDim.x) acc += zw[i * 64 + j];
   }
   sh[threadIdx.x] = acc;
   __syncthreads();
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ 
     if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) out[k] = sh[0];
+  if (threadIdx.x == 0) partial[(uint64_t)k * kZsumSlices + blockIdx.y] = sh[0];
 }
 
 // ------------------------------------------------------------ run_program
@@ -308,6 +312,8 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     if (zacc == nullptr) throw Error(SVB_E_CUDA, "fused <Z> without a scratch buffer");
     const uint64_t zp = (uint64_t)(uintptr_t)zacc;
     PassDev* last = reinterpret_cast<PassDev*>(dbuf) + (prog.passes.size() - 1);
+    // zsum_store writes every slot of a launched CTA; cleared so that the finish
+    // kernel may sum over an upper bound of the grid
     const PassDev& lp = prog.passes.back();
     SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * zacc_doubles(1u << (lp.m - lp.rb), lp.rb), st));
     SVB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp,
@@ -561,9 +567,17 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
                    prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
   if (z && z->fused) {
     const PassDev& lp = prog.passes.back();
-    k_zsum_finish<<<(unsigned)z->logical.size(), 256, 0, st>>>(z->d_acc, 1u << (lp.m - lp.rb), lp.rb, lp.m - lp.rb,
-                                                                lp.nout, z->d_out);
+    // CTAs of the last pass (the launch shapes of launch_passes / jit_launch_passes)
+    int dev = 0, nsm = 148;
+    SVB_CUDA(cudaGetDevice(&dev));
+    SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t ncta = std::min<uint64_t>(1ull << lp.nout, (uint64_t)nsm * kPassMinBlocks<R>);
+    const unsigned nv = (unsigned)z->logical.size();
+    double* partial = z->d_out + kZaccRows;
+    k_zsum_finish<<<dim3(nv, kZsumSlices), 256, 0, st>>>(z->d_acc, (uint32_t)ncta, 1u << (lp.m - lp.rb), lp.rb,
+                                                          lp.m - lp.rb, lp.nout, partial);
     SVB_CHECK_LAUNCH();
+    launch_sum_rows(partial, nv, kZsumSlices, z->d_out, st);
   }
   if (zin) *zero_pending = false;
   const double t_launch = tt.lap();

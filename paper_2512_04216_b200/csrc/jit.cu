@@ -341,7 +341,15 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       o << "      } else {\n";
       for (int v = 0; v < (1 << RB); ++v) o << "        a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
       o << "      }\n    } else {\n";
-      for (int v = 0; v < (1 << RB); ++v) o << "      a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+      if (pd.dmask) {  // never-written positions (support tracking) are zeros, not loaded
+        o << "      const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
+        for (int v = 0; v < (1 << RB); ++v) {
+          if (G[v] & pd.dmask) o << "      a[" << v << "] = svb::mk<R>(R(0), R(0));\n";
+          else o << "      a[" << v << "] = tdead0 ? svb::mk<R>(R(0), R(0)) : cur[sFl ^ " << K[v] << "u];\n";
+        }
+      } else {
+        for (int v = 0; v < (1 << RB); ++v) o << "      a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
+      }
       o << "    }\n";
     } else {
       for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
@@ -509,19 +517,18 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
     for (int l = 0; l < lo_bits; ++l) tmask |= 1ull << pd0.pos[l];
     const uint64_t dm_thr = pd0.dmask & tmask;
     if (dm_thr) iss << "    const bool tdead = (c.ld_tid & " << dm_thr << "ull) != 0;\n";
-    const std::string zero_pair = kPer == 2 ? "; dz[1] = svb::mk<R>(R(0), R(0))" : "";
     for (uint32_t k = 0; k < nld; ++k) {
       const uint32_t j = k * nthr * (uint32_t)kPer;
       uint64_t g = 0;
       for (int l = lo_bits; l < m; ++l)
         if ((j >> l) & 1u) g |= 1ull << pd0.pos[l];
-      const std::string zero = "{ svb::cplx<R>* dz = dst + (s0 ^ " + std::to_string(swz<R>(j)) +
-                               "u); dz[0] = svb::mk<R>(R(0), R(0))" + zero_pair + "; }";
+      // never-written positions are not stored at all: round 0 of a pass with a
+      // dmask takes them as constant zeros (emit_body), later rounds read what
+      // round 0 wrote
       if (g & pd0.dmask) {
-        iss << "    " << zero << "\n";
+        continue;
       } else if (dm_thr) {
-        iss << "    if (tdead) " << zero << " else svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g
-            << "ull);\n";
+        iss << "    if (!tdead) svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g << "ull);\n";
       } else {
         iss << "    svb::cp_async16(dst + (s0 ^ " << swz<R>(j) << "u), src + " << g << "ull);\n";
       }

@@ -316,7 +316,8 @@ def test_calibration_host_logic():
         _sys.path.remove(ref_src)
 
 
-@pytest.mark.parametrize("which", ["qft30_c128", "qft20_c128", "qft12_permstore", "syc_c64", "random_c64"])
+@pytest.mark.parametrize("which", ["qft30_c128", "qft20_c128", "qft12_permstore", "syc_c64", "random_c64",
+                                   "qft30_zero_start_z", "syc_c64_zero_start"])
 def test_jit_sources_compile(which):
     """NVRTC compiles every generated pass kernel (a failure would otherwise
     fall back to the interpreter body at run time)."""
@@ -328,6 +329,10 @@ def test_jit_sources_compile(which):
         n, prec, c = 20, 1, suite.qft_bench_circuit(20)
     elif which == "qft12_permstore":  # last pass stores to the bit-reversed addresses
         n, prec, c = 12, 1, suite.qft_bench_circuit(12)
+    elif which == "qft30_zero_start_z":  # support tracking (dmask loads) + fused <Z> on the last pass
+        n, prec, c = 30, 0x301, suite.qft_bench_circuit(30)
+    elif which == "syc_c64_zero_start":
+        n, prec, c = 28, 0x100, suite.sycamore_circuit(4, 7, 12, seed=0, measured=False)
     elif which == "syc_c64":
         n, prec, c = 28, 0, suite.sycamore_circuit(4, 7, 12, seed=0, measured=False)
     else:
