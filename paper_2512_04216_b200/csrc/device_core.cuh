@@ -648,6 +648,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* g) {
+  asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(g));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
@@ -766,6 +769,7 @@ template <typename R, int RB> struct PassCtx {
   uint32_t sd_tid, nld;
   int prefetch, zero_input;
   int direct;  // round 0 loads straight from HBM into registers (no ring)
+  int l2next;  // direct: the next tile exists (next_base); round 0 prefetches its live data into L2
   __device__ PassCtx(const PassDev& p) : pd(p) {}
 };
 
@@ -897,6 +901,7 @@ __device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg
     for (int i = 0; i < RB; ++i)
       if (v & (1 << i)) g |= goff[i];
     if (c.zero_input) a[v] = mk<R>((Fg | g) == 0 ? R(1) : R(0), R(0));
+    else if ((Fg | g) & c.pd.dmask) a[v] = mk<R>(R(0), R(0));  // never written (support tracking)
     else a[v] = __ldcs(c.state + (Fg | g));
   }
 }
@@ -1137,6 +1142,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.prefetch = 0;
   c.next_base = 0;
   c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
+  c.l2next = 0;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PassCtx<R, RB>::kHoist; ++k) {
@@ -1178,6 +1184,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages == 1) {
       c.prefetch = tn < ntiles;
       if (c.prefetch) c.next_base = tile_base_warp(pd, tn, lane);
+    } else if (stages == 0) {
+      c.l2next = tn < ntiles;
+      if (c.l2next) c.next_base = tile_base_warp(pd, tn, lane);
     }
     Body::template tile<R, RB>(pass, c, a, ring + (size_t)(stages > 1 ? (it & 1) : 0) * T, base, bs);
     // two stages: the ring slot is rewritten by the next iteration's issue.

@@ -339,7 +339,20 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       for (int v = 0; v < (1 << RB); ++v)
         o << "        a[" << v << "] = svb::mk<R>((Fg | " << G[v] << "ull) == 0 ? R(1) : R(0), R(0));\n";
       o << "      } else {\n";
-      for (int v = 0; v < (1 << RB); ++v) o << "        a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
+      if (pd.dmask) {  // support tracking: only written positions are read; the next tile's go to L2
+        o << "        const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
+        for (int v = 0; v < (1 << RB); ++v) {
+          if (G[v] & pd.dmask) o << "        a[" << v << "] = svb::mk<R>(R(0), R(0));\n";
+          else o << "        a[" << v << "] = tdead0 ? svb::mk<R>(R(0), R(0)) : __ldcs(g0 + " << G[v] << "ull);\n";
+        }
+        o << "        if (c.l2next && !tdead0) {\n"
+             "          const svb::cplx<R>* gn = c.state + ((Fg & ~base) | c.next_base);\n";
+        for (int v = 0; v < (1 << RB); ++v)
+          if (!(G[v] & pd.dmask)) o << "          svb::prefetch_l2(gn + " << G[v] << "ull);\n";
+        o << "        }\n";
+      } else {
+        for (int v = 0; v < (1 << RB); ++v) o << "        a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
+      }
       o << "      }\n    } else {\n";
       if (pd.dmask) {  // never-written positions (support tracking) are zeros, not loaded
         o << "      const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
@@ -721,7 +734,9 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
     int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p], pd.zsum);
-    if (stages == 1 && pd.direct && std::getenv("SVB_DIRECT")) stages = 0;  // measured slower (load latency exposed)
+    // direct first round: for support-tracked passes (few live loads per tile,
+    // no ring barrier); for full passes only on request (load latency exposed)
+    if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum);

@@ -633,7 +633,7 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
       }
       // round 0 without lane register bits: its layout is coalesced in HBM, so
       // a single-stage kernel can load it straight into registers (no ring)
-      pd.direct = (regsets[0] & lane_local) == 0 && pd.dmask == 0 ? 1 : 0;
+      pd.direct = (regsets[0] & lane_local) == 0 ? 1 : 0;
 
       // ---- encode the rounds
       //
