@@ -354,7 +354,7 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
 
 int svb_profile(svb_handle h, int enable) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);  // timing/profiling never materialises a lazy |0...0>
     h->prof.on = enable != 0;
     h->prof.ms[0] = h->prof.ms[1] = 0;
     h->prof.count[0] = h->prof.count[1] = 0;
@@ -367,7 +367,7 @@ int svb_profile(svb_handle h, int enable) {
 
 int svb_profile_read(svb_handle h, double* out) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);  // timing/profiling never materialises a lazy |0...0>
     out[0] = h->prof.ms[0];
     out[1] = (double)h->prof.count[0];
     out[2] = h->prof.bytes[0];
@@ -381,7 +381,7 @@ int svb_profile_read(svb_handle h, double* out) {
 // out[3*i + {0,1,2}] = (ms, HBM bytes, launches); returns the count in *n.
 int svb_profile_passes(svb_handle h, double* out, int cap, int* n) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);  // timing/profiling never materialises a lazy |0...0>
     const int k = (int)h->prof.idx_ms.size();
     *n = k;
     for (int i = 0; i < k && i < cap; ++i) {
@@ -394,7 +394,7 @@ int svb_profile_passes(svb_handle h, double* out, int cap, int* n) {
 
 int svb_timer_start(svb_handle h) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);  // timing/profiling never materialises a lazy |0...0>
     if (!h->t0) {
       SVB_CUDA(cudaEventCreate(&h->t0));
       SVB_CUDA(cudaEventCreate(&h->t1));
@@ -405,7 +405,7 @@ int svb_timer_start(svb_handle h) {
 
 int svb_timer_stop(svb_handle h, double* ms) {
   return guard([&] {
-    check_handle(h);
+    check_handle_nomat(h);  // timing/profiling never materialises a lazy |0...0>
     require(h->t0 != nullptr, SVB_E_ARG, "timer not started");
     SVB_CUDA(cudaEventRecord(h->t1, h->st));
     SVB_CUDA(cudaEventSynchronize(h->t1));

@@ -737,6 +737,12 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
+    // one-round direct pass, warp-independent (no ring, no CTA barrier per tile):
+    // measured slower (QFT-30 last pass 4.12 -> 4.97 ms), so only on request
+    static const bool wind = std::getenv("SVB_WARP_INDEPENDENT") != nullptr;
+    if (wind && stages == 0 && pd.nrounds == 1 &&
+        pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], -1, pd.zsum) <= kSmemMaxPerCTA)
+      stages = -1;
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum);

@@ -514,3 +514,26 @@ def test_zero_start_support_tracking(precision):
             np.testing.assert_allclose(z, want, atol=10 * tol, err_msg=f"{c.name} jit={jit}")
             assert relerr(s.to_numpy(), ref) < tol, (c.name, jit)
             s.close()
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_qft_dft_fused_z_26_qubits(precision):
+    """x-prep + QFT-26 from a lazy |0...0> (JIT passes, support tracking, free
+    initial layout, <Z_i> fused into the last pass): amplitudes against the DFT
+    closed form, and every <Z_i> is exactly 0 in exact arithmetic (flat |amp|^2)."""
+    n = 26
+    basis = 0x2B5C3E1
+    c = Circuit(n)
+    for q in range(n):
+        if (basis >> q) & 1:
+            c.gate("x", q)
+    suite.qft(n, c)
+    s = sv.DeviceState(n, precision)
+    z = s.apply_gates_z(sv.gate_array(c.instructions), list(range(n)))
+    assert float(np.max(np.abs(z))) < (1e-10 if precision == "c128" else 2e-5), z
+    got = s.to_numpy()
+    k = np.arange(1 << n, dtype=np.float64)
+    phase = np.mod(basis * k, float(1 << n)) / (1 << n)
+    want = np.exp(2j * math.pi * phase) / math.sqrt(1 << n)
+    assert relerr(got, want) < TOL[precision]
+    s.close()
