@@ -244,6 +244,42 @@ SVB_HD void u1_piv(cplx<R>* a, cplx<R> r0, cplx<R> r1) {
   }
 }
 
+// u1_piv with registers known to be zero (bit v of ZM: a[v] == 0, e.g. the
+// never-written positions of a support-tracked pass): no work on zero
+// operands (JIT only; the generator tracks ZM through the ops)
+template <typename R, int RK> SVB_HD cplx<R> piv_mul(cplx<R> o, cplx<R> r) {  // r*o
+  if constexpr (RK == 0) return mk<R>(R(0), R(0));
+  else if constexpr (RK == 1) return mk<R>(r.x * o.x, r.x * o.y);
+  else if constexpr (RK == 2) return mk<R>(-r.y * o.y, r.y * o.x);
+  else return cmul<R>(r, o);
+}
+template <typename R, int RK, bool PZ, bool OZ> SVB_HD cplx<R> piv_row_z(cplx<R> p, cplx<R> o, cplx<R> r) {
+  if constexpr (PZ && OZ) return mk<R>(R(0), R(0));
+  else if constexpr (OZ) return p;
+  else if constexpr (PZ) return piv_mul<R, RK>(o, r);
+  else return piv_row<R, RK>(p, o, r);
+}
+template <typename R, int RB, int B, int PC0, int PC1, int RK0, int RK1, uint32_t ZM>
+SVB_HD void u1_piv_z(cplx<R>* a, cplx<R> r0, cplx<R> r1) {
+#pragma unroll
+  for (int v = 0; v < (1 << RB); ++v) {
+    if (v & (1 << B)) continue;
+    const int w = v | (1 << B);
+    const cplx<R> x0 = a[v], x1 = a[w];
+    if (((ZM >> v) & 1u) && ((ZM >> w) & 1u)) continue;
+    if ((ZM >> v) & 1u) {
+      a[v] = PC0 ? piv_row_z<R, RK0, false, true>(x1, x0, r0) : piv_row_z<R, RK0, true, false>(x0, x1, r0);
+      a[w] = PC1 ? piv_row_z<R, RK1, false, true>(x1, x0, r1) : piv_row_z<R, RK1, true, false>(x0, x1, r1);
+    } else if ((ZM >> w) & 1u) {
+      a[v] = PC0 ? piv_row_z<R, RK0, true, false>(x1, x0, r0) : piv_row_z<R, RK0, false, true>(x0, x1, r0);
+      a[w] = PC1 ? piv_row_z<R, RK1, true, false>(x1, x0, r1) : piv_row_z<R, RK1, false, true>(x0, x1, r1);
+    } else {
+      a[v] = piv_row<R, RK0>(PC0 ? x1 : x0, PC0 ? x0 : x1, r0);
+      a[w] = piv_row<R, RK1>(PC1 ? x1 : x0, PC1 ? x0 : x1, r1);
+    }
+  }
+}
+
 // op-stream form (interpreter and structure-only JIT): ratios from the payload
 template <typename R, int RB, int B, int PC, bool REAL>
 SVB_HD void u1_piv_p(cplx<R>* a, const cplx<R>* r) {
@@ -1075,12 +1111,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // payloads that have uniform slots.
   // stages: 2 = double ring, 1 = single ring + prefetch, 0 = direct first round
   // (one tile of shared memory for the inter-round layouts, no cp.async)
-  // stages -1 = direct and warp-independent: a one-round pass needs no ring at
-  // all (registers in from HBM, out to HBM) and no CTA barrier per tile: every
-  // warp evaluates its own copy of the tile-uniform factors
-  const bool wmode = stages < 0;
-  const uint32_t ring_bytes =
-      wmode ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
+  const uint32_t ring_bytes = (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
   uint32_t staged = 0;
   if (ops_mode == 0) {
     const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
@@ -1110,7 +1141,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.uni = uni;
   // uniform slots are double-buffered by tile parity (the next tile's factors
   // are written while slow warps may still read this tile's)
-  c.pro = uni + (wmode ? (int)(blockDim.x >> 5) : 2) * pd.ndiag * kUniStride;
+  c.pro = uni + 2 * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   (void)nslots;
   double zl[RB + 3];
@@ -1146,7 +1177,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.zero_input = zero_input;
   c.prefetch = 0;
   c.next_base = 0;
-  c.direct = stages <= 0;  // launch chose the direct first round (pd.direct, single stage)
+  c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
   c.l2next = 0;
   __syncthreads();
 #pragma unroll
@@ -1177,20 +1208,6 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
     if (pd.perm_out) c.pbase = tile_base_warp(pd, t, lane, true);
-    if (wmode) {
-      // the warp's own uniform slots: its lanes finished reading the previous
-      // tile's factors before they are overwritten
-      c.uni = uni + warp * ndiag * kUniStride;
-      if (ndiag > 0) {
-        __syncwarp();
-        diag_uniform_items<R, RB>(smraw, s_doff, pd.items, pd.nitems, base, const_cast<cplx<R>*>(c.uni), 0, 1, lane);
-        __syncwarp();
-      }
-      c.l2next = tn < ntiles;
-      if (c.l2next) c.next_base = tile_base_warp(pd, tn, lane);
-      Body::template tile<R, RB>(pass, c, a, ring, base, bs);
-      continue;
-    }
     c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
       diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, base, const_cast<cplx<R>*>(c.uni),
@@ -1241,10 +1258,8 @@ template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
                                               int zsum = 0) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
-  const uint32_t ring = stages < 0 ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
-  const uint32_t uni_sets = stages < 0 ? (nthr >> 5) : 2u;  // per warp (stages -1) or double-buffered
-  return ring + ((staged_ops + 15u) & ~15u) +
-         (uni_sets * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
+  return (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
+         (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
          0u * (uint32_t)zsum;  // fused <Z> accumulates in global memory (zsum_tile)
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;

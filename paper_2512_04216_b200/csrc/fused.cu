@@ -341,7 +341,6 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     unsigned threads = 1u << (pd.m - RB);
     int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, pd.zsum);
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
-    if (stages == 0 && pd.nrounds == 1 && std::getenv("SVB_WARP_INDEPENDENT")) stages = -1;  // see jit.cu
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;

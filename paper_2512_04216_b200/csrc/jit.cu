@@ -368,6 +368,12 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       for (int v = 0; v < (1 << RB); ++v) o << "    a[" << v << "] = cur[sFl ^ " << K[v] << "u];\n";
     }
     if (k + 1 == pd.nrounds) o << "    svb::prefetch_next<R, RB, PassBody>(c);\n";
+    // registers statically zero: round 0 of a support-tracked pass (never-written
+    // positions), tracked through the leading pivot ops (any other op ends it)
+    uint32_t zm = 0;
+    if (k == 0 && pd.dmask && imm)
+      for (int v = 0; v < (1 << RB); ++v)
+        if (G[v] & pd.dmask) zm |= 1u << v;
     uint32_t off = rd.op_off;
     while (off < rd.op_end) {
       OpHdr h;
@@ -383,6 +389,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       }
       const std::string cond = h.rmask ? "true" : "false";
       const std::string rm = std::to_string(h.rmask) + "u, " + std::to_string(h.rval) + "u";
+      if (h.kind != OP_U1P && h.kind != OP_U1PR) zm = 0;  // zero tracking covers leading pivot ops only
       switch (h.kind) {
         case OP_DIAG:
           pc.round = k;
@@ -416,6 +423,24 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         case OP_U1P:
         case OP_U1PR: {
           const int pc0 = h.n & 1, pc1 = (h.n >> 1) & 1;
+          if (imm && zm && !h.fmask) {
+            auto rk = [](const cplx<R>& z) { return z.x == 0 && z.y == 0 ? 0 : z.y == 0 ? 1 : z.x == 0 ? 2 : 3; };
+            const int rk0 = rk(coef[0]), rk1 = rk(coef[1]);
+            o << "    svb::u1_piv_z<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk0 << ", " << rk1 << ", "
+              << zm << "u>(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
+            uint32_t nz = zm;  // zero outputs: both inputs zero, or (p zero and the ratio term zero)
+            for (int v = 0; v < (1 << RB); ++v) {
+              if (v & (1 << h.a)) continue;
+              const int w = v | (1 << h.a);
+              const bool z0 = (zm >> v) & 1u, z1 = (zm >> w) & 1u;
+              const bool p0z = pc0 ? z1 : z0, o0z = pc0 ? z0 : z1, p1z = pc1 ? z1 : z0, o1z = pc1 ? z0 : z1;
+              const bool y0z = p0z && (o0z || rk0 == 0), y1z = p1z && (o1z || rk1 == 0);
+              nz = (nz & ~((1u << v) | (1u << w))) | (y0z ? 1u << v : 0u) | (y1z ? 1u << w : 0u);
+            }
+            zm = nz;
+            break;
+          }
+          zm = 0;
           if (imm) {
             auto rk = [](const cplx<R>& z) { return z.x == 0 && z.y == 0 ? 0 : z.y == 0 ? 1 : z.x == 0 ? 2 : 3; };
             o << "    " << guard << "svb::u1_piv<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk(coef[0])
@@ -737,12 +762,6 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
-    // one-round direct pass, warp-independent (no ring, no CTA barrier per tile):
-    // measured slower (QFT-30 last pass 4.12 -> 4.97 ms), so only on request
-    static const bool wind = std::getenv("SVB_WARP_INDEPENDENT") != nullptr;
-    if (wind && stages == 0 && pd.nrounds == 1 &&
-        pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], -1, pd.zsum) <= kSmemMaxPerCTA)
-      stages = -1;
     const unsigned grid =
         (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum);
