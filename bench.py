@@ -46,13 +46,14 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 
 
 def measured_traffic():
-    """dram read+write bytes per launch of the dominant kernel from the committed
-    ncu --set full capture (profiles/r01_ncu_qft30_pass_full.json), or None."""
+    """dram read+write bytes per launch of the dominant kernel (the bench step's
+    last fused pass) from the committed ncu --set full capture
+    (profiles/r01_ncu_qft30_pass_full.json, record "qft30_top"), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_qft30_pass_full.json")) as fh:
             recs = json.load(fh)
-        vals = [(r["dram_read_bytes"] + r["dram_write_bytes"]) * 1e9 for r in recs]  # ncu reports GB
-        return float(sum(vals) / len(vals))
+        top = [r for r in recs if "top" in r.get("report", "")] or recs[:1]
+        return float((top[0]["dram_read_bytes"] + top[0]["dram_write_bytes"]) * 1e9)  # ncu reports GB
     except Exception:
         return None
 
