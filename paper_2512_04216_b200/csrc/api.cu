@@ -121,6 +121,16 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
     require(n_qubits >= 1 && n_qubits <= 40, SVB_E_ARG, "n_qubits out of range");
     require(precision == SVB_C64 || precision == SVB_C128, SVB_E_ARG, "bad precision");
     SVB_CUDA(cudaSetDevice(device));
+    {
+      // small per-call scratch (program upload, reduction workspaces) comes from
+      // the stream-ordered pool; keep its memory mapped across synchronisations
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = 1ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+    }
     h = new svb_state();
     h->n = n_qubits;
     h->prec = precision;
