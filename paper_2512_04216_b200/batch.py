@@ -69,7 +69,7 @@ def _small_batch(circuits, shots, seed, precision, device):
 
 
 def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", sampler: str = "cdf",
-              device: int = 0, workers: int = 4, qubit_cap: int = sv.DEFAULT_QUBIT_CAP):
+              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP):
     """Run every circuit with (shots, seed); returns a list of RunResult or
     exception objects, in input order.  Default sampler: the device CDF
     sampler (throughput); sampler="alias" keeps the reference's exact alias

@@ -1050,6 +1050,14 @@ struct InterpBody {
   }
   template <typename R, int RB>
   __device__ static __forceinline__ void prologue(const PassCtx<R, RB>&, State<R, RB>&) {}
+  // direct first round: the tile's round-0 amplitudes straight from HBM
+  template <typename R, int RB>
+  __device__ static __forceinline__ void preload(const PassCtx<R, RB>& c, cplx<R>* a, uint64_t base) {
+    uint32_t sFl;
+    uint64_t Fg;
+    round_fixed<R, RB>(c, 0, base, sFl, Fg);
+    load_global<R, RB>(c, Fg, c.pd.rounds[0], a);
+  }
   template <typename R, int RB>
   __device__ static __forceinline__ void tile(int, const PassCtx<R, RB>& c, cplx<R>* a, cplx<R>* cur,
                                               uint64_t base, const State<R, RB>&) {
@@ -1061,8 +1069,7 @@ struct InterpBody {
       round_fixed<R, RB>(c, k, base, sFl, Fg);
       uint32_t slot[1 << RB];
       layout_slots<R, RB>(sFl, rd, slot);
-      if (k == 0 && c.direct) load_global<R, RB>(c, Fg, rd, a);
-      else load_slots<R, RB>(a, cur, slot);
+      if (!(k == 0 && c.direct)) load_slots<R, RB>(a, cur, slot);  // direct: preload() filled a
       if (k + 1 == nrounds) prefetch_next<R, RB, InterpBody>(c);
       run_ops<R, RB>(a, Fg, c.ops, rd.op_off, rd.op_end, c.uni);
       if (k + 1 < nrounds) {
@@ -1208,6 +1215,14 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
     if (pd.perm_out) c.pbase = tile_base_warp(pd, t, lane, true);
+    if (stages == 0) {
+      // direct first round: issue the tile's HBM loads (and the next tile's L2
+      // prefetches) before the uniform factors and the barrier, so their
+      // latency overlaps them; a[] is free between tiles
+      c.l2next = tn < ntiles;
+      if (c.l2next) c.next_base = tile_base_warp(pd, tn, lane);
+      Body::template preload<R, RB>(c, a, base);
+    }
     c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
       diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, base, const_cast<cplx<R>*>(c.uni),
@@ -1220,9 +1235,6 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages == 1) {
       c.prefetch = tn < ntiles;
       if (c.prefetch) c.next_base = tile_base_warp(pd, tn, lane);
-    } else if (stages == 0) {
-      c.l2next = tn < ntiles;
-      if (c.l2next) c.next_base = tile_base_warp(pd, tn, lane);
     }
     Body::template tile<R, RB>(pass, c, a, ring + (size_t)(stages > 1 ? (it & 1) : 0) * T, base, bs);
     // two stages: the ring slot is rewritten by the next iteration's issue.

@@ -145,6 +145,7 @@ template <typename C> bool is1(const C& z) { return z.x == 1 && z.y == 0; }
 // at generation time (controlled phases leave half the amplitudes untouched).
 struct PrologueCtx {
   std::ostringstream* o = nullptr;  // prologue code (runs once per thread)
+  std::ostringstream* pre = nullptr;  // preload(): round-0 HBM loads of a direct first round
   int nslots = 0;                   // per-thread complex slots
   int round = 0;                    // round of the op being emitted
 };
@@ -333,27 +334,30 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         K[v | (1 << i)] = K[v] ^ swz<R>(1u << rd.reg_local[i]);
         G[v | (1 << i)] = G[v] | (1ull << pd.pos[rd.reg_local[i]]);
       }
-    if (k == 0) {  // direct first round (launch-time choice, see pass_kernel)
-      o << "    if (c.direct) {\n      const svb::cplx<R>* g0 = c.state + Fg;\n"
-           "      if (c.zero_input) {\n";
-      for (int v = 0; v < (1 << RB); ++v)
-        o << "        a[" << v << "] = svb::mk<R>((Fg | " << G[v] << "ull) == 0 ? R(1) : R(0), R(0));\n";
-      o << "      } else {\n";
-      if (pd.dmask) {  // support tracking: only written positions are read; the next tile's go to L2
-        o << "        const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
-        for (int v = 0; v < (1 << RB); ++v) {
-          if (G[v] & pd.dmask) o << "        a[" << v << "] = svb::mk<R>(R(0), R(0));\n";
-          else o << "        a[" << v << "] = tdead0 ? svb::mk<R>(R(0), R(0)) : __ldcs(g0 + " << G[v] << "ull);\n";
-        }
-        o << "        if (c.l2next && !tdead0) {\n"
-             "          const svb::cplx<R>* gn = c.state + ((Fg & ~base) | c.next_base);\n";
+    if (k == 0) {  // direct first round (launch-time choice): preload() already filled a[]
+      {
+        std::ostringstream& P = *pc.pre;
+        P << "    const svb::cplx<R>* g0 = c.state + Fg;\n    if (c.zero_input) {\n";
         for (int v = 0; v < (1 << RB); ++v)
-          if (!(G[v] & pd.dmask)) o << "          svb::prefetch_l2(gn + " << G[v] << "ull);\n";
-        o << "        }\n";
-      } else {
-        for (int v = 0; v < (1 << RB); ++v) o << "        a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
+          P << "      a[" << v << "] = svb::mk<R>((Fg | " << G[v] << "ull) == 0 ? R(1) : R(0), R(0));\n";
+        P << "    } else {\n";
+        if (pd.dmask) {  // support tracking: only written positions are read; the next tile's go to L2
+          P << "      const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
+          for (int v = 0; v < (1 << RB); ++v) {
+            if (G[v] & pd.dmask) P << "      a[" << v << "] = svb::mk<R>(R(0), R(0));\n";
+            else P << "      a[" << v << "] = tdead0 ? svb::mk<R>(R(0), R(0)) : __ldcs(g0 + " << G[v] << "ull);\n";
+          }
+          P << "      if (c.l2next && !tdead0) {\n"
+               "        const svb::cplx<R>* gn = c.state + ((Fg & ~base) | c.next_base);\n";
+          for (int v = 0; v < (1 << RB); ++v)
+            if (!(G[v] & pd.dmask)) P << "        svb::prefetch_l2(gn + " << G[v] << "ull);\n";
+          P << "      }\n";
+        } else {
+          for (int v = 0; v < (1 << RB); ++v) P << "      a[" << v << "] = __ldcs(g0 + " << G[v] << "ull);\n";
+        }
+        P << "    }\n";
       }
-      o << "      }\n    } else {\n";
+      o << "    if (!c.direct) {\n";
       if (pd.dmask) {  // never-written positions (support tracking) are zeros, not loaded
         o << "      const bool tdead0 = (Fg & " << pd.dmask << "ull) != 0;\n";
         for (int v = 0; v < (1 << RB); ++v) {
@@ -523,9 +527,10 @@ constexpr int kImmMinQubits = 28;
 // staged in shared memory (ops_mode 1).
 template <typename R> std::string jit_source_pass(const Program& prog, int p, int* nslots, bool* imm_out) {
   constexpr int RB = kRegBits<R>;
-  std::ostringstream body, pro;
+  std::ostringstream body, pro, pre;
   PrologueCtx pc;
   pc.o = &pro;
+  pc.pre = &pre;
   const PassDev& pd0 = prog.passes[p];
   const bool imm = prog.n >= kImmMinQubits;  // (not m + nout: support tracking shrinks nout)
   emit_body<R>(body, prog, p, RB, imm, pc);
@@ -579,6 +584,11 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
     << "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void prologue(const svb::PassCtx<R, RB>& c, State<R, RB>& st) {\n"
     << pro.str() << "    (void)c; (void)st;\n  }\n"
+       "  template <typename R, int RB>\n"
+       "  __device__ static __forceinline__ void preload(const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
+       "uint64_t base) {\n"
+       "    uint32_t sFl; uint64_t Fg;\n    svb::round_fixed<R, RB>(c, 0, base, sFl, Fg); (void)sFl;\n"
+    << pre.str() << "  }\n"
        "  template <typename R, int RB>\n"
        "  __device__ static __forceinline__ void tile(int pass, const svb::PassCtx<R, RB>& c, svb::cplx<R>* a, "
        "svb::cplx<R>* cur, uint64_t base, const State<R, RB>& st) {\n"

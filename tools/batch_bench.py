@@ -15,7 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--count", type=int, default=10000)
 ap.add_argument("--shots", type=int, default=1000)
 ap.add_argument("--precision", default="c128")
-ap.add_argument("--workers", type=int, default=4)
+ap.add_argument("--workers", type=int, default=8)
 ap.add_argument("--cpu", action="store_true")
 a = ap.parse_args()
 t0 = time.perf_counter()
