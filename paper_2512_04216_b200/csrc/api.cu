@@ -126,7 +126,7 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
       // the stream-ordered pool; keep its memory mapped across synchronisations
       cudaMemPool_t pool;
       if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t keep = 1ull << 30;
+        uint64_t keep = ~0ull;  // state buffers retry after a trim (state_malloc)
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
       }
       cudaGetLastError();
@@ -136,7 +136,7 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
     h->prec = precision;
     h->device = device;
     SVB_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
-    cudaError_t e = cudaMalloc(&h->amps, h->amp_bytes());
+    cudaError_t e = state_malloc(&h->amps, h->amp_bytes());
     if (e != cudaSuccess) {
       cudaGetLastError();
       h->amps = nullptr;

@@ -35,6 +35,23 @@ inline void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
 }
 
+// cudaMalloc for state-sized buffers: the stream-ordered pool keeps freed
+// scratch mapped (svb_create sets an unbounded release threshold), so on
+// failure the pool is trimmed and the allocation retried once.
+inline cudaError_t state_malloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaErrorMemoryAllocation) return e;
+  cudaGetLastError();
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  cudaGetLastError();
+  return cudaMalloc(p, bytes);
+}
+
 inline int grid_for(uint64_t work, int block, int max_blocks = 148 * 16) {
   uint64_t g = (work + block - 1) / block;
   if (g > (uint64_t)max_blocks) g = max_blocks;

@@ -425,7 +425,7 @@ void run_permutation(void** state, void** spare, int n, const std::vector<int>& 
   bool ident = true;
   for (int p = 0; p < n; ++p) ident = ident && dest[p] == p;
   if (ident) return;
-  if (*spare == nullptr) SVB_CUDA(cudaMalloc(spare, sizeof(cplx<R>) << n));
+  if (*spare == nullptr) SVB_CUDA(state_malloc(spare, sizeof(cplx<R>) << n));
   launch_permute<R>(reinterpret_cast<cplx<R>**>(state), reinterpret_cast<cplx<R>**>(spare), n, dest, st, stats);
 }
 template void run_permutation<float>(void**, void**, int, const std::vector<int>&, cudaStream_t, ProgramStats*);
@@ -549,7 +549,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   };
   if (z) z->fused = false;
   if (!prog.final_perm.empty() && *spare == nullptr) {
-    if (cudaMalloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
+    if (state_malloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
       cudaGetLastError();
       *spare = nullptr;
       opt.relabel_swaps = false;  // no room: swaps become in-tile permutation ops
