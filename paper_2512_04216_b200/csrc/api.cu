@@ -126,7 +126,7 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
       // the stream-ordered pool; keep its memory mapped across synchronisations
       cudaMemPool_t pool;
       if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t keep = ~0ull;  // state buffers retry after a trim (state_malloc)
+        uint64_t keep = 1ull << 30;  // (unbounded measured slower for the 2 GiB sampler scratch)
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
       }
       cudaGetLastError();

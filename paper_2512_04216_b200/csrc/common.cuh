@@ -35,9 +35,9 @@ inline void require(bool ok, int code, const std::string& msg) {
   if (!ok) throw Error(code, msg);
 }
 
-// cudaMalloc for state-sized buffers: the stream-ordered pool keeps freed
-// scratch mapped (svb_create sets an unbounded release threshold), so on
-// failure the pool is trimmed and the allocation retried once.
+// cudaMalloc for state-sized buffers: the stream-ordered pool keeps up to
+// 1 GiB of freed scratch mapped (svb_create), so on failure the pool is
+// trimmed and the allocation retried once.
 inline cudaError_t state_malloc(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);
   if (e != cudaErrorMemoryAllocation) return e;

@@ -1118,7 +1118,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // payloads that have uniform slots.
   // stages: 2 = double ring, 1 = single ring + prefetch, 0 = direct first round
   // (one tile of shared memory for the inter-round layouts, no cp.async)
-  const uint32_t ring_bytes = (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
+  // a one-round direct pass never touches the ring (registers from HBM, to HBM)
+  const uint32_t ring_bytes = (stages == 0 && pd.nrounds == 1)
+                                  ? 0u
+                                  : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
   uint32_t staged = 0;
   if (ops_mode == 0) {
     const int4* src = reinterpret_cast<const int4*>(ops_g + pd.ops_begin);
@@ -1268,13 +1271,22 @@ template <typename R> inline double pass_hbm_bytes(const PassDev& pd, bool zin) 
 
 template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
-                                              int zsum = 0) {
+                                              int zsum = 0, int nrounds = 2) {
   const uint32_t nthr = 1u << (m - kRegBits<R>);
-  return (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m) + ((staged_ops + 15u) & ~15u) +
+  const uint32_t ring =
+      (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
+  return ring + ((staged_ops + 15u) & ~15u) +
          (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
          0u * (uint32_t)zsum;  // fused <Z> accumulates in global memory (zsum_tile)
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
+// One-round direct passes of a support-tracked program (the QFT bench's last
+// pass): no ring, so three CTAs per SM fit; the JIT gives them
+// __launch_bounds__(.., 3) (<= 85 registers) for more warps in flight.
+__host__ __device__ inline bool direct_one_round(const PassDev& pd) {
+  return pd.direct && pd.dmask && pd.nrounds == 1;
+}
+constexpr int kDirectMinBlocks = 3;
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
 __host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {

@@ -345,7 +345,7 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
-    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, pd.zsum), st>>>(
+    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, pd.zsum, pd.nrounds), st>>>(
         state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);
@@ -571,7 +571,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     int dev = 0, nsm = 148;
     SVB_CUDA(cudaGetDevice(&dev));
     SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const uint64_t ncta = std::min<uint64_t>(1ull << lp.nout, (uint64_t)nsm * kPassMinBlocks<R>);
+    const uint64_t ncta = std::min<uint64_t>(1ull << lp.nout, (uint64_t)nsm * kDirectMinBlocks);  // upper bound
     const unsigned nv = (unsigned)z->logical.size();
     double* partial = z->d_out + kZaccRows;
     k_zsum_finish<<<dim3(nv, kZsumSlices), 256, 0, st>>>(z->d_acc, (uint32_t)ncta, 1u << (lp.m - lp.rb), lp.rb,

@@ -598,7 +598,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   const size_t at = b.find(from);
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << kPassMinBlocks<R>
+  const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? kDirectMinBlocks : kPassMinBlocks<R>;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << minb
     << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
@@ -772,9 +773,12 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
-    const unsigned grid =
-        (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
-    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum);
+    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum, pd.nrounds);
+    int per_sm = stages <= 1 ? kPassMinBlocks<R> : 1;
+    if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
+        (uint64_t)kDirectMinBlocks * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
+      per_sm = kDirectMinBlocks;
+    const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * per_sm);
     static const bool trace = std::getenv("SVB_TRACE") != nullptr;
     if (trace)
       std::fprintf(stderr, "[svb] jit pass %zu: m=%d rounds=%d stages=%d grid=%u smem=%u staged=%u ndiag=%d slots=%d\n",
@@ -783,7 +787,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     // per-function attribute: always the maximum (no race between threads)
     if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
-    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
+    // three-CTA one-round passes use little shared memory: leave L1 room for their spills
+    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, per_sm == kDirectMinBlocks ? 60 : 100);
     cplx<R>* s = state;
     cplx<R>* so = pd.perm_out ? out : state;
     const PassDev* pdp = dpass + p;

@@ -537,3 +537,24 @@ def test_qft_dft_fused_z_26_qubits(precision):
     want = np.exp(2j * math.pi * phase) / math.sqrt(1 << n)
     assert relerr(got, want) < TOL[precision]
     s.close()
+
+
+def test_fused_z_fallbacks_and_edges():
+    """svb_apply_z where the last pass cannot sum: too few qubits for a fused
+    program (per-gate kernels + one reduction pass), fusion off, an empty qubit
+    list, and a circuit with no gates."""
+    for n, fusion in ((6, True), (12, False)):
+        c = suite.random_circuit(n, 40, np.random.default_rng(n), measured=False)
+        ref = orc.unitary_state(c)
+        s = sv.DeviceState(n)
+        if not fusion:
+            s.set_option(_lib.OPT_FUSION, 0)
+        z = s.apply_gates_z(sv.gate_array(c.instructions), list(range(n)))
+        np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(n)], atol=1e-10)
+        assert relerr(s.to_numpy(), ref) < 1e-10
+        s.close()
+    s = sv.DeviceState(10)
+    assert s.apply_gates_z(sv.gate_array(suite.qft_bench_circuit(10).instructions), []).size == 0
+    z = s.apply_gates_z(sv.gate_array([]), [0, 3])
+    np.testing.assert_allclose(z, [orc.expectation_from_state(s.to_numpy(), (q,)) for q in (0, 3)], atol=1e-10)
+    s.close()
