@@ -302,15 +302,47 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
         d1real[i] = d0real[i];
       }
     }
-  if (need_c) {
-    if (creal) o << "      svb::mul_all_r<R, RB>(a, C.x);\n";
-    else o << "      svb::mul_all<R, RB>(a, C);\n";
-  }
+  // complex factors: with two or more, one product per register index (a
+  // product tree over the bits: F_v = F_(v - lowbit) * D1_lowbit, C folded into
+  // F_0) replaces a complex multiply per factor per amplitude
+  uint32_t cbits = 0;
   for (int i = 0; i < RB; ++i)
-    if (!d1one[i]) {
-      if (d1real[i]) o << "      svb::mul_half_r<R, RB, " << i << ">(a, D1_" << i << ".x);\n";
-      else o << "      svb::mul_half<R, RB, " << i << ">(a, D1_" << i << ");\n";
+    if (!d1one[i] && !d1real[i]) cbits |= 1u << i;
+  const bool cc = need_c && !creal;
+  if (__builtin_popcount(cbits) + (cc ? 1 : 0) >= 2) {
+    if (need_c && creal) o << "      svb::mul_all_r<R, RB>(a, C.x);\n";
+    o << "      { svb::cplx<R> F[" << (1 << RB) << "];\n";
+    for (int v = 0; v < (1 << RB); ++v) {
+      const uint32_t act = (uint32_t)v & cbits;
+      if (act == 0) {
+        if (cc) o << "        F[" << v << "] = C;\n";
+        continue;
+      }
+      if (act != (uint32_t)v) continue;  // F depends only on the active bits: reuse F[act]
+      const int low = __builtin_ctz(act);
+      const uint32_t rest = act & (act - 1);
+      if (rest == 0 && !cc) o << "        F[" << v << "] = D1_" << low << ";\n";
+      else o << "        F[" << v << "] = svb::cmul<R>(F[" << rest << "], D1_" << low << ");\n";
     }
+    for (int v = 0; v < (1 << RB); ++v) {
+      const uint32_t act = (uint32_t)v & cbits;
+      if (act == 0 && !cc) continue;
+      o << "        a[" << v << "] = svb::cmul<R>(a[" << v << "], F[" << act << "]);\n";
+    }
+    o << "      }\n";
+    for (int i = 0; i < RB; ++i)
+      if (!d1one[i] && d1real[i]) o << "      svb::mul_half_r<R, RB, " << i << ">(a, D1_" << i << ".x);\n";
+  } else {
+    if (need_c) {
+      if (creal) o << "      svb::mul_all_r<R, RB>(a, C.x);\n";
+      else o << "      svb::mul_all<R, RB>(a, C);\n";
+    }
+    for (int i = 0; i < RB; ++i)
+      if (!d1one[i]) {
+        if (d1real[i]) o << "      svb::mul_half_r<R, RB, " << i << ">(a, D1_" << i << ".x);\n";
+        else o << "      svb::mul_half<R, RB, " << i << ">(a, D1_" << i << ");\n";
+      }
+  }
   o << "    }\n";
 }
 
