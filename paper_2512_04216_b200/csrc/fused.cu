@@ -447,17 +447,32 @@ std::list<std::pair<ProgKey, std::shared_ptr<const void>>> g_prog_lru;
 std::unordered_map<ProgKey, decltype(g_prog_lru)::iterator, ProgKeyHash> g_prog_idx;
 constexpr size_t kProgCacheEntries = 32;
 
+// 128-bit key of the gate records: four independent multiply-rotate lanes
+// over 32-byte blocks (the hash runs on every apply: ~0.6 MB for QFT-30, so
+// it must be memory-speed, not a serial FNV chain)
 ProgKey prog_key(const void* data, size_t n, uint64_t salt) {
-  ProgKey k{0xcbf29ce484222325ull ^ salt, 0x84222325cbf29ce4ull + salt};
   const unsigned char* p = static_cast<const unsigned char*>(data);
-  for (size_t i = 0; i < n; i += 8) {
+  uint64_t h[4] = {0x9E3779B97F4A7C15ull ^ salt, 0xC2B2AE3D27D4EB4Full + salt, 0x165667B19E3779F9ull,
+                   0x27D4EB2F165667C5ull ^ (salt << 1)};
+  auto mix = [](uint64_t x, uint64_t w) {
+    x ^= w * 0x87C37B91114253D5ull;
+    x = (x << 31) | (x >> 33);
+    return x * 0x4CF5AD432745937Full;
+  };
+  size_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    uint64_t w[4];
+    std::memcpy(w, p + i, 32);
+    for (int l = 0; l < 4; ++l) h[l] = mix(h[l], w[l]);
+  }
+  for (int l = 0; i < n; i += 8, ++l) {
     uint64_t w = 0;
     std::memcpy(&w, p + i, std::min<size_t>(8, n - i));
-    k.a = (k.a ^ w) * 0x100000001B3ull;
-    k.a ^= k.a >> 29;
-    k.b = (k.b + w) * 0xC2B2AE3D27D4EB4Full;
-    k.b ^= k.b >> 31;
+    h[l & 3] = mix(h[l & 3], w);
   }
+  ProgKey k{h[0] ^ (h[2] * 0x9E3779B97F4A7C15ull) ^ n, h[1] ^ (h[3] * 0xC2B2AE3D27D4EB4Full) ^ (n << 7)};
+  k.a ^= k.a >> 29;
+  k.b ^= k.b >> 31;
   return k;
 }
 }  // namespace

@@ -109,18 +109,31 @@ struct Key128Hash {
 };
 std::unordered_map<Key128, ProgKernels, Key128Hash> g_prog;
 
+// four independent multiply-rotate lanes over 32-byte blocks (runs on every
+// apply over the program's pass descriptors and op stream)
 void mix_bytes(Key128& k, const void* data, size_t n) {
   const unsigned char* p = static_cast<const unsigned char*>(data);
-  for (size_t i = 0; i < n; i += 8) {
+  uint64_t h[4] = {k.a, k.b, k.a ^ 0x165667B19E3779F9ull, k.b + 0x27D4EB2F165667C5ull};
+  auto mix = [](uint64_t x, uint64_t w) {
+    x ^= w * 0x87C37B91114253D5ull;
+    x = (x << 31) | (x >> 33);
+    return x * 0x4CF5AD432745937Full;
+  };
+  size_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    uint64_t w[4];
+    std::memcpy(w, p + i, 32);
+    for (int l = 0; l < 4; ++l) h[l] = mix(h[l], w[l]);
+  }
+  for (int l = 0; i < n; i += 8, ++l) {
     uint64_t w = 0;
     std::memcpy(&w, p + i, std::min<size_t>(8, n - i));
-    k.a = (k.a ^ w) * 0x100000001B3ull;
-    k.a ^= k.a >> 29;
-    k.b = (k.b + w) * 0xC2B2AE3D27D4EB4Full;
-    k.b ^= k.b >> 31;
+    h[l & 3] = mix(h[l & 3], w);
   }
-  k.a ^= n;
-  k.b += n * 0x9E3779B97F4A7C15ull;
+  k.a = h[0] ^ (h[2] * 0x9E3779B97F4A7C15ull) ^ n;
+  k.b = h[1] ^ (h[3] * 0xC2B2AE3D27D4EB4Full) + n * 0x9E3779B97F4A7C15ull;
+  k.a ^= k.a >> 29;
+  k.b ^= k.b >> 31;
 }
 
 std::string hexf(double x, bool single) {
