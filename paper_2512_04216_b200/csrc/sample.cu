@@ -518,20 +518,34 @@ void alias_draw(const double* d_prob_row, const int64_t* d_alias_row, uint64_t m
 }
 
 // --------------------------------------------------------------- CDF draws
-// Fused |amp|^2 + leaf sums: one warp per 32-amplitude leaf.
+// Fused |amp|^2 + leaf sums: one warp per leaf of `leaf_len` (32 << k)
+// amplitudes, lanes on consecutive amplitudes.  Leaves grow with the state so
+// that the leaf and prefix arrays stay <= 2^24 doubles (128 MB: the scratch
+// stays mapped in the stream-ordered pool between calls).
 template <typename R>
-__global__ void k_leaf_sums_state(const cplx<R>* __restrict__ s, uint64_t nleaf, double* __restrict__ leaf) {
+__global__ void k_leaf_sums_state(const cplx<R>* __restrict__ s, uint64_t nleaf, uint32_t leaf_len,
+                                  double* __restrict__ leaf) {
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (uint64_t l = gw; l < nleaf; l += nw) {
-    cplx<R> a = s[l * 32 + lane];
-    double x = (double)a.x, y = (double)a.y;
-    double p = x * x + y * y;
+    double p = 0.0;
+    for (uint32_t j = lane; j < leaf_len; j += 32) {
+      const cplx<R> a = __ldcs(s + l * leaf_len + j);
+      const double x = (double)a.x, y = (double)a.y;
+      p += x * x + y * y;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
     if (lane == 0) leaf[l] = p;
   }
+}
+
+// leaf length for an m-amplitude state: 32, doubled until nleaf <= 2^24
+inline uint32_t cdf_leaf_len(uint64_t m) {
+  uint32_t L = 32;
+  while (m / L > (1ull << 24)) L <<= 1;
+  return L;
 }
 
 __global__ void k_leaf_sums_probs(const double* __restrict__ pr, uint64_t m, uint64_t nleaf,
@@ -546,7 +560,7 @@ __global__ void k_leaf_sums_probs(const double* __restrict__ pr, uint64_t m, uin
 
 template <typename Prob>
 __device__ __forceinline__ uint64_t cdf_pick(const double* __restrict__ cum, uint64_t nleaf, uint64_t m,
-                                             double target, Prob prob) {
+                                             double target, Prob prob, uint32_t leaf_len = 32) {
   uint64_t lo = 0, hi = nleaf;  // first leaf with cum > target
   while (lo < hi) {
     uint64_t mid = (lo + hi) >> 1;
@@ -555,7 +569,7 @@ __device__ __forceinline__ uint64_t cdf_pick(const double* __restrict__ cum, uin
   }
   if (lo >= nleaf) lo = nleaf - 1;
   double acc = lo ? cum[lo - 1] : 0.0;
-  uint64_t i0 = lo * 32, i1 = i0 + 32 < m ? i0 + 32 : m;
+  uint64_t i0 = lo * leaf_len, i1 = i0 + leaf_len < m ? i0 + leaf_len : m;
   uint64_t last_nz = i0;
   for (uint64_t i = i0; i < i1; ++i) {
     double p = prob(i);
@@ -570,7 +584,7 @@ __device__ __forceinline__ uint64_t cdf_pick(const double* __restrict__ cum, uin
 
 template <typename R>
 __global__ void k_cdf_draw_state(const cplx<R>* __restrict__ s, uint64_t m, const double* __restrict__ cum,
-                                 uint64_t nleaf, uint64_t shots, Pcg base, BitSrc bs, int w,
+                                 uint64_t nleaf, uint32_t leaf_len, uint64_t shots, Pcg base, BitSrc bs, int w,
                                  uint64_t* __restrict__ codes) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t s0 = t * kShotsPerThread;
@@ -586,7 +600,7 @@ __global__ void k_cdf_draw_state(const cplx<R>* __restrict__ s, uint64_t m, cons
   };
   for (uint64_t k = s0; k < s1; ++k) {
     double target = g.next_double() * total;
-    codes[k] = pack_code(cdf_pick(cum, nleaf, m, target, prob), bs, w);
+    codes[k] = pack_code(cdf_pick(cum, nleaf, m, target, prob, leaf_len), bs, w);
   }
 }
 
@@ -612,15 +626,16 @@ void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, con
               int w, uint64_t* d_codes, cudaStream_t st) {
   uint64_t m = 1ull << n;
   require(n >= 5, SVB_E_ARG, "cdf sampler needs n >= 5");
-  uint64_t nleaf = m / 32;
+  const uint32_t L = cdf_leaf_len(m);
+  uint64_t nleaf = m / L;
   DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
   k_leaf_sums_state<R><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const cplx<R>*>(state),
-                                                                    nleaf, leaf.as<double>());
+                                                                    nleaf, L, leaf.as<double>());
   SVB_CHECK_LAUNCH();
   cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
   uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
   k_cdf_draw_state<R><<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
-      static_cast<const cplx<R>*>(state), m, cum.as<double>(), nleaf, shots, pcg_from(pcg),
+      static_cast<const cplx<R>*>(state), m, cum.as<double>(), nleaf, L, shots, pcg_from(pcg),
       make_bitsrc(bit_src, w), w, d_codes);
   SVB_CHECK_LAUNCH();
 }
@@ -648,7 +663,8 @@ template void cdf_draw<double>(const void*, int, uint64_t, const uint64_t*, cons
 // tau = u_s * total falls in [lo, hi); its local target is tau - lo.  Codes
 // of foreign shots are set to the sentinel ~0 (dropped by the histogram).
 __global__ void k_slice_draw(const double* __restrict__ cum, const double* __restrict__ pr_unused,
-                             const void* __restrict__ state, int prec128, uint64_t m, uint64_t nleaf, uint64_t shots,
+                             const void* __restrict__ state, int prec128, uint64_t m, uint64_t nleaf,
+                             uint32_t leaf_len, uint64_t shots,
                              Pcg base, double lo, double hi, double total, BitSrc bs, int w, uint64_t code_or,
                              uint64_t* __restrict__ codes) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -675,7 +691,7 @@ __global__ void k_slice_draw(const double* __restrict__ cum, const double* __res
     double x = tau - lo;
     const double tl = cum[nleaf - 1];
     if (x >= tl) x = tl * (1.0 - 1e-16);
-    const uint64_t idx = cdf_pick(cum, nleaf, m, x, prob);
+    const uint64_t idx = cdf_pick(cum, nleaf, m, x, prob, leaf_len);
     uint64_t code = code_or;
     for (int p = 0; p < w; ++p)
       if (bs.b[p] >= 0) code |= ((idx >> bs.b[p]) & 1ull) << p;
@@ -687,22 +703,23 @@ __global__ void k_slice_draw(const double* __restrict__ cum, const double* __res
 void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uint64_t* pcg, double lo, double hi,
                 double total, const int32_t* bit_src, int w, uint64_t code_or, uint64_t* d_codes, cudaStream_t st) {
   const uint64_t m = 1ull << n;
-  const uint64_t nleaf = m / 32;
+  const uint32_t L = cdf_leaf_len(m);
+  const uint64_t nleaf = m / L;
   DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
   if (prec128)
     k_leaf_sums_state<double><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const double2*>(state), nleaf,
-                                                                         leaf.as<double>());
+                                                                         L, leaf.as<double>());
   else
     k_leaf_sums_state<float><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const float2*>(state), nleaf,
-                                                                        leaf.as<double>());
+                                                                        L, leaf.as<double>());
   SVB_CHECK_LAUNCH();
   cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
   BitSrc bs;
   for (int p = 0; p < 64; ++p) bs.b[p] = p < w ? (int8_t)bit_src[p] : (int8_t)-1;
   uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
   k_slice_draw<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(cum.as<double>(), nullptr, state, prec128, m,
-                                                                   nleaf, shots, pcg_from(pcg), lo, hi, total, bs, w,
-                                                                   code_or, d_codes);
+                                                                   nleaf, L, shots, pcg_from(pcg), lo, hi, total, bs,
+                                                                   w, code_or, d_codes);
   SVB_CHECK_LAUNCH();
 }
 

@@ -29,6 +29,7 @@ if "syc32" in which:
     s.profile(True); s.zero(); s.timer_start(); s.apply_gates(g); ms_apply = s.timer_stop(); p = s.profile_read()
     qubits = list(range(n)); src = list(range(n))
     for shots in (10**6,):
+        s.sample_codes(qubits, src, shots, sv.pcg_words(2), 1)  # first call grows the stream-ordered pool
         s.timer_start(); codes, freq = s.sample_codes(qubits, src, shots, sv.pcg_words(1), 1); ms_s = s.timer_stop()
         print(json.dumps({"config": "sycamore32_d20_c64", "gates": int(g.size), "first_apply_s": first, "apply_ms": ms_apply, "apply_dense_input_ms": ms_dense,
                           "passes": p["pass_launches"], "pass_ms_mean": p["pass_ms"] / max(p["pass_launches"], 1),
