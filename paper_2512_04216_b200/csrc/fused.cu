@@ -481,7 +481,8 @@ template <typename R>
 static Program cached_program(int n, const svb_gate* g, int ng, const SchedOptions& opt) {
   const uint64_t salt = (uint64_t)n | ((uint64_t)sizeof(R) << 8) | ((uint64_t)opt.rb << 16) |
                         ((uint64_t)opt.m << 24) | ((uint64_t)opt.relabel_swaps << 32) |
-                        ((uint64_t)opt.round_search << 33) | ((uint64_t)opt.zero_start << 34);
+                        ((uint64_t)opt.round_search << 33) | ((uint64_t)opt.zero_start << 34) |
+                        ((uint64_t)opt.initial_perm << 35);
   const ProgKey key = prog_key(g, sizeof(svb_gate) * (size_t)ng, salt);
   {
     std::lock_guard<std::mutex> lk(g_prog_mu);
@@ -563,7 +564,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     z->fused = true;
   };
   if (z) z->fused = false;
-  if (!prog.final_perm.empty() && *spare == nullptr) {
+  if ((!prog.final_perm.empty() || !prog.init_perm.empty()) && *spare == nullptr) {
     if (state_malloc(spare, sizeof(cplx<R>) << n) != cudaSuccess) {
       cudaGetLastError();
       *spare = nullptr;
@@ -572,6 +573,14 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     }
   }
   const double t_build = tt.lap();
+  if (!prog.init_perm.empty()) {  // the input into the layout that absorbs the swap relabeling
+    write_zero();
+    cplx<R>* s0 = static_cast<cplx<R>*>(*state);
+    cplx<R>* sp0 = static_cast<cplx<R>*>(*spare);
+    launch_permute<R>(&s0, &sp0, n, prog.init_perm, st, stats);
+    *state = s0;
+    *spare = sp0;
+  }
   z_setup(prog);
   const bool zin = zero_pending && *zero_pending && !prog.passes.empty();
   if (prog.passes.empty()) write_zero();
@@ -639,7 +648,8 @@ int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_pas
     *n_passes = (int64_t)p.passes.size();
     *n_rounds = r;
     *op_bytes = (int64_t)p.ops.size();
-    *has_perm = p.final_perm.empty() ? 0 : (p.perm_fused ? 2 : 1);  // 2: fused into the last pass
+    // 1: final permutation pass, 2: fused into the last pass, 3: initial permutation pass
+    *has_perm = !p.init_perm.empty() ? 3 : p.final_perm.empty() ? 0 : (p.perm_fused ? 2 : 1);
     return SVB_OK;
   } catch (const Error& e) {
     set_last_error(e.what());

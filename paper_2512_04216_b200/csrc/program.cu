@@ -416,13 +416,15 @@ static void fuse_final_permutation(Program& prog, int n) {
   prog.perm_fused = true;
 }
 
+// absorb: start from the qubit layout that makes the swap relabeling end on
+// the identity (a lazy |0...0> input, or an input permuted into that layout)
 template <typename R>
-Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
+static Program build_program_layout(int n, const svb_gate* gates, int ng, const SchedOptions& opt, bool absorb) {
   Program prog;
   prog.gates = ng;
   prog.n = n;
   std::vector<int> phys;
-  std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, opt.zero_start, phys);
+  std::vector<FOp> ops = fuse(n, gates, ng, opt.relabel_swaps, absorb, phys);
   const int m = std::min(opt.m, n);
   const int RB = opt.rb;
   require(m - RB >= 5 && m <= kMaxM, SVB_E_ARG, "fused program needs n >= rb + 5");
@@ -917,6 +919,33 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
   return prog;
 }
 
+static int64_t total_rounds(const Program& p) {
+  int64_t r = 0;
+  for (const PassDev& pd : p.passes) r += pd.nrounds;
+  return r;
+}
+
+// With swap relabeling on a written (non-lazy) input the final layout must be
+// undone by a permutation either way; doing it FIRST (permute the input into
+// the layout that absorbs the relabeling) can give much cheaper passes (the
+// QFT's bit reversal: 14 -> 8 rounds over its 4 passes), so both schedules are
+// built and the one with fewer passes, then fewer rounds, is kept.
+template <typename R>
+Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt) {
+  if (!opt.relabel_swaps || opt.zero_start) return build_program_layout<R>(n, gates, ng, opt, opt.zero_start);
+  Program a = build_program_layout<R>(n, gates, ng, opt, false);
+  if (a.final_perm.empty() || a.perm_fused || !opt.initial_perm) return a;
+  Program b = build_program_layout<R>(n, gates, ng, opt, true);
+  if (!b.final_perm.empty()) return a;
+  if (b.passes.size() > a.passes.size() ||
+      (b.passes.size() == a.passes.size() && total_rounds(b) >= total_rounds(a)))
+    return a;
+  // input bit q moves to physical bit phys_init[q]; a's final map is the inverse
+  b.init_perm.assign(n, 0);
+  for (int p = 0; p < n; ++p) b.init_perm[a.final_perm[p]] = p;
+  return b;
+}
+
 template Program build_program<float>(int, const svb_gate*, int, const SchedOptions&);
 template Program build_program<double>(int, const svb_gate*, int, const SchedOptions&);
 
@@ -974,6 +1003,17 @@ static void emulate_pass(cplx<R>* state, cplx<R>* out, int n, const PassDev& pd,
 
 template <typename R>
 void emulate_program(cplx<R>* state, int n, const Program& prog) {
+  if (!prog.init_perm.empty()) {
+    const uint64_t len = 1ull << n;
+    std::vector<cplx<R>> tmp(len);
+    for (uint64_t i = 0; i < len; ++i) {
+      uint64_t o = 0;
+      for (int p = 0; p < n; ++p)
+        if ((i >> p) & 1) o |= 1ull << prog.init_perm[p];
+      tmp[o] = state[i];
+    }
+    std::copy(tmp.begin(), tmp.end(), state);
+  }
   std::vector<cplx<R>> out(prog.perm_fused ? (size_t)1 << n : 0);
   for (const PassDev& pd : prog.passes) {
     if (pd.rb == 4) emulate_pass<R, 4>(state, out.data(), n, pd, prog.ops.data());

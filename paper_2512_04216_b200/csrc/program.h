@@ -48,6 +48,7 @@ struct Program {
   std::vector<uint8_t> ops;          // op stream (all passes)
   std::vector<int> final_perm;       // physical bit p must move to bit final_perm[p]; empty = identity
   bool perm_fused = false;
+  std::vector<int> init_perm;        // input bit q moves to bit init_perm[q] before the passes; empty = none
   uint64_t support = ~0ull;          // zero_start: qubits the passes wrote; positions with other bits are never written           // final_perm is done by the last pass's permuted store (PassDev::perm_out)
   int64_t gates = 0;
   int n = 0;                         // qubits of the state
@@ -58,6 +59,7 @@ struct SchedOptions {
   int m = 12;        // tile qubits
   bool relabel_swaps = true;
   bool zero_start = false;   // input is |0...0>: choose the initial qubit layout so no final permutation is needed
+  bool initial_perm = true;  // written input + swaps: may permute the input first (see build_program)
   bool round_search = true;  // reorder ops across rounds (else program order)
 };
 

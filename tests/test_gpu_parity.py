@@ -558,3 +558,25 @@ def test_fused_z_fallbacks_and_edges():
     z = s.apply_gates_z(sv.gate_array([]), [0, 3])
     np.testing.assert_allclose(z, [orc.expectation_from_state(s.to_numpy(), (q,)) for q in (0, 3)], atol=1e-10)
     s.close()
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_initial_permutation_schedule(precision):
+    """Swaps on a written input: the input is permuted first into the layout
+    that absorbs the relabeling (cheaper passes), JIT and interpreter bodies."""
+    for n in (14, 16):
+        c = suite.qft_bench_circuit(n)
+        assert sv.plan(n, c.instructions, precision)["permute_initial"]
+        prep = suite.random_circuit(n, 30, np.random.default_rng(n), measured=False)
+        ref = orc.unitary_state(prep)
+        for inst in c.instructions:
+            orc.apply_instruction(ref, n, inst)
+        for jit in (-1, 1):
+            s = sv.DeviceState(n, precision)
+            s.set_option(_lib.OPT_JIT_MIN_N, jit)
+            s.apply_instructions(prep.instructions)
+            z = s.apply_gates_z(sv.gate_array(c.instructions), list(range(n)))
+            assert relerr(s.to_numpy(), ref) < TOL[precision], (n, jit)
+            np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(n)],
+                                       atol=10 * TOL[precision])
+            s.close()
