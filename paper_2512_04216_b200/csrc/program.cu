@@ -940,9 +940,9 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
   if (b.passes.size() > a.passes.size() ||
       (b.passes.size() == a.passes.size() && total_rounds(b) >= total_rounds(a)))
     return a;
-  // input bit q moves to physical bit phys_init[q]; a's final map is the inverse
-  b.init_perm.assign(n, 0);
-  for (int p = 0; p < n; ++p) b.init_perm[a.final_perm[p]] = p;
+  // input bit q moves to physical bit phys_init[q] = tau^-1(q), and a's final
+  // map (physical bit p -> logical bit final_perm[p]) is that same tau^-1
+  b.init_perm = a.final_perm;
   return b;
 }
 

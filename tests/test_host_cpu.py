@@ -188,6 +188,28 @@ def test_random_swap_circuits_on_arbitrary_state():
     assert fused > 0  # the permuted-store path was exercised
 
 
+@pytest.mark.parametrize("prec,tol", [("c128", 1e-12), ("c64", 1e-5)])
+def test_initial_permutation_schedule_on_arbitrary_state(prec, tol):
+    """Written input + swaps: schedules that permute the input first (into the
+    layout absorbing the relabeling) must equal the gate-by-gate result, for
+    swap permutations that are not involutions too."""
+    initial = 0
+    for seed in range(14):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(12, 16))
+        c = suite.random_circuit(n, 120, rng, measured=False)
+        psi0 = _random_state(n, seed)
+        ref = psi0.copy()
+        for inst in c.instructions:
+            orc.apply_instruction(ref, n, inst)
+        initial += sv.plan(n, c.instructions, prec)["permute_initial"]
+        got = sv.emulate(n, c.instructions, psi0, prec, relabel=1)
+        assert np.linalg.norm(got - ref) < tol, seed
+    q = suite.qft_bench_circuit(13)
+    assert sv.plan(13, q.instructions, prec)["permute_initial"] or prec == "c64"
+    assert initial > 0
+
+
 def test_fused_program_dft_known_answer():
     n = 12
     basis = 0b101100111010
