@@ -367,6 +367,9 @@ def run_ours(args, rank: int, world: int, dist):
         "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": n_gates,
                    "parallelism": "replicas" if world > 1 else "single", "l2": "inputs larger than L2",
                    "hbm_passes_per_step": stats["passes"], "plan": plan,
+                   "start": ("lazy |0...0> each step: the passes launch only tiles inside the written support and "
+                             "synthesise never-written positions as exact zeros (DESIGN.md §3); `dense` below is the "
+                             "same circuit on an already-written input"),
                    "wall_ms_per_step": wall_ms / args.steps},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": measured_traffic(),
