@@ -226,6 +226,7 @@ class ShardedState:
             _lib.check(_lib.lib().svb_clear(self.shard.state.handle))
         self.swaps = 0
         self.bytes_sent = 0
+        self._plans: dict = {}  # apply() plans by (gates, layout)
 
     def reset(self) -> None:
         """Back to |0...0> with the identity layout (reuses the shard memory)."""
@@ -272,8 +273,37 @@ class ShardedState:
 
     # ----------------------------------------------------------------- gates
     def apply(self, instructions) -> None:
+        """Apply a gate list: local gates in fused batches, a global<->local swap
+        whenever a gate acts non-diagonally on a global qubit.  The plan (swap
+        choices and this rank's restricted gate records) depends only on the
+        gates, the current layout and the rank, so it is computed once and
+        replayed on later calls (the per-gate Python work is most of a step)."""
         insts = [i for i in instructions if i.kind in UNITARY_GATES]
+        key = (tuple((i.kind, tuple(i.qubits), tuple(i.params)) for i in insts), tuple(self.pos))
+        plan = self._plans.get(key)
+        if plan is None:
+            plan = self._plan(insts)
+            if len(self._plans) >= 8:
+                self._plans.pop(next(iter(self._plans)))
+            self._plans[key] = plan
+        for act in plan:
+            if act[0] == "gates":
+                self.shard.apply(act[1])
+            else:
+                self.swap_qubits(act[1], act[2])
+
+    def _plan(self, insts) -> list:
+        """Actions [("gates", records) | ("swap", G, L)] from the current layout
+        (the layout itself is left unchanged; replaying the swaps updates it)."""
         mats = [matrix_of(i) for i in insts]
+        pos = list(self.pos)
+
+        def inv_of():
+            inv = [0] * self.n
+            for lq, ph in enumerate(pos):
+                inv[ph] = lq
+            return inv
+
         # per qubit: indices of future non-diagonal uses (for victim choice)
         uses: list[list[int]] = [[] for _ in range(self.n)]
         for t, (inst, m) in enumerate(zip(insts, mats)):
@@ -282,11 +312,12 @@ class ShardedState:
                 if not _preserved(m, k, j):
                     uses[q].append(t)
         nxt = [0] * self.n
+        actions: list = []
         batch: list[np.ndarray] = []
 
         def flush():
             if batch:
-                self.shard.apply(np.concatenate(batch))
+                actions.append(("gates", np.concatenate(batch)))
                 batch.clear()
 
         for t, (inst, m) in enumerate(zip(insts, mats)):
@@ -295,10 +326,10 @@ class ShardedState:
                 while nxt[q] < len(uses[q]) and uses[q][nxt[q]] < t:
                     nxt[q] += 1
             for j, q in enumerate(inst.qubits):
-                if self.pos[q] >= self.nl and not _preserved(m, k, j):
+                if pos[q] >= self.nl and not _preserved(m, k, j):
                     flush()
-                    busy = {self.pos[x] for x in inst.qubits}
-                    inv = self._inv()
+                    busy = {pos[x] for x in inst.qubits}
+                    inv = inv_of()
                     best, best_next = None, -1
                     for L in range(self.nl):
                         if L in busy:
@@ -307,9 +338,12 @@ class ShardedState:
                         nu = uses[lq][nxt[lq]] if nxt[lq] < len(uses[lq]) else 1 << 60
                         if nu > best_next:
                             best, best_next = L, nu
-                    self.swap_qubits(self.pos[q], best)
+                    G = pos[q]
+                    actions.append(("swap", G, best))
+                    a, c = inv[G], inv[best]
+                    pos[a], pos[c] = best, G
             # restrict to this rank's values of preserved global qubits
-            qs = [self.pos[q] for q in inst.qubits]
+            qs = [pos[q] for q in inst.qubits]
             mm = m
             for j in reversed(range(k)):
                 if qs[j] >= self.nl:
@@ -322,6 +356,7 @@ class ShardedState:
                 continue
             batch.append(_gate_rec(qs, mm))
         flush()
+        return actions
 
     # ------------------------------------------------------------ reductions
     def _allreduce(self, x: np.ndarray) -> np.ndarray:
