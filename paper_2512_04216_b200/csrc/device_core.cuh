@@ -676,6 +676,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
@@ -1106,6 +1109,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   __shared__ uint64_t s_ldk[32];
   __shared__ uint32_t s_sdk[32];
   __shared__ uint32_t s_doff[kMaxDiag];  // staged offsets of the uniform DIAG payloads
+  __shared__ uint64_t s_ubar[3];         // one-round direct passes: uniform-slot barriers
   {
     const int4* src = reinterpret_cast<const int4*>(pdg);
     int4* dst = reinterpret_cast<int4*>(&pd);
@@ -1150,8 +1154,15 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.ops = smraw + ring_bytes - pd.ops_begin;  // ops_mode 0 only
   c.uni = uni;
   // uniform slots are double-buffered by tile parity (the next tile's factors
-  // are written while slow warps may still read this tile's)
-  c.pro = uni + 2 * pd.ndiag * kUniStride;
+  // are written while slow warps may still read this tile's).  One-round
+  // direct passes (no ring) triple-buffer them and replace the per-tile CTA
+  // barrier by split arrive/wait mbarriers: each warp evaluates its share of
+  // tile it+1's factors while tile it is in flight and arrives on
+  // s_ubar[(it+1)%3]; a warp waits on s_ubar[it%3] before tile it.  Passing
+  // that wait means every warp has started tile it-1, i.e. finished tile it-2,
+  // whose slot ((it+1)%3) is the one it then overwrites.
+  const bool upipe = stages == 0 && pd.nrounds == 1;
+  c.pro = uni + (upipe ? 3 : 2) * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   (void)nslots;
   double zl[RB + 3];
@@ -1189,6 +1200,10 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.next_base = 0;
   c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
   c.l2next = 0;
+  if (upipe && tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(&s_ubar[i], nwarps);
+    fence_mbar_init();
+  }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < PassCtx<R, RB>::kHoist; ++k) {
@@ -1208,6 +1223,16 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   typename Body::template State<R, RB> bs;
   Body::template prologue<R, RB>(c, bs);
   cplx<R> a[1 << RB];
+  const bool upipe_d = upipe && ndiag > 0;
+  if (upipe) {
+    if (upipe_d && t0 < ntiles) {
+      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, t0, lane), uni,
+                                warp, nwarps, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_ubar[0]);
+    }
+    __syncthreads();  // prologue slots visible
+  }
   int it = 0;
   for (uint32_t t = t0; t < ntiles; t += gridDim.x, ++it) {
     const uint32_t tn = t + gridDim.x;
@@ -1225,6 +1250,21 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
       c.l2next = tn < ntiles;
       if (c.l2next) c.next_base = tile_base_warp(pd, tn, lane);
       Body::template preload<R, RB>(c, a, base);
+    }
+    if (upipe) {
+      if (upipe_d) {
+        const int u = it % 3, un = u == 2 ? 0 : u + 1;
+        mbar_wait(&s_ubar[u], (uint32_t)(it / 3) & 1u);
+        if (tn < ntiles) {
+          diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, tn, lane),
+                                    uni + un * ndiag * kUniStride, warp, nwarps, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_ubar[un]);
+        }
+        c.uni = uni + u * ndiag * kUniStride;
+      }
+      Body::template tile<R, RB>(pass, c, a, ring, base, bs);
+      continue;
     }
     c.uni = uni + (it & 1) * ndiag * kUniStride;
     if (ndiag > 0)  // tile-uniform diagonal factors (before the ring wait: overlaps the copies)
@@ -1276,7 +1316,8 @@ __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int nd
   const uint32_t ring =
       (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
   return ring + ((staged_ops + 15u) & ~15u) +
-         (2u * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) * (uint32_t)sizeof(cplx<R>) +
+         (((stages == 0 && nrounds == 1) ? 3u : 2u) * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) *
+             (uint32_t)sizeof(cplx<R>) +
          0u * (uint32_t)zsum;  // fused <Z> accumulates in global memory (zsum_tile)
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
