@@ -95,6 +95,9 @@ static_assert(sizeof(DiagHdr) == 64, "DiagHdr layout");
 constexpr int kMaxUT = 12;
 // cplx per uniform slot: C, U0[5], U1[5], V[kMaxUT], pad
 constexpr int kUniStride = 24;
+// one-round direct passes: tile-uniform factors are produced kUPipeAhead tiles
+// ahead into a ring of 2 * kUPipeAhead + 1 shared-memory slots (pass_kernel)
+constexpr int kUPipeAhead = 2, kUPipeSlots = 2 * kUPipeAhead + 1;
 constexpr int kUniV = 11;
 
 constexpr int kMaxRounds = 24;
@@ -792,6 +795,7 @@ template <typename R, int RB> struct PassCtx {
   cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
   uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
   double* zl;            // fused <Z>: the thread's running sums [RB + 3] (zsum_tile)
+  double* zsm;           // or (ZSM kernels) in shared memory: [RB + 3][nthr], null otherwise
   const uint8_t* ops;  // op stream rebased onto shared memory
   const cplx<R>* uni;  // tile-uniform diagonal factors (shared memory)
   uint32_t tid;
@@ -966,16 +970,28 @@ __device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>
     for (int i = 0; i < RB; ++i)
       if (v & (1 << i)) s1[i] += pv;
   }
-  double* zl = c.zl;
-  zl[0] += T;
-#pragma unroll
-  for (int i = 0; i < RB; ++i) zl[1 + i] += fma(-2.0, s1[i], T);
   double tw = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
   const uint32_t lane = c.tid & 31u;
-  if ((int)lane < c.pd.nout) zl[RB + 1] += ((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw;
-  if ((int)lane + 32 < c.pd.nout) zl[RB + 2] += ((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw;
+  const double t0 = ((int)lane < c.pd.nout) ? (((base >> c.pd.outpos[lane]) & 1ull) ? -tw : tw) : 0.0;
+  const double t1 = ((int)lane + 32 < c.pd.nout) ? (((base >> c.pd.outpos[lane + 32]) & 1ull) ? -tw : tw) : 0.0;
+  if (c.zsm) {  // shared-memory running sums: no registers held across the tile's ops
+    double* z = c.zsm + c.tid;
+    const uint32_t st = c.nthr;
+    z[0] += T;
+#pragma unroll
+    for (int i = 0; i < RB; ++i) z[(1 + i) * st] += fma(-2.0, s1[i], T);
+    z[(RB + 1) * st] += t0;
+    z[(RB + 2) * st] += t1;
+    return;
+  }
+  double* zl = c.zl;
+  zl[0] += T;
+#pragma unroll
+  for (int i = 0; i < RB; ++i) zl[1 + i] += fma(-2.0, s1[i], T);
+  zl[RB + 1] += t0;
+  zl[RB + 2] += t1;
 }
 
 template <typename R, int RB>
@@ -984,6 +1000,14 @@ __device__ __forceinline__ void zsum_store(const PassCtx<R, RB>& c) {
   double* zs = reinterpret_cast<double*>(c.pd.zacc) + (size_t)blockIdx.x * (RB + 1) * nthr;
   double* zw = reinterpret_cast<double*>(c.pd.zacc) + (size_t)kZaccCols * (RB + 1) * nthr +
                ((size_t)blockIdx.x * (nthr >> 5) + (tid >> 5)) * 64;
+  if (c.zsm) {
+    const double* z = c.zsm + tid;
+#pragma unroll
+    for (int i = 0; i <= RB; ++i) zs[i * nthr + tid] = z[i * nthr];
+    zw[lane] = z[(RB + 1) * nthr];
+    zw[lane + 32] = z[(RB + 2) * nthr];
+    return;
+  }
 #pragma unroll
   for (int i = 0; i <= RB; ++i) zs[i * nthr + tid] = c.zl[i];
   zw[lane] = c.zl[RB + 1];
@@ -1098,7 +1122,7 @@ struct InterpBody {
 // then Body runs the tile's rounds out of shared memory and stores the last
 // layout straight from registers to HBM.
 // Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
-template <typename R, int RB, class Body>
+template <typename R, int RB, class Body, int ZSM = 0>
 __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
                                             const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
@@ -1109,7 +1133,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   __shared__ uint64_t s_ldk[32];
   __shared__ uint32_t s_sdk[32];
   __shared__ uint32_t s_doff[kMaxDiag];  // staged offsets of the uniform DIAG payloads
-  __shared__ uint64_t s_ubar[3];         // one-round direct passes: uniform-slot barriers
+  __shared__ uint64_t s_ubar[kUPipeSlots];  // one-round direct passes: uniform-slot barriers
   {
     const int4* src = reinterpret_cast<const int4*>(pdg);
     int4* dst = reinterpret_cast<int4*>(&pd);
@@ -1155,20 +1179,28 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.uni = uni;
   // uniform slots are double-buffered by tile parity (the next tile's factors
   // are written while slow warps may still read this tile's).  One-round
-  // direct passes (no ring) triple-buffer them and replace the per-tile CTA
-  // barrier by split arrive/wait mbarriers: each warp evaluates its share of
-  // tile it+1's factors while tile it is in flight and arrives on
-  // s_ubar[(it+1)%3]; a warp waits on s_ubar[it%3] before tile it.  Passing
-  // that wait means every warp has started tile it-1, i.e. finished tile it-2,
-  // whose slot ((it+1)%3) is the one it then overwrites.
+  // direct passes (no ring) replace the per-tile CTA barrier by split
+  // arrive/wait mbarriers over a ring of K = 2D + 1 slots (D = kUPipeAhead):
+  // before tile it a warp waits on s_ubar[it%K], then evaluates its share of
+  // tile it+D's factors into slot (it+D)%K and arrives on that slot's barrier.
+  // Passing the wait for tile it means every warp has passed the wait for tile
+  // it-D, i.e. finished tile it-D-1 -- the last user of slot (it+D)%K.  Warps
+  // may drift D tiles apart instead of one.
   const bool upipe = stages == 0 && pd.nrounds == 1;
-  c.pro = uni + (upipe ? 3 : 2) * pd.ndiag * kUniStride;
+  c.pro = uni + (upipe ? kUPipeSlots : 2) * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
-  (void)nslots;
-  double zl[RB + 3];
+  // fused <Z> running sums: registers, or (ZSM) shared memory after the
+  // prologue slots (pass_smem counts them), which frees RB + 3 doubles of
+  // registers across the tile's ops
+  double zl[ZSM ? 1 : RB + 3];
 #pragma unroll
-  for (int i = 0; i < RB + 3; ++i) zl[i] = 0.0;
+  for (int i = 0; i < (ZSM ? 1 : RB + 3); ++i) zl[i] = 0.0;
   c.zl = zl;
+  c.zsm = nullptr;
+  if (ZSM && pd.zsum) {
+    c.zsm = reinterpret_cast<double*>(c.pro + (size_t)nslots * blockDim.x);
+    for (uint32_t i = threadIdx.x; i < (RB + 3) * blockDim.x; i += blockDim.x) c.zsm[i] = 0.0;
+  }
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
@@ -1201,7 +1233,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
   c.l2next = 0;
   if (upipe && tid == 0) {
-    for (int i = 0; i < 3; ++i) mbar_init(&s_ubar[i], nwarps);
+    for (int i = 0; i < kUPipeSlots; ++i) mbar_init(&s_ubar[i], nwarps);
     fence_mbar_init();
   }
   __syncthreads();
@@ -1225,11 +1257,15 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   cplx<R> a[1 << RB];
   const bool upipe_d = upipe && ndiag > 0;
   if (upipe) {
-    if (upipe_d && t0 < ntiles) {
-      diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, t0, lane), uni,
-                                warp, nwarps, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_ubar[0]);
+    if (upipe_d) {
+      for (int d = 0; d < kUPipeAhead; ++d) {
+        const uint32_t td = t0 + (uint32_t)d * gridDim.x;
+        if (td >= ntiles) break;
+        diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, td, lane),
+                                  uni + d * ndiag * kUniStride, warp, nwarps, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_ubar[d]);
+      }
     }
     __syncthreads();  // prologue slots visible
   }
@@ -1253,11 +1289,13 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     if (upipe) {
       if (upipe_d) {
-        const int u = it % 3, un = u == 2 ? 0 : u + 1;
-        mbar_wait(&s_ubar[u], (uint32_t)(it / 3) & 1u);
-        if (tn < ntiles) {
-          diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, tn, lane),
-                                    uni + un * ndiag * kUniStride, warp, nwarps, lane);
+        const int u = it % kUPipeSlots, un = (it + kUPipeAhead) % kUPipeSlots;
+        mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+        const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
+        if (tf < ntiles) {
+          diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
+                                    tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
+                                    nwarps, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_ubar[un]);
         }
@@ -1316,9 +1354,11 @@ __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int nd
   const uint32_t ring =
       (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
   return ring + ((staged_ops + 15u) & ~15u) +
-         (((stages == 0 && nrounds == 1) ? 3u : 2u) * (uint32_t)ndiag * kUniStride + (uint32_t)nslots * nthr) *
+         (((stages == 0 && nrounds == 1) ? (uint32_t)kUPipeSlots : 2u) * (uint32_t)ndiag * kUniStride +
+          (uint32_t)nslots * nthr) *
              (uint32_t)sizeof(cplx<R>) +
-         0u * (uint32_t)zsum;  // fused <Z> accumulates in global memory (zsum_tile)
+         // zsum != 0: a ZSM kernel keeps the fused <Z> running sums in shared memory
+         (zsum ? (uint32_t)(kRegBits<R> + 3) * nthr * (uint32_t)sizeof(double) : 0u);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
 // One-round direct passes of a support-tracked program (the QFT bench's last
@@ -1328,6 +1368,9 @@ __host__ __device__ inline bool direct_one_round(const PassDev& pd) {
   return pd.direct && pd.dmask && pd.nrounds == 1;
 }
 constexpr int kDirectMinBlocks = 3;
+// JIT kernels of one-round direct passes with fused <Z> keep the running sums
+// in shared memory (pass_kernel's ZSM; pass_smem's zsum argument)
+__host__ __device__ inline int zsm_pass(const PassDev& pd) { return direct_one_round(pd) && pd.zsum ? 1 : 0; }
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
 __host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {

@@ -339,13 +339,13 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, pd.zsum);
+    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, 0);
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
-    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, pd.zsum, pd.nrounds), st>>>(
+    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, 0, pd.nrounds), st>>>(
         state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);

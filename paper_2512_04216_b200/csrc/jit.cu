@@ -649,7 +649,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody>(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
+    << RB << ", PassBody, " << zsm_pass(pd0) << ">(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
     << pc.nslots << ");\n}\n";
   return o.str();
 }
@@ -743,7 +743,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
           staged[p] += h.bytes - (uint32_t)sizeof(OpHdr);
         }
       }
-      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2, pd.zsum) > kSmemMaxPerCTA) return false;
+      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
@@ -814,11 +814,11 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p], pd.zsum);
+    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p], zsm_pass(pd));
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
-    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, pd.zsum, pd.nrounds);
+    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
     int per_sm = stages <= 1 ? kPassMinBlocks<R> : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
         (uint64_t)kDirectMinBlocks * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
@@ -878,6 +878,10 @@ extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng
       Program p = build_program<double>(n, gates, ng, o);
       if (zsum && !p.passes.empty()) p.passes.back().zsum = 1;
       for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<double>(p, (int)k, nullptr, nullptr));
+      if (std::getenv("SVB_TRACE"))
+        for (const PassDev& pd : p.passes)
+          std::fprintf(stderr, "[svb] jit_check pass: m=%d rounds=%d ndiag=%d nitems=%d ops_bytes=%u dmask=%llx\n", pd.m,
+                       pd.nrounds, pd.ndiag, pd.nitems, pd.ops_bytes, (unsigned long long)pd.dmask);
     } else {
       Program p = build_program<float>(n, gates, ng, o);
       if (zsum && !p.passes.empty()) p.passes.back().zsum = 1;
