@@ -6,6 +6,9 @@
 #ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#ifndef __CUDACC_RTC__
+#include <cstdlib>
+#endif
 #else
 typedef unsigned long long uint64_t;
 typedef long long int64_t;
@@ -97,7 +100,15 @@ constexpr int kMaxUT = 12;
 constexpr int kUniStride = 24;
 // one-round direct passes: tile-uniform factors are produced kUPipeAhead tiles
 // ahead into a ring of 2 * kUPipeAhead + 1 shared-memory slots (pass_kernel)
-constexpr int kUPipeAhead = 2, kUPipeSlots = 2 * kUPipeAhead + 1;
+// (SVB_UPIPE_AHEAD: experiments; the JIT defines it from the environment)
+#ifndef SVB_UPIPE_AHEAD
+#define SVB_UPIPE_AHEAD 1
+#endif
+// SVB_UWAIT_FIRST: wait for the tile's uniform slot before issuing its loads
+#ifndef SVB_UWAIT_FIRST
+#define SVB_UWAIT_FIRST 0
+#endif
+constexpr int kUPipeAhead = SVB_UPIPE_AHEAD, kUPipeSlots = 2 * kUPipeAhead + 1;
 constexpr int kUniV = 11;
 
 constexpr int kMaxRounds = 24;
@@ -1279,6 +1290,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
     if (pd.perm_out) c.pbase = tile_base_warp(pd, t, lane, true);
+    const int u = it % kUPipeSlots;
+    if (SVB_UWAIT_FIRST && upipe_d) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
     if (stages == 0) {
       // direct first round: issue the tile's HBM loads (and the next tile's L2
       // prefetches) before the uniform factors and the barrier, so their
@@ -1289,8 +1302,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     if (upipe) {
       if (upipe_d) {
-        const int u = it % kUPipeSlots, un = (it + kUPipeAhead) % kUPipeSlots;
-        mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+        const int un = (it + kUPipeAhead) % kUPipeSlots;
+        if (!SVB_UWAIT_FIRST) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
         const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
         if (tf < ntiles) {
           diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
@@ -1347,6 +1360,18 @@ template <typename R> inline double pass_hbm_bytes(const PassDev& pd, bool zin) 
 }
 #endif
 
+// host: the uniform-slot ring depth the JIT kernels are compiled with
+__host__ __device__ inline int upipe_slots() {
+#if defined(__CUDA_ARCH__) || defined(__CUDACC_RTC__)
+  return kUPipeSlots;
+#else
+  static const int k = [] {
+    const char* e = std::getenv("SVB_UPIPE_AHEAD");
+    return e ? 2 * std::atoi(e) + 1 : kUPipeSlots;
+  }();
+  return k;
+#endif
+}
 template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
                                               int zsum = 0, int nrounds = 2) {
@@ -1354,7 +1379,7 @@ __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int nd
   const uint32_t ring =
       (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
   return ring + ((staged_ops + 15u) & ~15u) +
-         (((stages == 0 && nrounds == 1) ? (uint32_t)kUPipeSlots : 2u) * (uint32_t)ndiag * kUniStride +
+         (((stages == 0 && nrounds == 1) ? (uint32_t)upipe_slots() : 2u) * (uint32_t)ndiag * kUniStride +
           (uint32_t)nslots * nthr) *
              (uint32_t)sizeof(cplx<R>) +
          // zsum != 0: a ZSM kernel keeps the fused <Z> running sums in shared memory
@@ -1368,6 +1393,16 @@ __host__ __device__ inline bool direct_one_round(const PassDev& pd) {
   return pd.direct && pd.dmask && pd.nrounds == 1;
 }
 constexpr int kDirectMinBlocks = 3;
+#ifndef __CUDACC_RTC__
+// CTAs per SM of one-round direct c128 passes (SVB_DIRECT_MINB: experiments)
+inline int direct_min_blocks() {
+  static const int k = [] {
+    const char* e = std::getenv("SVB_DIRECT_MINB");
+    return e ? std::atoi(e) : kDirectMinBlocks;
+  }();
+  return k;
+}
+#endif
 // JIT kernels of one-round direct passes with fused <Z> keep the running sums
 // in shared memory (pass_kernel's ZSM; pass_smem's zsum argument)
 __host__ __device__ inline int zsm_pass(const PassDev& pd) { return direct_one_round(pd) && pd.zsum ? 1 : 0; }

@@ -595,7 +595,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     int dev = 0, nsm = 148;
     SVB_CUDA(cudaGetDevice(&dev));
     SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const uint64_t ncta = std::min<uint64_t>(1ull << lp.nout, (uint64_t)nsm * kDirectMinBlocks);  // upper bound
+    const uint64_t ncta = std::min<uint64_t>(1ull << lp.nout, (uint64_t)nsm * std::max(kDirectMinBlocks, direct_min_blocks()));  // upper bound
     const unsigned nv = (unsigned)z->logical.size();
     double* partial = z->d_out + kZaccRows;
     k_zsum_finish<<<dim3(nv, kZsumSlices), 256, 0, st>>>(z->d_acc, (uint32_t)ncta, 1u << (lp.m - lp.rb), lp.rb,

@@ -582,6 +582,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (nslots) *nslots = pc.nslots;
   if (imm_out) *imm_out = imm;
   std::ostringstream o;
+  if (const char* e = std::getenv("SVB_UPIPE_AHEAD")) o << "#define SVB_UPIPE_AHEAD " << std::atoi(e) << "\n";
+  if (const char* e = std::getenv("SVB_UWAIT_FIRST")) o << "#define SVB_UWAIT_FIRST " << std::atoi(e) << "\n";
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
   // tile loads with the layout's offsets as immediates (see issue_tile)
   std::ostringstream iss;
@@ -643,7 +645,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   const size_t at = b.find(from);
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? kDirectMinBlocks : kPassMinBlocks<R>;
+  const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? direct_min_blocks() : kPassMinBlocks<R>;
   o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << minb
     << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
@@ -821,8 +823,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
     int per_sm = stages <= 1 ? kPassMinBlocks<R> : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
-        (uint64_t)kDirectMinBlocks * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
-      per_sm = kDirectMinBlocks;
+        (uint64_t)direct_min_blocks() * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
+      per_sm = direct_min_blocks();
     const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * per_sm);
     static const bool trace = std::getenv("SVB_TRACE") != nullptr;
     if (trace)
@@ -833,7 +835,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
       throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
     // three-CTA one-round passes use little shared memory: leave L1 room for their spills
-    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, per_sm == kDirectMinBlocks ? 60 : 100);
+    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, per_sm == direct_min_blocks() ? 60 : 100);
     cplx<R>* s = state;
     cplx<R>* so = pd.perm_out ? out : state;
     const PassDev* pdp = dpass + p;
