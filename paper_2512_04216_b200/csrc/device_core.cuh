@@ -108,7 +108,12 @@ constexpr int kUniStride = 24;
 #ifndef SVB_UWAIT_FIRST
 #define SVB_UWAIT_FIRST 0
 #endif
-constexpr int kUPipeAhead = SVB_UPIPE_AHEAD, kUPipeSlots = 2 * kUPipeAhead + 1;
+// SVB_UIN: the JIT body waits for the tile's slot before its first uniform
+// factor (pass_kernel's UIN; needs one more slot).  Measured slower: off.
+#ifndef SVB_UIN
+#define SVB_UIN 0
+#endif
+constexpr int kUPipeAhead = SVB_UPIPE_AHEAD, kUPipeSlots = 2 * kUPipeAhead + 1 + (SVB_UIN ? 1 : 0);
 constexpr int kUniV = 11;
 
 constexpr int kMaxRounds = 24;
@@ -824,6 +829,12 @@ template <typename R, int RB> struct PassCtx {
   int prefetch, zero_input;
   int direct;  // round 0 loads straight from HBM into registers (no ring)
   int l2next;  // direct: the next tile exists (next_base); round 0 prefetches its live data into L2
+  // uniform-slot sync inside the body (UIN kernels, upipe_sync): the tile's
+  // slot wait and the production of tile it+D's factors run where the JIT
+  // body first needs a uniform factor, after the ops that need none
+  int usync;              // this tile's slot wait is the body's (0: done by the loop)
+  uint32_t uslot;         // wait slot | parity << 16
+  uint64_t* ubar;         // the slot barriers (shared memory)
   __device__ PassCtx(const PassDev& p) : pd(p) {}
 };
 
@@ -1123,6 +1134,13 @@ struct InterpBody {
   }
 };
 
+// The tile's uniform-slot wait (UIN kernels, see pass_kernel), placed by the
+// JIT right before the body's first tile-uniform factor.
+template <typename R, int RB>
+__device__ __forceinline__ void upipe_sync(const PassCtx<R, RB>& c) {
+  if (c.usync) mbar_wait(&c.ubar[c.uslot & 0xffu], (c.uslot >> 16) & 1u);
+}
+
 // Persistent fused pass: each CTA walks tiles blockIdx.x, +gridDim.x, ...
 // Tiles stream HBM -> shared memory with cp.async (LDGSTS, 16 B per thread,
 // lanes on consecutive amplitudes: 512 B per warp request) into an
@@ -1133,7 +1151,7 @@ struct InterpBody {
 // then Body runs the tile's rounds out of shared memory and stores the last
 // layout straight from registers to HBM.
 // Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
-template <typename R, int RB, class Body, int ZSM = 0>
+template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0>
 __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
                                             const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
@@ -1243,6 +1261,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   c.next_base = 0;
   c.direct = stages == 0;  // launch chose the direct first round (pd.direct, single stage)
   c.l2next = 0;
+  c.usync = 0;
+  c.uslot = 0;
+  c.ubar = s_ubar;
   if (upipe && tid == 0) {
     for (int i = 0; i < kUPipeSlots; ++i) mbar_init(&s_ubar[i], nwarps);
     fence_mbar_init();
@@ -1292,6 +1313,24 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (pd.perm_out) c.pbase = tile_base_warp(pd, t, lane, true);
     const int u = it % kUPipeSlots;
     if (SVB_UWAIT_FIRST && upipe_d) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+    if (UIN && upipe_d) {
+      // produce tile it+D's factors first (registers are free between tiles);
+      // the body waits for tile it's slot where it first needs it.  Starting
+      // iteration it means this warp passed the wait for tile it-1, i.e. every
+      // warp has finished tile it-D-2, the last user of slot (it+D)%K when
+      // K = 2D + 2
+      const int un = (it + kUPipeAhead) % kUPipeSlots;
+      const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
+      if (tf < ntiles) {
+        diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
+                                  tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
+                                  nwarps, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_ubar[un]);
+      }
+      c.usync = 1;
+      c.uslot = (uint32_t)u | (((uint32_t)(it / kUPipeSlots) & 1u) << 16);
+    }
     if (stages == 0) {
       // direct first round: issue the tile's HBM loads (and the next tile's L2
       // prefetches) before the uniform factors and the barrier, so their
@@ -1303,9 +1342,9 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (upipe) {
       if (upipe_d) {
         const int un = (it + kUPipeAhead) % kUPipeSlots;
-        if (!SVB_UWAIT_FIRST) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
         const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
-        if (tf < ntiles) {
+        if (!SVB_UWAIT_FIRST && !UIN) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+        if (!UIN && tf < ntiles) {
           diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
                                     tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
                                     nwarps, lane);
@@ -1367,7 +1406,9 @@ __host__ __device__ inline int upipe_slots() {
 #else
   static const int k = [] {
     const char* e = std::getenv("SVB_UPIPE_AHEAD");
-    return e ? 2 * std::atoi(e) + 1 : kUPipeSlots;
+    const char* ui = std::getenv("SVB_UIN");
+    const int extra = ui ? (std::atoi(ui) != 0 ? 1 : 0) : (SVB_UIN ? 1 : 0);
+    return (e ? 2 * std::atoi(e) : 2 * SVB_UPIPE_AHEAD) + 1 + extra;
   }();
   return k;
 #endif
@@ -1406,6 +1447,13 @@ inline int direct_min_blocks() {
 // JIT kernels of one-round direct passes with fused <Z> keep the running sums
 // in shared memory (pass_kernel's ZSM; pass_smem's zsum argument)
 __host__ __device__ inline int zsm_pass(const PassDev& pd) { return direct_one_round(pd) && pd.zsum ? 1 : 0; }
+// ... and (SVB_UIN=1, measured slower) wait for the uniform slot inside the body
+#ifndef __CUDACC_RTC__
+inline bool uin_pass(const PassDev& pd) {  // host (JIT generation); SVB_UIN=0: sync in the loop
+  if (const char* e = std::getenv("SVB_UIN")) return std::atoi(e) != 0 && direct_one_round(pd);
+  return SVB_UIN && direct_one_round(pd);
+}
+#endif
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
 __host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {

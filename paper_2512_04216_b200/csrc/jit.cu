@@ -364,6 +364,10 @@ template <typename R>
 void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool imm, PrologueCtx& pc) {
   const PassDev& pd = prog.passes[p];
   o << "    case " << p << ": {\n";
+  // one-round direct passes: the uniform-slot sync (upipe_sync) goes right
+  // before the first op that reads a tile-uniform factor
+  const bool uin = uin_pass(pd);
+  bool usynced = false;
   for (int k = 0; k < pd.nrounds; ++k) {
     const RoundDev& rd = pd.rounds[k];
     o << "    // round " << k << "\n"
@@ -439,6 +443,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       const std::string cond = h.rmask ? "true" : "false";
       const std::string rm = std::to_string(h.rmask) + "u, " + std::to_string(h.rval) + "u";
       if (h.kind != OP_U1P && h.kind != OP_U1PR) zm = 0;  // zero tracking covers leading pivot ops only
+      const std::streampos mark = o.tellp();
       switch (h.kind) {
         case OP_DIAG:
           pc.round = k;
@@ -530,6 +535,19 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
           throw Error(SVB_E_CUDA, "jit: unknown op kind");
       }
       off += h.bytes;
+      if (uin && !usynced) {
+        std::string all = o.str();
+        if (all.find("c.uni", (size_t)mark) != std::string::npos) {
+          all.insert((size_t)mark, "    svb::upipe_sync<R, RB>(c);\n");
+          o.str(all);
+          o.seekp(0, std::ios::end);
+          usynced = true;
+        }
+      }
+    }
+    if (uin && !usynced && k + 1 == pd.nrounds) {
+      o << "    svb::upipe_sync<R, RB>(c);\n";
+      usynced = true;
     }
     if (k + 1 == pd.nrounds && pd.zsum) o << "    svb::zsum_tile<R, RB>(c, a, base);\n";
     if (k + 1 < pd.nrounds) {
@@ -584,6 +602,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   std::ostringstream o;
   if (const char* e = std::getenv("SVB_UPIPE_AHEAD")) o << "#define SVB_UPIPE_AHEAD " << std::atoi(e) << "\n";
   if (const char* e = std::getenv("SVB_UWAIT_FIRST")) o << "#define SVB_UWAIT_FIRST " << std::atoi(e) << "\n";
+  if (const char* e = std::getenv("SVB_UIN")) o << "#define SVB_UIN " << (std::atoi(e) != 0 ? 1 : 0) << "\n";
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
   // tile loads with the layout's offsets as immediates (see issue_tile)
   std::ostringstream iss;
@@ -651,7 +670,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody, " << zsm_pass(pd0) << ">(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
+    << RB << ", PassBody, " << zsm_pass(pd0) << ", " << (uin_pass(pd0) ? 1 : 0) << ">(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
     << pc.nslots << ");\n}\n";
   return o.str();
 }
