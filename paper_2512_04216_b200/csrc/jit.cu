@@ -850,11 +850,18 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       std::fprintf(stderr, "[svb] jit pass %zu: m=%d rounds=%d stages=%d grid=%u smem=%u staged=%u ndiag=%d slots=%d\n",
                    p, pd.m, pd.nrounds, stages, grid, smem, staged[p], pd.ndiag, nslots[p]);
     CUfunction f = fns[p];
-    // per-function attribute: always the maximum (no race between threads)
-    if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
-      throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
+    // per-function attributes, set once per (function, carveout) and thread:
+    // the shared memory limit is always the maximum (no race between threads);
     // three-CTA one-round passes use little shared memory: leave L1 room for their spills
-    dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, per_sm == direct_min_blocks() ? 60 : 100);
+    const int carve = per_sm == direct_min_blocks() ? 60 : 100;
+    thread_local std::unordered_map<CUfunction, int> configured;
+    auto cf = configured.find(f);
+    if (cf == configured.end() || cf->second != carve) {
+      if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
+        throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
+      dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carve);
+      configured[f] = carve;
+    }
     cplx<R>* s = state;
     cplx<R>* so = pd.perm_out ? out : state;
     const PassDev* pdp = dpass + p;
