@@ -113,7 +113,13 @@ constexpr int kUniStride = 24;
 #ifndef SVB_UIN
 #define SVB_UIN 0
 #endif
+// SVB_UGROUP: tiles per ring slot (one wait + one arrive per group of tiles;
+// the default loop path only)
+#ifndef SVB_UGROUP
+#define SVB_UGROUP 1
+#endif
 constexpr int kUPipeAhead = SVB_UPIPE_AHEAD, kUPipeSlots = 2 * kUPipeAhead + 1 + (SVB_UIN ? 1 : 0);
+constexpr int kUGroup = SVB_UGROUP;
 constexpr int kUniV = 11;
 
 constexpr int kMaxRounds = 24;
@@ -1216,7 +1222,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // it-D, i.e. finished tile it-D-1 -- the last user of slot (it+D)%K.  Warps
   // may drift D tiles apart instead of one.
   const bool upipe = stages == 0 && pd.nrounds == 1;
-  c.pro = uni + (upipe ? kUPipeSlots : 2) * pd.ndiag * kUniStride;
+  c.pro = uni + (upipe ? kUPipeSlots * kUGroup : 2) * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   // fused <Z> running sums: registers, or (ZSM) shared memory after the
   // prologue slots (pass_smem counts them), which frees RB + 3 doubles of
@@ -1291,10 +1297,14 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   if (upipe) {
     if (upipe_d) {
       for (int d = 0; d < kUPipeAhead; ++d) {
-        const uint32_t td = t0 + (uint32_t)d * gridDim.x;
-        if (td >= ntiles) break;
-        diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems, tile_base_warp(pd, td, lane),
-                                  uni + d * ndiag * kUniStride, warp, nwarps, lane);
+        if (t0 + (uint64_t)d * kUGroup * gridDim.x >= ntiles) break;
+        for (int g = 0; g < kUGroup; ++g) {
+          const uint64_t td = t0 + (uint64_t)(d * kUGroup + g) * gridDim.x;
+          if (td >= ntiles) break;
+          diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
+                                    tile_base_warp(pd, (uint32_t)td, lane),
+                                    uni + (d * kUGroup + g) * ndiag * kUniStride, warp, nwarps, lane);
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_ubar[d]);
       }
@@ -1341,17 +1351,39 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     }
     if (upipe) {
       if (upipe_d) {
-        const int un = (it + kUPipeAhead) % kUPipeSlots;
-        const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
-        if (!SVB_UWAIT_FIRST && !UIN) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
-        if (!UIN && tf < ntiles) {
-          diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
-                                    tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
-                                    nwarps, lane);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&s_ubar[un]);
+        if (kUGroup > 1 && !UIN && !SVB_UWAIT_FIRST) {
+          // groups of kUGroup tiles per slot: group P = it / G waits once and
+          // produces group P + D (same ring argument with groups as units)
+          const int P = it / kUGroup, gi = it % kUGroup, ug = P % kUPipeSlots;
+          if (gi == 0) {
+            const int ung = (P + kUPipeAhead) % kUPipeSlots;
+            mbar_wait(&s_ubar[ug], (uint32_t)(P / kUPipeSlots) & 1u);
+            if ((uint64_t)t + (uint64_t)kUPipeAhead * kUGroup * gridDim.x < ntiles) {
+              for (int g = 0; g < kUGroup; ++g) {
+                const uint64_t tf = (uint64_t)t + (uint64_t)(kUPipeAhead * kUGroup + g) * gridDim.x;
+                if (tf >= ntiles) break;
+                diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
+                                          tile_base_warp(pd, (uint32_t)tf, lane),
+                                          uni + (ung * kUGroup + g) * ndiag * kUniStride, warp, nwarps, lane);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&s_ubar[ung]);
+            }
+          }
+          c.uni = uni + (ug * kUGroup + gi) * ndiag * kUniStride;
+        } else {
+          const int un = (it + kUPipeAhead) % kUPipeSlots;
+          const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
+          if (!SVB_UWAIT_FIRST && !UIN) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+          if (!UIN && tf < ntiles) {
+            diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
+                                      tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
+                                      nwarps, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_ubar[un]);
+          }
+          c.uni = uni + u * ndiag * kUniStride;
         }
-        c.uni = uni + u * ndiag * kUniStride;
       }
       Body::template tile<R, RB>(pass, c, a, ring, base, bs);
       continue;
@@ -1408,7 +1440,9 @@ __host__ __device__ inline int upipe_slots() {
     const char* e = std::getenv("SVB_UPIPE_AHEAD");
     const char* ui = std::getenv("SVB_UIN");
     const int extra = ui ? (std::atoi(ui) != 0 ? 1 : 0) : (SVB_UIN ? 1 : 0);
-    return (e ? 2 * std::atoi(e) : 2 * SVB_UPIPE_AHEAD) + 1 + extra;
+    const char* gr = std::getenv("SVB_UGROUP");
+    const int group = gr ? (std::atoi(gr) > 1 ? std::atoi(gr) : 1) : SVB_UGROUP;
+    return ((e ? 2 * std::atoi(e) : 2 * SVB_UPIPE_AHEAD) + 1 + extra) * group;  // slots x tiles per slot
   }();
   return k;
 #endif
