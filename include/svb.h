@@ -125,6 +125,12 @@ int svb_marginal_probs(svb_handle h, const int32_t* qubits, int k, double* out);
 /* <Z_mask> for M masks in one pass over the state (expectation, statevector.py:277-292). */
 int svb_expect_z(svb_handle h, const uint64_t* masks, int m, double* out);
 
+/* Distance and overlap of two states of the same size on the same device
+ * (either precision): out[5] = {sum|a-b|^2, sum|a|^2, sum|b|^2, Re<a|b>,
+ * Im<a|b>}.  State fidelity |<a|b>|^2 as in metrics.mirror_fidelity
+ * (metrics.py:33-56), and the device-side parity check of large states. */
+int svb_compare(svb_handle a, svb_handle b, double* out);
+
 /* Terminal sampling (statevector.py:213-216 + result.py:50-82 + sampling.py:30-83).
  *   qubits[k]      ascending measured qubits;
  *   bit_src[w]     for output bit p (clbit rank p): bit index into the marginal index;
@@ -144,6 +150,12 @@ int svb_alias_table(int device, const double* probs, uint64_t m, double* prob_ro
  * m must be a power of two (a marginal).  out_idx[shots]: outcome indices. */
 int svb_alias_draw(int device, const double* probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
                    uint64_t* out_idx);
+
+/* AliasTable.sample_indices(rng, shots) (sampling.py:78-83) for a table
+ * already built (prob_row/alias_row as svb_alias_table returns; any m): the
+ * next `shots` doubles of the numpy PCG64 state pcg[4], one per draw. */
+int svb_alias_sample(int device, const double* prob_row, const int64_t* alias_row, uint64_t m, uint64_t shots,
+                     const uint64_t* pcg, uint64_t* out_idx);
 
 /* Sharded mode (global<->local qubit swaps, svb_dist in sharded.py):
  * raw device pointer of the state (synchronised), and gather/scatter of the

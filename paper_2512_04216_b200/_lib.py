@@ -68,6 +68,7 @@ _SIGS = {
     "svb_apply_z": (c_int, [_h, c_void_p, c_int, _i32p, c_int, _dp]),
     "svb_marginal_probs": (c_int, [_h, _i32p, c_int, _dp]),
     "svb_expect_z": (c_int, [_h, _u64p, c_int, _dp]),
+    "svb_compare": (c_int, [_h, _h, _dp]),
     "svb_sample": (c_int, [_h, _i32p, c_int, _i32p, c_int, c_uint64, _u64p, c_int, _u64p, _u64p, _u64p]),
     "svb_alias_table": (c_int, [c_int, _dp, c_uint64, _dp, _i64p]),
     "svb_rng_seed": (c_int, [_h, _u64p]),
@@ -79,6 +80,7 @@ _SIGS = {
     "svb_outer": (c_int, [_h, _h, _h]),
     "svb_permute_qubits": (c_int, [_h, POINTER(c_int32)]),
     "svb_select_half": (c_int, [_h, _h, c_int, c_int]),
+    "svb_alias_sample": (c_int, [c_int, _dp, _i64p, c_uint64, c_uint64, _u64p, _u64p]),
     "svb_alias_draw": (c_int, [c_int, _dp, c_uint64, c_uint64, POINTER(c_uint64), POINTER(c_uint64)]),
     "svb_sample_slice": (c_int, [_h, c_uint64, _u64p, c_double, c_double, c_double, _i32p, c_int, c_uint64, _u64p,
                                  _u64p, _u64p]),

@@ -464,6 +464,26 @@ int svb_expect_z(svb_handle h, const uint64_t* masks, int m, double* out) {
   });
 }
 
+int svb_compare(svb_handle a, svb_handle b, double* out) {
+  return guard([&] {
+    check_handle(b);
+    check_handle(a);
+    require(a->n == b->n && a->device == b->device, SVB_E_ARG, "states differ in size or device");
+    SVB_CUDA(cudaStreamSynchronize(b->st));
+    ensure_ws(a, compare_ws_doubles(a->n));
+    double* d_out = nullptr;
+    SVB_CUDA(cudaMallocAsync(&d_out, 5 * sizeof(double), a->st));
+    const bool a2 = a->prec == SVB_C128, b2 = b->prec == SVB_C128;
+    if (a2 && b2) launch_compare<double, double>(a->amps, b->amps, a->n, a->d_ws, d_out, a->st);
+    else if (a2) launch_compare<double, float>(a->amps, b->amps, a->n, a->d_ws, d_out, a->st);
+    else if (b2) launch_compare<float, double>(a->amps, b->amps, a->n, a->d_ws, d_out, a->st);
+    else launch_compare<float, float>(a->amps, b->amps, a->n, a->d_ws, d_out, a->st);
+    SVB_CUDA(cudaMemcpyAsync(out, d_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, a->st));
+    SVB_CUDA(cudaFreeAsync(d_out, a->st));
+    SVB_CUDA(cudaStreamSynchronize(a->st));
+  });
+}
+
 int svb_sample(svb_handle h, const int32_t* qubits, int k, const int32_t* bit_src, int w, uint64_t shots,
                const uint64_t* pcg, int sampler, uint64_t* out_codes, uint64_t* out_counts,
                uint64_t* n_unique) {
@@ -581,6 +601,46 @@ int svb_alias_draw(int device, const double* probs, uint64_t m, uint64_t shots, 
       SVB_CUDA(cudaMallocAsync(&dc, shots * sizeof(uint64_t), st));
       SVB_CUDA(cudaMemcpyAsync(dp, probs, m * sizeof(double), cudaMemcpyHostToDevice, st));
       alias_build(dp, m, dr, da, st);
+      alias_draw(dr, da, m, shots, pcg, ident.data(), w, dc, st);
+      SVB_CUDA(cudaMemcpyAsync(out_idx, dc, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      SVB_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+// AliasTable.sample_indices (sampling.py:78-83) for a table already built
+// (any m): v = u*m, idx = floor(v), idx if v - idx < prob[idx] else alias[idx],
+// with u the next `shots` doubles of the numpy PCG64 state pcg[4].
+int svb_alias_sample(int device, const double* prob_row, const int64_t* alias_row, uint64_t m, uint64_t shots,
+                     const uint64_t* pcg, uint64_t* out_idx) {
+  return guard([&] {
+    require(m >= 1 && m <= (1ull << 40), SVB_E_ARG, "alias_sample: bad table size");
+    require(shots >= 1, SVB_E_ARG, "shots must be positive");
+    SVB_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    SVB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double* dr = nullptr;
+    int64_t* da = nullptr;
+    uint64_t* dc = nullptr;
+    int w = 0;
+    while ((1ull << w) < m) ++w;
+    std::vector<int32_t> ident(64);
+    for (int p = 0; p < 64; ++p) ident[p] = p;
+    auto cleanup = [&] {
+      cudaFreeAsync(dr, st); cudaFreeAsync(da, st); cudaFreeAsync(dc, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    };
+    try {
+      SVB_CUDA(cudaMallocAsync(&dr, m * sizeof(double), st));
+      SVB_CUDA(cudaMallocAsync(&da, m * sizeof(int64_t), st));
+      SVB_CUDA(cudaMallocAsync(&dc, shots * sizeof(uint64_t), st));
+      SVB_CUDA(cudaMemcpyAsync(dr, prob_row, m * sizeof(double), cudaMemcpyHostToDevice, st));
+      SVB_CUDA(cudaMemcpyAsync(da, alias_row, m * sizeof(int64_t), cudaMemcpyHostToDevice, st));
       alias_draw(dr, da, m, shots, pcg, ident.data(), w, dc, st);
       SVB_CUDA(cudaMemcpyAsync(out_idx, dc, shots * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       SVB_CUDA(cudaStreamSynchronize(st));
@@ -734,6 +794,10 @@ int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops
       int kind = ops[3 * i];
       require(kind >= 0 && kind <= 2, SVB_E_ARG, "bad replay op");
       if (kind == 0) ngates = std::max(ngates, ops[3 * i + 1] + 1);
+      if (kind == 1) {  // one shot's clbits are packed into a uint64 code
+        const int r = clbit_rank[ops[3 * i + 2]];
+        require(r >= 0 && r < 64, SVB_E_ARG, "replay: clbit rank must be in [0, 64)");
+      }
     }
     validate_gates(work, gates, ngates);
     uint64_t* d_codes = nullptr;

@@ -364,6 +364,8 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
     int M = 0;
     for (int k = 0; k < nops; ++k) {
       require(ops[3 * k] >= 0 && ops[3 * k] <= 2, SVB_E_ARG, "bad replay op");
+      require(ops[3 * k] != 1 || (ops[3 * k + 2] >= 0 && ops[3 * k + 2] < 64), SVB_E_ARG,
+              "replay: clbit rank must be in [0, 64)");
       if (ops[3 * k] != 0) ++M;
       else require(ops[3 * k + 1] >= 0 && ops[3 * k + 1] < ngates, SVB_E_ARG, "bad gate index");
     }

@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -50,6 +52,20 @@ inline cudaError_t state_malloc(void** p, size_t bytes) {
   }
   cudaGetLastError();
   return cudaMalloc(p, bytes);
+}
+
+// Function attributes (max dynamic shared memory, carveout) are per device:
+// run `f` once for each device this process launches on.
+template <class F> inline void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 inline int grid_for(uint64_t work, int block, int max_blocks = 148 * 16) {

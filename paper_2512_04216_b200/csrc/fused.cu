@@ -319,11 +319,11 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     SVB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp,
                              cudaMemcpyHostToDevice, st));
   }
-  // the attribute is per function and process-wide: set it once to the largest
-  // size any program can request (a per-call value would race between threads
-  // launching different programs)
-  static std::once_flag once_pass;
-  std::call_once(once_pass, [] {
+  // the attribute is per function and device: set it once per device to the
+  // largest size any program can request (a per-call value would race between
+  // threads launching different programs)
+  static std::atomic<uint64_t> once_pass{0};
+  once_per_device(once_pass, [] {
     cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxPerCTA);
     cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   });
@@ -366,16 +366,16 @@ static void launch_permute(cplx<R>** state, cplx<R>** spare, int n, const std::v
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   const size_t smem = sizeof(cplx<R>) << pd.ml;
-  static std::once_flag once_perm;
-  std::call_once(once_perm, [] {
+  static std::atomic<uint64_t> once_perm{0};
+  once_per_device(once_perm, [] {
     cudaFuncSetAttribute(k_permute<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(cplx<R>) << 12));
   });
   Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
   if (pf) pf->begin(st, 1, 2.0 * (double)bytes);
   if constexpr (sizeof(R) == 8) {
     if (pd.ml == 12) {
-      static std::once_flag once_pipe;
-      std::call_once(once_pipe, [] {
+      static std::atomic<uint64_t> once_pipe{0};
+      once_per_device(once_pipe, [] {
         cudaFuncSetAttribute(k_permute_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4096 * 16);
       });
       const unsigned g1 = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm);

@@ -17,11 +17,13 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <shared_mutex>
 #include <sstream>
 #include <thread>
 #include <string>
@@ -70,6 +72,7 @@ struct Driver {
   CUresult (*load)(CUmodule*, const void*) = nullptr;
   CUresult (*getfn)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*setattr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*unload)(CUmodule) = nullptr;
   CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
                      void**, void**) = nullptr;
   bool ok = false;
@@ -80,7 +83,8 @@ struct Driver {
              q == cudaDriverEntryPointSuccess && *fn;
     };
     ok = get("cuModuleLoadData", (void**)&load) && get("cuModuleGetFunction", (void**)&getfn) &&
-         get("cuFuncSetAttribute", (void**)&setattr) && get("cuLaunchKernel", (void**)&launch);
+         get("cuFuncSetAttribute", (void**)&setattr) && get("cuLaunchKernel", (void**)&launch) &&
+         get("cuModuleUnload", (void**)&unload);
     if (!ok) cudaGetLastError();
   }
 };
@@ -88,10 +92,20 @@ struct Driver {
 struct Module {
   CUmodule mod = nullptr;
   std::vector<CUfunction> fns;
+  uint64_t last_use = 0;
 };
 
 std::mutex g_mu;
 std::unordered_map<std::string, Module> g_cache;  // key: device + source
+uint64_t g_tick = 0;  // LRU clock (under g_mu)
+// Bounds of the in-memory caches: programs whose coefficients are compiled in
+// as immediates (n >= 28) make a new kernel per angle set, so a parameter
+// sweep would otherwise grow them (and the loaded modules) without limit.
+constexpr size_t kMaxModules = 768, kMaxPrograms = 256;
+// Launchers hold it shared from the cache lookup to the last launch; module
+// eviction holds it exclusively (and synchronises the device) before
+// cuModuleUnload, so no function of an unloaded module is ever launched.
+std::shared_mutex g_launch_mu;
 // Whole programs seen before: their kernels and launch parameters, keyed by a
 // 128-bit hash of the encoded program (passes + op stream), so repeated
 // applies skip source generation (tens of ms of host time the GPU would idle).
@@ -99,6 +113,7 @@ struct ProgKernels {
   std::vector<CUfunction> fns;
   std::vector<int> nslots;
   std::vector<uint32_t> staged;
+  uint64_t last_use = 0;
 };
 struct Key128 {
   uint64_t a, b;
@@ -141,7 +156,21 @@ std::string hexf(double x, bool single) {
   if (single) std::snprintf(buf, sizeof buf, "%af", (double)(float)x);
   else std::snprintf(buf, sizeof buf, "%a", x);
   std::string s(buf);
-  if (s == "inf" || s == "-inf" || s == "nan" || s == "-nan" || s == "inff" || s == "-inff") return "0";
+  if (!std::isfinite(single ? (double)(float)x : x)) {
+    // non-finite coefficients keep their bit pattern (inf / NaN propagate
+    // exactly as in the interpreter and the reference)
+    if (single) {
+      const float f = (float)x;
+      uint32_t b;
+      std::memcpy(&b, &f, 4);
+      std::snprintf(buf, sizeof buf, "__int_as_float(0x%08x)", b);
+    } else {
+      uint64_t b;
+      std::memcpy(&b, &x, 8);
+      std::snprintf(buf, sizeof buf, "__longlong_as_double((long long)0x%016llxull)", (unsigned long long)b);
+    }
+    return std::string(buf);
+  }
   return s;
 }
 
@@ -721,6 +750,40 @@ static std::vector<char> jit_compile(const std::string& src, std::string* log) {
   return cubin;
 }
 
+// Keep the in-memory caches bounded (LRU).  Programs are dropped freely;
+// modules of this device are unloaded only after a device synchronisation
+// with every launcher excluded, and every program entry is dropped with them
+// (entries hold CUfunctions of the modules).
+void evict_lru(Driver& dr, int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_prog.size() > kMaxPrograms) {
+      std::vector<std::pair<uint64_t, Key128>> age;
+      for (auto& kv : g_prog) age.push_back({kv.second.last_use, kv.first});
+      std::sort(age.begin(), age.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (size_t i = 0; i < age.size() / 2; ++i) g_prog.erase(age[i].second);
+    }
+    if (g_cache.size() <= kMaxModules) return;
+  }
+  std::unique_lock<std::shared_mutex> ex(g_launch_mu);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_cache.size() <= kMaxModules) return;
+  const std::string pre = std::to_string(dev) + ":";
+  std::vector<std::pair<uint64_t, std::string>> age;
+  for (auto& kv : g_cache)
+    if (kv.first.compare(0, pre.size(), pre) == 0) age.push_back({kv.second.last_use, kv.first});
+  if (age.empty()) return;
+  std::sort(age.begin(), age.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+  cudaDeviceSynchronize();
+  cudaGetLastError();
+  g_prog.clear();
+  for (size_t i = 0; i < age.size() / 2; ++i) {
+    auto it = g_cache.find(age[i].second);
+    if (dr.unload) dr.unload(it->second.mod);
+    g_cache.erase(it);
+  }
+}
+
 template <typename R>
 bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
@@ -729,6 +792,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
   constexpr int RB = kRegBits<R>;
   int dev = 0;
   SVB_CUDA(cudaGetDevice(&dev));
+  evict_lru(dr, dev);
+  std::shared_lock<std::shared_mutex> launch_lk(g_launch_mu);
   const size_t np = prog.passes.size();
   std::vector<std::string> srcs(np), keys(np);
   std::vector<CUfunction> fns(np, nullptr);
@@ -743,6 +808,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_prog.find(pkey);
     if (it != g_prog.end()) {
+      it->second.last_use = ++g_tick;
       fns = it->second.fns;
       nslots = it->second.nslots;
       staged = it->second.staged;
@@ -770,8 +836,12 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
       auto it = g_cache.find(keys[p]);
-      if (it != g_cache.end()) fns[p] = it->second.fns[0];
-      else todo.push_back(p);
+      if (it != g_cache.end()) {
+        fns[p] = it->second.fns[0];
+        it->second.last_use = ++g_tick;
+      } else {
+        todo.push_back(p);
+      }
     }
   }
   if (!todo.empty()) {
@@ -824,13 +894,14 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       CUfunction f;
       if (dr.getfn(&f, m.mod, "svb_jit") != CUDA_SUCCESS) return false;
       m.fns.push_back(f);
+      m.last_use = ++g_tick;
       fns[p] = f;
       g_cache.emplace(keys[p], m);
     }
   }
   if (!hit) {
     std::lock_guard<std::mutex> lk(g_mu);
-    g_prog.emplace(pkey, ProgKernels{fns, nslots, staged});
+    g_prog.emplace(pkey, ProgKernels{fns, nslots, staged, ++g_tick});
   }
   for (size_t p = 0; p < np; ++p) {
     const PassDev& pd = prog.passes[p];

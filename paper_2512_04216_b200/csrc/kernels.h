@@ -29,6 +29,10 @@ void launch_measure(void* state, int n, int q, bool reset, uint64_t* d_rng, doub
                     int32_t* d_outcome, uint64_t* d_code, int rank, cudaStream_t st);
 size_t measure_ws_doubles(int n);
 template <typename R> void launch_half_copy(void* state, int n, void* buf, int L, int bit, int to_buf, cudaStream_t st);
+// a, b: 2^n amplitudes; out (device, 5 doubles) = {sum|a-b|^2, sum|a|^2, sum|b|^2, Re<a|b>, Im<a|b>}
+template <typename RA, typename RB>
+void launch_compare(const void* a, const void* b, int n, double* d_ws, double* d_out, cudaStream_t st);
+size_t compare_ws_doubles(int n);
 template <typename R> void launch_outer(void* dst, const void* a, const void* b, int na, int nb, cudaStream_t st);
 
 // sample.cu — PCG64, pairwise sum, alias table, samplers, histogram

@@ -378,4 +378,44 @@ template <typename R> void launch_outer(void* dst, const void* a, const void* b,
 template void launch_outer<float>(void*, const void*, const void*, int, int, cudaStream_t);
 template void launch_outer<double>(void*, const void*, const void*, int, int, cudaStream_t);
 template void launch_half_copy<double>(void*, int, void*, int, int, int, cudaStream_t);
+// Distance and overlap of two states (possibly of different precisions):
+// out[0] = sum |a-b|^2, out[1] = sum |a|^2, out[2] = sum |b|^2,
+// out[3] + i out[4] = <a|b>.  Per-block partials in fixed order, then k_sum_rows.
+template <typename RA, typename RB>
+__global__ void k_compare_partial(const cplx<RA>* __restrict__ a, const cplx<RB>* __restrict__ b, uint64_t len,
+                                  double* __restrict__ partial) {
+  __shared__ double sh[8];
+  double acc[5] = {0, 0, 0, 0, 0};
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += stride) {
+    const double ax = (double)a[i].x, ay = (double)a[i].y, bx = (double)b[i].x, by = (double)b[i].y;
+    const double dx = ax - bx, dy = ay - by;
+    acc[0] += dx * dx + dy * dy;
+    acc[1] += ax * ax + ay * ay;
+    acc[2] += bx * bx + by * by;
+    acc[3] += ax * bx + ay * by;
+    acc[4] += ax * by - ay * bx;
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const double r = block_sum256(acc[j], sh);
+    if (threadIdx.x == 0) partial[(uint64_t)j * gridDim.x + blockIdx.x] = r;
+  }
+}
+
+template <typename RA, typename RB>
+void launch_compare(const void* a, const void* b, int n, double* d_ws, double* d_out, cudaStream_t st) {
+  const uint64_t len = 1ull << n;
+  const int G = reduce_blocks(len);
+  k_compare_partial<RA, RB><<<G, 256, 0, st>>>(static_cast<const cplx<RA>*>(a), static_cast<const cplx<RB>*>(b), len,
+                                                d_ws);
+  SVB_CHECK_LAUNCH();
+  k_sum_rows<<<1, 256, 0, st>>>(d_ws, 5, G, d_out);
+  SVB_CHECK_LAUNCH();
+}
+size_t compare_ws_doubles(int n) { return 5 * (size_t)reduce_blocks(1ull << n) + 8; }
+template void launch_compare<double, double>(const void*, const void*, int, double*, double*, cudaStream_t);
+template void launch_compare<double, float>(const void*, const void*, int, double*, double*, cudaStream_t);
+template void launch_compare<float, double>(const void*, const void*, int, double*, double*, cudaStream_t);
+template void launch_compare<float, float>(const void*, const void*, int, double*, double*, cudaStream_t);
 }  // namespace svb

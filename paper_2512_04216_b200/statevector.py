@@ -247,6 +247,15 @@ class DeviceState:
         check(lib().svb_get_amplitudes(self.handle, ptr(out), 0, out.size))
         return out
 
+    def read(self, offset: int, count: int, out: np.ndarray | None = None) -> np.ndarray:
+        """Amplitudes [offset, offset + count) as complex128 (chunked read-back)."""
+        if out is None:
+            out = np.empty(int(count), dtype=np.complex128)
+        if out.dtype != np.complex128 or out.size != count or not out.flags.c_contiguous:
+            raise ValueError("out must be a contiguous complex128 array of length count")
+        check(lib().svb_get_amplitudes(self.handle, ptr(out), int(offset), int(count)))
+        return out
+
     def copy_from(self, other: "DeviceState") -> None:
         check(lib().svb_copy_state(self.handle, other.handle))
 
@@ -281,6 +290,15 @@ class DeviceState:
         out = np.empty(ms.size, dtype=np.float64)
         check(lib().svb_expect_z(self.handle, ptr(ms, _lib.c_uint64), int(ms.size), ptr(out, _lib.c_double)))
         return out
+
+    def compare(self, other: "DeviceState") -> dict:
+        """Device-side distance/overlap with another state of the same size:
+        ``rel`` = ||self - other|| / ||other||, ``fidelity`` = |<self|other>|^2."""
+        out = np.zeros(5, dtype=np.float64)
+        check(lib().svb_compare(self.handle, other.handle, ptr(out, _lib.c_double)))
+        d2, na, nb, re, im = (float(x) for x in out)
+        return {"dist2": d2, "norm2_self": na, "norm2_other": nb, "rel": (d2 / nb) ** 0.5 if nb > 0 else float("inf"),
+                "fidelity": (re * re + im * im) / (na * nb) if na > 0 and nb > 0 else 0.0}
 
     def sample_codes(self, qubits, bit_src, shots: int, rng_words: np.ndarray, sampler: int):
         qs = np.ascontiguousarray(qubits, dtype=np.int32)
@@ -588,6 +606,9 @@ def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
         prefix.apply_instructions(insts[:split])
         suffix = [x for x in insts[split:] if x.kind != "barrier"]
         clbits = clbit_order([(x.qubits[0], x.clbit) for x in suffix if x.kind == "measure"])
+        if len(clbits) > 64:
+            # the device packs one shot's clbits into a uint64 code
+            raise BackendError(f"mid-circuit replay supports at most 64 measured clbits, got {len(clbits)}")
         rank = np.full(max(clbits) + 1, -1, dtype=np.int32)
         for p, cl in enumerate(clbits):
             rank[cl] = p
@@ -647,13 +668,22 @@ class _Cached:
         self.device = device
         self.host = None
 
+    def serves(self, precision: str, device: int) -> bool:
+        return self.device.precision == _norm_prec(precision) and self.device.device == device
+
+
+def _norm_prec(precision) -> str:
+    return "c128" if _prec_code(precision) == _lib.SVB_C128 else "c64"
+
 
 _state_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
 def _cached_state(c, qubit_cap: int, precision: str = "c128", device: int = 0) -> _Cached:
+    """The cached post-unitary state of `c` (statevector.py:256-274), keyed by
+    the Circuit; an entry of another precision or device is recomputed."""
     entry = _state_cache.get(c)
-    if entry is not None:
+    if entry is not None and entry.serves(precision, device):
         return entry
     if c.n_qubits > qubit_cap:
         raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
@@ -699,7 +729,8 @@ def expectations(c, z_sets, qubit_cap: int = DEFAULT_QUBIT_CAP) -> np.ndarray:
     sums are taken by the program's last fused pass (no extra read pass); the
     state is cached as by final_state."""
     masks = [_z_mask(c, z) for z in z_sets]
-    if c not in _state_cache and masks and all(m and (m & (m - 1)) == 0 for m in masks):
+    cached = _state_cache.get(c)
+    if (cached is None or not cached.serves("c128", 0)) and masks and all(m and (m & (m - 1)) == 0 for m in masks):
         if c.n_qubits > qubit_cap:
             raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
         if not terminal_measurement_only(c):

@@ -27,6 +27,19 @@ from paper_2512_04216_b200.circuit import Circuit, Instruction  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the frozen reference suite runs in its own pytest process (its conftest.py
+# would shadow this one): tests/test_gpu_reference_suite.py
+collect_ignore = ["reference_suite"]
+
+
+def reference_src():
+    """Directory holding the reference package `polysim`: the offline install
+    baseline/_ref (travels to the GPU box) or the read-only source tree."""
+    for p in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "polysim")):
+            return p
+    return None
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device")

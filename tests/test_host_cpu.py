@@ -246,31 +246,49 @@ def test_plan_pass_counts():
 
 
 def test_polysim_shim_installs_and_restores():
-    """Drop-in swap of polysim.statevector; needs the reference."""
+    """Drop-in swap of polysim.statevector; needs the reference.
+    The qubit cap is lifted everywhere it was bound at import (dispatch.py:18,
+    predictor.py:119, the installed functions) and restored by uninstall."""
+    import inspect
     import sys as _sys
 
-    ref_src = "/root/reference/pkg/src"
-    if not os.path.isdir(ref_src):
-        pytest.skip("reference not present (GPU box)")
+    from conftest import reference_src
+
+    ref_src = reference_src()
+    if ref_src is None:
+        pytest.skip("reference package not available")
     _sys.path.insert(0, ref_src)
     try:
-        import polysim.statevector as ref_sv
-        from paper_2512_04216_b200 import polysim_shim
-
+        import polysim.dispatch as ref_dispatch
         import polysim.pblock as ref_pb
+        import polysim.predictor as ref_pred
+        import polysim.result as ref_res
+        import polysim.sampling as ref_samp
+        import polysim.statevector as ref_sv
         from paper_2512_04216_b200 import pblock as dev_pb
+        from paper_2512_04216_b200 import polysim_shim
+        from paper_2512_04216_b200 import sampling as dev_samp
 
-        orig, orig_pb = ref_sv.run, ref_pb.run
+        def cap_default(fn):
+            return inspect.signature(fn).parameters["qubit_cap"].default
+
+        orig, orig_pb, orig_at = ref_sv.run, ref_pb.run, ref_samp.AliasTable
         polysim_shim.install()
         assert ref_sv.run is sv.run and ref_sv.final_state is sv.final_state
-        assert ref_sv.DEFAULT_QUBIT_CAP == 26 and ref_pb.run is orig_pb
+        assert ref_sv.DEFAULT_QUBIT_CAP == 26 and ref_pb.run is orig_pb and ref_samp.AliasTable is orig_at
         polysim_shim.uninstall()
         assert ref_sv.run is orig
-        polysim_shim.install(qubit_cap=30, pblock=True)
-        assert ref_sv.DEFAULT_QUBIT_CAP == 30
+        polysim_shim.install(qubit_cap=30, pblock=True, sampling=True)
+        assert ref_sv.DEFAULT_QUBIT_CAP == 30 and sv.DEFAULT_QUBIT_CAP == 30
+        for fn in (ref_dispatch.run_circuit, ref_pred.select_backend, sv.run, sv.final_state, sv.expectation):
+            assert cap_default(fn) == 30, fn
         assert ref_pb.run is dev_pb.run and ref_pb.PBlockState is dev_pb.PBlockState
+        assert ref_samp.AliasTable is dev_samp.AliasTable and ref_res.AliasTable is dev_samp.AliasTable
         polysim_shim.uninstall()
         assert ref_sv.DEFAULT_QUBIT_CAP == 26 and ref_pb.run is orig_pb and ref_sv.run is orig
+        assert sv.DEFAULT_QUBIT_CAP == 26 and ref_samp.AliasTable is orig_at and ref_res.AliasTable is orig_at
+        for fn in (ref_dispatch.run_circuit, ref_pred.select_backend, sv.run, sv.final_state, sv.expectation):
+            assert cap_default(fn) == 26, fn
     finally:
         _sys.path.remove(ref_src)
 
