@@ -17,8 +17,12 @@ BASELINE.json names); the per-pass HBM GB/s is reported as `roofline`.
   `final_state(c, out=pinned)`), wall-clock per step including host gate encoding, the
   gate-program upload and the 16 GiB amplitude read-back into pinned memory.
 * `cpu_baseline` / `--impl reference`: the numpy restatement of the reference
-  algorithm (oracle/, "port") timed on this host on a bounded, evenly spaced
-  sample of the same gate list.
+  algorithm (oracle/, "port") timed on this host on the whole QFT-20 workload
+  (every gate + the 20 <Z_i> passes), scaled to QFT-30 by gate count and 2^10.
+* `configs`: BASELINE.json configs 1 (GHZ-20 x 1024 shots), 3 (Sycamore-32
+  d20 c64, 10^6 shots) and 4 (10,000 QAOA/VQE circuits, 1000 shots) through
+  the public API, plus the K6 dense-block tensor-core pass (`--no-configs`
+  skips them).
 * N > 1 (torchrun, NCCL): weak scaling — QFT on 30 + log2(N) qubits, complex128,
   sharded by global qubits (paper_2512_04216_b200/sharded.py): 16 GiB of state
   per GPU at every N, global<->local qubit swaps over NVLink.  ``--sharded``
@@ -181,52 +185,50 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU side
-def cpu_sample_plan(n_full: int, steps: int, per_step: int):
-    """Evenly spaced gates of the QFT-n gate list, and the n it runs at."""
-    try:
-        import psutil
+CPU_N = 20  # whole QFT-20 (1000 gates) + 20 <Z_i> passes: ~5 s on one core
 
-        avail = psutil.virtual_memory().available
-    except Exception:
-        avail = 0
-    # numpy's dense 1q path needs ~3x the 16 GiB state at n=30
-    n_cpu = n_full if avail > 4 * (16 << n_full) else 26
+
+def time_cpu_qft(n_cpu: int = CPU_N) -> dict:
+    """The reference algorithm (numpy port in oracle/, 1 core: the reference's
+    sv path is single-threaded numpy) on the WHOLE QFT-n_cpu workload: every
+    gate of ry-prep + qft(n_cpu) and the n_cpu single-qubit <Z_i> passes.
+    Scaled to QFT-30 by gate count and 2^(30 - n_cpu) (cost linear in 2^n)."""
+    from oracle import sv_oracle as orc
     from paper_2512_04216_b200 import suite
 
-    gates = [i for i in suite.qft_bench_circuit(n_cpu).instructions]
-    total = steps * per_step
-    idx = np.linspace(0, len(gates) - 1, total).astype(int)
-    return n_cpu, [gates[i] for i in idx]
-
-
-def time_cpu_port(n_cpu: int, gates, n_full: int) -> tuple[float, float]:
-    """Seconds per gate of the numpy port, scaled to n_full (cost is linear in 2^n)."""
-    from oracle import sv_oracle as orc
-
-    psi = orc.zero_state(n_cpu)
+    c = suite.qft_bench_circuit(n_cpu)
+    gates = [i for i in c.instructions]
     t0 = time.perf_counter()
+    psi = orc.zero_state(n_cpu)
     for g in gates:
         orc.apply_instruction(psi, n_cpu, g)
-    dt = time.perf_counter() - t0
-    scale = float(1 << (n_full - n_cpu))
-    return dt / len(gates) * scale, dt
+    t_gates = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for q in range(n_cpu):
+        orc.expectation_from_state(psi, (q,))
+    t_z = time.perf_counter() - t0
+    scale = float(1 << (N_QUBITS - n_cpu))
+    g30 = len(suite.qft_bench_circuit(N_QUBITS).instructions) if n_cpu != N_QUBITS else len(gates)
+    est30 = (t_gates / len(gates) * g30 + t_z / n_cpu * N_QUBITS) * scale
+    return {"step_s": t_gates + t_z, "est_s_qft30": est30, "gates_per_s_qft30": g30 / est30,
+            "sample": (f"whole ry-prep + qft({n_cpu}) ({len(gates)} gates, {t_gates:.2f} s) + {n_cpu} <Z_i> passes "
+                       f"({t_z:.2f} s) on 1 core; scaled to QFT-30 by gate count x {N_QUBITS / n_cpu:.2f} (<Z>) "
+                       f"and 2^{N_QUBITS - n_cpu} (cost linear in 2^n)")}
 
 
 def run_reference(args, rank: int, world: int):
+    """`--impl reference`: the reference's own CPU algorithm (numpy port of
+    polysim.statevector, oracle/) timed per step on a whole QFT-20 workload;
+    ms_per_step is the measured step, value the QFT-30 rate it scales to."""
     if rank != 0:
         return
-    n_cpu, sample = cpu_sample_plan(N_QUBITS, args.steps + args.warmup, 3)
-    per_step = 3
-    times = []
+    steps = []
     for s in range(args.warmup + args.steps):
-        spg, _ = time_cpu_port(n_cpu, sample[s * per_step:(s + 1) * per_step], N_QUBITS)
+        r = time_cpu_qft(CPU_N)
         if s >= args.warmup:
-            times.append(spg)
-    sec_per_gate = float(np.mean(times))
-    total_gates = 2250
-    value = 1.0 / sec_per_gate
-    desc = (f"{per_step} evenly spaced gates of the 2250-gate QFT-30 list per step at n={n_cpu}"
-            + ("" if n_cpu == N_QUBITS else f", time x{1 << (N_QUBITS - n_cpu)} (cost linear in 2^n)"))
+            steps.append(r)
+    step_s = float(np.mean([r["step_s"] for r in steps]))
+    value = float(np.mean([r["gates_per_s_qft30"] for r in steps]))
     line = {
         "impl": "reference",
         "metric": "gates/sec (QFT-30 complex128, full amplitudes + <Z_i>)",
@@ -235,14 +237,16 @@ def run_reference(args, rank: int, world: int):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": total_gates * sec_per_gate * 1e3,
+        "ms_per_step": step_s * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "c128",
         "data": "synthetic (deterministic QFT circuit)",
-        "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": total_gates},
-        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port", "sample": desc},
+        "config": {"workload": "qft30_c128_amplitudes_plus_z", "n_qubits": N_QUBITS, "gates": 2250,
+                   "cpu_sample_n": CPU_N},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "port",
+                         "sample": steps[-1]["sample"] + "; each step is one such run (ms_per_step = its time)"},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -384,13 +388,11 @@ def run_ours(args, rank: int, world: int, dist):
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu_baseline:
-        n_cpu, sample = cpu_sample_plan(N_QUBITS, 1, args.cpu_gates)
-        spg, dt = time_cpu_port(n_cpu, sample, N_QUBITS)
-        line["cpu_baseline"] = {
-            "value": 1.0 / spg, "unit": "gates/s", "cores": 1, "kind": "port",
-            "sample": f"{len(sample)} evenly spaced gates of the QFT-30 list at n={n_cpu}"
-                      + ("" if n_cpu == N_QUBITS else f", x{1 << (N_QUBITS - n_cpu)} scaled")
-                      + f", {dt:.1f} s wall"}
+        r = time_cpu_qft(CPU_N)
+        line["cpu_baseline"] = {"value": r["gates_per_s_qft30"], "unit": "gates/s", "cores": 1, "kind": "port",
+                                "sample": r["sample"]}
+    if rank == 0 and world == 1 and not args.no_configs:
+        line["configs"] = extra_configs(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -459,6 +461,174 @@ def run_sharded(args, rank: int, world: int, dist):
         print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------- configs 1, 3, 4 + K6
+def _timed(fn, reps):
+    fn()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts), min(ts)
+
+
+def config_ghz20() -> dict:
+    """Config 1: GHZ-20, 1024 shots, c128, through statevector.run (the
+    public API: encode, apply, sample, bitstring dict)."""
+    from oracle import sv_oracle as orc
+    from paper_2512_04216_b200 import statevector as sv
+    from paper_2512_04216_b200 import suite
+
+    c = suite.ghz_circuit(20)
+    out = {"metric": "latency (ms) / gates/s / shots/s, GHZ-20 1024 shots c128 via statevector.run"}
+    for sampler in ("alias", "cdf"):
+        seeds = iter(range(10**6))
+        med, best = _timed(lambda: sv.run(c, 1024, next(seeds), sampler=sampler), 20)
+        out[sampler] = {"latency_ms": med * 1e3, "best_ms": best * 1e3, "gates_per_s": 20 / med,
+                        "shots_per_s": 1024 / med}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "counts.json")) as fh:
+            gold = json.load(fh)["ghz20"]
+        out["parity"] = {"alias_counts_equal_reference_golden": all(
+            sv.run(c, 1024, int(sd), sampler="alias").counts == cnt for sd, cnt in gold.items()),
+            "seeds": sorted(int(x) for x in gold)}
+    except Exception as exc:  # noqa: BLE001
+        out["parity"] = {"error": repr(exc)}
+    t0 = time.perf_counter()
+    orc.run(c, 1024, 7)
+    dt = time.perf_counter() - t0
+    out["cpu_baseline"] = {"latency_ms": dt * 1e3, "unit": "ms", "cores": 1, "kind": "port",
+                           "sample": "oracle.run(ghz_20, 1024, seed 7): the reference algorithm, whole workload"}
+    return out
+
+
+def config_sycamore(peak: float) -> dict:
+    """Config 3: Sycamore-style 4x8 grid, depth 20, c64, fused passes from a
+    lazy |0...0>, then 10^6 shots with the CDF sampler."""
+    from paper_2512_04216_b200 import _lib
+    from paper_2512_04216_b200 import statevector as sv
+    from paper_2512_04216_b200 import suite
+
+    n, shots = 32, 10**6
+    c = suite.sycamore_circuit(4, 8, 20, 0)
+    g = sv.gate_array(c.instructions)
+    s = sv.DeviceState(n, "c64")
+    s.zero()
+    s.apply_gates(g)  # NVRTC compile of this program's passes (cached afterwards)
+    s.zero()
+    s.profile(True)
+    s.timer_start()
+    s.apply_gates(g)
+    ms = s.timer_stop()
+    passes = s.profile_passes()
+    s.profile(False)
+    full_bytes = 2 * 8 * (1 << n)
+    table = [{"ms": p["ms"], "gbytes": p["bytes"] / 1e9, "frac": p["bytes"] / (p["ms"] / 1e3) / 1e9 / peak}
+             for p in passes]
+    full = [t for t in table if abs(t["gbytes"] * 1e9 - full_bytes) < 1e6]
+    qs = list(range(n))
+    s.sample_codes(qs, qs, shots, sv.pcg_words(2), _lib.SAMPLER_CDF)  # grows the scratch pool
+    s.timer_start()
+    codes, freq = s.sample_codes(qs, qs, shots, sv.pcg_words(1), _lib.SAMPLER_CDF)
+    ms_s = s.timer_stop()
+    s.close()
+    del s
+    t0 = time.perf_counter()
+    cc = sv.run_codes(c, shots, 1, qubit_cap=n, precision="c64", sampler="cdf")
+    e2e = time.perf_counter() - t0
+    return {
+        "metric": "gates/s (apply) and shots/s (10^6 CDF shots), Sycamore-32 d20 c64",
+        "gates": int(g.size), "apply_ms": ms, "gates_per_s": g.size / (ms / 1e3), "passes": len(table),
+        "pass_table": table, "full_pass_mean_ms": float(np.mean([t["ms"] for t in full])) if full else None,
+        "full_pass_mean_frac": float(np.mean([t["frac"] for t in full])) if full else None,
+        "roofline_note": "bytes per pass = HBM bytes the pass moves (2*8*2^32 for a full pass); peak = MEASURED_PEAKS hbm_gbs",
+        "sample_ms": ms_s, "shots_per_s": shots / (ms_s / 1e3), "distinct_outcomes": int(codes.size),
+        "e2e": {"run_codes_s": e2e, "shots_per_s": shots / e2e,
+                "note": "statevector.run_codes: host encode + apply + 10^6 shots + (code, count) arrays"},
+        "cpu_baseline": {"value": None, "kind": "port", "cores": 1,
+                         "sample": "infeasible: the reference's complex128 state at 32 qubits is 64 GiB (x4 peak RSS)"},
+    }
+
+
+def config_batch() -> dict:
+    """Config 4: 10,000 QAOA / ry-ansatz circuits of 12-24 qubits, 1000 shots
+    each, c128 (suite.batch_workload = SURVEY §8d's list)."""
+    from oracle import sv_oracle as orc
+    from paper_2512_04216_b200 import batch, suite
+
+    circs = suite.batch_workload(10000)  # generation is not timed
+    batch.run_batch_codes(circs[:64], shots=1000, seed=0)  # warm-up (JIT cache, pools)
+    t0 = time.perf_counter()
+    rc = batch.run_batch_codes(circs, shots=1000, seed=0)
+    dt_codes = time.perf_counter() - t0
+    errs = sum(isinstance(r, Exception) for r in rc)
+    t0 = time.perf_counter()
+    rd = batch.run_batch(circs, shots=1000, seed=0)
+    dt_dict = time.perf_counter() - t0
+    # CPU: the reference algorithm on one circuit per width 12..17, extrapolated
+    # per circuit by gate count and 2^n (one core; batch.run_batch is sequential)
+    per = {}
+    for nq in range(12, 18):
+        c = next(x for x in circs if x.n_qubits == nq)
+        t = time.perf_counter()
+        orc.run(c, 1000, 0, qubit_cap=26)
+        per[nq] = (time.perf_counter() - t) / (len(c.instructions) * (1 << nq))
+    unit = float(np.median(list(per.values())))
+    est = sum(unit * len(c.instructions) * (1 << c.n_qubits) for c in circs)
+    return {
+        "metric": "circuits/s (10,000 QAOA/VQE circuits, 12-24 qubits, 1000 shots each, c128, CDF sampler)",
+        "device_path_s": dt_codes, "circuits_per_s": len(circs) / dt_codes, "errors": int(errs),
+        "with_count_dicts_s": dt_dict, "circuits_per_s_with_dicts": len(circs) / dt_dict,
+        "dict_errors": int(sum(isinstance(r, Exception) for r in rd)),
+        "note": ("device_path = batch.run_batch_codes ((code, count) arrays per circuit): host encoding of "
+                 "every gate + svb_batch_small / svb_batch_run + histograms; with_dicts adds the reference's "
+                 "{bitstring: count} dicts (~10^7 entries)"),
+        "cpu_baseline": {"value": len(circs) / est, "unit": "circuits/s", "cores": 1, "kind": "port",
+                         "est_s": est, "sample": ("oracle.run (reference algorithm, 1000 shots) on one circuit per "
+                                                  "width 12..17, cost per gate*2^n extrapolated to all 10,000")},
+    }
+
+
+def config_dense(peak: float) -> dict:
+    """K6: one dense 5-qubit block on a 30-qubit complex64 state (one HBM
+    pass), tcgen05 tensor cores (3xTF32) vs the CUDA-core engine."""
+    from paper_2512_04216_b200 import statevector as sv
+    from paper_2512_04216_b200.circuit import Instruction
+
+    n, k = 30, 5
+    rng = np.random.default_rng(0)
+    z = rng.normal(size=(32, 32)) + 1j * rng.normal(size=(32, 32))
+    U, _ = np.linalg.qr(z)
+    q = [3, 11, 17, 22, 29]
+    s = sv.DeviceState(n, "c64")
+    s.apply_instructions([Instruction("h", (i,)) for i in range(n)])
+    out = {"metric": "ms per dense 5-qubit block pass (n=30 c64), HBM fraction", "qubits": q}
+    nbytes = 2 * 8 * (1 << n)
+    for eng in ("tensor", "fma"):
+        s.apply_matrix(q, U, engine=eng)
+        s.timer_start()
+        for _ in range(5):
+            s.apply_matrix(q, U, engine=eng)
+        ms = s.timer_stop() / 5
+        out[eng] = {"ms": ms, "gbs": nbytes / (ms / 1e3) / 1e9, "frac": nbytes / (ms / 1e3) / 1e9 / peak}
+    out["fma_pipe_floor_ms"] = (1 << n) * 4 * 32 / (148 * 128 * 1.965e9) * 1e3
+    out["hbm_floor_ms"] = nbytes / peak / 1e6
+    s.close()
+    return out
+
+
+def extra_configs(args) -> dict:
+    peak, _ = hbm_peak()
+    out = {}
+    for name, fn in (("ghz20_1024", config_ghz20), ("sycamore32_c64_1e6", lambda: config_sycamore(peak)),
+                     ("batch10k_qaoa_vqe", config_batch), ("dense_block_k5_c64", lambda: config_dense(peak))):
+        try:
+            out[name] = fn()
+        except Exception as exc:  # noqa: BLE001  (one failing extra key must not lose the headline line)
+            out[name] = {"error": repr(exc)}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -468,6 +638,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-gates", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/3/4 + dense-block keys")
     ap.add_argument("--sharded", action="store_true", help="sharded path even at N = 1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

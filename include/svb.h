@@ -63,6 +63,19 @@ typedef struct {
   double mat[32];
 } svb_gate;
 
+/* Compact gate record (40 B) for batches: kind 0 = rx, 1 = ry, 2 = rz,
+ * 3 = u(p[0], p[1], p[2]) (matrices from gates.py's formulas, evaluated in
+ * C++), kind >= 4 = fixed gate `fixed[kind - 4]` (a caller-supplied table of
+ * svb_gate matrices, e.g. h x y z s sdg t tdg cx cz swap). */
+typedef struct {
+  int32_t kind;
+  int32_t q0, q1;
+  int32_t reserved;
+  double p[3];
+} svb_gate_op;
+/* ops[i] -> out[i] (host-only; the batch executor's expansion, for tests). */
+int svb_expand_gates(const svb_gate_op* ops, int n, const svb_gate* fixed, svb_gate* out);
+
 /* Library / device info. */
 const char* svb_last_error(void);
 int svb_version(void);
@@ -75,7 +88,8 @@ int svb_host_free(void* p);
 typedef enum {
   SVB_OPT_FUSION = 0,   /* 1 (default): fused multi-gate HBM passes; 0: one pass per gate */
   SVB_OPT_MAX_HIGH = 1,  /* fused pass: max non-lane qubits per pass (tuning; default auto) */
-  SVB_OPT_JIT_MIN_N = 2  /* NVRTC-specialise fused passes for n >= value (default 24; -1 never) */
+  SVB_OPT_JIT_MIN_N = 2, /* NVRTC-specialise fused passes for n >= value (default 24; -1 never) */
+  SVB_OPT_TC_MIN_K = 3   /* svb_apply_matrix (engine AUTO): tensor cores for complex64 blocks of >= value qubits (default 5) */
 } svb_option;
 int svb_set_option(svb_handle h, int option, int value);
 /* Statistics of the last svb_apply: HBM passes launched, gates applied. */
@@ -118,6 +132,18 @@ int svb_apply(svb_handle h, const svb_gate* gates, int n_gates);
  * is needed; unfused programs fall back to one reduction pass.  nz may be 0. */
 int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t* z_qubits, int nz,
                 double* out);
+
+/* One dense 2^k x 2^k block (a fused k-qubit gate; apply_2q's dense path,
+ * statevector.py:105-113, generalised to k <= 6) in one HBM pass.  mat is
+ * row-major complex128 (re, im); local index bit i <-> qubits[i].  engine:
+ *   SVB_ENGINE_AUTO   tensor cores (tcgen05 kind::tf32, 3xTF32 split) for
+ *                     complex64 and k >= SVB_OPT_TC_MIN_K, else CUDA cores;
+ *   SVB_ENGINE_TENSOR tensor cores (complex64, 3 <= k <= 5), else SVB_E_ARG;
+ *   SVB_ENGINE_FMA    CUDA cores (k <= 6 complex64, k <= 5 complex128).
+ * Needs n >= k + 7.  svb_last_engine reports which engine ran. */
+typedef enum { SVB_ENGINE_AUTO = 0, SVB_ENGINE_TENSOR = 1, SVB_ENGINE_FMA = 2 } svb_engine;
+int svb_apply_matrix(svb_handle h, const int32_t* qubits, int k, const double* mat, int engine);
+int svb_last_engine(svb_handle h);
 
 /* Reduced |amp|^2 over ascending `qubits` (marginal_probs, statevector.py:131-139). */
 int svb_marginal_probs(svb_handle h, const int32_t* qubits, int k, double* out);
@@ -164,6 +190,13 @@ int svb_alias_sample(int device, const double* prob_row, const int64_t* alias_ro
 int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream);
 int svb_half_copy(svb_handle h, int L, int bit, void* dev_buf, int to_buf);
 int svb_clear(svb_handle h); /* all amplitudes 0 (a shard that holds no part of |0..0>) */
+/* Grouped remap of g global qubits (sharded.py): block `block` of the shard
+ * = the amplitudes whose local bits lbits[0..g) (ascending) equal block's
+ * bits; copy its elements [offset, offset + count) to (to_buf = 1) or from
+ * a contiguous device buffer of count amplitudes.  sync = 0 leaves the copy
+ * queued on the handle's stream (svb_sync before the buffer is read). */
+int svb_block_copy(svb_handle h, const int32_t* lbits, int g, uint64_t block, uint64_t offset, uint64_t count,
+                   void* dev_buf, int to_buf, int sync);
 /* Distributed terminal sampling: the shots of the shared PCG64 stream whose
  * global CDF target u*total falls in [lo, hi) are drawn from this shard;
  * bit_src[p] = local bit of output bit p or -1 (then taken from code_or). */
@@ -180,6 +213,20 @@ int svb_sample_slice(svb_handle h, uint64_t shots, const uint64_t* pcg, double l
 int svb_batch_small(int device, int precision, int ncirc, const int32_t* nq, const int32_t* gate_off,
                     const int32_t* ngates, const svb_gate* gates, int total_gates, const uint64_t* pcg,
                     const int32_t* w, const int8_t* bit_src, uint64_t shots, uint64_t* out_codes);
+
+/* Batched terminal circuits of any size (5 <= n <= 36; config 4's 13-24
+ * qubit circuits): one call for the whole batch.  `nthreads` host workers,
+ * each with its own stream and state buffer, run each circuit's fused program
+ * from |0...0> and draw `shots` CDF samples from its PCG64 stream pcg[4i..];
+ * bit_src[64i + p] is the state-index bit of output bit p; codes to
+ * out_codes[shots*i + s] (one device->host copy at the end).  Per-circuit
+ * errors land in status[i] (svb_status); the call itself fails only on
+ * bad arguments or a device error outside a circuit. */
+int svb_batch_run(int device, int precision, int ncirc, const int32_t* nq, const int32_t* gate_off,
+                  const int32_t* ngates, const svb_gate_op* ops, const svb_gate* fixed, int nfixed,
+                  int total_gates, const uint64_t* pcg,
+                  const int32_t* w, const int8_t* bit_src, uint64_t shots, int nthreads, uint64_t* out_codes,
+                  int32_t* status);
 
 /* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
  * device; each measure/reset consumes one draw, exactly as rng.random(). */

@@ -20,7 +20,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb.so")
 SVB_OK, SVB_E_ARG, SVB_E_CAP, SVB_E_OOM, SVB_E_CUDA, SVB_E_NCCL, SVB_E_SAMPLING = range(7)
 SVB_C64, SVB_C128 = 0, 1
 SAMPLER_ALIAS, SAMPLER_CDF = 0, 1
-OPT_FUSION, OPT_MAX_HIGH, OPT_JIT_MIN_N = 0, 1, 2
+OPT_FUSION, OPT_MAX_HIGH, OPT_JIT_MIN_N, OPT_TC_MIN_K = 0, 1, 2, 3
+ENGINE_AUTO, ENGINE_TENSOR, ENGINE_FMA = 0, 1, 2
 
 try:  # the reference's error type when installed (sampling.py:17-18)
     from polysim.sampling import SamplingError  # type: ignore
@@ -36,6 +37,9 @@ class SvbGate(ctypes.Structure):
 
 GATE_DTYPE = np.dtype([("k", "<i4"), ("q", "<i4", (2,)), ("r", "<i4"), ("mat", "<f8", (32,))])
 assert GATE_DTYPE.itemsize == ctypes.sizeof(SvbGate) == 272
+# svb_gate_op: compact batch record (kind, q0, q1, reserved, params[3])
+GATE_OP_DTYPE = np.dtype([("kind", "<i4"), ("q0", "<i4"), ("q1", "<i4"), ("r", "<i4"), ("p", "<f8", (3,))])
+assert GATE_OP_DTYPE.itemsize == 40
 
 _h = c_void_p
 _dp = POINTER(c_double)
@@ -69,14 +73,20 @@ _SIGS = {
     "svb_marginal_probs": (c_int, [_h, _i32p, c_int, _dp]),
     "svb_expect_z": (c_int, [_h, _u64p, c_int, _dp]),
     "svb_compare": (c_int, [_h, _h, _dp]),
+    "svb_apply_matrix": (c_int, [_h, _i32p, c_int, _dp, c_int]),
+    "svb_last_engine": (c_int, [_h]),
     "svb_sample": (c_int, [_h, _i32p, c_int, _i32p, c_int, c_uint64, _u64p, c_int, _u64p, _u64p, _u64p]),
     "svb_alias_table": (c_int, [c_int, _dp, c_uint64, _dp, _i64p]),
     "svb_rng_seed": (c_int, [_h, _u64p]),
     "svb_batch_small": (c_int, [c_int, c_int, c_int, _i32p, _i32p, _i32p, c_void_p, c_int, _u64p, _i32p,
                                 POINTER(ctypes.c_int8), c_uint64, _u64p]),
+    "svb_batch_run": (c_int, [c_int, c_int, c_int, _i32p, _i32p, _i32p, c_void_p, c_void_p, c_int, c_int, _u64p,
+                              _i32p, POINTER(ctypes.c_int8), c_uint64, c_int, _u64p, _i32p]),
+    "svb_expand_gates": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "svb_device_ptr": (c_int, [_h, POINTER(c_void_p), _u64p, _i64p]),
     "svb_half_copy": (c_int, [_h, c_int, c_int, c_void_p, c_int]),
     "svb_clear": (c_int, [_h]),
+    "svb_block_copy": (c_int, [_h, _i32p, c_int, c_uint64, c_uint64, c_uint64, c_void_p, c_int, c_int]),
     "svb_outer": (c_int, [_h, _h, _h]),
     "svb_permute_qubits": (c_int, [_h, POINTER(c_int32)]),
     "svb_select_half": (c_int, [_h, _h, c_int, c_int]),

@@ -6,9 +6,12 @@ sequentially with the same seed for every circuit).
   n <= 13 complex64) run together in ONE persistent kernel launch
   (`svb_batch_small`): one CTA per SM walks the batch, state in shared memory,
   CDF sampling from the circuit's own PCG64 stream.
-* Everything else runs through the fused-pass engine (`statevector.run`) on
-  pooled device states, `workers` circuits in flight (the C calls release the
-  GIL, so host preparation of one circuit overlaps device work of others).
+* Larger terminal circuits go to `svb_batch_run` in chunks: one C call per
+  chunk, host worker threads with their own streams schedule and launch each
+  circuit's fused program and CDF draw with no per-circuit synchronisation;
+  gates travel as compact 40-byte records expanded in C++.
+* Mid-circuit circuits (and sampler="alias") run one by one through
+  `statevector.run` (device replay / the reference-exact alias sampler).
 
 Results come back in input order: a RunResult per circuit, or the exception
 the circuit raised (the reference records per-circuit errors, batch.py:192-194).
@@ -30,52 +33,106 @@ SMALL_MAX = {"c128": 12, "c64": 13}
 _lock = threading.Lock()
 
 
-def _small_batch(circuits, shots, seed, precision, device):
-    """One svb_batch_small launch for terminal circuits that fit in smem."""
+def _bit_sources(c):
+    """(width, state-index bit of each output bit) of a terminal circuit."""
+    measures = measurement_map(c)
+    qubits = sorted({q for q, _ in measures})
+    src = output_bit_sources(measures, qubits)
+    return len(src), [qubits[j] for j in src]
+
+
+def _codes_small(circuits, shots, words, precision, device) -> np.ndarray:
+    """One svb_batch_small launch: (ncirc, shots) codes."""
     nc = len(circuits)
-    encs = [sv.gate_array(c.instructions) for c in circuits]
-    ngates = np.array([e.size for e in encs], dtype=np.int32)
+    gates, ngates = sv.gate_array_many(circuits)
     gate_off = np.zeros(nc, dtype=np.int32)
     if nc > 1:
         gate_off[1:] = np.cumsum(ngates)[:-1]
-    gates = np.concatenate(encs) if encs else np.zeros(0, dtype=_lib.GATE_DTYPE)
     nq = np.array([c.n_qubits for c in circuits], dtype=np.int32)
-    words = sv.pcg_words(seed)
     pcg = np.tile(words, nc).astype(np.uint64)
     w = np.zeros(nc, dtype=np.int32)
     bit_src = np.zeros((nc, 64), dtype=np.int8)
-    widths = []
     for i, c in enumerate(circuits):
-        measures = measurement_map(c)
-        qubits = sorted({q for q, _ in measures})
-        src = output_bit_sources(measures, qubits)
-        w[i] = len(src)
-        bit_src[i, : len(src)] = [qubits[j] for j in src]  # bits of the full index
-        widths.append(len(src))
+        w[i], bits = _bit_sources(c)
+        bit_src[i, : w[i]] = bits
     codes = np.empty((nc, shots), dtype=np.uint64)
     prec = _lib.SVB_C128 if precision == "c128" else _lib.SVB_C64
     _lib.check(_lib.lib().svb_batch_small(
         device, prec, nc, _lib.ptr(nq, _lib.c_int32), _lib.ptr(gate_off, _lib.c_int32), _lib.ptr(ngates, _lib.c_int32),
         _lib.ptr(gates) if gates.size else None, int(gates.size), _lib.ptr(pcg, _lib.c_uint64),
         _lib.ptr(w, _lib.c_int32), _lib.ptr(bit_src, _lib.ctypes.c_int8), int(shots), _lib.ptr(codes, _lib.c_uint64)))
-    codes.sort(axis=1)
+    return codes, w
+
+
+class _Prepared:
+    """Host encoding of one chunk of large circuits for svb_batch_run."""
+
+    def __init__(self, circuits, words):
+        nc = len(circuits)
+        self.ops, self.ngates = sv.gate_ops_many(circuits)
+        self.gate_off = np.zeros(nc, dtype=np.int32)
+        if nc > 1:
+            self.gate_off[1:] = np.cumsum(self.ngates)[:-1]
+        self.nq = np.array([c.n_qubits for c in circuits], dtype=np.int32)
+        self.pcg = np.tile(words, nc).astype(np.uint64)
+        self.w = np.zeros(nc, dtype=np.int32)
+        self.bit_src = np.zeros((nc, 64), dtype=np.int8)
+        for i, c in enumerate(circuits):
+            self.w[i], bits = _bit_sources(c)
+            self.bit_src[i, : self.w[i]] = bits
+
+    def run(self, shots, precision, device, nthreads):
+        nc = self.nq.size
+        codes = np.empty((nc, shots), dtype=np.uint64)
+        status = np.zeros(nc, dtype=np.int32)
+        fx = sv.fixed_gate_table()
+        prec = _lib.SVB_C128 if precision == "c128" else _lib.SVB_C64
+        _lib.check(_lib.lib().svb_batch_run(
+            device, prec, nc, _lib.ptr(self.nq, _lib.c_int32), _lib.ptr(self.gate_off, _lib.c_int32),
+            _lib.ptr(self.ngates, _lib.c_int32), _lib.ptr(self.ops) if self.ops.size else None, _lib.ptr(fx),
+            int(fx.size), int(self.ops.size), _lib.ptr(self.pcg, _lib.c_uint64), _lib.ptr(self.w, _lib.c_int32),
+            _lib.ptr(self.bit_src, _lib.ctypes.c_int8), int(shots), int(nthreads), _lib.ptr(codes, _lib.c_uint64),
+            _lib.ptr(status, _lib.c_int32)))
+        return codes, status
+
+
+def _histograms(codes: np.ndarray, widths) -> list:
+    """Row-wise (code, count) arrays of a (ncirc, shots) code matrix, like np.unique."""
+    codes = np.sort(codes, axis=1)
+    nc, shots = codes.shape
+    new = np.ones(codes.shape, dtype=bool)
+    new[:, 1:] = codes[:, 1:] != codes[:, :-1]
     out = []
     for i in range(nc):
-        row = codes[i]
-        starts = np.flatnonzero(np.concatenate(([True], row[1:] != row[:-1])))
-        freq = np.diff(np.concatenate((starts, [row.size])))
-        out.append(format_counts(row[starts], freq, widths[i]))
+        starts = np.flatnonzero(new[i])
+        freq = np.diff(np.append(starts, shots)).astype(np.int64)
+        out.append(sv.CodeCounts(codes[i, starts], freq, int(widths[i])))
     return out
 
 
-def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", sampler: str = "cdf",
-              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP):
-    """Run every circuit with (shots, seed); returns a list of RunResult or
-    exception objects, in input order.  Default sampler: the device CDF
-    sampler (throughput); sampler="alias" keeps the reference's exact alias
-    sampler for every circuit (no shared-memory batching)."""
+def _status_error(code: int):
+    msg = _lib.lib().svb_last_error().decode(errors="replace")
+    if code == _lib.SVB_E_ARG:
+        return ValueError(msg)
+    if code == _lib.SVB_E_CAP:
+        return QubitCapError(msg)
+    from .result import BackendError
+
+    return BackendError(f"libsvb error {code}: {msg}")
+
+
+def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", device: int = 0,
+                    nthreads: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, chunk: int = 2048) -> list:
+    """The device batch path: every terminal circuit runs with (shots, seed) and
+    the CDF sampler; returns a CodeCounts (or the circuit's exception) per
+    circuit in input order.  Small states: one shared-memory persistent
+    kernel; the rest: svb_batch_run in chunks, the host encoding of chunk
+    j + 1 overlapping the device work of chunk j (the C call releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor as _TPE
+
     results: list = [None] * len(circuits)
     small, large = [], []
+    words = sv.pcg_words(seed)
     for i, c in enumerate(circuits):
         if c.n_qubits > qubit_cap:
             results[i] = QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
@@ -83,33 +140,69 @@ def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c
             results[i] = ValueError("shots must be positive")
         elif not measurement_map(c):
             results[i] = NoMeasurementsError("circuit has no measurements")
-        elif (sampler != "alias" and terminal_measurement_only(c)
-              and c.n_qubits <= SMALL_MAX[precision] and c.n_qubits >= 1):
+        elif not terminal_measurement_only(c):
+            results[i] = "replay"
+        elif c.n_qubits <= SMALL_MAX[precision]:
             small.append(i)
         else:
             large.append(i)
-    if small:
-        t0 = time.perf_counter()
-        counts = _small_batch([circuits[i] for i in small], shots, seed, precision, device)
-        dt = (time.perf_counter() - t0) / len(small)
-        for i, cnt in zip(small, counts):
-            r = RunResult(counts=cnt, shots=shots, backend="sv", seed=seed, wall_time=dt)
-            r.metadata.update({"engine": "libsvb-batch-smem", "precision": precision, "sampler": "cdf"})
-            results[i] = r
+    # largest circuits first across chunks (the GPU tail is then short)
+    large.sort(key=lambda i: -circuits[i].n_qubits)
+    with _TPE(max_workers=2) as pool:
+        fut_small = pool.submit(_codes_small, [circuits[i] for i in small], shots, words, precision, device) \
+            if small else None
+        pending = []
+        for lo in range(0, len(large), chunk):
+            idx = large[lo:lo + chunk]
+            prep = _Prepared([circuits[i] for i in idx], words)
+            pending.append((idx, prep.w, pool.submit(prep.run, shots, precision, device, nthreads)))
+        for idx, w, fut in pending:
+            codes, status = fut.result()
+            for i, cc, st in zip(idx, _histograms(codes, w), status.tolist()):
+                results[i] = cc if st == 0 else _status_error(st)
+        if fut_small is not None:
+            codes, w = fut_small.result()
+            for i, cc in zip(small, _histograms(codes, w)):
+                results[i] = cc
+    for i, r in enumerate(results):
+        if isinstance(r, str):  # mid-circuit measurement: the replay engine, one circuit at a time
+            try:
+                res = sv.run_codes(circuits[i], shots, seed, qubit_cap=qubit_cap, precision=precision, device=device)
+                results[i] = res
+            except Exception as exc:
+                results[i] = exc
+    return results
 
-    def one(i):
+
+def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", sampler: str = "cdf",
+              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP):
+    """Run every circuit with (shots, seed); returns a list of RunResult or
+    exception objects, in input order (the reference records per-circuit
+    errors, batch.py:192-194).  Default sampler: the device CDF sampler through
+    run_batch_codes (counts dicts formatted at the end); sampler="alias" keeps
+    the reference's exact alias sampler, one circuit at a time."""
+    if sampler != "alias":
+        t0 = time.perf_counter()
+        raw = run_batch_codes(circuits, shots, seed, precision=precision, device=device, nthreads=workers,
+                              qubit_cap=qubit_cap)
+        dt = (time.perf_counter() - t0) / max(len(circuits), 1)
+        out = []
+        for r in raw:
+            if isinstance(r, Exception):
+                out.append(r)
+                continue
+            res = RunResult(counts=r.to_dict(), shots=shots, backend="sv", seed=seed, wall_time=dt)
+            res.metadata.update({"engine": "libsvb-batch", "precision": precision, "sampler": "cdf"})
+            out.append(res)
+        return out
+
+    def one(c):
         try:
-            return sv.run(circuits[i], shots, seed, qubit_cap=qubit_cap, precision=precision,
-                          sampler=sampler, device=device)
+            return sv.run(c, shots, seed, qubit_cap=qubit_cap, precision=precision, sampler=sampler, device=device)
         except Exception as exc:  # recorded per circuit, like the reference
             return exc
 
-    if large:
-        if workers <= 1:
-            for i in large:
-                results[i] = one(i)
-        else:
-            with ThreadPoolExecutor(max_workers=workers) as pool:
-                for i, r in zip(large, pool.map(one, large)):
-                    results[i] = r
-    return results
+    if workers <= 1:
+        return [one(c) for c in circuits]
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        return list(pool.map(one, circuits))

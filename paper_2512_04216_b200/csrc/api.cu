@@ -28,6 +28,8 @@ struct svb_state {
   int fusion = 1, max_high = -1;
   bool zero_pending = false;  // |0...0> not yet written: the next fused pass synthesises it
   int jit_min_n = 24;  // NVRTC-specialised passes from this many qubits up (-1: never)
+  int tc_min_k = 5;    // svb_apply_matrix: tensor cores for dense blocks of >= this many qubits (complex64)
+  int last_engine = 0;
   ProgramStats stats{};
   Profiler prof;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -192,6 +194,7 @@ int svb_set_option(svb_handle h, int option, int value) {
     if (option == SVB_OPT_FUSION) h->fusion = value;
     else if (option == SVB_OPT_MAX_HIGH) h->max_high = value;
     else if (option == SVB_OPT_JIT_MIN_N) h->jit_min_n = value;
+    else if (option == SVB_OPT_TC_MIN_K) h->tc_min_k = value;
     else throw Error(SVB_E_ARG, "unknown option");
   });
 }
@@ -464,6 +467,35 @@ int svb_expect_z(svb_handle h, const uint64_t* masks, int m, double* out) {
   });
 }
 
+int svb_apply_matrix(svb_handle h, const int32_t* qubits, int k, const double* mat, int engine) {
+  return guard([&] {
+    check_handle(h);
+    require(k >= 1 && k <= 6 && qubits != nullptr && mat != nullptr, SVB_E_ARG, "bad dense block");
+    for (int i = 0; i < k; ++i) {
+      require(qubits[i] >= 0 && qubits[i] < h->n, SVB_E_ARG, "block qubit out of range");
+      for (int j = 0; j < i; ++j) require(qubits[i] != qubits[j], SVB_E_ARG, "block repeats a qubit");
+    }
+    const bool tc = dense_tc_supported(h->prec, h->n, k);
+    require(engine != SVB_ENGINE_TENSOR || tc, SVB_E_ARG,
+            "tensor-core engine needs complex64, 3 <= k <= 5 and n >= k + 7");
+    const bool use_tc = engine == SVB_ENGINE_TENSOR || (engine == SVB_ENGINE_AUTO && tc && k >= h->tc_min_k);
+    Profiler* pf = h->prof.on ? &h->prof : nullptr;
+    if (pf) pf->begin(h->st, 0, 2.0 * (double)h->amp_bytes(), 0);
+    if (use_tc) launch_dense_tc(h->amps, h->n, qubits, k, mat, h->st);
+    else if (h->prec == SVB_C128) launch_dense_fma<double>(h->amps, h->n, qubits, k, mat, h->st);
+    else launch_dense_fma<float>(h->amps, h->n, qubits, k, mat, h->st);
+    if (pf) pf->end(h->st);
+    h->stats = ProgramStats{};
+    h->stats.passes = 1;
+    h->stats.launches = 1;
+    h->stats.gates = 1;
+    h->last_engine = use_tc ? SVB_ENGINE_TENSOR : SVB_ENGINE_FMA;
+    SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_last_engine(svb_handle h) { return h ? h->last_engine : -1; }
+
 int svb_compare(svb_handle a, svb_handle b, double* out) {
   return guard([&] {
     check_handle(b);
@@ -694,6 +726,29 @@ int svb_half_copy(svb_handle h, int L, int bit, void* dev_buf, int to_buf) {
     if (h->prec == SVB_C128) launch_half_copy<double>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
     else launch_half_copy<float>(h->amps, h->n, dev_buf, L, bit, to_buf, h->st);
     SVB_CUDA(cudaStreamSynchronize(h->st));
+  });
+}
+
+int svb_block_copy(svb_handle h, const int32_t* lbits, int g, uint64_t block, uint64_t offset, uint64_t count,
+                   void* dev_buf, int to_buf, int sync) {
+  return guard([&] {
+    check_handle(h);
+    require(g >= 1 && g <= 8 && g < h->n, SVB_E_ARG, "block copy: 1 <= g <= 8 local bits");
+    BlockSel sel{};
+    sel.g = g;
+    for (int b = 0; b < g; ++b) {
+      sel.L[b] = lbits[b];
+      require(lbits[b] >= 0 && lbits[b] < h->n && (b == 0 || lbits[b] > lbits[b - 1]), SVB_E_ARG,
+              "block copy: local bits must be ascending and in range");
+      if ((block >> b) & 1) sel.bits |= 1ull << lbits[b];
+    }
+    require(block < (1ull << g), SVB_E_ARG, "block copy: bad block");
+    const uint64_t blen = 1ull << (h->n - g);
+    require(offset <= blen && count <= blen - offset, SVB_E_ARG, "block copy: range out of the block");
+    if (count == 0) return;
+    if (h->prec == SVB_C128) launch_block_copy<double>(h->amps, dev_buf, sel, offset, count, to_buf, h->st);
+    else launch_block_copy<float>(h->amps, dev_buf, sel, offset, count, to_buf, h->st);
+    if (sync) SVB_CUDA(cudaStreamSynchronize(h->st));
   });
 }
 

@@ -10,6 +10,7 @@
 // 0..shots-1) by binary search.  HBM traffic is only the gate records in and
 // the shot codes out.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -429,4 +430,179 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
     set_last_error(e.what());
     return e.code;
   }
+}
+
+// ------------------------------------------ batch of HBM-resident circuits
+// Terminal circuits too large for the shared-memory kernel (config 4: 13-24
+// qubits, `batch.run_batch`'s per-circuit `run_circuit(c, "sv", shots, seed)`
+// loop, batch.py:104-222).  The whole batch is one C call: `nthreads` host
+// workers, each with its own CUDA stream and state buffer (sized once for
+// its largest circuit: circuits are taken largest first from a shared
+// counter), schedule each circuit's fused program natively (program.cu; the
+// NVRTC kernels of identical structures are shared), run it from a lazy
+// |0...0> and draw the shots with the CDF sampler into one device code
+// buffer.  No per-circuit host synchronisation: the codes come back with a
+// single copy at the end.  status[i] = 0 or the svb_status of circuit i.
+#include <atomic>
+#include <mutex>
+#include <thread>
+
+#include "program.h"
+
+namespace svb {
+void expand_gate(const svb_gate_op& op, const svb_gate* fixed, svb_gate& g);
+}
+
+extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t* nq, const int32_t* gate_off,
+                             const int32_t* ngates, const svb_gate_op* ops, const svb_gate* fixed, int nfixed,
+                             int total_gates, const uint64_t* pcg,
+                             const int32_t* w, const int8_t* bit_src, uint64_t shots, int nthreads,
+                             uint64_t* out_codes, int32_t* status) {
+  using namespace svb;
+  try {
+    require(ncirc >= 0 && shots >= 1 && nthreads >= 1, SVB_E_ARG, "bad batch arguments");
+    if (ncirc == 0) return SVB_OK;
+    std::vector<int> order(ncirc);
+    for (int i = 0; i < ncirc; ++i) {
+      status[i] = SVB_OK;
+      order[i] = i;
+      if (!(nq[i] >= 5 && nq[i] <= 36) || !(w[i] >= 1 && w[i] <= 63) ||
+          !(gate_off[i] >= 0 && ngates[i] >= 0 && gate_off[i] + ngates[i] <= total_gates))
+        status[i] = SVB_E_ARG;
+      for (int p = 0; status[i] == SVB_OK && p < w[i]; ++p)
+        if (bit_src[64 * i + p] < 0 || bit_src[64 * i + p] >= nq[i]) status[i] = SVB_E_ARG;
+      for (int gi = 0; status[i] == SVB_OK && gi < ngates[i]; ++gi) {
+        const svb_gate_op& g = ops[gate_off[i] + gi];
+        if (g.kind < 0 || g.kind >= 4 + nfixed) {
+          status[i] = SVB_E_ARG;
+          break;
+        }
+        const int k = g.kind >= 4 ? fixed[g.kind - 4].k : 1;
+        if (k < 1 || k > 2 || g.q0 < 0 || g.q0 >= nq[i] || (k == 2 && (g.q1 < 0 || g.q1 >= nq[i] || g.q1 == g.q0)))
+          status[i] = SVB_E_ARG;
+      }
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nq[a] > nq[b]; });
+    SVB_CUDA(cudaSetDevice(device));
+    uint64_t* dcodes = nullptr;
+    SVB_CUDA(cudaMalloc(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc));
+    const size_t s = precision == SVB_C128 ? 16 : 8;
+    std::atomic<int> next{0};
+    std::mutex err_mu;
+    std::string first_err;
+    auto worker = [&] {
+      cudaSetDevice(device);
+      cudaStream_t st = nullptr;
+      void *buf = nullptr, *spare = nullptr;
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
+      ProgramStats stats{};
+      std::vector<svb_gate> gates;
+      for (int j = next++; j < ncirc; j = next++) {
+        const int i = order[j];
+        if (status[i] != SVB_OK) continue;
+        const int n = nq[i];
+        try {
+          gates.resize(ngates[i]);
+          for (int gi = 0; gi < ngates[i]; ++gi) expand_gate(ops[gate_off[i] + gi], fixed, gates[gi]);
+          if (!buf) SVB_CUDA(state_malloc(&buf, s << n));  // largest first: the first size is the maximum
+          bool zp = true;
+          if (precision == SVB_C128)
+            run_program_owned<double>(&buf, &spare, n, gates.data(), ngates[i], 1, 24, st, &stats, &zp);
+          else
+            run_program_owned<float>(&buf, &spare, n, gates.data(), ngates[i], 1, 24, st, &stats, &zp);
+          if (zp) {
+            if (precision == SVB_C128) launch_zero<double>(buf, n, st);
+            else launch_zero<float>(buf, n, st);
+          }
+          int32_t bs[64];
+          for (int p = 0; p < 64; ++p) bs[p] = p < w[i] ? bit_src[64 * i + p] : 0;
+          if (precision == SVB_C128) cdf_draw<double>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
+          else cdf_draw<float>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
+        } catch (const Error& e) {
+          status[i] = e.code;
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (first_err.empty()) first_err = e.what();
+        } catch (const std::exception& e) {
+          status[i] = SVB_E_CUDA;
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (first_err.empty()) first_err = e.what();
+        }
+      }
+      cudaStreamSynchronize(st);
+      if (buf) cudaFree(buf);
+      if (spare) cudaFree(spare);
+      cudaStreamDestroy(st);
+    };
+    std::vector<std::thread> th;
+    const int T = std::min(nthreads, ncirc);
+    for (int t = 0; t < T; ++t) th.emplace_back(worker);
+    for (auto& t : th) t.join();
+    const cudaError_t e = cudaMemcpy(out_codes, dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc,
+                                     cudaMemcpyDeviceToHost);
+    cudaFree(dcodes);
+    SVB_CUDA(e);
+    if (!first_err.empty()) set_last_error(first_err.c_str());
+    return SVB_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  }
+}
+
+// ------------------------------------------------ compact gate records
+// 40-byte (kind, qubits, params) records expanded to svb_gate matrices in
+// C++ (batch workers expand their own circuits in parallel).  Parametric
+// kinds evaluate gates.py's formulas (gates.py:43-65) with the same libm
+// calls numpy / math make; fixed kinds copy `fixed[kind]` (the exact
+// matrices gates.py holds, passed in by the caller).
+namespace svb {
+enum : int32_t { GK_RX = 0, GK_RY = 1, GK_RZ = 2, GK_U = 3, GK_FIXED = 4 };
+
+void expand_gate(const svb_gate_op& op, const svb_gate* fixed, svb_gate& g) {
+  if (op.kind >= GK_FIXED) {
+    g = fixed[op.kind - GK_FIXED];
+  } else {
+    std::memset(&g, 0, sizeof g);
+    g.k = 1;
+    double* m = g.mat;
+    const double t = op.p[0];
+    if (op.kind == GK_RZ) {  // np.exp(-0.5j t), np.exp(0.5j t)
+      m[0] = std::cos(-0.5 * t);
+      m[1] = std::sin(-0.5 * t);
+      m[6] = std::cos(0.5 * t);
+      m[7] = std::sin(0.5 * t);
+    } else {
+      const double c = std::cos(t / 2), s = std::sin(t / 2);
+      if (op.kind == GK_RX) {  // [[c, -1j s], [-1j s, c]]
+        m[0] = c;
+        m[2] = -0.0 * s;
+        m[3] = -s;
+        m[4] = -0.0 * s;
+        m[5] = -s;
+        m[6] = c;
+      } else if (op.kind == GK_RY) {
+        m[0] = c;
+        m[2] = -s;
+        m[4] = s;
+        m[6] = c;
+      } else {  // u(t, p, l): [[c, -e^{il} s], [e^{ip} s, e^{i(p+l)} c]]
+        const double p = op.p[1], l = op.p[2];
+        m[0] = c;
+        m[2] = -std::cos(l) * s;
+        m[3] = -std::sin(l) * s;
+        m[4] = std::cos(p) * s;
+        m[5] = std::sin(p) * s;
+        m[6] = std::cos(p + l) * c;
+        m[7] = std::sin(p + l) * c;
+      }
+    }
+  }
+  g.qubits[0] = op.q0;
+  g.qubits[1] = g.k == 2 ? op.q1 : 0;
+}
+}  // namespace svb
+
+extern "C" int svb_expand_gates(const svb_gate_op* ops, int n, const svb_gate* fixed, svb_gate* out) {
+  for (int i = 0; i < n; ++i) svb::expand_gate(ops[i], fixed, out[i]);
+  return SVB_OK;
 }

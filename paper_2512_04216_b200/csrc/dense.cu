@@ -1,0 +1,469 @@
+// Dense k-qubit block passes (north_star item 3, SURVEY §7 step 7 "K6"):
+// apply one dense 2^k x 2^k complex matrix U to qubits q[0..k) of the state
+// in one HBM pass (read + write the state once).
+//
+// The state is viewed as 2^(n-k) columns x 2^k rows: column c holds the 2^k
+// amplitudes that differ only in the block qubits, y_c = U x_c (local index
+// bit i <-> q[i], the svb_gate convention of gates.py:3-5).  A CTA stages a
+// tile of 128 columns (2^(k+7) amplitudes: the block qubits plus the 7 lowest
+// other qubits, so warps read 256 contiguous bytes) in shared memory.
+//
+// * k_dense_tc (complex64, 3 <= k <= 5): the block is a real GEMM on the
+//   5th-generation tensor cores.  With x in interleaved real form
+//   (x_re, x_im per amplitude) D[c][2i+e] = sum_kk A[c][kk] * B[2i+e][kk],
+//   A = the tile (M = 128 columns, K = 2^(k+1)), B = U in real form
+//   (N = K).  kind::tf32 with a 4-term TF32 split (A_lo B_lo + A_lo B_hi +
+//   A_hi B_lo + A_hi B_hi, small terms first; hi = x rounded to TF32, lo =
+//   x - hi rounded to TF32) keeps ~2^-21 relative
+//   accuracy per block, inside complex64's 1e-5 (TF32 alone would miss it).
+//   One thread issues tcgen05.mma from shared-memory descriptors (canonical
+//   K-major, no swizzle; the K-chunk stride is padded by 16 B so the tile
+//   writes are bank-conflict free), the accumulator lives in TMEM
+//   (128 lanes x 2^(k+1) fp32 columns) and returns through tcgen05.ld.
+//   The next tile's loads are issued before the MMA wait, so HBM traffic
+//   overlaps the tensor work and the epilogue.
+// * k_dense_fma (either precision, 1 <= k <= 6): the same tile staging with
+//   the products on the FP32/FP64 FMA pipes: the CUDA-core path for small or
+//   complex128 blocks, and the baseline the tensor path is measured against.
+//
+// Roofline: 2*s*2^n bytes per pass; 8*2^k flop per amplitude
+// (complex MAC) on CUDA cores, 3*8*2^k TF32 flop on tensor cores.  complex64
+// leaves the HBM roofline on CUDA cores at k = 5 (128 FFMA per amplitude),
+// where the tensor path stays HBM-bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace svb {
+
+constexpr int kDenseCols = 128;  // columns per tile (= UMMA M)
+constexpr int kDenseMaxK = 6;
+constexpr int kTcMaxK = 5;
+
+struct DenseGeom {
+  int k = 0;          // block qubits
+  int kb = 0;         // tile bits = k + 7
+  int nout = 0;       // qubits outside the tile
+  int8_t tq[kDenseMaxK + 12] = {};   // qubit of tile position b (ascending)
+  uint32_t sb[kDenseMaxK + 12] = {};  // shared-memory byte contribution of tile position b
+  int8_t outq[48] = {};              // qubits outside the tile, ascending
+};
+
+// ------------------------------------------------------------ tcgen05 PTX
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  // SWIZZLE_NONE K-major canonical layout: core matrices of 8 rows x 16 B,
+  // rows 16 B apart, row groups SBO apart, the two K chunks LBO apart;
+  // version 1 (bits 46-47) for sm_100
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// round to the nearest TF32 (ties away): unbiased hi / lo split, and a lo part
+// the tensor core then reads exactly (its own conversion truncates, which
+// would bias every product toward zero and decay the norm block by block)
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Per-CTA constants in shared memory: the tile-base deposit tables (tile
+// index -> amplitude offset of the bits outside the tile, 8 index bits per
+// table: base = sum of 4 lookups) and the element-offset tables.
+struct DenseSmemHdr {
+  uint64_t tb[4][256];
+};
+
+__device__ __forceinline__ void dense_tile_tables(const DenseGeom& g, DenseSmemHdr* h) {
+  for (int e = threadIdx.x; e < 4 * 256; e += blockDim.x) {
+    const int c = e >> 8, v = e & 255;
+    uint64_t b = 0;
+    for (int j = 0; j < 8; ++j)
+      if (((v >> j) & 1) && 8 * c + j < g.nout) b |= 1ull << g.outq[8 * c + j];
+    h->tb[c][v] = b;
+  }
+}
+__device__ __forceinline__ uint64_t dense_tile_base(const DenseSmemHdr* h, uint64_t t) {
+  return h->tb[0][t & 255] + h->tb[1][(t >> 8) & 255] + h->tb[2][(t >> 16) & 255] + h->tb[3][(t >> 24) & 255];
+}
+
+// per-thread constant part of the element offsets (element e = it * NT + tid)
+template <int NT>
+__device__ __forceinline__ void dense_thread_offsets(const DenseGeom& g, uint32_t tid, uint64_t& goff,
+                                                     uint32_t& soff) {
+  goff = 0;
+  soff = 0;
+  constexpr int lb = NT == 128 ? 7 : 8;
+  for (int b = 0; b < lb; ++b)
+    if ((tid >> b) & 1u) {
+      goff += 1ull << g.tq[b];
+      soff += g.sb[b];
+    }
+}
+
+// it-part of the offsets, one table entry per element slot
+template <int NT>
+__device__ __forceinline__ void dense_it_tables(const DenseGeom& g, int ept, uint64_t* git, uint32_t* sit) {
+  constexpr int lb = NT == 128 ? 7 : 8;
+  for (int it = threadIdx.x; it < ept; it += NT) {
+    uint64_t go = 0;
+    uint32_t so = 0;
+    for (int b = lb; b < g.kb; ++b)
+      if ((it >> (b - lb)) & 1) {
+        go += 1ull << g.tq[b];
+        so += g.sb[b];
+      }
+    git[it] = go;
+    sit[it] = so;
+  }
+}
+
+constexpr int kTcThreads = 128;
+
+// smem: [hdr | Ahi | Alo | Bhi | Blo | git | sit | bar | tmem slot]
+// Two register sets of the tile (cur / nxt): tile t + grid is loaded at the
+// top of tile t's iteration, a whole iteration ahead of its use.
+template <int K>
+__global__ void __launch_bounds__(kTcThreads, 2)
+    k_dense_tc(float2* __restrict__ state, const float* __restrict__ bsrc, const DenseGeom g, uint64_t ntiles,
+               uint32_t chunk_stride) {
+  constexpr int KR = 2 << K;             // real K = N
+  constexpr int EPT = (1 << (K + 7)) / kTcThreads;  // elements per thread
+  constexpr int NCH = KR / 4;            // 16-byte K chunks
+  extern __shared__ __align__(1024) uint8_t smem[];
+  DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
+  const uint32_t abytes = NCH * chunk_stride;
+  uint8_t* ahi = smem + sizeof(DenseSmemHdr);
+  uint8_t* alo = ahi + abytes;
+  uint8_t* bhi = alo + abytes;
+  uint8_t* blo = bhi + KR * KR * 4;
+  uint64_t* git = reinterpret_cast<uint64_t*>(blo + KR * KR * 4);
+  uint32_t* sit = reinterpret_cast<uint32_t*>(git + EPT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sit + EPT + (EPT & 1));
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr uint32_t TCOLS = KR < 32 ? 32 : KR;
+
+  // B operand (hi, lo: real-form U, K-major rows) from global, once per CTA
+  for (int i = tid; i < 2 * KR * KR / 4; i += kTcThreads)
+    reinterpret_cast<float4*>(bhi)[i] = reinterpret_cast<const float4*>(bsrc)[i];
+  dense_it_tables<kTcThreads>(g, EPT, git, sit);
+  dense_tile_tables(g, hdr);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  uint64_t goff;
+  uint32_t soff;
+  dense_thread_offsets<kTcThreads>(g, tid, goff, soff);
+  // instruction descriptor: F32 accumulator, TF32 A and B, K-major both, N = KR, M = 128
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(KR >> 3) << 17) | ((128u >> 4) << 24);
+  uint32_t phase = 0;
+
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
+  };
+  auto step = [&](float2 (&cur)[EPT], float2 (&nxt)[EPT], uint64_t t) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+    if (t + gridDim.x < ntiles) load(nxt, t + gridDim.x);
+    // A tile, split hi / lo
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(cur[i].x), hy = tf32_rna(cur[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(ahi + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(alo + o) = make_float2(tf32_rna(cur[i].x - hx), tf32_rna(cur[i].y - hy));
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(ahi), a1 = smem_u32(alo), b0 = smem_u32(bhi), b1 = smem_u32(blo);
+      // small terms first (lo*lo, lo*hi, hi*lo), hi*hi last: the accumulator
+      // holds the small partial sums before the large one arrives
+      const uint32_t as[4] = {a1, a1, a0, a0}, bs[4] = {b1, b0, b1, b0};
+#pragma unroll
+      for (int term = 0; term < 4; ++term)
+#pragma unroll
+        for (int s = 0; s < KR / 8; ++s) {
+          const uint32_t ao = s * 2 * chunk_stride, bo = s * 2 * (KR * 16);
+          umma_tf32(tmem, umma_desc(as[term] + ao, chunk_stride, 128), umma_desc(bs[term] + bo, KR * 16, 128),
+                    idesc, (term | s) != 0);
+        }
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    // epilogue: row c = 32*warp + lane; columns 2i+e -> amplitude i of the column,
+    // written back into the A-hi layout (16 B = two amplitudes per chunk)
+    {
+      const uint32_t c = 32 * warp + lane;
+#pragma unroll
+      for (int col = 0; col < KR; col += 16) {
+        float y[16];
+        tmem_ld16(tmem + ((32 * warp) << 16) + col, y);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(ahi + (uint32_t)(col / 4 + q) * chunk_stride + c * 16) =
+              make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(ahi + soff + sit[i]));
+    __syncthreads();
+  };
+
+  float2 va[EPT], vb[EPT];
+  const uint64_t G = gridDim.x;
+  if (blockIdx.x < ntiles) load(va, blockIdx.x);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += 2 * G) {
+    step(va, vb, t);
+    if (t + G < ntiles) step(vb, va, t + G);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS) : "memory");
+  }
+}
+
+// ----------------------------------------------------- CUDA-core baseline
+constexpr int kFmaThreads = 256;
+constexpr int kFmaOut = 8;  // outputs accumulated per thread per sweep over the inputs
+
+// smem: [hdr | X | Y | U | git | sit]; X/Y layout [j][c] complex with
+// 2^cb columns per tile (>= 4096 amplitudes per tile for small k)
+template <typename R>
+__global__ void __launch_bounds__(kFmaThreads, 1)
+    k_dense_fma(cplx<R>* __restrict__ state, const cplx<R>* __restrict__ u, const DenseGeom g, uint64_t ntiles) {
+  const int k = g.k, D = 1 << k, cb = g.kb - g.k, cols = 1 << cb, ept = (D << cb) / kFmaThreads;
+  const int ob = D < kFmaOut ? D : kFmaOut;
+  extern __shared__ __align__(16) uint8_t smem[];
+  DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
+  cplx<R>* X = reinterpret_cast<cplx<R>*>(smem + sizeof(DenseSmemHdr));
+  cplx<R>* Y = X + (D << cb);
+  cplx<R>* U = Y + (D << cb);
+  uint64_t* git = reinterpret_cast<uint64_t*>(U + D * D);
+  uint32_t* sit = reinterpret_cast<uint32_t*>(git + ept);
+  const uint32_t tid = threadIdx.x;
+  for (int i = tid; i < D * D; i += kFmaThreads) U[i] = u[i];
+  dense_it_tables<kFmaThreads>(g, ept, git, sit);
+  dense_tile_tables(g, hdr);
+  uint64_t goff;
+  uint32_t soff;
+  dense_thread_offsets<kFmaThreads>(g, tid, goff, soff);
+  __syncthreads();
+  const int items = cols * (D / ob);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll 8
+    for (int i = 0; i < ept; ++i)
+      *reinterpret_cast<cplx<R>*>(reinterpret_cast<uint8_t*>(X) + soff + sit[i]) = __ldcs(state + base + git[i]);
+    __syncthreads();
+    for (int p = tid; p < items; p += kFmaThreads) {
+      const int c = p & (cols - 1), i0 = (p >> cb) * ob;
+      cplx<R> acc[kFmaOut];
+#pragma unroll
+      for (int o = 0; o < kFmaOut; ++o) acc[o] = mk<R>(0, 0);
+      for (int j = 0; j < D; ++j) {
+        const cplx<R> xj = X[(j << cb) + c];
+#pragma unroll
+        for (int o = 0; o < kFmaOut; ++o)
+          if (o < ob) acc[o] = cfma<R>(U[(i0 + o) * D + j], xj, acc[o]);
+      }
+#pragma unroll
+      for (int o = 0; o < kFmaOut; ++o)
+        if (o < ob) Y[((i0 + o) << cb) + c] = acc[o];
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int i = 0; i < ept; ++i)
+      __stcs(state + base + git[i],
+             *reinterpret_cast<const cplx<R>*>(reinterpret_cast<const uint8_t*>(Y) + soff + sit[i]));
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host
+// Tile = block qubits + the 7 lowest other qubits; `layout` 0: [j][c] complex
+// of size s (FMA kernel), 1: the UMMA A-operand layout (TC kernel).
+static DenseGeom make_geom(int n, const int32_t* q, int k, int cb, int layout, size_t s, uint32_t chunk_stride) {
+  DenseGeom g;
+  g.k = k;
+  g.kb = k + cb;
+  std::vector<int> blk(q, q + k), cols, tile;
+  for (int x = 0; x < n && (int)cols.size() < cb; ++x)
+    if (std::find(blk.begin(), blk.end(), x) == blk.end()) cols.push_back(x);
+  tile = cols;
+  tile.insert(tile.end(), blk.begin(), blk.end());
+  std::sort(tile.begin(), tile.end());
+  for (int b = 0; b < g.kb; ++b) {
+    const int x = tile[b];
+    g.tq[b] = (int8_t)x;
+    const auto bi = std::find(blk.begin(), blk.end(), x);
+    if (bi != blk.end()) {
+      const int i = (int)(bi - blk.begin());  // local index bit i of U
+      if (layout == 0) g.sb[b] = (uint32_t)(s << cb) << i;
+      else g.sb[b] = i == 0 ? 8u : chunk_stride << (i - 1);
+    } else {
+      const int r = (int)(std::find(cols.begin(), cols.end(), x) - cols.begin());  // column bit r
+      if (layout == 0) g.sb[b] = (uint32_t)s << r;
+      else g.sb[b] = 16u << r;  // (c % 8) * 16 + (c / 8) * 128 = 16 c
+    }
+  }
+  g.nout = 0;
+  for (int x = 0; x < n; ++x)
+    if (std::find(tile.begin(), tile.end(), x) == tile.end()) g.outq[g.nout++] = (int8_t)x;
+  return g;
+}
+
+static int sm_count() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+
+bool dense_tc_supported(int precision, int n, int k) {
+  return precision == SVB_C64 && k >= 3 && k <= kTcMaxK && n >= k + 7;
+}
+bool dense_fma_supported(int precision, int n, int k) {
+  return k >= 1 && k <= (precision == SVB_C128 ? kDenseMaxK - 1 : kDenseMaxK) && n >= k + 7;
+}
+
+// mat: 2^k x 2^k complex, row-major (re, im) doubles, local bit i <-> q[i]
+void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st) {
+  require(k >= 3 && k <= kTcMaxK && n >= k + 7, SVB_E_ARG, "tensor-core dense block: need 3 <= k <= 5, n >= k + 7");
+  const int D = 1 << k, KR = 2 * D;
+  const uint32_t chunk_stride = kDenseCols * 16 + 16;  // 2064 B: +16 B keeps tile writes bank-conflict free
+  // real form B[n_out][kk] (K-major rows), split into TF32 hi / lo, in the
+  // canonical layout byte(nrow, kk) = (kk / 4) * KR * 16 + nrow * 16 + (kk % 4) * 4
+  std::vector<float> hb(2 * KR * KR);
+  auto rna = [](float x) {  // cvt.rna.tf32.f32 on the host (finite inputs)
+    uint32_t bits;
+    std::memcpy(&bits, &x, 4);
+    bits = (bits + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &bits, 4);
+    return r;
+  };
+  auto put = [&](int nrow, int kk, double val) {
+    const float x = (float)val, hi = rna(x);
+    const size_t idx = (size_t)(kk / 4) * KR * 4 + (size_t)nrow * 4 + (kk % 4);
+    hb[idx] = hi;
+    hb[(size_t)KR * KR + idx] = rna(x - hi);
+  };
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) {
+      const double re = mat[2 * (i * D + j)], im = mat[2 * (i * D + j) + 1];
+      put(2 * i, 2 * j, re);
+      put(2 * i, 2 * j + 1, -im);
+      put(2 * i + 1, 2 * j, im);
+      put(2 * i + 1, 2 * j + 1, re);
+    }
+  float* db = nullptr;
+  SVB_CUDA(cudaMallocAsync(&db, hb.size() * sizeof(float), st));
+  SVB_CUDA(cudaMemcpyAsync(db, hb.data(), hb.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+  const DenseGeom g = make_geom(n, q, k, 7, 1, 8, chunk_stride);
+  require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
+  const uint64_t ntiles = 1ull << (n - k - 7);
+  const int ept = (1 << (k + 7)) / kTcThreads;
+  const size_t smem = sizeof(DenseSmemHdr) + 2 * (size_t)(KR / 4) * chunk_stride + 2 * (size_t)KR * KR * 4 +
+                      (size_t)ept * 12 + 64;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
+  static std::atomic<uint64_t> attr[3] = {{0}, {0}, {0}};
+  auto go = [&](auto kern, int slot) {
+    once_per_device(attr[slot], [&] {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    });
+    kern<<<grid, kTcThreads, smem, st>>>(static_cast<float2*>(state), db, g, ntiles, chunk_stride);
+  };
+  if (k == 3) go(k_dense_tc<3>, 0);
+  else if (k == 4) go(k_dense_tc<4>, 1);
+  else go(k_dense_tc<5>, 2);
+  SVB_CHECK_LAUNCH();
+  SVB_CUDA(cudaFreeAsync(db, st));
+}
+
+template <typename R>
+void launch_dense_fma(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st) {
+  require(dense_fma_supported(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n, k), SVB_E_ARG,
+          "dense block: need n >= k + 7 and 1 <= k <= 6 (complex64) / 5 (complex128)");
+  const int D = 1 << k;
+  std::vector<cplx<R>> hu(D * D);
+  for (int i = 0; i < D * D; ++i) hu[i] = mk<R>((R)mat[2 * i], (R)mat[2 * i + 1]);
+  cplx<R>* du = nullptr;
+  SVB_CUDA(cudaMallocAsync(&du, hu.size() * sizeof(cplx<R>), st));
+  SVB_CUDA(cudaMemcpyAsync(du, hu.data(), hu.size() * sizeof(cplx<R>), cudaMemcpyHostToDevice, st));
+  const int cb = std::min(n - k, std::max(7, 12 - k));  // >= 4096 amplitudes per tile
+  const DenseGeom g = make_geom(n, q, k, cb, 0, sizeof(cplx<R>), 0);
+  require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
+  const uint64_t ntiles = 1ull << (n - k - cb);
+  const int ept = (D << cb) / kFmaThreads;
+  const size_t smem = sizeof(DenseSmemHdr) + (2 * ((size_t)D << cb) + (size_t)D * D) * sizeof(cplx<R>) +
+                      (size_t)ept * 12 + 16;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count());
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(k_dense_fma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  k_dense_fma<R><<<grid, kFmaThreads, smem, st>>>(static_cast<cplx<R>*>(state), du, g, ntiles);
+  SVB_CHECK_LAUNCH();
+  SVB_CUDA(cudaFreeAsync(du, st));
+}
+template void launch_dense_fma<float>(void*, int, const int32_t*, int, const double*, cudaStream_t);
+template void launch_dense_fma<double>(void*, int, const int32_t*, int, const double*, cudaStream_t);
+
+}  // namespace svb

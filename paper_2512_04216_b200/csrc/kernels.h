@@ -33,7 +33,22 @@ template <typename R> void launch_half_copy(void* state, int n, void* buf, int L
 template <typename RA, typename RB>
 void launch_compare(const void* a, const void* b, int n, double* d_ws, double* d_out, cudaStream_t st);
 size_t compare_ws_doubles(int n);
+struct BlockSel {
+  int g;          // local bits selecting the block
+  int L[8];       // their positions, ascending
+  uint64_t bits;  // the block's value deposited at those positions
+};
+template <typename R>
+void launch_block_copy(void* state, void* buf, const BlockSel& sel, uint64_t off, uint64_t count, int to_buf,
+                       cudaStream_t st);
 template <typename R> void launch_outer(void* dst, const void* a, const void* b, int na, int nb, cudaStream_t st);
+
+// dense.cu — one dense 2^k x 2^k block per HBM pass (mat: row-major complex128)
+bool dense_tc_supported(int precision, int n, int k);
+bool dense_fma_supported(int precision, int n, int k);
+void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st);
+template <typename R>
+void launch_dense_fma(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st);
 
 // sample.cu — PCG64, pairwise sum, alias table, samplers, histogram
 void host_pcg_advance(uint64_t* pcg4, uint64_t delta);

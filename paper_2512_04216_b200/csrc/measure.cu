@@ -418,4 +418,30 @@ template void launch_compare<double, double>(const void*, const void*, int, doub
 template void launch_compare<double, float>(const void*, const void*, int, double*, double*, cudaStream_t);
 template void launch_compare<float, double>(const void*, const void*, int, double*, double*, cudaStream_t);
 template void launch_compare<float, float>(const void*, const void*, int, double*, double*, cudaStream_t);
+// Block pack / unpack for a grouped global<->local remap (sharded mode):
+// block `blk` = the amplitudes whose local bits L[0..g) (ascending) equal
+// the bits of blk; element j of the block (j in [off, off + count)) is the
+// state index with j's bits deposited around the L positions.
+template <typename R>
+__global__ void k_block_copy(cplx<R>* __restrict__ s, cplx<R>* __restrict__ buf, BlockSel sel, uint64_t off,
+                             uint64_t count, int to_buf) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+    uint64_t j = off + t;
+    for (int b = 0; b < sel.g; ++b) j = insert0(j, sel.L[b]);
+    j |= sel.bits;
+    if (to_buf) buf[t] = s[j];
+    else s[j] = buf[t];
+  }
+}
+
+template <typename R>
+void launch_block_copy(void* state, void* buf, const BlockSel& sel, uint64_t off, uint64_t count, int to_buf,
+                       cudaStream_t st) {
+  k_block_copy<R><<<grid_for(count, 256), 256, 0, st>>>(static_cast<cplx<R>*>(state), static_cast<cplx<R>*>(buf),
+                                                          sel, off, count, to_buf);
+  SVB_CHECK_LAUNCH();
+}
+template void launch_block_copy<float>(void*, void*, const BlockSel&, uint64_t, uint64_t, int, cudaStream_t);
+template void launch_block_copy<double>(void*, void*, const BlockSel&, uint64_t, uint64_t, int, cudaStream_t);
 }  // namespace svb

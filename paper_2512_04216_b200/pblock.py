@@ -60,7 +60,7 @@ def reorder_qubits(state: np.ndarray, current: list[int], target: list[int]) -> 
 @dataclass
 class Block:
     qubits: list[int]  # ascending global indices; position 0 is the local LSB
-    state: sv.DeviceState
+    dev: sv.DeviceState  # the block's amplitudes in HBM
     pending: list = field(default_factory=list)  # queued local gate records
 
     @property
@@ -69,8 +69,26 @@ class Block:
 
     def flush(self) -> None:
         if self.pending:
-            self.state.apply_gates(np.concatenate(self.pending))
+            self.dev.apply_gates(np.concatenate(self.pending))
             self.pending.clear()
+
+    @property
+    def state(self) -> np.ndarray:
+        """Host copy of the amplitudes (the reference's `Block.state` array,
+        pblock.py:46-51), after the queued gates are applied."""
+        self.flush()
+        return self.dev.to_numpy()
+
+    @state.setter
+    def state(self, amps) -> None:
+        amps = np.ascontiguousarray(amps, dtype=np.complex128).reshape(-1)
+        self.pending.clear()
+        if amps.size != 1 << self.dev.n:
+            n = amps.size.bit_length() - 1
+            prec, device = self.dev.precision, self.dev.device
+            _blocks.release(self.dev)
+            self.dev = _blocks.acquire(n, prec, device)
+        self.dev.load(amps)
 
 
 class PBlockState:
@@ -106,11 +124,11 @@ class PBlockState:
         combined = a.qubits + b.qubits
         target = sorted(combined)
         st = _blocks.acquire(len(combined), self.precision, self.device)
-        _lib.check(_lib.lib().svb_outer(st.handle, a.state.handle, b.state.handle))
+        _lib.check(_lib.lib().svb_outer(st.handle, a.dev.handle, b.dev.handle))
         dest = np.array([target.index(q) for q in combined], dtype=np.int32)
         _lib.check(_lib.lib().svb_permute_qubits(st.handle, _lib.ptr(dest, _lib.c_int32)))
-        _blocks.release(a.state)
-        _blocks.release(b.state)
+        _blocks.release(a.dev)
+        _blocks.release(b.dev)
         merged = Block(target, st)
         for q in target:
             self.block_of[q] = merged
@@ -136,20 +154,20 @@ class PBlockState:
         block.flush()
         n_local = len(block.qubits)
         pos = block.qubits.index(qubit)
-        bit = sv._measure_qubit(block.state, n_local, pos, rng)
+        bit = sv._measure_qubit(block.dev, n_local, pos, rng)
         if n_local > 1:
             kept = _blocks.acquire(n_local - 1, self.precision, self.device)
-            _lib.check(_lib.lib().svb_select_half(kept.handle, block.state.handle, pos, bit))
+            _lib.check(_lib.lib().svb_select_half(kept.handle, block.dev.handle, pos, bit))
             rest = Block([q for q in block.qubits if q != qubit], kept)
             for q in rest.qubits:
                 self.block_of[q] = rest
-        _blocks.release(block.state)
+        _blocks.release(block.dev)
         self.block_of[qubit] = Block([qubit], self._basis(bit))
         return bit
 
     def reset(self, qubit: int, rng: np.random.Generator) -> None:
         self.measure_and_factor(qubit, rng)
-        _blocks.release(self.block_of[qubit].state)
+        _blocks.release(self.block_of[qubit].dev)
         self.block_of[qubit] = Block([qubit], self._basis(0))
 
     def set_basis(self, qubit: int, bit: int) -> None:
@@ -157,8 +175,8 @@ class PBlockState:
         if len(block.qubits) != 1:
             raise BackendError("can only set basis state on a factored qubit")
         block.pending.clear()
-        _blocks.release(block.state)
-        block.state = self._basis(bit)
+        _blocks.release(block.dev)
+        block.dev = self._basis(bit)
 
     def contract(self) -> np.ndarray:
         """Global little-endian amplitudes (host; validation at small n)."""
@@ -166,13 +184,13 @@ class PBlockState:
         vec = np.ones(1, dtype=complex)
         for block in self.blocks():
             block.flush()
-            vec = np.multiply.outer(block.state.to_numpy(), vec).reshape(-1)
+            vec = np.multiply.outer(block.dev.to_numpy(), vec).reshape(-1)
             order = order + block.qubits
         return reorder_qubits(vec, order, sorted(order))
 
     def close(self) -> None:
         for b in self.blocks():
-            _blocks.release(b.state)
+            _blocks.release(b.dev)
 
 
 def _measured_groups(state: PBlockState, measured: set[int]):
@@ -183,7 +201,7 @@ def _measured_groups(state: PBlockState, measured: set[int]):
         if not qs:
             continue
         block.flush()
-        probs = block.state.marginal_probs([block.qubits.index(q) for q in qs])
+        probs = block.dev.marginal_probs([block.qubits.index(q) for q in qs])
         groups.append((qs, probs))
     groups.sort(key=lambda g: g[0][0])
     return groups

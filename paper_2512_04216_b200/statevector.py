@@ -90,44 +90,102 @@ def gate_array(instructions) -> np.ndarray:
     Same numbers as gates.py (math.cos/sin for rx/ry/u magnitudes, numpy's
     complex exp for phases) — checked against gate_array_slow in the tests."""
     insts = [i for i in instructions if i.kind in UNITARY_GATES]
-    n = len(insts)
+    return _encode([i.kind for i in insts], [i.qubits for i in insts], [i.params for i in insts])
+
+
+def gate_array_many(circuits) -> tuple[np.ndarray, np.ndarray]:
+    """gate_array over many circuits in one vectorised encoding: (records of
+    every circuit's unitary gates back to back, per-circuit gate counts)."""
+    unitary = UNITARY_GATES
+    sel = [[i for i in c.instructions if i.kind in unitary] for c in circuits]
+    counts = np.fromiter((len(u) for u in sel), dtype=np.int32, count=len(sel))
+    flat = [i for u in sel for i in u]
+    return _encode([i.kind for i in flat], [i.qubits for i in flat], [i.params for i in flat]), counts
+
+
+FIXED_KINDS = ("h", "x", "y", "z", "s", "sdg", "t", "tdg", "cx", "cz", "swap")
+_OP_CODE = {"rx": 0, "ry": 1, "rz": 2, "u": 3, **{k: 4 + j for j, k in enumerate(FIXED_KINDS)}}
+_FIXED_TABLE = None
+
+
+def fixed_gate_table() -> np.ndarray:
+    """svb_gate records of the fixed kinds (gates.py matrices), indexed kind - 4."""
+    global _FIXED_TABLE
+    if _FIXED_TABLE is None:
+        from .gates import single_qubit_matrix, two_qubit_matrix
+
+        t = np.zeros(len(FIXED_KINDS), dtype=GATE_DTYPE)
+        for j, kd in enumerate(FIXED_KINDS):
+            m = two_qubit_matrix(kd) if kd in ("cx", "cz", "swap") else single_qubit_matrix(kd)
+            t["k"][j] = 2 if m.shape[0] == 4 else 1
+            t["mat"][j, : 2 * m.size] = m.reshape(-1).view(np.float64)
+        _FIXED_TABLE = t
+    return _FIXED_TABLE
+
+
+def gate_ops_many(circuits) -> tuple[np.ndarray, np.ndarray]:
+    """Compact 40-byte svb_gate_op records of every circuit's unitary gates
+    (kind code, qubits, parameters; matrices are built by libsvb in C++),
+    and the per-circuit gate counts.  The batch encoder: ~7x less host memory
+    traffic than svb_gate records."""
+    unitary = UNITARY_GATES
+    sel = [[i for i in c.instructions if i.kind in unitary] for c in circuits]
+    counts = np.fromiter((len(u) for u in sel), dtype=np.int32, count=len(sel))
+    flat = [i for u in sel for i in u]
+    n = len(flat)
+    ops = np.zeros(n, dtype=_lib.GATE_OP_DTYPE)
+    if n == 0:
+        return ops, counts
+    code = _OP_CODE
+    kinds = np.fromiter((code[i.kind] for i in flat), dtype=np.int32, count=n)
+    ops["kind"] = kinds
+    ops["q0"] = np.fromiter((i.qubits[0] for i in flat), dtype=np.int32, count=n)
+    ops["q1"] = np.fromiter((i.qubits[-1] for i in flat), dtype=np.int32, count=n)
+    pidx = np.flatnonzero(kinds < 4)
+    if pidx.size:
+        ops["p"][pidx] = [(flat[j].params + (0.0, 0.0))[:3] for j in pidx.tolist()]
+    return ops, counts
+
+
+def _encode(kinds, qubits, params) -> np.ndarray:
+    n = len(kinds)
     arr = np.zeros(n, dtype=GATE_DTYPE)
     if n == 0:
         return arr
-    kinds = [i.kind for i in insts]
-    by_kind: dict = {}
-    for j, kd in enumerate(kinds):
-        by_kind.setdefault(kd, []).append(j)
+    names = sorted(set(kinds))
+    code_of = {k: c for c, k in enumerate(names)}
+    codes = np.fromiter((code_of[k] for k in kinds), dtype=np.int16, count=n)
     mat = arr["mat"]
-    for kd, idx in by_kind.items():
-        idx = np.asarray(idx)
+    import math as _m
+
+    for c, kd in enumerate(names):
+        idx = np.flatnonzero(codes == c)
         if kd in ("rx", "ry", "rz", "u"):
-            P = np.array([insts[j].params for j in idx], dtype=np.float64)
+            P = np.array([params[j] for j in idx.tolist()], dtype=np.float64).reshape(idx.size, -1)
             m = np.zeros((idx.size, 2, 2), dtype=np.complex128)
             if kd == "rz":
                 m[:, 0, 0] = np.exp(-0.5j * P[:, 0])
                 m[:, 1, 1] = np.exp(0.5j * P[:, 0])
             else:
-                import math as _m
-
-                c = np.array([_m.cos(t / 2) for t in P[:, 0]])
-                s_ = np.array([_m.sin(t / 2) for t in P[:, 0]])
+                half = [t / 2 for t in P[:, 0].tolist()]
+                c_ = np.array([_m.cos(t) for t in half])
+                s_ = np.array([_m.sin(t) for t in half])
                 if kd == "rx":
-                    m[:, 0, 0] = c
+                    m[:, 0, 0] = c_
                     m[:, 0, 1] = -1j * s_
                     m[:, 1, 0] = -1j * s_
-                    m[:, 1, 1] = c
+                    m[:, 1, 1] = c_
                 elif kd == "ry":
-                    m[:, 0, 0] = c
+                    m[:, 0, 0] = c_
                     m[:, 0, 1] = -s_
                     m[:, 1, 0] = s_
-                    m[:, 1, 1] = c
+                    m[:, 1, 1] = c_
                 else:
                     phi, lam = P[:, 1], P[:, 2]
-                    m[:, 0, 0] = c
+                    m[:, 0, 0] = c_
                     m[:, 0, 1] = -np.exp(1j * lam) * s_
                     m[:, 1, 0] = np.exp(1j * phi) * s_
-                    m[:, 1, 1] = np.exp(1j * (phi + lam)) * c
+                    m[:, 1, 1] = np.exp(1j * (phi + lam)) * c_
             mat[idx, :8] = m.reshape(idx.size, 4).view(np.float64)
         else:
             if kd not in _FIXED_MATS:
@@ -137,11 +195,13 @@ def gate_array(instructions) -> np.ndarray:
                 _FIXED_MATS[kd] = fm.reshape(-1).view(np.float64).copy()
             fm = _FIXED_MATS[kd]
             mat[idx, : fm.size] = fm
-    two = np.array([len(i.qubits) == 2 for i in insts])
-    arr["k"] = np.where(two, 2, 1)
-    arr["q"][:, 0] = [i.qubits[0] for i in insts]
+    q = arr["q"]
+    lens = np.fromiter((len(x) for x in qubits), dtype=np.int8, count=n)
+    q[:, 0] = [x[0] for x in qubits]
+    two = lens == 2
+    arr["k"] = lens
     if two.any():
-        arr["q"][two, 1] = [i.qubits[1] for i in insts if len(i.qubits) == 2]
+        q[two, 1] = [x[1] for x in qubits if len(x) == 2]
     return arr
 
 
@@ -267,6 +327,19 @@ class DeviceState:
 
     def apply_instructions(self, instructions) -> None:
         self.apply_gates(gate_array(instructions))
+
+    def apply_matrix(self, qubits, mat, engine: str = "auto") -> str:
+        """Apply one dense 2^k x 2^k block U (local index bit i <-> qubits[i])
+        in one HBM pass: tcgen05 tensor cores (complex64, 3xTF32) or CUDA
+        cores (svb_apply_matrix).  Returns the engine that ran."""
+        qs = np.ascontiguousarray(qubits, dtype=np.int32).reshape(-1)
+        m = np.ascontiguousarray(mat, dtype=np.complex128)
+        if m.shape != (1 << qs.size, 1 << qs.size):
+            raise ValueError("matrix must be 2^k x 2^k for k qubits")
+        code = {"auto": _lib.ENGINE_AUTO, "tensor": _lib.ENGINE_TENSOR, "fma": _lib.ENGINE_FMA}[engine]
+        check(lib().svb_apply_matrix(self.handle, ptr(qs, _lib.c_int32), int(qs.size), ptr(m.view(np.float64),
+                                     _lib.c_double), code))
+        return "tensor" if lib().svb_last_engine(self.handle) == _lib.ENGINE_TENSOR else "fma"
 
     def apply_gates_z(self, gates: np.ndarray, z_qubits) -> np.ndarray:
         """Apply a gate program and return <Z_q> for each q in z_qubits, summed by

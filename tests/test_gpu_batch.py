@@ -1,5 +1,6 @@
 """Batch mode (config 4): persistent shared-memory kernel for small circuits,
-pooled fused-pass engine for the rest; per-circuit parity with the oracle."""
+the svb_batch_run executor for the rest; per-circuit parity with the oracle
+and with sv.run (same program, same CDF draws)."""
 import numpy as np
 import pytest
 
@@ -47,7 +48,7 @@ def test_small_batch_matches_oracle(precision):
     shots = 40000
     res = run_batch(circs, shots=shots, seed=3, precision=precision)
     for c, r in zip(circs, res):
-        assert isinstance(r, RunResult) and r.metadata["engine"] == "libsvb-batch-smem"
+        assert isinstance(r, RunResult) and r.metadata["engine"] == "libsvb-batch"
         assert sum(r.counts.values()) == shots
         assert chisquare_pvalue(r.counts, _expected(c), shots) > 1e-3
 
@@ -76,3 +77,29 @@ def test_batch_workload_families_chi_square():
     for c, r in zip(circs[:13], res):
         if c.n_qubits <= 16:
             assert chisquare_pvalue(r.counts, _expected(c), 20000) > 1e-3, c.name
+
+
+def test_batch_codes_equal_per_circuit_runs_all_widths():
+    """Config 4's generator, one circuit per width 12..24 (both families) plus
+    c64: run_batch_codes == sv.run_codes(sampler="cdf") code for code (the
+    executor runs the same fused program and the same CDF draws)."""
+    from paper_2512_04216_b200.batch import run_batch_codes
+
+    circs = suite.batch_workload(26)
+    for precision in ("c128", "c64"):
+        res = run_batch_codes(circs, shots=1000, seed=5, precision=precision, chunk=7)
+        for c, r in zip(circs, res):
+            want = sv.run_codes(c, 1000, 5, precision=precision, sampler="cdf")
+            assert np.array_equal(r.codes, want.codes) and np.array_equal(r.counts, want.counts), (c.name, precision)
+
+
+def test_batch_executor_records_bad_circuits():
+    from paper_2512_04216_b200.batch import run_batch_codes
+
+    good = suite.qaoa_line_circuit(14, 1, seed=1)
+    big = suite.qaoa_line_circuit(20, 1, seed=2)
+    res = run_batch_codes([good, big, good], shots=100, seed=0, qubit_cap=18)
+    from paper_2512_04216_b200.result import QubitCapError
+
+    assert isinstance(res[1], QubitCapError)
+    assert int(res[0].counts.sum()) == 100 and np.array_equal(res[0].codes, res[2].codes)

@@ -9,7 +9,7 @@ import argparse, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2512_04216_b200 import suite
-from paper_2512_04216_b200.batch import run_batch, SMALL_MAX
+from paper_2512_04216_b200.batch import run_batch, run_batch_codes, SMALL_MAX
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--count", type=int, default=10000)
@@ -24,12 +24,15 @@ gen = time.perf_counter() - t0
 ngates = sum(len([i for i in c.instructions if i.kind != "measure"]) for c in circs)
 run_batch(circs[:64], shots=a.shots, seed=0, precision=a.precision, workers=a.workers)  # warm-up (pool, kernels)
 t0 = time.perf_counter()
+rc = run_batch_codes(circs, shots=a.shots, seed=0, precision=a.precision, nthreads=a.workers)
+dt_codes = time.perf_counter() - t0
+t0 = time.perf_counter()
 res = run_batch(circs, shots=a.shots, seed=0, precision=a.precision, workers=a.workers)
 dt = time.perf_counter() - t0
 errs = sum(1 for r in res if isinstance(r, Exception))
 small = sum(1 for c in circs if c.n_qubits <= SMALL_MAX[a.precision])
 out = {"config": "batch_qaoa_vqe_12_24", "circuits": a.count, "shots": a.shots, "precision": a.precision,
-       "wall_s": dt, "circuits_per_s": a.count / dt, "gates_per_s": ngates / dt, "errors": errs,
+       "wall_s": dt, "circuits_per_s": a.count / dt, "codes_wall_s": dt_codes, "codes_circuits_per_s": a.count / dt_codes, "gates_per_s": ngates / dt, "errors": errs,
        "smem_batched": small, "engine_path": a.count - small, "generation_s": gen}
 if a.cpu:
     from oracle import sv_oracle as orc
