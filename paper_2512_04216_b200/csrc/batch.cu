@@ -11,6 +11,7 @@
 // the shot codes out.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -487,6 +488,8 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     uint64_t* dcodes = nullptr;
     SVB_CUDA(cudaMalloc(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc));
     const size_t s = precision == SVB_C128 ? 16 : 8;
+    // NVRTC specialisation from this many qubits up (SVB_BATCH_JIT_MIN_N, default 24)
+    static const int jit_min = std::getenv("SVB_BATCH_JIT_MIN_N") ? std::atoi(std::getenv("SVB_BATCH_JIT_MIN_N")) : 24;
     std::atomic<int> next{0};
     std::mutex err_mu;
     std::string first_err;
@@ -507,9 +510,9 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
           if (!buf) SVB_CUDA(state_malloc(&buf, s << n));  // largest first: the first size is the maximum
           bool zp = true;
           if (precision == SVB_C128)
-            run_program_owned<double>(&buf, &spare, n, gates.data(), ngates[i], 1, 24, st, &stats, &zp);
+            run_program_owned<double>(&buf, &spare, n, gates.data(), ngates[i], 1, jit_min, st, &stats, &zp);
           else
-            run_program_owned<float>(&buf, &spare, n, gates.data(), ngates[i], 1, 24, st, &stats, &zp);
+            run_program_owned<float>(&buf, &spare, n, gates.data(), ngates[i], 1, jit_min, st, &stats, &zp);
           if (zp) {
             if (precision == SVB_C128) launch_zero<double>(buf, n, st);
             else launch_zero<float>(buf, n, st);

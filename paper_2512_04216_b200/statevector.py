@@ -829,18 +829,9 @@ def plan(n: int, instructions, precision: str = "c128", zero_start: bool = False
             "permute_fused": perm.value == 2, "permute_initial": perm.value == 3, "gates": int(arr.size)}
 
 
-def emulate(n: int, instructions, amps: np.ndarray, precision: str = "c128", relabel: bool = True) -> np.ndarray:
-    """Run the fused program on the CPU emulator (test hook; same scheduler and
-    op interpreter as the device kernel).  Returns the new amplitudes."""
-    arr = gate_array(instructions)
-    out = np.ascontiguousarray(amps, dtype=np.complex128).copy()
-    check(lib().svb_emulate_apply(n, _prec_code(precision), ptr(arr), int(arr.size), ptr(out), int(relabel)))
-    return out
-
-
 __all__ = [
     "DEFAULT_QUBIT_CAP", "DeviceState", "run", "run_codes", "CodeCounts", "final_state", "expectation", "expectations",
     "zero_state", "apply_1q", "apply_2q", "apply_instruction", "marginal_probs",
-    "_measure_qubit", "_reset_qubit", "plan", "emulate", "gate_array", "pcg_words",
+    "_measure_qubit", "_reset_qubit", "plan", "gate_array", "gate_array_many", "gate_ops_many", "pcg_words",
     "ONE_QUBIT_GATES", "single_qubit_matrix",
 ]

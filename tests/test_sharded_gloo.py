@@ -1,10 +1,12 @@
-"""Sharded (global-qubit) execution over world_size 2 and 4 with gloo on CPU.
+"""Sharded (global-qubit) execution over world_size 2, 4 and 8 with gloo on CPU.
 
-Each rank runs the same planner, the same global<->local swap exchange and the
-same reductions as on GPUs; the local arithmetic uses libsvb's CPU emulator of
-the fused program (the device path differs only in where the shard lives).
-Checked against the oracle: gathered amplitudes, <Z> all-reduce, and
-distributed CDF sampling on the shared PCG64 stream."""
+Each rank runs the same planner, the same grouped all-to-all remaps (chunked,
+two stages), free relabels of untouched qubits, lazy zero shards and the same
+reductions as on GPUs; the local arithmetic uses libsvb's CPU emulator of the
+fused program (tests/sharded_emulator.py; the device path differs only in
+where the shard lives).  Checked against the oracle: gathered amplitudes,
+<Z> all-reduce, distributed CDF sampling on the shared PCG64 stream, and the
+per-remap bytes model."""
 import json
 import os
 import socket
@@ -28,8 +30,10 @@ def _worker(rank, world, port, out_dir, case):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     from paper_2512_04216_b200 import suite
-    from paper_2512_04216_b200.sharded import ShardedState
+    from paper_2512_04216_b200.sharded import ShardedState, remap_bytes
+    from sharded_emulator import EmulatedShard
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -39,18 +43,27 @@ def _worker(rank, world, port, out_dir, case):
             c = suite.random_circuit(n, case["gates"], rng, measured=False)
         elif case["kind"] == "qft":
             c = suite.qft_bench_circuit(n)
+        elif case["kind"] == "qftplain":
+            c = suite.qft(n)
         else:
             c = suite.sycamore_circuit(case["rows"], n // case["rows"], case["depth"], seed=case["seed"], measured=False)
         backend = case.get("backend", "emulate")
-        st = ShardedState(n, case["precision"], backend=backend, staging="host")
+        backend = EmulatedShard if backend == "emulate" else backend
+        st = ShardedState(n, case["precision"], backend=backend, staging="host",
+                          chunk_bytes=case.get("chunk_bytes", 1 << 29))
+        writes0 = getattr(st.shard, "writes", 0)
         st.apply(c.instructions)
+        remaps = st.remaps
+        sent = st.bytes_sent
+        relabels = st.relabels
         z = st.expectations([(q,) for q in range(n)] + [(0, n - 1), tuple(range(n))])
         counts = st.sample([(q, q) for q in range(n)], case["shots"], case["seed"] + 1)
         amps = st.gather()
         if rank == 0:
             np.save(os.path.join(out_dir, "amps.npy"), amps)
             with open(os.path.join(out_dir, "res.json"), "w") as fh:
-                json.dump({"z": list(z), "counts": counts, "swaps": st.swaps}, fh)
+                json.dump({"z": list(z), "counts": counts, "swaps": st.swaps, "remaps": remaps, "sent": sent,
+                           "relabels": relabels, "writes0": writes0}, fh)
     finally:
         dist.destroy_process_group()
 
@@ -76,6 +89,8 @@ def _oracle(case):
         c = suite.random_circuit(n, case["gates"], rng, measured=False)
     elif case["kind"] == "qft":
         c = suite.qft_bench_circuit(n)
+    elif case["kind"] == "qftplain":
+        c = suite.qft(n)
     else:
         c = suite.sycamore_circuit(case["rows"], n // case["rows"], case["depth"], seed=case["seed"], measured=False)
     psi = orc.unitary_state(c)
@@ -89,6 +104,10 @@ CASES = [
     (4, {"kind": "random", "n": 11, "gates": 150, "seed": 4, "precision": "c128", "shots": 20000}),
     (2, {"kind": "qft", "n": 11, "seed": 5, "precision": "c128", "shots": 20000}),
     (4, {"kind": "sycamore", "n": 12, "rows": 3, "depth": 8, "seed": 6, "precision": "c64", "shots": 20000}),
+    (8, {"kind": "random", "n": 12, "gates": 160, "seed": 7, "precision": "c128", "shots": 20000}),
+    (8, {"kind": "sycamore", "n": 12, "rows": 3, "depth": 10, "seed": 9, "precision": "c64", "shots": 20000,
+         "chunk_bytes": 4096}),
+    (4, {"kind": "qft", "n": 12, "seed": 10, "precision": "c128", "shots": 20000, "chunk_bytes": 2048}),
 ]
 
 
@@ -108,6 +127,7 @@ def test_sharded_matches_oracle(world, case):
     assert chisquare_pvalue(res["counts"], expected, case["shots"]) > 1e-3
     if case["kind"] != "qft":
         assert res["swaps"] > 0  # the circuit touched global qubits non-diagonally
+    assert res["writes0"] == 0  # lazy zero: no shard was written before the first exchange
 
 
 def test_sharded_counts_independent_of_rank_count():
@@ -143,3 +163,27 @@ def test_sharded_device_shards_host_staged(world, case):
     probs = np.abs(psi) ** 2
     expected = {format(i, f"0{n}b"): float(p) for i, p in enumerate(probs) if p > 1e-14}
     assert chisquare_pvalue(res["counts"], expected, case["shots"]) > 1e-3
+
+
+def test_grouped_remap_bytes_model_and_relabels():
+    """Grouped remaps move fewer bytes than one-qubit swaps: every remap of g'
+    qubits sends (1 - 2^-g') of the shard per rank (the bytes model), QFT's
+    first global gates are free relabels (untouched qubits), and a remap
+    moves several qubits at once on 8 ranks."""
+    import math
+
+    case = {"kind": "random", "n": 12, "gates": 200, "seed": 21, "precision": "c128", "shots": 4000}
+    _, res = _run(8, case)
+    nl, item = 12 - 3, 16
+    shard = item << nl
+    assert res["remaps"] > 0 and res["swaps"] >= res["remaps"]
+    # bytes per rank <= remaps * (1 - 2^-3) * shard, and each remap sends >= half a shard
+    assert res["sent"] <= res["remaps"] * (shard - (shard >> 3))
+    assert res["sent"] >= res["remaps"] * (shard >> 1)
+    assert res["swaps"] > res["remaps"]  # at least one remap grouped several qubits
+    q = {"kind": "qftplain", "n": 12, "seed": 22, "precision": "c128", "shots": 4000}
+    amps, rq = _run(4, q)
+    assert rq["relabels"] >= 1  # qft(n) starts with h on the top (global) qubit: a free relabel
+    psi, _ = _oracle(q)
+    assert np.linalg.norm(amps - psi) / np.linalg.norm(psi) < 1e-10
+    assert math.isfinite(sum(rq["z"]))
