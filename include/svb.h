@@ -114,6 +114,14 @@ int svb_destroy(svb_handle h);
 int svb_set_zero(svb_handle h);
 int svb_copy_state(svb_handle dst, svb_handle src); /* prefix.copy(), statevector.py:168 */
 int svb_n_qubits(svb_handle h);
+/* Kernel-level numpy API on device-resident memory (statevector.py:33-154 as
+ * used by calibration.py:215-228 and pblock.py:93-154): a complex128 state in
+ * CUDA managed memory (svb_managed_alloc) wrapped by a handle that does not
+ * own it (svb_create_view).  Calls on the view run on the device in place;
+ * the host sees the result after the call returns (every call synchronises). */
+int svb_managed_alloc(uint64_t bytes, int device, void** out);
+int svb_managed_free(void* p);
+int svb_create_view(int n_qubits, int device, void* amps, svb_handle* out);
 
 /* Host <-> device amplitudes (final_state, statevector.py:259-274; and the
  * kernel-level numpy-array API used by pblock.py:93-154, calibration.py:215-228). */
@@ -138,7 +146,7 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
  * row-major complex128 (re, im); local index bit i <-> qubits[i].  engine:
  *   SVB_ENGINE_AUTO   tensor cores (tcgen05 kind::tf32, 3xTF32 split) for
  *                     complex64 and k >= SVB_OPT_TC_MIN_K, else CUDA cores;
- *   SVB_ENGINE_TENSOR tensor cores (complex64, 3 <= k <= 5), else SVB_E_ARG;
+ *   SVB_ENGINE_TENSOR tensor cores (complex64, 3 <= k <= 6), else SVB_E_ARG;
  *   SVB_ENGINE_FMA    CUDA cores (k <= 6 complex64, k <= 5 complex128).
  * Needs n >= k + 7.  svb_last_engine reports which engine ran. */
 typedef enum { SVB_ENGINE_AUTO = 0, SVB_ENGINE_TENSOR = 1, SVB_ENGINE_FMA = 2 } svb_engine;

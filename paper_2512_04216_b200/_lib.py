@@ -63,6 +63,9 @@ _SIGS = {
     "svb_profile_passes": (c_int, [_h, _dp, c_int, _i32p]),
     "svb_create": (c_int, [c_int, c_int, c_int, POINTER(c_void_p)]),
     "svb_destroy": (c_int, [_h]),
+    "svb_managed_alloc": (c_int, [c_uint64, c_int, POINTER(c_void_p)]),
+    "svb_managed_free": (c_int, [c_void_p]),
+    "svb_create_view": (c_int, [c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "svb_set_zero": (c_int, [_h]),
     "svb_copy_state": (c_int, [_h, _h]),
     "svb_n_qubits": (c_int, [_h]),

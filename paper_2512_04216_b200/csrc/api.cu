@@ -30,6 +30,7 @@ struct svb_state {
   int jit_min_n = 24;  // NVRTC-specialised passes from this many qubits up (-1: never)
   int tc_min_k = 5;    // svb_apply_matrix: tensor cores for dense blocks of >= this many qubits (complex64)
   int last_engine = 0;
+  void* external = nullptr;  // svb_create_view: caller-owned amplitudes (never freed, always current)
   ProgramStats stats{};
   Profiler prof;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -70,6 +71,15 @@ static void materialize(svb_handle h) {
 static void check_handle(svb_handle h) {
   check_handle_nomat(h);
   materialize(h);
+}
+
+// A view's amplitudes must stay in the caller's buffer: when a program ended
+// with an out-of-place permutation into the spare buffer, copy back.
+static void restore_view(svb_handle h) {
+  if (!h->external || h->amps == h->external) return;
+  SVB_CUDA(cudaMemcpyAsync(h->external, h->amps, h->amp_bytes(), cudaMemcpyDeviceToDevice, h->st));
+  h->spare = h->amps;
+  h->amps = h->external;
 }
 
 static void ensure_ws(svb_handle h, size_t doubles) {
@@ -162,6 +172,52 @@ int svb_create(int n_qubits, int precision, int device, svb_handle* out) {
   return SVB_OK;
 }
 
+// Managed (unified) memory for the kernel-level numpy API: zero_state()
+// returns an array in this memory, so apply_1q / apply_2q / marginal_probs on
+// it run on the device with no host<->device copy (pages migrate on demand
+// and stay in HBM while only kernels touch them).
+int svb_managed_alloc(uint64_t bytes, int device, void** out) {
+  return guard([&] {
+    SVB_CUDA(cudaSetDevice(device));
+    SVB_CUDA(cudaMallocManaged(out, bytes, cudaMemAttachGlobal));
+    cudaMemLocation loc{};
+    loc.type = cudaMemLocationTypeDevice;
+    loc.id = device;
+    cudaMemAdvise(*out, bytes, cudaMemAdviseSetPreferredLocation, loc);
+    cudaGetLastError();
+  });
+}
+int svb_managed_free(void* p) {
+  return guard([&] { SVB_CUDA(cudaFree(p)); });
+}
+
+int svb_create_view(int n_qubits, int device, void* amps, svb_handle* out) {
+  svb_state* h = nullptr;
+  int rc = guard([&] {
+    require(n_qubits >= 1 && n_qubits <= 40 && amps != nullptr, SVB_E_ARG, "bad view");
+    SVB_CUDA(cudaSetDevice(device));
+    h = new svb_state();
+    h->n = n_qubits;
+    h->prec = SVB_C128;
+    h->device = device;
+    h->amps = amps;
+    h->external = amps;
+    SVB_CUDA(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    SVB_CUDA(cudaMalloc(&h->d_rng, 4 * sizeof(uint64_t) + 16));
+    h->d_outcome = reinterpret_cast<int32_t*>(h->d_rng + 4);
+  });
+  if (rc != SVB_OK) {
+    if (h) {
+      if (h->st) cudaStreamDestroy(h->st);
+      delete h;
+    }
+    *out = nullptr;
+    return rc;
+  }
+  *out = h;
+  return SVB_OK;
+}
+
 int svb_destroy(svb_handle h) {
   if (!h) return SVB_OK;
   return guard([&] {
@@ -169,8 +225,8 @@ int svb_destroy(svb_handle h) {
     SVB_CUDA(cudaStreamSynchronize(h->st));
     if (h->d_ws) cudaFreeAsync(h->d_ws, h->st);
     SVB_CUDA(cudaStreamSynchronize(h->st));
-    cudaFree(h->amps);
-    if (h->spare) cudaFree(h->spare);
+    if (h->amps != h->external) cudaFree(h->amps);
+    if (h->spare && h->spare != h->external) cudaFree(h->spare);
     cudaFree(h->d_rng);
     if (h->t0) cudaEventDestroy(h->t0);
     if (h->t1) cudaEventDestroy(h->t1);
@@ -212,6 +268,10 @@ int svb_set_zero(svb_handle h) {
   return guard([&] {
     check_handle_nomat(h);
     h->zero_pending = true;  // lazy: written by the first consumer (or synthesised by the next pass)
+    if (h->external) {       // a view is read by the host directly: write it now
+      materialize(h);
+      SVB_CUDA(cudaStreamSynchronize(h->st));
+    }
   });
 }
 
@@ -297,6 +357,7 @@ int svb_apply(svb_handle h, const svb_gate* gates, int n_gates) {
       run_program_owned<double>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats, &h->zero_pending);
     else
       run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats, &h->zero_pending);
+    restore_view(h);
     auto t1 = std::chrono::steady_clock::now();
     SVB_CUDA(cudaStreamSynchronize(h->st));
     if (h->prof.on) h->prof.collect();
@@ -334,6 +395,7 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
     else
       run_program_owned<float>(&h->amps, &h->spare, h->n, gates, n_gates, h->fusion, h->jit_min_n, h->st, &h->stats,
                                &h->zero_pending, &z);
+    restore_view(h);
     if (nz == 0) {
       SVB_CUDA(cudaStreamSynchronize(h->st));
       if (h->prof.on) h->prof.collect();
@@ -477,7 +539,7 @@ int svb_apply_matrix(svb_handle h, const int32_t* qubits, int k, const double* m
     }
     const bool tc = dense_tc_supported(h->prec, h->n, k);
     require(engine != SVB_ENGINE_TENSOR || tc, SVB_E_ARG,
-            "tensor-core engine needs complex64, 3 <= k <= 5 and n >= k + 7");
+            "tensor-core engine needs complex64, 3 <= k <= 6 and n >= k + 7");
     const bool use_tc = engine == SVB_ENGINE_TENSOR || (engine == SVB_ENGINE_AUTO && tc && k >= h->tc_min_k);
     Profiler* pf = h->prof.on ? &h->prof : nullptr;
     if (pf) pf->begin(h->st, 0, 2.0 * (double)h->amp_bytes(), 0);
@@ -782,6 +844,7 @@ int svb_permute_qubits(svb_handle h, const int32_t* dest) {
     }
     if (h->prec == SVB_C128) run_permutation<double>(&h->amps, &h->spare, h->n, d, h->st, &h->stats);
     else run_permutation<float>(&h->amps, &h->spare, h->n, d, h->st, &h->stats);
+    restore_view(h);
     SVB_CUDA(cudaStreamSynchronize(h->st));
   });
 }

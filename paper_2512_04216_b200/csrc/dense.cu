@@ -8,7 +8,8 @@
 // tile of 128 columns (2^(k+7) amplitudes: the block qubits plus the 7 lowest
 // other qubits, so warps read 256 contiguous bytes) in shared memory.
 //
-// * k_dense_tc (complex64, 3 <= k <= 5): the block is a real GEMM on the
+// * k_dense_tc (complex64, 3 <= k <= 5; k_dense_tc6 for k = 6, with the
+//   unitary as the TMEM operand): the block is a real GEMM on the
 //   5th-generation tensor cores.  With x in interleaved real form
 //   (x_re, x_im per amplitude) D[c][2i+e] = sum_kk A[c][kk] * B[2i+e][kk],
 //   A = the tile (M = 128 columns, K = 2^(k+1)), B = U in real form
@@ -43,7 +44,7 @@ namespace svb {
 
 constexpr int kDenseCols = 128;  // columns per tile (= UMMA M)
 constexpr int kDenseMaxK = 6;
-constexpr int kTcMaxK = 5;
+constexpr int kTcMaxK = 6;
 
 struct DenseGeom {
   int k = 0;          // block qubits
@@ -279,6 +280,160 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   }
 }
 
+// ---------------------------------------------- k = 6: U as the TMEM operand
+// For 6-qubit blocks the real-form unitary (128 x 128 fp32, hi and lo) does
+// not fit in shared memory next to the tile, so the roles swap: A = U lives in
+// TMEM (lane = output row, columns = K; written once per CTA with
+// tcgen05.st), B = the tile (N = 128 state columns, K = 128 reals) in shared
+// memory, D[out][column] in TMEM.  3-term split (U_lo X_hi, U_hi X_lo,
+// U_hi X_hi).  TMEM: U_hi [0,128), U_lo [128,256), D [256,384).
+constexpr int kTc6Threads = 256;
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+
+// usrc: real-form U rows (128 x 128 fp32, row-major) hi then lo
+__global__ void __launch_bounds__(kTc6Threads, 1)
+    k_dense_tc6(float2* __restrict__ state, const float* __restrict__ usrc, const DenseGeom g, uint64_t ntiles,
+                uint32_t chunk_stride) {
+  constexpr int KR = 128;
+  constexpr int EPT = (1 << 13) / kTc6Threads;  // 32
+  constexpr int NCH = KR / 4;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
+  const uint32_t xbytes = NCH * chunk_stride;
+  uint8_t* xhi = smem + sizeof(DenseSmemHdr);
+  uint8_t* xlo = xhi + xbytes;
+  uint64_t* git = reinterpret_cast<uint64_t*>(xlo + xbytes);
+  uint32_t* sit = reinterpret_cast<uint32_t*>(git + EPT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sit + EPT);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3;
+
+  dense_it_tables<kTc6Threads>(g, EPT, git, sit);
+  dense_tile_tables(g, hdr);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "n"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t t_uhi = tmem, t_ulo = tmem + 128, t_d = tmem + 256;
+  {  // U rows into TMEM: warps 0-3 the hi half, warps 4-7 the lo half; lane = row
+    const int row = 32 * quad + lane;
+    const float* src = usrc + (warp >= 4 ? KR * KR : 0) + (size_t)row * KR;
+    const uint32_t base = (warp >= 4 ? t_ulo : t_uhi) + ((32 * quad) << 16);
+#pragma unroll
+    for (int c = 0; c < KR; c += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = src[c + i];
+      tmem_st16(base + c, v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint64_t goff;
+  uint32_t soff;
+  dense_thread_offsets<kTc6Threads>(g, tid, goff, soff);
+  // M = 128 (U rows), N = 128 (state columns), TF32 A (TMEM) and B (smem), F32 D
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  uint32_t phase = 0;
+
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
+  };
+  auto step = [&](float2 (&cur)[EPT], float2 (&nxt)[EPT], uint64_t t) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+    if (t + gridDim.x < ntiles) load(nxt, t + gridDim.x);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(cur[i].x), hy = tf32_rna(cur[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(xhi + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(xlo + o) = make_float2(tf32_rna(cur[i].x - hx), tf32_rna(cur[i].y - hy));
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t b0 = smem_u32(xhi), b1 = smem_u32(xlo);
+      const uint32_t as[3] = {t_ulo, t_uhi, t_uhi}, bs[3] = {b0, b1, b0};
+#pragma unroll
+      for (int term = 0; term < 3; ++term)
+#pragma unroll
+        for (int s = 0; s < KR / 8; ++s)
+          umma_tf32_ts(t_d, as[term] + 8 * s, umma_desc(bs[term] + s * 2 * chunk_stride, chunk_stride, 128), idesc,
+                       (term | s) != 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    {  // D row n = output real index (re/im of amplitude n / 2), columns = state columns
+      const uint32_t n = 32 * quad + lane;
+      const uint32_t nb = (n >> 2) * chunk_stride + ((n >> 1) & 1) * 8 + (n & 1) * 4;
+      const int c0 = warp >= 4 ? 64 : 0;
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        float y[16];
+        tmem_ld16(t_d + ((32 * quad) << 16) + c0 + c, y);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) *reinterpret_cast<float*>(xhi + nb + (c0 + c + i) * 16) = y[i];
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(xhi + soff + sit[i]));
+    __syncthreads();
+  };
+
+  float2 va[EPT], vb[EPT];
+  const uint64_t G = gridDim.x;
+  if (blockIdx.x < ntiles) load(va, blockIdx.x);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += 2 * G) {
+    step(va, vb, t);
+    if (t + G < ntiles) step(vb, va, t + G);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512) : "memory");
+  }
+}
+
 // ----------------------------------------------------- CUDA-core baseline
 constexpr int kFmaThreads = 256;
 constexpr int kFmaOut = 8;  // outputs accumulated per thread per sweep over the inputs
@@ -286,7 +441,7 @@ constexpr int kFmaOut = 8;  // outputs accumulated per thread per sweep over the
 // smem: [hdr | X | Y | U | git | sit]; X/Y layout [j][c] complex with
 // 2^cb columns per tile (>= 4096 amplitudes per tile for small k)
 template <typename R>
-__global__ void __launch_bounds__(kFmaThreads, 1)
+__global__ void __launch_bounds__(kFmaThreads, 2)
     k_dense_fma(cplx<R>* __restrict__ state, const cplx<R>* __restrict__ u, const DenseGeom g, uint64_t ntiles) {
   const int k = g.k, D = 1 << k, cb = g.kb - g.k, cols = 1 << cb, ept = (D << cb) / kFmaThreads;
   const int ob = D < kFmaOut ? D : kFmaOut;
@@ -384,10 +539,58 @@ bool dense_fma_supported(int precision, int n, int k) {
 }
 
 // mat: 2^k x 2^k complex, row-major (re, im) doubles, local bit i <-> q[i]
+static void launch_dense_tc6(void* state, int n, const int32_t* q, const double* mat, cudaStream_t st,
+                             uint32_t chunk_stride) {
+  constexpr int D = 64, KR = 128;
+  auto rna = [](float x) {
+    uint32_t bits;
+    std::memcpy(&bits, &x, 4);
+    bits = (bits + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &bits, 4);
+    return r;
+  };
+  // real-form rows U_real[nrow][kk], row-major, hi then lo
+  std::vector<float> hu(2 * KR * KR);
+  auto put = [&](int nrow, int kk, double val) {
+    const float x = (float)val, hi = rna(x);
+    hu[(size_t)nrow * KR + kk] = hi;
+    hu[(size_t)KR * KR + (size_t)nrow * KR + kk] = rna(x - hi);
+  };
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) {
+      const double re = mat[2 * (i * D + j)], im = mat[2 * (i * D + j) + 1];
+      put(2 * i, 2 * j, re);
+      put(2 * i, 2 * j + 1, -im);
+      put(2 * i + 1, 2 * j, im);
+      put(2 * i + 1, 2 * j + 1, re);
+    }
+  float* du = nullptr;
+  SVB_CUDA(cudaMallocAsync(&du, hu.size() * sizeof(float), st));
+  SVB_CUDA(cudaMemcpyAsync(du, hu.data(), hu.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+  const DenseGeom g = make_geom(n, q, 6, 7, 1, 8, chunk_stride);
+  require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
+  const uint64_t ntiles = 1ull << (n - 13);
+  const int ept = (1 << 13) / kTc6Threads;
+  const size_t smem = sizeof(DenseSmemHdr) + 2 * (size_t)(KR / 4) * chunk_stride + (size_t)ept * 12 + 64;
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count());
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [] {
+    cudaFuncSetAttribute(k_dense_tc6, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+  });
+  k_dense_tc6<<<grid, kTc6Threads, smem, st>>>(static_cast<float2*>(state), du, g, ntiles, chunk_stride);
+  SVB_CHECK_LAUNCH();
+  SVB_CUDA(cudaFreeAsync(du, st));
+}
+
 void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st) {
-  require(k >= 3 && k <= kTcMaxK && n >= k + 7, SVB_E_ARG, "tensor-core dense block: need 3 <= k <= 5, n >= k + 7");
+  require(k >= 3 && k <= kTcMaxK && n >= k + 7, SVB_E_ARG, "tensor-core dense block: need 3 <= k <= 6, n >= k + 7");
   const int D = 1 << k, KR = 2 * D;
   const uint32_t chunk_stride = kDenseCols * 16 + 16;  // 2064 B: +16 B keeps tile writes bank-conflict free
+  if (k == 6) {
+    launch_dense_tc6(state, n, q, mat, st, chunk_stride);
+    return;
+  }
   // real form B[n_out][kk] (K-major rows), split into TF32 hi / lo, in the
   // canonical layout byte(nrow, kk) = (kk / 4) * KR * 16 + nrow * 16 + (kk % 4) * 4
   std::vector<float> hb(2 * KR * KR);
@@ -454,7 +657,8 @@ void launch_dense_fma(void* state, int n, const int32_t* q, int k, const double*
   const int ept = (D << cb) / kFmaThreads;
   const size_t smem = sizeof(DenseSmemHdr) + (2 * ((size_t)D << cb) + (size_t)D * D) * sizeof(cplx<R>) +
                       (size_t)ept * 12 + 16;
-  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count());
+  const int per_sm = smem <= 110 * 1024 ? 2 : 1;  // two CTAs per SM when their tiles fit
+  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
   static std::atomic<uint64_t> attr{0};
   once_per_device(attr, [] {
     cudaFuncSetAttribute(k_dense_fma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

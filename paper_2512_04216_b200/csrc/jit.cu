@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <shared_mutex>
 #include <sstream>
@@ -97,6 +98,7 @@ struct Module {
 
 std::mutex g_mu;
 std::unordered_map<std::string, Module> g_cache;  // key: device + source
+std::unordered_map<std::string, std::shared_ptr<std::mutex>> g_key_locks;  // in-flight compiles
 uint64_t g_tick = 0;  // LRU clock (under g_mu)
 // Bounds of the in-memory caches: programs whose coefficients are compiled in
 // as immediates (n >= 28) make a new kernel per angle set, so a parameter
@@ -843,6 +845,37 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
         todo.push_back(p);
       }
     }
+  }
+  // one compiler per kernel source: threads that need a source another thread
+  // is compiling wait for it (the batch executor's workers meet the same
+  // structures at the same time), then find it in g_cache
+  std::vector<std::unique_lock<std::mutex>> key_locks;
+  if (!todo.empty()) {
+    std::vector<std::pair<std::string, std::shared_ptr<std::mutex>>> ks;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      for (size_t p : todo) {
+        auto& m = g_key_locks[keys[p]];
+        if (!m) m = std::make_shared<std::mutex>();
+        ks.push_back({keys[p], m});
+      }
+    }
+    std::sort(ks.begin(), ks.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    ks.erase(std::unique(ks.begin(), ks.end(), [](const auto& a, const auto& b) { return a.first == b.first; }),
+             ks.end());
+    for (auto& k : ks) key_locks.emplace_back(*k.second);
+    std::lock_guard<std::mutex> lk(g_mu);
+    std::vector<size_t> still;
+    for (size_t p : todo) {
+      auto it = g_cache.find(keys[p]);
+      if (it != g_cache.end()) {
+        fns[p] = it->second.fns[0];
+        it->second.last_use = ++g_tick;
+      } else {
+        still.push_back(p);
+      }
+    }
+    todo.swap(still);
   }
   if (!todo.empty()) {
     // disk cache, then NVRTC for the rest (one thread per pass kernel)

@@ -174,18 +174,112 @@ template <typename T> static T d2h_scalar(const T* d, cudaStream_t st) {
   return h;
 }
 
-template <typename In, typename Out>
-static void cub_exclusive_sum(const In* in, Out* out, uint64_t n, cudaStream_t st) {
-  size_t bytes = 0;
-  SVB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
-  DevBuf tmp(bytes, st);
-  SVB_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
+// Device prefix sums (own kernels, fixed combine order: results are
+// reproducible run to run).  Three launches: per-CTA tile scans of 2048
+// elements (8 per thread, warp shuffles, then the 8 warp totals), one CTA
+// scanning the tile totals, and the tile offsets added back.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+
+template <typename T> __device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const T u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
 }
-static void cub_inclusive_sum(const double* in, double* out, uint64_t n, cudaStream_t st) {
-  size_t bytes = 0;
-  SVB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, (int64_t)n, st));
-  DevBuf tmp(bytes, st);
-  SVB_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, bytes, in, out, (int64_t)n, st));
+
+// inclusive scan of this CTA's tile into out (no offset), tile total to tot[b]
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const T* __restrict__ in, T* __restrict__ out,
+                                                             uint64_t n, T* __restrict__ tot, int exclusive) {
+  __shared__ T wsum[kScanThreads / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  T x[kScanItems];
+  T run = T(0);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    x[i] = base + i < n ? in[base + i] : T(0);
+    run += x[i];
+  }
+  const T incl = warp_incl_scan(run);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  T woff = T(0);
+  for (int w = 0; w < warp; ++w) woff += wsum[w];
+  T acc = woff + incl - run;  // exclusive prefix of this thread
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (exclusive) {
+      if (base + i < n) out[base + i] = acc;
+      acc += x[i];
+    } else {
+      acc += x[i];
+      if (base + i < n) out[base + i] = acc;
+    }
+  }
+  if (threadIdx.x == kScanThreads - 1) {
+    T t = T(0);
+    for (int w = 0; w < kScanThreads / 32; ++w) t += wsum[w];
+    tot[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of the tile totals in place (one CTA, sequential chunks)
+template <typename T> __global__ void __launch_bounds__(kScanThreads) k_scan_totals(T* __restrict__ tot, uint64_t nt) {
+  __shared__ T carry_s;
+  __shared__ T wsum[kScanThreads / 32];
+  if (threadIdx.x == 0) carry_s = T(0);
+  __syncthreads();
+  for (uint64_t c0 = 0; c0 < nt; c0 += kScanThreads) {
+    const uint64_t i = c0 + threadIdx.x;
+    const T v = i < nt ? tot[i] : T(0);
+    const T incl = warp_incl_scan(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    T woff = carry_s;
+    for (int w = 0; w < warp; ++w) woff += wsum[w];
+    if (i < nt) tot[i] = woff + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      T t = T(0);
+      for (int w = 0; w < kScanThreads / 32; ++w) t += wsum[w];
+      carry_s += t;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void k_scan_add(T* __restrict__ out, uint64_t n, const T* __restrict__ tot) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && i >= (uint64_t)kScanTile) out[i] += tot[i / kScanTile];
+}
+
+template <typename T> static void device_scan(const T* in, T* out, uint64_t n, bool exclusive, cudaStream_t st) {
+  if (n == 0) return;
+  const uint64_t nt = (n + kScanTile - 1) / kScanTile;
+  DevBuf tot(sizeof(T) * nt, st);
+  k_scan_tiles<T><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, tot.as<T>(), exclusive ? 1 : 0);
+  SVB_CHECK_LAUNCH();
+  if (nt > 1) {
+    k_scan_totals<T><<<1, kScanThreads, 0, st>>>(tot.as<T>(), nt);
+    SVB_CHECK_LAUNCH();
+    k_scan_add<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, tot.as<T>());
+    SVB_CHECK_LAUNCH();
+  }
+}
+
+template <typename In, typename Out>
+static void scan_exclusive(const In* in, Out* out, uint64_t n, cudaStream_t st) {
+  static_assert(sizeof(In) == sizeof(Out), "scan keeps the element type");
+  device_scan<Out>(reinterpret_cast<const Out*>(in), out, n, true, st);
+}
+static void scan_inclusive(const double* in, double* out, uint64_t n, cudaStream_t st) {
+  device_scan<double>(in, out, n, false, st);
 }
 
 // np.cumsum is a left-to-right accumulation; ties between deficit and capacity
@@ -401,7 +495,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
   k_alias_init<<<grid_for(m, B), B, 0, st>>>(d_probs, m, factor, scaled.as<double>(), d_prob_row,
                                              d_alias_row, flag.as<int64_t>());
   SVB_CHECK_LAUNCH();
-  cub_exclusive_sum(flag.as<int64_t>(), pos.as<int64_t>(), m, st);
+  scan_exclusive(flag.as<int64_t>(), pos.as<int64_t>(), m, st);
   uint64_t nl = (uint64_t)d2h_scalar(pos.as<int64_t>() + (m - 1), st) +
                 (uint64_t)d2h_scalar(flag.as<int64_t>() + (m - 1), st);
   uint64_t ns = m - nl;
@@ -440,7 +534,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     SVB_CHECK_LAUNCH();
     k_run_heads<<<grid_for(ns, B), B, 0, st>>>(owner.as<int64_t>(), ns, head.as<int64_t>());
     SVB_CHECK_LAUNCH();
-    cub_exclusive_sum(head.as<int64_t>(), hpos.as<int64_t>(), ns, st);
+    scan_exclusive(head.as<int64_t>(), hpos.as<int64_t>(), ns, st);
     k_run_starts<<<grid_for(ns, B), B, 0, st>>>(head.as<int64_t>(), hpos.as<int64_t>(), ns, starts.as<int64_t>());
     SVB_CHECK_LAUNCH();
     const uint64_t nruns = (uint64_t)d2h_scalar(hpos.as<int64_t>() + (ns - 1), st) +
@@ -458,7 +552,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     }
     k_conv_flags<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, conv.as<int64_t>());
     SVB_CHECK_LAUNCH();
-    cub_exclusive_sum(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);
+    scan_exclusive(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);
     uint64_t nconv = (uint64_t)d2h_scalar(cpos.as<int64_t>() + (nl - 1), st) +
                      (uint64_t)d2h_scalar(conv.as<int64_t>() + (nl - 1), st);
     if (nconv == 0) break;  // sampling.py:60-63
@@ -632,7 +726,7 @@ void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, con
   k_leaf_sums_state<R><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const cplx<R>*>(state),
                                                                     nleaf, L, leaf.as<double>());
   SVB_CHECK_LAUNCH();
-  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
   uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
   k_cdf_draw_state<R><<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
       static_cast<const cplx<R>*>(state), m, cum.as<double>(), nleaf, L, shots, pcg_from(pcg),
@@ -646,7 +740,7 @@ void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uin
   DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
   k_leaf_sums_probs<<<(unsigned)((nleaf + 255) / 256), 256, 0, st>>>(d_probs, m, nleaf, leaf.as<double>());
   SVB_CHECK_LAUNCH();
-  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
   uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
   k_cdf_draw_probs<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
       d_probs, m, cum.as<double>(), nleaf, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes);
@@ -713,7 +807,7 @@ void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uin
     k_leaf_sums_state<float><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const float2*>(state), nleaf,
                                                                         L, leaf.as<double>());
   SVB_CHECK_LAUNCH();
-  cub_inclusive_sum(leaf.as<double>(), cum.as<double>(), nleaf, st);
+  scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
   BitSrc bs;
   for (int p = 0; p < 64; ++p) bs.b[p] = p < w ? (int8_t)bit_src[p] : (int8_t)-1;
   uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;

@@ -293,12 +293,13 @@ class ShardedState:
         insts = [i for i in instructions if i.kind in UNITARY_GATES]
         key = (tuple((i.kind, tuple(i.qubits), tuple(i.params)) for i in insts), tuple(self.pos),
                tuple(self.touched))
-        plan = self._plans.get(key)
-        if plan is None:
-            plan = self._plan(insts)
+        entry = self._plans.get(key)
+        if entry is None:
+            entry = (self._plan(insts), plan_touched(self.touched, insts))
             if len(self._plans) >= 8:
                 self._plans.pop(next(iter(self._plans)))
-            self._plans[key] = plan
+            self._plans[key] = entry
+        plan, touched_after = entry
         for act in plan:
             if act[0] == "gates":
                 if not self.zero_shard:  # gates map the zero vector to itself
@@ -312,7 +313,7 @@ class ShardedState:
                 self.relabels += len(act[1])
             else:
                 self.remap(act[1])
-        self.touched = list(plan_touched(self.touched, insts))
+        self.touched = list(touched_after)
 
     def _plan(self, insts) -> list:
         """Actions [("gates", records) | ("relabel", pairs) | ("remap", pairs)]

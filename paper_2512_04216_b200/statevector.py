@@ -226,6 +226,16 @@ class DeviceState:
         check(lib().svb_create(self.n, _prec_code(precision), device, _lib.ctypes.byref(h)))
         self._h = h
 
+    @classmethod
+    def _view(cls, n: int, address: int, device: int = 0) -> "DeviceState":
+        """A handle on caller-owned complex128 device/managed memory (svb_create_view)."""
+        self = cls.__new__(cls)
+        self.n, self.precision, self.device = int(n), "c128", device
+        h = _lib.c_void_p()
+        check(lib().svb_create_view(self.n, device, _lib.c_void_p(address), _lib.ctypes.byref(h)))
+        self._h = h
+        return self
+
     # lifetime
     def close(self) -> None:
         h, self._h = getattr(self, "_h", None), None
@@ -475,14 +485,51 @@ class _StatePool:
 _pool = _StatePool()
 
 
+# zero_state() arrays: complex128 states in CUDA managed memory, each with a
+# view handle, so the kernel-level calls on them run in place on the device
+# (no host<->device copy per call; pages stay in HBM while only kernels touch
+# them).  address -> (n, view DeviceState)
+_views: dict = {}
+
+
+def _release_managed(address: int) -> None:
+    entry = _views.pop(address, None)
+    if entry is not None:
+        entry[1].close()
+    try:
+        lib().svb_managed_free(_lib.c_void_p(address))
+    except Exception:
+        pass
+
+
+def _managed_state(n: int, device: int = 0) -> np.ndarray:
+    import ctypes as _ct
+    import weakref as _wr
+
+    p = _lib.c_void_p()
+    check(lib().svb_managed_alloc(16 << n, device, _ct.byref(p)))
+    raw = (_ct.c_double * (2 << n)).from_address(p.value)
+    view = DeviceState._view(n, p.value, device)
+    _views[p.value] = (n, view)
+    _wr.finalize(raw, _release_managed, p.value)
+    view.zero()
+    return np.frombuffer(raw, dtype=np.complex128)
+
+
 def _device_of(amps, n):
-    """numpy array -> temporary DeviceState (kernel-level API); DeviceState -> itself."""
+    """Kernel-level API operand -> (DeviceState, temporary?).  A DeviceState is
+    used as is; a zero_state() array (managed memory) through its view, in
+    place; any other complex128 ndarray through a temporary device copy."""
     if isinstance(amps, DeviceState):
         return amps, False
     if not isinstance(amps, np.ndarray) or amps.dtype != np.complex128:
         raise TypeError("amps must be a complex128 ndarray or a DeviceState")
     if amps.size != 1 << n:
         raise ValueError("amplitude vector length does not match n")
+    if amps.flags.c_contiguous:
+        entry = _views.get(amps.ctypes.data)
+        if entry is not None and entry[0] == n:
+            return entry[1], False
     return DeviceState.from_numpy(amps), True
 
 
@@ -497,8 +544,10 @@ def _write_back(dev: DeviceState, amps) -> None:
 
 # ------------------------------------------------------- kernel-level API
 def zero_state(n: int) -> np.ndarray:
-    """statevector.py:125-128 (host array; see DeviceState for device states)."""
-    return DeviceState(n).to_numpy()
+    """statevector.py:125-128: |0...0> as a complex128 ndarray.  The array
+    lives in CUDA managed memory, so apply_1q / apply_2q / apply_instruction /
+    marginal_probs / _measure_qubit on it run in place on the device."""
+    return _managed_state(int(n))
 
 
 def apply_1q(amps, n: int, q: int, m) -> None:

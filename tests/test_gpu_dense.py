@@ -59,7 +59,7 @@ def random_state(n, seed, precision="c128"):
     return s, orc.unitary_state(c)
 
 
-@pytest.mark.parametrize("k", [3, 4, 5])
+@pytest.mark.parametrize("k", [3, 4, 5, 6])
 def test_tensor_engine_random_unitaries(k):
     rng = np.random.default_rng(100 + k)
     for trial in range(4):
@@ -118,21 +118,25 @@ def test_engine_selection_and_errors():
     assert d.apply_matrix([0, 3, 5, 7, 9], random_unitary(5, rng)) == "fma"
     with pytest.raises(ValueError):
         d.apply_matrix([0, 3, 5], random_unitary(3, rng), engine="tensor")
+    s6 = sv.DeviceState(14, "c64")
+    assert s6.apply_matrix([0, 2, 4, 6, 8, 13], random_unitary(6, rng)) == "tensor"
+    s6.close()
     with pytest.raises(ValueError):
         d.apply_matrix([0, 0, 5], random_unitary(3, rng))
     d.close()
 
 
-def test_tensor_engine_large_state_mirror():
-    """n = 30 complex64: 16 random 5-qubit blocks then their inverses in
+@pytest.mark.parametrize("k", [5, 6])
+def test_tensor_engine_large_state_mirror(k):
+    """n = 30 complex64: 16 random k-qubit blocks then their inverses in
     reverse order return the input state (device-side comparison)."""
-    rng = np.random.default_rng(11)
+    rng = np.random.default_rng(11 + k)
     n = 30
     a = sv.DeviceState(n, "c64")
     a.apply_instructions(suite.random_circuit(n, 120, np.random.default_rng(2), measured=False).instructions)
     b = sv.DeviceState(n, "c64")
     b.copy_from(a)
-    blocks = [([int(x) for x in rng.choice(n, size=5, replace=False)], random_unitary(5, rng)) for _ in range(16)]
+    blocks = [([int(x) for x in rng.choice(n, size=k, replace=False)], random_unitary(k, rng)) for _ in range(16)]
     for q, U in blocks:
         a.apply_matrix(q, U, engine="tensor")
     for q, U in reversed(blocks):

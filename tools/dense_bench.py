@@ -26,7 +26,7 @@ for prec in ("c64", "c128"):
     nbytes = 2 * (8 if prec == "c64" else 16) * (1 << n)
     for k in range(1, 7):
         for engine in ("tensor", "fma"):
-            if engine == "tensor" and (prec != "c64" or not 3 <= k <= 5):
+            if engine == "tensor" and (prec != "c64" or not 3 <= k <= 6):
                 continue
             if prec == "c128" and k > 5:
                 continue
