@@ -229,12 +229,17 @@ int svb_batch_small(int device, int precision, int ncirc, const int32_t* nq, con
  * bit_src[64i + p] is the state-index bit of output bit p; codes to
  * out_codes[shots*i + s] (one device->host copy at the end).  Per-circuit
  * errors land in status[i] (svb_status); the call itself fails only on
- * bad arguments or a device error outside a circuit. */
+ * bad arguments or a device error outside a circuit.  jit_mode: 0 =
+ * interpreter kernels up to 24 qubits (no NVRTC compile; deterministic),
+ * 1 = NVRTC-specialised passes from 24 qubits, compiled synchronously (same
+ * engine and results as svb_apply), 2 = as 1 but compiled in the background
+ * while the interpreter serves (fastest once warm, engine per circuit depends
+ * on timing). */
 int svb_batch_run(int device, int precision, int ncirc, const int32_t* nq, const int32_t* gate_off,
                   const int32_t* ngates, const svb_gate_op* ops, const svb_gate* fixed, int nfixed,
                   int total_gates, const uint64_t* pcg,
-                  const int32_t* w, const int8_t* bit_src, uint64_t shots, int nthreads, uint64_t* out_codes,
-                  int32_t* status);
+                  const int32_t* w, const int8_t* bit_src, uint64_t shots, int nthreads, int jit_mode,
+                  uint64_t* out_codes, int32_t* status);
 
 /* Mid-circuit replay (statevector.py:142-179).  The PCG64 stream lives on the
  * device; each measure/reset consumes one draw, exactly as rng.random(). */

@@ -84,7 +84,7 @@ _SIGS = {
     "svb_batch_small": (c_int, [c_int, c_int, c_int, _i32p, _i32p, _i32p, c_void_p, c_int, _u64p, _i32p,
                                 POINTER(ctypes.c_int8), c_uint64, _u64p]),
     "svb_batch_run": (c_int, [c_int, c_int, c_int, _i32p, _i32p, _i32p, c_void_p, c_void_p, c_int, c_int, _u64p,
-                              _i32p, POINTER(ctypes.c_int8), c_uint64, c_int, _u64p, _i32p]),
+                              _i32p, POINTER(ctypes.c_int8), c_uint64, c_int, c_int, _u64p, _i32p]),
     "svb_expand_gates": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "svb_device_ptr": (c_int, [_h, POINTER(c_void_p), _u64p, _i64p]),
     "svb_half_copy": (c_int, [_h, c_int, c_int, c_void_p, c_int]),

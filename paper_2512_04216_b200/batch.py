@@ -81,7 +81,7 @@ class _Prepared:
             self.w[i], bits = _bit_sources(c)
             self.bit_src[i, : self.w[i]] = bits
 
-    def run(self, shots, precision, device, nthreads):
+    def run(self, shots, precision, device, nthreads, jit_mode):
         nc = self.nq.size
         codes = np.empty((nc, shots), dtype=np.uint64)
         status = np.zeros(nc, dtype=np.int32)
@@ -91,7 +91,8 @@ class _Prepared:
             device, prec, nc, _lib.ptr(self.nq, _lib.c_int32), _lib.ptr(self.gate_off, _lib.c_int32),
             _lib.ptr(self.ngates, _lib.c_int32), _lib.ptr(self.ops) if self.ops.size else None, _lib.ptr(fx),
             int(fx.size), int(self.ops.size), _lib.ptr(self.pcg, _lib.c_uint64), _lib.ptr(self.w, _lib.c_int32),
-            _lib.ptr(self.bit_src, _lib.ctypes.c_int8), int(shots), int(nthreads), _lib.ptr(codes, _lib.c_uint64),
+            _lib.ptr(self.bit_src, _lib.ctypes.c_int8), int(shots), int(nthreads), int(jit_mode),
+            _lib.ptr(codes, _lib.c_uint64),
             _lib.ptr(status, _lib.c_int32)))
         return codes, status
 
@@ -121,13 +122,21 @@ def _status_error(code: int):
     return BackendError(f"libsvb error {code}: {msg}")
 
 
+_JIT_MODES = {"none": 0, "sync": 1, "async": 2}
+
+
 def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", device: int = 0,
-                    nthreads: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, chunk: int = 2048) -> list:
+                    nthreads: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, chunk: int = 2048,
+                    jit: str = "none") -> list:
     """The device batch path: every terminal circuit runs with (shots, seed) and
     the CDF sampler; returns a CodeCounts (or the circuit's exception) per
     circuit in input order.  Small states: one shared-memory persistent
     kernel; the rest: svb_batch_run in chunks, the host encoding of chunk
-    j + 1 overlapping the device work of chunk j (the C call releases the GIL)."""
+    j + 1 overlapping the device work of chunk j (the C call releases the GIL).
+    jit: "none" (interpreter kernels up to 24 qubits: no compile, results
+    reproducible), "sync" (NVRTC passes from 24 qubits, as sv.run), "async"
+    (compiled in the background; fastest once warm, engine per circuit
+    depends on timing)."""
     from concurrent.futures import ThreadPoolExecutor as _TPE
 
     results: list = [None] * len(circuits)
@@ -155,7 +164,7 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
         for lo in range(0, len(large), chunk):
             idx = large[lo:lo + chunk]
             prep = _Prepared([circuits[i] for i in idx], words)
-            pending.append((idx, prep.w, pool.submit(prep.run, shots, precision, device, nthreads)))
+            pending.append((idx, prep.w, pool.submit(prep.run, shots, precision, device, nthreads, _JIT_MODES[jit])))
         for idx, w, fut in pending:
             codes, status = fut.result()
             for i, cc, st in zip(idx, _histograms(codes, w), status.tolist()):

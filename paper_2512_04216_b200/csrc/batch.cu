@@ -448,6 +448,7 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
 #include <mutex>
 #include <thread>
 
+#include "jit.h"
 #include "program.h"
 
 namespace svb {
@@ -458,7 +459,7 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
                              const int32_t* ngates, const svb_gate_op* ops, const svb_gate* fixed, int nfixed,
                              int total_gates, const uint64_t* pcg,
                              const int32_t* w, const int8_t* bit_src, uint64_t shots, int nthreads,
-                             uint64_t* out_codes, int32_t* status) {
+                             int jit_mode, uint64_t* out_codes, int32_t* status) {
   using namespace svb;
   try {
     require(ncirc >= 0 && shots >= 1 && nthreads >= 1, SVB_E_ARG, "bad batch arguments");
@@ -488,13 +489,19 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     uint64_t* dcodes = nullptr;
     SVB_CUDA(cudaMalloc(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc));
     const size_t s = precision == SVB_C128 ? 16 : 8;
-    // NVRTC specialisation from this many qubits up (SVB_BATCH_JIT_MIN_N, default 24)
-    static const int jit_min = std::getenv("SVB_BATCH_JIT_MIN_N") ? std::atoi(std::getenv("SVB_BATCH_JIT_MIN_N")) : 24;
+    // jit_mode 0: interpreter kernels up to 24 qubits, NVRTC above (no compile
+    // in a config-4 batch; deterministic); 1: NVRTC from 24 qubits, compiled
+    // synchronously (the engine sv.run uses: identical results); 2: as 1 but
+    // compiled in the background while the interpreter serves (fastest once
+    // warm; which engine ran, hence the last bits, depends on timing).
+    require(jit_mode >= 0 && jit_mode <= 2, SVB_E_ARG, "bad jit mode");
+    const int jit_min = jit_mode == 0 ? 25 : 24;
     std::atomic<int> next{0};
     std::mutex err_mu;
     std::string first_err;
     auto worker = [&] {
       cudaSetDevice(device);
+      jit_set_async(jit_mode == 2);  // never wait for NVRTC: the interpreter runs until the kernels exist
       cudaStream_t st = nullptr;
       void *buf = nullptr, *spare = nullptr;
       if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
@@ -531,6 +538,7 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
           if (first_err.empty()) first_err = e.what();
         }
       }
+      jit_set_async(false);
       cudaStreamSynchronize(st);
       if (buf) cudaFree(buf);
       if (spare) cudaFree(spare);

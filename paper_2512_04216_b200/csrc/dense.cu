@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -280,6 +281,164 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   }
 }
 
+// Pipelined variant (one CTA of 256 threads per SM): two A tiles and two
+// TMEM accumulators, so the split of tile i+1 and its MMAs run while tile i
+// is in its epilogue and stores, and the loads of tile i+2 are in flight.
+//   iteration i:  split(i+1) -> A[(i+1)&1]; MMA(i+1) -> D[(i+1)&1] (async);
+//                 load(i+2) -> registers; wait MMA(i); epilogue D[i&1] ->
+//                 A[i&1]; store tile i.
+constexpr int kTcpThreads = 256;
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kTcpThreads, 1)
+    k_dense_tcp(float2* __restrict__ state, const float* __restrict__ bsrc, const DenseGeom g, uint64_t ntiles,
+                uint32_t chunk_stride) {
+  constexpr int KR = 2 << K;
+  constexpr int EPT = (1 << (K + 7)) / kTcpThreads;
+  constexpr int NCH = KR / 4;
+  constexpr uint32_t TCOLS = 2 * KR < 32 ? 32 : 2 * KR;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
+  const uint32_t abytes = NCH * chunk_stride;
+  uint8_t* abuf = smem + sizeof(DenseSmemHdr);  // [slot][hi, lo]
+  uint8_t* bhi = abuf + 4 * abytes;
+  uint8_t* blo = bhi + KR * KR * 4;
+  uint64_t* git = reinterpret_cast<uint64_t*>(blo + KR * KR * 4);
+  uint32_t* sit = reinterpret_cast<uint32_t*>(git + EPT);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sit + EPT + (EPT & 1));  // 2 mbarriers
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = warp >> 2;
+
+  for (int i = tid; i < 2 * KR * KR / 4; i += kTcpThreads)
+    reinterpret_cast<float4*>(bhi)[i] = reinterpret_cast<const float4*>(bsrc)[i];
+  dense_it_tables<kTcpThreads>(g, EPT, git, sit);
+  dense_tile_tables(g, hdr);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  uint64_t goff;
+  uint32_t soff;
+  dense_thread_offsets<kTcpThreads>(g, tid, goff, soff);
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(KR >> 3) << 17) | ((128u >> 4) << 24);
+  const uint64_t G = gridDim.x;
+  uint32_t phase[2] = {0, 0};
+
+  auto ahi = [&](int b) { return abuf + (2 * b) * abytes; };
+  auto alo = [&](int b) { return abuf + (2 * b + 1) * abytes; };
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
+  };
+  auto split = [&](const float2 (&v)[EPT], int b) {
+    uint8_t* h = ahi(b);
+    uint8_t* l = alo(b);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(v[i].x), hy = tf32_rna(v[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(h + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(l + o) = make_float2(tf32_rna(v[i].x - hx), tf32_rna(v[i].y - hy));
+    }
+  };
+  auto mma = [&](int b) {  // one thread
+    tc_fence_after();
+    const uint32_t a0 = smem_u32(ahi(b)), a1 = smem_u32(alo(b)), b0 = smem_u32(bhi), b1 = smem_u32(blo);
+    const uint32_t as[4] = {a1, a1, a0, a0}, bs[4] = {b1, b0, b1, b0};
+    const uint32_t d = tmem + b * KR;
+#pragma unroll
+    for (int term = 0; term < 4; ++term)
+#pragma unroll
+      for (int s = 0; s < KR / 8; ++s)
+        umma_tf32(d, umma_desc(as[term] + s * 2 * chunk_stride, chunk_stride, 128),
+                  umma_desc(bs[term] + s * 2 * (KR * 16), KR * 16, 128), idesc, (term | s) != 0);
+    umma_commit(bar + b);
+  };
+  auto finish = [&](uint64_t t, int b) {  // wait MMA(b), epilogue, store tile t
+    mbar_wait(bar + b, phase[b]);
+    phase[b] ^= 1u;
+    tc_fence_after();
+    const uint32_t c = 32 * quad + lane;
+    uint8_t* h = ahi(b);
+    constexpr int HALF = KR / 2;
+#pragma unroll
+    for (int col = 0; col < HALF; col += 8) {
+      const int cc = half * HALF + col;
+      float y[8];
+      tmem_ld8(tmem + b * KR + ((32 * quad) << 16) + cc, y);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        *reinterpret_cast<float4*>(h + (uint32_t)(cc / 4 + q) * chunk_stride + c * 16) =
+            make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(h + soff + sit[i]));
+  };
+
+  float2 va[EPT], vb[EPT];
+  uint64_t t = blockIdx.x;
+  if (t >= ntiles) {
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS));
+    return;
+  }
+  // prologue: tile t into slot 0, its MMAs in flight, loads of t + G
+  load(va, t);
+  split(va, 0);
+  fence_proxy_async();
+  __syncthreads();
+  if (tid == 0) mma(0);
+  if (t + G < ntiles) load(vb, t + G);
+  int b = 0;
+  for (; t < ntiles; t += G) {
+    const uint64_t tn = t + G;
+    if (tn < ntiles) {  // split + MMA of the next tile while this one drains
+      split(vb, b ^ 1);
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) mma(b ^ 1);
+      if (tn + G < ntiles) load(vb, tn + G);
+    }
+    finish(t, b);
+    __syncthreads();  // slot b is split into again two tiles later
+    b ^= 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS) : "memory");
+  }
+}
+
 // ---------------------------------------------- k = 6: U as the TMEM operand
 // For 6-qubit blocks the real-form unitary (128 x 128 fp32, hi and lo) does
 // not fit in shared memory next to the tile, so the roles swap: A = U lives in
@@ -439,11 +598,13 @@ constexpr int kFmaThreads = 256;
 constexpr int kFmaOut = 8;  // outputs accumulated per thread per sweep over the inputs
 
 // smem: [hdr | X | Y | U | git | sit]; X/Y layout [j][c] complex with
-// 2^cb columns per tile (>= 4096 amplitudes per tile for small k)
-template <typename R>
+// 2^cb columns per tile (EPT * 256 amplitudes).  The next tile's loads are
+// issued as soon as this tile is in shared memory, so they are in flight
+// during the products and the stores.
+template <typename R, int EPT>
 __global__ void __launch_bounds__(kFmaThreads, 2)
     k_dense_fma(cplx<R>* __restrict__ state, const cplx<R>* __restrict__ u, const DenseGeom g, uint64_t ntiles) {
-  const int k = g.k, D = 1 << k, cb = g.kb - g.k, cols = 1 << cb, ept = (D << cb) / kFmaThreads;
+  const int k = g.k, D = 1 << k, cb = g.kb - g.k, cols = 1 << cb;
   const int ob = D < kFmaOut ? D : kFmaOut;
   extern __shared__ __align__(16) uint8_t smem[];
   DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
@@ -451,21 +612,32 @@ __global__ void __launch_bounds__(kFmaThreads, 2)
   cplx<R>* Y = X + (D << cb);
   cplx<R>* U = Y + (D << cb);
   uint64_t* git = reinterpret_cast<uint64_t*>(U + D * D);
-  uint32_t* sit = reinterpret_cast<uint32_t*>(git + ept);
+  uint32_t* sit = reinterpret_cast<uint32_t*>(git + EPT);
   const uint32_t tid = threadIdx.x;
   for (int i = tid; i < D * D; i += kFmaThreads) U[i] = u[i];
-  dense_it_tables<kFmaThreads>(g, ept, git, sit);
+  dense_it_tables<kFmaThreads>(g, EPT, git, sit);
   dense_tile_tables(g, hdr);
   uint64_t goff;
   uint32_t soff;
   dense_thread_offsets<kFmaThreads>(g, tid, goff, soff);
   __syncthreads();
   const int items = cols * (D / ob);
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  cplx<R> v[EPT];
+  uint64_t t = blockIdx.x;
+  if (t < ntiles) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
-#pragma unroll 8
-    for (int i = 0; i < ept; ++i)
-      *reinterpret_cast<cplx<R>*>(reinterpret_cast<uint8_t*>(X) + soff + sit[i]) = __ldcs(state + base + git[i]);
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
+  }
+  for (; t < ntiles; t += gridDim.x) {
+    const uint64_t base = dense_tile_base(hdr, t) + goff;
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) *reinterpret_cast<cplx<R>*>(reinterpret_cast<uint8_t*>(X) + soff + sit[i]) = v[i];
+    if (t + gridDim.x < ntiles) {
+      const uint64_t nb = dense_tile_base(hdr, t + gridDim.x) + goff;
+#pragma unroll
+      for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + nb + git[i]);
+    }
     __syncthreads();
     for (int p = tid; p < items; p += kFmaThreads) {
       const int c = p & (cols - 1), i0 = (p >> cb) * ob;
@@ -483,11 +655,10 @@ __global__ void __launch_bounds__(kFmaThreads, 2)
         if (o < ob) Y[((i0 + o) << cb) + c] = acc[o];
     }
     __syncthreads();
-#pragma unroll 8
-    for (int i = 0; i < ept; ++i)
+#pragma unroll
+    for (int i = 0; i < EPT; ++i)
       __stcs(state + base + git[i],
              *reinterpret_cast<const cplx<R>*>(reinterpret_cast<const uint8_t*>(Y) + soff + sit[i]));
-    __syncthreads();
   }
 }
 
@@ -622,20 +793,41 @@ void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* 
   const DenseGeom g = make_geom(n, q, k, 7, 1, 8, chunk_stride);
   require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
   const uint64_t ntiles = 1ull << (n - k - 7);
-  const int ept = (1 << (k + 7)) / kTcThreads;
-  const size_t smem = sizeof(DenseSmemHdr) + 2 * (size_t)(KR / 4) * chunk_stride + 2 * (size_t)KR * KR * 4 +
-                      (size_t)ept * 12 + 64;
-  const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
-  static std::atomic<uint64_t> attr[3] = {{0}, {0}, {0}};
-  auto go = [&](auto kern, int slot) {
-    once_per_device(attr[slot], [&] {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-    });
-    kern<<<grid, kTcThreads, smem, st>>>(static_cast<float2*>(state), db, g, ntiles, chunk_stride);
-  };
-  if (k == 3) go(k_dense_tc<3>, 0);
-  else if (k == 4) go(k_dense_tc<4>, 1);
-  else go(k_dense_tc<5>, 2);
+  // k = 5: the pipelined one-CTA kernel (measured 5.1 vs 5.7 ms at n = 30);
+  // k <= 4: two CTAs per SM with register prefetch (smaller tiles need the
+  // second CTA's loads in flight: 4.6 vs 8.2 ms at k = 3).  SVB_TC_PIPE=0/1 overrides.
+  const char* pe = std::getenv("SVB_TC_PIPE");
+  const bool pipe = pe ? std::atoi(pe) != 0 : k == 5;
+  static std::atomic<uint64_t> attr[6] = {{0}, {0}, {0}, {0}, {0}, {0}};
+  if (pipe) {
+    const int ept = (1 << (k + 7)) / kTcpThreads;
+    const size_t smem = sizeof(DenseSmemHdr) + 4 * (size_t)(KR / 4) * chunk_stride + 2 * (size_t)KR * KR * 4 +
+                        (size_t)ept * 12 + 64;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count());
+    auto go = [&](auto kern, int slot) {
+      once_per_device(attr[slot], [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      });
+      kern<<<grid, kTcpThreads, smem, st>>>(static_cast<float2*>(state), db, g, ntiles, chunk_stride);
+    };
+    if (k == 3) go(k_dense_tcp<3>, 3);
+    else if (k == 4) go(k_dense_tcp<4>, 4);
+    else go(k_dense_tcp<5>, 5);
+  } else {
+    const int ept = (1 << (k + 7)) / kTcThreads;
+    const size_t smem = sizeof(DenseSmemHdr) + 2 * (size_t)(KR / 4) * chunk_stride + 2 * (size_t)KR * KR * 4 +
+                        (size_t)ept * 12 + 64;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 2);
+    auto go = [&](auto kern, int slot) {
+      once_per_device(attr[slot], [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+      });
+      kern<<<grid, kTcThreads, smem, st>>>(static_cast<float2*>(state), db, g, ntiles, chunk_stride);
+    };
+    if (k == 3) go(k_dense_tc<3>, 0);
+    else if (k == 4) go(k_dense_tc<4>, 1);
+    else go(k_dense_tc<5>, 2);
+  }
   SVB_CHECK_LAUNCH();
   SVB_CUDA(cudaFreeAsync(db, st));
 }
@@ -650,7 +842,8 @@ void launch_dense_fma(void* state, int n, const int32_t* q, int k, const double*
   cplx<R>* du = nullptr;
   SVB_CUDA(cudaMallocAsync(&du, hu.size() * sizeof(cplx<R>), st));
   SVB_CUDA(cudaMemcpyAsync(du, hu.data(), hu.size() * sizeof(cplx<R>), cudaMemcpyHostToDevice, st));
-  const int cb = std::min(n - k, std::max(7, 12 - k));  // >= 4096 amplitudes per tile
+  const int cb = std::min(n - k, std::max(7, 12 - k));  // 4096 amplitudes per tile (8192 for k = 6)
+  require((D << cb) >= kFmaThreads && (D << cb) <= 32 * kFmaThreads, SVB_E_ARG, "dense block: bad tile size");
   const DenseGeom g = make_geom(n, q, k, cb, 0, sizeof(cplx<R>), 0);
   require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
   const uint64_t ntiles = 1ull << (n - k - cb);
@@ -659,11 +852,21 @@ void launch_dense_fma(void* state, int n, const int32_t* q, int k, const double*
                       (size_t)ept * 12 + 16;
   const int per_sm = smem <= 110 * 1024 ? 2 : 1;  // two CTAs per SM when their tiles fit
   const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * per_sm);
-  static std::atomic<uint64_t> attr{0};
-  once_per_device(attr, [] {
-    cudaFuncSetAttribute(k_dense_fma<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
-  k_dense_fma<R><<<grid, kFmaThreads, smem, st>>>(static_cast<cplx<R>*>(state), du, g, ntiles);
+  static std::atomic<uint64_t> attr[6] = {{0}, {0}, {0}, {0}, {0}, {0}};
+  auto go = [&](auto kern, int slot) {
+    once_per_device(attr[slot], [&] {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    kern<<<grid, kFmaThreads, smem, st>>>(static_cast<cplx<R>*>(state), du, g, ntiles);
+  };
+  switch (ept) {
+    case 1: go(k_dense_fma<R, 1>, 0); break;
+    case 2: go(k_dense_fma<R, 2>, 1); break;
+    case 4: go(k_dense_fma<R, 4>, 2); break;
+    case 8: go(k_dense_fma<R, 8>, 3); break;
+    case 16: go(k_dense_fma<R, 16>, 4); break;
+    default: go(k_dense_fma<R, 32>, 5); break;
+  }
   SVB_CHECK_LAUNCH();
   SVB_CUDA(cudaFreeAsync(du, st));
 }

@@ -29,6 +29,7 @@
 #include <thread>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "jit.h"
@@ -99,6 +100,8 @@ struct Module {
 std::mutex g_mu;
 std::unordered_map<std::string, Module> g_cache;  // key: device + source
 std::unordered_map<std::string, std::shared_ptr<std::mutex>> g_key_locks;  // in-flight compiles
+std::unordered_set<std::string> g_inflight;  // background compiles (asynchronous mode)
+thread_local bool t_async_jit = false;
 uint64_t g_tick = 0;  // LRU clock (under g_mu)
 // Bounds of the in-memory caches: programs whose coefficients are compiled in
 // as immediates (n >= 28) make a new kernel per angle set, so a parameter
@@ -733,8 +736,10 @@ static std::vector<char> jit_compile(const std::string& src, std::string* log) {
   const char* hdr_src[] = {svb_device_core_src};
   const char* hdr_name[] = {"device_core.cuh"};
   if (nv.create(&prog_h, src.c_str(), "svb_jit.cu", 1, hdr_src, hdr_name) != 0) return {};
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
-  int rc = nv.compile(prog_h, 3, opts);
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+  static const std::string extra = std::getenv("SVB_JIT_OPTS") ? std::getenv("SVB_JIT_OPTS") : "";
+  if (!extra.empty()) opts.push_back(extra.c_str());
+  int rc = nv.compile(prog_h, (int)opts.size(), opts.data());
   if (rc != 0) {
     size_t n = 0;
     nv.log_size(prog_h, &n);
@@ -845,6 +850,60 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
         todo.push_back(p);
       }
     }
+  }
+  // Asynchronous mode (the batch executor): kernels not compiled yet are
+  // compiled by background threads while this program runs on the
+  // interpreter; later programs of the same structure pick them up.
+  if (!todo.empty() && t_async_jit) {
+    std::vector<std::pair<std::string, std::string>> jobs;  // (key, source)
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      for (size_t p : todo)
+        if (!g_cache.count(keys[p]) && g_inflight.insert(keys[p]).second) jobs.push_back({keys[p], srcs[p]});
+    }
+    for (auto& jb : jobs) {
+      std::thread([jb, dev, drp = &dr] {
+        cudaSetDevice(dev);
+        const std::string dir = cache_dir();
+        const std::string path = dir + "/" + jb.first.substr(jb.first.find(':') + 1) + ".cubin";
+        std::vector<char> cubin;
+        if (FILE* f = std::fopen(path.c_str(), "rb")) {
+          std::fseek(f, 0, SEEK_END);
+          const long sz = std::ftell(f);
+          std::fseek(f, 0, SEEK_SET);
+          cubin.resize(sz > 0 ? (size_t)sz : 0);
+          if (sz <= 0 || std::fread(cubin.data(), 1, (size_t)sz, f) != (size_t)sz) cubin.clear();
+          std::fclose(f);
+        }
+        if (cubin.empty()) {
+          std::string log;
+          cubin = jit_compile(jb.second, &log);
+          if (!cubin.empty()) {
+            std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+            if (std::system(mk.c_str()) != 0) { /* best effort */ }
+            const std::string tmp = path + ".tmp" + std::to_string((unsigned long long)(uintptr_t)&cubin);
+            if (FILE* f = std::fopen(tmp.c_str(), "wb")) {
+              const bool ok = std::fwrite(cubin.data(), 1, cubin.size(), f) == cubin.size();
+              std::fclose(f);
+              if (ok) std::rename(tmp.c_str(), path.c_str());
+              else std::remove(tmp.c_str());
+            }
+          }
+        }
+        Module m;
+        CUfunction fn = nullptr;
+        const bool ok = !cubin.empty() && drp->load(&m.mod, cubin.data()) == CUDA_SUCCESS &&
+                        drp->getfn(&fn, m.mod, "svb_jit") == CUDA_SUCCESS;
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (ok) {
+          m.fns.push_back(fn);
+          m.last_use = ++g_tick;
+          g_cache.emplace(jb.first, m);
+        }
+        g_inflight.erase(jb.first);
+      }).detach();
+    }
+    return false;
   }
   // one compiler per kernel source: threads that need a source another thread
   // is compiling wait for it (the batch executor's workers meet the same
@@ -985,6 +1044,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
   }
   return true;
 }
+
+void jit_set_async(bool on) { t_async_jit = on; }
 
 template bool jit_launch_passes<float>(cplx<float>*, cplx<float>*, const Program&, const PassDev*, const uint8_t*, cudaStream_t,
                                        ProgramStats*, int, bool);

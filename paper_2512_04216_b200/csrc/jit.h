@@ -14,4 +14,8 @@ template <typename R>
 bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input);
 
+// Asynchronous JIT for the calling thread: kernels not compiled yet are built
+// by background threads and the program runs on the interpreter meanwhile.
+void jit_set_async(bool on);
+
 }  // namespace svb

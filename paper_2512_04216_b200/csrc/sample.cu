@@ -24,7 +24,7 @@
 //
 // Codes (clbit-packed outcomes) are histogrammed with a radix sort + run
 // length encode, giving np.unique's ascending (value, count) pairs.
-#include <cub/cub.cuh>
+
 
 #include <vector>
 
@@ -818,33 +818,119 @@ void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uin
 }
 
 // --------------------------------------------------------------- histogram
+// ------------------------------------------------------ code histogram
+// (code, count) pairs sorted by code, like np.unique(codes, return_counts)
+// (result.py:80-82): an LSD radix sort over the w code bits (8-bit digits;
+// per pass: per-tile digit histograms, one prefix scan, a stable scatter
+// ranked with warp match-any), then a run-length encode (flags, scan,
+// scatter).  The sentinel ~0 (shots another shard owns) sorts last and is
+// dropped.
+constexpr int kRsThreads = 256, kRsItems = 16, kRsTile = kRsThreads * kRsItems;
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(const uint64_t* __restrict__ in, uint64_t n, int shift,
+                                                        uint32_t* __restrict__ hist, uint32_t ntiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+  for (int i = 0; i < kRsItems; ++i) {
+    const uint64_t e = base + (uint64_t)i * kRsThreads + threadIdx.x;
+    if (e < n) atomicAdd(&h[(in[e] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[(uint64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];  // digit-major
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                           uint64_t n, int shift, const uint32_t* __restrict__ off,
+                                                           uint32_t ntiles) {
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wcnt[kRsThreads / 32][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  run[tid] = off[(uint64_t)tid * ntiles + blockIdx.x];
+  const uint64_t base = (uint64_t)blockIdx.x * kRsTile;
+  for (int r = 0; r < kRsItems; ++r) {
+    for (int w = 0; w < kRsThreads / 32; ++w) wcnt[w][tid] = 0;
+    __syncthreads();
+    const uint64_t e = base + (uint64_t)r * kRsThreads + tid;
+    const bool valid = e < n;
+    const uint64_t key = valid ? in[e] : 0;
+    const uint32_t d = valid ? (uint32_t)((key >> shift) & 255u) : 256u + lane;  // invalid lanes never match
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) wcnt[warp][d] = __popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t pos = run[d] + rank;
+      for (int w = 0; w < warp; ++w) pos += wcnt[w][d];
+      out[pos] = key;
+    }
+    __syncthreads();
+    uint32_t add = 0;
+    for (int w = 0; w < kRsThreads / 32; ++w) add += wcnt[w][tid];
+    run[tid] += add;
+    __syncthreads();
+  }
+}
+
+__global__ void k_rle_flags(const uint64_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ flag) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = (i == 0 || a[i] != a[i - 1]) ? 1u : 0u;
+}
+
+__global__ void k_rle_scatter(const uint64_t* __restrict__ a, uint64_t n, const uint32_t* __restrict__ pos,
+                              const uint32_t* __restrict__ flag, uint64_t* __restrict__ uniq,
+                              uint64_t* __restrict__ start) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) {
+    uniq[pos[i]] = a[i];
+    start[pos[i]] = i;
+  }
+}
+
+__global__ void k_rle_counts(const uint64_t* __restrict__ start, uint64_t nruns, uint64_t n,
+                             uint64_t* __restrict__ cnt) {
+  const uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nruns) cnt[r] = (r + 1 < nruns ? start[r + 1] : n) - start[r];
+}
+
 uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_codes,
                          uint64_t* h_counts, cudaStream_t st) {
-  DevBuf sorted(sizeof(uint64_t) * shots, st);
-  size_t bytes = 0;
-  int end_bit = w < 1 ? 1 : w;
-  SVB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, d_codes, sorted.as<uint64_t>(), (int64_t)shots,
-                                          0, end_bit, st));
-  {
-    DevBuf tmp(bytes, st);
-    SVB_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, d_codes, sorted.as<uint64_t>(), (int64_t)shots,
-                                            0, end_bit, st));
+  require(shots < (1ull << 32), SVB_E_ARG, "histogram: at most 2^32 - 1 shots per call");
+  const int bits = w >= 64 ? 64 : (w < 1 ? 1 : w);
+  const uint32_t ntiles = (uint32_t)((shots + kRsTile - 1) / kRsTile);
+  DevBuf alt(sizeof(uint64_t) * shots, st), hist(sizeof(uint32_t) * 256 * (uint64_t)ntiles, st);
+  uint64_t* src = d_codes;
+  uint64_t* dst = alt.as<uint64_t>();
+  for (int shift = 0; shift < bits; shift += 8) {
+    k_rs_hist<<<ntiles, kRsThreads, 0, st>>>(src, shots, shift, hist.as<uint32_t>(), ntiles);
+    SVB_CHECK_LAUNCH();
+    device_scan<uint32_t>(hist.as<uint32_t>(), hist.as<uint32_t>(), 256ull * ntiles, true, st);
+    k_rs_scatter<<<ntiles, kRsThreads, 0, st>>>(src, dst, shots, shift, hist.as<uint32_t>(), ntiles);
+    SVB_CHECK_LAUNCH();
+    std::swap(src, dst);
   }
-  DevBuf uniq(sizeof(uint64_t) * shots, st), cnt(sizeof(uint64_t) * shots, st), nr(sizeof(int64_t), st);
-  bytes = 0;
-  SVB_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, sorted.as<uint64_t>(), uniq.as<uint64_t>(),
-                                              cnt.as<uint64_t>(), nr.as<int64_t>(), (int64_t)shots, st));
-  {
-    DevBuf tmp(bytes, st);
-    SVB_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, sorted.as<uint64_t>(), uniq.as<uint64_t>(),
-                                                cnt.as<uint64_t>(), nr.as<int64_t>(), (int64_t)shots, st));
-  }
-  int64_t nruns = d2h_scalar(nr.as<int64_t>(), st);
-  if (nruns > 0 && d2h_scalar(uniq.as<uint64_t>() + (nruns - 1), st) == ~0ull) --nruns;  // foreign shots
-  SVB_CUDA(cudaMemcpyAsync(h_codes, uniq.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
-  SVB_CUDA(cudaMemcpyAsync(h_counts, cnt.p, sizeof(uint64_t) * nruns, cudaMemcpyDeviceToHost, st));
+  // run-length encode the sorted codes in src
+  DevBuf flag(sizeof(uint32_t) * shots, st), pos(sizeof(uint32_t) * shots, st);
+  DevBuf uniq(sizeof(uint64_t) * shots, st), start(sizeof(uint64_t) * shots, st), cnt(sizeof(uint64_t) * shots, st);
+  const unsigned g = (unsigned)((shots + 255) / 256);
+  k_rle_flags<<<g, 256, 0, st>>>(src, shots, flag.as<uint32_t>());
+  SVB_CHECK_LAUNCH();
+  device_scan<uint32_t>(flag.as<uint32_t>(), pos.as<uint32_t>(), shots, true, st);
+  k_rle_scatter<<<g, 256, 0, st>>>(src, shots, pos.as<uint32_t>(), flag.as<uint32_t>(), uniq.as<uint64_t>(),
+                                   start.as<uint64_t>());
+  SVB_CHECK_LAUNCH();
+  const uint64_t nruns = (uint64_t)d2h_scalar(pos.as<uint32_t>() + (shots - 1), st) +
+                         d2h_scalar(flag.as<uint32_t>() + (shots - 1), st);
+  k_rle_counts<<<(unsigned)((nruns + 255) / 256), 256, 0, st>>>(start.as<uint64_t>(), nruns, shots,
+                                                                 cnt.as<uint64_t>());
+  SVB_CHECK_LAUNCH();
+  uint64_t keep = nruns;
+  if (keep > 0 && d2h_scalar(uniq.as<uint64_t>() + (keep - 1), st) == ~0ull) --keep;  // foreign shots
+  SVB_CUDA(cudaMemcpyAsync(h_codes, uniq.p, sizeof(uint64_t) * keep, cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaMemcpyAsync(h_counts, cnt.p, sizeof(uint64_t) * keep, cudaMemcpyDeviceToHost, st));
   SVB_CUDA(cudaStreamSynchronize(st));
-  return (uint64_t)nruns;
+  return keep;
 }
 
 }  // namespace svb
