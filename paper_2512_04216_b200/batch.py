@@ -127,16 +127,17 @@ _JIT_MODES = {"none": 0, "sync": 1, "async": 2}
 
 def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", device: int = 0,
                     nthreads: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, chunk: int = 2048,
-                    jit: str = "none") -> list:
+                    jit: str = "sync") -> list:
     """The device batch path: every terminal circuit runs with (shots, seed) and
     the CDF sampler; returns a CodeCounts (or the circuit's exception) per
     circuit in input order.  Small states: one shared-memory persistent
     kernel; the rest: svb_batch_run in chunks, the host encoding of chunk
     j + 1 overlapping the device work of chunk j (the C call releases the GIL).
-    jit: "none" (interpreter kernels up to 24 qubits: no compile, results
-    reproducible), "sync" (NVRTC passes from 24 qubits, as sv.run), "async"
-    (compiled in the background; fastest once warm, engine per circuit
-    depends on timing)."""
+    jit: "sync" (default: NVRTC-specialised passes from 24 qubits exactly as
+    sv.run, so results equal sv.run's; a cold process pays one compile per
+    circuit structure, cached on disk), "none" (interpreter kernels up to 24
+    qubits: no compile), "async" (compiled in the background while the
+    interpreter serves; the engine of a circuit then depends on timing)."""
     from concurrent.futures import ThreadPoolExecutor as _TPE
 
     results: list = [None] * len(circuits)
@@ -184,7 +185,7 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
 
 
 def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", sampler: str = "cdf",
-              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP):
+              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, jit: str = "sync"):
     """Run every circuit with (shots, seed); returns a list of RunResult or
     exception objects, in input order (the reference records per-circuit
     errors, batch.py:192-194).  Default sampler: the device CDF sampler through
@@ -193,7 +194,7 @@ def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c
     if sampler != "alias":
         t0 = time.perf_counter()
         raw = run_batch_codes(circuits, shots, seed, precision=precision, device=device, nthreads=workers,
-                              qubit_cap=qubit_cap)
+                              qubit_cap=qubit_cap, jit=jit)
         dt = (time.perf_counter() - t0) / max(len(circuits), 1)
         out = []
         for r in raw:

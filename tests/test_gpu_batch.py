@@ -87,13 +87,13 @@ def test_batch_codes_equal_per_circuit_runs_all_widths():
 
     circs = suite.batch_workload(26)
     for precision in ("c128", "c64"):
-        res = run_batch_codes(circs, shots=1000, seed=5, precision=precision, chunk=7, jit="sync")
+        res = run_batch_codes(circs, shots=1000, seed=5, precision=precision, chunk=7)
         for c, r in zip(circs, res):
             want = sv.run_codes(c, 1000, 5, precision=precision, sampler="cdf")
             assert np.array_equal(r.codes, want.codes) and np.array_equal(r.counts, want.counts), (c.name, precision)
-    # default (interpreter kernels, no compile) is reproducible run to run
-    a = run_batch_codes(circs, shots=1000, seed=5)
-    b = run_batch_codes(circs, shots=1000, seed=5)
+    # interpreter kernels (no compile) are reproducible run to run
+    a = run_batch_codes(circs, shots=1000, seed=5, jit="none")
+    b = run_batch_codes(circs, shots=1000, seed=5, jit="none")
     for x, y in zip(a, b):
         assert np.array_equal(x.codes, y.codes) and np.array_equal(x.counts, y.counts)
 
