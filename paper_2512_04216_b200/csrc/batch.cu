@@ -486,6 +486,7 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nq[a] > nq[b]; });
     SVB_CUDA(cudaSetDevice(device));
+    keep_pool_mapped(device);
     uint64_t* dcodes = nullptr;
     SVB_CUDA(cudaMalloc(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc));
     const size_t s = precision == SVB_C128 ? 16 : 8;

@@ -68,6 +68,18 @@ template <class F> inline void once_per_device(std::atomic<uint64_t>& done, F&& 
   done.fetch_or(bit, std::memory_order_release);
 }
 
+// Keep up to 1 GiB of freed stream-ordered scratch mapped in the device's
+// default pool (per-call scratch: program uploads, sampler leaves, workspaces);
+// with the default threshold of 0 every free unmaps at the next sync.
+inline void keep_pool_mapped(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = 1ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+}
+
 inline int grid_for(uint64_t work, int block, int max_blocks = 148 * 16) {
   uint64_t g = (work + block - 1) / block;
   if (g > (uint64_t)max_blocks) g = max_blocks;

@@ -124,58 +124,34 @@ __device__ __forceinline__ uint64_t dense_tile_base(const DenseSmemHdr* h, uint6
 }
 
 // per-thread constant part of the element offsets (element e = it * NT + tid)
-// first = 1: elements are amplitude pairs (tile position 0 = qubit 0, the
-// pair's second amplitude; 16-byte global accesses)
 template <int NT>
 __device__ __forceinline__ void dense_thread_offsets(const DenseGeom& g, uint32_t tid, uint64_t& goff,
-                                                     uint32_t& soff, int first = 0) {
+                                                     uint32_t& soff) {
   goff = 0;
   soff = 0;
   constexpr int lb = NT == 128 ? 7 : 8;
   for (int b = 0; b < lb; ++b)
     if ((tid >> b) & 1u) {
-      goff += 1ull << g.tq[first + b];
-      soff += g.sb[first + b];
+      goff += 1ull << g.tq[b];
+      soff += g.sb[b];
     }
 }
 
 // it-part of the offsets, one table entry per element slot
 template <int NT>
-__device__ __forceinline__ void dense_it_tables(const DenseGeom& g, int ept, uint64_t* git, uint32_t* sit,
-                                                int first = 0) {
+__device__ __forceinline__ void dense_it_tables(const DenseGeom& g, int ept, uint64_t* git, uint32_t* sit) {
   constexpr int lb = NT == 128 ? 7 : 8;
   for (int it = threadIdx.x; it < ept; it += NT) {
     uint64_t go = 0;
     uint32_t so = 0;
-    for (int b = first + lb; b < g.kb; ++b)
-      if ((it >> (b - first - lb)) & 1) {
+    for (int b = lb; b < g.kb; ++b)
+      if ((it >> (b - lb)) & 1) {
         go += 1ull << g.tq[b];
         so += g.sb[b];
       }
     git[it] = go;
     sit[it] = so;
   }
-}
-
-// TF32 hi / lo split of an amplitude pair into the A (or B) tile layout:
-// the pair's amplitudes sit sb0 bytes apart (8: adjacent in one 16-byte
-// chunk, one 128-bit store; else two 64-bit stores)
-__device__ __forceinline__ void split_pair(uint8_t* hi, uint8_t* lo, uint32_t o, uint32_t sb0, float4 x) {
-  const float h0 = tf32_rna(x.x), h1 = tf32_rna(x.y), h2 = tf32_rna(x.z), h3 = tf32_rna(x.w);
-  const float l0 = tf32_rna(x.x - h0), l1 = tf32_rna(x.y - h1), l2 = tf32_rna(x.z - h2), l3 = tf32_rna(x.w - h3);
-  if (sb0 == 8) {
-    *reinterpret_cast<float4*>(hi + o) = make_float4(h0, h1, h2, h3);
-    *reinterpret_cast<float4*>(lo + o) = make_float4(l0, l1, l2, l3);
-  } else {
-    *reinterpret_cast<float2*>(hi + o) = make_float2(h0, h1);
-    *reinterpret_cast<float2*>(hi + o + sb0) = make_float2(h2, h3);
-    *reinterpret_cast<float2*>(lo + o) = make_float2(l0, l1);
-    *reinterpret_cast<float2*>(lo + o + sb0) = make_float2(l2, l3);
-  }
-}
-__device__ __forceinline__ float4 gather_pair(const uint8_t* buf, uint32_t o, uint32_t sb0) {
-  const float2 a = *reinterpret_cast<const float2*>(buf + o), b = *reinterpret_cast<const float2*>(buf + o + sb0);
-  return make_float4(a.x, a.y, b.x, b.y);
 }
 
 constexpr int kTcThreads = 128;
@@ -188,8 +164,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     k_dense_tc(float2* __restrict__ state, const float* __restrict__ bsrc, const DenseGeom g, uint64_t ntiles,
                uint32_t chunk_stride) {
   constexpr int KR = 2 << K;             // real K = N
-  constexpr int EPT = (1 << (K + 7)) / kTcThreads;  // amplitudes per thread
-  constexpr int EP = EPT / 2;                        // amplitude pairs per thread
+  constexpr int EPT = (1 << (K + 7)) / kTcThreads;  // elements per thread
   constexpr int NCH = KR / 4;            // 16-byte K chunks
   extern __shared__ __align__(1024) uint8_t smem[];
   DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
@@ -208,7 +183,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   // B operand (hi, lo: real-form U, K-major rows) from global, once per CTA
   for (int i = tid; i < 2 * KR * KR / 4; i += kTcThreads)
     reinterpret_cast<float4*>(bhi)[i] = reinterpret_cast<const float4*>(bsrc)[i];
-  dense_it_tables<kTcThreads>(g, EP, git, sit, 1);
+  dense_it_tables<kTcThreads>(g, EPT, git, sit);
   dense_tile_tables(g, hdr);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
@@ -227,23 +202,27 @@ __global__ void __launch_bounds__(kTcThreads, 2)
   const uint32_t tmem = *tslot;
   uint64_t goff;
   uint32_t soff;
-  dense_thread_offsets<kTcThreads>(g, tid, goff, soff, 1);
-  const uint32_t sb0 = g.sb[0];
+  dense_thread_offsets<kTcThreads>(g, tid, goff, soff);
   // instruction descriptor: F32 accumulator, TF32 A and B, K-major both, N = KR, M = 128
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(KR >> 3) << 17) | ((128u >> 4) << 24);
   uint32_t phase = 0;
 
-  auto load = [&](float4 (&v)[EP], uint64_t t) {
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
 #pragma unroll
-    for (int i = 0; i < EP; ++i) v[i] = __ldcs(reinterpret_cast<const float4*>(state + base + git[i]));
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
   };
-  auto step = [&](float4 (&cur)[EP], float4 (&nxt)[EP], uint64_t t) {
+  auto step = [&](float2 (&cur)[EPT], float2 (&nxt)[EPT], uint64_t t) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
     if (t + gridDim.x < ntiles) load(nxt, t + gridDim.x);
     // A tile, split hi / lo
 #pragma unroll
-    for (int i = 0; i < EP; ++i) split_pair(ahi, alo, soff + sit[i], sb0, cur[i]);
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(cur[i].x), hy = tf32_rna(cur[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(ahi + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(alo + o) = make_float2(tf32_rna(cur[i].x - hx), tf32_rna(cur[i].y - hy));
+    }
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -282,12 +261,12 @@ __global__ void __launch_bounds__(kTcThreads, 2)
     tc_fence_before();
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < EP; ++i)
-      __stcs(reinterpret_cast<float4*>(state + base + git[i]), gather_pair(ahi, soff + sit[i], sb0));
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(ahi + soff + sit[i]));
     __syncthreads();
   };
 
-  float4 va[EP], vb[EP];
+  float2 va[EPT], vb[EPT];
   const uint64_t G = gridDim.x;
   if (blockIdx.x < ntiles) load(va, blockIdx.x);
   for (uint64_t t = blockIdx.x; t < ntiles; t += 2 * G) {
@@ -326,7 +305,6 @@ __global__ void __launch_bounds__(kTcpThreads, 1)
                 uint32_t chunk_stride) {
   constexpr int KR = 2 << K;
   constexpr int EPT = (1 << (K + 7)) / kTcpThreads;
-  constexpr int EP = EPT / 2;
   constexpr int NCH = KR / 4;
   constexpr uint32_t TCOLS = 2 * KR < 32 ? 32 : 2 * KR;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -343,7 +321,7 @@ __global__ void __launch_bounds__(kTcpThreads, 1)
 
   for (int i = tid; i < 2 * KR * KR / 4; i += kTcpThreads)
     reinterpret_cast<float4*>(bhi)[i] = reinterpret_cast<const float4*>(bsrc)[i];
-  dense_it_tables<kTcpThreads>(g, EP, git, sit, 1);
+  dense_it_tables<kTcpThreads>(g, EPT, git, sit);
   dense_tile_tables(g, hdr);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
@@ -363,24 +341,28 @@ __global__ void __launch_bounds__(kTcpThreads, 1)
   const uint32_t tmem = *tslot;
   uint64_t goff;
   uint32_t soff;
-  dense_thread_offsets<kTcpThreads>(g, tid, goff, soff, 1);
-  const uint32_t sb0 = g.sb[0];
+  dense_thread_offsets<kTcpThreads>(g, tid, goff, soff);
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(KR >> 3) << 17) | ((128u >> 4) << 24);
   const uint64_t G = gridDim.x;
   uint32_t phase[2] = {0, 0};
 
   auto ahi = [&](int b) { return abuf + (2 * b) * abytes; };
   auto alo = [&](int b) { return abuf + (2 * b + 1) * abytes; };
-  auto load = [&](float4 (&v)[EP], uint64_t t) {
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
 #pragma unroll
-    for (int i = 0; i < EP; ++i) v[i] = __ldcs(reinterpret_cast<const float4*>(state + base + git[i]));
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
   };
-  auto split = [&](const float4 (&v)[EP], int b) {
+  auto split = [&](const float2 (&v)[EPT], int b) {
     uint8_t* h = ahi(b);
     uint8_t* l = alo(b);
 #pragma unroll
-    for (int i = 0; i < EP; ++i) split_pair(h, l, soff + sit[i], sb0, v[i]);
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(v[i].x), hy = tf32_rna(v[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(h + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(l + o) = make_float2(tf32_rna(v[i].x - hx), tf32_rna(v[i].y - hy));
+    }
   };
   auto mma = [&](int b) {  // one thread
     tc_fence_after();
@@ -416,11 +398,11 @@ __global__ void __launch_bounds__(kTcpThreads, 1)
     __syncthreads();
     const uint64_t base = dense_tile_base(hdr, t) + goff;
 #pragma unroll
-    for (int i = 0; i < EP; ++i)
-      __stcs(reinterpret_cast<float4*>(state + base + git[i]), gather_pair(h, soff + sit[i], sb0));
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(h + soff + sit[i]));
   };
 
-  float4 va[EP], vb[EP];
+  float2 va[EPT], vb[EPT];
   uint64_t t = blockIdx.x;
   if (t >= ntiles) {
     tc_fence_before();
@@ -492,7 +474,6 @@ __global__ void __launch_bounds__(kTc6Threads, 1)
                 uint32_t chunk_stride) {
   constexpr int KR = 128;
   constexpr int EPT = (1 << 13) / kTc6Threads;  // 32
-  constexpr int EP = EPT / 2;
   constexpr int NCH = KR / 4;
   extern __shared__ __align__(1024) uint8_t smem[];
   DenseSmemHdr* hdr = reinterpret_cast<DenseSmemHdr*>(smem);
@@ -505,7 +486,7 @@ __global__ void __launch_bounds__(kTc6Threads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3;
 
-  dense_it_tables<kTc6Threads>(g, EP, git, sit, 1);
+  dense_it_tables<kTc6Threads>(g, EPT, git, sit);
   dense_tile_tables(g, hdr);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
@@ -540,22 +521,26 @@ __global__ void __launch_bounds__(kTc6Threads, 1)
   tc_fence_after();
   uint64_t goff;
   uint32_t soff;
-  dense_thread_offsets<kTc6Threads>(g, tid, goff, soff, 1);
-  const uint32_t sb0 = g.sb[0];
+  dense_thread_offsets<kTc6Threads>(g, tid, goff, soff);
   // M = 128 (U rows), N = 128 (state columns), TF32 A (TMEM) and B (smem), F32 D
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   uint32_t phase = 0;
 
-  auto load = [&](float4 (&v)[EP], uint64_t t) {
+  auto load = [&](float2 (&v)[EPT], uint64_t t) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
 #pragma unroll
-    for (int i = 0; i < EP; ++i) v[i] = __ldcs(reinterpret_cast<const float4*>(state + base + git[i]));
+    for (int i = 0; i < EPT; ++i) v[i] = __ldcs(state + base + git[i]);
   };
-  auto step = [&](float4 (&cur)[EP], float4 (&nxt)[EP], uint64_t t) {
+  auto step = [&](float2 (&cur)[EPT], float2 (&nxt)[EPT], uint64_t t) {
     const uint64_t base = dense_tile_base(hdr, t) + goff;
     if (t + gridDim.x < ntiles) load(nxt, t + gridDim.x);
 #pragma unroll
-    for (int i = 0; i < EP; ++i) split_pair(xhi, xlo, soff + sit[i], sb0, cur[i]);
+    for (int i = 0; i < EPT; ++i) {
+      const float hx = tf32_rna(cur[i].x), hy = tf32_rna(cur[i].y);
+      const uint32_t o = soff + sit[i];
+      *reinterpret_cast<float2*>(xhi + o) = make_float2(hx, hy);
+      *reinterpret_cast<float2*>(xlo + o) = make_float2(tf32_rna(cur[i].x - hx), tf32_rna(cur[i].y - hy));
+    }
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
@@ -588,12 +573,12 @@ __global__ void __launch_bounds__(kTc6Threads, 1)
     tc_fence_before();
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < EP; ++i)
-      __stcs(reinterpret_cast<float4*>(state + base + git[i]), gather_pair(xhi, soff + sit[i], sb0));
+    for (int i = 0; i < EPT; ++i)
+      __stcs(state + base + git[i], *reinterpret_cast<const float2*>(xhi + soff + sit[i]));
     __syncthreads();
   };
 
-  float4 va[EP], vb[EP];
+  float2 va[EPT], vb[EPT];
   const uint64_t G = gridDim.x;
   if (blockIdx.x < ntiles) load(va, blockIdx.x);
   for (uint64_t t = blockIdx.x; t < ntiles; t += 2 * G) {

@@ -1088,6 +1088,11 @@ extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng
         std::fclose(f);
       }
     }
+    if (std::getenv("SVB_JIT_NOCOMPILE")) {  // timing of source generation alone
+      *cubin_bytes = 0;
+      for (auto& x : srcs) *cubin_bytes += (int64_t)x.size();
+      return SVB_OK;
+    }
     std::vector<std::vector<char>> cubins(srcs.size());
     std::vector<std::string> logs(srcs.size());
     std::vector<std::thread> th;

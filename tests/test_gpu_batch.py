@@ -66,9 +66,14 @@ def test_mixed_batch_routes_and_records_errors():
     for c, r in zip(circs[:-1], res[:-1]):
         assert isinstance(r, RunResult)
         assert sum(r.counts.values()) == 2000
-    # circuits beyond shared memory take the regular path: identical to sv.run
+    # circuits beyond shared memory take the executor: identical to sv.run
     for k in (2, 3, 4, 5):
         assert res[k].counts == sv.run(circs[k], 2000, 9, sampler="cdf").counts
+    # ... and every routed circuit against the oracle's exact distribution
+    for c, r in zip(circs[:-2], res[:-2]):
+        assert chisquare_pvalue(r.counts, _expected(c), 2000) > 1e-3, c.name
+    # mid-circuit circuit: the oracle's own replay, bit for bit
+    assert res[-2].counts == orc.run(mid, 2000, 9)
 
 
 def test_batch_workload_families_chi_square():

@@ -44,7 +44,9 @@ def test_pblock_single_block_equals_statevector_counts():
     (the reference's test_pblock.py:110-121)."""
     c = suite.ghz_circuit(12)
     for seed in (0, 7):
-        assert pb.run(c, 2048, seed).counts == sv.run(c, 2048, seed).counts
+        got = pb.run(c, 2048, seed).counts
+        assert got == sv.run(c, 2048, seed).counts
+        assert got == orc.run(c, 2048, seed)  # and both equal the reference algorithm
 
 
 def test_block_operations_vs_oracle():

@@ -10,7 +10,7 @@ rng = np.random.default_rng(0)
 U, _ = np.linalg.qr(rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k)))
 s = sv.DeviceState(n, "c64")
 s.apply_instructions([Instruction("h", (i,)) for i in range(n)])
-q = [3, 11, 17, 22, 29][:k]
+q = [3, 11, 17, 22, 29, 7][:k]
 for eng in ("tensor", "fma"):
     s.apply_matrix(q, U, engine=eng)
 print("ok")
