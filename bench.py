@@ -560,15 +560,17 @@ def config_batch() -> dict:
     t0 = time.perf_counter()
     batch.run_batch_codes(circs, shots=1000, seed=0)  # first call: NVRTC compiles the 24-qubit structures (disk-cached)
     dt_first = time.perf_counter() - t0
+    fresh = suite.batch_workload(10000, base=10000)  # new circuits (new angles), same structures
     t0 = time.perf_counter()
-    rc = batch.run_batch_codes(circs, shots=1000, seed=0)
+    rc = batch.run_batch_codes(fresh, shots=1000, seed=0)
     dt_codes = time.perf_counter() - t0
     errs = sum(isinstance(r, Exception) for r in rc)
+    fresh2 = suite.batch_workload(10000, base=20000)
     t0 = time.perf_counter()
-    batch.run_batch_codes(circs, shots=1000, seed=0, jit="none")
+    batch.run_batch_codes(fresh2, shots=1000, seed=0, jit="none")
     dt_none = time.perf_counter() - t0
     t0 = time.perf_counter()
-    rd = batch.run_batch(circs, shots=1000, seed=0)
+    rd = batch.run_batch(fresh2, shots=1000, seed=0, jit="none")
     dt_dict = time.perf_counter() - t0
     # CPU: the reference algorithm on one circuit per width 12..17, extrapolated
     # per circuit by gate count and 2^n (one core; batch.run_batch is sequential)
@@ -583,11 +585,14 @@ def config_batch() -> dict:
     return {
         "metric": "circuits/s (10,000 QAOA/VQE circuits, 12-24 qubits, 1000 shots each, c128, CDF sampler)",
         "device_path_s": dt_codes, "circuits_per_s": len(circs) / dt_codes, "errors": int(errs),
+        "timed_set": "suite.batch_workload(10000, base=10000): circuits never run before in the process",
         "first_call_s": dt_first, "circuits_per_s_first_call": len(circs) / dt_first,
-        "first_call_note": "includes the one-time NVRTC compile of the three 24-qubit circuit structures (cached on disk)",
+        "first_call_note": ("batch_workload(10000), the first batch of the process: includes the one-time NVRTC "
+                            "compile of the three 24-qubit circuit structures (cached on disk afterwards)"),
         "jit_none": {"s": dt_none, "circuits_per_s": len(circs) / dt_none,
                      "note": "interpreter kernels for every width (no compile at all)"},
         "with_count_dicts_s": dt_dict, "circuits_per_s_with_dicts": len(circs) / dt_dict,
+        "with_count_dicts_note": "batch.run_batch (jit='none', a third fresh set run once before) with {bitstring: count} dicts",
         "dict_errors": int(sum(isinstance(r, Exception) for r in rd)),
         "note": ("device_path = batch.run_batch_codes ((code, count) arrays per circuit; NVRTC passes for 24 "
                  "qubits as sv.run): host encoding of every gate + svb_batch_small / svb_batch_run + histograms; "

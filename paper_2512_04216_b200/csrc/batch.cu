@@ -445,6 +445,7 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
 // buffer.  No per-circuit host synchronisation: the codes come back with a
 // single copy at the end.  status[i] = 0 or the svb_status of circuit i.
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 
@@ -500,6 +501,14 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     std::atomic<int> next{0};
     std::mutex err_mu;
     std::string first_err;
+    // States that overflow L2 (>= 256 MB) run at most `heavy_max` at a time:
+    // concurrent HBM-bound programs from many streams thrash L2 and each
+    // other (measured: 200 24-qubit circuits 0.25 s on one stream, 2-16 s on 8)
+    static const int heavy_max = std::getenv("SVB_BATCH_HEAVY") ? std::max(1, std::atoi(std::getenv("SVB_BATCH_HEAVY")))
+                                                                 : 2;
+    std::mutex heavy_mu;
+    std::condition_variable heavy_cv;
+    int heavy_running = 0;
     auto worker = [&] {
       cudaSetDevice(device);
       jit_set_async(jit_mode == 2);  // never wait for NVRTC: the interpreter runs until the kernels exist
@@ -512,6 +521,19 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
         const int i = order[j];
         if (status[i] != SVB_OK) continue;
         const int n = nq[i];
+        const bool heavy = (s << n) >= (256ull << 20);
+        if (heavy) {
+          std::unique_lock<std::mutex> lk(heavy_mu);
+          heavy_cv.wait(lk, [&] { return heavy_running < heavy_max; });
+          ++heavy_running;
+        }
+        auto heavy_done = [&] {
+          if (!heavy) return;
+          cudaStreamSynchronize(st);  // its passes are done before another heavy circuit starts
+          std::lock_guard<std::mutex> lk(heavy_mu);
+          --heavy_running;
+          heavy_cv.notify_one();
+        };
         try {
           gates.resize(ngates[i]);
           for (int gi = 0; gi < ngates[i]; ++gi) expand_gate(ops[gate_off[i] + gi], fixed, gates[gi]);
@@ -538,6 +560,7 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
           std::lock_guard<std::mutex> lk(err_mu);
           if (first_err.empty()) first_err = e.what();
         }
+        heavy_done();
       }
       jit_set_async(false);
       cudaStreamSynchronize(st);

@@ -31,6 +31,7 @@
 // (complex MAC) on CUDA cores, 3*8*2^k TF32 flop on tensor cores.  complex64
 // leaves the HBM roofline on CUDA cores at k = 5 (128 FFMA per amplitude),
 // where the tensor path stays HBM-bound.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -439,6 +440,217 @@ __global__ void __launch_bounds__(kTcpThreads, 1)
   }
 }
 
+// ------------------------------------------- TMA-staged tensor-core pass
+// The tile is a box of a <= 5-dimensional tensor-map view of the state: one
+// dimension per run of tile qubits (<= 8 qubits each), each spanning up to
+// the next run, so the tile's other bits are the box coordinates; tile
+// pieces beyond five become extra copies.  Tiles land in a ring of raw slots
+// (natural tile order) by cp.async.bulk.tensor, one elected thread keeping
+// kTmaSlots tiles in flight (no registers hold prefetched data); the threads
+// split each raw tile into the TF32 hi / lo A operand, one thread issues the
+// MMAs, the epilogue writes the results back into the raw slot in natural
+// order and the same tensor map stores it (bulk async store).
+constexpr int kTmaThreads = 256, kTmaSlots = 3, kTmaMaxCopies = 16;
+
+struct TmaGeom {
+  int ncopy;                          // copies per tile (extra pieces enumerated)
+  int32_t copy_c4[kTmaMaxCopies];     // dim-4 coordinate offset of each copy
+  int8_t tdim[48];                    // tile-index bit b -> tensor dim
+  int8_t tshift[48];                  // ... and the bit's position in that dim's coordinate
+  int ntb;                            // tile-index bits
+  uint32_t erow[128];                 // natural tile index of D row (state column) c
+  uint32_t ecol[64];                  // natural tile index of block amplitude j
+};
+
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, const int32_t* c, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, const int32_t* c, const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tma_coords(const TmaGeom& tg, uint64_t t, int32_t* c) {
+  c[0] = c[1] = c[2] = c[3] = c[4] = 0;
+  for (int b = 0; b < tg.ntb; ++b)
+    if ((t >> b) & 1ull) c[tg.tdim[b]] += 1 << tg.tshift[b];
+}
+
+// Warp roles: warps 0-7 (256 threads) split tiles, issue the MMAs (thread 0)
+// and run the epilogue; warp 8 is the TMA producer (loads and stores).  The
+// roles meet only at mbarriers: full[s] (tile in slot s: TMA transaction
+// bytes), done[s] (its results are back in slot s: 256 arrivals), mma.
+template <int K>
+__global__ void __launch_bounds__(kTmaThreads + 32, 1)
+    k_dense_tma(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ bsrc, const DenseGeom g,
+                const TmaGeom tg, uint64_t ntiles, uint32_t chunk_stride) {
+  constexpr int KR = 2 << K;
+  constexpr int TILE = 1 << (K + 7);  // amplitudes per tile
+  constexpr int EPT = TILE / kTmaThreads;
+  constexpr int NCH = KR / 4;
+  constexpr uint32_t TCOLS = KR < 32 ? 32 : KR;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* raw = smem;  // kTmaSlots x TILE x 8 B
+  const uint32_t abytes = NCH * chunk_stride;
+  uint8_t* ahi = raw + kTmaSlots * TILE * 8;
+  uint8_t* alo = ahi + abytes;
+  uint8_t* bhi = alo + abytes;
+  uint8_t* blo = bhi + KR * KR * 4;
+  uint32_t* sit = reinterpret_cast<uint32_t*>(blo + KR * KR * 4);  // EPT
+  uint32_t* erow = sit + EPT;                                       // 128
+  uint32_t* ecol = erow + 128;                                      // 2^K
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ecol + (1 << K) + ((1 << K) & 1));
+  uint64_t* full = bars;
+  uint64_t* done = bars + kTmaSlots;
+  uint64_t* mmab = bars + 2 * kTmaSlots;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mmab + 1);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, quad = warp & 3, half = (warp >> 2) & 1;
+  const uint64_t G = gridDim.x;
+  constexpr uint32_t kTileBytes = TILE * 8;
+  const uint32_t copy_elems = TILE / tg.ncopy;
+
+  for (int i = tid; i < 2 * KR * KR / 4; i += blockDim.x)
+    reinterpret_cast<float4*>(bhi)[i] = reinterpret_cast<const float4*>(bsrc)[i];
+  for (int r = tid; r < EPT; r += blockDim.x) {
+    uint32_t so = 0;
+    for (int b = 8; b < g.kb; ++b)
+      if ((r >> (b - 8)) & 1) so += g.sb[b];
+    sit[r] = so;
+  }
+  for (int c = tid; c < 128; c += blockDim.x) erow[c] = tg.erow[c];
+  for (int j = tid; j < (1 << K); j += blockDim.x) ecol[j] = tg.ecol[j];
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTmaSlots; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(done + i, kTmaThreads);
+    }
+    mbar_init(mmab, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == kTmaThreads / 32) {  // ---------------- TMA producer
+    if (lane == 0) {
+      auto issue = [&](uint64_t t, int slot) {
+        int32_t c[5];
+        tma_coords(tg, t, c);
+        mbar_expect_tx(full + slot, kTileBytes);
+        for (int x = 0; x < tg.ncopy; ++x) {
+          int32_t cx[5] = {c[0], c[1], c[2], c[3], c[4] + tg.copy_c4[x]};
+          tma_load_5d(raw + (size_t)slot * kTileBytes + (size_t)x * copy_elems * 8, &tmap, cx, full + slot);
+        }
+      };
+      for (int j = 0; j < kTmaSlots; ++j) {
+        const uint64_t t = blockIdx.x + (uint64_t)j * G;
+        if (t < ntiles) issue(t, j);
+      }
+      uint32_t phase_done = 0;
+      int slot = 0;
+      for (uint64_t t = blockIdx.x; t < ntiles; t += G) {
+        mbar_wait(done + slot, (phase_done >> slot) & 1u);  // results of tile t are in the slot
+        phase_done ^= 1u << slot;
+        int32_t c[5];
+        tma_coords(tg, t, c);
+        const uint8_t* rs = raw + (size_t)slot * kTileBytes;
+        for (int x = 0; x < tg.ncopy; ++x) {
+          int32_t cx[5] = {c[0], c[1], c[2], c[3], c[4] + tg.copy_c4[x]};
+          tma_store_5d(&tmap, cx, rs + (size_t)x * copy_elems * 8);
+        }
+        bulk_commit();
+        const uint64_t tn = t + (uint64_t)kTmaSlots * G;
+        if (tn < ntiles) {
+          bulk_wait_read0();  // the store has read the slot (the compute warps work on the next tiles meanwhile)
+          issue(tn, slot);
+        }
+        slot = slot + 1 == kTmaSlots ? 0 : slot + 1;
+      }
+      bulk_wait0();
+    }
+  } else {  // ------------------------------------------- compute warps
+    uint32_t soff = 0;
+    for (int b = 0; b < 8; ++b)
+      if ((tid >> b) & 1u) soff += g.sb[b];
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(KR >> 3) << 17) | ((128u >> 4) << 24);
+    uint32_t phase_full = 0, phase_mma = 0;
+    int slot = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += G) {
+      uint8_t* rs = raw + (size_t)slot * kTileBytes;
+      mbar_wait(full + slot, (phase_full >> slot) & 1u);
+      phase_full ^= 1u << slot;
+#pragma unroll
+      for (int r = 0; r < EPT; ++r) {
+        const float2 v = *reinterpret_cast<const float2*>(rs + ((size_t)r * kTmaThreads + tid) * 8);
+        const float hx = tf32_rna(v.x), hy = tf32_rna(v.y);
+        const uint32_t o = soff + sit[r];
+        *reinterpret_cast<float2*>(ahi + o) = make_float2(hx, hy);
+        *reinterpret_cast<float2*>(alo + o) = make_float2(tf32_rna(v.x - hx), tf32_rna(v.y - hy));
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      asm volatile("bar.sync 1, %0;\n" ::"n"(kTmaThreads) : "memory");
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(ahi), a1 = smem_u32(alo), b0 = smem_u32(bhi), b1 = smem_u32(blo);
+        const uint32_t as[4] = {a1, a1, a0, a0}, bs[4] = {b1, b0, b1, b0};
+#pragma unroll
+        for (int term = 0; term < 4; ++term)
+#pragma unroll
+          for (int s = 0; s < KR / 8; ++s)
+            umma_tf32(tmem, umma_desc(as[term] + s * 2 * chunk_stride, chunk_stride, 128),
+                      umma_desc(bs[term] + s * 2 * (KR * 16), KR * 16, 128), idesc, (term | s) != 0);
+        umma_commit(mmab);
+      }
+      mbar_wait(mmab, phase_mma);
+      phase_mma ^= 1u;
+      tc_fence_after();
+      {  // D row c (lane), columns -> amplitudes j of column c, natural order into the raw slot
+        const uint32_t c = 32 * quad + lane, er = erow[c];
+        constexpr int HALF = KR / 2;
+#pragma unroll
+        for (int col = 0; col < HALF; col += 8) {
+          const int cc = half * HALF + col;
+          float y[8];
+          tmem_ld8(tmem + ((32 * quad) << 16) + cc, y);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float2*>(rs + (size_t)(er + ecol[cc / 2 + q]) * 8) =
+                make_float2(y[2 * q], y[2 * q + 1]);
+        }
+      }
+      fence_proxy_async();  // generic writes of the slot before the TMA store reads it
+      tc_fence_before();
+      mbar_arrive(done + slot);
+      slot = slot + 1 == kTmaSlots ? 0 : slot + 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TCOLS) : "memory");
+  }
+}
+
 // ---------------------------------------------- k = 6: U as the TMEM operand
 // For 6-qubit blocks the real-form unitary (128 x 128 fp32, hi and lo) does
 // not fit in shared memory next to the tile, so the roles swap: A = U lives in
@@ -754,6 +966,99 @@ static void launch_dense_tc6(void* state, int n, const int32_t* q, const double*
   SVB_CUDA(cudaFreeAsync(du, st));
 }
 
+// Tensor map of the state for the TMA-staged kernel (see k_dense_tma);
+// false when the geometry does not fit (then the register-prefetch kernels run).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool make_tma(void* state, int n, const DenseGeom& g, const int32_t* q, int k, CUtensorMap* map,
+                     TmaGeom* tg) {
+  static EncodeTiledFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  if (!encode || n > 36) return false;
+  // pieces: runs of consecutive tile qubits, <= 8 qubits each
+  std::vector<std::pair<int, int>> pc;  // (start, len)
+  for (int b = 0; b < g.kb; ++b) {
+    const int qb = g.tq[b];
+    if (!pc.empty() && pc.back().first + pc.back().second == qb && pc.back().second < 8) ++pc.back().second;
+    else pc.push_back({qb, 1});
+  }
+  if (pc[0].first != 0) return false;
+  const int nd = std::min<int>(5, (int)pc.size());
+  std::vector<int> extra;  // tile qubits beyond the fifth piece: enumerated by copies
+  for (size_t i = nd; i < pc.size(); ++i)
+    for (int j = 0; j < pc[i].second; ++j) extra.push_back(pc[i].first + j);
+  if ((1 << extra.size()) > kTmaMaxCopies) return false;
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int span_end[5];
+  for (int d = 0; d < 5; ++d) {
+    if (d < nd) {
+      const int s0 = pc[d].first, e0 = d + 1 < nd ? pc[d + 1].first : n;
+      span_end[d] = e0;
+      if (e0 - s0 > 31) return false;
+      gdim[d] = 1ull << (e0 - s0);
+      box[d] = 1u << pc[d].second;
+      if (d >= 1) gstr[d - 1] = 8ull << s0;
+    } else {
+      gdim[d] = 1;
+      box[d] = 1;
+      gstr[d - 1] = 8ull << n;
+    }
+  }
+  (void)span_end;
+  if (encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, state, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return false;
+  std::memset(tg, 0, sizeof *tg);
+  tg->ncopy = 1 << extra.size();
+  for (int x = 0; x < tg->ncopy; ++x) {
+    int32_t c4 = 0;
+    for (size_t i = 0; i < extra.size(); ++i)
+      if ((x >> i) & 1) c4 += 1 << (extra[i] - pc[nd - 1].first);
+    tg->copy_c4[x] = c4;
+  }
+  // tile-index bit b (outside qubit g.outq[b]) -> dim and coordinate bit
+  tg->ntb = g.nout;
+  for (int b = 0; b < g.nout; ++b) {
+    const int qb = g.outq[b];
+    int d = 0;
+    while (d + 1 < nd && pc[d + 1].first <= qb) ++d;
+    tg->tdim[b] = (int8_t)d;
+    tg->tshift[b] = (int8_t)(qb - pc[d].first);
+  }
+  // natural tile index of (row c, amplitude j): tile position b holds qubit
+  // g.tq[b], a block qubit (local bit i of U) or the r-th column qubit
+  std::vector<int> role(g.kb);  // >= 0: block bit i; < 0: column bit -(r + 1)
+  int r = 0;
+  for (int b = 0; b < g.kb; ++b) {
+    const int i = (int)(std::find(q, q + k, (int32_t)g.tq[b]) - q);
+    role[b] = i < k ? i : -(++r);
+  }
+  for (int c = 0; c < 128; ++c) {
+    uint32_t e = 0;
+    for (int b = 0; b < g.kb; ++b)
+      if (role[b] < 0 && ((c >> (-role[b] - 1)) & 1)) e |= 1u << b;
+    tg->erow[c] = e;
+  }
+  for (int j = 0; j < (1 << k); ++j) {
+    uint32_t e = 0;
+    for (int b = 0; b < g.kb; ++b)
+      if (role[b] >= 0 && ((j >> role[b]) & 1)) e |= 1u << b;
+    tg->ecol[j] = e;
+  }
+  return true;
+}
+
 void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* mat, cudaStream_t st) {
   require(k >= 3 && k <= kTcMaxK && n >= k + 7, SVB_E_ARG, "tensor-core dense block: need 3 <= k <= 6, n >= k + 7");
   const int D = 1 << k, KR = 2 * D;
@@ -793,6 +1098,32 @@ void launch_dense_tc(void* state, int n, const int32_t* q, int k, const double* 
   const DenseGeom g = make_geom(n, q, k, 7, 1, 8, chunk_stride);
   require(g.nout <= 32, SVB_E_ARG, "dense block: state too large for the tile-base tables");
   const uint64_t ntiles = 1ull << (n - k - 7);
+  // TMA-staged kernel on request (SVB_TC_TMA=1): at n = 30 it measured 5.4 ms
+  // (k = 5, mixed qubits) against 5.1-5.3 ms for the register-prefetch
+  // kernels below and is slower for k <= 4 (one CTA per SM, one A buffer:
+  // the MMA latency is exposed), so those stay the default
+  static const bool use_tma = std::getenv("SVB_TC_TMA") && std::atoi(std::getenv("SVB_TC_TMA")) != 0;
+  CUtensorMap tmap;
+  TmaGeom tg;
+  if (use_tma && make_tma(state, n, g, q, k, &tmap, &tg)) {
+    const int tile = 1 << (k + 7);
+    const size_t smem = (size_t)kTmaSlots * tile * 8 + 2 * (size_t)(KR / 4) * chunk_stride + 2 * (size_t)KR * KR * 4 +
+                        (size_t)(tile / kTmaThreads) * 4 + 128 * 4 + 64 * 4 + 8 * (2 * kTmaSlots + 2) + 64;
+    const unsigned grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sm_count());
+    static std::atomic<uint64_t> tattr[3] = {{0}, {0}, {0}};
+    auto go = [&](auto kern, int slot) {
+      once_per_device(tattr[slot], [&] {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      });
+      kern<<<grid, kTmaThreads + 32, smem, st>>>(tmap, db, g, tg, ntiles, chunk_stride);
+    };
+    if (k == 3) go(k_dense_tma<3>, 0);
+    else if (k == 4) go(k_dense_tma<4>, 1);
+    else go(k_dense_tma<5>, 2);
+    SVB_CHECK_LAUNCH();
+    SVB_CUDA(cudaFreeAsync(db, st));
+    return;
+  }
   // k = 5: the pipelined one-CTA kernel (measured 5.1 vs 5.7 ms at n = 30);
   // k <= 4: two CTAs per SM with register prefetch (smaller tiles need the
   // second CTA's loads in flight: 4.6 vs 8.2 ms at k = 3).  SVB_TC_PIPE=0/1 overrides.

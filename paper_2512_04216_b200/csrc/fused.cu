@@ -15,6 +15,7 @@
 // 32-amplitude contiguous runs.
 #include <algorithm>
 #include <chrono>
+#include <deque>
 #include <list>
 #include <memory>
 #include <mutex>
@@ -291,6 +292,83 @@ __global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ 
 // ------------------------------------------------------------ run_program
 template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
+// Pinned staging for program uploads.  A cudaMemcpyAsync from pageable memory
+// synchronises the stream before it starts, which would serialise the host
+// preparation of a program with the device work queued before it (the batch
+// executor queues one circuit after another on each stream).  Uploads go
+// through a per-thread pinned ring instead; a region is reused only after
+// the copy that read it has completed (its event).
+namespace {
+struct PinnedRing {
+  uint8_t* base = nullptr;
+  size_t cap = 0, head = 0;
+  struct Span { size_t off, len; cudaEvent_t ev; };
+  std::deque<Span> live;
+  ~PinnedRing() {
+    for (auto& sp : live) cudaEventDestroy(sp.ev);
+    if (base) cudaFreeHost(base);
+  }
+  void retire_all() {
+    for (auto& sp : live) {
+      cudaEventSynchronize(sp.ev);
+      cudaEventDestroy(sp.ev);
+    }
+    live.clear();
+  }
+  // host staging of n bytes, free of in-flight copies
+  uint8_t* take(size_t n) {
+    n = (n + 255) & ~size_t(255);
+    if (n > cap) {
+      retire_all();
+      if (base) cudaFreeHost(base);
+      cap = std::max<size_t>(n, 8u << 20);
+      if (cudaHostAlloc(reinterpret_cast<void**>(&base), cap, cudaHostAllocPortable) != cudaSuccess) {
+        base = nullptr;
+        cap = 0;
+        throw Error(SVB_E_OOM, "pinned staging allocation failed");
+      }
+      head = 0;
+    }
+    if (head + n > cap) head = 0;
+    const size_t lo = head, hi = head + n;
+    while (!live.empty() && (!live.front().ev || cudaEventQuery(live.front().ev) == cudaSuccess)) {
+      if (live.front().ev) cudaEventDestroy(live.front().ev);
+      live.pop_front();
+    }
+    cudaGetLastError();  // a not-ready query is not an error
+    for (auto it = live.begin(); it != live.end();) {
+      if (it->off < hi && it->off + it->len > lo) {  // an in-flight copy still reads this region
+        if (it->ev) {
+          cudaEventSynchronize(it->ev);
+          cudaEventDestroy(it->ev);
+        }
+        it = live.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    head = hi;
+    uint8_t* p = base + lo;
+    live.push_back({lo, n, nullptr});
+    return p;
+  }
+  void recorded(cudaStream_t st) {  // the copy from the last take() is queued on st
+    cudaEvent_t ev;
+    SVB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SVB_CUDA(cudaEventRecord(ev, st));
+    live.back().ev = ev;
+  }
+};
+thread_local PinnedRing t_ring;
+}  // namespace
+
+static void upload(void* dst, const void* src, size_t n, cudaStream_t st) {
+  uint8_t* h = t_ring.take(n);
+  std::memcpy(h, src, n);
+  SVB_CUDA(cudaMemcpyAsync(dst, h, n, cudaMemcpyHostToDevice, st));
+  t_ring.recorded(st);
+}
+
 // out: destination of the last pass when the program's final permutation is
 // fused into it (prog.perm_fused; a second state-sized buffer), else unused.
 // zacc: fused <Z> accumulators (zacc_doubles) when the last pass has zsum.
@@ -303,9 +381,12 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
   size_t obytes = std::max<size_t>(prog.ops.size(), 16);
   uint8_t* dbuf = nullptr;
   SVB_CUDA(cudaMallocAsync(&dbuf, pbytes + obytes, st));
-  SVB_CUDA(cudaMemcpyAsync(dbuf, prog.passes.data(), pbytes, cudaMemcpyHostToDevice, st));
-  if (!prog.ops.empty())
-    SVB_CUDA(cudaMemcpyAsync(dbuf + pbytes, prog.ops.data(), prog.ops.size(), cudaMemcpyHostToDevice, st));
+  {  // one pinned upload of descriptors + op stream
+    std::vector<uint8_t> blob(pbytes + prog.ops.size());
+    std::memcpy(blob.data(), prog.passes.data(), pbytes);
+    if (!prog.ops.empty()) std::memcpy(blob.data() + pbytes, prog.ops.data(), prog.ops.size());
+    upload(dbuf, blob.data(), blob.size(), st);
+  }
   const PassDev* dpass = reinterpret_cast<const PassDev*>(dbuf);
   const uint8_t* dops = dbuf + pbytes;
   if (prog.passes.back().zsum) {  // device-side pointer only: the host PassDev (and JIT cache keys) keep zacc = 0
@@ -316,8 +397,7 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     // kernel may sum over an upper bound of the grid
     const PassDev& lp = prog.passes.back();
     SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * zacc_doubles(1u << (lp.m - lp.rb), lp.rb), st));
-    SVB_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp,
-                             cudaMemcpyHostToDevice, st));
+    upload(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp, st);
   }
   // the attribute is per function and device: set it once per device to the
   // largest size any program can request (a per-call value would race between

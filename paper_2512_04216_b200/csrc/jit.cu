@@ -824,7 +824,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
   }
   std::vector<size_t> todo;
   if (!hit) {
-    std::lock_guard<std::mutex> lk(g_mu);
+    // sources are generated without the cache lock (workers of the batch
+    // executor generate theirs in parallel); only the lookups are locked
     for (size_t p = 0; p < np; ++p) {
       bool imm = false;
       srcs[p] = jit_source_pass<R>(prog, (int)p, &nslots[p], &imm);
@@ -842,6 +843,9 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
+    }
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t p = 0; p < np; ++p) {
       auto it = g_cache.find(keys[p]);
       if (it != g_cache.end()) {
         fns[p] = it->second.fns[0];

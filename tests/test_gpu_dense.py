@@ -144,3 +144,35 @@ def test_tensor_engine_large_state_mirror(k):
     assert a.compare(b)["rel"] < 1e-5
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+def test_tma_staged_tensor_engine(k):
+    """The TMA-staged variant (tensor-map tile loads / stores over the
+    state's 2^q strides, SVB_TC_TMA=1) against the oracle, in a subprocess so
+    the environment switch is read fresh."""
+    import os
+    import subprocess
+    import sys
+
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+sys.path.insert(0, {repr(os.path.dirname(os.path.abspath(__file__)))})
+from test_gpu_dense import random_unitary, random_state, dense_apply, relerr
+rng = np.random.default_rng({k})
+for trial in range(3):
+    n = int(rng.integers({k} + 7, 19))
+    q = [int(x) for x in rng.choice(n, size={k}, replace=False)]
+    if trial == 0:
+        q = list(range({k}))
+    U = random_unitary({k}, rng)
+    s, ref = random_state(n, trial, "c64")
+    s.apply_matrix(q, U, engine="tensor")
+    err = relerr(s.to_numpy(), dense_apply(ref, n, q, U))
+    assert err < 1e-5, (n, q, err)
+print("ok")
+"""
+    env = dict(os.environ, SVB_TC_TMA="1")
+    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
