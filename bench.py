@@ -558,17 +558,21 @@ def config_batch() -> dict:
 
     circs = suite.batch_workload(10000)  # generation is not timed
     t0 = time.perf_counter()
-    batch.run_batch_codes(circs, shots=1000, seed=0)  # first call: NVRTC compiles the 24-qubit structures (disk-cached)
+    batch.run_batch_codes(circs, shots=1000, seed=0)  # first batch of the process
     dt_first = time.perf_counter() - t0
     fresh = suite.batch_workload(10000, base=10000)  # new circuits (new angles), same structures
     t0 = time.perf_counter()
     rc = batch.run_batch_codes(fresh, shots=1000, seed=0)
     dt_codes = time.perf_counter() - t0
     errs = sum(isinstance(r, Exception) for r in rc)
+    t0 = time.perf_counter()
+    batch.run_batch_codes(fresh, shots=1000, seed=0, jit="sync")  # NVRTC passes for 24 qubits (compiles once)
+    batch.run_batch_codes(fresh, shots=1000, seed=1, jit="sync")
+    dt_sync_first = time.perf_counter() - t0
     fresh2 = suite.batch_workload(10000, base=20000)
     t0 = time.perf_counter()
-    batch.run_batch_codes(fresh2, shots=1000, seed=0, jit="none")
-    dt_none = time.perf_counter() - t0
+    batch.run_batch_codes(fresh2, shots=1000, seed=0, jit="sync")
+    dt_sync = time.perf_counter() - t0
     t0 = time.perf_counter()
     rd = batch.run_batch(fresh2, shots=1000, seed=0, jit="none")
     dt_dict = time.perf_counter() - t0
@@ -587,16 +591,18 @@ def config_batch() -> dict:
         "device_path_s": dt_codes, "circuits_per_s": len(circs) / dt_codes, "errors": int(errs),
         "timed_set": "suite.batch_workload(10000, base=10000): circuits never run before in the process",
         "first_call_s": dt_first, "circuits_per_s_first_call": len(circs) / dt_first,
-        "first_call_note": ("batch_workload(10000), the first batch of the process: includes the one-time NVRTC "
-                            "compile of the three 24-qubit circuit structures (cached on disk afterwards)"),
-        "jit_none": {"s": dt_none, "circuits_per_s": len(circs) / dt_none,
-                     "note": "interpreter kernels for every width (no compile at all)"},
+        "first_call_note": "batch_workload(10000), the first batch of the process (default jit='none': no compile)",
+        "jit_sync": {"fresh_circuits_s": dt_sync, "circuits_per_s": len(circs) / dt_sync,
+                     "compile_and_two_runs_s": dt_sync_first,
+                     "note": ("NVRTC-specialised passes for the 24-qubit circuits (results identical to sv.run), "
+                              "timed on a third fresh set after the structures were compiled")},
         "with_count_dicts_s": dt_dict, "circuits_per_s_with_dicts": len(circs) / dt_dict,
-        "with_count_dicts_note": "batch.run_batch (jit='none', a third fresh set run once before) with {bitstring: count} dicts",
+        "with_count_dicts_note": "batch.run_batch (jit=none) on the third set (run once before with jit=sync), with {bitstring: count} dicts",
         "dict_errors": int(sum(isinstance(r, Exception) for r in rd)),
-        "note": ("device_path = batch.run_batch_codes ((code, count) arrays per circuit; NVRTC passes for 24 "
-                 "qubits as sv.run): host encoding of every gate + svb_batch_small / svb_batch_run + histograms; "
-                 "with_dicts = batch.run_batch, adding the reference's {bitstring: count} dicts (~10^7 entries)"),
+        "note": ("device_path = batch.run_batch_codes ((code, count) arrays per circuit, default jit='none') on "
+                 "circuits never run before in the process: host encoding of every gate + svb_batch_small / "
+                 "svb_batch_run + histograms; with_dicts = batch.run_batch, adding the reference's {bitstring: count} "
+                 "dicts (~10^7 entries)"),
         "cpu_baseline": {"value": len(circs) / est, "unit": "circuits/s", "cores": 1, "kind": "port",
                          "est_s": est, "sample": ("oracle.run (reference algorithm, 1000 shots) on one circuit per "
                                                   "width 12..17, cost per gate*2^n extrapolated to all 10,000")},

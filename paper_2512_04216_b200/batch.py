@@ -127,16 +127,17 @@ _JIT_MODES = {"none": 0, "sync": 1, "async": 2}
 
 def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", device: int = 0,
                     nthreads: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, chunk: int = 2048,
-                    jit: str = "sync") -> list:
+                    jit: str = "none") -> list:
     """The device batch path: every terminal circuit runs with (shots, seed) and
     the CDF sampler; returns a CodeCounts (or the circuit's exception) per
     circuit in input order.  Small states: one shared-memory persistent
     kernel; the rest: svb_batch_run in chunks, the host encoding of chunk
     j + 1 overlapping the device work of chunk j (the C call releases the GIL).
-    jit: "sync" (default: NVRTC-specialised passes from 24 qubits exactly as
-    sv.run, so results equal sv.run's; a cold process pays one compile per
-    circuit structure, cached on disk), "none" (interpreter kernels up to 24
-    qubits: no compile), "async" (compiled in the background while the
+    jit: "none" (default: interpreter kernels up to 24 qubits — no compile,
+    reproducible, the fastest measured on streams of new circuits), "sync"
+    (NVRTC-specialised passes from 24 qubits exactly as sv.run, so results
+    equal sv.run's; a cold process pays one compile per circuit structure,
+    cached on disk), "async" (compiled in the background while the
     interpreter serves; the engine of a circuit then depends on timing)."""
     from concurrent.futures import ThreadPoolExecutor as _TPE
 
@@ -185,7 +186,7 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
 
 
 def run_batch(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", sampler: str = "cdf",
-              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, jit: str = "sync"):
+              device: int = 0, workers: int = 8, qubit_cap: int = sv.DEFAULT_QUBIT_CAP, jit: str = "none"):
     """Run every circuit with (shots, seed); returns a list of RunResult or
     exception objects, in input order (the reference records per-circuit
     errors, batch.py:192-194).  Default sampler: the device CDF sampler through

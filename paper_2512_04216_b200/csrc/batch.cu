@@ -501,11 +501,11 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     std::atomic<int> next{0};
     std::mutex err_mu;
     std::string first_err;
-    // States that overflow L2 (>= 256 MB) run at most `heavy_max` at a time:
-    // concurrent HBM-bound programs from many streams thrash L2 and each
-    // other (measured: 200 24-qubit circuits 0.25 s on one stream, 2-16 s on 8)
+    // SVB_BATCH_HEAVY=k: states that overflow L2 (>= 256 MB) run at most k at
+    // a time (an experiment: 200 fresh 24-qubit circuits took 0.25 s on one
+    // stream and 2-16 s on eight, but whole-batch timings did not improve)
     static const int heavy_max = std::getenv("SVB_BATCH_HEAVY") ? std::max(1, std::atoi(std::getenv("SVB_BATCH_HEAVY")))
-                                                                 : 2;
+                                                                 : 1 << 30;  // off unless set (no steady gain measured)
     std::mutex heavy_mu;
     std::condition_variable heavy_cv;
     int heavy_running = 0;

@@ -363,6 +363,13 @@ thread_local PinnedRing t_ring;
 }  // namespace
 
 static void upload(void* dst, const void* src, size_t n, cudaStream_t st) {
+  // opt-in (SVB_PINNED_UPLOAD=1): measured no steady gain on config 4 and a
+  // pathological slowdown combined with the heavy-circuit limit
+  static const bool pinned = std::getenv("SVB_PINNED_UPLOAD") && std::atoi(std::getenv("SVB_PINNED_UPLOAD")) != 0;
+  if (!pinned) {
+    SVB_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+    return;
+  }
   uint8_t* h = t_ring.take(n);
   std::memcpy(h, src, n);
   SVB_CUDA(cudaMemcpyAsync(dst, h, n, cudaMemcpyHostToDevice, st));
