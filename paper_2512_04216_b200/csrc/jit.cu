@@ -1018,17 +1018,23 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       std::fprintf(stderr, "[svb] jit pass %zu: m=%d rounds=%d stages=%d grid=%u smem=%u staged=%u ndiag=%d slots=%d\n",
                    p, pd.m, pd.nrounds, stages, grid, smem, staged[p], pd.ndiag, nslots[p]);
     CUfunction f = fns[p];
-    // per-function attributes, set once per (function, carveout) and thread:
-    // the shared memory limit is always the maximum (no race between threads);
+    // per-function attributes, set once per (function, carveout) in the
+    // process (changing attributes of a function other threads are launching
+    // costs driver synchronisation: the batch executor's fresh worker threads
+    // must not redo it); the shared memory limit is always the maximum;
     // three-CTA one-round passes use little shared memory: leave L1 room for their spills
     const int carve = per_sm == direct_min_blocks() ? 60 : 100;
-    thread_local std::unordered_map<CUfunction, int> configured;
-    auto cf = configured.find(f);
-    if (cf == configured.end() || cf->second != carve) {
-      if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
-        throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
-      dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carve);
-      configured[f] = carve;
+    {
+      static std::mutex attr_mu;
+      static std::unordered_map<CUfunction, int> configured;
+      std::lock_guard<std::mutex> lk(attr_mu);
+      auto cf = configured.find(f);
+      if (cf == configured.end() || cf->second != carve) {
+        if (dr.setattr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kSmemMaxPerCTA) != CUDA_SUCCESS)
+          throw Error(SVB_E_CUDA, "jit: cannot set shared memory size");
+        dr.setattr(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carve);
+        configured[f] = carve;
+      }
     }
     cplx<R>* s = state;
     cplx<R>* so = pd.perm_out ? out : state;
