@@ -15,7 +15,7 @@ import numpy as np
 
 from .result import BackendError, QubitCapError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb.so")
+LIB_PATH = os.environ.get("SVB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb.so")
 
 SVB_OK, SVB_E_ARG, SVB_E_CAP, SVB_E_OOM, SVB_E_CUDA, SVB_E_NCCL, SVB_E_SAMPLING = range(7)
 SVB_C64, SVB_C128 = 0, 1

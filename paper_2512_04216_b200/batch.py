@@ -18,7 +18,6 @@ the circuit raised (the reference records per-circuit errors, batch.py:192-194).
 """
 from __future__ import annotations
 
-import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -30,7 +29,6 @@ from .features import terminal_measurement_only
 from .result import NoMeasurementsError, QubitCapError, RunResult, format_counts, measurement_map, output_bit_sources
 
 SMALL_MAX = {"c128": 12, "c64": 13}
-_lock = threading.Lock()
 
 
 def _bit_sources(c):

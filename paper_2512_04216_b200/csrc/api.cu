@@ -27,7 +27,7 @@ struct svb_state {
   size_t ws_doubles = 0;
   int fusion = 1, max_high = -1;
   bool zero_pending = false;  // |0...0> not yet written: the next fused pass synthesises it
-  int jit_min_n = 24;  // NVRTC-specialised passes from this many qubits up (-1: never)
+  int jit_min_n = kDefaultJitMinQubits;  // NVRTC-specialised passes from this many qubits up (-1: never)
   int tc_min_k = 5;    // svb_apply_matrix: tensor cores for dense blocks of >= this many qubits (complex64)
   int last_engine = 0;
   void* external = nullptr;  // svb_create_view: caller-owned amplitudes (never freed, always current)
@@ -382,8 +382,8 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
     for (int j = 0; j < nz; ++j) require(z_qubits[j] >= 0 && z_qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
-    const size_t zacc = zacc_doubles(kPassThreads<float> > kPassThreads<double> ? kPassThreads<float>
-                                                                                 : kPassThreads<double>, kRegBits<double>);
+    const size_t zacc = std::max({zacc_doubles(kPassThreads<float, 4>, 4), zacc_doubles(kPassThreads<float, 5>, 5),
+                                  zacc_doubles(kPassThreads<double, 4>, 4)});
     ensure_ws(h, zacc + kZaccRows + (size_t)kZaccRows * 32 + expect_ws_doubles(h->n, nz > 0 ? nz : 1) + 64);
     ZRequest z;
     z.want = nz > 0;

@@ -445,6 +445,7 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
 // buffer.  No per-circuit host synchronisation: the codes come back with a
 // single copy at the end.  status[i] = 0 or the svb_status of circuit i.
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -487,9 +488,22 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nq[a] > nq[b]; });
     SVB_CUDA(cudaSetDevice(device));
-    keep_pool_mapped(device);
+    // every buffer of the batch comes from the stream-ordered pool, kept
+    // mapped for the whole call (cudaMalloc / cudaFree would synchronise the
+    // device at every worker's start and end); trimmed back afterwards
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    cudaStream_t main_st;
+    SVB_CUDA(cudaStreamCreateWithFlags(&main_st, cudaStreamNonBlocking));
     uint64_t* dcodes = nullptr;
-    SVB_CUDA(cudaMalloc(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc));
+    SVB_CUDA(cudaMallocAsync(&dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc, main_st));
+    SVB_CUDA(cudaStreamSynchronize(main_st));
+    static const bool prof = std::getenv("SVB_BATCH_PROFILE") != nullptr;
+    std::atomic<int64_t> t_host_prog{0}, t_host_draw{0}, t_wait{0};
     const size_t s = precision == SVB_C128 ? 16 : 8;
     // jit_mode 0: interpreter kernels up to 24 qubits, NVRTC above (no compile
     // in a config-4 batch; deterministic); 1: NVRTC from 24 qubits, compiled
@@ -513,7 +527,7 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
       cudaSetDevice(device);
       jit_set_async(jit_mode == 2);  // never wait for NVRTC: the interpreter runs until the kernels exist
       cudaStream_t st = nullptr;
-      void *buf = nullptr, *spare = nullptr;
+      void *buf = nullptr, *spare = nullptr, *buf_pool = nullptr;
       if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
       ProgramStats stats{};
       std::vector<svb_gate> gates;
@@ -535,9 +549,13 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
           heavy_cv.notify_one();
         };
         try {
+          const auto c0 = std::chrono::steady_clock::now();
           gates.resize(ngates[i]);
           for (int gi = 0; gi < ngates[i]; ++gi) expand_gate(ops[gate_off[i] + gi], fixed, gates[gi]);
-          if (!buf) SVB_CUDA(state_malloc(&buf, s << n));  // largest first: the first size is the maximum
+          if (!buf) {  // largest first: the first size is the maximum
+            SVB_CUDA(cudaMallocAsync(&buf, s << n, st));
+            buf_pool = buf;
+          }
           bool zp = true;
           if (precision == SVB_C128)
             run_program_owned<double>(&buf, &spare, n, gates.data(), ngates[i], 1, jit_min, st, &stats, &zp);
@@ -547,10 +565,16 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
             if (precision == SVB_C128) launch_zero<double>(buf, n, st);
             else launch_zero<float>(buf, n, st);
           }
+          const auto c1 = std::chrono::steady_clock::now();
           int32_t bs[64];
           for (int p = 0; p < 64; ++p) bs[p] = p < w[i] ? bit_src[64 * i + p] : 0;
           if (precision == SVB_C128) cdf_draw<double>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
           else cdf_draw<float>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
+          if (prof) {
+            const auto c2 = std::chrono::steady_clock::now();
+            t_host_prog += std::chrono::duration_cast<std::chrono::microseconds>(c1 - c0).count();
+            t_host_draw += std::chrono::duration_cast<std::chrono::microseconds>(c2 - c1).count();
+          }
         } catch (const Error& e) {
           status[i] = e.code;
           std::lock_guard<std::mutex> lk(err_mu);
@@ -563,18 +587,34 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
         heavy_done();
       }
       jit_set_async(false);
+      const auto w0 = std::chrono::steady_clock::now();
+      // buf came from the pool; a spare the engine allocated (permutation
+      // passes) came from cudaMalloc; the two may have been swapped
+      void* pooled = buf_pool;
+      void* other = buf == buf_pool ? spare : buf;
+      if (pooled) cudaFreeAsync(pooled, st);
       cudaStreamSynchronize(st);
-      if (buf) cudaFree(buf);
-      if (spare) cudaFree(spare);
+      if (other) cudaFree(other);
+      if (prof) t_wait += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - w0).count();
       cudaStreamDestroy(st);
     };
     std::vector<std::thread> th;
     const int T = std::min(nthreads, ncirc);
     for (int t = 0; t < T; ++t) th.emplace_back(worker);
     for (auto& t : th) t.join();
-    const cudaError_t e = cudaMemcpy(out_codes, dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc,
-                                     cudaMemcpyDeviceToHost);
-    cudaFree(dcodes);
+    const cudaError_t e = cudaMemcpyAsync(out_codes, dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc,
+                                          cudaMemcpyDeviceToHost, main_st);
+    cudaFreeAsync(dcodes, main_st);
+    cudaStreamSynchronize(main_st);
+    cudaStreamDestroy(main_st);
+    if (pool) {  // back to the library's usual threshold (keep_pool_mapped) and release the rest
+      uint64_t keep = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      cudaMemPoolTrimTo(pool, keep);
+    }
+    if (prof)
+      std::fprintf(stderr, "[svb] batch_run %d circuits: host program %.1f ms, host draw %.1f ms, final wait %.1f ms (summed over workers)\n",
+                   ncirc, t_host_prog / 1e3, t_host_draw / 1e3, t_wait / 1e3);
     SVB_CUDA(e);
     if (!first_err.empty()) set_last_error(first_err.c_str());
     return SVB_OK;

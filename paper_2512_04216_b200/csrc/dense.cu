@@ -999,11 +999,9 @@ static bool make_tma(void* state, int n, const DenseGeom& g, const int32_t* q, i
   if ((1 << extra.size()) > kTmaMaxCopies) return false;
   cuuint64_t gdim[5], gstr[4];
   cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
-  int span_end[5];
   for (int d = 0; d < 5; ++d) {
     if (d < nd) {
       const int s0 = pc[d].first, e0 = d + 1 < nd ? pc[d + 1].first : n;
-      span_end[d] = e0;
       if (e0 - s0 > 31) return false;
       gdim[d] = 1ull << (e0 - s0);
       box[d] = 1u << pc[d].second;
@@ -1014,7 +1012,6 @@ static bool make_tma(void* state, int n, const DenseGeom& g, const int32_t* q, i
       gstr[d - 1] = 8ull << n;
     }
   }
-  (void)span_end;
   if (encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, state, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
       CUDA_SUCCESS)

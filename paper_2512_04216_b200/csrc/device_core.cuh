@@ -30,16 +30,67 @@ template <typename R> using cplx = typename CT<R>::T;
 template <typename R> __host__ __device__ __forceinline__ cplx<R> mk(R x, R y) {
   cplx<R> r; r.x = x; r.y = y; return r;
 }
+// complex64 on sm_100: both components of a complex value go through one
+// packed f32x2 instruction (FFMA2 / FMUL2, each lane an IEEE fp32 operation
+// rounded to nearest, as the scalar form).  The scalar-operand broadcast and
+// the swapped / lane-negated operand are FFMA2 operand modifiers, so a complex
+// multiply-add is 2 instructions instead of 4 and the Sycamore-style c64
+// passes, which were issue-bound, issue half the FMA instructions.
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000 && !defined(SVB_NO_FFMA2)
+#define SVB_FFMA2 1
+#endif
 template <typename R>
 __host__ __device__ __forceinline__ cplx<R> cmul(cplx<R> a, cplx<R> b) {
-  return mk<R>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4)
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+  else
+#endif
+    return mk<R>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 // acc + a*b
 template <typename R>
 __host__ __device__ __forceinline__ cplx<R> cfma(cplx<R> a, cplx<R> b, cplx<R> acc) {
-  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
-  return acc;
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4)
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __ffma2_rn(make_float2(a.x, a.x), b, acc));
+  else
+#endif
+  {
+    acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+    return acc;
+  }
+}
+// s*x, acc + s*x and acc + i*s*x for a real s
+template <typename R> __host__ __device__ __forceinline__ cplx<R> rmul(R s, cplx<R> x) {
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4) return __fmul2_rn(make_float2(s, s), x);
+  else
+#endif
+    return mk<R>(s * x.x, s * x.y);
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> rfma(R s, cplx<R> x, cplx<R> acc) {
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4) return __ffma2_rn(make_float2(s, s), x, acc);
+  else
+#endif
+    return mk<R>(fma(s, x.x, acc.x), fma(s, x.y, acc.y));
+}
+template <typename R> __host__ __device__ __forceinline__ cplx<R> ifma(R s, cplx<R> x, cplx<R> acc) {
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4) return __ffma2_rn(make_float2(s, s), make_float2(-x.y, x.x), acc);
+  else
+#endif
+    return mk<R>(fma(-s, x.y, acc.x), fma(s, x.x, acc.y));
+}
+// i*s*x
+template <typename R> __host__ __device__ __forceinline__ cplx<R> imul(R s, cplx<R> x) {
+#ifdef SVB_FFMA2
+  if constexpr (sizeof(R) == 4) return __fmul2_rn(make_float2(s, s), make_float2(-x.y, x.x));
+  else
+#endif
+    return mk<R>(-s * x.y, s * x.x);
 }
 template <typename R> __host__ __device__ __forceinline__ R norm2(cplx<R> a) {
   return a.x * a.x + a.y * a.y;
@@ -205,8 +256,8 @@ SVB_HD void u1_real(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval)
     if (v & (1 << B)) continue;
     if (COND && (v & rmask) != rval) continue;
     const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
-    a[v] = mk<R>(fma(m1, x1.x, m0 * x0.x), fma(m1, x1.y, m0 * x0.y));
-    a[v | (1 << B)] = mk<R>(fma(m3, x1.x, m2 * x0.x), fma(m3, x1.y, m2 * x0.y));
+    a[v] = rfma<R>(m1, x1, rmul<R>(m0, x0));
+    a[v | (1 << B)] = rfma<R>(m3, x1, rmul<R>(m2, x0));
   }
 }
 
@@ -219,8 +270,8 @@ SVB_HD void u1_rx(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval) {
     if (v & (1 << B)) continue;
     if (COND && (v & rmask) != rval) continue;
     const cplx<R> x0 = a[v], x1 = a[v | (1 << B)];
-    a[v] = mk<R>(fma(-mb, x1.y, ma * x0.x), fma(mb, x1.x, ma * x0.y));
-    a[v | (1 << B)] = mk<R>(fma(-mc, x0.y, md * x1.x), fma(mc, x0.x, md * x1.y));
+    a[v] = ifma<R>(mb, x1, rmul<R>(ma, x0));
+    a[v | (1 << B)] = ifma<R>(mc, x0, rmul<R>(md, x1));
   }
 }
 
@@ -253,8 +304,8 @@ SVB_HD void u1_anti(cplx<R>* a, const cplx<R>* m, uint32_t rmask, uint32_t rval)
 // one output row of a unit-pivot op: p + r*o; RK: 0 r = 0, 1 real, 2 imaginary, 3 complex
 template <typename R, int RK> SVB_HD cplx<R> piv_row(cplx<R> p, cplx<R> o, cplx<R> r) {
   if constexpr (RK == 0) return p;
-  else if constexpr (RK == 1) return mk<R>(fma(r.x, o.x, p.x), fma(r.x, o.y, p.y));
-  else if constexpr (RK == 2) return mk<R>(fma(-r.y, o.y, p.x), fma(r.y, o.x, p.y));
+  else if constexpr (RK == 1) return rfma<R>(r.x, o, p);
+  else if constexpr (RK == 2) return ifma<R>(r.y, o, p);
   else return cfma<R>(r, o, p);
 }
 
@@ -274,8 +325,8 @@ SVB_HD void u1_piv(cplx<R>* a, cplx<R> r0, cplx<R> r1) {
 // operands (JIT only; the generator tracks ZM through the ops)
 template <typename R, int RK> SVB_HD cplx<R> piv_mul(cplx<R> o, cplx<R> r) {  // r*o
   if constexpr (RK == 0) return mk<R>(R(0), R(0));
-  else if constexpr (RK == 1) return mk<R>(r.x * o.x, r.x * o.y);
-  else if constexpr (RK == 2) return mk<R>(-r.y * o.y, r.y * o.x);
+  else if constexpr (RK == 1) return rmul<R>(r.x, o);
+  else if constexpr (RK == 2) return imul<R>(r.y, o);
   else return cmul<R>(r, o);
 }
 template <typename R, int RK, bool PZ, bool OZ> SVB_HD cplx<R> piv_row_z(cplx<R> p, cplx<R> o, cplx<R> r) {
@@ -725,10 +776,24 @@ constexpr int kStages = 2;
 // complex128: 16 amplitudes x 256 threads (m = 12); complex64: 16 x 512 (m = 13),
 // i.e. twice the warps per SM for the cheaper type.
 template <typename R> constexpr int kRegBits = 4;
-template <typename R> constexpr int kPassThreads = sizeof(R) == 8 ? 256 : 512;
+// NVRTC-specialised complex64 passes hold 32 amplitudes per thread (5 register
+// bits): a 2^13 tile is 256 threads and two CTAs share an SM, so one CTA's
+// shared-memory exchange and barrier overlap the other's FFMA2 bursts
+// (Sycamore-32 c64: 347 -> 300 ms).  The interpreter keeps 4 (at 5 it spills).
+#ifdef SVB_C64_RB4
+template <typename R> constexpr int kJitRegBits = 4;
+#else
+template <typename R> constexpr int kJitRegBits = sizeof(R) == 8 ? 4 : 5;
+#endif
+// Launch shape of a pass with RB register bits: the threads of a default tile
+// (m = 12 complex128, 13 complex64) and the CTAs per SM it is compiled for.
 // complex128 passes run two CTAs per SM (single-stage ring each, <= 128
-// registers per thread): 16 warps hide the FP64 and shared-memory latency
-template <typename R> constexpr int kPassMinBlocks = sizeof(R) == 8 ? 2 : 1;
+// registers per thread): 16 warps hide the FP64 and shared-memory latency;
+// complex64 at RB = 4: one 512-thread CTA; at RB = 5: two 256-thread CTAs.
+__host__ __device__ constexpr int pass_tile_m(int rsize) { return rsize == 8 ? 12 : 13; }
+__host__ __device__ constexpr int pass_min_blocks_of(int rsize, int rb) { return (rsize == 8 || rb >= 5) ? 2 : 1; }
+template <typename R, int RB> constexpr int kPassThreads = 1 << (pass_tile_m((int)sizeof(R)) - RB);
+template <typename R, int RB> constexpr int kPassMinBlocks = pass_min_blocks_of((int)sizeof(R), RB);
 
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
 
@@ -1057,12 +1122,12 @@ template <typename R, int RB, int I>
 __device__ __forceinline__ void mul_half_r(cplx<R>* a, R d) {  // real factor (e.g. cz signs)
 #pragma unroll
   for (int v = 0; v < (1 << RB); ++v)
-    if (v & (1 << I)) a[v] = mk<R>(a[v].x * d, a[v].y * d);
+    if (v & (1 << I)) a[v] = rmul<R>(d, a[v]);
 }
 template <typename R, int RB>
 __device__ __forceinline__ void mul_all_r(cplx<R>* a, R d) {
 #pragma unroll
-  for (int v = 0; v < (1 << RB); ++v) a[v] = mk<R>(a[v].x * d, a[v].y * d);
+  for (int v = 0; v < (1 << RB); ++v) a[v] = rmul<R>(d, a[v]);
 }
 template <typename R, int RB>
 __device__ __forceinline__ void mul_all(cplx<R>* a, cplx<R> d) {
@@ -1412,7 +1477,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
 }
 
 template <typename R, int RB>
-__global__ void __launch_bounds__(kPassThreads<R>, kPassMinBlocks<R>)
+__global__ void __launch_bounds__(kPassThreads<R, RB>, kPassMinBlocks<R, RB>)
     k_pass(cplx<R>* state, cplx<R>* out, const PassDev* __restrict__ pdg,
            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int zero_input, int stages) {
   pass_kernel<R, RB, InterpBody>(state, out, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
@@ -1448,9 +1513,9 @@ __host__ __device__ inline int upipe_slots() {
 #endif
 }
 template <typename R>
-__host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
+__host__ __device__ inline uint32_t pass_smem(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
                                               int zsum = 0, int nrounds = 2) {
-  const uint32_t nthr = 1u << (m - kRegBits<R>);
+  const uint32_t nthr = 1u << (m - rb);
   const uint32_t ring =
       (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
   return ring + ((staged_ops + 15u) & ~15u) +
@@ -1458,7 +1523,7 @@ __host__ __device__ inline uint32_t pass_smem(int m, uint32_t staged_ops, int nd
           (uint32_t)nslots * nthr) *
              (uint32_t)sizeof(cplx<R>) +
          // zsum != 0: a ZSM kernel keeps the fused <Z> running sums in shared memory
-         (zsum ? (uint32_t)(kRegBits<R> + 3) * nthr * (uint32_t)sizeof(double) : 0u);
+         (zsum ? (uint32_t)(rb + 3) * nthr * (uint32_t)sizeof(double) : 0u);
 }
 constexpr uint32_t kSmemPerSM = 228u * 1024u, kSmemReservedPerCTA = 1024u, kPassStaticSmem = 4096u;
 // One-round direct passes of a support-tracked program (the QFT bench's last
@@ -1490,10 +1555,10 @@ inline bool uin_pass(const PassDev& pd) {  // host (JIT generation); SVB_UIN=0: 
 #endif
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
-__host__ __device__ inline int pass_stages(int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {
-  if (kPassMinBlocks<R> < 2) return 2;
+__host__ __device__ inline int pass_stages(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {
+  if (pass_min_blocks_of((int)sizeof(R), rb) < 2) return 2;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
-  return pass_smem<R>(m, staged_ops, ndiag, nslots, 1, zsum) <= per_cta ? 1 : 2;
+  return pass_smem<R>(rb, m, staged_ops, ndiag, nslots, 1, zsum) <= per_cta ? 1 : 2;
 }
 
 }  // namespace svb

@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(256) k_zsum_finish(const double* __restrict__ 
 }
 
 // ------------------------------------------------------------ run_program
-template <typename R> static constexpr int rb_of() { return kRegBits<R>; }
 
 // Pinned staging for program uploads.  A cudaMemcpyAsync from pageable memory
 // synchronises the stream before it starts, which would serialise the host
@@ -376,13 +375,43 @@ static void upload(void* dst, const void* src, size_t n, cudaStream_t st) {
   t_ring.recorded(st);
 }
 
+// Interpreter launches of a program's passes (k_pass<R, RB>).
+template <typename R, int RB>
+static void interp_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass,
+                          const uint8_t* dops, cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
+  // the attribute is per function and device: set it once per device to the
+  // largest size any program can request (a per-call value would race between
+  // threads launching different programs)
+  static std::atomic<uint64_t> once_pass{0};
+  once_per_device(once_pass, [] {
+    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxPerCTA);
+    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  });
+  for (size_t p = 0; p < prog.passes.size(); ++p) {
+    const PassDev& pd = prog.passes[p];
+    uint64_t tiles = 1ull << pd.nout;
+    unsigned threads = 1u << (pd.m - RB);
+    int stages = pass_stages<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, 0);
+    if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
+    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R, RB> : 1));
+    Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
+    const int zin = (zero_input && p == 0) ? 1 : 0;
+    if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
+    k_pass<R, RB><<<grid, threads, pass_smem<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, stages, 0, pd.nrounds), st>>>(
+        state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
+    SVB_CHECK_LAUNCH();
+    if (pf) pf->end(st);
+    stats->passes += 1;
+    stats->launches += 1;
+  }
+}
+
 // out: destination of the last pass when the program's final permutation is
 // fused into it (prog.perm_fused; a second state-sized buffer), else unused.
 // zacc: fused <Z> accumulators (zacc_doubles) when the last pass has zsum.
 template <typename R>
 static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& prog, cudaStream_t st,
                           ProgramStats* stats, bool use_jit, bool zero_input, double* zacc = nullptr) {
-  constexpr int RB = rb_of<R>();
   if (prog.passes.empty()) return;
   size_t pbytes = prog.passes.size() * sizeof(PassDev);
   size_t obytes = std::max<size_t>(prog.ops.size(), 16);
@@ -406,14 +435,6 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     SVB_CUDA(cudaMemsetAsync(zacc, 0, sizeof(double) * zacc_doubles(1u << (lp.m - lp.rb), lp.rb), st));
     upload(reinterpret_cast<uint8_t*>(last) + offsetof(PassDev, zacc), &zp, sizeof zp, st);
   }
-  // the attribute is per function and device: set it once per device to the
-  // largest size any program can request (a per-call value would race between
-  // threads launching different programs)
-  static std::atomic<uint64_t> once_pass{0};
-  once_per_device(once_pass, [] {
-    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxPerCTA);
-    cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  });
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -422,22 +443,13 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
     SVB_CUDA(cudaFreeAsync(dbuf, st));
     return;
   }
-  for (size_t p = 0; p < prog.passes.size(); ++p) {
-    const PassDev& pd = prog.passes[p];
-    uint64_t tiles = 1ull << pd.nout;
-    unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, 0);
-    if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
-    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R> : 1));
-    Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
-    const int zin = (zero_input && p == 0) ? 1 : 0;
-    if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
-    k_pass<R, RB><<<grid, threads, pass_smem<R>(pd.m, pd.ops_bytes, pd.ndiag, 0, stages, 0, pd.nrounds), st>>>(
-        state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
-    SVB_CHECK_LAUNCH();
-    if (pf) pf->end(st);
-    stats->passes += 1;
-    stats->launches += 1;
+  const int rb = prog.passes[0].rb;
+  if constexpr (sizeof(R) == 4) {
+    if (rb == 5) interp_passes<R, 5>(state, out, prog, dpass, dops, st, stats, nsm, zero_input);
+    else interp_passes<R, 4>(state, out, prog, dpass, dops, st, stats, nsm, zero_input);
+  } else {
+    if (rb != 4) throw Error(SVB_E_ARG, "complex128 passes have 4 register bits");
+    interp_passes<R, 4>(state, out, prog, dpass, dops, st, stats, nsm, zero_input);
   }
   SVB_CUDA(cudaFreeAsync(dbuf, st));
 }
@@ -612,7 +624,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
                        cudaStream_t st, ProgramStats* stats, bool* zero_pending, ZRequest* z) {
   TraceTimer tt;
   stats->gates += ng;
-  SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n);
+  SchedOptions opt = default_options(sizeof(R) == 8 ? SVB_C128 : SVB_C64, n, jit_min_n >= 0 && n >= jit_min_n);
   auto write_zero = [&] {
     if (zero_pending && *zero_pending) {
       launch_zero<R>(*state, n, st);
@@ -727,7 +739,7 @@ int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_pas
   try {
     const bool zero_start = (precision & 0x100) != 0;  // flag bit: schedule for a lazy |0...0> input
     precision &= 0xff;
-    SchedOptions o = default_options(precision, n);
+    SchedOptions o = default_options(precision, n, n >= kDefaultJitMinQubits);
     o.zero_start = zero_start;
     Program p = precision == SVB_C128 ? build_program<double>(n, gates, ng, o) : build_program<float>(n, gates, ng, o);
     int64_t r = 0;
@@ -748,7 +760,7 @@ int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_pas
 // amps are complex128 in/out.  Test hook for the scheduler without a GPU.
 int svb_emulate_apply(int n, int precision, const svb_gate* gates, int ng, double* amps, int relabel) {
   try {
-    SchedOptions o = default_options(precision, n);
+    SchedOptions o = default_options(precision, n, n >= kDefaultJitMinQubits);
     o.relabel_swaps = relabel != 0;
     o.zero_start = relabel == 2;  // caller passes |0...0> (lazy-zero layout choice)
     uint64_t len = 1ull << n;

@@ -623,7 +623,7 @@ constexpr int kImmMinQubits = 28;
 // `imm`: coefficients are immediates, so only the uniform DIAG payloads are
 // staged in shared memory (ops_mode 1).
 template <typename R> std::string jit_source_pass(const Program& prog, int p, int* nslots, bool* imm_out) {
-  constexpr int RB = kRegBits<R>;
+  const int RB = prog.passes[p].rb;
   std::ostringstream body, pro, pre;
   PrologueCtx pc;
   pc.o = &pro;
@@ -699,8 +699,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   const size_t at = b.find(from);
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
-  const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? direct_min_blocks() : kPassMinBlocks<R>;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kPassThreads<R> << ", " << minb
+  const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? direct_min_blocks() : pass_min_blocks_of((int)sizeof(R), RB);
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pass_tile_m((int)sizeof(R)) - RB)) << ", " << minb
     << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
@@ -796,7 +796,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
   static Driver dr;
   if (!dr.ok || prog.passes.empty()) return false;
-  constexpr int RB = kRegBits<R>;
+  const int RB = prog.passes[0].rb;
   int dev = 0;
   SVB_CUDA(cudaGetDevice(&dev));
   evict_lru(dr, dev);
@@ -839,7 +839,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
           staged[p] += h.bytes - (uint32_t)sizeof(OpHdr);
         }
       }
-      if (pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], 2, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
+      if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 2, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
@@ -1003,12 +1003,12 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.m, staged[p], pd.ndiag, nslots[p], zsm_pass(pd));
+    int stages = pass_stages<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], zsm_pass(pd));
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
-    const unsigned smem = pass_smem<R>(pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
-    int per_sm = stages <= 1 ? kPassMinBlocks<R> : 1;
+    const unsigned smem = pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
+    int per_sm = stages <= 1 ? pass_min_blocks_of((int)sizeof(R), pd.rb) : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
         (uint64_t)direct_min_blocks() * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
       per_sm = direct_min_blocks();
@@ -1075,7 +1075,7 @@ extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng
     const bool zero_start = (precision & 0x100) != 0;  // flag bit: schedule for a lazy |0...0> input
     const bool zsum = (precision & 0x200) != 0;        // flag bit: last pass accumulates fused <Z>
     precision &= 0xff;
-    SchedOptions o = default_options(precision, n);
+    SchedOptions o = default_options(precision, n, true);
     o.zero_start = zero_start;
     std::vector<std::string> srcs;
     if (precision == SVB_C128) {

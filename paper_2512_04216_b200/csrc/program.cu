@@ -358,9 +358,9 @@ template <typename R> bool slots_fit(const Program& prog, const PassDev& pd) {
       off += h.bytes;
     }
   }
-  if (kPassMinBlocks<R> < 2) return true;
+  if (pass_min_blocks_of((int)sizeof(R), pd.rb) < 2) return true;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
-  return pass_smem<R>(pd.m, staged, pd.ndiag, slots, 1) <= per_cta;
+  return pass_smem<R>(pd.rb, pd.m, staged, pd.ndiag, slots, 1) <= per_cta;
 }
 
 // Fuse the program's final qubit permutation into its last pass: when that
@@ -1037,10 +1037,11 @@ void emulate_program(cplx<R>* state, int n, const Program& prog) {
 template void emulate_program<float>(cplx<float>*, int, const Program&);
 template void emulate_program<double>(cplx<double>*, int, const Program&);
 
-SchedOptions default_options(int precision, int n) {
+SchedOptions default_options(int precision, int n, bool jit) {
+  (void)n;
   SchedOptions o;
-  if (precision == SVB_C128) { o.rb = 4; o.m = 12; }
-  else { o.rb = kRegBits<float>; o.m = 13; }
+  if (precision == SVB_C128) { o.rb = jit ? kJitRegBits<double> : kRegBits<double>; o.m = 12; }
+  else { o.rb = jit ? kJitRegBits<float> : kRegBits<float>; o.m = 13; }
   return o;
 }
 

@@ -63,7 +63,9 @@ struct SchedOptions {
   bool round_search = true;  // reorder ops across rounds (else program order)
 };
 
-SchedOptions default_options(int precision, int n);
+// jit: the options of a program the NVRTC passes will run (kJitRegBits)
+SchedOptions default_options(int precision, int n, bool jit = false);
+constexpr int kDefaultJitMinQubits = 24;  // a handle's NVRTC threshold (SVB_OPT_JIT_MIN_N)
 
 template <typename R>
 Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt);
