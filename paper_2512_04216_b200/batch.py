@@ -121,6 +121,13 @@ def _status_error(code: int):
 
 
 _JIT_MODES = {"none": 0, "sync": 1, "async": 2}
+last_timing: dict = {}  # wall-clock breakdown of the last run_batch_codes call (seconds)
+
+
+def _timed(fn, *args):
+    t0 = time.perf_counter()
+    r = fn(*args)
+    return r, time.perf_counter() - t0
 
 
 def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: str = "c128", device: int = 0,
@@ -129,8 +136,9 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
     """The device batch path: every terminal circuit runs with (shots, seed) and
     the CDF sampler; returns a CodeCounts (or the circuit's exception) per
     circuit in input order.  Small states: one shared-memory persistent
-    kernel; the rest: svb_batch_run in chunks, the host encoding of chunk
-    j + 1 overlapping the device work of chunk j (the C call releases the GIL).
+    kernel; the rest: two svb_batch_run calls (the `chunk` largest circuits,
+    then the others, encoded while the first call runs: the C call releases
+    the GIL).
     jit: "none" (default: interpreter kernels up to 24 qubits — no compile,
     reproducible, the fastest measured on streams of new circuits), "sync"
     (NVRTC-specialised passes from 24 qubits exactly as sv.run, so results
@@ -139,6 +147,9 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
     interpreter serves; the engine of a circuit then depends on timing)."""
     from concurrent.futures import ThreadPoolExecutor as _TPE
 
+    tm = last_timing
+    tm.clear()
+    t_start = time.perf_counter()
     results: list = [None] * len(circuits)
     small, large = [], []
     words = sv.pcg_words(seed)
@@ -157,20 +168,39 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
             large.append(i)
     # largest circuits first across chunks (the GPU tail is then short)
     large.sort(key=lambda i: -circuits[i].n_qubits)
-    with _TPE(max_workers=2) as pool:
-        fut_small = pool.submit(_codes_small, [circuits[i] for i in small], shots, words, precision, device) \
-            if small else None
+    tm["classify_s"] = time.perf_counter() - t_start
+    # two C calls, one after the other (never concurrent: two calls would
+    # double the workers contending for the device): the first `chunk`
+    # largest circuits, then the rest, encoded while the first call runs;
+    # the shared-memory batch of small circuits runs beside them
+    bounds = [0] + ([chunk] if len(large) > chunk else []) + [len(large)]
+    with _TPE(max_workers=1) as small_pool, _TPE(max_workers=1) as pool:
+        fut_small = small_pool.submit(_timed, _codes_small, [circuits[i] for i in small], shots, words, precision,
+                                      device) if small else None
         pending = []
-        for lo in range(0, len(large), chunk):
-            idx = large[lo:lo + chunk]
+        t0 = time.perf_counter()
+        for lo, hi in zip(bounds[:-1], bounds[1:]):
+            if hi <= lo:
+                continue
+            idx = large[lo:hi]
             prep = _Prepared([circuits[i] for i in idx], words)
-            pending.append((idx, prep.w, pool.submit(prep.run, shots, precision, device, nthreads, _JIT_MODES[jit])))
+            pending.append((idx, prep.w, pool.submit(_timed, prep.run, shots, precision, device, nthreads,
+                                                     _JIT_MODES[jit])))
+        tm["encode_s"] = time.perf_counter() - t0
+        tm["chunk_call_s"], tm["chunk_wait_s"], tm["hist_s"] = [], 0.0, 0.0
         for idx, w, fut in pending:
-            codes, status = fut.result()
+            t0 = time.perf_counter()
+            (codes, status), dt = fut.result()
+            t1 = time.perf_counter()
+            tm["chunk_wait_s"] += t1 - t0
+            tm["chunk_call_s"].append(dt)
             for i, cc, st in zip(idx, _histograms(codes, w), status.tolist()):
                 results[i] = cc if st == 0 else _status_error(st)
+            tm["hist_s"] += time.perf_counter() - t1
         if fut_small is not None:
-            codes, w = fut_small.result()
+            t0 = time.perf_counter()
+            (codes, w), tm["small_call_s"] = fut_small.result()
+            tm["small_wait_s"] = time.perf_counter() - t0
             for i, cc in zip(small, _histograms(codes, w)):
                 results[i] = cc
     for i, r in enumerate(results):
@@ -180,6 +210,7 @@ def run_batch_codes(circuits, shots: int = 1000, seed: int = 0, *, precision: st
                 results[i] = res
             except Exception as exc:
                 results[i] = exc
+    tm["total_s"] = time.perf_counter() - t_start
     return results
 
 

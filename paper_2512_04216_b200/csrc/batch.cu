@@ -449,6 +449,61 @@ extern "C" int svb_replay_small(int device, int precision, int n, const double* 
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+namespace {
+std::mutex g_batch_pool_mu;
+int g_batch_calls = 0;  // svb_batch_run calls in flight (pool release threshold)
+
+// Per-device arena of the workers' state buffers and sampler scratch, kept
+// across svb_batch_run calls.  Growing the stream-ordered pool by a few GiB at
+// the start of every call stalled all workers for 8-600 ms (the growth waits
+// for work already on the device, e.g. the shared-memory batch beside it);
+// the arena is allocated once (cudaMalloc), grown only for a larger state,
+// and released when a state allocation runs out of memory (state_malloc).
+struct BatchArena {
+  std::mutex mu;
+  std::vector<void*> bufs;
+  std::vector<double*> scratch;
+  size_t buf_bytes = 0, scratch_doubles = 0;
+  void release() {
+    for (void* p : bufs) cudaFree(p);
+    for (double* p : scratch) cudaFree(p);
+    bufs.clear();
+    scratch.clear();
+    buf_bytes = scratch_doubles = 0;
+  }
+  // T buffers of >= bytes and scratch of >= sd doubles (caller holds mu)
+  bool ensure(int T, size_t bytes, size_t sd) {
+    if ((int)bufs.size() >= T && buf_bytes >= bytes && scratch_doubles >= sd) return true;
+    release();
+    for (int t = 0; t < T; ++t) {
+      void* b = nullptr;
+      double* d = nullptr;
+      if (cudaMalloc(&b, bytes) != cudaSuccess || cudaMalloc(reinterpret_cast<void**>(&d), sizeof(double) * sd) != cudaSuccess) {
+        if (b) cudaFree(b);
+        cudaGetLastError();
+        release();
+        return false;
+      }
+      bufs.push_back(b);
+      scratch.push_back(d);
+    }
+    buf_bytes = bytes;
+    scratch_doubles = sd;
+    return true;
+  }
+};
+BatchArena g_arena[16];
+}  // namespace
+
+namespace svb {
+// state_malloc's out-of-memory path: give the idle batch arenas back
+void release_batch_arenas() {
+  for (BatchArena& a : g_arena) {
+    std::unique_lock<std::mutex> lk(a.mu, std::try_to_lock);
+    if (lk.owns_lock()) a.release();
+  }
+}
+}  // namespace svb
 
 #include "jit.h"
 #include "program.h"
@@ -488,13 +543,31 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return nq[a] > nq[b]; });
     SVB_CUDA(cudaSetDevice(device));
+    const size_t s_amp = precision == SVB_C128 ? 16 : 8;
+    int nmax = 0;
+    for (int i = 0; i < ncirc; ++i)
+      if (status[i] == SVB_OK) nmax = std::max(nmax, (int)nq[i]);
+    const int T = std::min(nthreads, ncirc);
+    BatchArena* arena = device >= 0 && device < 16 ? &g_arena[device] : nullptr;
+    std::unique_lock<std::mutex> arena_lk;
+    if (arena && nmax > 0) {  // a concurrent call uses the pool instead
+      arena_lk = std::unique_lock<std::mutex>(arena->mu, std::try_to_lock);
+      if (!arena_lk.owns_lock() || !arena->ensure(T, s_amp << nmax, cdf_scratch_doubles(nmax))) arena = nullptr;
+    } else {
+      arena = nullptr;
+    }
     // every buffer of the batch comes from the stream-ordered pool, kept
     // mapped for the whole call (cudaMalloc / cudaFree would synchronise the
     // device at every worker's start and end); trimmed back afterwards
+    // (concurrent calls: the first one in raises the threshold, the last one
+    // out restores it, so no call trims the pool under another's workers)
     cudaMemPool_t pool = nullptr;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      std::lock_guard<std::mutex> lk(g_batch_pool_mu);
+      if (g_batch_calls++ == 0) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
     }
     cudaGetLastError();
     cudaStream_t main_st;
@@ -504,6 +577,22 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     SVB_CUDA(cudaStreamSynchronize(main_st));
     static const bool prof = std::getenv("SVB_BATCH_PROFILE") != nullptr;
     std::atomic<int64_t> t_host_prog{0}, t_host_draw{0}, t_wait{0};
+    // SVB_BATCH_TRACE=file: per circuit host timestamps and device start/end
+    // events, appended as CSV (i, n, worker, host begin/launched/drawn us,
+    // device begin/end us; all relative to the call's start)
+    static const char* trace_path = std::getenv("SVB_BATCH_TRACE");
+    struct TraceRec { int worker = -1; double h0 = 0, h1 = 0, h2 = 0; cudaEvent_t e0 = nullptr, e1 = nullptr; };
+    std::vector<TraceRec> trace(trace_path ? ncirc : 0);
+    const auto tr0 = std::chrono::steady_clock::now();
+    cudaEvent_t tr_ev0 = nullptr;
+    if (trace_path) {
+      cudaEventCreate(&tr_ev0);
+      cudaEventRecord(tr_ev0, main_st);
+    }
+    std::atomic<int> worker_ids{0};
+    auto us_since = [&](std::chrono::steady_clock::time_point t) {
+      return std::chrono::duration<double, std::micro>(t - tr0).count();
+    };
     const size_t s = precision == SVB_C128 ? 16 : 8;
     // jit_mode 0: interpreter kernels up to 24 qubits, NVRTC above (no compile
     // in a config-4 batch; deterministic); 1: NVRTC from 24 qubits, compiled
@@ -524,10 +613,13 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     std::condition_variable heavy_cv;
     int heavy_running = 0;
     auto worker = [&] {
+      const int wid = worker_ids++;
+      const bool own = arena == nullptr;  // buffers from the pool (else the arena's slot wid)
       cudaSetDevice(device);
       jit_set_async(jit_mode == 2);  // never wait for NVRTC: the interpreter runs until the kernels exist
       cudaStream_t st = nullptr;
       void *buf = nullptr, *spare = nullptr, *buf_pool = nullptr;
+      double* cdf_scratch = nullptr;  // leaf sums / prefix of the CDF draw, sized for the worker's first (largest) circuit
       if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return;
       ProgramStats stats{};
       std::vector<svb_gate> gates;
@@ -550,10 +642,23 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
         };
         try {
           const auto c0 = std::chrono::steady_clock::now();
+          if (trace_path) {
+            trace[i].worker = wid;
+            trace[i].h0 = us_since(c0);
+            cudaEventCreate(&trace[i].e0);
+            cudaEventCreate(&trace[i].e1);
+            cudaEventRecord(trace[i].e0, st);
+          }
           gates.resize(ngates[i]);
           for (int gi = 0; gi < ngates[i]; ++gi) expand_gate(ops[gate_off[i] + gi], fixed, gates[gi]);
           if (!buf) {  // largest first: the first size is the maximum
-            SVB_CUDA(cudaMallocAsync(&buf, s << n, st));
+            if (own) {
+              SVB_CUDA(cudaMallocAsync(&buf, s << n, st));
+              SVB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cdf_scratch), sizeof(double) * cdf_scratch_doubles(n), st));
+            } else {
+              buf = arena->bufs[wid];
+              cdf_scratch = arena->scratch[wid];
+            }
             buf_pool = buf;
           }
           bool zp = true;
@@ -568,8 +673,15 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
           const auto c1 = std::chrono::steady_clock::now();
           int32_t bs[64];
           for (int p = 0; p < 64; ++p) bs[p] = p < w[i] ? bit_src[64 * i + p] : 0;
-          if (precision == SVB_C128) cdf_draw<double>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
-          else cdf_draw<float>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st);
+          if (precision == SVB_C128)
+            cdf_draw_scratch<double>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st, cdf_scratch);
+          else
+            cdf_draw_scratch<float>(buf, n, shots, pcg + 4 * i, bs, w[i], dcodes + shots * i, st, cdf_scratch);
+          if (trace_path) {
+            cudaEventRecord(trace[i].e1, st);
+            trace[i].h1 = us_since(c1);
+            trace[i].h2 = us_since(std::chrono::steady_clock::now());
+          }
           if (prof) {
             const auto c2 = std::chrono::steady_clock::now();
             t_host_prog += std::chrono::duration_cast<std::chrono::microseconds>(c1 - c0).count();
@@ -592,14 +704,14 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
       // passes) came from cudaMalloc; the two may have been swapped
       void* pooled = buf_pool;
       void* other = buf == buf_pool ? spare : buf;
-      if (pooled) cudaFreeAsync(pooled, st);
+      if (own && pooled) cudaFreeAsync(pooled, st);
+      if (own && cdf_scratch) cudaFreeAsync(cdf_scratch, st);
       cudaStreamSynchronize(st);
       if (other) cudaFree(other);
       if (prof) t_wait += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - w0).count();
       cudaStreamDestroy(st);
     };
     std::vector<std::thread> th;
-    const int T = std::min(nthreads, ncirc);
     for (int t = 0; t < T; ++t) th.emplace_back(worker);
     for (auto& t : th) t.join();
     const cudaError_t e = cudaMemcpyAsync(out_codes, dcodes, sizeof(uint64_t) * shots * (uint64_t)ncirc,
@@ -607,10 +719,32 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     cudaFreeAsync(dcodes, main_st);
     cudaStreamSynchronize(main_st);
     cudaStreamDestroy(main_st);
+    if (trace_path) {
+      if (FILE* f = std::fopen(trace_path, "a")) {
+        for (int i = 0; i < ncirc; ++i) {
+          const TraceRec& r = trace[i];
+          float g0 = -1, g1 = -1;
+          if (r.e0 && r.e1) {
+            cudaEventElapsedTime(&g0, tr_ev0, r.e0);
+            cudaEventElapsedTime(&g1, tr_ev0, r.e1);
+          }
+          std::fprintf(f, "%d,%d,%d,%.1f,%.1f,%.1f,%.1f,%.1f\n", i, nq[i], r.worker, r.h0, r.h1, r.h2, g0 * 1e3, g1 * 1e3);
+          if (r.e0) cudaEventDestroy(r.e0);
+          if (r.e1) cudaEventDestroy(r.e1);
+        }
+        std::fprintf(f, "end,%.1f\n", us_since(std::chrono::steady_clock::now()));
+        std::fclose(f);
+      }
+      cudaEventDestroy(tr_ev0);
+      cudaGetLastError();
+    }
     if (pool) {  // back to the library's usual threshold (keep_pool_mapped) and release the rest
-      uint64_t keep = 1ull << 30;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      cudaMemPoolTrimTo(pool, keep);
+      std::lock_guard<std::mutex> lk(g_batch_pool_mu);
+      if (--g_batch_calls == 0) {
+        uint64_t keep = 1ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        cudaMemPoolTrimTo(pool, keep);
+      }
     }
     if (prof)
       std::fprintf(stderr, "[svb] batch_run %d circuits: host program %.1f ms, host draw %.1f ms, final wait %.1f ms (summed over workers)\n",

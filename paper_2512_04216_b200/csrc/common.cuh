@@ -38,12 +38,14 @@ inline void require(bool ok, int code, const std::string& msg) {
 }
 
 // cudaMalloc for state-sized buffers: the stream-ordered pool keeps up to
-// 1 GiB of freed scratch mapped (svb_create), so on failure the pool is
-// trimmed and the allocation retried once.
+// 1 GiB of freed scratch mapped (svb_create) and the batch executor keeps its
+// worker buffers, so on failure both are released and the allocation retried once.
+void release_batch_arenas();  // batch.cu: the batch executor's cached buffers
 inline cudaError_t state_malloc(void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);
   if (e != cudaErrorMemoryAllocation) return e;
   cudaGetLastError();
+  release_batch_arenas();
   int dev = 0;
   cudaMemPool_t pool;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

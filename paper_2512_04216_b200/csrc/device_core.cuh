@@ -394,8 +394,15 @@ SVB_HD void u2_perm(cplx<R>* a, const int32_t* src, const cplx<R>* ph, uint32_t 
     if (v & ((1 << B1) | (1 << B2))) continue;
     if ((v & rmask) != rval) continue;
     const int i0 = v, i1 = v | (1 << B1), i2 = v | (1 << B2), i3 = v | (1 << B1) | (1 << B2);
-    cplx<R> x[4] = {a[i0], a[i1], a[i2], a[i3]};
-    auto pick = [&](int s) { return s == 0 ? x[0] : s == 1 ? x[1] : s == 2 ? x[2] : x[3]; };
+    const cplx<R> x0 = a[i0], x1 = a[i1], x2 = a[i2], x3 = a[i3];
+    // selects, not an indexed array (a runtime index into x[] put it in local memory)
+    auto pick = [x0, x1, x2, x3](int s) {
+      cplx<R> r = x0;
+      r = s == 1 ? x1 : r;
+      r = s == 2 ? x2 : r;
+      r = s == 3 ? x3 : r;
+      return r;
+    };
     a[i0] = cmul<R>(p0, pick(s0));
     a[i1] = cmul<R>(p1, pick(s1));
     a[i2] = cmul<R>(p2, pick(s2));
@@ -794,6 +801,12 @@ __host__ __device__ constexpr int pass_tile_m(int rsize) { return rsize == 8 ? 1
 __host__ __device__ constexpr int pass_min_blocks_of(int rsize, int rb) { return (rsize == 8 || rb >= 5) ? 2 : 1; }
 template <typename R, int RB> constexpr int kPassThreads = 1 << (pass_tile_m((int)sizeof(R)) - RB);
 template <typename R, int RB> constexpr int kPassMinBlocks = pass_min_blocks_of((int)sizeof(R), RB);
+// the interpreter kernel k_pass<R, RB> (SVB_INTERP_MINB1: one CTA per SM, no register cap below 255)
+#ifdef SVB_INTERP_MINB1
+template <typename R, int RB> constexpr int kInterpMinBlocks = 1;
+#else
+template <typename R, int RB> constexpr int kInterpMinBlocks = kPassMinBlocks<R, RB>;
+#endif
 
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }
 
@@ -1477,7 +1490,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
 }
 
 template <typename R, int RB>
-__global__ void __launch_bounds__(kPassThreads<R, RB>, kPassMinBlocks<R, RB>)
+__global__ void __launch_bounds__(kPassThreads<R, RB>, kInterpMinBlocks<R, RB>)
     k_pass(cplx<R>* state, cplx<R>* out, const PassDev* __restrict__ pdg,
            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int zero_input, int stages) {
   pass_kernel<R, RB, InterpBody>(state, out, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
@@ -1555,8 +1568,9 @@ inline bool uin_pass(const PassDev& pd) {  // host (JIT generation); SVB_UIN=0: 
 #endif
 constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
-__host__ __device__ inline int pass_stages(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0) {
-  if (pass_min_blocks_of((int)sizeof(R), rb) < 2) return 2;
+__host__ __device__ inline int pass_stages(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0,
+                                           int minb = 0) {
+  if ((minb > 0 ? minb : pass_min_blocks_of((int)sizeof(R), rb)) < 2) return 2;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
   return pass_smem<R>(rb, m, staged_ops, ndiag, nslots, 1, zsum) <= per_cta ? 1 : 2;
 }

@@ -391,9 +391,9 @@ static void interp_passes(cplx<R>* state, cplx<R>* out, const Program& prog, con
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, 0);
+    int stages = pass_stages<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, 0, kInterpMinBlocks<R, RB>);
     if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
-    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kPassMinBlocks<R, RB> : 1));
+    unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kInterpMinBlocks<R, RB> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);

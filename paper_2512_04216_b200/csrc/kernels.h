@@ -66,6 +66,11 @@ void alias_draw(const double* d_prob_row, const int64_t* d_alias_row, uint64_t m
 template <typename R>
 void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
               int w, uint64_t* d_codes, cudaStream_t st);
+// scratch: >= cdf_scratch_doubles(n) doubles of device memory (else per-call pool buffers)
+template <typename R>
+void cdf_draw_scratch(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
+                      int w, uint64_t* d_codes, cudaStream_t st, double* scratch);
+uint64_t cdf_scratch_doubles(int n);
 void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
                     const int32_t* bit_src, int w, uint64_t* d_codes, cudaStream_t st);
 void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uint64_t* pcg, double lo, double hi,

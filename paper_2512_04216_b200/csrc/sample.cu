@@ -259,16 +259,19 @@ __global__ void k_scan_add(T* __restrict__ out, uint64_t n, const T* __restrict_
   if (i < n && i >= (uint64_t)kScanTile) out[i] += tot[i / kScanTile];
 }
 
-template <typename T> static void device_scan(const T* in, T* out, uint64_t n, bool exclusive, cudaStream_t st) {
+// tot_scratch: >= ceil(n / kScanTile) elements of device memory, or null (pool buffer)
+template <typename T>
+static void device_scan(const T* in, T* out, uint64_t n, bool exclusive, cudaStream_t st, T* tot_scratch = nullptr) {
   if (n == 0) return;
   const uint64_t nt = (n + kScanTile - 1) / kScanTile;
-  DevBuf tot(sizeof(T) * nt, st);
-  k_scan_tiles<T><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, tot.as<T>(), exclusive ? 1 : 0);
+  DevBuf tot_buf(tot_scratch ? 0 : sizeof(T) * nt, st);
+  T* tot = tot_scratch ? tot_scratch : tot_buf.as<T>();
+  k_scan_tiles<T><<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, tot, exclusive ? 1 : 0);
   SVB_CHECK_LAUNCH();
   if (nt > 1) {
-    k_scan_totals<T><<<1, kScanThreads, 0, st>>>(tot.as<T>(), nt);
+    k_scan_totals<T><<<1, kScanThreads, 0, st>>>(tot, nt);
     SVB_CHECK_LAUNCH();
-    k_scan_add<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, tot.as<T>());
+    k_scan_add<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, tot);
     SVB_CHECK_LAUNCH();
   }
 }
@@ -278,8 +281,8 @@ static void scan_exclusive(const In* in, Out* out, uint64_t n, cudaStream_t st) 
   static_assert(sizeof(In) == sizeof(Out), "scan keeps the element type");
   device_scan<Out>(reinterpret_cast<const Out*>(in), out, n, true, st);
 }
-static void scan_inclusive(const double* in, double* out, uint64_t n, cudaStream_t st) {
-  device_scan<double>(in, out, n, false, st);
+static void scan_inclusive(const double* in, double* out, uint64_t n, cudaStream_t st, double* tot = nullptr) {
+  device_scan<double>(in, out, n, false, st, tot);
 }
 
 // np.cumsum is a left-to-right accumulation; ties between deficit and capacity
@@ -575,15 +578,22 @@ __device__ __forceinline__ uint64_t pack_code(uint64_t idx, const BitSrc& bs, in
   return code;
 }
 
-constexpr uint64_t kShotsPerThread = 64;
+// Shots per draw thread: one shot per thread until 64k threads are in flight
+// (a binary search is a chain of dependent loads, so latency, not bandwidth,
+// bounds small draws: 1000 shots at 64 per thread took ~0.8 ms), then up to
+// 64.  Each shot s uses PCG stream position s, so the codes do not depend on it.
+inline uint32_t shots_per_thread(uint64_t shots) {
+  const uint64_t k = shots >> 16;
+  return (uint32_t)(k < 1 ? 1 : k > 64 ? 64 : k);
+}
 
 __global__ void k_alias_draw(const double* __restrict__ prob_row, const int64_t* __restrict__ alias_row,
                              uint64_t m, uint64_t shots, Pcg base, BitSrc bs, int w,
-                             uint64_t* __restrict__ codes) {
+                             uint64_t* __restrict__ codes, uint32_t spt) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t s0 = t * kShotsPerThread;
+  uint64_t s0 = t * spt;
   if (s0 >= shots) return;
-  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  uint64_t s1 = s0 + spt < shots ? s0 + spt : shots;
   Pcg g = base;
   g.advance(s0);
   const double fm = (double)m;
@@ -605,9 +615,10 @@ static BitSrc make_bitsrc(const int32_t* bit_src, int w) {
 void alias_draw(const double* d_prob_row, const int64_t* d_alias_row, uint64_t m, uint64_t shots,
                 const uint64_t* pcg, const int32_t* bit_src, int w, uint64_t* d_codes,
                 cudaStream_t st) {
-  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  const uint32_t spt = shots_per_thread(shots);
+  uint64_t nthreads = (shots + spt - 1) / spt;
   k_alias_draw<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
-      d_prob_row, d_alias_row, m, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes);
+      d_prob_row, d_alias_row, m, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes, spt);
   SVB_CHECK_LAUNCH();
 }
 
@@ -679,11 +690,11 @@ __device__ __forceinline__ uint64_t cdf_pick(const double* __restrict__ cum, uin
 template <typename R>
 __global__ void k_cdf_draw_state(const cplx<R>* __restrict__ s, uint64_t m, const double* __restrict__ cum,
                                  uint64_t nleaf, uint32_t leaf_len, uint64_t shots, Pcg base, BitSrc bs, int w,
-                                 uint64_t* __restrict__ codes) {
+                                 uint64_t* __restrict__ codes, uint32_t spt) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t s0 = t * kShotsPerThread;
+  uint64_t s0 = t * spt;
   if (s0 >= shots) return;
-  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  uint64_t s1 = s0 + spt < shots ? s0 + spt : shots;
   Pcg g = base;
   g.advance(s0);
   const double total = cum[nleaf - 1];
@@ -700,11 +711,11 @@ __global__ void k_cdf_draw_state(const cplx<R>* __restrict__ s, uint64_t m, cons
 
 __global__ void k_cdf_draw_probs(const double* __restrict__ pr, uint64_t m, const double* __restrict__ cum,
                                  uint64_t nleaf, uint64_t shots, Pcg base, BitSrc bs, int w,
-                                 uint64_t* __restrict__ codes) {
+                                 uint64_t* __restrict__ codes, uint32_t spt) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t s0 = t * kShotsPerThread;
+  uint64_t s0 = t * spt;
   if (s0 >= shots) return;
-  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  uint64_t s1 = s0 + spt < shots ? s0 + spt : shots;
   Pcg g = base;
   g.advance(s0);
   const double total = cum[nleaf - 1];
@@ -715,23 +726,38 @@ __global__ void k_cdf_draw_probs(const double* __restrict__ pr, uint64_t m, cons
   }
 }
 
+uint64_t cdf_scratch_doubles(int n) {  // leaf sums, their prefix, the scan's tile totals
+  const uint64_t m = 1ull << n, nleaf = m / cdf_leaf_len(m);
+  return 2 * nleaf + (nleaf + kScanTile - 1) / kScanTile;
+}
+
 template <typename R>
-void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
-              int w, uint64_t* d_codes, cudaStream_t st) {
+void cdf_draw_scratch(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
+                      int w, uint64_t* d_codes, cudaStream_t st, double* scratch) {
   uint64_t m = 1ull << n;
   require(n >= 5, SVB_E_ARG, "cdf sampler needs n >= 5");
   const uint32_t L = cdf_leaf_len(m);
   uint64_t nleaf = m / L;
-  DevBuf leaf(sizeof(double) * nleaf, st), cum(sizeof(double) * nleaf, st);
+  double* leaf = scratch;
+  double* cum = scratch + nleaf;
   k_leaf_sums_state<R><<<grid_for(nleaf * 32, 256), 256, 0, st>>>(static_cast<const cplx<R>*>(state),
-                                                                    nleaf, L, leaf.as<double>());
+                                                                    nleaf, L, leaf);
   SVB_CHECK_LAUNCH();
-  scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
-  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  scan_inclusive(leaf, cum, nleaf, st, scratch + 2 * nleaf);
+  const uint32_t spt = shots_per_thread(shots);
+  uint64_t nthreads = (shots + spt - 1) / spt;
   k_cdf_draw_state<R><<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
-      static_cast<const cplx<R>*>(state), m, cum.as<double>(), nleaf, L, shots, pcg_from(pcg),
-      make_bitsrc(bit_src, w), w, d_codes);
+      static_cast<const cplx<R>*>(state), m, cum, nleaf, L, shots, pcg_from(pcg),
+      make_bitsrc(bit_src, w), w, d_codes, spt);
   SVB_CHECK_LAUNCH();
+}
+
+template <typename R>
+void cdf_draw(const void* state, int n, uint64_t shots, const uint64_t* pcg, const int32_t* bit_src,
+              int w, uint64_t* d_codes, cudaStream_t st) {
+  require(n >= 5, SVB_E_ARG, "cdf sampler needs n >= 5");
+  DevBuf scratch(sizeof(double) * cdf_scratch_doubles(n), st);
+  cdf_draw_scratch<R>(state, n, shots, pcg, bit_src, w, d_codes, st, scratch.as<double>());
 }
 
 void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uint64_t* pcg,
@@ -741,9 +767,10 @@ void cdf_draw_probs(const double* d_probs, uint64_t m, uint64_t shots, const uin
   k_leaf_sums_probs<<<(unsigned)((nleaf + 255) / 256), 256, 0, st>>>(d_probs, m, nleaf, leaf.as<double>());
   SVB_CHECK_LAUNCH();
   scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
-  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  const uint32_t spt = shots_per_thread(shots);
+  uint64_t nthreads = (shots + spt - 1) / spt;
   k_cdf_draw_probs<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(
-      d_probs, m, cum.as<double>(), nleaf, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes);
+      d_probs, m, cum.as<double>(), nleaf, shots, pcg_from(pcg), make_bitsrc(bit_src, w), w, d_codes, spt);
   SVB_CHECK_LAUNCH();
 }
 
@@ -751,6 +778,10 @@ template void cdf_draw<float>(const void*, int, uint64_t, const uint64_t*, const
                               uint64_t*, cudaStream_t);
 template void cdf_draw<double>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
                                uint64_t*, cudaStream_t);
+template void cdf_draw_scratch<float>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
+                                      uint64_t*, cudaStream_t, double*);
+template void cdf_draw_scratch<double>(const void*, int, uint64_t, const uint64_t*, const int32_t*, int,
+                                       uint64_t*, cudaStream_t, double*);
 
 // ------------------------------------------------- sharded CDF slice draw
 // Shot s (stream position s) belongs to this shard when its global target
@@ -760,11 +791,11 @@ __global__ void k_slice_draw(const double* __restrict__ cum, const double* __res
                              const void* __restrict__ state, int prec128, uint64_t m, uint64_t nleaf,
                              uint32_t leaf_len, uint64_t shots,
                              Pcg base, double lo, double hi, double total, BitSrc bs, int w, uint64_t code_or,
-                             uint64_t* __restrict__ codes) {
+                             uint64_t* __restrict__ codes, uint32_t spt) {
   uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint64_t s0 = t * kShotsPerThread;
+  uint64_t s0 = t * spt;
   if (s0 >= shots) return;
-  uint64_t s1 = s0 + kShotsPerThread < shots ? s0 + kShotsPerThread : shots;
+  uint64_t s1 = s0 + spt < shots ? s0 + spt : shots;
   Pcg g = base;
   g.advance(s0);
   auto prob = [&](uint64_t i) {
@@ -810,10 +841,11 @@ void slice_draw(const void* state, int prec128, int n, uint64_t shots, const uin
   scan_inclusive(leaf.as<double>(), cum.as<double>(), nleaf, st);
   BitSrc bs;
   for (int p = 0; p < 64; ++p) bs.b[p] = p < w ? (int8_t)bit_src[p] : (int8_t)-1;
-  uint64_t nthreads = (shots + kShotsPerThread - 1) / kShotsPerThread;
+  const uint32_t spt = shots_per_thread(shots);
+  uint64_t nthreads = (shots + spt - 1) / spt;
   k_slice_draw<<<(unsigned)((nthreads + 127) / 128), 128, 0, st>>>(cum.as<double>(), nullptr, state, prec128, m,
                                                                    nleaf, L, shots, pcg_from(pcg), lo, hi, total, bs,
-                                                                   w, code_or, d_codes);
+                                                                   w, code_or, d_codes, spt);
   SVB_CHECK_LAUNCH();
 }
 
