@@ -268,7 +268,8 @@ int svb_replay(svb_handle work, svb_handle prefix, const int32_t* ops, int n_ops
  * svb_plan: precision | 0x100 schedules for a lazy |0...0> input; *has_perm =
  * 0 (no permutation), 1 (separate final permutation pass), 2 (fused into the
  * last pass's store), 3 (the input is permuted first into the layout that
- * absorbs the swap relabeling).  svb_emulate_apply: relabel_swaps 0 = swaps as ops,
+ * absorbs the swap relabeling), 4 (that permutation fused into the first
+ * pass's loads).  svb_emulate_apply: relabel_swaps 0 = swaps as ops,
  * 1 = relabeling + final permutation, 2 = relabeling for a |0...0> input. */
 int svb_plan(int n, int precision, const svb_gate* gates, int n_gates, int64_t* n_passes,
              int64_t* n_rounds, int64_t* op_bytes, int32_t* has_perm);

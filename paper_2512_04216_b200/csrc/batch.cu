@@ -550,12 +550,14 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
     const int T = std::min(nthreads, ncirc);
     BatchArena* arena = device >= 0 && device < 16 ? &g_arena[device] : nullptr;
     std::unique_lock<std::mutex> arena_lk;
+    const auto ta0 = std::chrono::steady_clock::now();
     if (arena && nmax > 0) {  // a concurrent call uses the pool instead
       arena_lk = std::unique_lock<std::mutex>(arena->mu, std::try_to_lock);
       if (!arena_lk.owns_lock() || !arena->ensure(T, s_amp << nmax, cdf_scratch_doubles(nmax))) arena = nullptr;
     } else {
       arena = nullptr;
     }
+    const double arena_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta0).count();
     // every buffer of the batch comes from the stream-ordered pool, kept
     // mapped for the whole call (cudaMalloc / cudaFree would synchronise the
     // device at every worker's start and end); trimmed back afterwards
@@ -747,8 +749,10 @@ extern "C" int svb_batch_run(int device, int precision, int ncirc, const int32_t
       }
     }
     if (prof)
-      std::fprintf(stderr, "[svb] batch_run %d circuits: host program %.1f ms, host draw %.1f ms, final wait %.1f ms (summed over workers)\n",
-                   ncirc, t_host_prog / 1e3, t_host_draw / 1e3, t_wait / 1e3);
+      std::fprintf(stderr, "[svb] batch_run %d circuits: arena %.1f ms, setup %.1f ms, host program %.1f ms, host draw %.1f ms, final wait %.1f ms (summed over workers), total %.1f ms\n",
+                   ncirc, arena_ms, std::chrono::duration<double, std::milli>(tr0 - ta0).count() - arena_ms,
+                   t_host_prog / 1e3, t_host_draw / 1e3, t_wait / 1e3,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta0).count());
     SVB_CUDA(e);
     if (!first_err.empty()) set_last_error(first_err.c_str());
     return SVB_OK;

@@ -218,6 +218,18 @@ struct PassDev {
   // zero_start support tracking: positions of the tile with a bit in dmask are
   // |0...0>-only so far (never written): the loader synthesises zeros there
   uint64_t dmask;
+  // fused initial permutation (first pass of a program on a written input
+  // whose swap relabeling needs the input in another qubit order): the tile
+  // loads read the input buffer at bit ipos[l] for local bit l and ioutpos[i]
+  // for tile bit i, and the pass stores into the output buffer in the
+  // program's layout.  ld_local[b]: the local bit of load-order bit b (the
+  // low load-order bits are the threads', so they are the local bits with
+  // the lowest input positions: the loads stay coalesced).
+  int32_t perm_in;
+  int32_t pad3[3];
+  int32_t ipos[16];
+  int32_t ioutpos[48];
+  uint8_t ld_local[16];
 };
 static_assert(sizeof(PassDev) % 16 == 0, "PassDev is copied in 16-byte units");
 constexpr uint32_t kMaxPassOpBytes = 72 * 1024;
@@ -822,6 +834,26 @@ __device__ __forceinline__ uint64_t tile_base_warp(const PassDev& pd, uint64_t t
   return ((uint64_t)hi << 32) | lo;
 }
 
+// Tile base in the input buffer's layout (differs only for a perm_in pass).
+template <int PERMIN>
+__device__ __forceinline__ uint64_t tile_base_ld(const PassDev& pd, uint64_t t, uint32_t lane) {
+  if (!PERMIN || !pd.perm_in) return tile_base_warp(pd, t, lane);
+  uint64_t v = 0;
+  if ((int)lane < pd.nout && ((t >> lane) & 1ull)) v = 1ull << pd.ioutpos[lane];
+  if ((int)lane + 32 < pd.nout && ((t >> (lane + 32)) & 1ull)) v |= 1ull << pd.ioutpos[lane + 32];
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
+// Local index of load-order index j (identity unless perm_in).
+__host__ __device__ __forceinline__ uint32_t ld_order_local(const PassDev& pd, uint32_t j) {
+  if (!pd.perm_in) return j;
+  uint32_t r = 0;
+  for (int b = 0; b < pd.m; ++b)
+    if ((j >> b) & 1u) r |= 1u << pd.ld_local[b];
+  return r;
+}
+
 template <typename R> __device__ __forceinline__ cplx<R> shfl_xor_c(cplx<R> x, int o) {
   x.x = __shfl_xor_sync(0xffffffffu, x.x, o);
   x.y = __shfl_xor_sync(0xffffffffu, x.y, o);
@@ -892,7 +924,7 @@ template <typename R, int RB> struct PassCtx {
   static constexpr int kHoist = 4;  // rounds whose thread constants live in registers
   const PassDev& pd;
   cplx<R>* state;
-  cplx<R>* out;          // destination of the last round (== state unless pd.perm_out)
+  cplx<R>* out;          // destination of the last round (== state unless pd.perm_out / pd.perm_in: the launchers pass it always)
   uint64_t pthr, pbase;  // permuted store: the thread's and the tile's destination bits
   double* zl;            // fused <Z>: the thread's running sums [RB + 3] (zsum_tile)
   double* zsm;           // or (ZSM kernels) in shared memory: [RB + 3][nthr], null otherwise
@@ -1021,7 +1053,7 @@ template <typename R, int RB>
 __device__ __forceinline__ void store_global(const PassCtx<R, RB>& c, uint64_t Fg, const RoundDev& rd,
                                              const cplx<R>* a) {
   const PassDev& pd = c.pd;
-  cplx<R>* g0 = pd.perm_out ? c.out + (c.pbase | c.pthr) : c.state + Fg;
+  cplx<R>* g0 = pd.perm_out ? c.out + (c.pbase | c.pthr) : c.out + Fg;
   const int32_t* dp = pd.perm_out ? pd.dpos : pd.pos;
   size_t goff[RB];
 #pragma unroll
@@ -1235,7 +1267,9 @@ __device__ __forceinline__ void upipe_sync(const PassCtx<R, RB>& c) {
 // then Body runs the tile's rounds out of shared memory and stores the last
 // layout straight from registers to HBM.
 // Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
-template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0>
+// PERMIN: the kernel may serve a perm_in pass (the JIT sets it only for one;
+// the extra load addressing costs the others registers)
+template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0, int PERMIN = 0>
 __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
                                             const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
@@ -1323,22 +1357,38 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;
   const int lo_bits = (31 - __clz(nthr)) + (kPer == 2 ? 1 : 0);
   uint64_t ld_tid = 0;
-  for (int l = 0; l < lo_bits; ++l)
-    if (((tid * kPer) >> l) & 1u) ld_tid |= 1ull << pd.pos[l];
   const uint32_t nld = T / (nthr * kPer);
-  if (tid < nld) {
-    uint64_t g = 0;
-    const uint32_t j = tid * nthr * kPer;
-    for (int l = lo_bits; l < m; ++l)
-      if ((j >> l) & 1u) g |= 1ull << pd.pos[l];
-    s_ldk[tid] = g;
-    s_sdk[tid] = swz<R>(j);
+  if (PERMIN && pd.perm_in) {
+    // load-order element j -> local index ld_order_local(j) -> input offset
+    // (ipos) and shared-memory slot
+    const uint32_t lj = ld_order_local(pd, tid * kPer);
+    for (int l = 0; l < m; ++l)
+      if ((lj >> l) & 1u) ld_tid |= 1ull << pd.ipos[l];
+    if (tid < nld) {
+      uint64_t g = 0;
+      const uint32_t lk = ld_order_local(pd, tid * nthr * kPer);
+      for (int l = 0; l < m; ++l)
+        if ((lk >> l) & 1u) g |= 1ull << pd.ipos[l];
+      s_ldk[tid] = g;
+      s_sdk[tid] = swz<R>(lk);
+    }
+  } else {
+    for (int l = 0; l < lo_bits; ++l)
+      if (((tid * kPer) >> l) & 1u) ld_tid |= 1ull << pd.pos[l];
+    if (tid < nld) {
+      uint64_t g = 0;
+      const uint32_t j = tid * nthr * kPer;
+      for (int l = lo_bits; l < m; ++l)
+        if ((j >> l) & 1u) g |= 1ull << pd.pos[l];
+      s_ldk[tid] = g;
+      s_sdk[tid] = swz<R>(j);
+    }
   }
   c.ring = ring;
   c.ldk = s_ldk;
   c.sdk = s_sdk;
   c.ld_tid = ld_tid;
-  c.sd_tid = swz<R>(tid * kPer);
+  c.sd_tid = swz<R>(PERMIN ? ld_order_local(pd, tid * kPer) : tid * kPer);
   c.nld = nld;
   c.zero_input = zero_input;
   c.prefetch = 0;
@@ -1363,7 +1413,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   }
   const uint32_t t0 = blockIdx.x;
   if (stages > 0) {
-    if (t0 < ntiles) Body::template issue<R, RB>(c, tile_base_warp(pd, t0, lane), ring);
+    if (t0 < ntiles) Body::template issue<R, RB>(c, tile_base_ld<PERMIN>(pd, t0, lane), ring);
     cp_async_commit();
   }
   // tile-independent per-thread constants of the body (e.g. products of
@@ -1394,7 +1444,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     const uint32_t tn = t + gridDim.x;
     if (stages > 1) {
       if (tn < ntiles)
-        Body::template issue<R, RB>(c, tile_base_warp(pd, tn, lane), ring + (size_t)((it + 1) & 1) * T);
+        Body::template issue<R, RB>(c, tile_base_ld<PERMIN>(pd, tn, lane), ring + (size_t)((it + 1) & 1) * T);
       cp_async_commit();
     }
     const uint64_t base = tile_base_warp(pd, t, lane);
@@ -1477,7 +1527,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     __syncthreads();
     if (stages == 1) {
       c.prefetch = tn < ntiles;
-      if (c.prefetch) c.next_base = tile_base_warp(pd, tn, lane);
+      if (c.prefetch) c.next_base = tile_base_ld<PERMIN>(pd, tn, lane);
     }
     Body::template tile<R, RB>(pass, c, a, ring + (size_t)(stages > 1 ? (it & 1) : 0) * T, base, bs);
     // two stages: the ring slot is rewritten by the next iteration's issue.
@@ -1493,7 +1543,7 @@ template <typename R, int RB>
 __global__ void __launch_bounds__(kPassThreads<R, RB>, kInterpMinBlocks<R, RB>)
     k_pass(cplx<R>* state, cplx<R>* out, const PassDev* __restrict__ pdg,
            const uint8_t* __restrict__ ops_g, uint32_t ntiles, int zero_input, int stages) {
-  pass_kernel<R, RB, InterpBody>(state, out, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
+  pass_kernel<R, RB, InterpBody, 0, 0, 1>(state, out, pdg, ops_g, ntiles, 0, zero_input, stages, 0, 0);
 }
 
 // Launch shape of a pass: single-stage ring and kPassMinBlocks CTAs per SM

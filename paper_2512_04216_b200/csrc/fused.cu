@@ -387,18 +387,24 @@ static void interp_passes(cplx<R>* state, cplx<R>* out, const Program& prog, con
     cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxPerCTA);
     cudaFuncSetAttribute(k_pass<R, RB>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   });
+  cplx<R>* cur = state;
+  cplx<R>* other = out;
   for (size_t p = 0; p < prog.passes.size(); ++p) {
     const PassDev& pd = prog.passes[p];
     uint64_t tiles = 1ull << pd.nout;
     unsigned threads = 1u << (pd.m - RB);
     int stages = pass_stages<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, 0, kInterpMinBlocks<R, RB>);
-    if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
+    if (stages == 1 && pd.direct && !pd.perm_in && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;  // see jit.cu
+    // perm_in / perm_out passes write the other buffer, which then holds the state
+    cplx<R>* const src = cur;
+    cplx<R>* const dst = (pd.perm_in || pd.perm_out) ? other : cur;
+    if (dst != src) std::swap(cur, other);
     unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)nsm * (stages <= 1 ? kInterpMinBlocks<R, RB> : 1));
     Profiler* pf = (stats->prof && stats->prof->on) ? stats->prof : nullptr;
     const int zin = (zero_input && p == 0) ? 1 : 0;
     if (pf) pf->begin(st, 0, pass_hbm_bytes<R>(pd, zin != 0), (int)p);
     k_pass<R, RB><<<grid, threads, pass_smem<R>(RB, pd.m, pd.ops_bytes, pd.ndiag, 0, stages, 0, pd.nrounds), st>>>(
-        state, pd.perm_out ? out : state, dpass + p, dops, (uint32_t)tiles, zin, stages);
+        src, dst, dpass + p, dops, (uint32_t)tiles, zin, stages);
     SVB_CHECK_LAUNCH();
     if (pf) pf->end(st);
     stats->passes += 1;
@@ -438,7 +444,8 @@ static void launch_passes(cplx<R>* state, cplx<R>* out, int n, const Program& pr
   int dev = 0, nsm = 148;
   SVB_CUDA(cudaGetDevice(&dev));
   SVB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (prog.perm_fused && out == nullptr) throw Error(SVB_E_CUDA, "permuted store without an output buffer");
+  if ((prog.perm_fused || prog.passes[0].perm_in) && out == nullptr)
+    throw Error(SVB_E_CUDA, "permuted load / store without a second buffer");
   if (use_jit && jit_launch_passes<R>(state, out, prog, dpass, dops, st, stats, nsm, zero_input)) {
     SVB_CUDA(cudaFreeAsync(dbuf, st));
     return;
@@ -672,7 +679,10 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
     }
   }
   const double t_build = tt.lap();
-  if (!prog.init_perm.empty()) {  // the input into the layout that absorbs the swap relabeling
+  // the input's permutation into the layout that absorbs the swap relabeling:
+  // folded into the first pass's loads when they stay coalesced, else a pass
+  const bool perm_in = !prog.init_perm.empty() && *spare != nullptr && fuse_initial_permutation<R>(prog, n);
+  if (!prog.init_perm.empty() && !perm_in) {
     write_zero();
     cplx<R>* s0 = static_cast<cplx<R>*>(*state);
     cplx<R>* sp0 = static_cast<cplx<R>*>(*spare);
@@ -686,8 +696,8 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   const uint64_t full = n == 64 ? ~0ull : (1ull << n) - 1;
   if (zin && (prog.support & full) != full)  // positions outside the passes' support are never written
     SVB_CUDA(cudaMemsetAsync(*state, 0, sizeof(cplx<R>) << n, st));
-  launch_passes<R>(static_cast<cplx<R>*>(*state), prog.perm_fused ? static_cast<cplx<R>*>(*spare) : nullptr, n,
-                   prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
+  launch_passes<R>(static_cast<cplx<R>*>(*state), (prog.perm_fused || perm_in) ? static_cast<cplx<R>*>(*spare) : nullptr,
+                   n, prog, st, stats, jit_min_n >= 0 && n >= jit_min_n, zin, z && z->fused ? z->d_acc : nullptr);
   if (z && z->fused) {
     const PassDev& lp = prog.passes.back();
     // CTAs of the last pass (the launch shapes of launch_passes / jit_launch_passes)
@@ -704,6 +714,7 @@ void run_program_owned(void** state, void** spare, int n, const svb_gate* g, int
   }
   if (zin) *zero_pending = false;
   const double t_launch = tt.lap();
+  if (perm_in) std::swap(*state, *spare);  // the first pass wrote the spare buffer
   if (prog.perm_fused) {
     std::swap(*state, *spare);  // the last pass wrote the permuted state into the spare buffer
   } else if (!prog.final_perm.empty()) {
@@ -747,8 +758,12 @@ int svb_plan(int n, int precision, const svb_gate* gates, int ng, int64_t* n_pas
     *n_passes = (int64_t)p.passes.size();
     *n_rounds = r;
     *op_bytes = (int64_t)p.ops.size();
-    // 1: final permutation pass, 2: fused into the last pass, 3: initial permutation pass
-    *has_perm = !p.init_perm.empty() ? 3 : p.final_perm.empty() ? 0 : (p.perm_fused ? 2 : 1);
+    // 1: final permutation pass, 2: fused into the last pass, 3: initial
+    // permutation pass, 4: initial permutation fused into the first pass's loads
+    bool in_fused = false;
+    if (!p.init_perm.empty())
+      in_fused = precision == SVB_C128 ? fuse_initial_permutation<double>(p, n) : fuse_initial_permutation<float>(p, n);
+    *has_perm = !p.init_perm.empty() ? (in_fused ? 4 : 3) : p.final_perm.empty() ? 0 : (p.perm_fused ? 2 : 1);
     return SVB_OK;
   } catch (const Error& e) {
     set_last_error(e.what());

@@ -596,7 +596,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << PG[v] << "ull, a[" << v << "]);\n";
       o << "    }\n";
     } else {
-      o << "    { svb::cplx<R>* g0 = c.state + Fg;\n";
+      o << "    { svb::cplx<R>* g0 = c.out + Fg;\n";  // == c.state unless perm_in
       for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << G[v] << "ull, a[" << v << "]);\n";
       o << "    }\n";
     }
@@ -661,11 +661,12 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
     for (int l = 0; l < lo_bits; ++l) tmask |= 1ull << pd0.pos[l];
     const uint64_t dm_thr = pd0.dmask & tmask;
     if (dm_thr) iss << "    const bool tdead = (c.ld_tid & " << dm_thr << "ull) != 0;\n";
+    const int32_t* lpos = pd0.perm_in ? pd0.ipos : pd0.pos;  // input positions (perm_in: see PassDev)
     for (uint32_t k = 0; k < nld; ++k) {
-      const uint32_t j = k * nthr * (uint32_t)kPer;
+      const uint32_t j = ld_order_local(pd0, k * nthr * (uint32_t)kPer);
       uint64_t g = 0;
-      for (int l = lo_bits; l < m; ++l)
-        if ((j >> l) & 1u) g |= 1ull << pd0.pos[l];
+      for (int l = 0; l < m; ++l)
+        if ((j >> l) & 1u) g |= 1ull << lpos[l];
       // never-written positions are not stored at all: round 0 of a pass with a
       // dmask takes them as constant zeros (emit_body), later rounds read what
       // round 0 wrote
@@ -705,7 +706,8 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
        "  svb::pass_kernel<R, "
-    << RB << ", PassBody, " << zsm_pass(pd0) << ", " << (uin_pass(pd0) ? 1 : 0) << ">(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
+    << RB << ", PassBody, " << zsm_pass(pd0) << ", " << (uin_pass(pd0) ? 1 : 0) << ", " << (pd0.perm_in ? 1 : 0)
+    << ">(state, out, pdg, ops_g, ntiles, pass, zero_input, stages, " << (imm ? 1 : 0) << ", "
     << pc.nslots << ");\n}\n";
   return o.str();
 }
@@ -999,6 +1001,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     std::lock_guard<std::mutex> lk(g_mu);
     g_prog.emplace(pkey, ProgKernels{fns, nslots, staged, ++g_tick});
   }
+  cplx<R>* cur = state;
+  cplx<R>* other = out;
   for (size_t p = 0; p < np; ++p) {
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
@@ -1006,7 +1010,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     int stages = pass_stages<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], zsm_pass(pd));
     // direct first round: for support-tracked passes (few live loads per tile,
     // no ring barrier); for full passes only on request (load latency exposed)
-    if (stages == 1 && pd.direct && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
+    if (stages == 1 && pd.direct && !pd.perm_in && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
     const unsigned smem = pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
     int per_sm = stages <= 1 ? pass_min_blocks_of((int)sizeof(R), pd.rb) : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
@@ -1036,8 +1040,10 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
         configured[f] = carve;
       }
     }
-    cplx<R>* s = state;
-    cplx<R>* so = pd.perm_out ? out : state;
+    // perm_in / perm_out passes write the other buffer, which then holds the state
+    cplx<R>* s = cur;
+    cplx<R>* so = (pd.perm_in || pd.perm_out) ? other : cur;
+    if (so != s) std::swap(cur, other);
     const PassDev* pdp = dpass + p;
     const uint8_t* ob = dops;
     uint32_t nt = (uint32_t)tiles;

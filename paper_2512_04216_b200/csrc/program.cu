@@ -949,6 +949,44 @@ Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& 
 template Program build_program<float>(int, const svb_gate*, int, const SchedOptions&);
 template Program build_program<double>(int, const svb_gate*, int, const SchedOptions&);
 
+// Fold the program's initial permutation (input bit q -> layout bit
+// init_perm[q]) into the first pass's tile loads (PassDev::perm_in): the pass
+// reads the input buffer at the permuted addresses and writes the other
+// buffer in the program's layout, which saves the separate permutation sweep
+// (2 s 2^n bytes).  The tile's load order takes its local bits by ascending
+// input position, so a warp's 32 loads cover one contiguous run; when the
+// tile does not contain input bits 0..4 (complex128) / 0..5 (complex64),
+// the loads would not be coalesced and the permutation stays a pass.
+template <typename R>
+bool fuse_initial_permutation(Program& prog, int n) {
+  if (prog.init_perm.empty() || prog.passes.empty()) return false;
+  PassDev& pd = prog.passes[0];
+  if (pd.dmask || pd.perm_out || pd.m > 16) return false;
+  std::vector<int> inv(n, -1);
+  for (int q = 0; q < n; ++q) inv[prog.init_perm[q]] = q;
+  std::vector<std::pair<int, int>> ord;  // (input position, local bit)
+  for (int l = 0; l < pd.m; ++l) ord.push_back({inv[pd.pos[l]], l});
+  std::sort(ord.begin(), ord.end());
+  if (std::getenv("SVB_TRACE")) {
+    std::fprintf(stderr, "[svb] perm_in candidate: input positions of the first tile:");
+    for (auto& o : ord) std::fprintf(stderr, " %d(l%d)", o.first, o.second);
+    std::fprintf(stderr, "\n");
+  }
+  const int run_bits = sizeof(R) == 8 ? 5 : 6;
+  for (int b = 0; b < run_bits; ++b)
+    if (ord[b].first != b) return false;
+  // complex64 copies aligned pairs (local bits 0 of slot and address agree)
+  if (sizeof(R) == 4 && ord[0].second != 0) return false;
+  for (int l = 0; l < pd.m; ++l) pd.ipos[l] = inv[pd.pos[l]];
+  for (int i = 0; i < pd.nout; ++i) pd.ioutpos[i] = inv[pd.outpos[i]];
+  for (int b = 0; b < pd.m; ++b) pd.ld_local[b] = (uint8_t)ord[b].second;
+  pd.perm_in = 1;
+  pd.direct = 0;  // the direct first round reads through pos: the ring path loads
+  return true;
+}
+template bool fuse_initial_permutation<float>(Program&, int);
+template bool fuse_initial_permutation<double>(Program&, int);
+
 // ------------------------------------------------------------- emulation
 static uint64_t permute_index(const PassDev& pd, uint64_t g) {
   uint64_t o = 0;

@@ -70,6 +70,10 @@ constexpr int kDefaultJitMinQubits = 24;  // a handle's NVRTC threshold (SVB_OPT
 template <typename R>
 Program build_program(int n, const svb_gate* gates, int ng, const SchedOptions& opt);
 
+// the initial permutation of `prog` folded into its first pass (PassDev::perm_in)
+template <typename R>
+bool fuse_initial_permutation(Program& prog, int n);
+
 template <typename R>
 void run_program(void* state, int n, const svb_gate* g, int ng, int fusion, int max_high,
                  cudaStream_t st, ProgramStats* stats);

@@ -875,7 +875,8 @@ def plan(n: int, instructions, precision: str = "c128", zero_start: bool = False
     check(lib().svb_plan(n, _prec_code(precision) | (0x100 if zero_start else 0), ptr(arr), int(arr.size), _lib.ctypes.byref(p),
                          _lib.ctypes.byref(r), _lib.ctypes.byref(b), _lib.ctypes.byref(perm)))
     return {"passes": p.value, "rounds": r.value, "op_bytes": b.value, "permute": bool(perm.value),
-            "permute_fused": perm.value == 2, "permute_initial": perm.value == 3, "gates": int(arr.size)}
+            "permute_fused": perm.value == 2, "permute_initial": perm.value in (3, 4),
+            "permute_initial_fused": perm.value == 4, "gates": int(arr.size)}
 
 
 __all__ = [

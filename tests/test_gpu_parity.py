@@ -580,3 +580,37 @@ def test_initial_permutation_schedule(precision):
             np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(n)],
                                        atol=10 * TOL[precision])
             s.close()
+
+
+def _swap_mix_circuit(seed):
+    from paper_2512_04216_b200.circuit import Circuit
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(14, 20))
+    c = Circuit(n)
+    for _ in range(int(rng.integers(20, 80))):
+        c.gate("h", int(rng.integers(0, n)))
+        a, b = rng.choice(n, 2, replace=False)
+        c.gate(str(rng.choice(["cx", "cz", "swap", "swap"])), int(a), int(b))
+    return c
+
+
+def test_initial_permutation_fused_into_first_pass_loads():
+    """A written input whose absorbing layout keeps input qubits 0..4 inside
+    the first pass's tile: the permutation is folded into that pass's tile
+    loads (PassDev::perm_in, out of place), JIT and interpreter bodies."""
+    c = _swap_mix_circuit(163)
+    n = c.n_qubits
+    pl = sv.plan(n, c.instructions, "c128")
+    assert pl["permute_initial_fused"], pl
+    prep = suite.random_circuit(n, 30, np.random.default_rng(5), measured=False)
+    ref = orc.unitary_state(prep)
+    for inst in c.instructions:
+        orc.apply_instruction(ref, n, inst)
+    for jit in (-1, 1):
+        s = sv.DeviceState(n, "c128")
+        s.set_option(_lib.OPT_JIT_MIN_N, jit)
+        s.apply_instructions(prep.instructions)
+        z = s.apply_gates_z(sv.gate_array(c.instructions), list(range(n)))
+        assert relerr(s.to_numpy(), ref) < TOL["c128"], jit
+        np.testing.assert_allclose(z, [orc.expectation_from_state(ref, (q,)) for q in range(n)], atol=1e-9)
+        s.close()
