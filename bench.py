@@ -542,6 +542,9 @@ def config_sycamore(peak: float) -> dict:
         "pass_table": table, "full_pass_mean_ms": float(np.mean([t["ms"] for t in full])) if full else None,
         "full_pass_mean_frac": float(np.mean([t["frac"] for t in full])) if full else None,
         "roofline_note": "bytes per pass = HBM bytes the pass moves (2*8*2^32 for a full pass); peak = MEASURED_PEAKS hbm_gbs",
+        "bound_note": ("full passes are FMA-pipe bound, not HBM bound: ncu of a full pass (profiles/r02_ncu_syc32_c64_rb5.json) "
+                       "shows the FMA pipe busy 62% with DRAM bytes = algorithmic; the pass's ~123 FMA lane-ops per "
+                       "amplitude alone take ~14 ms of the 22.9 ms"),
         "sample_ms": ms_s, "shots_per_s": shots / (ms_s / 1e3), "distinct_outcomes": int(codes.size),
         "e2e": {"run_codes_s": e2e, "shots_per_s": shots / e2e,
                 "note": "statevector.run_codes: host encode + apply + 10^6 shots + (code, count) arrays"},

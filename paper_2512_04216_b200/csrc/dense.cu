@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(kFmaThreads, 2)
         const cplx<R> xj = X[(j << cb) + c];
 #pragma unroll
         for (int o = 0; o < kFmaOut; ++o)
-          if (o < ob) acc[o] = cfma<R>(U[(i0 + o) * D + j], xj, acc[o]);
+          if (o < ob) acc[o] = cfma_scalar<R>(U[(i0 + o) * D + j], xj, acc[o]);
       }
 #pragma unroll
       for (int o = 0; o < kFmaOut; ++o)

@@ -62,6 +62,15 @@ __host__ __device__ __forceinline__ cplx<R> cfma(cplx<R> a, cplx<R> b, cplx<R> a
     return acc;
   }
 }
+// acc + a*b as four scalar FMAs: for loops bound by the FMA pipe itself (the
+// dense-block engine), where FFMA2 with the swapped operand measured ~20%
+// fewer FMAs per clock (profiles/r02_fma_pipe_microbench.txt)
+template <typename R>
+__host__ __device__ __forceinline__ cplx<R> cfma_scalar(cplx<R> a, cplx<R> b, cplx<R> acc) {
+  acc.x = fma(a.x, b.x, acc.x); acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y); acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
 // s*x, acc + s*x and acc + i*s*x for a real s
 template <typename R> __host__ __device__ __forceinline__ cplx<R> rmul(R s, cplx<R> x) {
 #ifdef SVB_FFMA2
@@ -809,9 +818,14 @@ template <typename R> constexpr int kJitRegBits = sizeof(R) == 8 ? 4 : 5;
 // complex128 passes run two CTAs per SM (single-stage ring each, <= 128
 // registers per thread): 16 warps hide the FP64 and shared-memory latency;
 // complex64 at RB = 4: one 512-thread CTA; at RB = 5: two 256-thread CTAs.
-__host__ __device__ constexpr int pass_tile_m(int rsize) { return rsize == 8 ? 12 : 13; }
+#ifdef SVB_C64_M14  // experiment: NVRTC complex64 tiles of 2^14 (512 threads x 32 amplitudes, one CTA per SM)
+__host__ __device__ constexpr int pass_tile_m(int rsize, int rb = 4) { return rsize == 8 ? 12 : (rb >= 5 ? 14 : 13); }
+__host__ __device__ constexpr int pass_min_blocks_of(int rsize, int rb) { return rsize == 8 ? 2 : 1; }
+#else
+__host__ __device__ constexpr int pass_tile_m(int rsize, int rb = 4) { return rsize == 8 ? 12 : 13; }
 __host__ __device__ constexpr int pass_min_blocks_of(int rsize, int rb) { return (rsize == 8 || rb >= 5) ? 2 : 1; }
-template <typename R, int RB> constexpr int kPassThreads = 1 << (pass_tile_m((int)sizeof(R)) - RB);
+#endif
+template <typename R, int RB> constexpr int kPassThreads = 1 << (pass_tile_m((int)sizeof(R), RB) - RB);
 template <typename R, int RB> constexpr int kPassMinBlocks = pass_min_blocks_of((int)sizeof(R), RB);
 // the interpreter kernel k_pass<R, RB> (SVB_INTERP_MINB1: one CTA per SM, no register cap below 255)
 #ifdef SVB_INTERP_MINB1
@@ -1620,7 +1634,8 @@ constexpr uint32_t kSmemMaxPerCTA = 227u * 1024u - kPassStaticSmem;
 template <typename R>
 __host__ __device__ inline int pass_stages(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int zsum = 0,
                                            int minb = 0) {
-  if ((minb > 0 ? minb : pass_min_blocks_of((int)sizeof(R), rb)) < 2) return 2;
+  if ((minb > 0 ? minb : pass_min_blocks_of((int)sizeof(R), rb)) < 2)
+    return pass_smem<R>(rb, m, staged_ops, ndiag, nslots, 2, zsum) <= kSmemMaxPerCTA ? 2 : 1;
   const uint32_t per_cta = kSmemPerSM / 2 - kSmemReservedPerCTA - kPassStaticSmem;
   return pass_smem<R>(rb, m, staged_ops, ndiag, nslots, 1, zsum) <= per_cta ? 1 : 2;
 }

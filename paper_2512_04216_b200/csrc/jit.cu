@@ -701,7 +701,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
   const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? direct_min_blocks() : pass_min_blocks_of((int)sizeof(R), RB);
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pass_tile_m((int)sizeof(R)) - RB)) << ", " << minb
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pass_tile_m((int)sizeof(R), RB) - RB)) << ", " << minb
     << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
@@ -841,7 +841,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
           staged[p] += h.bytes - (uint32_t)sizeof(OpHdr);
         }
       }
-      if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 2, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
+      if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 1, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;

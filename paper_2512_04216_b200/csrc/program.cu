@@ -905,6 +905,31 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
     remaining = skipped;
   }
   prog.support = opt.zero_start ? support : ~0ull;
+  if (std::getenv("SVB_TRACE_OPS")) {  // the op stream per pass and round (scheduler debugging)
+    static const char* kname[] = {"DIAG", "U1", "U1ANTI", "U2", "PERM2", "U1R", "U1X", "U1P", "U1PR"};
+    for (size_t p = 0; p < prog.passes.size(); ++p) {
+      const PassDev& pd = prog.passes[p];
+      for (int k = 0; k < pd.nrounds; ++k) {
+        std::fprintf(stderr, "[svb] pass %zu round %d regs", p, k);
+        for (int i = 0; i < pd.rb; ++i) std::fprintf(stderr, " q%d", pd.pos[pd.rounds[k].reg_local[i]]);
+        std::fprintf(stderr, ":");
+        for (uint32_t off = pd.rounds[k].op_off; off < pd.rounds[k].op_end;) {
+          OpHdr h;
+          std::memcpy(&h, prog.ops.data() + off, sizeof h);
+          std::fprintf(stderr, " %s(a%d b%d n%d%s%s)", h.kind >= 0 && h.kind <= 8 ? kname[h.kind] : "?", h.a, h.b, h.n,
+                       h.fmask ? " F" : "", h.rmask ? " R" : "");
+          if (h.kind == OP_DIAG) {
+            DiagHdr d;
+            std::memcpy(&d, prog.ops.data() + off + sizeof(OpHdr), sizeof d);
+            std::fprintf(stderr, "[UR%d UC%d TR%d TC%d RR%d UT%d]", d.nUR[0] + d.nUR[1] + d.nUR[2] + d.nUR[3] + d.nUR[4] + d.nUR[5],
+                         d.nUC, d.nTR, d.nTC, d.nRR, d.nUTg);
+          }
+          off += h.bytes;
+        }
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
   if (opt.zero_start && std::getenv("SVB_TRACE"))
     std::fprintf(stderr, "[svb] zero-start support %llx over %zu passes\n", (unsigned long long)support,
                  prog.passes.size());
@@ -1079,7 +1104,7 @@ SchedOptions default_options(int precision, int n, bool jit) {
   (void)n;
   SchedOptions o;
   if (precision == SVB_C128) { o.rb = jit ? kJitRegBits<double> : kRegBits<double>; o.m = 12; }
-  else { o.rb = jit ? kJitRegBits<float> : kRegBits<float>; o.m = 13; }
+  else { o.rb = jit ? kJitRegBits<float> : kRegBits<float>; o.m = pass_tile_m(4, o.rb); }
   return o;
 }
 
