@@ -438,10 +438,12 @@ class PinnedBuffer:
 
 
 class _StatePool:
-    """Idle device states kept for reuse by run() (small circuits pay no
-    cudaMalloc / stream creation per call).  Bounded by bytes; LIFO per key."""
+    """Idle device states kept for reuse by run() and the final_state /
+    expectation cache (no cudaMalloc / cudaFree / stream creation per call).
+    Bounded by bytes (32 GiB: one idle 31-qubit complex128 state); LIFO per
+    key; emptied when a new state does not fit in device memory."""
 
-    def __init__(self, cap_bytes: int = 8 << 30, per_key: int = 4):
+    def __init__(self, cap_bytes: int = 32 << 30, per_key: int = 4):
         import threading
 
         self.cap = cap_bytes
@@ -461,7 +463,13 @@ class _StatePool:
             if lst:
                 self.bytes -= self._size(n, key[1])
                 return lst.pop()
-        return DeviceState(n, precision, device)
+        try:
+            return DeviceState(n, precision, device)
+        except (BackendError, QubitCapError):
+            if not self.bytes:
+                raise
+            self.clear()  # idle states held device memory the new one needs
+            return DeviceState(n, precision, device)
 
     def release(self, st: DeviceState) -> None:
         key = (st.n, st.precision, st.device)
@@ -475,11 +483,11 @@ class _StatePool:
         st.close()
 
     def clear(self) -> None:
-        for lst in self.idle.values():
+        with self.lock:
+            idle, self.idle, self.bytes = self.idle, {}, 0
+        for lst in idle.values():
             for st in lst:
                 st.close()
-        self.idle.clear()
-        self.bytes = 0
 
 
 _pool = _StatePool()
@@ -784,11 +792,22 @@ def _run_replay(c, shots, seed, workers, precision, device, meta) -> dict:
 
 
 class _Cached:
-    __slots__ = ("device", "host")
+    """A cached post-unitary state; when its Circuit is collected the device
+    state goes back to the pool (a 16 GiB cudaMalloc + cudaFree per new
+    circuit cost more than the QFT-30 program itself)."""
+    __slots__ = ("device", "host", "__weakref__")
 
     def __init__(self, device: DeviceState):
         self.device = device
         self.host = None
+
+    def __del__(self):
+        d, self.device = getattr(self, "device", None), None
+        if d is not None:
+            try:
+                _pool.release(d)
+            except Exception:
+                pass
 
     def serves(self, precision: str, device: int) -> bool:
         return self.device.precision == _norm_prec(precision) and self.device.device == device
@@ -811,7 +830,7 @@ def _cached_state(c, qubit_cap: int, precision: str = "c128", device: int = 0) -
         raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
     if not terminal_measurement_only(c):
         raise BackendError("expectation values need a circuit without mid-circuit collapse")
-    state = DeviceState(c.n_qubits, precision, device)
+    state = _pool.acquire(c.n_qubits, precision, device).zero()
     state.apply_instructions(c.instructions)
     entry = _Cached(state)
     _state_cache[c] = entry
@@ -857,7 +876,7 @@ def expectations(c, z_sets, qubit_cap: int = DEFAULT_QUBIT_CAP) -> np.ndarray:
             raise QubitCapError(f"{c.n_qubits} qubits exceeds the configured cap {qubit_cap}")
         if not terminal_measurement_only(c):
             raise BackendError("expectation values need a circuit without mid-circuit collapse")
-        state = DeviceState(c.n_qubits, "c128")
+        state = _pool.acquire(c.n_qubits, "c128", 0).zero()
         qs = [m.bit_length() - 1 for m in masks]
         vals = state.apply_gates_z(gate_array(c.instructions), qs)
         _state_cache[c] = _Cached(state)
