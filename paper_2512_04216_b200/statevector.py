@@ -450,7 +450,9 @@ class _StatePool:
         self.per_key = per_key
         self.idle: dict = {}
         self.bytes = 0
-        self.lock = threading.Lock()
+        # re-entrant: a garbage collection inside a locked section may run a
+        # _Cached finaliser, which releases its state into this pool
+        self.lock = threading.RLock()
 
     @staticmethod
     def _size(n, precision):
