@@ -588,7 +588,7 @@ static Program cached_program(int n, const svb_gate* g, int ng, const SchedOptio
   const uint64_t salt = (uint64_t)n | ((uint64_t)sizeof(R) << 8) | ((uint64_t)opt.rb << 16) |
                         ((uint64_t)opt.m << 24) | ((uint64_t)opt.relabel_swaps << 32) |
                         ((uint64_t)opt.round_search << 33) | ((uint64_t)opt.zero_start << 34) |
-                        ((uint64_t)opt.initial_perm << 35);
+                        ((uint64_t)opt.initial_perm << 35) | ((uint64_t)opt.structural << 36);
   const ProgKey key = prog_key(g, sizeof(svb_gate) * (size_t)ng, salt);
   {
     std::lock_guard<std::mutex> lk(g_prog_mu);

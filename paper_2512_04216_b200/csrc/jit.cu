@@ -23,6 +23,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <chrono>
 #include <mutex>
 #include <shared_mutex>
 #include <sstream>
@@ -251,6 +252,14 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
       cone = cone && is1(tc[k].d[e]);
       creal = creal && tc[k].d[e].y == 0;
     }
+  if (!imm) {
+    // structure-only code: a factor is skipped only when no term contributes
+    // to it (a value that happens to be 1 -- e.g. the deferred scale of a
+    // pivot whose choice flips with the angle -- must not change the source)
+    for (int i = 0; i < RB; ++i) d0one[i] = d1one[i] = h.nUR[i] == 0;
+    for (int k = 0; k < h.nTR; ++k) d0one[tr[k].ra] = d1one[tr[k].ra] = false;
+    cone = h.nUC == 0 && h.nUTg == 0 && h.nTC == 0;
+  }
   o << "    {\n";
   const std::string us = "c.uni + " + std::to_string(h.slot * kUniStride);
   const bool has_uc = h.slot >= 0 && (h.nUC > 0 || h.nUTg > 0);
@@ -534,9 +543,12 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
             o << "    " << guard << "svb::u1_piv<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk(coef[0])
               << ", " << rk(coef[1]) << ">(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
           } else {
-            o << "    " << guard << "svb::u1_piv_p<R, RB, " << h.a << ", " << (h.n & 3) << ", "
-              << (h.kind == OP_U1PR ? "true" : "false") << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + "
-              << pay << "));\n";
+            // the pivot choice depends on the angles (the larger entry of each
+            // row): read from the op header at run time, so every angle set
+            // of this structure shares the kernel
+            o << "    " << guard << "svb::u1_piv_pc<R, RB, " << h.a << ", " << (h.kind == OP_U1PR ? "true" : "false")
+              << ">(reinterpret_cast<const int32_t*>(c.ops + " << (pay - (uint32_t)sizeof(OpHdr))
+              << ")[3] & 3, a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "));\n";
           }
           break;
         }
@@ -617,7 +629,7 @@ bool jit_available() {
 // Programs on at least this many qubits get coefficients as immediates (a
 // one-off compile is negligible next to their passes); smaller ones get
 // structure-only code that circuits differing only in angles share.
-constexpr int kImmMinQubits = 28;
+constexpr int kImmMinQubits = kJitImmMinQubits;
 
 // `nslots`: per-thread prologue slots (shared memory, [slot][thread]);
 // `imm`: coefficients are immediates, so only the uniform DIAG payloads are
@@ -799,10 +811,15 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
   static Driver dr;
   if (!dr.ok || prog.passes.empty()) return false;
   const int RB = prog.passes[0].rb;
+  static const bool jprof = std::getenv("SVB_JIT_PROFILE") != nullptr;
+  const auto jt0 = std::chrono::steady_clock::now();
+  auto jms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - jt0).count(); };
+  double j_evict = 0, j_gen = 0, j_lookup = 0;
   int dev = 0;
   SVB_CUDA(cudaGetDevice(&dev));
   evict_lru(dr, dev);
   std::shared_lock<std::shared_mutex> launch_lk(g_launch_mu);
+  if (jprof) j_evict = jms();
   const size_t np = prog.passes.size();
   std::vector<std::string> srcs(np), keys(np);
   std::vector<CUfunction> fns(np, nullptr);
@@ -846,6 +863,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
     }
+    if (jprof) j_gen = jms();
     std::lock_guard<std::mutex> lk(g_mu);
     for (size_t p = 0; p < np; ++p) {
       auto it = g_cache.find(keys[p]);
@@ -857,6 +875,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       }
     }
   }
+  if (jprof) j_lookup = jms();
   // Asynchronous mode (the batch executor): kernels not compiled yet are
   // compiled by background threads while this program runs on the
   // interpreter; later programs of the same structure pick them up.
@@ -1058,6 +1077,9 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     stats->passes += 1;
     stats->launches += 1;
   }
+  if (jprof)
+    std::fprintf(stderr, "[svb] jit_launch: evict+lock %.3f gen %.3f lookup %.3f total %.3f ms (hit %d)\n", j_evict, j_gen,
+                 j_lookup, jms(), hit ? 1 : 0);
   return true;
 }
 

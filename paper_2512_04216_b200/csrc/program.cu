@@ -655,6 +655,11 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
       pd.ops_begin = (uint32_t)prog.ops.size();
       std::vector<cd> dl(n, cd(1.0, 0.0));
       cd K(1.0, 0.0);
+      // structural mode: which pending diagonals were ever set (flushed even
+      // when they come out as 1) and pivots since the last rescale
+      std::vector<char> dtouch(n, 0);
+      bool ktouch = false;
+      int npiv = 0;
       int last_u1 = -1;
       for (auto& rd : rounds)
         for (int idx : rd.second) {
@@ -787,6 +792,8 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
                 // 1q diagonal on a tile qubit: fold into the pending diagonal
                 K *= d.c[0];
                 dl[d.q[0]] *= d.c[1] / d.c[0];
+                dtouch[d.q[0]] = 1;
+                ktouch = true;
                 continue;
               }
               terms.push_back(DT{d.q[0], d.q[1], {d.c[0], d.c[1], d.c[2], d.c[3]}});
@@ -820,12 +827,16 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
             if (zero(M[1]) && zero(M[2])) {  // diagonal: defer entirely
               K *= M[0];
               dl[q] = snap(M[3] / M[0]);
+              dtouch[q] = 1;
+              ktouch = true;
               ++i;
               continue;
             }
             if (zero(M[0]) && zero(M[3])) {  // anti-diagonal: plain swap + deferred diag(m01, m10)
               K *= M[1];
               dl[q] = snap(M[2] / M[1]);
+              dtouch[q] = 1;
+              ktouch = true;
               const cd sw[4] = {cd(0.0, 0.0), cd(1.0, 0.0), cd(1.0, 0.0), cd(0.0, 0.0)};
               encode_u1(OP_U1ANTI, b, sw, 0, 0, 0, 0);
               ++i;
@@ -834,11 +845,15 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
             // the stored amplitudes carry 1/K: once |K| drifts far from 1 (long
             // passes of pivoted ops), emit this op in full to rescale (keeps
             // complex64 values far from overflow / underflow)
+            // (structural mode: every 8 / 64 pivots; a pivot scales by >= 2^-8.5,
+            // so |K| stays within 2^68 (c64) / 2^544 (c128) of 1)
             const double klog = std::fabs(std::log2(std::abs(K)));
-            const bool rescale = klog > (sizeof(R) == 4 ? 20.0 : 100.0);
+            const bool rescale = opt.structural ? npiv >= (sizeof(R) == 4 ? 8 : 64)
+                                                : klog > (sizeof(R) == 4 ? 20.0 : 100.0);
             if (list[i] == last_u1 || rescale) {  // absorbs K; emitted in full
               for (auto& z : M) z = snap(z) * K;  // snap is absolute: before scaling
               K = cd(1.0, 0.0);
+              npiv = 0;
               encode_u1(u1_type(M), b, M, 0, 0, 0, 0);
               ++i;
               continue;
@@ -856,6 +871,9 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
             const cd r0 = snap(M[1 - pc0] / p0), r1 = snap(M[2 + (1 - pc1)] / p1);
             K *= p0;
             dl[q] = close(p1, p0) ? cd(1.0, 0.0) : snap(p1 / p0);
+            dtouch[q] = 1;
+            ktouch = true;
+            ++npiv;
             const bool real = r0.imag() == 0 && r1.imag() == 0;
             size_t at = enc.begin(real ? OP_U1PR : OP_U1P, b, 0, pc0 | (pc1 << 1), 0, 0, 0, 0);
             enc.put(cvt<R>(r0));
@@ -885,10 +903,11 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
           std::vector<DT> terms;
           for (int q = 0; q < n; ++q) {
             const cd d1 = snap(dl[q]);
-            if (!(d1.real() == 1.0 && d1.imag() == 0.0)) terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
+            if (!(d1.real() == 1.0 && d1.imag() == 0.0) || (opt.structural && dtouch[q]))
+              terms.push_back(DT{q, -1, {cd(1.0, 0.0), d1, cd(1.0, 0.0), d1}});
           }
           if (std::abs(K - cd(1.0, 0.0)) <= 0x1p-50) K = cd(1.0, 0.0);  // not snap(): |K| may be tiny
-          if (!(K.real() == 1.0 && K.imag() == 0.0)) terms.push_back(DT{-1, -1, {K, K, K, K}});
+          if (!(K.real() == 1.0 && K.imag() == 0.0) || (opt.structural && ktouch)) terms.push_back(DT{-1, -1, {K, K, K, K}});
           if (!terms.empty()) encode_diag(terms);
         }
         rd.op_end = (uint32_t)prog.ops.size();
@@ -1101,10 +1120,10 @@ template void emulate_program<float>(cplx<float>*, int, const Program&);
 template void emulate_program<double>(cplx<double>*, int, const Program&);
 
 SchedOptions default_options(int precision, int n, bool jit) {
-  (void)n;
   SchedOptions o;
   if (precision == SVB_C128) { o.rb = jit ? kJitRegBits<double> : kRegBits<double>; o.m = 12; }
   else { o.rb = jit ? kJitRegBits<float> : kRegBits<float>; o.m = pass_tile_m(4, o.rb); }
+  o.structural = jit && n < kJitImmMinQubits;
   return o;
 }
 

@@ -61,7 +61,14 @@ struct SchedOptions {
   bool zero_start = false;   // input is |0...0>: choose the initial qubit layout so no final permutation is needed
   bool initial_perm = true;  // written input + swaps: may permute the input first (see build_program)
   bool round_search = true;  // reorder ops across rounds (else program order)
+  // structure-only NVRTC code (n < kJitImmMinQubits): the op stream's shape
+  // must not depend on the angles, so that circuits differing only in angles
+  // share kernels -- deferred pivot diagonals are flushed for every qubit that
+  // had one (even when the factor comes out as exactly 1) and the rescale of
+  // the carried scalar happens every few pivots instead of when |K| drifts
+  bool structural = false;
 };
+constexpr int kJitImmMinQubits = 28;  // from here the NVRTC passes take coefficients as immediates
 
 // jit: the options of a program the NVRTC passes will run (kJitRegBits)
 SchedOptions default_options(int precision, int n, bool jit = false);

@@ -398,3 +398,26 @@ def test_jit_sources_compile(which):
         pytest.skip("NVRTC not available")
     assert rc == 0, buf.value.decode(errors="replace")[:2000]
     assert cb.value > 0
+
+
+def test_structure_only_jit_sources_do_not_depend_on_angles(tmp_path, monkeypatch):
+    """Below 28 qubits the NVRTC passes load their coefficients, so circuits
+    that differ only in angles must generate the same kernel sources (a VQE /
+    QAOA loop compiles once): the pivot choice is read at run time and the
+    deferred diagonals are flushed by structure, not by value."""
+    import ctypes as _ct
+
+    monkeypatch.setenv("SVB_JIT_NOCOMPILE", "1")
+    seen = {}
+    circs = [c for c in suite.batch_workload(13 * 40, base=10000) if c.n_qubits == 24]
+    for i, c in enumerate(circs):
+        path = tmp_path / f"{i}.cu"
+        monkeypatch.setenv("SVB_JIT_DUMP", str(path))
+        g = sv.gate_array(c.instructions)
+        cb = _ct.c_int64()
+        buf = _ct.create_string_buffer(1 << 12)
+        rc = _lib.lib().svb_jit_check(24, 1 | 0x100, g.ctypes.data_as(_ct.c_void_p), int(g.size), _ct.byref(cb), buf, 1 << 12)
+        assert rc == 0, buf.value
+        seen.setdefault(c.name.rsplit("_", 1)[0] + c.name.rsplit("_", 1)[1].split("x")[1], set()).add(path.read_text())
+    # one source per family: qaoa (1 and 2 layers) and the ry ansatz
+    assert len(seen) == 3 and all(len(v) == 1 for v in seen.values()), {k: len(v) for k, v in seen.items()}
