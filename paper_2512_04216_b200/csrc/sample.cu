@@ -1,3 +1,4 @@
+#include <climits>
 // Terminal-measurement sampling on the device.
 //
 // Two samplers share one uniform stream — numpy's PCG64 as seeded by
@@ -345,6 +346,49 @@ static void seq_cumsum(const double* in, double* out, uint64_t n, cudaStream_t s
   SVB_CHECK_LAUNCH();
 }
 
+// Exponent of the lowest set bit of each nonnegative finite x (x = k 2^e with
+// k odd), min-reduced into *emin.
+__global__ void k_lsb_exp_min(const double* __restrict__ in, uint64_t n, int* __restrict__ emin) {
+  int e = INT_MAX;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(in[i]);
+    const int ex = (int)((b >> 52) & 0x7ff);
+    unsigned long long mant = b & ((1ull << 52) - 1);
+    if (ex == 0 && mant == 0) continue;  // zero
+    if (ex != 0) mant |= 1ull << 52;
+    const int lsb = __ffsll((long long)mant) - 1 + (ex == 0 ? 1 : ex) - 1075;
+    e = min(e, lsb);
+  }
+  for (int o = 16; o > 0; o >>= 1) e = min(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if ((threadIdx.x & 31) == 0 && e != INT_MAX) atomicMin(emin, e);
+}
+
+// np.cumsum (a left-to-right chain of roundings) without the chain when it
+// provably never rounds: every element is a multiple of 2^e and the total
+// stays below 2^(52 + e), so every partial sum in any order is exact and the
+// parallel scan gives the sequential result bit for bit (GHZ / uniform /
+// basis-state distributions: deficits 1.0, capacities 2^k - 1).  Otherwise
+// (and for short inputs) the sequential chain runs.
+static void cumsum_exact(const double* in, double* out, uint64_t n, cudaStream_t st) {
+  if (n < 8192) {
+    seq_cumsum(in, out, n, st);
+    return;
+  }
+  DevBuf em(sizeof(int), st);
+  const int big = INT_MAX;
+  SVB_CUDA(cudaMemcpyAsync(em.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  k_lsb_exp_min<<<grid_for(n, 256), 256, 0, st>>>(in, n, em.as<int>());
+  SVB_CHECK_LAUNCH();
+  device_scan<double>(in, out, n, false, st);
+  const int e = d2h_scalar(em.as<int>(), st);
+  const double total = d2h_scalar(out + (n - 1), st);
+  const bool exact = e != INT_MAX && total < std::ldexp(1.0, 52 + e);
+  static const bool trace = std::getenv("SVB_TRACE") != nullptr;
+  if (trace) std::fprintf(stderr, "[svb] cumsum n=%llu %s\n", (unsigned long long)n, exact ? "parallel (exact)" : "sequential");
+  if (exact) return;
+  seq_cumsum(in, out, n, st);
+}
+
 // ------------------------------------------------------------- alias build
 __global__ void k_alias_init(const double* __restrict__ probs, uint64_t m, double factor,
                              double* __restrict__ scaled, double* __restrict__ prob_row,
@@ -450,9 +494,40 @@ __global__ void __launch_bounds__(256) k_absorb_long(const int64_t* __restrict__
                                                      const double* __restrict__ deficit, double* __restrict__ rem,
                                                      const uint64_t* __restrict__ long_runs) {
   __shared__ double tot;
+  __shared__ double wsum[8];
+  __shared__ int wexp[8];
   const uint64_t r = long_runs[blockIdx.x];
   const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
-  seq_block(deficit + b, e - b, nullptr, &tot);
+  // the in-order sum never rounds when every term is a multiple of 2^lsb and
+  // the total stays below 2^(52 + lsb) (see cumsum_exact): then any order
+  // gives it, so the block reduces in parallel; else the sequential chain
+  double part = 0.0;
+  int lsb = INT_MAX;
+  for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    const double x = deficit[i];
+    part += x;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & ((1ull << 52) - 1);
+    if (ex == 0 && mant == 0) continue;
+    if (ex != 0) mant |= 1ull << 52;
+    lsb = min(lsb, __ffsll((long long)mant) - 1 + (ex == 0 ? 1 : ex) - 1075);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    part += __shfl_xor_sync(0xffffffffu, part, o);
+    lsb = min(lsb, __shfl_xor_sync(0xffffffffu, lsb, o));
+  }
+  if ((threadIdx.x & 31) == 0) { wsum[threadIdx.x >> 5] = part; wexp[threadIdx.x >> 5] = lsb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    int l = INT_MAX;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += wsum[w]; l = min(l, wexp[w]); }
+    wexp[0] = (l == INT_MAX || t < ldexp(1.0, 52 + l)) ? 1 : 0;
+    tot = t;
+  }
+  __syncthreads();
+  if (!wexp[0]) seq_block(deficit + b, e - b, nullptr, &tot);
   __syncthreads();
   if (threadIdx.x == 0) {
     const int64_t o = owner[b];
@@ -529,8 +604,8 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     k_deficit<<<grid_for(ns, B), B, 0, st>>>(scaled.as<double>(), S, ns, deficit.as<double>());
     k_capacity<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, cap.as<double>());
     SVB_CHECK_LAUNCH();
-    seq_cumsum(deficit.as<double>(), dcum.as<double>(), ns, st);
-    seq_cumsum(cap.as<double>(), ccum.as<double>(), nl, st);
+    cumsum_exact(deficit.as<double>(), dcum.as<double>(), ns, st);
+    cumsum_exact(cap.as<double>(), ccum.as<double>(), nl, st);
     k_owner<<<grid_for(ns, B), B, 0, st>>>(dcum.as<double>(), ns, ccum.as<double>(), nl, S, L,
                                            scaled.as<double>(), owner.as<int64_t>(), d_prob_row,
                                            d_alias_row);

@@ -197,6 +197,33 @@ def test_alias_tables_bit_exact_vs_reference_golden():
         np.testing.assert_array_equal(al, a[f"a{i}_alias"], err_msg=str(i))
 
 
+def test_alias_tables_bit_exact_large_exact_and_rounding_cumsums():
+    """Tables of >= 8192 outcomes against the oracle's restatement of
+    AliasTable.from_probs: distributions whose deficit / capacity prefix sums
+    never round take the parallel scan (uniform over a subset, GHZ-like,
+    dyadic), the others the sequential chain (random); both bit-exact."""
+    rng = np.random.default_rng(11)
+    cases = []
+    for m, k in ((1 << 14, 3), (1 << 16, 1 << 9), (1 << 15, 1 << 15)):
+        p = np.zeros(m)
+        p[rng.choice(m, size=k, replace=False)] = 1.0 / k
+        cases.append(p)
+    d = rng.integers(0, 8, size=1 << 14).astype(float)
+    cases.append(d / d.sum() if d.sum() else d)          # dyadic weights (exact)
+    r = rng.random(1 << 15) ** 3
+    cases.append(r / r.sum())                              # random (rounding chain)
+    L = _lib.lib()
+    for i, p in enumerate(cases):
+        p = np.ascontiguousarray(p)
+        pr = np.empty_like(p)
+        al = np.empty(p.size, dtype=np.int64)
+        _lib.check(L.svb_alias_table(0, _lib.ptr(p, _lib.c_double), p.size, _lib.ptr(pr, _lib.c_double),
+                                     _lib.ptr(al, _lib.c_int64)))
+        want_p, want_a = orc.alias_table(p)
+        np.testing.assert_array_equal(pr, want_p, err_msg=str(i))
+        np.testing.assert_array_equal(al, want_a, err_msg=str(i))
+
+
 def test_alias_table_rejects_bad_vectors():
     L = _lib.lib()
     for p in (np.array([0.5, 0.6]), np.array([-0.1, 1.1])):
