@@ -416,14 +416,18 @@ def run_sharded(args, rank: int, world: int, dist):
 
     st = ShardedState(n, PRECISION, device=device, backend="device")
 
+    zq = list(range(n))
+
     def step():
         st.reset()
-        st.apply(c.instructions)
-        z = st.expectations([(q,) for q in range(n)])
+        z = st.apply(c.instructions, z_qubits=zq)  # <Z_i> summed by the last local batch's fused pass
         return z, st.swaps, st.bytes_sent
 
     for _ in range(max(args.warmup, 1)):
         step()
+    local = getattr(st.shard, "state", None)  # this rank's DeviceState (device backend)
+    if local is not None:
+        local.profile(True)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -437,6 +441,19 @@ def run_sharded(args, rank: int, world: int, dist):
         e1.synchronize()
         wall_ms = (time.perf_counter() - w0) * 1e3 / args.steps
     total_ms = e0.elapsed_time(e1)
+    roof = None
+    if local is not None:
+        # this rank's fused passes over the timed steps (CUDA events on the
+        # shard's stream): HBM bytes they move / their time, against the peak
+        pr = local.profile_read()
+        local.profile(False)
+        peak, peak_kind = hbm_peak()
+        if pr["pass_ms"] > 0:
+            ach = pr["pass_bytes"] / (pr["pass_ms"] / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                    "kernel": "svb_jit fused passes of the local shard (all passes of a step, rank 0)",
+                    "peak_kind": peak_kind, "bytes_per_step": pr["pass_bytes"] / args.steps,
+                    "pass_ms_per_step": pr["pass_ms"] / args.steps, "launches_per_step": pr["pass_launches"] / args.steps}
     barrier()
     if dist is not None:
         t = torch.tensor([total_ms, wall_ms], dtype=torch.float64, device="cuda")
@@ -457,6 +474,9 @@ def run_sharded(args, rank: int, world: int, dist):
                 "note": "wall clock per step, max over ranks: gate encoding + upload, passes, swaps, <Z_i> to the host"},
         "clocks": clk.summary(),
     }
+    if roof is not None:
+        line["roofline"] = roof
+        line["gpu_launches"] = int(roof["launches_per_step"] * args.steps)  # fused passes (exchange copies not counted)
     if rank == 0:
         print(json.dumps(line), flush=True)
 

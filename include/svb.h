@@ -137,7 +137,9 @@ int svb_apply(svb_handle h, const svb_gate* gates, int n_gates);
  * state (single-qubit Z; statevector.py:277-292 per qubit, after
  * statevector.py:116-122 for every gate).  The sums are accumulated by the
  * program's last fused pass as it stores the state, so no separate read pass
- * is needed; unfused programs fall back to one reduction pass.  nz may be 0. */
+ * is needed; unfused programs fall back to one reduction pass.  nz may be 0.
+ * z_qubits[j] = -1 returns sum |a|^2 (the norm: a shard's share of the <Z> of
+ * a qubit held in the rank bits). */
 int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t* z_qubits, int nz,
                 double* out);
 

@@ -379,7 +379,8 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
     check_handle_nomat(h);
     validate_gates(h, gates, n_gates);
     require(nz >= 0, SVB_E_ARG, "bad qubit count");
-    for (int j = 0; j < nz; ++j) require(z_qubits[j] >= 0 && z_qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
+    // qubit -1: sum p (the norm; a shard's share of a global qubit's <Z>)
+    for (int j = 0; j < nz; ++j) require(z_qubits[j] >= -1 && z_qubits[j] < h->n, SVB_E_ARG, "qubit out of range");
     h->stats = ProgramStats{};
     h->stats.prof = &h->prof;
     const size_t zacc = std::max({zacc_doubles(kPassThreads<float, 4>, 4), zacc_doubles(kPassThreads<float, 5>, 5),
@@ -411,11 +412,11 @@ int svb_apply_z(svb_handle h, const svb_gate* gates, int n_gates, const int32_t*
         if (z.logical[k] >= 0) { by_q[z.logical[k]] = vals[k]; seen[z.logical[k]] = 1; }
       // a qubit outside the passes' support (zero_start) is |0> in every
       // amplitude that is not zero: <Z> = sum p
-      for (int j = 0; j < nz; ++j) out[j] = seen[z_qubits[j]] ? by_q[z_qubits[j]] : vals.back();
+      for (int j = 0; j < nz; ++j) out[j] = (z_qubits[j] >= 0 && seen[z_qubits[j]]) ? by_q[z_qubits[j]] : vals.back();
     } else {
       materialize(h);
       std::vector<uint64_t> masks(nz);
-      for (int j = 0; j < nz; ++j) masks[j] = 1ull << z_qubits[j];
+      for (int j = 0; j < nz; ++j) masks[j] = z_qubits[j] >= 0 ? 1ull << z_qubits[j] : 0ull;
       double* d_out = z.d_out;
       double* d_ws = z.d_out + kZaccRows + (size_t)kZaccRows * 32;
       if (h->prec == SVB_C128) launch_expect_z<double>(h->amps, h->n, masks.data(), nz, d_out, d_ws, h->st);

@@ -134,6 +134,11 @@ class _DeviceShard:
     def expect(self, masks) -> np.ndarray:
         return self.state.expect_z(masks)
 
+    def apply_z(self, gates: np.ndarray, qubits) -> np.ndarray:
+        """Apply, with sum p (-1)^bit for each local qubit (-1: sum p) taken by
+        the program's last pass as it stores the shard."""
+        return self.state.apply_gates_z(gates, qubits)
+
     def to_numpy(self) -> np.ndarray:
         return self.state.to_numpy()
 
@@ -285,11 +290,18 @@ class ShardedState:
         self.remap([(G, L)])
 
     # ----------------------------------------------------------------- gates
-    def apply(self, instructions) -> None:
+    def apply(self, instructions, z_qubits=None):
         """Apply a gate list: local gates in fused batches, free relabels of
         untouched qubits, grouped remaps when a gate acts non-diagonally on a
         global qubit.  Plans depend only on the gates, the layout, the set of
-        touched qubits and the rank: computed once and replayed."""
+        touched qubits and the rank: computed once and replayed.
+
+        z_qubits (optional): also return <Z_q> of those logical qubits after
+        the gates.  When the plan ends with a batch of local gates, the local
+        sums come from that batch's last fused pass (no separate read pass):
+        a local qubit contributes sum p (-1)^bit, a global one +-sum p by this
+        rank's bit; one all-reduce adds the shards.  Otherwise one reduction
+        pass (expectations)."""
         insts = [i for i in instructions if i.kind in UNITARY_GATES]
         key = (tuple((i.kind, tuple(i.qubits), tuple(i.params)) for i in insts), tuple(self.pos),
                tuple(self.touched))
@@ -300,9 +312,21 @@ class ShardedState:
                 self._plans.pop(next(iter(self._plans)))
             self._plans[key] = entry
         plan, touched_after = entry
-        for act in plan:
+        fuse_z = (z_qubits is not None and bool(plan) and plan[-1][0] == "gates"
+                  and hasattr(self.shard, "apply_z"))
+        zloc = None
+        for ai, act in enumerate(plan):
             if act[0] == "gates":
-                if not self.zero_shard:  # gates map the zero vector to itself
+                if self.zero_shard:  # gates map the zero vector to itself
+                    continue
+                if fuse_z and ai == len(plan) - 1:
+                    # the layout no longer changes: local qubits by physical bit, -1 = the norm
+                    phys = [self.pos[q] for q in z_qubits]
+                    req = sorted({p for p in phys if p < self.nl}) + [-1]
+                    got = dict(zip(req, self.shard.apply_z(act[1], req)))
+                    zloc = np.array([got[p] if p < self.nl else (-got[-1] if self._rank_bit(p) else got[-1])
+                                     for p in phys])
+                else:
                     self.shard.apply(act[1])
             elif act[0] == "relabel":
                 inv = self._inv()
@@ -314,6 +338,13 @@ class ShardedState:
             else:
                 self.remap(act[1])
         self.touched = list(touched_after)
+        if z_qubits is None:
+            return None
+        if not fuse_z:
+            return self.expectations([(q,) for q in z_qubits])
+        if zloc is None:  # a shard of zeros
+            zloc = np.zeros(len(z_qubits))
+        return self._allreduce(zloc)
 
     def _plan(self, insts) -> list:
         """Actions [("gates", records) | ("relabel", pairs) | ("remap", pairs)]

@@ -353,7 +353,8 @@ class DeviceState:
 
     def apply_gates_z(self, gates: np.ndarray, z_qubits) -> np.ndarray:
         """Apply a gate program and return <Z_q> for each q in z_qubits, summed by
-        the program's last fused pass while it stores the state (svb_apply_z)."""
+        the program's last fused pass while it stores the state (svb_apply_z);
+        q = -1 gives sum |a|^2."""
         gates = np.ascontiguousarray(gates, dtype=GATE_DTYPE)
         qs = np.ascontiguousarray(z_qubits, dtype=np.int32).reshape(-1)
         out = np.empty(qs.size, dtype=np.float64)

@@ -68,6 +68,11 @@ class EmulatedShard:
             out.append(float(np.sum(p * (1.0 - 2.0 * par))))
         return np.array(out)
 
+    def apply_z(self, gates: np.ndarray, qubits) -> np.ndarray:
+        """apply + sum p (-1)^bit per local qubit (-1: sum p), as the device's fused last pass."""
+        self.apply(gates)
+        return self.expect([(1 << q) if q >= 0 else 0 for q in qubits])
+
     def to_numpy(self) -> np.ndarray:
         return self.amps.copy()
 

@@ -59,11 +59,15 @@ def _worker(rank, world, port, out_dir, case):
         z = st.expectations([(q,) for q in range(n)] + [(0, n - 1), tuple(range(n))])
         counts = st.sample([(q, q) for q in range(n)], case["shots"], case["seed"] + 1)
         amps = st.gather()
+        # the same circuit with <Z_q> taken by the last local batch's fused pass
+        st2 = ShardedState(n, case["precision"], backend=backend, staging="host",
+                           chunk_bytes=case.get("chunk_bytes", 1 << 29))
+        zf = st2.apply(c.instructions, z_qubits=list(range(n)))
         if rank == 0:
             np.save(os.path.join(out_dir, "amps.npy"), amps)
             with open(os.path.join(out_dir, "res.json"), "w") as fh:
-                json.dump({"z": list(z), "counts": counts, "swaps": st.swaps, "remaps": remaps, "sent": sent,
-                           "relabels": relabels, "writes0": writes0}, fh)
+                json.dump({"z": list(z), "zf": [float(x) for x in zf], "counts": counts, "swaps": st.swaps,
+                           "remaps": remaps, "sent": sent, "relabels": relabels, "writes0": writes0}, fh)
     finally:
         dist.destroy_process_group()
 
@@ -121,6 +125,7 @@ def test_sharded_matches_oracle(world, case):
     assert np.linalg.norm(amps - psi) / np.linalg.norm(psi) < tol
     np.testing.assert_allclose(res["z"], z, atol=tol * 10)
     n = case["n"]
+    np.testing.assert_allclose(res["zf"], z[:n], atol=tol * 10)  # fused <Z_q> (ShardedState.apply(z_qubits=))
     probs = np.abs(psi) ** 2
     expected = {format(i, f"0{n}b"): float(p) for i, p in enumerate(probs) if p > 1e-14}
     assert sum(res["counts"].values()) == case["shots"]
@@ -160,6 +165,7 @@ def test_sharded_device_shards_host_staged(world, case):
     assert np.linalg.norm(amps - psi) / np.linalg.norm(psi) < tol
     np.testing.assert_allclose(res["z"], z, atol=tol * 10)
     n = case["n"]
+    np.testing.assert_allclose(res["zf"], z[:n], atol=tol * 10)  # fused <Z_q> (ShardedState.apply(z_qubits=))
     probs = np.abs(psi) ** 2
     expected = {format(i, f"0{n}b"): float(p) for i, p in enumerate(probs) if p > 1e-14}
     assert chisquare_pvalue(res["counts"], expected, case["shots"]) > 1e-3
