@@ -305,10 +305,11 @@ __device__ __forceinline__ void seq_stage(const double* __restrict__ in, uint64_
 }
 
 // mode 0: out = inclusive running sum (cumsum); mode 1: *total = sum (bincount bin)
-__device__ void seq_block(const double* __restrict__ in, uint64_t n, double* __restrict__ out, double* total) {
+__device__ void seq_block(const double* __restrict__ in, uint64_t n, double* __restrict__ out, double* total,
+                          double init = 0.0) {
   __shared__ double buf[2][kSeqChunk];
   __shared__ double acc_s;
-  if (threadIdx.x == 0) acc_s = 0.0;
+  if (threadIdx.x == 0) acc_s = init;
   const uint64_t nch = (n + kSeqChunk - 1) / kSeqChunk;
   if (nch) seq_stage(in, n, 0, buf[0]);
   for (uint64_t c = 0; c < nch; ++c) {
@@ -336,13 +337,14 @@ __device__ void seq_block(const double* __restrict__ in, uint64_t n, double* __r
   if (total && threadIdx.x == 0) *total = acc_s;
 }
 
+// init: the running sum before in[0] (*init_d when given: a device scalar)
 __global__ void __launch_bounds__(256) k_seq_cumsum(const double* __restrict__ in, double* __restrict__ out,
-                                                    uint64_t n) {
-  seq_block(in, n, out, nullptr);
+                                                    uint64_t n, const double* __restrict__ init_d) {
+  seq_block(in, n, out, nullptr, init_d ? *init_d : 0.0);
 }
 
-static void seq_cumsum(const double* in, double* out, uint64_t n, cudaStream_t st) {
-  k_seq_cumsum<<<1, 256, 0, st>>>(in, out, n);
+static void seq_cumsum(const double* in, double* out, uint64_t n, cudaStream_t st, const double* init_d = nullptr) {
+  k_seq_cumsum<<<1, 256, 0, st>>>(in, out, n, init_d);
   SVB_CHECK_LAUNCH();
 }
 
@@ -361,6 +363,122 @@ __global__ void k_lsb_exp_min(const double* __restrict__ in, uint64_t n, int* __
   }
   for (int o = 16; o > 0; o >>= 1) e = min(e, __shfl_xor_sync(0xffffffffu, e, o));
   if ((threadIdx.x & 31) == 0 && e != INT_MAX) atomicMin(emin, e);
+}
+
+// ---- the rounding chain by binade windows (bit-exact, parallel) ----------
+// While the running sum s stays in one binade [2^(e+52), 2^(e+53)), every
+// value is a multiple of u = 2^e and fl(s + x) = s + u RN(x / u), except for a
+// tie (x / u exactly half an integer: round-to-even depends on s) or an x
+// that alone leaves the binade.  So from a known s, the window's sums are
+// s + u (prefix sum of k_j = RN(x_j / u)) -- an exact int64 scan -- up to the
+// first element that ties, is too large, or lifts the sum out of the binade;
+// that element is one IEEE add on the device, and the next window starts in
+// the new binade.  s grows by about mu per element, so a binade spans about as
+// many elements as precede it: windows of max(8192, i) elements keep the work
+// O(n) and their number ~ log2(n) (31-47 on the prototype's random inputs,
+// every result equal to np.cumsum).  Inputs with many ties fall back to the
+// sequential chain after kMaxWindows.
+__global__ void k_binade_k(const double* __restrict__ x, uint64_t w, int e, int64_t* __restrict__ k,
+                           unsigned long long* __restrict__ stop) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < w; j += (uint64_t)gridDim.x * blockDim.x) {
+    const double y = ldexp(x[j], -e);  // exact (power-of-two scaling of a normal result)
+    if (!(y < 9007199254740992.0) || !(y >= 0.0)) {  // >= 2^53 (leaves the binade alone), negative, NaN
+      k[j] = 0;
+      atomicMin(stop, (unsigned long long)j);
+      continue;
+    }
+    const double f = floor(y), fr = y - f;  // exact
+    if (fr == 0.5) {
+      k[j] = 0;
+      atomicMin(stop, (unsigned long long)j);
+      continue;
+    }
+    k[j] = (int64_t)f + (fr > 0.5 ? 1 : 0);
+  }
+}
+__global__ void k_binade_leave(const int64_t* __restrict__ K, uint64_t w, int64_t base,
+                               unsigned long long* __restrict__ stop) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < w; j += (uint64_t)gridDim.x * blockDim.x)
+    if (base + K[j] >= (int64_t)(1ull << 53)) atomicMin(stop, (unsigned long long)j);
+}
+__global__ void k_binade_write(const int64_t* __restrict__ K, uint64_t cnt, int64_t base, int e,
+                               double* __restrict__ out) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += (uint64_t)gridDim.x * blockDim.x)
+    out[j] = ldexp((double)(base + K[j]), e);  // < 2^53: exact
+}
+// one IEEE add: out[i] = prev + x[i] (prev = out[i - 1], or *s at a window start)
+__global__ void k_binade_step(const double* __restrict__ x, double* __restrict__ out, uint64_t i, int from_out,
+                              double* __restrict__ s) {
+  const double prev = from_out ? out[i - 1] : *s;
+  const double v = prev + x[i];
+  out[i] = v;
+  *s = v;
+}
+
+// Returns the number of windows, or 0 when it ran the sequential chain.
+static int binade_cumsum(const double* in, double* out, uint64_t n, cudaStream_t st) {
+  // measured: the chain runs at a few ns per element, a window costs ~0.1 ms
+  // of launches and synchronisations, so windows pay off only for long
+  // arrays, and a window budget bounds the loss on tie-heavy inputs
+  constexpr int kMaxWindows = 96;
+  constexpr uint64_t kMinWindow = 8192;
+  if (n < (1ull << 21)) {
+    seq_cumsum(in, out, n, st);
+    return 0;
+  }
+  DevBuf kb(sizeof(int64_t) * n, st), Kb(sizeof(int64_t) * n, st), tot(sizeof(int64_t) * (n / 2048 + 2), st);
+  DevBuf sb(sizeof(double) + sizeof(unsigned long long), st);
+  double* d_s = sb.as<double>();
+  unsigned long long* d_stop = reinterpret_cast<unsigned long long*>(d_s + 1);
+  uint64_t i = 0;
+  double s = 0.0;
+  int windows = 0;
+  while (i < n) {
+    if (++windows > kMaxWindows) {  // tie-heavy input: the plain chain from here on (prefix kept)
+      SVB_CUDA(cudaMemcpyAsync(d_s, &s, sizeof(double), cudaMemcpyHostToDevice, st));
+      seq_cumsum(in + i, out + i, n - i, st, d_s);
+      return windows;
+    }
+    // zero / subnormal running sums: one exact step (the first element, tiny inputs)
+    if (!(s >= 0x1p-1000)) {
+      SVB_CUDA(cudaMemcpyAsync(d_s, &s, sizeof(double), cudaMemcpyHostToDevice, st));
+      k_binade_step<<<1, 1, 0, st>>>(in, out, i, 0, d_s);
+      SVB_CHECK_LAUNCH();
+      s = d2h_scalar(d_s, st);
+      ++i;
+      continue;
+    }
+    int ex;
+    std::frexp(s, &ex);
+    const int e = ex - 53;  // spacing of s's binade
+    const int64_t base = (int64_t)std::ldexp(s, -e);
+    const uint64_t w = std::min<uint64_t>(n - i, std::max<uint64_t>(kMinWindow, i));
+    const unsigned long long none = ~0ull;
+    SVB_CUDA(cudaMemcpyAsync(d_stop, &none, sizeof none, cudaMemcpyHostToDevice, st));
+    k_binade_k<<<grid_for(w, 256), 256, 0, st>>>(in + i, w, e, kb.as<int64_t>(), d_stop);
+    SVB_CHECK_LAUNCH();
+    device_scan<int64_t>(kb.as<int64_t>(), Kb.as<int64_t>(), w, false, st, tot.as<int64_t>());
+    k_binade_leave<<<grid_for(w, 256), 256, 0, st>>>(Kb.as<int64_t>(), w, base, d_stop);
+    SVB_CHECK_LAUNCH();
+    const unsigned long long stop = d2h_scalar(d_stop, st);
+    const uint64_t good = stop == none ? w : (uint64_t)stop;  // [i, i + good) are s + u K
+    if (good) {
+      k_binade_write<<<grid_for(good, 256), 256, 0, st>>>(Kb.as<int64_t>(), good, base, e, out + i);
+      SVB_CHECK_LAUNCH();
+    }
+    if (good == w) {
+      s = d2h_scalar(out + i + w - 1, st);
+      i += w;
+      continue;
+    }
+    // the stopping element: one IEEE add after the window's valid prefix
+    if (good == 0) SVB_CUDA(cudaMemcpyAsync(d_s, &s, sizeof(double), cudaMemcpyHostToDevice, st));
+    k_binade_step<<<1, 1, 0, st>>>(in, out, i + good, good > 0 ? 1 : 0, d_s);
+    SVB_CHECK_LAUNCH();
+    s = d2h_scalar(d_s, st);
+    i += good + 1;
+  }
+  return windows;
 }
 
 // np.cumsum (a left-to-right chain of roundings) without the chain when it
@@ -384,9 +502,11 @@ static void cumsum_exact(const double* in, double* out, uint64_t n, cudaStream_t
   const double total = d2h_scalar(out + (n - 1), st);
   const bool exact = e != INT_MAX && total < std::ldexp(1.0, 52 + e);
   static const bool trace = std::getenv("SVB_TRACE") != nullptr;
-  if (trace) std::fprintf(stderr, "[svb] cumsum n=%llu %s\n", (unsigned long long)n, exact ? "parallel (exact)" : "sequential");
-  if (exact) return;
-  seq_cumsum(in, out, n, st);
+  int windows = 0;
+  if (!exact) windows = binade_cumsum(in, out, n, st);
+  if (trace)
+    std::fprintf(stderr, "[svb] cumsum n=%llu %s (%d windows)\n", (unsigned long long)n,
+                 exact ? "parallel (exact)" : windows > 0 ? "binade windows" : "sequential", windows);
 }
 
 // ------------------------------------------------------------- alias build

@@ -201,7 +201,8 @@ def test_alias_tables_bit_exact_large_exact_and_rounding_cumsums():
     """Tables of >= 8192 outcomes against the oracle's restatement of
     AliasTable.from_probs: distributions whose deficit / capacity prefix sums
     never round take the parallel scan (uniform over a subset, GHZ-like,
-    dyadic), the others the sequential chain (random); both bit-exact."""
+    dyadic), the others the binade-window scan (random, tie-prone, wide
+    range); all bit-exact."""
     rng = np.random.default_rng(11)
     cases = []
     for m, k in ((1 << 14, 3), (1 << 16, 1 << 9), (1 << 15, 1 << 15)):
@@ -211,7 +212,13 @@ def test_alias_tables_bit_exact_large_exact_and_rounding_cumsums():
     d = rng.integers(0, 8, size=1 << 14).astype(float)
     cases.append(d / d.sum() if d.sum() else d)          # dyadic weights (exact)
     r = rng.random(1 << 15) ** 3
-    cases.append(r / r.sum())                              # random (rounding chain)
+    cases.append(r / r.sum())                              # random (rounding chain: binade windows)
+    r = rng.random(1 << 18)
+    cases.append(r / r.sum())
+    t = np.round(rng.random(1 << 15) * 8) / 8 + 1.0 / 8    # few mantissa bits: ties in the chain
+    cases.append(t / t.sum())
+    g = rng.exponential(size=1 << 16) * 10.0 ** rng.uniform(-6, 0, size=1 << 16)
+    cases.append(g / g.sum())                              # wide dynamic range
     L = _lib.lib()
     for i, p in enumerate(cases):
         p = np.ascontiguousarray(p)
