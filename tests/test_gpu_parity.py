@@ -219,6 +219,8 @@ def test_alias_tables_bit_exact_large_exact_and_rounding_cumsums():
     cases.append(t / t.sum())
     g = rng.exponential(size=1 << 16) * 10.0 ** rng.uniform(-6, 0, size=1 << 16)
     cases.append(g / g.sum())                              # wide dynamic range
+    big = rng.random(1 << 23) ** 2                         # >= 2^21-element chains: binade windows
+    cases.append(big / big.sum())
     L = _lib.lib()
     for i, p in enumerate(cases):
         p = np.ascontiguousarray(p)
