@@ -22,9 +22,9 @@ build/device_core_src.o: paper_2512_04216_b200/csrc/device_core.cuh
 $(LIB): $(OBJ) build/device_core_src.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) build/device_core_src.o -ldl
 
-# experiment build with ALTFLAGS (e.g. -DSVB_C64_RB4, -DSVB_INTERP_MINB1) for A/B runs (SVB_LIB=build/alt/libsvb.so)
+# experiment build with ALTFLAGS (e.g. -DSVB_C64_RB4, -DSVB_INTERP_MINB2, -DSVB_C64_M14) for A/B runs (SVB_LIB=build/alt/libsvb.so)
 ALT := build/alt
-ALTFLAGS ?= -DSVB_INTERP_MINB1
+ALTFLAGS ?= -DSVB_INTERP_MINB2
 alt:
 	@mkdir -p $(ALT)
 	for f in $(SRC); do b=$$(basename $$f .cu); $(NVCC) $(NVFLAGS) $(ALTFLAGS) -c $$f -o $(ALT)/$$b.o > $(ALT)/$$b.log 2>&1 || exit 1; done

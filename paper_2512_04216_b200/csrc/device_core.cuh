@@ -827,11 +827,14 @@ __host__ __device__ constexpr int pass_min_blocks_of(int rsize, int rb) { return
 #endif
 template <typename R, int RB> constexpr int kPassThreads = 1 << (pass_tile_m((int)sizeof(R), RB) - RB);
 template <typename R, int RB> constexpr int kPassMinBlocks = pass_min_blocks_of((int)sizeof(R), RB);
-// the interpreter kernel k_pass<R, RB> (SVB_INTERP_MINB1: one CTA per SM, no register cap below 255)
-#ifdef SVB_INTERP_MINB1
-template <typename R, int RB> constexpr int kInterpMinBlocks = 1;
-#else
+// the interpreter kernel k_pass<R, RB>: one CTA per SM with a double ring.
+// At two CTAs (<= 128 registers) the complex128 body spilled 5.4 KB; without
+// the cap it does not spill, and config 4 (every circuit on the interpreter)
+// measured 1.52 vs 1.63 s.  (SVB_INTERP_MINB2: the two-CTA shape, A/B runs.)
+#ifdef SVB_INTERP_MINB2
 template <typename R, int RB> constexpr int kInterpMinBlocks = kPassMinBlocks<R, RB>;
+#else
+template <typename R, int RB> constexpr int kInterpMinBlocks = 1;
 #endif
 
 template <typename R> __host__ __device__ constexpr uint32_t tile_bytes_of(int m) { return (uint32_t)sizeof(cplx<R>) << m; }

@@ -543,12 +543,11 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
             o << "    " << guard << "svb::u1_piv<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk(coef[0])
               << ", " << rk(coef[1]) << ">(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
           } else {
-            // the pivot choice depends on the angles (the larger entry of each
-            // row): read from the op header at run time, so every angle set
-            // of this structure shares the kernel
-            o << "    " << guard << "svb::u1_piv_pc<R, RB, " << h.a << ", " << (h.kind == OP_U1PR ? "true" : "false")
-              << ">(reinterpret_cast<const int32_t*>(c.ops + " << (pay - (uint32_t)sizeof(OpHdr))
-              << ")[3] & 3, a, reinterpret_cast<const svb::cplx<R>*>(c.ops + " << pay << "));\n";
+            // (the pivot choice is part of the source: it depends on the
+            // angles only near a singular pivot, |m_rr| < 2^-8 |m_r,1-r|)
+            o << "    " << guard << "svb::u1_piv_p<R, RB, " << h.a << ", " << (h.n & 3) << ", "
+              << (h.kind == OP_U1PR ? "true" : "false") << ">(a, reinterpret_cast<const svb::cplx<R>*>(c.ops + "
+              << pay << "));\n";
           }
           break;
         }

@@ -1124,6 +1124,7 @@ SchedOptions default_options(int precision, int n, bool jit) {
   if (precision == SVB_C128) { o.rb = jit ? kJitRegBits<double> : kRegBits<double>; o.m = 12; }
   else { o.rb = jit ? kJitRegBits<float> : kRegBits<float>; o.m = pass_tile_m(4, o.rb); }
   o.structural = jit && n < kJitImmMinQubits;
+  if (const char* e = std::getenv("SVB_STRUCTURAL")) o.structural = o.structural && std::atoi(e) != 0;  // A/B runs
   return o;
 }
 
