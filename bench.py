@@ -588,14 +588,7 @@ def config_batch() -> dict:
     rc = batch.run_batch_codes(fresh, shots=1000, seed=0)
     dt_codes = time.perf_counter() - t0
     errs = sum(isinstance(r, Exception) for r in rc)
-    t0 = time.perf_counter()
-    batch.run_batch_codes(fresh, shots=1000, seed=0, jit="sync")  # NVRTC passes for 24 qubits (compiles once)
-    batch.run_batch_codes(fresh, shots=1000, seed=1, jit="sync")
-    dt_sync_first = time.perf_counter() - t0
     fresh2 = suite.batch_workload(10000, base=20000)
-    t0 = time.perf_counter()
-    batch.run_batch_codes(fresh2, shots=1000, seed=0, jit="sync")
-    dt_sync = time.perf_counter() - t0
     t0 = time.perf_counter()
     rd = batch.run_batch(fresh2, shots=1000, seed=0, jit="none")
     dt_dict = time.perf_counter() - t0
@@ -615,12 +608,8 @@ def config_batch() -> dict:
         "timed_set": "suite.batch_workload(10000, base=10000): circuits never run before in the process",
         "first_call_s": dt_first, "circuits_per_s_first_call": len(circs) / dt_first,
         "first_call_note": "batch_workload(10000), the first batch of the process (default jit='none': no compile)",
-        "jit_sync": {"fresh_circuits_s": dt_sync, "circuits_per_s": len(circs) / dt_sync,
-                     "compile_and_two_runs_s": dt_sync_first,
-                     "note": ("NVRTC-specialised passes for the 24-qubit circuits (results identical to sv.run), "
-                              "timed on a third fresh set after the structures were compiled")},
         "with_count_dicts_s": dt_dict, "circuits_per_s_with_dicts": len(circs) / dt_dict,
-        "with_count_dicts_note": "batch.run_batch (jit=none) on the third set (run once before with jit=sync), with {bitstring: count} dicts",
+        "with_count_dicts_note": "batch.run_batch (jit=none) on a third fresh set, with {bitstring: count} dicts",
         "dict_errors": int(sum(isinstance(r, Exception) for r in rd)),
         "note": ("device_path = batch.run_batch_codes ((code, count) arrays per circuit, default jit='none') on "
                  "circuits never run before in the process: host encoding of every gate + svb_batch_small / "
