@@ -1286,12 +1286,15 @@ __device__ __forceinline__ void upipe_sync(const PassCtx<R, RB>& c) {
 // Dynamic shared memory: ring | op stream (16-B padded) | uniform slots.
 // PERMIN: the kernel may serve a perm_in pass (the JIT sets it only for one;
 // the extra load addressing costs the others registers)
-template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0, int PERMIN = 0>
+// STAGES >= 0: the launch's ring depth as a compile-time constant (NVRTC
+// kernels: the other paths are dead code -- fewer instructions and spills)
+template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0, int PERMIN = 0, int STAGES = -1>
 __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
                                             const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
-                                            int zero_input = 0, int stages = kStages, int ops_mode = 0,
+                                            int zero_input = 0, int stages_arg = kStages, int ops_mode = 0,
                                             int nslots = 0) {
+  const int stages = STAGES >= 0 ? STAGES : stages_arg;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ PassDev pd;
   __shared__ uint64_t s_ldk[32];

@@ -804,6 +804,15 @@ void evict_lru(Driver& dr, int dev) {
   }
 }
 
+// Ring depth of a pass's launch: pass_stages, and the direct first round for
+// support-tracked passes (few live loads per tile, no ring barrier); for full
+// passes only on request (load latency exposed)
+template <typename R> static int launch_stages(const PassDev& pd, uint32_t staged, int nslots) {
+  int stages = pass_stages<R>(pd.rb, pd.m, staged, pd.ndiag, nslots, zsm_pass(pd));
+  if (stages == 1 && pd.direct && !pd.perm_in && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
+  return stages;
+}
+
 template <typename R>
 bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
                        cudaStream_t st, ProgramStats* stats, int nsm, bool zero_input) {
@@ -858,6 +867,13 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
         }
       }
       if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 1, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
+      {  // the ring depth this pass will launch with, compiled in (see pass_kernel's STAGES)
+        const int stg = launch_stages<R>(pd, staged[p], nslots[p]);
+        const std::string from = "(state, out, pdg, ops_g, ntiles, pass, zero_input, stages,";
+        const size_t at = srcs[p].rfind(from);
+        const size_t lt = at == std::string::npos ? at : srcs[p].rfind(">", at);
+        if (lt != std::string::npos) srcs[p].insert(lt, ", " + std::to_string(stg));
+      }
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
       keys[p] = std::to_string(dev) + ":" + buf;
@@ -1025,10 +1041,7 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const PassDev& pd = prog.passes[p];
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
-    int stages = pass_stages<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], zsm_pass(pd));
-    // direct first round: for support-tracked passes (few live loads per tile,
-    // no ring barrier); for full passes only on request (load latency exposed)
-    if (stages == 1 && pd.direct && !pd.perm_in && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
+    int stages = launch_stages<R>(pd, staged[p], nslots[p]);
     const unsigned smem = pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
     int per_sm = stages <= 1 ? pass_min_blocks_of((int)sizeof(R), pd.rb) : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
