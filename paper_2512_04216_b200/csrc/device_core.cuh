@@ -1288,13 +1288,17 @@ __device__ __forceinline__ void upipe_sync(const PassCtx<R, RB>& c) {
 // the extra load addressing costs the others registers)
 // STAGES >= 0: the launch's ring depth as a compile-time constant (NVRTC
 // kernels: the other paths are dead code -- fewer instructions and spills)
-template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0, int PERMIN = 0, int STAGES = -1>
+// NR >= 0 / ZIN >= 0: the pass's round count and lazy-|0..0> input flag, also
+// compiled in by the NVRTC kernels
+template <typename R, int RB, class Body, int ZSM = 0, int UIN = 0, int PERMIN = 0, int STAGES = -1, int NR = -1,
+          int ZIN = -1>
 __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
                                             const PassDev* __restrict__ pdg,
                                             const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass = 0,
-                                            int zero_input = 0, int stages_arg = kStages, int ops_mode = 0,
+                                            int zero_input_arg = 0, int stages_arg = kStages, int ops_mode = 0,
                                             int nslots = 0) {
   const int stages = STAGES >= 0 ? STAGES : stages_arg;
+  const int zero_input = ZIN >= 0 ? ZIN : zero_input_arg;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ PassDev pd;
   __shared__ uint64_t s_ldk[32];
@@ -1314,7 +1318,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // stages: 2 = double ring, 1 = single ring + prefetch, 0 = direct first round
   // (one tile of shared memory for the inter-round layouts, no cp.async)
   // a one-round direct pass never touches the ring (registers from HBM, to HBM)
-  const uint32_t ring_bytes = (stages == 0 && pd.nrounds == 1)
+  const int nrounds_c = NR >= 0 ? NR : pd.nrounds;
+  const uint32_t ring_bytes = (stages == 0 && nrounds_c == 1)
                                   ? 0u
                                   : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
   uint32_t staged = 0;
@@ -1340,7 +1345,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   PassCtx<R, RB> c(pd);
   c.state = state;
   c.out = out;
-  c.pthr = pd.perm_out ? thread_fixed_perm(pd, pd.rounds[pd.nrounds - 1], threadIdx.x) : 0;
+  c.pthr = pd.perm_out ? thread_fixed_perm(pd, pd.rounds[nrounds_c - 1], threadIdx.x) : 0;
   c.pbase = 0;
   c.ops = smraw + ring_bytes - pd.ops_begin;  // ops_mode 0 only
   c.uni = uni;
@@ -1353,7 +1358,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // Passing the wait for tile it means every warp has passed the wait for tile
   // it-D, i.e. finished tile it-D-1 -- the last user of slot (it+D)%K.  Warps
   // may drift D tiles apart instead of one.
-  const bool upipe = stages == 0 && pd.nrounds == 1;
+  const bool upipe = stages == 0 && nrounds_c == 1;
   c.pro = uni + (upipe ? kUPipeSlots * kUGroup : 2) * pd.ndiag * kUniStride;
   c.nthr = blockDim.x;
   // fused <Z> running sums: registers, or (ZSM) shared memory after the
@@ -1371,7 +1376,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, warp = tid >> 5;
   c.tid = tid;
   const uint32_t nwarps = nthr >> 5;
-  const int m = pd.m, nrounds = pd.nrounds, ndiag = pd.ndiag;
+  const int m = pd.m, nrounds = nrounds_c, ndiag = pd.ndiag;
   const uint32_t T = 1u << m;
   cplx<R>* ring = reinterpret_cast<cplx<R>*>(smraw);
   constexpr int kPer = sizeof(cplx<R>) == 16 ? 1 : 2;

@@ -867,12 +867,15 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
         }
       }
       if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 1, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
-      {  // the ring depth this pass will launch with, compiled in (see pass_kernel's STAGES)
+      {  // the launch's ring depth, round count and lazy-input flag, compiled in
+         // (pass_kernel's STAGES / NR / ZIN)
         const int stg = launch_stages<R>(pd, staged[p], nslots[p]);
+        const int zin = (zero_input && p == 0) ? 1 : 0;
         const std::string from = "(state, out, pdg, ops_g, ntiles, pass, zero_input, stages,";
         const size_t at = srcs[p].rfind(from);
         const size_t lt = at == std::string::npos ? at : srcs[p].rfind(">", at);
-        if (lt != std::string::npos) srcs[p].insert(lt, ", " + std::to_string(stg));
+        if (lt != std::string::npos)
+          srcs[p].insert(lt, ", " + std::to_string(stg) + ", " + std::to_string(pd.nrounds) + ", " + std::to_string(zin));
       }
       char buf[40];
       std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)fnv1a(srcs[p], salt));
