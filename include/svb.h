@@ -192,6 +192,11 @@ int svb_alias_draw(int device, const double* probs, uint64_t m, uint64_t shots, 
  * next `shots` doubles of the numpy PCG64 state pcg[4], one per draw. */
 int svb_alias_sample(int device, const double* prob_row, const int64_t* alias_row, uint64_t m, uint64_t shots,
                      const uint64_t* pcg, uint64_t* out_idx);
+/* The same draws from a device-resident table (uploaded once): handle from
+ * svb_alias_upload, freed by svb_alias_release.  sampling.py:72-77 */
+int svb_alias_upload(int device, const double* prob_row, const int64_t* alias_row, uint64_t m, void** out_table);
+int svb_alias_sample_table(void* table, uint64_t shots, const uint64_t* pcg, uint64_t* out_idx);
+int svb_alias_release(void* table);
 
 /* Sharded mode (global<->local qubit swaps, svb_dist in sharded.py):
  * raw device pointer of the state (synchronised), and gather/scatter of the

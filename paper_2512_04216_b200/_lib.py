@@ -94,6 +94,9 @@ _SIGS = {
     "svb_permute_qubits": (c_int, [_h, POINTER(c_int32)]),
     "svb_select_half": (c_int, [_h, _h, c_int, c_int]),
     "svb_alias_sample": (c_int, [c_int, _dp, _i64p, c_uint64, c_uint64, _u64p, _u64p]),
+    "svb_alias_upload": (c_int, [c_int, _dp, _i64p, c_uint64, ctypes.POINTER(c_void_p)]),
+    "svb_alias_sample_table": (c_int, [c_void_p, c_uint64, _u64p, _u64p]),
+    "svb_alias_release": (c_int, [c_void_p]),
     "svb_alias_draw": (c_int, [c_int, _dp, c_uint64, c_uint64, POINTER(c_uint64), POINTER(c_uint64)]),
     "svb_sample_slice": (c_int, [_h, c_uint64, _u64p, c_double, c_double, c_double, _i32p, c_int, c_uint64, _u64p,
                                  _u64p, _u64p]),

@@ -747,6 +747,109 @@ int svb_alias_sample(int device, const double* prob_row, const int64_t* alias_ro
   });
 }
 
+// Device-resident alias tables: sampling.AliasTable uploads its rows once and
+// draws from them (a per-call upload made a 2^20-row table's draws ~3x the
+// cost of a 16-row table's, against the reference's O(1)-per-draw test).
+struct svb_alias_dev {
+  int device = 0;
+  uint64_t m = 0;
+  double* prob = nullptr;
+  int64_t* alias = nullptr;
+};
+
+int svb_alias_upload(int device, const double* prob_row, const int64_t* alias_row, uint64_t m, void** out_table) {
+  svb_alias_dev* t = nullptr;
+  const int rc = guard([&] {
+    require(m >= 1 && m <= (1ull << 40), SVB_E_ARG, "alias_upload: bad table size");
+    SVB_CUDA(cudaSetDevice(device));
+    t = new svb_alias_dev();
+    t->device = device;
+    t->m = m;
+    if (cudaMalloc(&t->prob, m * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&t->alias, m * sizeof(int64_t)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(SVB_E_OOM, "alias_upload: device allocation failed");
+    }
+    SVB_CUDA(cudaMemcpy(t->prob, prob_row, m * sizeof(double), cudaMemcpyHostToDevice));
+    SVB_CUDA(cudaMemcpy(t->alias, alias_row, m * sizeof(int64_t), cudaMemcpyHostToDevice));
+  });
+  if (rc != SVB_OK && t) {
+    cudaFree(t->prob);
+    cudaFree(t->alias);
+    delete t;
+    t = nullptr;
+  }
+  *out_table = t;
+  return rc;
+}
+
+int svb_alias_sample_table(void* table, uint64_t shots, const uint64_t* pcg, uint64_t* out_idx) {
+  return guard([&] {
+    require(table != nullptr, SVB_E_ARG, "alias_sample_table: null table");
+    require(shots >= 1, SVB_E_ARG, "shots must be positive");
+    const svb_alias_dev* t = static_cast<const svb_alias_dev*>(table);
+    SVB_CUDA(cudaSetDevice(t->device));
+    // one stream per thread and device, and the pool's freed scratch kept
+    // mapped: a per-call stream and a re-mapped output buffer made the cost of
+    // a draw batch vary by milliseconds
+    keep_pool_mapped(t->device);
+    static thread_local cudaStream_t streams[16] = {};
+    cudaStream_t& st = streams[t->device & 15];
+    if (!st) SVB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    uint64_t* dc = nullptr;
+    int w = 0;
+    while ((1ull << w) < t->m) ++w;
+    int32_t ident[64];
+    for (int p = 0; p < 64; ++p) ident[p] = p;
+    static const bool trace = std::getenv("SVB_TRACE") != nullptr;
+    const auto h0 = std::chrono::steady_clock::now();
+    try {
+      SVB_CUDA(cudaMallocAsync(&dc, shots * sizeof(uint64_t), st));
+      alias_draw(t->prob, t->alias, t->m, shots, pcg, ident, w, dc, st);
+      if (trace) {
+        SVB_CUDA(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[svb] alias_sample_table m=%llu shots=%llu draw %.3f ms\n", (unsigned long long)t->m,
+                     (unsigned long long)shots,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+      }
+      // large batches land in a pinned staging buffer (DMA at link speed
+      // whatever state the caller's pages are in), then one host copy
+      const size_t bytes = shots * sizeof(uint64_t);
+      static thread_local void* pin = nullptr;
+      static thread_local size_t pin_bytes = 0;
+      if (bytes >= (512u << 10) && pin_bytes < bytes) {
+        if (pin) cudaFreeHost(pin);
+        pin = nullptr;
+        pin_bytes = 0;
+        if (cudaHostAlloc(&pin, bytes, cudaHostAllocPortable) == cudaSuccess) pin_bytes = bytes;
+        else cudaGetLastError();
+      }
+      const bool staged = bytes >= (512u << 10) && pin_bytes >= bytes;
+      SVB_CUDA(cudaMemcpyAsync(staged ? pin : out_idx, dc, bytes, cudaMemcpyDeviceToHost, st));
+      SVB_CUDA(cudaFreeAsync(dc, st));
+      SVB_CUDA(cudaStreamSynchronize(st));
+      if (staged) std::memcpy(out_idx, pin, bytes);
+      if (trace)
+        std::fprintf(stderr, "[svb] alias_sample_table total %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      throw;
+    }
+  });
+}
+
+int svb_alias_release(void* table) {
+  return guard([&] {
+    svb_alias_dev* t = static_cast<svb_alias_dev*>(table);
+    if (!t) return;
+    cudaSetDevice(t->device);
+    cudaFree(t->prob);
+    cudaFree(t->alias);
+    delete t;
+  });
+}
+
 int svb_device_ptr(svb_handle h, void** ptr, uint64_t* bytes, int64_t* stream) {
   return guard([&] {
     check_handle(h);

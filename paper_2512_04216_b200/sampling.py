@@ -22,6 +22,20 @@ from . import _lib
 from ._lib import SamplingError, check, lib, ptr
 
 
+class _DeviceRows:
+    """Owner of a device-resident table (svb_alias_upload / svb_alias_release)."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().svb_alias_release(self.handle)
+        except Exception:
+            pass
+
+
 @dataclass
 class AliasTable:
     size: int
@@ -57,12 +71,33 @@ class AliasTable:
             return np.empty(0, dtype=np.int64)
         words = pcg_words(rng)
         out = np.empty(n, dtype=np.uint64)
-        pr = np.ascontiguousarray(self.prob, dtype=np.float64)
-        al = np.ascontiguousarray(self.alias, dtype=np.int64)
-        check(lib().svb_alias_sample(self.device, ptr(pr, _lib.c_double), ptr(al, _lib.c_int64), self.size, n,
-                                     ptr(words, _lib.c_uint64), ptr(out, _lib.c_uint64)))
+        check(lib().svb_alias_sample_table(self._device_table(), n, ptr(words, _lib.c_uint64),
+                                           ptr(out, _lib.c_uint64)))
         rng.bit_generator.advance(n)
         return out.view(np.int64)
+
+    def __getstate__(self):  # the device rows stay with the process that uploaded them
+        state = dict(self.__dict__)
+        state.pop("_dev", None)
+        return state
+
+    def _device_table(self):
+        """The rows on the device, uploaded once per (prob, alias) pair: per-draw
+        cost independent of the table size (sampling.py:72-77; a per-call upload
+        made big tables' draws ~3x dearer).  Re-uploaded when the attributes are
+        reassigned; in-place edits of the arrays are not tracked."""
+        key = (id(self.prob), id(self.alias), self.size, self.device)
+        cached = self.__dict__.get("_dev")
+        if cached is not None and cached[0] == key:
+            return cached[1].handle
+        pr = np.ascontiguousarray(self.prob, dtype=np.float64)
+        al = np.ascontiguousarray(self.alias, dtype=np.int64)
+        h = _lib.c_void_p()
+        check(lib().svb_alias_upload(self.device, ptr(pr, _lib.c_double), ptr(al, _lib.c_int64), self.size,
+                                     _lib.ctypes.byref(h)))
+        table = _DeviceRows(h)
+        self.__dict__["_dev"] = (key, table)
+        return table.handle
 
     def sample_one(self, rng) -> int:
         v = rng.random() * self.size
