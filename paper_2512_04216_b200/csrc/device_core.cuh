@@ -938,7 +938,10 @@ __device__ void diag_uniform_items(const uint8_t* ops, const uint32_t* diag_off,
 // Per-CTA context of a fused pass, shared by the interpreter body and the
 // JIT-generated bodies.
 template <typename R, int RB> struct PassCtx {
-  static constexpr int kHoist = 4;  // rounds whose thread constants live in registers
+#ifndef SVB_HOIST
+#define SVB_HOIST 4
+#endif
+  static constexpr int kHoist = SVB_HOIST;  // rounds whose thread constants live in registers
   const PassDev& pd;
   cplx<R>* state;
   cplx<R>* out;          // destination of the last round (== state unless pd.perm_out / pd.perm_in: the launchers pass it always)
