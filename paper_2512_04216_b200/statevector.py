@@ -223,7 +223,12 @@ class DeviceState:
         self.precision = "c128" if _prec_code(precision) == _lib.SVB_C128 else "c64"
         self.device = device
         h = _lib.c_void_p()
-        check(lib().svb_create(self.n, _prec_code(precision), device, _lib.ctypes.byref(h)))
+        rc = lib().svb_create(self.n, _prec_code(precision), device, _lib.ctypes.byref(h))
+        if rc == _lib.SVB_E_OOM and _pool.bytes:
+            # idle pooled states (final_state / run cache) hold the memory: drop them and retry once
+            _pool.clear()
+            rc = lib().svb_create(self.n, _prec_code(precision), device, _lib.ctypes.byref(h))
+        check(rc)
         self._h = h
 
     @classmethod
@@ -466,13 +471,7 @@ class _StatePool:
             if lst:
                 self.bytes -= self._size(n, key[1])
                 return lst.pop()
-        try:
-            return DeviceState(n, precision, device)
-        except (BackendError, QubitCapError):
-            if not self.bytes:
-                raise
-            self.clear()  # idle states held device memory the new one needs
-            return DeviceState(n, precision, device)
+        return DeviceState(n, precision, device)  # (an out-of-memory create empties this pool and retries)
 
     def release(self, st: DeviceState) -> None:
         key = (st.n, st.precision, st.device)
