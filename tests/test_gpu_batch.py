@@ -114,3 +114,28 @@ def test_batch_executor_records_bad_circuits():
 
     assert isinstance(res[1], QubitCapError)
     assert int(res[0].counts.sum()) == 100 and np.array_equal(res[0].codes, res[2].codes)
+
+
+def test_concurrent_batch_calls_share_the_device():
+    """Two threads running batches at once: one call gets the worker arena,
+    the other its own pool buffers (svb_batch_run's try-lock); both give the
+    sequential results (interpreter kernels: reproducible)."""
+    import threading
+
+    from paper_2512_04216_b200.batch import run_batch_codes
+
+    sets = [suite.batch_workload(60, base=500 + 100 * k) for k in range(2)]
+    want = [run_batch_codes(s, shots=500, seed=3, jit="none") for s in sets]
+    got = [None, None]
+
+    def work(k):
+        got[k] = run_batch_codes(sets[k], shots=500, seed=3, jit="none", chunk=16)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for a, b in zip(want, got):
+        for x, y in zip(a, b):
+            assert np.array_equal(x.codes, y.codes) and np.array_equal(x.counts, y.counts)
