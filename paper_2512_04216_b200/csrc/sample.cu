@@ -128,6 +128,22 @@ __global__ void k_pair_level(const double* __restrict__ in, uint64_t nout, doubl
   if (i < nout) out[i] = in[2 * i] + in[2 * i + 1];
 }
 
+// the last halving levels in one CTA (n <= 2048, a power of two): the same
+// pairs in the same order as k_pair_level, levels separated by barriers
+__global__ void __launch_bounds__(1024) k_pair_tail(const double* __restrict__ in, uint64_t n, double* __restrict__ out) {
+  __shared__ double buf[2048];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) buf[i] = in[i];
+  __syncthreads();
+  for (uint64_t w = n / 2; w >= 1; w /= 2) {
+    double v = 0.0;
+    if (threadIdx.x < w) v = buf[2 * threadIdx.x] + buf[2 * threadIdx.x + 1];
+    __syncthreads();
+    if (threadIdx.x < w) buf[threadIdx.x] = v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = buf[0];
+}
+
 double pairwise_sum_device(const double* d_x, uint64_t m, double* d_ws, cudaStream_t st) {
   double h = 0.0;
   bool pow2 = (m & (m - 1)) == 0;
@@ -143,12 +159,17 @@ double pairwise_sum_device(const double* d_x, uint64_t m, double* d_ws, cudaStre
   double* b = d_ws + nl;
   k_pairwise_leaves<<<(unsigned)((nl + 255) / 256), 256, 0, st>>>(d_x, nl, a);
   SVB_CHECK_LAUNCH();
-  while (nl > 1) {
+  while (nl > 2048) {
     uint64_t no = nl / 2;
     k_pair_level<<<(unsigned)((no + 255) / 256), 256, 0, st>>>(a, no, b);
     SVB_CHECK_LAUNCH();
     double* t = a; a = b; b = t;
     nl = no;
+  }
+  if (nl > 1) {
+    k_pair_tail<<<1, 1024, 0, st>>>(a, nl, b);
+    SVB_CHECK_LAUNCH();
+    a = b;
   }
   SVB_CUDA(cudaMemcpyAsync(&h, a, sizeof(double), cudaMemcpyDeviceToHost, st));
   SVB_CUDA(cudaStreamSynchronize(st));
@@ -173,6 +194,19 @@ template <typename T> static T d2h_scalar(const T* d, cudaStream_t st) {
   SVB_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
   SVB_CUDA(cudaStreamSynchronize(st));
   return h;
+}
+// *a + *b with one synchronisation (both copies into a pinned pair)
+template <typename T> static T d2h_sum2(const T* a, const T* b, cudaStream_t st) {
+  static thread_local T* pin = nullptr;
+  if (!pin && cudaHostAlloc(reinterpret_cast<void**>(&pin), 2 * sizeof(T), cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    pin = nullptr;
+    return d2h_scalar(a, st) + d2h_scalar(b, st);
+  }
+  SVB_CUDA(cudaMemcpyAsync(pin, a, sizeof(T), cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaMemcpyAsync(pin + 1, b, sizeof(T), cudaMemcpyDeviceToHost, st));
+  SVB_CUDA(cudaStreamSynchronize(st));
+  return pin[0] + pin[1];
 }
 
 // Device prefix sums (own kernels, fixed combine order: results are
@@ -609,29 +643,37 @@ __global__ void k_absorb(const int64_t* __restrict__ starts, uint64_t nruns, uin
   }
 }
 
-__global__ void __launch_bounds__(256) k_absorb_long(const int64_t* __restrict__ starts, uint64_t nruns, uint64_t ns,
-                                                     const int64_t* __restrict__ owner,
-                                                     const double* __restrict__ deficit, double* __restrict__ rem,
-                                                     const uint64_t* __restrict__ long_runs) {
-  __shared__ double tot;
+__device__ __forceinline__ int lsb_exp(double x) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  unsigned long long mant = bits & ((1ull << 52) - 1);
+  if (ex == 0 && mant == 0) return INT_MAX;
+  if (ex != 0) mant |= 1ull << 52;
+  return __ffsll((long long)mant) - 1 + (ex == 0 ? 1 : ex) - 1075;
+}
+
+// Long runs are reduced grid-wide: blockIdx.y picks the run, gridDim.x blocks
+// stride through it with four independent loads in flight per thread (one
+// block per run was load-latency bound: a 2^19-element GHZ-20 run took 1 ms).
+// Each block leaves (partial sum, lowest set exponent) for k_absorb_long_fin.
+constexpr int kAbsorbParts = 64;
+__global__ void __launch_bounds__(256) k_absorb_long_part(const int64_t* __restrict__ starts, uint64_t nruns,
+                                                          uint64_t ns, const double* __restrict__ deficit,
+                                                          const uint64_t* __restrict__ long_runs,
+                                                          double* __restrict__ psum, int* __restrict__ plsb) {
   __shared__ double wsum[8];
   __shared__ int wexp[8];
-  const uint64_t r = long_runs[blockIdx.x];
+  const uint64_t r = long_runs[blockIdx.y];
   const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
-  // the in-order sum never rounds when every term is a multiple of 2^lsb and
-  // the total stays below 2^(52 + lsb) (see cumsum_exact): then any order
-  // gives it, so the block reduces in parallel; else the sequential chain
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
   double part = 0.0;
   int lsb = INT_MAX;
-  for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-    const double x = deficit[i];
-    part += x;
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-    const int ex = (int)((bits >> 52) & 0x7ff);
-    unsigned long long mant = bits & ((1ull << 52) - 1);
-    if (ex == 0 && mant == 0) continue;
-    if (ex != 0) mant |= 1ull << 52;
-    lsb = min(lsb, __ffsll((long long)mant) - 1 + (ex == 0 ? 1 : ex) - 1075);
+  for (uint64_t i = b + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e; i += 4 * S) {
+    double x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = i + k * S < e ? deficit[i + k * S] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { part += x[k]; lsb = min(lsb, lsb_exp(x[k])); }
   }
   for (int o = 16; o > 0; o >>= 1) {
     part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -643,11 +685,42 @@ __global__ void __launch_bounds__(256) k_absorb_long(const int64_t* __restrict__
     double t = 0.0;
     int l = INT_MAX;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { t += wsum[w]; l = min(l, wexp[w]); }
-    wexp[0] = (l == INT_MAX || t < ldexp(1.0, 52 + l)) ? 1 : 0;
-    tot = t;
+    psum[(uint64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    plsb[(uint64_t)blockIdx.y * gridDim.x + blockIdx.x] = l;
+  }
+}
+
+// The in-order sum never rounds when every term is a multiple of 2^lsb and
+// the total stays below 2^(52 + lsb) (see cumsum_exact): then any order gives
+// it and the partials stand; else the run is re-summed as the sequential chain.
+__global__ void __launch_bounds__(256) k_absorb_long_fin(const int64_t* __restrict__ starts, uint64_t nruns,
+                                                         uint64_t ns, const int64_t* __restrict__ owner,
+                                                         const double* __restrict__ deficit, double* __restrict__ rem,
+                                                         const uint64_t* __restrict__ long_runs,
+                                                         const double* __restrict__ psum,
+                                                         const int* __restrict__ plsb, int parts) {
+  __shared__ double tot;
+  __shared__ int exact;
+  const uint64_t r = long_runs[blockIdx.x];
+  const uint64_t b = (uint64_t)starts[r], e = r + 1 < nruns ? (uint64_t)starts[r + 1] : ns;
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    int l = INT_MAX;
+    for (int k = threadIdx.x; k < parts; k += 32) {
+      t += psum[(uint64_t)blockIdx.x * parts + k];
+      l = min(l, plsb[(uint64_t)blockIdx.x * parts + k]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      t += __shfl_xor_sync(0xffffffffu, t, o);
+      l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
+    }
+    if (threadIdx.x == 0) {
+      tot = t;
+      exact = (l == INT_MAX || t < ldexp(1.0, 52 + l)) ? 1 : 0;
+    }
   }
   __syncthreads();
-  if (!wexp[0]) seq_block(deficit + b, e - b, nullptr, &tot);
+  if (!exact) seq_block(deficit + b, e - b, nullptr, &tot);
   __syncthreads();
   if (threadIdx.x == 0) {
     const int64_t o = owner[b];
@@ -694,8 +767,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
                                              d_alias_row, flag.as<int64_t>());
   SVB_CHECK_LAUNCH();
   scan_exclusive(flag.as<int64_t>(), pos.as<int64_t>(), m, st);
-  uint64_t nl = (uint64_t)d2h_scalar(pos.as<int64_t>() + (m - 1), st) +
-                (uint64_t)d2h_scalar(flag.as<int64_t>() + (m - 1), st);
+  uint64_t nl = (uint64_t)d2h_sum2(pos.as<int64_t>() + (m - 1), flag.as<int64_t>() + (m - 1), st);
   uint64_t ns = m - nl;
   if (nl == 0 || ns == 0) return;
 
@@ -735,8 +807,7 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     scan_exclusive(head.as<int64_t>(), hpos.as<int64_t>(), ns, st);
     k_run_starts<<<grid_for(ns, B), B, 0, st>>>(head.as<int64_t>(), hpos.as<int64_t>(), ns, starts.as<int64_t>());
     SVB_CHECK_LAUNCH();
-    const uint64_t nruns = (uint64_t)d2h_scalar(hpos.as<int64_t>() + (ns - 1), st) +
-                           (uint64_t)d2h_scalar(head.as<int64_t>() + (ns - 1), st);
+    const uint64_t nruns = (uint64_t)d2h_sum2(hpos.as<int64_t>() + (ns - 1), head.as<int64_t>() + (ns - 1), st);
     SVB_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(unsigned long long), st));
     k_absorb<<<grid_for(nruns, 64), 64, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
                                                  deficit.as<double>(), Rm, long_runs.as<uint64_t>(),
@@ -744,15 +815,22 @@ void alias_build(double* d_probs, uint64_t m, double* d_prob_row, int64_t* d_ali
     SVB_CHECK_LAUNCH();
     const unsigned long long nl_runs = d2h_scalar(nlong.as<unsigned long long>(), st);
     if (nl_runs) {
-      k_absorb_long<<<(unsigned)nl_runs, 256, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
-                                                       deficit.as<double>(), Rm, long_runs.as<uint64_t>());
+      const uint64_t want = (uint64_t)4 * 148 / nl_runs;
+      const int parts = (int)(want < 1 ? 1 : want > (uint64_t)kAbsorbParts ? kAbsorbParts : want);
+      DevBuf psum(sizeof(double) * nl_runs * parts, st), plsb(sizeof(int) * nl_runs * parts, st);
+      k_absorb_long_part<<<dim3((unsigned)parts, (unsigned)nl_runs), 256, 0, st>>>(
+          starts.as<int64_t>(), nruns, ns, deficit.as<double>(), long_runs.as<uint64_t>(), psum.as<double>(),
+          plsb.as<int>());
+      SVB_CHECK_LAUNCH();
+      k_absorb_long_fin<<<(unsigned)nl_runs, 256, 0, st>>>(starts.as<int64_t>(), nruns, ns, owner.as<int64_t>(),
+                                                           deficit.as<double>(), Rm, long_runs.as<uint64_t>(),
+                                                           psum.as<double>(), plsb.as<int>(), parts);
       SVB_CHECK_LAUNCH();
     }
     k_conv_flags<<<grid_for(nl, B), B, 0, st>>>(Rm, nl, conv.as<int64_t>());
     SVB_CHECK_LAUNCH();
     scan_exclusive(conv.as<int64_t>(), cpos.as<int64_t>(), nl, st);
-    uint64_t nconv = (uint64_t)d2h_scalar(cpos.as<int64_t>() + (nl - 1), st) +
-                     (uint64_t)d2h_scalar(conv.as<int64_t>() + (nl - 1), st);
+    uint64_t nconv = (uint64_t)d2h_sum2(cpos.as<int64_t>() + (nl - 1), conv.as<int64_t>() + (nl - 1), st);
     if (nconv == 0) break;  // sampling.py:60-63
     k_convert<<<grid_for(nl, B), B, 0, st>>>(conv.as<int64_t>(), cpos.as<int64_t>(), nl, L, Rm, S,
                                              scaled.as<double>(), L2, Rm2);
@@ -1147,8 +1225,7 @@ uint64_t histogram_codes(uint64_t* d_codes, uint64_t shots, int w, uint64_t* h_c
   k_rle_scatter<<<g, 256, 0, st>>>(src, shots, pos.as<uint32_t>(), flag.as<uint32_t>(), uniq.as<uint64_t>(),
                                    start.as<uint64_t>());
   SVB_CHECK_LAUNCH();
-  const uint64_t nruns = (uint64_t)d2h_scalar(pos.as<uint32_t>() + (shots - 1), st) +
-                         d2h_scalar(flag.as<uint32_t>() + (shots - 1), st);
+  const uint64_t nruns = (uint64_t)d2h_sum2(pos.as<uint32_t>() + (shots - 1), flag.as<uint32_t>() + (shots - 1), st);
   k_rle_counts<<<(unsigned)((nruns + 255) / 256), 256, 0, st>>>(start.as<uint64_t>(), nruns, shots,
                                                                  cnt.as<uint64_t>());
   SVB_CHECK_LAUNCH();

@@ -219,6 +219,12 @@ def test_alias_tables_bit_exact_large_exact_and_rounding_cumsums():
     cases.append(t / t.sum())
     g = rng.exponential(size=1 << 16) * 10.0 ** rng.uniform(-6, 0, size=1 << 16)
     cases.append(g / g.sum())                              # wide dynamic range
+    h = rng.random(1 << 16) * 1e-3                         # 4 heavy outcomes absorb runs of ~16k
+    h[rng.choice(h.size, size=4, replace=False)] = 10.0    # random deficits: long sequential bins
+    cases.append(h / h.sum())
+    u = np.zeros(1 << 17)
+    u[rng.choice(u.size, size=6, replace=False)] = 1.0 / 6  # long runs with exact bins (parallel)
+    cases.append(u)
     big = rng.random(1 << 23) ** 2                         # >= 2^21-element chains: binade windows
     cases.append(big / big.sum())
     L = _lib.lib()
