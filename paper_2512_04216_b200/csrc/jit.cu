@@ -834,7 +834,9 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
   std::vector<CUfunction> fns(np, nullptr);
   std::vector<int> nslots(np, 0);
   std::vector<uint32_t> staged(np, 0);
-  const uint64_t salt = fnv1a(svb_device_core_src, fnv1a("svb-jit-v1 sm_100a"));
+  // the engine source's hash, once per process (a byte-serial pass over ~90 KB
+  // on every apply was 80 us of host time before the first launch)
+  static const uint64_t salt = fnv1a(svb_device_core_src, fnv1a("svb-jit-v1 sm_100a"));
   Key128 pkey{salt ^ (uint64_t)dev, 0x243F6A8885A308D3ull + sizeof(R)};
   mix_bytes(pkey, prog.passes.data(), prog.passes.size() * sizeof(PassDev));
   mix_bytes(pkey, prog.ops.data(), prog.ops.size());
