@@ -165,6 +165,11 @@ constexpr int kUniStride = 24;
 #define SVB_UPIPE_AHEAD 1
 #endif
 // SVB_UWAIT_FIRST: wait for the tile's uniform slot before issuing its loads
+#ifndef SVB_UPIPE_PROBE
+// timing probes only (results are wrong): 1 = skip the uniform-slot waits,
+// 2 = also skip evaluating the uniform factors
+#define SVB_UPIPE_PROBE 0
+#endif
 #ifndef SVB_UWAIT_FIRST
 #define SVB_UWAIT_FIRST 0
 #endif
@@ -1530,8 +1535,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
         } else {
           const int un = (it + kUPipeAhead) % kUPipeSlots;
           const uint64_t tf = (uint64_t)t + (uint64_t)kUPipeAhead * gridDim.x;
-          if (!SVB_UWAIT_FIRST && !UIN) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
-          if (!UIN && tf < ntiles) {
+          if (!SVB_UWAIT_FIRST && !UIN && SVB_UPIPE_PROBE == 0) mbar_wait(&s_ubar[u], (uint32_t)(it / kUPipeSlots) & 1u);
+          if (!UIN && tf < ntiles && SVB_UPIPE_PROBE < 2) {
             diag_uniform_items<R, RB>(smraw + ring_bytes, s_doff, pd.items, pd.nitems,
                                       tile_base_warp(pd, (uint32_t)tf, lane), uni + un * ndiag * kUniStride, warp,
                                       nwarps, lane);

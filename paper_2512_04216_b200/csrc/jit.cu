@@ -649,6 +649,7 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (const char* e = std::getenv("SVB_UWAIT_FIRST")) o << "#define SVB_UWAIT_FIRST " << std::atoi(e) << "\n";
   if (const char* e = std::getenv("SVB_UIN")) o << "#define SVB_UIN " << (std::atoi(e) != 0 ? 1 : 0) << "\n";
   if (const char* e = std::getenv("SVB_UGROUP")) o << "#define SVB_UGROUP " << std::max(1, std::atoi(e)) << "\n";
+  if (const char* e = std::getenv("SVB_UPIPE_PROBE")) o << "#define SVB_UPIPE_PROBE " << std::atoi(e) << "\n";
   if (const char* e = std::getenv("SVB_HOIST")) o << "#define SVB_HOIST " << std::max(1, std::atoi(e)) << "\n";
   o << "#include \"device_core.cuh\"\nusing R = " << (sizeof(R) == 8 ? "double" : "float") << ";\n";
   // tile loads with the layout's offsets as immediates (see issue_tile)

@@ -10,7 +10,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-template <int K, bool STRIDED, bool LOAD, int AHEAD, int PF>
+template <int LV>
+__device__ __forceinline__ double2 ldv(const double2* p) {
+  if (LV == 0) return __ldcs(p);
+  if (LV == 3) return __ldg(p);
+  double2 v;
+  if (LV == 1)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  else
+    asm volatile("ld.global.L2::256B.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+template <int K, bool STRIDED, bool LOAD, int AHEAD, int PF, int LV = 0>
 __global__ void __launch_bounds__(256) k_pass(const double2* __restrict__ in, double2* __restrict__ out,
                                               uint32_t ntiles, double c0, uint32_t t0 = 0) {
   // AHEAD > 0: the loads of the next AHEAD tiles are in flight in registers
@@ -19,7 +31,7 @@ __global__ void __launch_bounds__(256) k_pass(const double2* __restrict__ in, do
 #pragma unroll
   for (int j = 0; j < AHEAD; ++j) {
     const uint32_t tj = t0 + blockIdx.x + j * gridDim.x;
-    q[j] = tj < ntiles ? __ldcs(in + ((((uint64_t)tj << 8) | threadIdx.x) & lmask)) : make_double2(0, 0);
+    q[j] = tj < ntiles ? ldv<LV>(in + ((((uint64_t)tj << 8) | threadIdx.x) & lmask)) : make_double2(0, 0);
   }
   uint32_t it = 0;
   for (uint32_t t = t0 + blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
@@ -37,13 +49,13 @@ __global__ void __launch_bounds__(256) k_pass(const double2* __restrict__ in, do
     double2 x = make_double2(c0, 0.5);
     if (LOAD) {
       if (AHEAD == 0) {
-        x = __ldcs(in + (base & lmask));
+        x = ldv<LV>(in + (base & lmask));
       } else {
         x = q[0];
 #pragma unroll
         for (int j = 0; j + 1 < AHEAD; ++j) q[j] = q[j + 1];
         const uint32_t tn = t + AHEAD * gridDim.x;
-        q[AHEAD - 1] = tn < ntiles ? __ldcs(in + ((((uint64_t)tn << 8) | threadIdx.x) & lmask)) : make_double2(0, 0);
+        q[AHEAD - 1] = tn < ntiles ? ldv<LV>(in + ((((uint64_t)tn << 8) | threadIdx.x) & lmask)) : make_double2(0, 0);
       }
     }
 #pragma unroll
@@ -106,16 +118,16 @@ template <class F> float best(F f) {
   return bt;
 }
 
-template <int K, bool S, bool L, int AH = 0, int PF = 0>
+template <int K, bool S, bool L, int AH = 0, int PF = 0, int LV = 0>
 void run(const double2* x, double2* y, int per, int nsm) {
   const uint32_t ntiles = 1u << 18;
   const int g = nsm * per;
-  const float t = best([&] { k_pass<K, S, L, AH, PF><<<g, 256>>>(x, y, ntiles, 0.999); });
+  const float t = best([&] { k_pass<K, S, L, AH, PF, LV><<<g, 256>>>(x, y, ntiles, 0.999); });
   const double wbytes = 16.0 * (1ull << 30);
   const double rbytes = L ? 16.0 * (1ull << 26) : 0.0;
   std::printf("{\"K\": %d, \"fp64_per_amp\": %d, \"strided\": %d, \"load\": %d, \"ctas_per_sm\": %d, \"ms\": %.3f, "
-              "\"gbs\": %.1f, \"ahead\": %d, \"l2_prefetch_tiles\": %d}\n",
-              K, 2 * K, (int)S, (int)L, per, t, (wbytes + rbytes) / t / 1e6, AH, PF);
+              "\"gbs\": %.1f, \"ahead\": %d, \"l2_prefetch_tiles\": %d, \"load_variant\": %d}\n",
+              K, 2 * K, (int)S, (int)L, per, t, (wbytes + rbytes) / t / 1e6, AH, PF, LV);
 }
 
 int main() {
@@ -126,11 +138,10 @@ int main() {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   for (int per : {3, 8}) {
-    run<14, true, true, 1>(x, y, per, nsm);
-    run_segmented<14>(x, y, per, nsm, 32);
-    run_segmented<14>(x, y, per, nsm, 64);
-    run_segmented<14>(x, y, per, nsm, 128);
-    run_segmented<14>(x, y, per, nsm, 256);
+    run<14, true, true, 1, 0, 0>(x, y, per, nsm);
+    run<14, true, true, 1, 0, 1>(x, y, per, nsm);
+    run<14, true, true, 1, 0, 2>(x, y, per, nsm);
+    run<14, true, true, 1, 0, 3>(x, y, per, nsm);
   }
   return 0;
 }
