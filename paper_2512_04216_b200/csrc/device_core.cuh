@@ -165,6 +165,12 @@ constexpr int kUniStride = 24;
 #define SVB_UPIPE_AHEAD 1
 #endif
 // SVB_UWAIT_FIRST: wait for the tile's uniform slot before issuing its loads
+// SVB_BULK_ROWS (set by the JIT per kernel): the one-round direct pass stores
+// its tile through shared memory with one 4 KB bulk copy per register row
+// (thread bits = the state's lowest qubits, so each row is one contiguous run)
+#ifndef SVB_BULK_ROWS
+#define SVB_BULK_ROWS 0
+#endif
 #ifndef SVB_UPIPE_PROBE
 // timing probes only (results are wrong): 1 = skip the uniform-slot waits,
 // 2 = also skip evaluating the uniform factors
@@ -800,6 +806,20 @@ __device__ __forceinline__ void prefetch_l2(const void* g) {
   asm volatile("prefetch.global.L2::evict_last [%0];\n" ::"l"(g));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+// bulk (TMA-engine) stores of contiguous rows from shared memory
+__device__ __forceinline__ void bulk_store_row(void* gdst, const void* ssrc, uint32_t bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+// this thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// generic-proxy shared-memory writes visible to the async (bulk copy) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
@@ -1327,7 +1347,8 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
   // (one tile of shared memory for the inter-round layouts, no cp.async)
   // a one-round direct pass never touches the ring (registers from HBM, to HBM)
   const int nrounds_c = NR >= 0 ? NR : pd.nrounds;
-  const uint32_t ring_bytes = (stages == 0 && nrounds_c == 1)
+  // (SVB_BULK_ROWS: the tile-sized region is the store staging of the rows)
+  const uint32_t ring_bytes = (stages == 0 && nrounds_c == 1 && !SVB_BULK_ROWS)
                                   ? 0u
                                   : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << pd.m);
   uint32_t staged = 0;
@@ -1569,6 +1590,7 @@ __device__ __forceinline__ void pass_kernel(cplx<R>* state, cplx<R>* out,
     if (stages > 1) __syncthreads();
   }
   cp_async_wait<0>();
+  if (SVB_BULK_ROWS && threadIdx.x < (1u << RB)) bulk_wait_all();
   if (pd.zsum) zsum_store<R, RB>(c);
 }
 
@@ -1610,10 +1632,11 @@ __host__ __device__ inline int upipe_slots() {
 }
 template <typename R>
 __host__ __device__ inline uint32_t pass_smem(int rb, int m, uint32_t staged_ops, int ndiag, int nslots, int stages,
-                                              int zsum = 0, int nrounds = 2) {
+                                              int zsum = 0, int nrounds = 2, int bulk = 0) {
   const uint32_t nthr = 1u << (m - rb);
-  const uint32_t ring =
-      (stages == 0 && nrounds == 1) ? 0u : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
+  const uint32_t ring = (stages == 0 && nrounds == 1 && !bulk)
+                            ? 0u
+                            : (uint32_t)(stages > 0 ? stages : 1) * ((uint32_t)sizeof(cplx<R>) << m);
   return ring + ((staged_ops + 15u) & ~15u) +
          (((stages == 0 && nrounds == 1) ? (uint32_t)upipe_slots() : 2u) * (uint32_t)ndiag * kUniStride +
           (uint32_t)nslots * nthr) *

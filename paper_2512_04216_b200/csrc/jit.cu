@@ -402,6 +402,20 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
   o << "    }\n";
 }
 
+// One-round direct complex128 passes whose thread bits are the state's lowest
+// qubits in order: each register row of a tile is one contiguous run, so the
+// tile can leave through shared memory as bulk copies (SVB_BULK_ROWS, chosen
+// at launch when the launch is direct).  SVB_BULK_ROWS=0 in the environment
+// keeps register stores.
+bool bulk_rows_eligible(const PassDev& pd, int rsize) {
+  static const bool off = std::getenv("SVB_BULK_ROWS") && std::atoi(std::getenv("SVB_BULK_ROWS")) == 0;
+  if (off || rsize != 8 || !direct_one_round(pd) || pd.perm_out || pd.perm_in) return false;
+  const RoundDev& rd = pd.rounds[0];
+  for (int b = 0; b < pd.m - pd.rb; ++b)
+    if (pd.pos[rd.thr_local[b]] != b) return false;
+  return true;
+}
+
 // Emit the straight-line Body of one pass.
 template <typename R>
 void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool imm, PrologueCtx& pc) {
@@ -607,9 +621,30 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << PG[v] << "ull, a[" << v << "]);\n";
       o << "    }\n";
     } else {
+      const bool rows = bulk_rows_eligible(pd, (int)sizeof(R));
+      if (rows) {
+        // SVB_BULK_ROWS (decided at launch): register row v of the tile is one
+        // contiguous run of nthr amplitudes at Fg - tid + G[v]; rows go through
+        // shared memory and leave as bulk copies issued by threads 0..2^RB-1
+        o << "#if SVB_BULK_ROWS\n"
+             "    { svb::cplx<R>* stg = c.ring;\n"
+             "      if (c.tid < " << (1 << RB) << "u) svb::bulk_wait_read();\n"
+             "      __syncthreads();\n";
+        for (int v = 0; v < (1 << RB); ++v) o << "      stg[" << v << " * c.nthr + c.tid] = a[" << v << "];\n";
+        o << "      svb::fence_proxy_async_smem();\n"
+             "      __syncthreads();\n"
+             "      if (c.tid < " << (1 << RB) << "u) {\n"
+             "        uint64_t go = 0;\n";
+        for (int i = 0; i < RB; ++i) o << "        if (c.tid & " << (1u << i) << "u) go |= " << G[1 << i] << "ull;\n";
+        o << "        svb::bulk_store_row(c.out + (Fg - c.tid) + go, stg + c.tid * c.nthr, c.nthr * (uint32_t)sizeof(svb::cplx<R>));\n"
+             "      }\n"
+             "    }\n"
+             "#else\n";
+      }
       o << "    { svb::cplx<R>* g0 = c.out + Fg;\n";  // == c.state unless perm_in
       for (int v = 0; v < (1 << RB); ++v) o << "      __stcs(g0 + " << G[v] << "ull, a[" << v << "]);\n";
       o << "    }\n";
+      if (rows) o << "#endif\n";
     }
   }
   o << "    } break;\n";
@@ -714,7 +749,12 @@ template <typename R> std::string jit_source_pass(const Program& prog, int p, in
   if (at != std::string::npos) b.replace(at, from.size(), "    case 0: {");
   o << b << "    default: break;\n    }\n    (void)pass;\n  }\n};\n";
   const int minb = (sizeof(R) == 8 && direct_one_round(pd0)) ? direct_min_blocks() : pass_min_blocks_of((int)sizeof(R), RB);
-  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pass_tile_m((int)sizeof(R), RB) - RB)) << ", " << minb
+  // bulk row stores: the staging tile leaves room for two CTAs per SM
+  const std::string minb_s = bulk_rows_eligible(pd0, (int)sizeof(R))
+                                 ? "(SVB_BULK_ROWS ? " + std::to_string(pass_min_blocks_of((int)sizeof(R), RB)) + " : " +
+                                       std::to_string(minb) + ")"
+                                 : std::to_string(minb);
+  o << "extern \"C\" __global__ void __launch_bounds__(" << (1 << (pass_tile_m((int)sizeof(R), RB) - RB)) << ", " << minb_s
     << ") svb_jit(svb::cplx<R>* state, svb::cplx<R>* out, "
        "const svb::PassDev* __restrict__ pdg, const uint8_t* __restrict__ ops_g, uint32_t ntiles, int pass, "
        "int zero_input, int stages) {\n"
@@ -814,6 +854,10 @@ template <typename R> static int launch_stages(const PassDev& pd, uint32_t stage
   if (stages == 1 && pd.direct && !pd.perm_in && (pd.dmask || std::getenv("SVB_DIRECT"))) stages = 0;
   return stages;
 }
+// bulk row stores need the direct launch (the tile region is free for staging)
+template <typename R> static bool launch_bulk(const PassDev& pd, int stages) {
+  return stages == 0 && bulk_rows_eligible(pd, (int)sizeof(R));
+}
 
 template <typename R>
 bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const PassDev* dpass, const uint8_t* dops,
@@ -872,8 +916,9 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
       }
       if (pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], 1, zsm_pass(pd)) > kSmemMaxPerCTA) return false;
       {  // the launch's ring depth, round count and lazy-input flag, compiled in
-         // (pass_kernel's STAGES / NR / ZIN)
+         // (pass_kernel's STAGES / NR / ZIN), and the bulk row stores
         const int stg = launch_stages<R>(pd, staged[p], nslots[p]);
+        if (launch_bulk<R>(pd, stg)) srcs[p].insert(0, "#define SVB_BULK_ROWS 1\n");
         const int zin = (zero_input && p == 0) ? 1 : 0;
         const std::string from = "(state, out, pdg, ops_g, ntiles, pass, zero_input, stages,";
         const size_t at = srcs[p].rfind(from);
@@ -1049,7 +1094,8 @@ bool jit_launch_passes(cplx<R>* state, cplx<R>* out, const Program& prog, const 
     const uint64_t tiles = 1ull << pd.nout;
     const unsigned threads = 1u << (pd.m - RB);
     int stages = launch_stages<R>(pd, staged[p], nslots[p]);
-    const unsigned smem = pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds);
+    const unsigned smem = pass_smem<R>(pd.rb, pd.m, staged[p], pd.ndiag, nslots[p], stages, zsm_pass(pd), pd.nrounds,
+                                       launch_bulk<R>(pd, stages) ? 1 : 0);
     int per_sm = stages <= 1 ? pass_min_blocks_of((int)sizeof(R), pd.rb) : 1;
     if (sizeof(R) == 8 && stages == 0 && direct_one_round(pd) &&
         (uint64_t)direct_min_blocks() * (smem + kSmemReservedPerCTA + kPassStaticSmem) <= kSmemPerSM)
