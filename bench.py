@@ -51,15 +51,18 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 
 def measured_traffic():
     """dram read+write bytes per launch of the dominant kernel (the bench step's
-    last fused pass) from the committed ncu --set full capture
-    (profiles/r01_ncu_qft30_pass_full.json, record "qft30_top"), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_qft30_pass_full.json")) as fh:
-            recs = json.load(fh)
-        top = [r for r in recs if "top" in r.get("report", "")] or recs[:1]
-        return float((top[0]["dram_read_bytes"] + top[0]["dram_write_bytes"]) * 1e9)  # ncu reports GB
-    except Exception:
-        return None
+    last fused pass) from the committed ncu --set full capture of the current
+    kernel (profiles/r02_ncu_qft30_pass_bulk.json; r01's capture of the
+    register-store version as a fallback), or None."""
+    for name in ("r02_ncu_qft30_pass_bulk.json", "r01_ncu_qft30_pass_full.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                recs = json.load(fh)
+            top = [r for r in recs if "top" in r.get("report", "")] or recs[:1]
+            return float((top[0]["dram_read_bytes"] + top[0]["dram_write_bytes"]) * 1e9)  # ncu reports GB
+        except Exception:
+            continue
+    return None
 
 
 def hbm_peak():
