@@ -1184,6 +1184,10 @@ extern "C" int svb_jit_check(int n, int precision, const svb_gate* gates, int ng
       if (zsum && !p.passes.empty()) p.passes.back().zsum = 1;
       for (size_t k = 0; k < p.passes.size(); ++k) srcs.push_back(jit_source_pass<float>(p, (int)k, nullptr, nullptr));
     }
+    // passes with a bulk-row-store epilogue also compile in that variant
+    // (the launch chooses it when the pass runs direct)
+    for (size_t k = 0, n0 = srcs.size(); k < n0; ++k)
+      if (srcs[k].find("#if SVB_BULK_ROWS") != std::string::npos) srcs.push_back("#define SVB_BULK_ROWS 1\n" + srcs[k]);
     if (std::getenv("SVB_JIT_DUMP") && !srcs.empty()) {
       FILE* f = std::fopen(std::getenv("SVB_JIT_DUMP"), "w");
       if (f) {

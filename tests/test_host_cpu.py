@@ -400,6 +400,36 @@ def test_jit_sources_compile(which):
     assert cb.value > 0
 
 
+def test_bulk_row_store_epilogue_emitted_only_where_rows_are_contiguous(tmp_path, monkeypatch):
+    """The one-round direct complex128 pass whose thread bits are qubits 0..7
+    (the QFT-30 bench's last pass) gets the bulk-row-store epilogue
+    (SVB_BULK_ROWS: rows through shared memory, cp.async.bulk); passes whose
+    register rows are not contiguous runs (a written-input QFT-20, complex64
+    Sycamore) keep register stores only."""
+    import ctypes as _ct
+
+    monkeypatch.setenv("SVB_JIT_NOCOMPILE", "1")
+
+    def dump(n, prec, c, name):
+        path = tmp_path / name
+        monkeypatch.setenv("SVB_JIT_DUMP", str(path))
+        g = sv.gate_array(c.instructions)
+        cb = _ct.c_int64()
+        buf = _ct.create_string_buffer(1 << 12)
+        rc = _lib.lib().svb_jit_check(n, prec, g.ctypes.data_as(_ct.c_void_p), int(g.size), _ct.byref(cb), buf, 1 << 12)
+        assert rc == 0, buf.value
+        return path.read_text()
+
+    src = dump(30, 0x301, suite.qft_bench_circuit(30), "qft30.cu")
+    bodies = src.split('#include "device_core.cuh"')[1:]
+    assert len(bodies) == 5  # four passes + the bulk variant jit_check also compiles
+    assert ["#if SVB_BULK_ROWS" in b for b in bodies[:4]] == [False, False, False, True]
+    assert "svb::bulk_store_row(" in bodies[3] and src.count("#define SVB_BULK_ROWS 1") == 1
+    assert "#if SVB_BULK_ROWS" not in dump(20, 1, suite.qft_bench_circuit(20), "qft20.cu")
+    syc = suite.sycamore_circuit(4, 7, 12, seed=0, measured=False)
+    assert "#if SVB_BULK_ROWS" not in dump(28, 0x100, syc, "syc.cu")
+
+
 def test_structure_only_jit_sources_do_not_depend_on_angles(tmp_path, monkeypatch):
     """Below 28 qubits the NVRTC passes load their coefficients, so circuits
     that differ only in angles generate the same kernel sources (a VQE / QAOA

@@ -105,11 +105,60 @@ template <class F> float best(F f);
 // Stores staged through shared memory and written by bulk copies: the 16
 // register rows of a tile are 16 contiguous 4 KB runs; one thread issues one
 // cp.async.bulk per run once the CTA's rows are in shared memory.
-template <int K, int AHEAD>
-__global__ void __launch_bounds__(256) k_pass_bulk(const double2* __restrict__ in, double2* __restrict__ out,
-                                                   uint32_t ntiles, double c0) {
-  extern __shared__ __align__(128) double2 stile[];  // 16 rows x 256
+template <int K, int AHEAD, int NT = 256>
+__global__ void __launch_bounds__(NT) k_pass_bulk(const double2* __restrict__ in, double2* __restrict__ out,
+                                                  uint32_t ntiles, double c0) {
+  extern __shared__ __align__(128) double2 stile[];  // 16 rows x NT
   const uint64_t lmask = (1ull << 26) - 1;
+  double2 q[AHEAD > 0 ? AHEAD : 1];
+#pragma unroll
+  for (int j = 0; j < AHEAD; ++j) {
+    const uint32_t tj = blockIdx.x + j * gridDim.x;
+    q[j] = tj < ntiles ? __ldcs(in + ((((uint64_t)tj * NT) | threadIdx.x) & lmask)) : make_double2(0, 0);
+  }
+  for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    double2 x = q[0];
+#pragma unroll
+    for (int j = 0; j + 1 < AHEAD; ++j) q[j] = q[j + 1];
+    const uint32_t tn = t + AHEAD * gridDim.x;
+    q[AHEAD - 1] = tn < ntiles ? __ldcs(in + ((((uint64_t)tn * NT) | threadIdx.x) & lmask)) : make_double2(0, 0);
+    double2 a[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) a[r] = make_double2(x.x + r, x.y - r);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        a[r].x = fma(a[r].x, c0, a[r].y);
+        a[r].y = fma(a[r].y, c0, -a[r].x);
+      }
+    // the previous tile's bulk stores must have read shared memory
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) stile[r * NT + threadIdx.x] = a[r];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 16) {
+      const int r = threadIdx.x;
+      double2* dst = out + (((uint64_t)t * NT) | ((uint64_t)r << 26));
+      const uint32_t src = (uint32_t)__cvta_generic_to_shared(stile + r * NT);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(src), "r"((uint32_t)(NT * 16)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+  }
+  if (threadIdx.x < 16) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// Per-warp variant: each warp stages its 32 lanes x 16 rows and its lanes
+// 0..15 issue one 512 B bulk copy per row: no CTA barrier, only __syncwarp.
+template <int K, int AHEAD>
+__global__ void __launch_bounds__(256) k_pass_bulkw(const double2* __restrict__ in, double2* __restrict__ out,
+                                                    uint32_t ntiles, double c0) {
+  extern __shared__ __align__(128) double2 stile[];  // 8 warps x 16 rows x 32
+  const uint64_t lmask = (1ull << 26) - 1;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  double2* ws = stile + warp * 16 * 32;
   double2 q[AHEAD > 0 ? AHEAD : 1];
 #pragma unroll
   for (int j = 0; j < AHEAD; ++j) {
@@ -132,32 +181,42 @@ __global__ void __launch_bounds__(256) k_pass_bulk(const double2* __restrict__ i
         a[r].x = fma(a[r].x, c0, a[r].y);
         a[r].y = fma(a[r].y, c0, -a[r].x);
       }
-    // the previous tile's bulk stores must have read shared memory
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-    __syncthreads();
+    if (lane < 16) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 16; ++r) stile[r * 256 + threadIdx.x] = a[r];
+    for (int r = 0; r < 16; ++r) ws[r * 32 + lane] = a[r];
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x < 16) {
-      const int r = threadIdx.x;
-      double2* dst = out + ((((uint64_t)t << 8)) | ((uint64_t)r << 26));
-      const uint32_t src = (uint32_t)__cvta_generic_to_shared(stile + r * 256);
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 4096;\n" ::"l"(dst), "r"(src) : "memory");
+    __syncwarp();
+    if (lane < 16) {
+      const int r = lane;
+      double2* dst = out + ((((uint64_t)t << 8) | (warp << 5)) | ((uint64_t)r << 26));
+      const uint32_t src = (uint32_t)__cvta_generic_to_shared(ws + r * 32);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;\n" ::"l"(dst), "r"(src) : "memory");
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
   }
-  if (threadIdx.x < 16) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  if (lane < 16) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 template <int K, int AH>
-void run_bulk(const double2* x, double2* y, int per, int nsm) {
+void run_bulkw(const double2* x, double2* y, int per, int nsm) {
   const uint32_t ntiles = 1u << 18;
   const int g = nsm * per;
-  cudaFuncSetAttribute(k_pass_bulk<K, AH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  const float t = best([&] { k_pass_bulk<K, AH><<<g, 256, 65536>>>(x, y, ntiles, 0.999); });
-  std::printf("{\"K\": %d, \"bulk_stores\": 1, \"ctas_per_sm\": %d, \"ahead\": %d, \"ms\": %.3f, \"err\": \"%s\"}\n", K, per,
-              AH, t, cudaGetErrorString(cudaGetLastError()));
+  cudaFuncSetAttribute(k_pass_bulkw<K, AH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  const float t = best([&] { k_pass_bulkw<K, AH><<<g, 256, 65536>>>(x, y, ntiles, 0.999); });
+  std::printf("{\"K\": %d, \"bulk_stores_per_warp_512B\": 1, \"ctas_per_sm\": %d, \"ahead\": %d, \"ms\": %.3f, \"err\": \"%s\"}\n",
+              K, per, AH, t, cudaGetErrorString(cudaGetLastError()));
+}
+
+template <int K, int AH, int NT = 256>
+void run_bulk(const double2* x, double2* y, int per, int nsm) {
+  const uint32_t ntiles = (1u << 26) / NT;
+  const int g = nsm * per;
+  const int sm = 16 * NT * 16;
+  cudaFuncSetAttribute(k_pass_bulk<K, AH, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  const float t = best([&] { k_pass_bulk<K, AH, NT><<<g, NT, sm>>>(x, y, ntiles, 0.999); });
+  std::printf("{\"K\": %d, \"bulk_stores\": 1, \"row_bytes\": %d, \"ctas_per_sm\": %d, \"ahead\": %d, \"ms\": %.3f, \"err\": \"%s\"}\n", K,
+              NT * 16, per, AH, t, cudaGetErrorString(cudaGetLastError()));
 }
 
 template <class F> float best(F f) {
@@ -197,11 +256,10 @@ int main() {
   cudaMemset(x, 0, bytes);
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  for (int per : {2, 3}) {
-    run<14, true, true, 1, 0, 0>(x, y, per, nsm);
-    run_bulk<14, 1>(x, y, per, nsm);
-    run_bulk<14, 2>(x, y, per, nsm);
-    run_bulk<0, 1>(x, y, per, nsm);
-  }
+  run_bulk<14, 1, 256>(x, y, 2, nsm);
+  run_bulk<14, 1, 512>(x, y, 1, nsm);
+  run_bulk<14, 2, 512>(x, y, 1, nsm);
+  run_bulk<0, 1, 512>(x, y, 1, nsm);
+  run_bulk<14, 1, 256>(x, y, 1, nsm);
   return 0;
 }
