@@ -931,6 +931,8 @@ static Program build_program_layout(int n, const svb_gate* gates, int ng, const 
       for (int k = 0; k < pd.nrounds; ++k) {
         std::fprintf(stderr, "[svb] pass %zu round %d regs", p, k);
         for (int i = 0; i < pd.rb; ++i) std::fprintf(stderr, " q%d", pd.pos[pd.rounds[k].reg_local[i]]);
+        std::fprintf(stderr, " thr");
+        for (int b = 0; b < pd.m - pd.rb; ++b) std::fprintf(stderr, " q%d", pd.pos[pd.rounds[k].thr_local[b]]);
         std::fprintf(stderr, ":");
         for (uint32_t off = pd.rounds[k].op_off; off < pd.rounds[k].op_end;) {
           OpHdr h;

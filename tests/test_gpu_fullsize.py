@@ -89,6 +89,32 @@ def test_qft30_bench_path_vs_closed_form():
     s.close()
 
 
+@pytest.mark.parametrize("n,fused_z", [(24, True), (25, False), (26, True), (27, False), (28, True), (29, False)])
+def test_qft_lazy_zero_bulk_row_store_sizes_vs_closed_form(n, fused_z):
+    """The bench's program shape at 24..29 qubits: the last pass is the
+    one-round direct pass whose tile rows leave as bulk copies (SVB_BULK_ROWS),
+    with and without the fused <Z> sums; structure-only (n < 28) and immediate
+    (n >= 28) NVRTC bodies.  Amplitudes at 1e-10 normwise, <Z_i> at 1e-10."""
+    torch = _torch()
+    c = suite.qft_bench_circuit(n)
+    gates = sv.gate_array(c.instructions)
+    s = sv.DeviceState(n, "c128")
+    for _ in range(2):
+        s.zero()
+        if fused_z:
+            z = s.apply_gates_z(gates, list(range(n)))
+        else:
+            s.apply_gates(gates)
+    theta = [0.1 * (q + 1) for q in range(n)]
+    cs = [math.cos(t / 2) for t in theta]
+    ss = [math.sin(t / 2) for t in theta]
+    rel, zref = _compare_chunks(torch, s, n, cs, ss, range(0, 1 << n, CHUNK), zq=list(range(n)))
+    assert rel < 1e-10, rel
+    if fused_z:
+        np.testing.assert_allclose(z, zref, atol=1e-10)
+    s.close()
+
+
 def test_qft30_round_trip_restores_product_state():
     """ry-prep QFT-30 then QFT^-1 (the bench circuit and its inverse, one
     program) returns the analytic product state (x)_q ry(0.1 (q+1))|0>."""
