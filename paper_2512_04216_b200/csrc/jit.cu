@@ -198,9 +198,29 @@ struct PrologueCtx {
   int round = 0;                    // round of the op being emitted
 };
 
+// A DIAG that only multiplies each amplitude by per-register-bit factors
+// (no tile/thread-uniform scalar C, no |0>-half factors, no register pairs):
+// it can be fused with a preceding product state (emit_diag's `prod`).
+template <typename R> bool diag_per_bit_only(const uint8_t* payload, int RB) {
+  DiagHdr h;
+  std::memcpy(&h, payload, sizeof h);
+  if (h.nUC || h.nUTg || h.nTC || h.nRR) return false;
+  const DiagTerm<R>* u = reinterpret_cast<const DiagTerm<R>*>(payload + sizeof(DiagHdr));
+  int nur = 0;
+  for (int i = 0; i < RB; ++i) nur += h.nUR[i];
+  for (int k = 0; k < nur + h.nTR; ++k)
+    if (!is1(u[k].d[0]) || !is1(u[k].d[2])) return false;
+  return true;
+}
+
+// prod (support-tracked round 0, immediates): the registers hold the product
+// state a[v] = a[0] * prod_{i in v} prod[i] of leading pivot ops that were not
+// emitted; the DIAG (diag_per_bit_only) then builds a[v] = a[0] * prod E_i with
+// E_i = prod[i] * D1_i in one tree: 15 complex products instead of the pivot
+// expansions, the factor tree and a multiply per amplitude.
 template <typename R>
 void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, int RB, bool imm,
-               PrologueCtx& pc) {
+               PrologueCtx& pc, const cplx<R>* prod = nullptr) {
   // factor e of a term: an immediate (large programs) or a load from the op
   // payload in shared memory (structure-only code shared across angles)
   auto dref = [&](const void* term, int e) {
@@ -339,6 +359,26 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
           o << "      svb::mul_quad<R, RB, " << (int)rr[k].ra << ", " << (int)rr[k].rb << ", " << q << ">(a, "
             << dref(rr + k, q) << ");\n";
       }
+  if (prod) {
+    for (int i = 0; i < RB; ++i) {
+      const bool preal = prod[i].y == 0;
+      o << "      const svb::cplx<R> E_" << i << " = ";
+      if (d1one[i]) o << cimm<R>(prod[i]);
+      else if (preal) o << "svb::rmul<R>(" << hexf((double)prod[i].x, sizeof(R) == 4) << ", D1_" << i << ")";
+      else o << "svb::cmul<R>(D1_" << i << ", " << cimm<R>(prod[i]) << ")";
+      o << ";\n";
+    }
+    for (int v = 1; v < (1 << RB); ++v) {
+      const int low = __builtin_ctz((unsigned)v);
+      const int rest = v & (v - 1);
+      if (d1one[low] && prod[low].y == 0)
+        o << "      a[" << v << "] = svb::rmul<R>(E_" << low << ".x, a[" << rest << "]);\n";
+      else
+        o << "      a[" << v << "] = svb::cmul<R>(a[" << rest << "], E_" << low << ");\n";
+    }
+    o << "    }\n";
+    return;
+  }
   // fold D0 into C (unit-modulus entries: 1/D0 = conj(D0)), then apply
   bool need_c = !cone;
   for (int i = 0; i < RB; ++i)
@@ -484,12 +524,37 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
     if (k == 0 && pd.dmask && imm)
       for (int v = 0; v < (1 << RB); ++v)
         if (G[v] & pd.dmask) zm |= 1u << v;
+    // product-state fusion (see emit_diag's prod): while round 0 starts from a
+    // single live register (a[0]) and each leading pivot op expands it along a
+    // new register bit, the ops are held back (deferred) with their ratios;
+    // a following per-bit DIAG then builds the whole product in one tree
+    const uint32_t nregs = 1u << RB, allv = (nregs >= 32 ? 0xffffffffu : (1u << nregs) - 1u);
+    bool prod_ok = zm == (allv & ~1u) && !std::getenv("SVB_NO_PROD_FUSE");
+    uint32_t prod_bits = 0;
+    cplx<R> prodf[8];
+    std::string deferred;
+    auto zm_of = [&](uint32_t bits) {  // zero registers of a product over `bits`
+      uint32_t z = 0;
+      for (uint32_t v = 0; v < nregs; ++v)
+        if (v & ~bits) z |= 1u << v;
+      return z;
+    };
     uint32_t off = rd.op_off;
     while (off < rd.op_end) {
       OpHdr h;
       std::memcpy(&h, prog.ops.data() + off, sizeof h);
       const uint32_t pay = off + (uint32_t)sizeof(OpHdr);
       const cplx<R>* coef = reinterpret_cast<const cplx<R>*>(prog.ops.data() + pay);
+      bool fuse_diag = false;
+      if (h.kind != OP_U1P && h.kind != OP_U1PR && !deferred.empty()) {
+        if (h.kind == OP_DIAG && prod_bits == nregs - 1 && diag_per_bit_only<R>(prog.ops.data() + pay, RB)) {
+          fuse_diag = true;
+        } else {
+          o << deferred;
+        }
+        deferred.clear();
+        prod_ok = false;
+      }
       std::string guard;
       if (h.fmask) {
         char buf[96];
@@ -504,7 +569,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
       switch (h.kind) {
         case OP_DIAG:
           pc.round = k;
-          emit_diag<R>(o, prog.ops.data() + pay, pay, RB, imm, pc);
+          emit_diag<R>(o, prog.ops.data() + pay, pay, RB, imm, pc, fuse_diag ? prodf : nullptr);
           break;
         case OP_U1R:
           if (imm) {
@@ -537,8 +602,24 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
           if (imm && zm && !h.fmask) {
             auto rk = [](const cplx<R>& z) { return z.x == 0 && z.y == 0 ? 0 : z.y == 0 ? 1 : z.x == 0 ? 2 : 3; };
             const int rk0 = rk(coef[0]), rk1 = rk(coef[1]);
-            o << "    svb::u1_piv_z<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk0 << ", " << rk1 << ", "
-              << zm << "u>(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
+            // along a new bit with the live half as pivot of row 0 and the
+            // other of row 1: a[v] stays, a[v | bit] = ratio1 * a[v]
+            const bool expands = prod_ok && !((prod_bits >> h.a) & 1u) && pc0 == 0 && pc1 == 1 && zm == zm_of(prod_bits);
+            if (!expands && !deferred.empty()) {
+              o << deferred;
+              deferred.clear();
+            }
+            if (!expands) prod_ok = false;
+            std::ostringstream call;
+            call << "    svb::u1_piv_z<R, RB, " << h.a << ", " << pc0 << ", " << pc1 << ", " << rk0 << ", " << rk1 << ", "
+                 << zm << "u>(a, " << cimm<R>(coef[0]) << ", " << cimm<R>(coef[1]) << ");\n";
+            if (expands) {
+              prodf[h.a] = coef[1];
+              prod_bits |= 1u << h.a;
+              deferred += call.str();
+            } else {
+              o << call.str();
+            }
             uint32_t nz = zm;  // zero outputs: both inputs zero, or (p zero and the ratio term zero)
             for (int v = 0; v < (1 << RB); ++v) {
               if (v & (1 << h.a)) continue;
@@ -551,6 +632,11 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
             zm = nz;
             break;
           }
+          if (!deferred.empty()) {
+            o << deferred;
+            deferred.clear();
+          }
+          prod_ok = false;
           zm = 0;
           if (imm) {
             auto rk = [](const cplx<R>& z) { return z.x == 0 && z.y == 0 ? 0 : z.y == 0 ? 1 : z.x == 0 ? 2 : 3; };
@@ -604,6 +690,7 @@ void emit_body(std::ostringstream& o, const Program& prog, int p, int RB, bool i
         }
       }
     }
+    if (!deferred.empty()) o << deferred;  // the round ended inside the expansion
     if (uin && !usynced && k + 1 == pd.nrounds) {
       o << "    svb::upipe_sync<R, RB>(c);\n";
       usynced = true;
