@@ -1142,17 +1142,23 @@ __device__ __forceinline__ void load_global(const PassCtx<R, RB>& c, uint64_t Fg
 // Global layout (doubles): per thread [cta][RB + 1][nthr], then per warp [cta][nwarps][64].
 template <typename R, int RB>
 __device__ __forceinline__ void zsum_tile(const PassCtx<R, RB>& c, const cplx<R>* a, uint64_t base) {
-  double T = 0.0, s1[RB];
+  // halving tree over the register bits: level i sums the pairs along bit i
+  // (their odd halves give s1[i] = sum of p_v with bit i set); ~2^(RB+1)
+  // additions instead of 2^RB (RB/2 + 1)
+  double q[1 << RB], s1[RB];
 #pragma unroll
-  for (int i = 0; i < RB; ++i) s1[i] = 0.0;
+  for (int v = 0; v < (1 << RB); ++v) q[v] = (double)a[v].x * (double)a[v].x + (double)a[v].y * (double)a[v].y;
 #pragma unroll
-  for (int v = 0; v < (1 << RB); ++v) {  // running sums: no array of p_v
-    const double pv = (double)a[v].x * (double)a[v].x + (double)a[v].y * (double)a[v].y;
-    T += pv;
+  for (int i = 0; i < RB; ++i) {
+    const int h = 1 << (RB - 1 - i);  // pairs at this level
+    double odd = q[1];
 #pragma unroll
-    for (int i = 0; i < RB; ++i)
-      if (v & (1 << i)) s1[i] += pv;
+    for (int j = 1; j < h; ++j) odd += q[2 * j + 1];
+    s1[i] = odd;
+#pragma unroll
+    for (int j = 0; j < h; ++j) q[j] = q[2 * j] + q[2 * j + 1];
   }
+  const double T = q[0];
   double tw = T;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tw += __shfl_xor_sync(0xffffffffu, tw, o);
