@@ -295,6 +295,7 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
       o << "      svb::cplx<R> D1_" << i << " = "
         << (has_ur ? "(" + us + ")[" + std::to_string(6 + i) + "]" : "svb::mk<R>(R(1), R(0))") << ";\n";
   }
+  uint32_t pro_scaled = 0;  // prod: bits whose ratio went into a prologue slot
   // register-bit x thread-bit terms depend only on the thread's own local bits:
   // their products are evaluated once per thread in the prologue (st.v[slot])
   for (int i = 0; i < RB; ++i) {
@@ -334,6 +335,11 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
         P << "      acc = svb::cmul<R>(acc, svb::csel<R>((int)((F >> " << (int)tr[k].qb << ") & 1ull), "
           << dref(tr + k, half) << ", " << dref(tr + k, 2 + half) << "));\n";
       }
+      if (prod && half == 1) {  // the product tree's ratio of this bit, once per thread
+        if (prod[i].y == 0) P << "      acc = svb::rmul<R>(" << hexf((double)prod[i].x, sizeof(R) == 4) << ", acc);\n";
+        else P << "      acc = svb::cmul<R>(acc, " << cimm<R>(prod[i]) << ");\n";
+        pro_scaled |= 1u << i;
+      }
       P << "      c.pro[" << slot << " * c.nthr + c.tid] = acc; }\n";
       o << "      D" << half << "_" << i << " = svb::cmul<R>(D" << half << "_" << i << ", c.pro[" << slot
         << " * c.nthr + c.tid]);\n";
@@ -363,7 +369,8 @@ void emit_diag(std::ostringstream& o, const uint8_t* payload, uint32_t pay_off, 
     for (int i = 0; i < RB; ++i) {
       const bool preal = prod[i].y == 0;
       o << "      const svb::cplx<R> E_" << i << " = ";
-      if (d1one[i]) o << cimm<R>(prod[i]);
+      if ((pro_scaled >> i) & 1u) o << "D1_" << i;
+      else if (d1one[i]) o << cimm<R>(prod[i]);
       else if (preal) o << "svb::rmul<R>(" << hexf((double)prod[i].x, sizeof(R) == 4) << ", D1_" << i << ")";
       else o << "svb::cmul<R>(D1_" << i << ", " << cimm<R>(prod[i]) << ")";
       o << ";\n";
