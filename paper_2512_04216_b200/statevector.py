@@ -447,7 +447,10 @@ class _StatePool:
     """Idle device states kept for reuse by run() and the final_state /
     expectation cache (no cudaMalloc / cudaFree / stream creation per call).
     Bounded by bytes (32 GiB: one idle 31-qubit complex128 state); LIFO per
-    key; emptied when a new state does not fit in device memory."""
+    key; the state released last is kept, idle states released earlier are
+    closed to make room for it (a 32-qubit complex64 state after a 30-qubit
+    complex128 one was closed instead, and the next run paid a 32 GiB
+    cudaMalloc); emptied when a new state does not fit in device memory."""
 
     def __init__(self, cap_bytes: int = 32 << 30, per_key: int = 4):
         import threading
@@ -476,13 +479,25 @@ class _StatePool:
     def release(self, st: DeviceState) -> None:
         key = (st.n, st.precision, st.device)
         size = self._size(st.n, st.precision)
+        evicted = []
         with self.lock:
             lst = self.idle.setdefault(key, [])
-            if len(lst) < self.per_key and self.bytes + size <= self.cap:
+            if len(lst) < self.per_key and size <= self.cap:
+                # oldest releases first (dicts keep insertion order; each key's
+                # list is LIFO, so its front is its oldest)
+                for k in list(self.idle):
+                    while self.bytes + size > self.cap and self.idle[k]:
+                        evicted.append(self.idle[k].pop(0))
+                        self.bytes -= self._size(k[0], k[1])
+                    if not self.idle[k] and k != key:
+                        del self.idle[k]
                 lst.append(st)
                 self.bytes += size
-                return
-        st.close()
+                st = None
+        for e in evicted:
+            e.close()
+        if st is not None:
+            st.close()
 
     def clear(self) -> None:
         with self.lock:

@@ -482,3 +482,28 @@ def test_structure_only_jit_sources_do_not_depend_on_angles(tmp_path, monkeypatc
             assert rc == 0, buf.value
             srcs.add(path.read_text())
         assert len(srcs) == 1, (fam.__name__, len(srcs))
+
+
+def test_state_pool_keeps_the_latest_release():
+    """The idle-state pool (32 GiB) keeps the state released last and closes
+    older idle states to make room; a state larger than the cap is closed."""
+
+    class Fake:
+        def __init__(self, n, precision):
+            self.n, self.precision, self.device, self.closed = n, precision, 0, False
+
+        def close(self):
+            self.closed = True
+
+    pool = sv._StatePool()
+    a, b, c = Fake(30, "c128"), Fake(32, "c64"), Fake(30, "c128")
+    pool.release(a)
+    assert pool.bytes == 16 << 30 and not a.closed
+    pool.release(b)  # 32 GiB: a is closed to make room
+    assert a.closed and not b.closed and pool.bytes == 32 << 30
+    pool.release(c)
+    assert b.closed and not c.closed and pool.bytes == 16 << 30
+    big = Fake(33, "c128")
+    pool.release(big)
+    assert big.closed and pool.bytes == 16 << 30
+    assert pool.acquire(30, "c128", 0) is c and pool.bytes == 0
