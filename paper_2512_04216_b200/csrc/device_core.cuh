@@ -480,6 +480,39 @@ SVB_HD void diag_uniform_serial(const uint8_t* payload, uint64_t base, cplx<R>* 
   slot[0] = c;
 }
 
+// A register-pair diagonal term (quadrant factors e[ba + 2 bb]) with the pair
+// as template arguments: the quadrant of every register is then a constant
+// (a runtime pair cost three selects per register -- ~17% of the interpreter's
+// instructions on the config-4 QAOA passes), and a quadrant whose factor is
+// exactly 1 is skipped (a warp-uniform branch: controlled phases touch one).
+template <typename R, int RB, int RA, int RBB>
+SVB_HD void rr_quads(cplx<R>* a, const cplx<R>* e) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const cplx<R> f = ldc<R>(e + q);
+    if (f.x == R(1) && f.y == R(0)) continue;
+#pragma unroll
+    for (int v = 0; v < (1 << RB); ++v)
+      if ((((v >> RA) & 1) | (((v >> RBB) & 1) << 1)) == q) a[v] = cmul<R>(a[v], f);
+  }
+}
+template <typename R, int RB>
+SVB_HD void rr_apply(cplx<R>* a, int ra, int rb, const cplx<R>* e) {
+#define SVB_RR(A, B) \
+  case (A) * 8 + (B): \
+    if constexpr ((A) < RB && (B) < RB) rr_quads<R, RB, A, B>(a, e); \
+    break;
+  switch (ra * 8 + rb) {
+    SVB_RR(0, 1) SVB_RR(0, 2) SVB_RR(0, 3) SVB_RR(0, 4)
+    SVB_RR(1, 0) SVB_RR(1, 2) SVB_RR(1, 3) SVB_RR(1, 4)
+    SVB_RR(2, 0) SVB_RR(2, 1) SVB_RR(2, 3) SVB_RR(2, 4)
+    SVB_RR(3, 0) SVB_RR(3, 1) SVB_RR(3, 2) SVB_RR(3, 4)
+    SVB_RR(4, 0) SVB_RR(4, 1) SVB_RR(4, 2) SVB_RR(4, 3)
+    default: break;
+  }
+#undef SVB_RR
+}
+
 template <typename R, int RB>
 SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cplx<R>* uni) {
   constexpr int V = 1 << RB;
@@ -535,12 +568,7 @@ SVB_HD void diag_apply(cplx<R>* a, uint64_t Fg, const uint8_t* payload, const cp
   for (int k = 0; k < nRR; ++k, ++t) {
     const uint32_t w = ldop(reinterpret_cast<const uint32_t*>(t));
     const int ra = (int8_t)(w & 0xff), rb = (int8_t)((w >> 8) & 0xff);
-    const cplx<R> e0 = ldc<R>(t->d), e1 = ldc<R>(t->d + 1), e2 = ldc<R>(t->d + 2), e3 = ldc<R>(t->d + 3);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      const int ba = (v >> ra) & 1, bb = (v >> rb) & 1;
-      a[v] = cmul<R>(a[v], ba ? (bb ? e3 : e1) : (bb ? e2 : e0));
-    }
+    rr_apply<R, RB>(a, ra, rb, t->d);
   }
   // a[v] *= C * prod_i (v_i ? D1[i] : D0[i]).  Fold D0[i] into C so each
   // register bit contributes one ratio on its v_i = 1 half; skip factors that
