@@ -208,3 +208,43 @@ def test_capacity_ghz33_c128():
     assert abs(float(s.expect_z([0])[0]) - 1.0) < 1e-12
     np.testing.assert_allclose(s.expect_z([1 << q for q in range(n)]), 0.0, atol=1e-12)
     s.close()
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[2])
+from paper_2512_04216_b200 import statevector as sv, suite
+n = 28
+g = sv.gate_array(suite.qft_bench_circuit(n).instructions)
+s = sv.DeviceState(n, "c128")
+s.zero()
+z = s.apply_gates_z(g, list(range(n)))
+buf = np.empty(1 << 20, dtype=np.complex128)
+head = s.read(0, 1 << 20, buf).copy()
+tail = s.read((1 << n) - (1 << 20), 1 << 20, buf).copy()
+np.savez(sys.argv[1], z=z, head=head, tail=tail)
+"""
+
+
+def test_bulk_store_and_product_tree_match_their_plain_variants(tmp_path):
+    """The bench-shaped QFT-28 (immediates, product-state round 0, bulk-row
+    stores on the last pass) against the same program with register stores
+    (SVB_BULK_ROWS=0) and without the product tree (SVB_NO_PROD_FUSE=1), each
+    in its own process (the knobs are read once): the stores must agree bit
+    for bit, the reassociated arithmetic to 1e-12."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "variant.py"
+    script.write_text(_VARIANT_SCRIPT)
+    out = {}
+    for name, env in (("default", {}), ("regstores", {"SVB_BULK_ROWS": "0"}), ("noprod", {"SVB_NO_PROD_FUSE": "1"})):
+        path = tmp_path / f"{name}.npz"
+        subprocess.run([sys.executable, str(script), str(path), root], check=True, env={**os.environ, **env},
+                       timeout=600)
+        out[name] = np.load(path)
+    for k in ("z", "head", "tail"):
+        np.testing.assert_array_equal(out["default"][k], out["regstores"][k])
+        np.testing.assert_allclose(out["default"][k], out["noprod"][k], rtol=0, atol=1e-12)
